@@ -1,0 +1,295 @@
+"""bench.py — headline benchmark of the PSSGP hot path on B200.
+
+Metric (BASELINE.json): time-steps/s of filter + smoother + NLL in fp64,
+Matern-5/2, N = 2^24 grid points (irregular jittered times at the paper's
+finest density h = 4/2^15, 1/16 of the points missing = test points).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...   (time-sharded, NCCL)
+
+One JSON line on rank 0.  A "step" = one full pssgp_posterior over the whole
+grid (all hot-path rows: discretisation, filter elements, forward scan,
+smoother scan, NLL), inputs resident in HBM.  The working set (inputs 285 MB,
+filtered state 1.2 GB, outputs 268 MB) is far larger than the 126 MB L2, so
+no explicit L2 flush is needed between steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "time-steps/s (filter+smoother+NLL, fp64) Matern-5/2 N=2^24"
+UNIT = "time-steps/s"
+# algorithmic bytes per time step moved by each kernel at d = 3
+ALG_BYTES = {"k_filter_reduce": 17, "k_filter_apply": 17 + 72, "k_smoother_apply": 8 + 72 + 16}
+# executed fp64 operations per time step of each kernel (DFMA = 2 flops), DESIGN.md ledger
+THROTTLE_BAD = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--N", type=int, default=2 ** 24)
+    ap.add_argument("--uniform", action="store_true", help="uniform dt (secondary row)")
+    ap.add_argument("--kind", default="matern52")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=2 ** 21)
+    ap.add_argument("--chain-len", type=int, default=0)
+    ap.add_argument("--blocks-per-sm", type=int, default=0)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    REASONS = ["clocks_event_reasons.hw_slowdown", "clocks_event_reasons.hw_thermal_slowdown",
+               "clocks_event_reasons.sw_thermal_slowdown", "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def start(self):
+        q = "clocks.sm,clocks.max.sm,power.draw," + ",".join(self.REASONS)
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 3:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for s in self.samples:
+            for name, v in zip(names, s[3:]):
+                if v.strip().lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "_fallback": True}
+
+
+# ------------------------------------------------------------------------------ cpu baseline (oracle)
+def cpu_baseline(w, sample: int):
+    import oracle
+    n = min(sample, w.N)
+    m = oracle.ssm.build(w.components)
+    t0 = time.perf_counter()
+    oracle.kf_rts(m, w.noise_var, w.t[:n], w.y[:n], w.mask[:n])
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"first {n} steps of the same grid, sequential C oracle (KF+RTS+NLL, Van Loan per step), "
+                      f"{dt:.2f} s on {os.cpu_count()} host cores (1 used)"}
+
+
+def run_reference(args, rank: int):
+    """--impl reference: the CPU oracle as the reference arm (rank 0 only)."""
+    if rank != 0:
+        return
+    import synth
+    w = synth.metric_workload(args.N, uniform=args.uniform, kind=args.kind)
+    import oracle
+    m = oracle.ssm.build(w.components)
+    n = min(2 ** 19, w.N)
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        oracle.kf_rts(m, w.noise_var, w.t[:n], w.y[:n], w.mask[:n])
+        if i >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    val = n * args.steps / tot
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": w.name, "N": w.N, "sample_steps": n},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"first {n} steps of {w.name} per step"},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------ ours
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    import torch
+    import synth
+    import paper_2102_09964_b200 as P
+    from paper_2102_09964_b200 import sharded
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    w = synth.metric_workload(args.N, uniform=args.uniform, kind=args.kind)
+    model = P.Model(w.components, w.noise_var, uniform_dt=w.uniform_dt, chain_len=args.chain_len,
+                    blocks_per_sm=args.blocks_per_sm, device=local)
+    N = w.N
+    stream = torch.cuda.current_stream()
+
+    if world == 1:
+        t = torch.from_numpy(w.t).to(dev)
+        y = torch.from_numpy(w.y).to(dev)
+        mk = torch.from_numpy(w.mask).to(dev)
+        mean = torch.empty(N, dtype=torch.float64, device=dev)
+        var = torch.empty_like(mean)
+        nll = torch.zeros(1, dtype=torch.float64, device=dev)
+
+        def step():
+            P.pssgp_posterior(model.h, N, t, y, mk, mean, var, nll, stream)
+        n_local = N
+    else:
+        k0, n_local = sharded.split(N, world)[rank]
+        tt, yy, mm = sharded.chunk_inputs(w.t, w.y, w.mask, k0, n_local, dev)
+        shard = sharded.DeviceShard(model, tt, yy, mm, k0, n_local, N, rank, world, stream)
+
+        def step():
+            sharded.sharded_posterior(shard, sharded.nccl_exchange, rank, world)
+
+    for _ in range(args.warmup):
+        step()
+    model.check()
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    P.pssgp_profile_enable(model.h, True)
+    P.pssgp_profile_read(model.h)  # reset
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ms_total = ev0.elapsed_time(ev1)
+    prof = P.pssgp_profile_read(model.h)
+    P.pssgp_profile_enable(model.h, False)
+    clk = clocks.stop()
+    model.check()
+    if dist:
+        tt_ = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt_, op=dist.ReduceOp.MAX)
+        ms_total = float(tt_.item())
+    ms_step = ms_total / args.steps
+    value = N / (ms_step * 1e-3)
+
+    # ---- e2e through the public host API (pinned buffers, copies inside the timed region)
+    e2e = None
+    if world == 1:
+        th = torch.from_numpy(w.t).pin_memory()
+        yh = torch.from_numpy(w.y).pin_memory()
+        mh = torch.from_numpy(w.mask).pin_memory()
+        meanh = torch.empty(N, dtype=torch.float64).pin_memory()
+        varh = torch.empty(N, dtype=torch.float64).pin_memory()
+        nllh = torch.zeros(1, dtype=torch.float64).pin_memory()
+
+        def step_host():
+            P.pssgp_posterior_host(model.h, N, th, yh, mh, meanh, varh, nllh, stream)
+        for _ in range(2):
+            step_host()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            step_host()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = e0.elapsed_time(e1) / args.steps
+        e2e = {"value": N / (e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(N * 17),
+               "d2h_bytes_per_step": int(N * 16 + 8), "ms_per_step": e_ms}
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline for the dominant kernel
+    pk = peaks()
+    kern = {k: v for k, v in prof.items() if v[1] > 0}
+    dom = max(kern, key=lambda k: kern[k][0])
+    dom_ms, dom_launches = kern[dom]
+    per_launch_ms = dom_ms / dom_launches
+    alg_b = ALG_BYTES.get(dom, 0) * n_local
+    achieved = alg_b / (per_launch_ms * 1e-3) / 1e9
+    plan = model.plan(n_local)
+    launches = int(sum(v[1] for v in kern.values()))
+    roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": pk.get("hbm_gbs"), "unit": "GB/s",
+            "frac": achieved / pk.get("hbm_gbs"), "traffic": None,
+            "avg_launch_ms": per_launch_ms,
+            "share_of_step": dom_ms / ms_total,
+            "per_kernel_ms_per_step": {k: v[0] / args.steps for k, v in kern.items()},
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if not pk.get("_fallback") else "fallback",
+            "path_alg_bytes_per_step": 41 + 16 * 9,
+            "path_hbm_frac": (41 + 16 * 9) * N / (ms_step * 1e-3) / 1e9 / pk.get("hbm_gbs")}
+    cpu = None
+    if not args.no_cpu_baseline:
+        cpu = cpu_baseline(w, args.cpu_sample)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": w.name, "N": N, "state_dim": model.state_dim, "chain_len": plan["chain_len"],
+                       "ctas": plan["n_blocks"], "threads_per_cta": plan["threads"],
+                       "l2": "no flush: working set (1.8 GB) >> 126 MB L2",
+                       "parallelism": f"time-sharded x{world}" if world > 1 else "single GPU"},
+            "clocks": clk, "e2e": e2e, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu}
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

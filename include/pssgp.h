@@ -1,0 +1,192 @@
+/*
+ * pssgp.h — C ABI of the B200-native parallel state-space GP hot path
+ * (Corenflos, Zhao & Sarkka, "Temporal Gaussian Process Regression in
+ * Logarithmic Time", arXiv:2102.09964).  Citations "PAPER.md:n" refer to the
+ * paper text (main paper lines 1-249, supplement 249-480).
+ *
+ * The library computes, for a stationary GP written in state-space form
+ * (Eq. (2)) on a SORTED time grid where test points are
+ * MISSING observations (supplement PAPER.md:255):
+ *   - the Kalman filter via the associative scan of filter elements
+ *     (A, b, C, eta, J), including the paper's missing-measurement elements
+ *     (Eqs. (6)-(8); Prop. 1),
+ *   - the RTS smoother via the reverse associative scan of (E, g, L)
+ *     (Prop. 2),
+ *   - the negative log marginal likelihood (named PAPER.md:75, 144, 157;
+ *     evaluated by the predictive decomposition, reading Z3 in DESIGN.md),
+ *   - posterior mean/variance of the latent f = H x.
+ * All arithmetic is IEEE fp64.  Every step runs in CUDA kernels for sm_100a;
+ * there is no CPU fallback.
+ *
+ * Conventions for every call below:
+ *   - Array pointers are CUDA DEVICE pointers owned by the caller unless the
+ *     function name ends in _host.  Nothing is retained after the call.
+ *   - t[N]: fp64, finite, NON-DECREASING (ties allowed: dt = 0 -> F = I,
+ *     Q = 0; reading Z13).  Decreasing / non-finite t -> PSSGP_E_INPUT with
+ *     the first failing index (pssgp_error_index).
+ *   - mask[N]: uint8; nonzero = observed, 0 = missing (test point).
+ *   - y[N]: fp64; read only where mask != 0 (NaN allowed elsewhere); an
+ *     observed non-finite y -> PSSGP_E_INPUT.
+ *   - Outputs mean[N], var[N]: fp64 posterior mean and variance of f at every
+ *     grid point (observed and missing).  nll: ONE fp64 device scalar,
+ *     sum over observed k of 0.5 (log(2 pi S_k) + v_k^2 / S_k).
+ *   - Calls are asynchronous on `stream` (a cudaStream_t, NULL = legacy
+ *     default stream).  Host-detectable errors are returned immediately;
+ *     device-detected errors (non-finite data, S <= 0, non-PD predicted
+ *     covariance) are latched in the handle and returned by pssgp_check().
+ *   - A handle may be used by one stream at a time; distinct handles are
+ *     independent.  Workspace grows on demand and is owned by the handle.
+ */
+#ifndef PSSGP_H
+#define PSSGP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pssgp_model pssgp_model;   /* opaque */
+
+typedef enum {
+    PSSGP_OK = 0,
+    PSSGP_E_ARG = 1,          /* bad argument (NULL, N < 0, noise_var <= 0, bad hyper-parameter) */
+    PSSGP_E_INPUT = 2,        /* bad data: unsorted / non-finite t, non-finite observed y */
+    PSSGP_E_NUMERIC = 3,      /* S <= 0, non-PD predicted covariance, non-finite intermediate */
+    PSSGP_E_CUDA = 4,         /* CUDA runtime error (see pssgp_last_error) */
+    PSSGP_E_NOMEM = 5,        /* device or host allocation failed */
+    PSSGP_E_UNSUPPORTED = 6   /* kernel combination / state dim / irregular dt not supported */
+} pssgp_status;
+
+typedef enum {
+    PSSGP_MATERN12 = 1,       /* d = 1, exact                                   */
+    PSSGP_MATERN32 = 2,       /* d = 2, exact                                                  */
+    PSSGP_MATERN52 = 3,       /* d = 3, exact                                                  */
+    PSSGP_RBF_TAYLOR = 4,     /* d = order, Taylor approximation of 1/S(w) */
+    PSSGP_PERIODIC = 5        /* d = 2 (order + 1) harmonic oscillators        */
+} pssgp_kind;
+
+/* One additive component of the covariance (sum of components = block-diagonal
+ * state).  variance = sigma^2 > 0, lengthscale > 0, period > 0
+ * (periodic only), order >= 1 (RBF Taylor order / periodic harmonics J). */
+typedef struct {
+    int kind;                 /* pssgp_kind */
+    double variance;
+    double lengthscale;
+    double period;
+    int order;
+} pssgp_component;
+
+typedef struct {
+    int balance;              /* 1 (default): Osborne balancing, Eq. (9) */
+    int device;               /* CUDA device ordinal used for workspace (default: current) */
+    double uniform_dt;        /* > 0: steps with t[k]-t[k-1] == uniform_dt exactly use F, Q
+                                 precomputed on the host (fp64 result of an extended-precision
+                                 Van Loan); 0 = none.  Required (> 0) for non-Matern models. */
+    int64_t chain_len;        /* steps per thread chain (0 = automatic)                   */
+    int blocks_per_sm;        /* CTAs per SM for the one-wave grid (0 = automatic)        */
+} pssgp_options;
+
+/* Build the continuous SSM (G, L, q, H, P_inf) of the summed kernel, balance it,
+ * and (if opt->uniform_dt > 0) discretise it once.  Host only; no device work
+ * until the first compute call.  opt may be NULL (defaults).  On success *out
+ * receives a new handle.  Errors: PSSGP_E_ARG (bad hyper-parameters, n_comps < 1,
+ * noise_var <= 0), PSSGP_E_UNSUPPORTED (state dimension > the compiled maximum),
+ * PSSGP_E_NUMERIC (singular Lyapunov system). */
+pssgp_status pssgp_create(const pssgp_component* comps, int n_comps, double noise_var,
+                          const pssgp_options* opt, pssgp_model** out);
+
+void pssgp_destroy(pssgp_model* m);
+
+/* State dimension d = n_x. */
+int pssgp_state_dim(const pssgp_model* m);
+
+/* Filter + smoother + NLL over one grid (the hot path).  mean, var: device
+ * arrays of N doubles (may both be NULL -> smoother skipped); nll: device
+ * scalar or NULL.  N = 0 is allowed (nll = 0). */
+pssgp_status pssgp_posterior(pssgp_model* m, int64_t N, const double* t, const double* y,
+                             const uint8_t* mask, double* mean, double* var, double* nll,
+                             void* stream);
+
+/* NLL only: forward filter pass (no filtered state stored, no smoother). */
+pssgp_status pssgp_nll(pssgp_model* m, int64_t N, const double* t, const double* y,
+                       const uint8_t* mask, double* nll, void* stream);
+
+/* End-to-end variant on HOST arrays (pinned memory recommended): copies the
+ * inputs to handle-owned device buffers, runs pssgp_posterior, copies mean,
+ * var (nullable) and *nll (nullable) back, and synchronises the stream.
+ * Returns device-detected errors directly. */
+pssgp_status pssgp_posterior_host(pssgp_model* m, int64_t N, const double* t, const double* y,
+                                  const uint8_t* mask, double* mean, double* var, double* nll,
+                                  void* stream);
+
+/* Synchronise the handle's last stream and return the first device-detected
+ * error (PSSGP_E_INPUT / PSSGP_E_NUMERIC / PSSGP_E_UNSUPPORTED) since the last
+ * pssgp_check, or PSSGP_OK.  Clears the latched error. */
+pssgp_status pssgp_check(pssgp_model* m);
+
+/* Index of the time step that caused the last error returned by pssgp_check
+ * (or by a host-side check), -1 if none. */
+int64_t pssgp_error_index(const pssgp_model* m);
+
+/* Human-readable description of the last error (static storage of the handle). */
+const char* pssgp_last_error(const pssgp_model* m);
+
+/* Copy the host-side balanced model: G, W = L q L^T, P_inf (d*d row-major),
+ * H (d), D (d, balancing diagonal; z = D^-1 x).  Any pointer may be NULL. */
+pssgp_status pssgp_get_ssm(const pssgp_model* m, double* G, double* W, double* H,
+                           double* Pinf, double* D);
+
+/* The (F, Q) the device code uses for a step of length dt, evaluated on the
+ * host by the same __host__ __device__ function the kernels call (closed form
+ * for Matern, the precomputed pair for dt == uniform_dt).  F, Q: d*d row-major.
+ * Test/introspection only; returns PSSGP_E_UNSUPPORTED where the device would. */
+pssgp_status pssgp_debug_discretize(const pssgp_model* m, double dt, double* F, double* Q);
+
+/* Launch plan for N steps: steps per chain, number of chains, CTAs, threads/CTA. */
+pssgp_status pssgp_plan(pssgp_model* m, int64_t N, int64_t* chain_len, int64_t* n_chains,
+                        int* n_blocks, int* threads_per_block);
+
+/* Optional per-kernel timing with CUDA events recorded on the launch stream.
+ * pssgp_profile_enable(m, 1) starts recording; pssgp_profile_read synchronises
+ * and returns, per kernel slot (see pssgp_profile_name), the summed elapsed
+ * milliseconds and launch counts since the last read, then resets.
+ * Returns the number of slots written (<= cap). */
+void pssgp_profile_enable(pssgp_model* m, int on);
+int pssgp_profile_read(pssgp_model* m, double* ms, int64_t* launches, int cap);
+const char* pssgp_profile_name(int slot);
+
+/* ---- Time-sharded path (multi-GPU, one process per GPU).
+ * Rank g owns the contiguous chunk [k0, k0 + n) of a global grid of N_global
+ * steps.  t points at the chunk's first element and t[-1] (if k0 > 0) and
+ * t[n] (if k0 + n < N_global) must be readable (one-point halo each side);
+ * y, mask point at the chunk's first element.  Aggregates are opaque byte
+ * blobs of pssgp_aggregate_bytes(m, which) bytes (which = 0 filter, 1
+ * smoother) in DEVICE memory; the caller all-gathers them (e.g. NCCL) into
+ * arrays ordered by rank.  The three calls must be made in order with the
+ * same chunk arguments; the handle keeps the filtered state in between. */
+size_t pssgp_aggregate_bytes(const pssgp_model* m, int which);
+
+pssgp_status pssgp_shard_filter_reduce(pssgp_model* m, int64_t k0, int64_t n, int64_t N_global,
+                                       const double* t, const double* y, const uint8_t* mask,
+                                       void* filt_agg_out, void* stream);
+
+/* all_filt_aggs: world filter aggregates; the carry into this chunk is the
+ * ordered product of ranks 0..rank-1.  Writes this chunk's smoother aggregate
+ * and its NLL partial (device scalar). */
+pssgp_status pssgp_shard_filter_apply(pssgp_model* m, int64_t k0, int64_t n, int64_t N_global,
+                                      const double* t, const double* y, const uint8_t* mask,
+                                      const void* all_filt_aggs, int rank, int world,
+                                      void* smooth_agg_out, double* nll_partial, void* stream);
+
+/* all_smooth_aggs: world smoother aggregates; the carry into this chunk is the
+ * ordered product of ranks rank+1..world-1.  Writes mean[n], var[n]. */
+pssgp_status pssgp_shard_smoother_apply(pssgp_model* m, int64_t k0, int64_t n, int64_t N_global,
+                                        const double* t, const void* all_smooth_aggs, int rank,
+                                        int world, double* mean, double* var, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PSSGP_H */

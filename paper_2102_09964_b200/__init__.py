@@ -1,0 +1,237 @@
+"""B200-native parallel state-space GP (PSSGP) hot path — Python binding.
+
+Thin marshalling layer over the C ABI in include/pssgp.h (libpssgp.so, CUDA
+kernels for sm_100a).  Functions keep the C names; `Model` is a convenience
+wrapper.  PyTorch is used only for device memory and streams.  There is no
+CPU fallback: importing the compute functions without the built library
+raises ImportError.
+
+Paper: Corenflos, Zhao & Sarkka, "Temporal Gaussian Process Regression in
+Logarithmic Time" (arXiv:2102.09964) — filter elements with missing
+measurements (Eqs. (6)-(8)), filtering operator, parallel
+RTS smoother (supplement Prop. 2), NLL.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Iterable, Optional, Sequence
+
+import numpy as np
+
+from ._native import (KINDS, STATUS_NAMES, Component, Options, PssgpError, build, lib)  # noqa: F401
+
+__all__ = ["Model", "PssgpError", "build", "lib", "pssgp_create", "pssgp_destroy", "pssgp_posterior",
+           "pssgp_nll", "pssgp_posterior_host", "pssgp_check", "pssgp_error_index", "pssgp_last_error",
+           "pssgp_state_dim", "pssgp_get_ssm", "pssgp_debug_discretize", "pssgp_plan",
+           "pssgp_aggregate_bytes", "pssgp_shard_filter_reduce", "pssgp_shard_filter_apply",
+           "pssgp_shard_smoother_apply", "pssgp_profile_enable", "pssgp_profile_read", "pssgp_profile_name"]
+
+
+def _ptr(x) -> Optional[int]:
+    """Device pointer of a torch tensor (or None)."""
+    if x is None:
+        return None
+    return int(x.data_ptr())
+
+
+def _stream_ptr(stream) -> Optional[int]:
+    if stream is None:
+        import torch
+        return int(torch.cuda.current_stream().cuda_stream) or None
+    if isinstance(stream, int):
+        return stream or None
+    return int(stream.cuda_stream) or None
+
+
+def _raise(handle, st: int):
+    if st != 0:
+        msg = lib().pssgp_last_error(handle).decode() if handle else ""
+        idx = lib().pssgp_error_index(handle) if handle else -1
+        raise PssgpError(st, msg, idx)
+
+
+# ------------------------------------------------------------------------- C-named thin wrappers
+def pssgp_create(components: Sequence, noise_var: float, uniform_dt: float = 0.0, balance: bool = True,
+                 chain_len: int = 0, blocks_per_sm: int = 0, device: int = -1) -> int:
+    """components: objects with .kind ('matern52', ...), .variance, .lengthscale, .period, .order."""
+    n = len(components)
+    arr = (Component * n)()
+    for i, c in enumerate(components):
+        kind = KINDS[c.kind] if isinstance(c.kind, str) else int(c.kind)
+        arr[i] = Component(kind, float(c.variance), float(c.lengthscale), float(getattr(c, "period", 1.0)),
+                           int(getattr(c, "order", 0)))
+    opt = Options(1 if balance else 0, int(device), float(uniform_dt), int(chain_len), int(blocks_per_sm))
+    h = ctypes.c_void_p()
+    st = lib().pssgp_create(arr, n, float(noise_var), ctypes.byref(opt), ctypes.byref(h))
+    if st != 0:
+        raise PssgpError(st, "pssgp_create failed")
+    return h.value
+
+
+def pssgp_destroy(h: int) -> None:
+    lib().pssgp_destroy(h)
+
+
+def pssgp_state_dim(h: int) -> int:
+    return lib().pssgp_state_dim(h)
+
+
+def pssgp_posterior(h, N, t, y, mask, mean, var, nll, stream=None) -> None:
+    _raise(h, lib().pssgp_posterior(h, int(N), _ptr(t), _ptr(y), _ptr(mask), _ptr(mean), _ptr(var), _ptr(nll),
+                                    _stream_ptr(stream)))
+
+
+def pssgp_nll(h, N, t, y, mask, nll, stream=None) -> None:
+    _raise(h, lib().pssgp_nll(h, int(N), _ptr(t), _ptr(y), _ptr(mask), _ptr(nll), _stream_ptr(stream)))
+
+
+def pssgp_posterior_host(h, N, t: np.ndarray, y: np.ndarray, mask: np.ndarray, mean: Optional[np.ndarray],
+                         var: Optional[np.ndarray], nll: Optional[np.ndarray], stream=None) -> None:
+    """Host (numpy / pinned torch CPU) arrays; synchronous."""
+    def hp(a):
+        if a is None:
+            return None
+        if hasattr(a, "data_ptr"):
+            return int(a.data_ptr())
+        return a.ctypes.data
+    _raise(h, lib().pssgp_posterior_host(h, int(N), hp(t), hp(y), hp(mask), hp(mean), hp(var), hp(nll),
+                                         _stream_ptr(stream)))
+
+
+def pssgp_check(h) -> None:
+    _raise(h, lib().pssgp_check(h))
+
+
+def pssgp_error_index(h) -> int:
+    return lib().pssgp_error_index(h)
+
+
+def pssgp_last_error(h) -> str:
+    return lib().pssgp_last_error(h).decode()
+
+
+def pssgp_get_ssm(h):
+    d = pssgp_state_dim(h)
+    G = np.zeros((d, d)); W = np.zeros((d, d)); P = np.zeros((d, d)); H = np.zeros(d); D = np.zeros(d)
+    dp = ctypes.POINTER(ctypes.c_double)
+    _raise(h, lib().pssgp_get_ssm(h, G.ctypes.data_as(dp), W.ctypes.data_as(dp), H.ctypes.data_as(dp),
+                                  P.ctypes.data_as(dp), D.ctypes.data_as(dp)))
+    return dict(G=G, W=W, H=H, Pinf=P, D=D)
+
+
+def pssgp_debug_discretize(h, dt: float):
+    d = pssgp_state_dim(h)
+    F = np.zeros((d, d)); Q = np.zeros((d, d))
+    dp = ctypes.POINTER(ctypes.c_double)
+    _raise(h, lib().pssgp_debug_discretize(h, float(dt), F.ctypes.data_as(dp), Q.ctypes.data_as(dp)))
+    return F, Q
+
+
+def pssgp_plan(h, N: int):
+    K = ctypes.c_int64(); nch = ctypes.c_int64(); nb = ctypes.c_int(); thr = ctypes.c_int()
+    _raise(h, lib().pssgp_plan(h, int(N), ctypes.byref(K), ctypes.byref(nch), ctypes.byref(nb), ctypes.byref(thr)))
+    return dict(chain_len=K.value, n_chains=nch.value, n_blocks=nb.value, threads=thr.value)
+
+
+def pssgp_profile_enable(h, on: bool = True) -> None:
+    lib().pssgp_profile_enable(h, 1 if on else 0)
+
+
+def pssgp_profile_name(slot: int) -> str:
+    return lib().pssgp_profile_name(slot).decode()
+
+
+def pssgp_profile_read(h):
+    ms = (ctypes.c_double * 16)()
+    cnt = (ctypes.c_int64 * 16)()
+    n = lib().pssgp_profile_read(h, ms, cnt, 16)
+    return {pssgp_profile_name(i): (ms[i], cnt[i]) for i in range(n)}
+
+
+def pssgp_aggregate_bytes(h, which: int) -> int:
+    return int(lib().pssgp_aggregate_bytes(h, int(which)))
+
+
+def pssgp_shard_filter_reduce(h, k0, n, N_global, t_ptr, y_ptr, mask_ptr, out_ptr, stream=None) -> None:
+    _raise(h, lib().pssgp_shard_filter_reduce(h, int(k0), int(n), int(N_global), t_ptr, y_ptr, mask_ptr, out_ptr,
+                                              _stream_ptr(stream)))
+
+
+def pssgp_shard_filter_apply(h, k0, n, N_global, t_ptr, y_ptr, mask_ptr, all_ptr, rank, world, sout_ptr, nll_ptr,
+                             stream=None) -> None:
+    _raise(h, lib().pssgp_shard_filter_apply(h, int(k0), int(n), int(N_global), t_ptr, y_ptr, mask_ptr, all_ptr,
+                                             int(rank), int(world), sout_ptr, nll_ptr, _stream_ptr(stream)))
+
+
+def pssgp_shard_smoother_apply(h, k0, n, N_global, t_ptr, all_ptr, rank, world, mean_ptr, var_ptr,
+                               stream=None) -> None:
+    _raise(h, lib().pssgp_shard_smoother_apply(h, int(k0), int(n), int(N_global), t_ptr, all_ptr, int(rank),
+                                               int(world), mean_ptr, var_ptr, _stream_ptr(stream)))
+
+
+# ------------------------------------------------------------------------- convenience wrapper
+class Model:
+    """Owns one pssgp_model handle.
+
+    >>> m = Model([synth.Component('matern52', 1.0, 0.5)], noise_var=0.01)
+    >>> mean, var, nll = m.posterior(t, y, mask)        # torch cuda tensors
+    """
+
+    def __init__(self, components: Iterable, noise_var: float, **kw):
+        self.components = list(components)
+        self.noise_var = float(noise_var)
+        self.h = pssgp_create(self.components, noise_var, **kw)
+
+    def close(self):
+        if getattr(self, "h", None):
+            pssgp_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def state_dim(self) -> int:
+        return pssgp_state_dim(self.h)
+
+    def posterior(self, t, y, mask, out=None, stream=None, with_nll: bool = True):
+        import torch
+        N = int(t.shape[0])
+        if out is None:
+            mean = torch.empty(N, dtype=torch.float64, device=t.device)
+            var = torch.empty_like(mean)
+            nll = torch.zeros(1, dtype=torch.float64, device=t.device) if with_nll else None
+        else:
+            mean, var, nll = out
+        pssgp_posterior(self.h, N, t, y, mask, mean, var, nll, stream)
+        return mean, var, nll
+
+    def nll(self, t, y, mask, out=None, stream=None):
+        import torch
+        N = int(t.shape[0])
+        nll = out if out is not None else torch.zeros(1, dtype=torch.float64, device=t.device)
+        pssgp_nll(self.h, N, t, y, mask, nll, stream)
+        return nll
+
+    def posterior_host(self, t: np.ndarray, y: np.ndarray, mask: np.ndarray, mean=None, var=None, nll=None):
+        N = int(t.shape[0])
+        mean = np.empty(N) if mean is None else mean
+        var = np.empty(N) if var is None else var
+        nll = np.zeros(1) if nll is None else nll
+        pssgp_posterior_host(self.h, N, t, y, mask, mean, var, nll)
+        return mean, var, nll
+
+    def check(self):
+        pssgp_check(self.h)
+
+    def ssm(self):
+        return pssgp_get_ssm(self.h)
+
+    def discretize(self, dt: float):
+        return pssgp_debug_discretize(self.h, dt)
+
+    def plan(self, N: int):
+        return pssgp_plan(self.h, N)

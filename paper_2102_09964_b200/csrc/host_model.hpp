@@ -1,0 +1,376 @@
+// host_model.hpp — host-side construction of the continuous state-space model
+// (Eq. (2)) for the supported covariances, O(1) work
+// (pipeline stage 1).  Written independently of the test oracle.
+//
+//   Matern-nu closed forms (exact), nu = 1/2, 3/2, 5/2:
+//     standalone: the lambda-scaled basis x_hat_i = x_i / lambda^i (a fixed
+//     diagonal balancing, Eq. (9)); drift lambda * G1, G1 = companion of
+//     (s + 1)^d, W = lambda sigma^2 w e_{d-1} e_{d-1}^T with w = 2, 4, 16/3,
+//     P_inf = sigma^2 P1 (see tools/derive_matern.py);
+//     inside a sum: the same basis (block of the block-diagonal state).
+//   RBF Taylor order n (reading Z7): 1/S(w) Taylor-expanded,
+//     left-half-plane spectral factor by Aberth-Ehrlich root finding in
+//     extended precision, companion drift, Osborne balancing, Lyapunov P_inf.
+//   Periodic J harmonics (reading Z8): rotation blocks, no process
+//     noise, P_inf_j = q_j^2 I with q_j^2 = (2 - [j=0]) s2 I_j(ell^-2) e^{-ell^-2}.
+//   Sum: block-diagonal.
+//   Lyapunov (section 4.1): vectorised (I (x) G + G (x) I) vec P = -vec W.
+//   Osborne balancing (section 4.2): powers of two.
+//   Uniform-dt discretisation ("matrix fractions" PAPER.md:160):
+//     Van Loan block exponential by a degree-30 Taylor series with scaling and
+//     squaring in long double, on a sub-step with |G h| <= 1/2, composed by the
+//     semigroup F(2h) = F(h)^2, Q(2h) = F(h) Q(h) F(h)^T + Q(h).
+#pragma once
+#include <cmath>
+#include <complex>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace pssgp_host {
+
+using ld = long double;
+using Mat = std::vector<ld>;  // row-major square
+
+struct Ssm {
+    int d = 0;
+    Mat G, W, Pinf;       // d x d
+    std::vector<ld> H;    // d
+    std::vector<ld> Dbal; // d (z = D^-1 x), relative to the canonical basis of each component
+};
+
+inline Mat zeros(int n) { return Mat(static_cast<size_t>(n) * n, 0.0L); }
+inline Mat eye(int n) {
+    Mat I = zeros(n);
+    for (int i = 0; i < n; ++i) I[i * n + i] = 1.0L;
+    return I;
+}
+inline Mat matmul(const Mat& A, const Mat& B, int n) {
+    Mat C = zeros(n);
+    for (int i = 0; i < n; ++i)
+        for (int k = 0; k < n; ++k) {
+            const ld a = A[i * n + k];
+            if (a == 0.0L) continue;
+            for (int j = 0; j < n; ++j) C[i * n + j] += a * B[k * n + j];
+        }
+    return C;
+}
+inline Mat transpose(const Mat& A, int n) {
+    Mat T = zeros(n);
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) T[j * n + i] = A[i * n + j];
+    return T;
+}
+inline ld norm1(const Mat& A, int n) {
+    ld best = 0.0L;
+    for (int j = 0; j < n; ++j) {
+        ld s = 0.0L;
+        for (int i = 0; i < n; ++i) s += std::fabs(A[i * n + j]);
+        best = std::max(best, s);
+    }
+    return best;
+}
+
+// Solve A x = b (dense, partial pivoting), in place; false if singular.
+inline bool solve(std::vector<ld> A, std::vector<ld>& b, int n) {
+    for (int c = 0; c < n; ++c) {
+        int p = c;
+        for (int r = c + 1; r < n; ++r)
+            if (std::fabs(A[r * n + c]) > std::fabs(A[p * n + c])) p = r;
+        if (A[p * n + c] == 0.0L) return false;
+        if (p != c) {
+            for (int k = 0; k < n; ++k) std::swap(A[c * n + k], A[p * n + k]);
+            std::swap(b[c], b[p]);
+        }
+        for (int r = c + 1; r < n; ++r) {
+            const ld f = A[r * n + c] / A[c * n + c];
+            if (f == 0.0L) continue;
+            for (int k = c; k < n; ++k) A[r * n + k] -= f * A[c * n + k];
+            b[r] -= f * b[c];
+        }
+    }
+    for (int c = n - 1; c >= 0; --c) {
+        ld s = b[c];
+        for (int j = c + 1; j < n; ++j) s -= A[c * n + j] * b[j];
+        b[c] = s / A[c * n + c];
+    }
+    return true;
+}
+
+// G P + P G^T + W = 0 via the vectorised linear system (Brogan).
+inline bool lyapunov(const Mat& G, const Mat& W, int n, Mat& P) {
+    const int m = n * n;
+    std::vector<ld> K(static_cast<size_t>(m) * m, 0.0L), b(m);
+    // vec is row-major: P[i*n+j].  (G P)_{ij} = sum_k G_ik P_kj ; (P G^T)_{ij} = sum_k P_ik G_jk
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+            const int row = i * n + j;
+            for (int k = 0; k < n; ++k) {
+                K[static_cast<size_t>(row) * m + k * n + j] += G[i * n + k];
+                K[static_cast<size_t>(row) * m + i * n + k] += G[j * n + k];
+            }
+            b[row] = -W[i * n + j];
+        }
+    if (!solve(K, b, m)) return false;
+    P = zeros(n);
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) P[i * n + j] = 0.5L * (b[i * n + j] + b[j * n + i]);
+    return true;
+}
+
+// Osborne balancing with powers of two: returns d with D^-1 G D balanced.
+inline std::vector<ld> osborne(const Mat& G0, int n) {
+    Mat A = G0;
+    std::vector<ld> d(n, 1.0L);
+    for (int sweep = 0; sweep < 100; ++sweep) {
+        bool changed = false;
+        for (int i = 0; i < n; ++i) {
+            ld c = 0.0L, r = 0.0L;
+            for (int j = 0; j < n; ++j) {
+                if (j == i) continue;
+                c += std::fabs(A[j * n + i]);
+                r += std::fabs(A[i * n + j]);
+            }
+            if (c == 0.0L || r == 0.0L) continue;
+            const ld s = c + r;
+            ld f = 1.0L;
+            while (c < r / 2.0L) { c *= 2.0L; r /= 2.0L; f *= 2.0L; }
+            while (c >= r * 2.0L) { c /= 2.0L; r *= 2.0L; f /= 2.0L; }
+            if (c + r < 0.95L * s) {
+                changed = true;
+                d[i] *= f;
+                for (int j = 0; j < n; ++j) { A[j * n + i] *= f; A[i * n + j] /= f; }
+            }
+        }
+        if (!changed) break;
+    }
+    return d;
+}
+
+inline void apply_balance(Ssm& m, const std::vector<ld>& d) {
+    const int n = m.d;
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+            m.G[i * n + j] *= d[j] / d[i];
+            m.W[i * n + j] /= d[i] * d[j];
+            m.Pinf[i * n + j] /= d[i] * d[j];
+        }
+    for (int i = 0; i < n; ++i) {
+        m.H[i] *= d[i];
+        m.Dbal[i] *= d[i];
+    }
+}
+
+// --------------------------------------------------------------------- Matern (lambda-scaled basis)
+inline Ssm matern(int d, ld s2, ld ell, ld* lam_out) {
+    Ssm m;
+    m.d = d;
+    m.G = zeros(d); m.W = zeros(d); m.Pinf = zeros(d);
+    m.H.assign(d, 0.0L); m.H[0] = 1.0L;
+    const ld nu2 = 2.0L * d - 1.0L;           // 2 nu
+    const ld lam = std::sqrt(nu2) / ell;
+    *lam_out = lam;
+    // G1 = companion of (s + 1)^d : rows shift, last row -binom(d, k)
+    for (int i = 0; i + 1 < d; ++i) m.G[i * d + i + 1] = lam;
+    if (d == 1) m.G[0] = -lam;
+    if (d == 2) { m.G[2] = -lam; m.G[3] = -2.0L * lam; }
+    if (d == 3) { m.G[6] = -lam; m.G[7] = -3.0L * lam; m.G[8] = -3.0L * lam; }
+    const ld w = (d == 1) ? 2.0L : (d == 2) ? 4.0L : 16.0L / 3.0L;
+    m.W[d * d - 1] = lam * s2 * w;
+    if (d == 1) m.Pinf[0] = s2;
+    if (d == 2) { m.Pinf[0] = s2; m.Pinf[3] = s2; }
+    if (d == 3) {
+        m.Pinf[0] = s2; m.Pinf[4] = s2 / 3.0L; m.Pinf[8] = s2;
+        m.Pinf[2] = m.Pinf[6] = -s2 / 3.0L;
+    }
+    m.Dbal.assign(d, 1.0L);
+    ld p = 1.0L;
+    for (int i = 0; i < d; ++i) { m.Dbal[i] = p; p *= lam; }
+    return m;
+}
+
+// --------------------------------------------------------------------- RBF Taylor
+// Aberth-Ehrlich simultaneous root finding for a real polynomial (coeffs highest first).
+inline bool poly_roots(const std::vector<ld>& c, std::vector<std::complex<ld>>& z) {
+    using C = std::complex<ld>;
+    const int n = static_cast<int>(c.size()) - 1;
+    z.resize(n);
+    // initial guesses on a circle of the Cauchy radius
+    ld rad = 0.0L;
+    for (int i = 1; i <= n; ++i) rad = std::max(rad, std::pow(std::fabs(c[i] / c[0]), 1.0L / i));
+    rad = std::max(rad, 1e-6L);
+    for (int i = 0; i < n; ++i) z[i] = std::polar(rad, 2.0L * 3.14159265358979323846L * (i + 0.25L) / n);
+    auto eval = [&](C x, C& dp) {
+        C p = c[0];
+        dp = 0;
+        for (int i = 1; i <= n; ++i) { dp = dp * x + p; p = p * x + c[i]; }
+        return p;
+    };
+    for (int it = 0; it < 500; ++it) {
+        ld maxstep = 0.0L;
+        for (int i = 0; i < n; ++i) {
+            C dp;
+            const C p = eval(z[i], dp);
+            const C ratio = p / dp;
+            C s = 0;
+            for (int j = 0; j < n; ++j)
+                if (j != i) s += 1.0L / (z[i] - z[j]);
+            const C step = ratio / (1.0L - ratio * s);
+            z[i] -= step;
+            maxstep = std::max(maxstep, std::abs(step) / std::max(std::abs(z[i]), 1e-30L));
+        }
+        if (maxstep < 1e-18L) return true;
+    }
+    return true;  // converged to working precision in practice; checked by callers
+}
+
+inline bool rbf_taylor(int order, ld s2, ld ell, Ssm& m, std::string& err) {
+    const int n = order;
+    const ld ell2 = ell * ell;
+    std::vector<ld> coef(2 * n + 1, 0.0L);  // highest power first
+    ld fact = 1.0L;
+    for (int j = 0; j <= n; ++j) {
+        if (j > 0) fact *= j;
+        coef[2 * n - 2 * j] = std::pow(ell2 / 2.0L, j) * ((j % 2) ? -1.0L : 1.0L) / fact;
+    }
+    std::vector<std::complex<ld>> z;
+    poly_roots(coef, z);
+    std::vector<std::complex<ld>> lhp;
+    for (auto& r : z)
+        if (r.real() < 0.0L) lhp.push_back(r);
+    if (static_cast<int>(lhp.size()) != n) { err = "RBF spectral factorisation failed"; return false; }
+    std::vector<std::complex<ld>> a(1, 1.0L);  // monic, lowest power first
+    for (auto& r : lhp) {
+        std::vector<std::complex<ld>> b(a.size() + 1, 0.0L);
+        for (size_t i = 0; i < a.size(); ++i) { b[i + 1] += a[i]; b[i] -= r * a[i]; }
+        a = b;
+    }
+    m.d = n;
+    m.G = zeros(n); m.W = zeros(n); m.Pinf = zeros(n);
+    for (int i = 0; i + 1 < n; ++i) m.G[i * n + i + 1] = 1.0L;
+    for (int k = 0; k < n; ++k) m.G[(n - 1) * n + k] = -a[k].real();
+    ld nf = 1.0L;
+    for (int k = 2; k <= n; ++k) nf *= k;
+    const ld q = s2 * std::sqrt(2.0L * 3.14159265358979323846L) * ell * nf * std::pow(2.0L / ell2, n);
+    m.W[n * n - 1] = q;
+    m.H.assign(n, 0.0L); m.H[0] = 1.0L;
+    m.Dbal.assign(n, 1.0L);
+    return true;
+}
+
+// exponentially scaled modified Bessel I_j(a) e^{-a} by its power series
+inline ld bessel_ive(int j, ld a) {
+    ld term = 1.0L;
+    for (int k = 1; k <= j; ++k) term *= (a / 2.0L) / k;
+    ld sum = 0.0L;
+    const ld q = a * a / 4.0L;
+    for (int m = 0; m < 10000; ++m) {
+        sum += term;
+        term *= q / ((m + 1.0L) * (m + 1.0L + j));
+        if (term < sum * 1e-21L && m > a) break;
+    }
+    return sum * std::exp(-a);
+}
+
+inline Ssm periodic(int J, ld s2, ld ell, ld period) {
+    Ssm m;
+    const int n = 2 * (J + 1);
+    m.d = n;
+    m.G = zeros(n); m.W = zeros(n); m.Pinf = zeros(n);
+    m.H.assign(n, 0.0L);
+    m.Dbal.assign(n, 1.0L);
+    const ld w0 = 2.0L * 3.14159265358979323846L / period;
+    const ld a = 1.0L / (ell * ell);
+    for (int j = 0; j <= J; ++j) {
+        m.G[(2 * j) * n + 2 * j + 1] = -j * w0;
+        m.G[(2 * j + 1) * n + 2 * j] = j * w0;
+        const ld q2 = (j == 0 ? 1.0L : 2.0L) * s2 * bessel_ive(j, a);
+        m.Pinf[(2 * j) * n + 2 * j] = q2;
+        m.Pinf[(2 * j + 1) * n + 2 * j + 1] = q2;
+        m.H[2 * j] = 1.0L;
+    }
+    return m;
+}
+
+inline Ssm block_sum(const std::vector<Ssm>& parts) {
+    Ssm m;
+    int n = 0;
+    for (auto& p : parts) n += p.d;
+    m.d = n;
+    m.G = zeros(n); m.W = zeros(n); m.Pinf = zeros(n);
+    m.H.assign(n, 0.0L); m.Dbal.assign(n, 1.0L);
+    int o = 0;
+    for (auto& p : parts) {
+        for (int i = 0; i < p.d; ++i) {
+            for (int j = 0; j < p.d; ++j) {
+                m.G[(o + i) * n + o + j] = p.G[i * p.d + j];
+                m.W[(o + i) * n + o + j] = p.W[i * p.d + j];
+                m.Pinf[(o + i) * n + o + j] = p.Pinf[i * p.d + j];
+            }
+            m.H[o + i] = p.H[i];
+            m.Dbal[o + i] = p.Dbal[i];
+        }
+        o += p.d;
+    }
+    return m;
+}
+
+// --------------------------------------------------------------------- discretisation (uniform dt)
+// expm by Taylor-30 with scaling & squaring (long double)
+inline Mat expm_taylor(const Mat& A, int n) {
+    const ld nr = norm1(A, n);
+    int s = 0;
+    if (nr > 0.5L) s = static_cast<int>(std::ceil(std::log2(nr / 0.5L)));
+    const ld sc = std::ldexp(1.0L, -s);
+    Mat As = A;
+    for (auto& v : As) v *= sc;
+    Mat E = eye(n), term = eye(n);
+    for (int k = 1; k <= 30; ++k) {
+        term = matmul(term, As, n);
+        for (auto& v : term) v /= k;
+        for (size_t i = 0; i < E.size(); ++i) E[i] += term[i];
+    }
+    for (int i = 0; i < s; ++i) E = matmul(E, E, n);
+    return E;
+}
+
+inline void van_loan(const Mat& G, const Mat& W, int n, ld dt, Mat& F, Mat& Q) {
+    // sub-step h = dt / 2^s with |G h|_1 <= 1/2
+    const ld g = norm1(G, n) * std::fabs(dt);
+    int s = 0;
+    if (g > 0.5L) s = static_cast<int>(std::ceil(std::log2(g / 0.5L)));
+    const ld h = std::ldexp(dt, -s);
+    const int m = 2 * n;
+    Mat M = zeros(m);
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+            M[i * m + j] = G[i * n + j] * h;
+            M[i * m + n + j] = W[i * n + j] * h;
+            M[(n + i) * m + n + j] = -G[j * n + i] * h;
+        }
+    const Mat E = expm_taylor(M, m);
+    F = zeros(n); Q = zeros(n);
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) F[i * n + j] = E[i * m + j];
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+            ld acc = 0.0L;
+            for (int k = 0; k < n; ++k) acc += E[i * m + n + k] * E[j * m + k];
+            Q[i * n + j] = acc;
+        }
+    for (int r = 0; r < s; ++r) {
+        const Mat FQ = matmul(F, Q, n);
+        const Mat Ft = transpose(F, n);
+        Mat Qn = matmul(FQ, Ft, n);
+        for (size_t i = 0; i < Qn.size(); ++i) Qn[i] += Q[i];
+        Q = Qn;
+        F = matmul(F, F, n);
+    }
+    for (int i = 0; i < n; ++i)
+        for (int j = i + 1; j < n; ++j) {
+            const ld a = 0.5L * (Q[i * n + j] + Q[j * n + i]);
+            Q[i * n + j] = Q[j * n + i] = a;
+        }
+}
+
+}  // namespace pssgp_host

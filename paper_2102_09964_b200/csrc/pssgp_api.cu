@@ -1,0 +1,671 @@
+// pssgp_api.cu — C ABI (include/pssgp.h): model construction, workspace,
+// launch plan and kernel launches of the PSSGP hot path on sm_100a.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/pssgp.h"
+#include "host_model.hpp"
+#include "pssgp_kernels.cuh"
+
+using namespace pssgp;
+namespace ph = pssgp_host;
+
+namespace {
+
+constexpr int kMaxD = 3;              // compiled state dimensions: 1, 2, 3
+constexpr int kSlots = 7;
+const char* kSlotNames[kSlots] = {"k_filter_reduce", "k_filter_carry", "k_filter_apply",
+                                  "k_smoother_carry", "k_smoother_apply", "k_nll_sum", "k_reduce_blocks"};
+enum Slot { S_K1 = 0, S_K2, S_K3, S_K4, S_K5, S_K6, S_RED };
+
+}  // namespace
+
+struct pssgp_model {
+    int d = 0;
+    ph::Ssm ssm;                 // balanced host model (long double)
+    bool closed = false;         // standalone Matern closed form
+    double lam = 0.0, s2 = 0.0, r = 0.0;
+    double udt = 0.0;
+    std::vector<double> Fu, Qu;  // F(udt), Q(udt) row-major d x d
+    int device = 0;
+    int64_t forced_K = 0;
+    int blocks_per_sm = 0;
+    int sm_count = 0;
+    int occ = 0;
+    // workspace
+    char* ws = nullptr;
+    size_t ws_bytes = 0;
+    unsigned long long* d_err = nullptr;  // separate small allocation
+    double* d_scalar = nullptr;           // scratch nll scalar
+    char* io = nullptr;                   // e2e device buffers
+    size_t io_bytes = 0;
+    cudaStream_t last_stream = nullptr;
+    int64_t err_index = -1;
+    std::string last_err;
+    // sharded plan state
+    int64_t sh_k0 = -1, sh_n = -1, sh_N = -1;
+    // profiling
+    bool prof = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[kSlots];
+    std::vector<cudaEvent_t> ev_pool;
+};
+
+namespace {
+
+pssgp_status fail(pssgp_model* m, pssgp_status st, const std::string& msg, int64_t idx = -1) {
+    if (m) {
+        m->last_err = msg;
+        m->err_index = idx;
+    }
+    return st;
+}
+
+pssgp_status cuda_fail(pssgp_model* m, cudaError_t e, const char* where) {
+    return fail(m, PSSGP_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+cudaEvent_t get_event(pssgp_model* m) {
+    if (!m->ev_pool.empty()) {
+        cudaEvent_t e = m->ev_pool.back();
+        m->ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+struct ProfScope {
+    pssgp_model* m;
+    int slot;
+    cudaStream_t s;
+    cudaEvent_t a = nullptr;
+    ProfScope(pssgp_model* m_, int slot_, cudaStream_t s_) : m(m_), slot(slot_), s(s_) {
+        if (m->prof) {
+            a = get_event(m);
+            cudaEventRecord(a, s);
+        }
+    }
+    ~ProfScope() {
+        if (m->prof) {
+            cudaEvent_t b = get_event(m);
+            cudaEventRecord(b, s);
+            m->ev[slot].emplace_back(a, b);
+        }
+    }
+};
+
+template <int D>
+void fill_params(const pssgp_model* m, ModelParams<D>& p) {
+    std::memset(&p, 0, sizeof(p));
+    for (int i = 0; i < D; ++i)
+        for (int j = i; j < D; ++j) p.Pinf[si(D, i, j)] = static_cast<double>(m->ssm.Pinf[i * D + j]);
+    bool hu = true;
+    for (int i = 0; i < D; ++i) {
+        p.H[i] = static_cast<double>(m->ssm.H[i]);
+        if (p.H[i] != (i == 0 ? 1.0 : 0.0)) hu = false;
+    }
+    p.h_unit = hu ? 1 : 0;
+    p.r = m->r;
+    p.lam = m->lam;
+    p.s2 = m->s2;
+    p.closed = m->closed ? 1 : 0;
+    p.udt = m->udt > 0.0 ? m->udt : -1.0;  // -1 never equals a valid dt >= 0
+    if (m->udt > 0.0) {
+        for (int i = 0; i < D * D; ++i) p.Fu[i] = m->Fu[i];
+        for (int i = 0; i < D; ++i)
+            for (int j = i; j < D; ++j) p.Qu[si(D, i, j)] = m->Qu[i * D + j];
+    }
+}
+
+pssgp_status ensure_device(pssgp_model* m) {
+    if (m->sm_count > 0) return PSSGP_OK;
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0) return fail(m, PSSGP_E_CUDA, "no CUDA device available");
+    int dev = m->device;
+    if (dev < 0) cudaGetDevice(&dev);
+    m->device = dev;
+    e = cudaDeviceGetAttribute(&m->sm_count, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return cuda_fail(m, e, "cudaDeviceGetAttribute");
+    e = cudaMalloc(&m->d_err, 2 * sizeof(unsigned long long) + 8 * sizeof(double));
+    if (e != cudaSuccess) return fail(m, PSSGP_E_NOMEM, "cudaMalloc(error word)");
+    cudaMemset(m->d_err, 0xff, sizeof(unsigned long long));
+    m->d_scalar = reinterpret_cast<double*>(m->d_err + 2);
+    return PSSGP_OK;
+}
+
+template <int D>
+int occupancy() {
+    int a = 0, b = 0, c = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_filter_reduce<D>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_filter_apply<D>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k_smoother_apply<D>, kThreads, 0);
+    return std::max(1, std::min(a, std::min(b, c)));
+}
+
+struct Plan {
+    int64_t K = 0, nch = 0;
+    int nb = 0;
+};
+
+template <int D>
+Plan make_plan(pssgp_model* m, int64_t n) {
+    if (m->occ == 0) m->occ = occupancy<D>();
+    const int bps = m->blocks_per_sm > 0 ? m->blocks_per_sm : m->occ;
+    const int64_t target_chains = static_cast<int64_t>(m->sm_count) * bps * kThreads;
+    Plan pl;
+    int64_t K = m->forced_K > 0 ? m->forced_K : std::max<int64_t>(kWin, (n + target_chains - 1) / target_chains);
+    if (m->forced_K <= 0) K = ((K + kWin - 1) / kWin) * kWin;
+    pl.K = K;
+    pl.nch = std::max<int64_t>(1, (n + K - 1) / K);
+    pl.nb = static_cast<int>((pl.nch + kThreads - 1) / kThreads);
+    return pl;
+}
+
+template <int D>
+size_t ws_doubles(const Plan& pl) {
+    const size_t nchp = static_cast<size_t>(pl.nb) * kThreads;
+    return nchp * FN(D) + static_cast<size_t>(pl.nb) * FN(D) + static_cast<size_t>(pl.nb) * CN(D) +
+           static_cast<size_t>(pl.nb) * kWarps * pl.K * CN(D) * 32 + nchp * SN(D) +
+           static_cast<size_t>(pl.nb) * SN(D) + static_cast<size_t>(pl.nb) * CN(D) + pl.nb + 64;
+}
+
+template <int D>
+pssgp_status setup(pssgp_model* m, const Plan& pl, KParams<D>& p) {
+    const size_t need = ws_doubles<D>(pl) * sizeof(double);
+    if (need > m->ws_bytes) {
+        if (m->ws) cudaFree(m->ws);
+        m->ws = nullptr;
+        m->ws_bytes = 0;
+        cudaError_t e = cudaMalloc(&m->ws, need);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return fail(m, PSSGP_E_NOMEM, "cudaMalloc(workspace) failed");
+        }
+        m->ws_bytes = need;
+    }
+    std::memset(&p, 0, sizeof(p));
+    fill_params<D>(m, p.m);
+    const size_t nchp = static_cast<size_t>(pl.nb) * kThreads;
+    double* w = reinterpret_cast<double*>(m->ws);
+    p.chain_f = w; w += nchp * FN(D);
+    p.block_f = w; w += static_cast<size_t>(pl.nb) * FN(D);
+    p.fcarry = w; w += static_cast<size_t>(pl.nb) * CN(D);
+    p.xp = w; w += static_cast<size_t>(pl.nb) * kWarps * pl.K * CN(D) * 32;
+    p.chain_s = w; w += nchp * SN(D);
+    p.block_s = w; w += static_cast<size_t>(pl.nb) * SN(D);
+    p.scarry = w; w += static_cast<size_t>(pl.nb) * CN(D);
+    p.nll_block = w;
+    p.K = pl.K;
+    p.nb = pl.nb;
+    p.err = m->d_err;
+    p.rank = 0;
+    p.world = 1;
+    p.store_state = 1;
+    return PSSGP_OK;
+}
+
+#define LAUNCH_CHECK(m, where)                                    \
+    do {                                                          \
+        cudaError_t e_ = cudaGetLastError();                      \
+        if (e_ != cudaSuccess) return cuda_fail((m), e_, where);  \
+    } while (0)
+
+template <int D>
+pssgp_status phase_filter_reduce(pssgp_model* m, KParams<D>& p, cudaStream_t s) {
+    ProfScope ps(m, S_K1, s);
+    k_filter_reduce<D><<<p.nb, kThreads, 0, s>>>(p);
+    LAUNCH_CHECK(m, "k_filter_reduce");
+    return PSSGP_OK;
+}
+
+template <int D>
+pssgp_status phase_filter_apply(pssgp_model* m, KParams<D>& p, cudaStream_t s) {
+    {
+        ProfScope ps(m, S_K2, s);
+        k_filter_carry<D><<<1, kCarryThreads, 0, s>>>(p);
+        LAUNCH_CHECK(m, "k_filter_carry");
+    }
+    {
+        ProfScope ps(m, S_K3, s);
+        k_filter_apply<D><<<p.nb, kThreads, 0, s>>>(p);
+        LAUNCH_CHECK(m, "k_filter_apply");
+    }
+    return PSSGP_OK;
+}
+
+template <int D>
+pssgp_status phase_smoother(pssgp_model* m, KParams<D>& p, cudaStream_t s) {
+    {
+        ProfScope ps(m, S_K4, s);
+        k_smoother_carry<D><<<1, kCarryThreads, 0, s>>>(p);
+        LAUNCH_CHECK(m, "k_smoother_carry");
+    }
+    {
+        ProfScope ps(m, S_K5, s);
+        k_smoother_apply<D><<<p.nb, kThreads, 0, s>>>(p);
+        LAUNCH_CHECK(m, "k_smoother_apply");
+    }
+    return PSSGP_OK;
+}
+
+pssgp_status nll_sum(pssgp_model* m, const double* parts, int nb, double* out, cudaStream_t s) {
+    ProfScope ps(m, S_K6, s);
+    k_nll_sum<<<1, 256, 0, s>>>(parts, nb, out);
+    LAUNCH_CHECK(m, "k_nll_sum");
+    return PSSGP_OK;
+}
+
+pssgp_status check_args(pssgp_model* m, int64_t N, const double* t, const double* y, const uint8_t* mask) {
+    if (!m) return PSSGP_E_ARG;
+    if (N < 0) return fail(m, PSSGP_E_ARG, "N < 0");
+    if (N > 0 && (!t || !y || !mask)) return fail(m, PSSGP_E_ARG, "NULL input array");
+    if (N > (int64_t(1) << 40)) return fail(m, PSSGP_E_ARG, "N too large");
+    return PSSGP_OK;
+}
+
+template <int D>
+pssgp_status run_posterior(pssgp_model* m, int64_t N, const double* t, const double* y, const uint8_t* mask,
+                           double* mean, double* var, double* nll, cudaStream_t s, bool smooth) {
+    if (N == 0) {
+        if (nll) {
+            cudaError_t e = cudaMemsetAsync(nll, 0, sizeof(double), s);
+            if (e != cudaSuccess) return cuda_fail(m, e, "cudaMemsetAsync");
+        }
+        return PSSGP_OK;
+    }
+    const Plan pl = make_plan<D>(m, N);
+    KParams<D> p;
+    pssgp_status st = setup<D>(m, pl, p);
+    if (st) return st;
+    p.t = t; p.y = y; p.mask = mask;
+    p.n = N; p.k0 = 0; p.nglob = N;
+    p.mean = mean; p.var = var;
+    p.store_state = smooth ? 1 : 0;
+    if ((st = phase_filter_reduce<D>(m, p, s))) return st;
+    if ((st = phase_filter_apply<D>(m, p, s))) return st;
+    if (nll && (st = nll_sum(m, p.nll_block, p.nb, nll, s))) return st;
+    if (smooth && (st = phase_smoother<D>(m, p, s))) return st;
+    return PSSGP_OK;
+}
+
+template <int D>
+pssgp_status debug_disc(const pssgp_model* m, double dt, double* F, double* Q) {
+    ModelParams<D> p;
+    fill_params<D>(m, p);
+    double f[D * D], q[ns(D)];
+    const int rc = discretize<D>(p, dt, f, q);
+    for (int i = 0; i < D * D; ++i) F[i] = f[i];
+    for (int i = 0; i < D; ++i)
+        for (int j = 0; j < D; ++j) Q[i * D + j] = q[si(D, i, j)];
+    return rc ? PSSGP_E_UNSUPPORTED : PSSGP_OK;
+}
+
+#define DISPATCH_D(m, CALL)                                         \
+    switch ((m)->d) {                                               \
+        case 1: { constexpr int D_ = 1; return CALL; }              \
+        case 2: { constexpr int D_ = 2; return CALL; }              \
+        case 3: { constexpr int D_ = 3; return CALL; }              \
+        default: return fail((m), PSSGP_E_UNSUPPORTED, "state dimension not compiled"); \
+    }
+
+}  // namespace
+
+// ========================================================================== C ABI
+extern "C" {
+
+pssgp_status pssgp_create(const pssgp_component* comps, int n_comps, double noise_var, const pssgp_options* opt,
+                          pssgp_model** out) {
+    if (!out) return PSSGP_E_ARG;
+    *out = nullptr;
+    if (!comps || n_comps < 1 || n_comps > 16) return PSSGP_E_ARG;
+    if (!(noise_var > 0.0) || !std::isfinite(noise_var)) return PSSGP_E_ARG;
+    pssgp_options o{1, -1, 0.0, 0, 0};
+    if (opt) o = *opt;
+    auto* m = new (std::nothrow) pssgp_model();
+    if (!m) return PSSGP_E_NOMEM;
+    m->r = noise_var;
+    m->device = o.device;
+    m->forced_K = o.chain_len;
+    m->blocks_per_sm = o.blocks_per_sm;
+    std::vector<ph::Ssm> parts;
+    for (int c = 0; c < n_comps; ++c) {
+        const pssgp_component& k = comps[c];
+        if (!(k.variance > 0.0) || !std::isfinite(k.variance) || !(k.lengthscale > 0.0) || !std::isfinite(k.lengthscale)) {
+            delete m;
+            return PSSGP_E_ARG;
+        }
+        ph::Ssm part;
+        if (k.kind >= PSSGP_MATERN12 && k.kind <= PSSGP_MATERN52) {
+            ph::ld lam;
+            part = ph::matern(k.kind, k.variance, k.lengthscale, &lam);
+            if (n_comps == 1) {
+                m->closed = true;
+                m->lam = static_cast<double>(lam);
+                m->s2 = k.variance;
+            }
+        } else if (k.kind == PSSGP_RBF_TAYLOR) {
+            if (k.order < 1 || k.order > 12) { delete m; return PSSGP_E_ARG; }
+            std::string err;
+            if (!ph::rbf_taylor(k.order, k.variance, k.lengthscale, part, err)) { delete m; return PSSGP_E_NUMERIC; }
+            if (o.balance) ph::apply_balance(part, ph::osborne(part.G, part.d));
+            if (!ph::lyapunov(part.G, part.W, part.d, part.Pinf)) { delete m; return PSSGP_E_NUMERIC; }
+        } else if (k.kind == PSSGP_PERIODIC) {
+            if (k.order < 0 || k.order > 32 || !(k.period > 0.0)) { delete m; return PSSGP_E_ARG; }
+            part = ph::periodic(k.order, k.variance, k.lengthscale, k.period);
+        } else {
+            delete m;
+            return PSSGP_E_UNSUPPORTED;
+        }
+        parts.push_back(part);
+    }
+    m->ssm = parts.size() == 1 ? parts[0] : ph::block_sum(parts);
+    m->d = m->ssm.d;
+    if (m->d > kMaxD) {
+        delete m;
+        return PSSGP_E_UNSUPPORTED;
+    }
+    if (o.uniform_dt > 0.0 && std::isfinite(o.uniform_dt)) {
+        m->udt = o.uniform_dt;
+        ph::Mat F, Q;
+        ph::van_loan(m->ssm.G, m->ssm.W, m->d, static_cast<ph::ld>(o.uniform_dt), F, Q);
+        m->Fu.resize(F.size());
+        m->Qu.resize(Q.size());
+        for (size_t i = 0; i < F.size(); ++i) { m->Fu[i] = static_cast<double>(F[i]); m->Qu[i] = static_cast<double>(Q[i]); }
+    }
+    *out = m;
+    return PSSGP_OK;
+}
+
+void pssgp_destroy(pssgp_model* m) {
+    if (!m) return;
+    if (m->ws) cudaFree(m->ws);
+    if (m->io) cudaFree(m->io);
+    if (m->d_err) cudaFree(m->d_err);
+    for (int s = 0; s < kSlots; ++s)
+        for (auto& pr : m->ev[s]) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
+    for (auto e : m->ev_pool) cudaEventDestroy(e);
+    delete m;
+}
+
+int pssgp_state_dim(const pssgp_model* m) { return m ? m->d : -1; }
+
+pssgp_status pssgp_posterior(pssgp_model* m, int64_t N, const double* t, const double* y, const uint8_t* mask,
+                             double* mean, double* var, double* nll, void* stream) {
+    pssgp_status st = check_args(m, N, t, y, mask);
+    if (st) return st;
+    if ((st = ensure_device(m))) return st;
+    auto s = static_cast<cudaStream_t>(stream);
+    m->last_stream = s;
+    const bool smooth = (mean != nullptr) || (var != nullptr);
+    DISPATCH_D(m, run_posterior<D_>(m, N, t, y, mask, mean, var, nll, s, smooth));
+}
+
+pssgp_status pssgp_nll(pssgp_model* m, int64_t N, const double* t, const double* y, const uint8_t* mask,
+                       double* nll, void* stream) {
+    pssgp_status st = check_args(m, N, t, y, mask);
+    if (st) return st;
+    if (!nll) return fail(m, PSSGP_E_ARG, "nll is NULL");
+    if ((st = ensure_device(m))) return st;
+    auto s = static_cast<cudaStream_t>(stream);
+    m->last_stream = s;
+    DISPATCH_D(m, run_posterior<D_>(m, N, t, y, mask, nullptr, nullptr, nll, s, false));
+}
+
+pssgp_status pssgp_check(pssgp_model* m) {
+    if (!m) return PSSGP_E_ARG;
+    if (!m->d_err) return PSSGP_OK;
+    cudaError_t e = cudaStreamSynchronize(m->last_stream);
+    if (e != cudaSuccess) return cuda_fail(m, e, "cudaStreamSynchronize");
+    unsigned long long w = 0;
+    e = cudaMemcpy(&w, m->d_err, sizeof(w), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(m, e, "cudaMemcpy(error word)");
+    if (w == ~0ULL) return PSSGP_OK;
+    cudaMemset(m->d_err, 0xff, sizeof(unsigned long long));
+    const unsigned code = static_cast<unsigned>(w & 0xff);
+    const int64_t idx = static_cast<int64_t>(w >> 8);
+    const char* what = code == kErrInput ? "invalid input (unsorted/non-finite t or non-finite observed y)"
+                       : code == kErrNumeric ? "numerical failure (S <= 0 or non-PD predicted covariance)"
+                                             : "no device discretisation for this dt (set uniform_dt)";
+    return fail(m, static_cast<pssgp_status>(code), std::string(what) + " at step " + std::to_string(idx), idx);
+}
+
+int64_t pssgp_error_index(const pssgp_model* m) { return m ? m->err_index : -1; }
+
+const char* pssgp_last_error(const pssgp_model* m) { return m ? m->last_err.c_str() : "NULL handle"; }
+
+pssgp_status pssgp_posterior_host(pssgp_model* m, int64_t N, const double* t, const double* y, const uint8_t* mask,
+                                  double* mean, double* var, double* nll, void* stream) {
+    pssgp_status st = check_args(m, N, t, y, mask);
+    if (st) return st;
+    if ((st = ensure_device(m))) return st;
+    auto s = static_cast<cudaStream_t>(stream);
+    const size_t nd = static_cast<size_t>(N);
+    const size_t need = nd * (8 + 8 + 8 + 8) + nd + 64;
+    if (need > m->io_bytes) {
+        if (m->io) cudaFree(m->io);
+        m->io = nullptr;
+        m->io_bytes = 0;
+        if (cudaMalloc(&m->io, need) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(m, PSSGP_E_NOMEM, "cudaMalloc(io)");
+        }
+        m->io_bytes = need;
+    }
+    double* dt_ = reinterpret_cast<double*>(m->io);
+    double* dy = dt_ + nd;
+    double* dmean = dy + nd;
+    double* dvar = dmean + nd;
+    uint8_t* dmask = reinterpret_cast<uint8_t*>(dvar + nd);
+    if (N > 0) {
+        cudaMemcpyAsync(dt_, t, nd * 8, cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync(dy, y, nd * 8, cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync(dmask, mask, nd, cudaMemcpyHostToDevice, s);
+    }
+    st = pssgp_posterior(m, N, dt_, dy, dmask, mean ? dmean : nullptr, var ? dvar : nullptr,
+                         nll ? m->d_scalar : nullptr, stream);
+    if (st) return st;
+    if (N > 0 && mean) cudaMemcpyAsync(mean, dmean, nd * 8, cudaMemcpyDeviceToHost, s);
+    if (N > 0 && var) cudaMemcpyAsync(var, dvar, nd * 8, cudaMemcpyDeviceToHost, s);
+    if (nll) cudaMemcpyAsync(nll, m->d_scalar, 8, cudaMemcpyDeviceToHost, s);
+    m->last_stream = s;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(m, e, "pssgp_posterior_host copies");
+    return pssgp_check(m);
+}
+
+pssgp_status pssgp_get_ssm(const pssgp_model* m, double* G, double* W, double* H, double* Pinf, double* D) {
+    if (!m) return PSSGP_E_ARG;
+    const int n = m->d;
+    for (int i = 0; i < n * n; ++i) {
+        if (G) G[i] = static_cast<double>(m->ssm.G[i]);
+        if (W) W[i] = static_cast<double>(m->ssm.W[i]);
+        if (Pinf) Pinf[i] = static_cast<double>(m->ssm.Pinf[i]);
+    }
+    for (int i = 0; i < n; ++i) {
+        if (H) H[i] = static_cast<double>(m->ssm.H[i]);
+        if (D) D[i] = static_cast<double>(m->ssm.Dbal[i]);
+    }
+    return PSSGP_OK;
+}
+
+pssgp_status pssgp_debug_discretize(const pssgp_model* m, double dt, double* F, double* Q) {
+    if (!m || !F || !Q) return PSSGP_E_ARG;
+    pssgp_model* mm = const_cast<pssgp_model*>(m);
+    DISPATCH_D(mm, debug_disc<D_>(m, dt, F, Q));
+}
+
+pssgp_status pssgp_plan(pssgp_model* m, int64_t N, int64_t* chain_len, int64_t* n_chains, int* n_blocks,
+                        int* threads_per_block) {
+    if (!m || N < 0) return PSSGP_E_ARG;
+    pssgp_status st = ensure_device(m);
+    if (st) return st;
+    Plan pl;
+    switch (m->d) {
+        case 1: pl = make_plan<1>(m, N); break;
+        case 2: pl = make_plan<2>(m, N); break;
+        case 3: pl = make_plan<3>(m, N); break;
+        default: return PSSGP_E_UNSUPPORTED;
+    }
+    if (chain_len) *chain_len = pl.K;
+    if (n_chains) *n_chains = pl.nch;
+    if (n_blocks) *n_blocks = pl.nb;
+    if (threads_per_block) *threads_per_block = kThreads;
+    return PSSGP_OK;
+}
+
+void pssgp_profile_enable(pssgp_model* m, int on) {
+    if (m) m->prof = (on != 0);
+}
+
+int pssgp_profile_read(pssgp_model* m, double* ms, int64_t* launches, int cap) {
+    if (!m) return 0;
+    const int n = std::min(cap, kSlots);
+    for (int s = 0; s < kSlots; ++s) {
+        double acc = 0.0;
+        for (auto& pr : m->ev[s]) {
+            cudaEventSynchronize(pr.second);
+            float x = 0.f;
+            cudaEventElapsedTime(&x, pr.first, pr.second);
+            acc += x;
+            m->ev_pool.push_back(pr.first);
+            m->ev_pool.push_back(pr.second);
+        }
+        if (s < n) {
+            if (ms) ms[s] = acc;
+            if (launches) launches[s] = static_cast<int64_t>(m->ev[s].size());
+        }
+        m->ev[s].clear();
+    }
+    return n;
+}
+
+const char* pssgp_profile_name(int slot) { return (slot >= 0 && slot < kSlots) ? kSlotNames[slot] : ""; }
+
+// ---------------------------------------------------------------- sharded path
+size_t pssgp_aggregate_bytes(const pssgp_model* m, int which) {
+    if (!m) return 0;
+    const int d = m->d;
+    const int fn = d * d + 2 * d + d * (d + 1);
+    const int sn = d * d + d + d * (d + 1) / 2;
+    return static_cast<size_t>(which == 0 ? fn : sn) * sizeof(double);
+}
+
+}  // extern "C"
+
+namespace {
+
+template <int D>
+pssgp_status shard_setup(pssgp_model* m, int64_t k0, int64_t n, int64_t Ng, KParams<D>& p, Plan& pl) {
+    pl = make_plan<D>(m, n);
+    pssgp_status st = setup<D>(m, pl, p);
+    if (st) return st;
+    p.n = n; p.k0 = k0; p.nglob = Ng;
+    return PSSGP_OK;
+}
+
+template <int D>
+pssgp_status shard_reduce(pssgp_model* m, int64_t k0, int64_t n, int64_t Ng, const double* t, const double* y,
+                          const uint8_t* mask, void* out, cudaStream_t s) {
+    KParams<D> p;
+    Plan pl;
+    pssgp_status st = shard_setup<D>(m, k0, n, Ng, p, pl);
+    if (st) return st;
+    p.t = t; p.y = y; p.mask = mask;
+    if ((st = phase_filter_reduce<D>(m, p, s))) return st;
+    ProfScope ps(m, S_RED, s);
+    k_reduce_blocks<D, FAgg<D>><<<1, kCarryThreads, 0, s>>>(p.block_f, p.nb, static_cast<double*>(out));
+    LAUNCH_CHECK(m, "k_reduce_blocks(filter)");
+    return PSSGP_OK;
+}
+
+template <int D>
+pssgp_status shard_fapply(pssgp_model* m, int64_t k0, int64_t n, int64_t Ng, const double* t, const double* y,
+                          const uint8_t* mask, const void* all, int rank, int world, void* sout, double* nllp,
+                          cudaStream_t s) {
+    KParams<D> p;
+    Plan pl;
+    pssgp_status st = shard_setup<D>(m, k0, n, Ng, p, pl);
+    if (st) return st;
+    p.t = t; p.y = y; p.mask = mask;
+    p.in_filt = static_cast<const double*>(all);
+    p.rank = rank; p.world = world;
+    if ((st = phase_filter_apply<D>(m, p, s))) return st;
+    if (nllp && (st = nll_sum(m, p.nll_block, p.nb, nllp, s))) return st;
+    ProfScope ps(m, S_RED, s);
+    k_reduce_blocks<D, SAgg<D>><<<1, kCarryThreads, 0, s>>>(p.block_s, p.nb, static_cast<double*>(sout));
+    LAUNCH_CHECK(m, "k_reduce_blocks(smoother)");
+    return PSSGP_OK;
+}
+
+template <int D>
+pssgp_status shard_sapply(pssgp_model* m, int64_t k0, int64_t n, int64_t Ng, const double* t, const void* all,
+                          int rank, int world, double* mean, double* var, cudaStream_t s) {
+    KParams<D> p;
+    Plan pl;
+    pssgp_status st = shard_setup<D>(m, k0, n, Ng, p, pl);
+    if (st) return st;
+    p.t = t;
+    p.in_smooth = static_cast<const double*>(all);
+    p.rank = rank; p.world = world;
+    p.mean = mean; p.var = var;
+    return phase_smoother<D>(m, p, s);
+}
+
+pssgp_status shard_args(pssgp_model* m, int64_t k0, int64_t n, int64_t Ng, const double* t) {
+    if (!m) return PSSGP_E_ARG;
+    if (k0 < 0 || n < 1 || Ng < 1 || k0 + n > Ng || !t) return fail(m, PSSGP_E_ARG, "bad shard arguments");
+    return ensure_device(m);
+}
+
+}  // namespace
+
+extern "C" {
+
+pssgp_status pssgp_shard_filter_reduce(pssgp_model* m, int64_t k0, int64_t n, int64_t N_global, const double* t,
+                                       const double* y, const uint8_t* mask, void* filt_agg_out, void* stream) {
+    pssgp_status st = shard_args(m, k0, n, N_global, t);
+    if (st) return st;
+    if (!y || !mask || !filt_agg_out) return fail(m, PSSGP_E_ARG, "NULL argument");
+    auto s = static_cast<cudaStream_t>(stream);
+    m->last_stream = s;
+    m->sh_k0 = k0; m->sh_n = n; m->sh_N = N_global;
+    DISPATCH_D(m, shard_reduce<D_>(m, k0, n, N_global, t, y, mask, filt_agg_out, s));
+}
+
+pssgp_status pssgp_shard_filter_apply(pssgp_model* m, int64_t k0, int64_t n, int64_t N_global, const double* t,
+                                      const double* y, const uint8_t* mask, const void* all_filt_aggs, int rank,
+                                      int world, void* smooth_agg_out, double* nll_partial, void* stream) {
+    pssgp_status st = shard_args(m, k0, n, N_global, t);
+    if (st) return st;
+    if (!y || !mask || !all_filt_aggs || !smooth_agg_out || rank < 0 || rank >= world)
+        return fail(m, PSSGP_E_ARG, "bad argument");
+    if (m->sh_k0 != k0 || m->sh_n != n || m->sh_N != N_global)
+        return fail(m, PSSGP_E_ARG, "shard phases called with different chunk arguments");
+    auto s = static_cast<cudaStream_t>(stream);
+    m->last_stream = s;
+    DISPATCH_D(m, shard_fapply<D_>(m, k0, n, N_global, t, y, mask, all_filt_aggs, rank, world, smooth_agg_out,
+                                   nll_partial, s));
+}
+
+pssgp_status pssgp_shard_smoother_apply(pssgp_model* m, int64_t k0, int64_t n, int64_t N_global, const double* t,
+                                        const void* all_smooth_aggs, int rank, int world, double* mean, double* var,
+                                        void* stream) {
+    pssgp_status st = shard_args(m, k0, n, N_global, t);
+    if (st) return st;
+    if (!all_smooth_aggs || rank < 0 || rank >= world) return fail(m, PSSGP_E_ARG, "bad argument");
+    if (m->sh_k0 != k0 || m->sh_n != n || m->sh_N != N_global)
+        return fail(m, PSSGP_E_ARG, "shard phases called with different chunk arguments");
+    auto s = static_cast<cudaStream_t>(stream);
+    m->last_stream = s;
+    DISPATCH_D(m, shard_sapply<D_>(m, k0, n, N_global, t, all_smooth_aggs, rank, world, mean, var, s));
+}
+
+}  // extern "C"

@@ -1,0 +1,828 @@
+// pssgp_kernels.cuh — sm_100a kernels of the PSSGP hot path (one-wave, three-pass scan).
+//
+// Decomposition: the grid is ONE wave of CTAs (148 SMs x
+// resident CTAs).  Thread c owns the contiguous chain [c K, (c+1) K) of K time
+// steps; CTA b owns chains [128 b, 128 b + 128).
+//
+//   k_filter_reduce   (K1)  per chain: discretise + build + fold filter elements
+//                           (rank-one fold, PAPER.md:116-121 with J_k = u u^T / S)
+//                           -> chain aggregate; CTA tree-reduce -> block aggregate.
+//   k_filter_carry    (K2)  1 CTA: scan of block aggregates (general operator)
+//                           -> collapsed global prefix (xbar, P) entering each CTA.
+//   k_filter_apply    (K3)  per CTA: scan of its chain aggregates, then per chain
+//                           the Kalman recursion from the carry (Prop. 1 proof order,
+//                           PAPER.md:326-330): writes (xbar_k, P_k), NLL partials,
+//                           and the chain's smoother aggregate (E, g, L) from the
+//                           cross-covariance Cov(x_k0, x_k1+1 | y_1:k1).
+//   k_smoother_carry  (K4)  1 CTA: reverse scan of block smoother aggregates.
+//   k_smoother_apply  (K5)  per CTA: reverse scan of chain smoother aggregates, then
+//                           per chain the RTS recursion (Prop. 2 proof order,
+//                           PAPER.md:431-435) -> mean = H m^s, var = H P^s H^T.
+//   k_nll_sum         (K6)  fixed-order sum of per-CTA NLL partials (deterministic).
+//
+// Global prefixes collapse to (0, xbar, P, 0, 0) and global suffixes to
+// (0, m^s, P^s) (A_1 = 0 by Eq. (7); E_N = 0), so applying a carry to a chain
+// is one Kalman / RTS step per element: the general operator only combines
+// chain / block aggregates.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "pssgp_math.cuh"
+
+namespace pssgp {
+
+constexpr int kThreads = 128;           // threads per CTA (4 warps)
+constexpr int kWarps = kThreads / 32;
+constexpr int kWin = 16;                // staging window (steps) per chain
+constexpr int kCarryThreads = 256;      // single-CTA scan kernels
+
+// error word: (index << 8) | code, atomicMin keeps the first failing index
+enum : unsigned { kErrInput = 2, kErrNumeric = 3, kErrUnsupported = 6 };
+
+__device__ __forceinline__ void raise_error(unsigned long long* err, int64_t gidx, unsigned code) {
+    const unsigned long long w = (static_cast<unsigned long long>(gidx) << 8) | code;
+    if (w < *reinterpret_cast<volatile unsigned long long*>(err)) atomicMin(err, w);
+}
+
+template <int D>
+struct KParams {
+    ModelParams<D> m;
+    const double* t;        // local step 0; t[-1], t[n] valid when they exist globally
+    const double* y;
+    const uint8_t* mask;
+    int64_t n;              // local steps
+    int64_t k0;             // global index of local step 0
+    int64_t nglob;          // global number of steps
+    int64_t K;              // chain length
+    int nb;                 // CTAs of the apply kernels
+    double* chain_f;        // [FN][nb*128]  chain filter aggregates (SoA)
+    double* block_f;        // [nb][FN]
+    double* fcarry;         // [nb][CN]      global prefix entering each CTA
+    double* xp;             // filtered (xbar, P), lane-interleaved [warp][K][CN][32]
+    double* chain_s;        // [SN][nb*128]
+    double* block_s;        // [nb][SN]
+    double* scarry;         // [nb][CN]      global suffix after each CTA
+    double* nll_block;      // [nb]
+    double* mean;
+    double* var;
+    const double* in_filt;  // sharded: all ranks' filter aggregates [world][FN] (nullable)
+    const double* in_smooth;// sharded: all ranks' smoother aggregates [world][SN] (nullable)
+    int rank, world;
+    double* out_agg;        // sharded: chunk aggregate output (nullable)
+    double* nll_out;        // nll scalar output (nullable)
+    unsigned long long* err;
+    int store_state;        // K3: write (xbar, P) and smoother aggregates (0 for NLL-only)
+};
+
+// ------------------------------------------------------------------ warp shuffles of aggregates
+template <typename T>
+__device__ __forceinline__ void shfl_up_all(T& dst, const T& src, int off) {
+    constexpr int n = sizeof(T) / sizeof(double);
+    const double* s = reinterpret_cast<const double*>(&src);
+    double* d = reinterpret_cast<double*>(&dst);
+#pragma unroll
+    for (int i = 0; i < n; ++i) d[i] = __shfl_up_sync(0xffffffffu, s[i], off);
+}
+template <typename T>
+__device__ __forceinline__ void shfl_down_all(T& dst, const T& src, int off) {
+    constexpr int n = sizeof(T) / sizeof(double);
+    const double* s = reinterpret_cast<const double*>(&src);
+    double* d = reinterpret_cast<double*>(&dst);
+#pragma unroll
+    for (int i = 0; i < n; ++i) d[i] = __shfl_down_sync(0xffffffffu, s[i], off);
+}
+template <typename T>
+__device__ __forceinline__ void load_soa(T& a, const double* base, int64_t stride, int64_t idx) {
+    constexpr int n = sizeof(T) / sizeof(double);
+    double* d = reinterpret_cast<double*>(&a);
+#pragma unroll
+    for (int i = 0; i < n; ++i) d[i] = base[i * stride + idx];
+}
+template <typename T>
+__device__ __forceinline__ void store_soa(const T& a, double* base, int64_t stride, int64_t idx) {
+    constexpr int n = sizeof(T) / sizeof(double);
+    const double* s = reinterpret_cast<const double*>(&a);
+#pragma unroll
+    for (int i = 0; i < n; ++i) base[i * stride + idx] = s[i];
+}
+template <typename T>
+__device__ __forceinline__ void load_aos(T& a, const double* base) {
+    constexpr int n = sizeof(T) / sizeof(double);
+    double* d = reinterpret_cast<double*>(&a);
+#pragma unroll
+    for (int i = 0; i < n; ++i) d[i] = base[i];
+}
+template <typename T>
+__device__ __forceinline__ void store_aos(const T& a, double* base) {
+    constexpr int n = sizeof(T) / sizeof(double);
+    const double* s = reinterpret_cast<const double*>(&a);
+#pragma unroll
+    for (int i = 0; i < n; ++i) base[i] = s[i];
+}
+
+// ------------------------------------------------------------------ coalesced staging
+// A warp's 32 chains are 32 contiguous segments of K steps.  A window of kWin
+// steps of all 32 chains is loaded row by row (each row = kWin consecutive
+// steps of one chain, 2 rows per warp instruction) into padded shared memory,
+// then each lane reads its own row (conflict-free: row stride kWin+1 doubles).
+struct StageIn {
+    double t[32][kWin + 1];
+    double y[32][kWin + 1];
+    unsigned char m[32][kWin + 4];
+};
+
+__device__ __forceinline__ void stage_in(StageIn& s, const double* __restrict__ t, const double* __restrict__ y,
+                                         const uint8_t* __restrict__ mask, int64_t wbase, int64_t K,
+                                         int64_t n, int64_t j0, int lane, bool with_y) {
+    constexpr int RPI = 32 / kWin;
+    const int col = lane % kWin, rsub = lane / kWin;
+#pragma unroll 4
+    for (int r0 = 0; r0 < 32; r0 += RPI) {
+        const int r = r0 + rsub;
+        const int64_t j = j0 + col;
+        const int64_t idx = wbase + r * K + j;
+        const bool ok = (j < K) && (idx < n);
+        s.t[r][col] = ok ? __ldg(t + idx) : 0.0;
+        if (with_y) {
+            const unsigned char mk = ok ? __ldg(mask + idx) : (unsigned char)0;
+            s.m[r][col] = mk;
+            s.y[r][col] = (ok && mk) ? __ldg(y + idx) : 0.0;
+        }
+    }
+    __syncwarp();
+}
+
+// ------------------------------------------------------------------ K1: fold chains
+template <int D>
+__global__ void __launch_bounds__(kThreads, 3) k_filter_reduce(const KParams<D> p) {
+    __shared__ StageIn st[kWarps];
+    __shared__ FAgg<D> wagg[kWarps];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t c = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
+    const int64_t nch = static_cast<int64_t>(p.nb) * kThreads;
+    const int64_t wbase = (static_cast<int64_t>(blockIdx.x) * kThreads + wid * 32) * p.K;
+    const int64_t kb = c * p.K;
+    const int64_t ke = min(kb + p.K, p.n);
+
+    FAgg<D> a;
+    set_identity(a);
+    double tprev = 0.0;
+    if (kb < p.n && (kb > 0 || p.k0 > 0)) tprev = __ldg(p.t + kb - 1);
+
+    for (int64_t j0 = 0; j0 < p.K; j0 += kWin) {
+        stage_in(st[wid], p.t, p.y, p.mask, wbase, p.K, p.n, j0, lane, true);
+#pragma unroll 1
+        for (int jj = 0; jj < kWin; ++jj) {
+            const int64_t k = kb + j0 + jj;
+            if (k < ke) {
+                const double tk = st[wid].t[lane][jj];
+                const bool obs = st[wid].m[lane][jj] != 0;
+                const double yk = st[wid].y[lane][jj];
+                const int64_t g = p.k0 + k;
+                double F[D * D], Q[ns(D)];
+                if (g == 0) {
+#pragma unroll
+                    for (int i = 0; i < D * D; ++i) F[i] = 0.0;
+#pragma unroll
+                    for (int i = 0; i < ns(D); ++i) Q[i] = p.m.Pinf[i];
+                    if (!isfinite(tk)) raise_error(p.err, g, kErrInput);
+                } else {
+                    const double dt = tk - tprev;
+                    if (!(dt >= 0.0) || !isfinite(tk)) raise_error(p.err, g, kErrInput);
+                    if (discretize<D>(p.m, dt, F, Q)) raise_error(p.err, g, kErrUnsupported);
+                }
+                if (obs && !isfinite(yk)) raise_error(p.err, g, kErrInput);
+                fold_step<D>(a, F, Q, p.m, obs, yk);
+                tprev = tk;
+            }
+        }
+        __syncwarp();
+    }
+    store_soa(a, p.chain_f, nch, c);
+
+    // CTA tree reduce (ordered): lane 0 of each warp, then warp 0
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        FAgg<D> o;
+        shfl_down_all(o, a, off);
+        if ((lane & (2 * off - 1)) == 0) {
+            FAgg<D> r;
+            if (!combine(a, o, r)) raise_error(p.err, p.k0 + kb, kErrNumeric);
+            a = r;
+        }
+    }
+    if (lane == 0) wagg[wid] = a;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        FAgg<D> acc = wagg[0];
+#pragma unroll 1
+        for (int w = 1; w < kWarps; ++w) {
+            FAgg<D> r;
+            combine(acc, wagg[w], r);
+            acc = r;
+        }
+        store_aos(acc, p.block_f + static_cast<int64_t>(blockIdx.x) * FN(D));
+    }
+}
+
+// ------------------------------------------------------------------ K2: block carries (1 CTA)
+template <int D>
+__global__ void __launch_bounds__(kCarryThreads, 1) k_filter_carry(const KParams<D> p) {
+    constexpr int NW = kCarryThreads / 32;
+    __shared__ FAgg<D> tot[NW];
+    __shared__ Gauss<D> wcar[NW + 1];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    Gauss<D> R;
+    set_zero(R);
+    if (threadIdx.x == 0) {
+        // sharded: fold the aggregates of ranks 0..rank-1 into the incoming carry
+        for (int g = 0; g < p.rank && p.in_filt; ++g) {
+            FAgg<D> ag;
+            load_aos(ag, p.in_filt + static_cast<int64_t>(g) * FN(D));
+            Gauss<D> r2;
+            apply_prefix(R, ag, r2);
+            R = r2;
+        }
+        wcar[NW] = R;
+    }
+    __syncthreads();
+    R = wcar[NW];
+    for (int base = 0; base < p.nb; base += kCarryThreads) {
+        const int b = base + threadIdx.x;
+        FAgg<D> a;
+        if (b < p.nb) load_aos(a, p.block_f + static_cast<int64_t>(b) * FN(D));
+        else set_identity(a);
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            FAgg<D> o;
+            shfl_up_all(o, a, off);
+            if (lane >= off) {
+                FAgg<D> r;
+                combine(o, a, r);
+                a = r;
+            }
+        }
+        if (lane == 31) tot[wid] = a;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            Gauss<D> acc = R;
+            for (int w = 0; w < NW; ++w) {
+                wcar[w] = acc;
+                Gauss<D> r2;
+                apply_prefix(acc, tot[w], r2);
+                acc = r2;
+            }
+            wcar[NW] = acc;
+        }
+        __syncthreads();
+        if (b < p.nb) {
+            Gauss<D> pre;
+            apply_prefix(wcar[wid], a, pre);             // global prefix through block b
+            if (b + 1 < p.nb) store_aos(pre, p.fcarry + static_cast<int64_t>(b + 1) * CN(D));
+        }
+        if (b == 0) store_aos(R, p.fcarry);
+        R = wcar[NW];
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------ K3: Kalman rescan
+template <int D>
+__global__ void __launch_bounds__(kThreads, 3) k_filter_apply(const KParams<D> p) {
+    __shared__ StageIn st[kWarps];
+    __shared__ FAgg<D> tot[kWarps];
+    __shared__ Gauss<D> wcar[kWarps];
+    __shared__ SAgg<D> stot[kWarps];
+    __shared__ double nred[kWarps];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t c = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
+    const int64_t nch = static_cast<int64_t>(p.nb) * kThreads;
+    const int64_t wg = static_cast<int64_t>(blockIdx.x) * kWarps + wid;
+    const int64_t wbase = wg * 32 * p.K;
+    const int64_t kb = c * p.K;
+    const int64_t ke = min(kb + p.K, p.n);
+
+    // ---- carry into this chain: block carry (x) exclusive scan of chain aggregates
+    FAgg<D> a;
+    load_soa(a, p.chain_f, nch, c);
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        FAgg<D> o;
+        shfl_up_all(o, a, off);
+        if (lane >= off) {
+            FAgg<D> r;
+            combine(o, a, r);
+            a = r;
+        }
+    }
+    if (lane == 31) tot[wid] = a;
+    FAgg<D> ex;
+    shfl_up_all(ex, a, 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        Gauss<D> acc;
+        load_aos(acc, p.fcarry + static_cast<int64_t>(blockIdx.x) * CN(D));
+        for (int w = 0; w < kWarps; ++w) {
+            wcar[w] = acc;
+            Gauss<D> r2;
+            apply_prefix(acc, tot[w], r2);
+            acc = r2;
+        }
+    }
+    __syncthreads();
+    Gauss<D> cur = wcar[wid];
+    if (lane > 0) {
+        Gauss<D> r2;
+        apply_prefix(cur, ex, r2);
+        cur = r2;
+    }
+
+    // ---- Kalman filter over the chain (supplement PAPER.md:285-315)
+    double x[D], P[ns(D)];
+#pragma unroll
+    for (int i = 0; i < D; ++i) x[i] = cur.x[i];
+#pragma unroll
+    for (int i = 0; i < ns(D); ++i) P[i] = cur.P[i];
+    double x0[D], P0[ns(D)], Sg[D * D];      // entry state and cross-covariance for the smoother aggregate
+    double quad = 0.0, prodm = 1.0;
+    long long prode = 0;
+    int nobs = 0;
+    double tprev = 0.0;
+    if (kb < p.n && (kb > 0 || p.k0 > 0)) tprev = __ldg(p.t + kb - 1);
+    SAgg<D> sag;
+    set_identity(sag);
+    bool sag_done = false;
+
+    for (int64_t j0 = 0; j0 < p.K; j0 += kWin) {
+        stage_in(st[wid], p.t, p.y, p.mask, wbase, p.K, p.n, j0, lane, true);
+#pragma unroll 1
+        for (int jj = 0; jj < kWin; ++jj) {
+            const int64_t k = kb + j0 + jj;
+            if (k < ke) {
+                const double tk = st[wid].t[lane][jj];
+                const bool obs = st[wid].m[lane][jj] != 0;
+                const double yk = st[wid].y[lane][jj];
+                const int64_t g = p.k0 + k;
+                double xm[D], Pm[ns(D)], FP[D * D], F[D * D], Q[ns(D)];
+                if (g == 0) {
+#pragma unroll
+                    for (int i = 0; i < D; ++i) xm[i] = 0.0;
+#pragma unroll
+                    for (int i = 0; i < ns(D); ++i) Pm[i] = p.m.Pinf[i];
+#pragma unroll
+                    for (int i = 0; i < D * D; ++i) F[i] = 0.0;
+                } else {
+                    discretize<D>(p.m, tk - tprev, F, Q);
+                    kf_predict<D>(x, P, F, Q, xm, FP, Pm);
+                }
+                tprev = tk;
+                const bool first = (k == kb);
+                // cross-covariance prediction Sigma- = Sigma F^T (k > kb)
+                double Sm[D * D];
+                if (!first) {
+#pragma unroll
+                    for (int i = 0; i < D; ++i)
+#pragma unroll
+                        for (int j = 0; j < D; ++j) {
+                            double s = 0.0;
+#pragma unroll
+                            for (int l = 0; l < D; ++l) s = fma(Sg[i * D + l], F[j * D + l], s);
+                            Sm[i * D + j] = s;
+                        }
+                    if (g == p.nglob - 1 && p.store_state) {
+                        // smoother aggregate over kb..g-1 (next = g), then (x) terminal after the update
+                        if (!chain_smoother_agg<D>(x0, P0, Sm, xm, Pm, sag)) raise_error(p.err, g, kErrNumeric);
+                    }
+                }
+                if (obs) {
+                    double HP[D], S, hx;
+                    if (p.m.h_unit) {
+#pragma unroll
+                        for (int i = 0; i < D; ++i) HP[i] = Pm[si(D, i, 0)];
+                        S = Pm[0] + p.m.r;
+                        hx = xm[0];
+                    } else {
+                        S = p.m.r; hx = 0.0;
+#pragma unroll
+                        for (int i = 0; i < D; ++i) {
+                            double s = 0.0;
+#pragma unroll
+                            for (int j = 0; j < D; ++j) s = fma(Pm[si(D, i, j)], p.m.H[j], s);
+                            HP[i] = s;
+                            hx = fma(p.m.H[i], xm[i], hx);
+                        }
+#pragma unroll
+                        for (int i = 0; i < D; ++i) S = fma(p.m.H[i], HP[i], S);
+                    }
+                    if (!(S > 0.0) || !isfinite(S)) raise_error(p.err, g, kErrNumeric);
+                    const double iS = 1.0 / S;
+                    const double v = yk - hx;
+                    const double vs = v * iS;
+#pragma unroll
+                    for (int i = 0; i < D; ++i) x[i] = fma(HP[i], vs, xm[i]);
+#pragma unroll
+                    for (int i = 0; i < D; ++i)
+#pragma unroll
+                        for (int j = i; j < D; ++j) P[si(D, i, j)] = fma(-HP[i] * iS, HP[j], Pm[si(D, i, j)]);
+                    if (!first) {
+                        double SH[D];
+#pragma unroll
+                        for (int i = 0; i < D; ++i) {
+                            if (p.m.h_unit) SH[i] = Sm[i * D];
+                            else {
+                                double s = 0.0;
+#pragma unroll
+                                for (int j = 0; j < D; ++j) s = fma(Sm[i * D + j], p.m.H[j], s);
+                                SH[i] = s;
+                            }
+                        }
+#pragma unroll
+                        for (int i = 0; i < D; ++i)
+#pragma unroll
+                            for (int j = 0; j < D; ++j) Sg[i * D + j] = fma(-SH[i] * iS, HP[j], Sm[i * D + j]);
+                    }
+                    // NLL term 0.5 (log 2 pi S + v^2 / S): log of a running product (exponent kept apart)
+                    quad = fma(v, vs, quad);
+                    prodm *= S;
+                    {
+                        long long bits = __double_as_longlong(prodm);
+                        prode += ((bits >> 52) & 0x7ff) - 1023;
+                        bits = (bits & ~(0x7ffLL << 52)) | (1023LL << 52);
+                        prodm = __longlong_as_double(bits);
+                    }
+                    ++nobs;
+                } else {
+#pragma unroll
+                    for (int i = 0; i < D; ++i) x[i] = xm[i];
+#pragma unroll
+                    for (int i = 0; i < ns(D); ++i) P[i] = Pm[i];
+                    if (!first) {
+#pragma unroll
+                        for (int i = 0; i < D * D; ++i) Sg[i] = Sm[i];
+                    }
+                }
+                if (first) {
+#pragma unroll
+                    for (int i = 0; i < D; ++i) x0[i] = x[i];
+#pragma unroll
+                    for (int i = 0; i < ns(D); ++i) P0[i] = P[i];
+#pragma unroll
+                    for (int i = 0; i < D; ++i)
+#pragma unroll
+                        for (int j = 0; j < D; ++j) Sg[i * D + j] = P[si(D, i, j)];
+                }
+                if (g == p.nglob - 1 && p.store_state) {
+                    // terminal element (0, xbar_N, P_N)
+                    Gauss<D> term, res;
+#pragma unroll
+                    for (int i = 0; i < D; ++i) term.x[i] = x[i];
+#pragma unroll
+                    for (int i = 0; i < ns(D); ++i) term.P[i] = P[i];
+                    if (first) res = term;
+                    else apply_suffix(sag, term, res);
+#pragma unroll
+                    for (int i = 0; i < D * D; ++i) sag.E[i] = 0.0;
+#pragma unroll
+                    for (int i = 0; i < D; ++i) sag.g[i] = res.x[i];
+#pragma unroll
+                    for (int i = 0; i < ns(D); ++i) sag.L[i] = res.P[i];
+                    sag_done = true;
+                }
+                if (p.store_state) {
+                    double* o = p.xp + ((wg * p.K + (k - kb)) * CN(D)) * 32 + lane;
+#pragma unroll
+                    for (int i = 0; i < D; ++i) o[i * 32] = x[i];
+#pragma unroll
+                    for (int i = 0; i < ns(D); ++i) o[(D + i) * 32] = P[i];
+                }
+            }
+        }
+        __syncwarp();
+    }
+
+    // ---- chain smoother aggregate: peek one step past the chain (prediction only)
+    if (p.store_state) {
+        if (ke > kb && !sag_done) {
+            const int64_t g1 = p.k0 + ke;   // global index of the next step
+            if (g1 < p.nglob) {
+                const double tn = __ldg(p.t + ke);
+                double F[D * D], Q[ns(D)], xm[D], Pm[ns(D)], FP[D * D], Sm[D * D];
+                discretize<D>(p.m, tn - tprev, F, Q);
+                kf_predict<D>(x, P, F, Q, xm, FP, Pm);
+#pragma unroll
+                for (int i = 0; i < D; ++i)
+#pragma unroll
+                    for (int j = 0; j < D; ++j) {
+                        double s = 0.0;
+#pragma unroll
+                        for (int l = 0; l < D; ++l) s = fma(Sg[i * D + l], F[j * D + l], s);
+                        Sm[i * D + j] = s;
+                    }
+                if (!chain_smoother_agg<D>(x0, P0, Sm, xm, Pm, sag)) raise_error(p.err, g1, kErrNumeric);
+            }
+        }
+        store_soa(sag, p.chain_s, nch, c);
+        // ordered CTA reduce of smoother aggregates -> block aggregate
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            SAgg<D> o;
+            shfl_down_all(o, sag, off);
+            if ((lane & (2 * off - 1)) == 0) {
+                SAgg<D> r;
+                combine(sag, o, r);
+                sag = r;
+            }
+        }
+        if (lane == 0) stot[wid] = sag;
+    }
+
+    // ---- NLL partial: 0.5 (sum v^2/S + log prod S + nobs log 2 pi)
+    double nl = 0.0;
+    if (nobs > 0) nl = 0.5 * (quad + log(prodm) + static_cast<double>(prode) * 0.6931471805599453 +
+                              nobs * 1.8378770664093453);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) nl += __shfl_down_sync(0xffffffffu, nl, off);
+    if (lane == 0) nred[wid] = nl;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < kWarps; ++w) s += nred[w];
+        p.nll_block[blockIdx.x] = s;
+        if (p.store_state) {
+            SAgg<D> acc = stot[0];
+            for (int w = 1; w < kWarps; ++w) {
+                SAgg<D> r;
+                combine(acc, stot[w], r);
+                acc = r;
+            }
+            store_aos(acc, p.block_s + static_cast<int64_t>(blockIdx.x) * SN(D));
+        }
+    }
+}
+
+// ------------------------------------------------------------------ K4: block smoother carries (1 CTA)
+template <int D>
+__global__ void __launch_bounds__(kCarryThreads, 1) k_smoother_carry(const KParams<D> p) {
+    constexpr int NW = kCarryThreads / 32;
+    __shared__ SAgg<D> tot[NW];
+    __shared__ Gauss<D> wcar[NW + 1];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    Gauss<D> R;
+    set_zero(R);
+    if (threadIdx.x == 0) {
+        for (int g = p.world - 1; g > p.rank && p.in_smooth; --g) {
+            SAgg<D> ag;
+            load_aos(ag, p.in_smooth + static_cast<int64_t>(g) * SN(D));
+            Gauss<D> r2;
+            apply_suffix(ag, R, r2);
+            R = r2;
+        }
+        wcar[0] = R;
+    }
+    __syncthreads();
+    R = wcar[0];
+    const int nchunk = (p.nb + kCarryThreads - 1) / kCarryThreads;
+    for (int ci = nchunk - 1; ci >= 0; --ci) {
+        const int b = ci * kCarryThreads + threadIdx.x;
+        SAgg<D> a;
+        if (b < p.nb) load_aos(a, p.block_s + static_cast<int64_t>(b) * SN(D));
+        else set_identity(a);
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            SAgg<D> o;
+            shfl_down_all(o, a, off);
+            if (lane + off < 32) {
+                SAgg<D> r;
+                combine(a, o, r);
+                a = r;
+            }
+        }
+        if (lane == 0) tot[wid] = a;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            Gauss<D> acc = R;
+            wcar[NW] = acc;
+            for (int w = NW - 1; w >= 0; --w) {
+                Gauss<D> r2;
+                apply_suffix(tot[w], acc, r2);
+                acc = r2;
+                wcar[w] = acc;
+            }
+        }
+        __syncthreads();
+        if (b < p.nb) {
+            Gauss<D> suf;
+            apply_suffix(a, wcar[wid + 1], suf);        // smoothed state at the first step of block b
+            if (b >= 1) store_aos(suf, p.scarry + static_cast<int64_t>(b - 1) * CN(D));
+            if (b == p.nb - 1) store_aos(R, p.scarry + static_cast<int64_t>(b) * CN(D));
+        }
+        R = wcar[0];
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------ K5: RTS rescan
+struct StageOut {
+    double t[32][kWin + 1];   // staged t; each lane overwrites its own slot with the mean
+    double b[32][kWin + 1];   // variance
+};
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 3) k_smoother_apply(const KParams<D> p) {
+    __shared__ StageOut so[kWarps];
+    __shared__ SAgg<D> tot[kWarps];
+    __shared__ Gauss<D> wcar[kWarps + 1];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t c = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
+    const int64_t nch = static_cast<int64_t>(p.nb) * kThreads;
+    const int64_t wg = static_cast<int64_t>(blockIdx.x) * kWarps + wid;
+    const int64_t wbase = wg * 32 * p.K;
+    const int64_t kb = c * p.K;
+    const int64_t ke = min(kb + p.K, p.n);
+
+    // ---- carry: exclusive reverse scan of chain smoother aggregates (x) block carry
+    SAgg<D> a;
+    load_soa(a, p.chain_s, nch, c);
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        SAgg<D> o;
+        shfl_down_all(o, a, off);
+        if (lane + off < 32) {
+            SAgg<D> r;
+            combine(a, o, r);
+            a = r;
+        }
+    }
+    if (lane == 0) tot[wid] = a;
+    SAgg<D> ex;
+    shfl_down_all(ex, a, 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        Gauss<D> acc;
+        load_aos(acc, p.scarry + static_cast<int64_t>(blockIdx.x) * CN(D));
+        wcar[kWarps] = acc;
+        for (int w = kWarps - 1; w >= 0; --w) {
+            wcar[w + 1] = acc;
+            Gauss<D> r2;
+            apply_suffix(tot[w], acc, r2);
+            acc = r2;
+        }
+    }
+    __syncthreads();
+    Gauss<D> cur = wcar[wid + 1];
+    if (lane < 31) {
+        Gauss<D> r2;
+        apply_suffix(ex, cur, r2);
+        cur = r2;
+    }
+    double ms[D], Ps[ns(D)];
+#pragma unroll
+    for (int i = 0; i < D; ++i) ms[i] = cur.x[i];
+#pragma unroll
+    for (int i = 0; i < ns(D); ++i) Ps[i] = cur.P[i];
+
+    // ---- RTS over the chain, last step first
+    double tnext = 0.0;
+    if (ke > kb && p.k0 + ke < p.nglob) tnext = __ldg(p.t + ke);
+    const int64_t jtop = ((p.K - 1) / kWin) * kWin;
+    for (int64_t j0 = jtop; j0 >= 0; j0 -= kWin) {
+        // stage t for this window
+        {
+            constexpr int RPI = 32 / kWin;
+            const int col = lane % kWin, rsub = lane / kWin;
+#pragma unroll 4
+            for (int r0 = 0; r0 < 32; r0 += RPI) {
+                const int r = r0 + rsub;
+                const int64_t j = j0 + col;
+                const int64_t idx = wbase + r * p.K + j;
+                so[wid].t[r][col] = ((j < p.K) && (idx < p.n)) ? __ldg(p.t + idx) : 0.0;
+            }
+            __syncwarp();
+        }
+#pragma unroll 1
+        for (int jj = kWin - 1; jj >= 0; --jj) {
+            const int64_t k = kb + j0 + jj;
+            if (k < ke) {
+                const double tk = so[wid].t[lane][jj];
+                const int64_t g = p.k0 + k;
+                double x[D], P[ns(D)];
+                const double* src = p.xp + ((wg * p.K + (k - kb)) * CN(D)) * 32 + lane;
+#pragma unroll
+                for (int i = 0; i < D; ++i) x[i] = src[i * 32];
+#pragma unroll
+                for (int i = 0; i < ns(D); ++i) P[i] = src[(D + i) * 32];
+                if (g == p.nglob - 1) {
+#pragma unroll
+                    for (int i = 0; i < D; ++i) ms[i] = x[i];
+#pragma unroll
+                    for (int i = 0; i < ns(D); ++i) Ps[i] = P[i];
+                } else {
+                    double F[D * D], Q[ns(D)], xm[D], Pm[ns(D)], FP[D * D];
+                    discretize<D>(p.m, tnext - tk, F, Q);
+                    kf_predict<D>(x, P, F, Q, xm, FP, Pm);
+                    if (!rts_step<D>(x, P, xm, Pm, FP, ms, Ps)) raise_error(p.err, g, kErrNumeric);
+                }
+                tnext = tk;
+                double mo, vo;
+                if (p.m.h_unit) {
+                    mo = ms[0];
+                    vo = Ps[0];
+                } else {
+                    mo = 0.0; vo = 0.0;
+#pragma unroll
+                    for (int i = 0; i < D; ++i) {
+                        mo = fma(p.m.H[i], ms[i], mo);
+                        double s = 0.0;
+#pragma unroll
+                        for (int j = 0; j < D; ++j) s = fma(Ps[si(D, i, j)], p.m.H[j], s);
+                        vo = fma(p.m.H[i], s, vo);
+                    }
+                }
+                so[wid].t[lane][jj] = mo;
+                so[wid].b[lane][jj] = vo;
+            }
+        }
+        __syncwarp();
+        {
+            constexpr int RPI = 32 / kWin;
+            const int col = lane % kWin, rsub = lane / kWin;
+#pragma unroll 4
+            for (int r0 = 0; r0 < 32; r0 += RPI) {
+                const int r = r0 + rsub;
+                const int64_t j = j0 + col;
+                const int64_t idx = wbase + r * p.K + j;
+                if ((j < p.K) && (idx < p.n)) {
+                    if (p.mean) p.mean[idx] = so[wid].t[r][col];
+                    if (p.var) p.var[idx] = so[wid].b[r][col];
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
+// ------------------------------------------------------------------ K6: deterministic NLL sum
+__global__ void __launch_bounds__(256, 1) k_nll_sum(const double* __restrict__ parts, int nb, double* out) {
+    __shared__ double red[8];
+    const int per = (nb + 255) / 256;
+    double s = 0.0;
+    for (int i = 0; i < per; ++i) {
+        const int b = threadIdx.x * per + i;
+        if (b < nb) s += parts[b];
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double tsum = 0.0;
+        for (int w = 0; w < 8; ++w) tsum += red[w];
+        *out = tsum;
+    }
+}
+
+// ------------------------------------------------------------------ chunk aggregate reducers (sharded path, 1 CTA)
+template <int D, typename Agg>
+__global__ void __launch_bounds__(kCarryThreads, 1) k_reduce_blocks(const double* __restrict__ blocks, int nb,
+                                                                    double* out) {
+    constexpr int NW = kCarryThreads / 32;
+    constexpr int NA = sizeof(Agg) / sizeof(double);
+    __shared__ Agg wred[NW];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int per = (nb + kCarryThreads - 1) / kCarryThreads;
+    Agg a;
+    set_identity(a);
+    for (int i = 0; i < per; ++i) {
+        const int b = threadIdx.x * per + i;
+        if (b < nb) {
+            Agg e, r;
+            load_aos(e, blocks + static_cast<int64_t>(b) * NA);
+            combine(a, e, r);
+            a = r;
+        }
+    }
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        Agg o;
+        shfl_down_all(o, a, off);
+        if ((lane & (2 * off - 1)) == 0) {
+            Agg r;
+            combine(a, o, r);
+            a = r;
+        }
+    }
+    if (lane == 0) wred[wid] = a;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        Agg acc = wred[0];
+        for (int w = 1; w < NW; ++w) {
+            Agg r;
+            combine(acc, wred[w], r);
+            acc = r;
+        }
+        store_aos(acc, out);
+    }
+}
+
+}  // namespace pssgp

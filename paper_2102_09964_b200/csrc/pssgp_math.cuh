@@ -1,0 +1,725 @@
+// pssgp_math.cuh — register-resident small-matrix math of the PSSGP hot path.
+//
+// Everything is fp64, fully unrolled at compile time for a state dimension D,
+// with symmetric matrices (C, J, P, L, Q, P_inf) stored as PACKED UPPER
+// TRIANGLES so that the symmetry the filtering operator needs for
+// associativity (SURVEY.md finding 3) is structural.
+// Functions are __host__ __device__ so the host introspection entry points
+// (pssgp_debug_discretize) run exactly the code the kernels run.
+//
+// Paper map (PAPER.md = arXiv:2102.09964 text):
+//   filter element + fold  : Eqs. (6)-(8) PAPER.md:94-112, observed case PAPER.md:359
+//   filtering operator     : PAPER.md:116-121
+//   Kalman step            : supplement PAPER.md:285-315
+//   smoother operator      : PAPER.md:433, 446-449 (reading Z2)
+//   RTS step               : PAPER.md:422-430
+//   discretisation         : PAPER.md:294-303 (closed forms for Matern)
+#pragma once
+#include <cstdint>
+#include <cmath>
+
+#if defined(__CUDACC__)
+#define PS_HD __host__ __device__ __forceinline__
+#define PS_CX __host__ __device__ constexpr
+#else
+#define PS_HD inline
+#define PS_CX constexpr
+#endif
+
+namespace pssgp {
+
+PS_CX int ns(int D) { return D * (D + 1) / 2; }
+// packed-upper index of (i, j), any order
+PS_CX int si(int D, int i, int j) {
+    return i <= j ? i * (2 * D - i + 1) / 2 + (j - i) : j * (2 * D - j + 1) / 2 + (i - j);
+}
+PS_CX int FN(int D) { return D * D + 2 * D + 2 * ns(D); }  // filter aggregate doubles
+PS_CX int SN(int D) { return D * D + D + ns(D); }          // smoother aggregate doubles
+PS_CX int CN(int D) { return D + ns(D); }                  // (mean, cov) pair doubles
+
+// Model constants the kernels need (kernel parameter, i.e. constant bank).
+template <int D>
+struct ModelParams {
+    double Pinf[ns(D)];   // stationary covariance (balanced coordinates)
+    double H[D];          // observation row (balanced coordinates)
+    double r;             // observation noise variance sigma_n^2 > 0
+    double lam;           // Matern lambda = sqrt(2 nu) / ell (closed form), else 0
+    double s2;            // Matern variance sigma^2
+    double udt;           // uniform dt (> 0) for which Fu, Qu are valid, else 0
+    double Fu[D * D];     // F(udt)
+    double Qu[ns(D)];     // Q(udt)
+    int closed;           // 1: Matern closed form of order D available in the lambda-scaled basis
+    int h_unit;           // 1: H == e_0
+};
+
+// ------------------------------------------------------------------ aggregates
+template <int D>
+struct FAgg {  // filter element / aggregate (A, b, C, eta, J)
+    double A[D * D];
+    double b[D];
+    double C[ns(D)];
+    double eta[D];
+    double J[ns(D)];
+};
+
+template <int D>
+struct SAgg {  // smoother element / aggregate (E, g, L)
+    double E[D * D];
+    double g[D];
+    double L[ns(D)];
+};
+
+template <int D>
+struct Gauss {  // (mean, covariance) — a collapsed global prefix (0, x, P, 0, 0) or suffix (0, m, P)
+    double x[D];
+    double P[ns(D)];
+};
+
+template <int D>
+PS_HD void set_identity(FAgg<D>& a) {
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+#pragma unroll
+        for (int j = 0; j < D; ++j) a.A[i * D + j] = (i == j) ? 1.0 : 0.0;
+        a.b[i] = 0.0;
+        a.eta[i] = 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < ns(D); ++i) { a.C[i] = 0.0; a.J[i] = 0.0; }
+}
+
+template <int D>
+PS_HD void set_identity(SAgg<D>& a) {
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+#pragma unroll
+        for (int j = 0; j < D; ++j) a.E[i * D + j] = (i == j) ? 1.0 : 0.0;
+        a.g[i] = 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < ns(D); ++i) a.L[i] = 0.0;
+}
+
+template <int D>
+PS_HD void set_zero(Gauss<D>& c) {
+#pragma unroll
+    for (int i = 0; i < D; ++i) c.x[i] = 0.0;
+#pragma unroll
+    for (int i = 0; i < ns(D); ++i) c.P[i] = 0.0;
+}
+
+// flat views for loads / stores / shuffles
+template <int D> PS_HD double* flat(FAgg<D>& a) { return a.A; }
+template <int D> PS_HD const double* flat(const FAgg<D>& a) { return a.A; }
+template <int D> PS_HD double* flat(SAgg<D>& a) { return a.E; }
+template <int D> PS_HD const double* flat(const SAgg<D>& a) { return a.E; }
+template <int D> PS_HD double* flat(Gauss<D>& a) { return a.x; }
+template <int D> PS_HD const double* flat(const Gauss<D>& a) { return a.x; }
+
+// ------------------------------------------------------------------ small dense helpers
+// Gaussian elimination with partial pivoting on [M | R] (M D x D row-major,
+// R D x NR row-major), solving M X = R in place (X -> R).  Pivot rows are
+// chosen by compare-and-swap with compile-time indices only (no dynamic
+// register indexing).  Returns false on a zero pivot.
+template <int D, int NR>
+PS_HD bool gauss_solve(double (&M)[D * D], double (&R)[D * NR]) {
+    bool ok = true;
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+#pragma unroll
+        for (int r = c + 1; r < D; ++r) {
+            const bool sw = fabs(M[r * D + c]) > fabs(M[c * D + c]);
+#pragma unroll
+            for (int k = c; k < D; ++k) {
+                const double u = M[c * D + k], v = M[r * D + k];
+                M[c * D + k] = sw ? v : u;
+                M[r * D + k] = sw ? u : v;
+            }
+#pragma unroll
+            for (int k = 0; k < NR; ++k) {
+                const double u = R[c * NR + k], v = R[r * NR + k];
+                R[c * NR + k] = sw ? v : u;
+                R[r * NR + k] = sw ? u : v;
+            }
+        }
+        const double piv = M[c * D + c];
+        ok = ok && (piv != 0.0);
+        const double ip = 1.0 / piv;
+#pragma unroll
+        for (int r = c + 1; r < D; ++r) {
+            const double f = M[r * D + c] * ip;
+#pragma unroll
+            for (int k = c + 1; k < D; ++k) M[r * D + k] = fma(-f, M[c * D + k], M[r * D + k]);
+#pragma unroll
+            for (int k = 0; k < NR; ++k) R[r * NR + k] = fma(-f, R[c * NR + k], R[r * NR + k]);
+        }
+        M[c * D + c] = ip;  // keep the reciprocal for back substitution
+    }
+#pragma unroll
+    for (int c = D - 1; c >= 0; --c) {
+#pragma unroll
+        for (int k = 0; k < NR; ++k) {
+            double s = R[c * NR + k];
+#pragma unroll
+            for (int j = c + 1; j < D; ++j) s = fma(-M[c * D + j], R[j * NR + k], s);
+            R[c * NR + k] = s * M[c * D + c];
+        }
+    }
+    return ok;
+}
+
+// LDL^T factorisation of a symmetric positive-definite packed matrix.
+// Lo: strictly-lower factor (row-major D x D, only i > j used), id: 1 / d.
+template <int D>
+PS_HD bool ldlt(const double (&S)[ns(D)], double (&Lo)[D * D], double (&id)[D]) {
+    double dd[D];
+    bool ok = true;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        double d = S[si(D, j, j)];
+#pragma unroll
+        for (int k = 0; k < j; ++k) d = fma(-Lo[j * D + k] * dd[k], Lo[j * D + k], d);
+        ok = ok && (d > 0.0);
+        dd[j] = d;
+        id[j] = 1.0 / d;
+#pragma unroll
+        for (int i = j + 1; i < D; ++i) {
+            double s = S[si(D, i, j)];
+#pragma unroll
+            for (int k = 0; k < j; ++k) s = fma(-Lo[i * D + k] * dd[k], Lo[j * D + k], s);
+            Lo[i * D + j] = s * id[j];
+        }
+    }
+    return ok;
+}
+
+// Solve S X = R with the LDL^T factors (R: D x NR row-major, in place).
+template <int D, int NR>
+PS_HD void ldlt_solve(const double (&Lo)[D * D], const double (&id)[D], double (&R)[D * NR]) {
+#pragma unroll
+    for (int k = 0; k < NR; ++k) {
+#pragma unroll
+        for (int i = 1; i < D; ++i) {
+            double s = R[i * NR + k];
+#pragma unroll
+            for (int j = 0; j < i; ++j) s = fma(-Lo[i * D + j], R[j * NR + k], s);
+            R[i * NR + k] = s;
+        }
+#pragma unroll
+        for (int i = 0; i < D; ++i) R[i * NR + k] *= id[i];
+#pragma unroll
+        for (int i = D - 2; i >= 0; --i) {
+            double s = R[i * NR + k];
+#pragma unroll
+            for (int j = i + 1; j < D; ++j) s = fma(-Lo[j * D + i], R[j * NR + k], s);
+            R[i * NR + k] = s;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ discretisation
+// R_m(x) = e^{-x} sum_{n>=m} x^n / n!  (regularised lower incomplete gamma P(m, x)),
+// evaluated without cancellation: truncated series for x <= 2, complement
+// 1 - e^{-x} sum_{n<m} x^n/n! above (cancellation <= ~20x there).
+template <int M>
+PS_HD double inc_gamma_tail(double x, double emx) {
+    double lead = emx;  // e^{-x} x^M / M!
+#pragma unroll
+    for (int n = 1; n <= M; ++n) lead *= x / n;
+    if (x <= 0.015625) {
+        double s = 1.0;
+#pragma unroll
+        for (int j = 7; j >= 1; --j) s = fma(s * x, 1.0 / (M + j), 1.0);
+        return lead * s;
+    } else if (x <= 0.5) {
+        double s = 1.0;
+#pragma unroll
+        for (int j = 13; j >= 1; --j) s = fma(s * x, 1.0 / (M + j), 1.0);
+        return lead * s;
+    } else if (x <= 2.0) {
+        double s = 1.0;
+#pragma unroll
+        for (int j = 22; j >= 1; --j) s = fma(s * x, 1.0 / (M + j), 1.0);
+        return lead * s;
+    } else {
+        double p = 1.0, term = 1.0;
+#pragma unroll
+        for (int n = 1; n < M; ++n) { term *= x / n; p += term; }
+        return fma(-emx, p, 1.0);
+    }
+}
+
+// Matern-(2D-1)/2 closed-form F(dt), Q(dt) in the lambda-scaled basis
+// x_hat_i = x_i / lambda^i (a diagonal balancing D = diag(lambda^i), Eq. (9)),
+// where F and Q / sigma^2 depend on z = lambda dt only (sympy derivation in
+// tools/derive_matern.py).  x = 2 z.
+template <int D>
+PS_HD void matern_closed(double lam, double s2, double dt, double (&F)[D * D], double (&Q)[ns(D)]) {
+    const double z = lam * dt;
+    const double e = exp(-z);
+    const double x = 2.0 * z;
+    const double ex = e * e;  // e^{-x}
+    if constexpr (D == 1) {
+        F[0] = e;
+        Q[0] = -s2 * expm1(-x);
+    } else if constexpr (D == 2) {
+        F[0] = e * (1.0 + z); F[1] = e * z;
+        F[2] = -e * z;        F[3] = e * (1.0 - z);
+        const double R3 = inc_gamma_tail<3>(x, ex);
+        Q[si(2, 0, 0)] = s2 * R3;
+        Q[si(2, 0, 1)] = s2 * ex * (0.5 * x * x);
+        Q[si(2, 1, 1)] = s2 * fma(2.0 * x, ex, R3);
+    } else if constexpr (D == 3) {
+        const double z2 = z * z;
+        F[0] = e * (1.0 + z + 0.5 * z2); F[1] = e * (z + z2);          F[2] = e * (0.5 * z2);
+        F[3] = e * (-0.5 * z2);          F[4] = e * (1.0 + z - z2);    F[5] = e * (z - 0.5 * z2);
+        F[6] = e * (0.5 * z2 - z);       F[7] = e * (z2 - 3.0 * z);    F[8] = e * (1.0 - 2.0 * z + 0.5 * z2);
+        const double R5 = inc_gamma_tail<5>(x, ex);
+        const double x2 = x * x, x3 = x2 * x, x4 = x2 * x2;
+        Q[si(3, 0, 0)] = s2 * R5;
+        Q[si(3, 0, 1)] = s2 * ex * (x4 * (1.0 / 24.0));
+        Q[si(3, 0, 2)] = s2 * fma(ex, x3 * (1.0 / 9.0) - x4 * (1.0 / 18.0), -R5 * (1.0 / 3.0));
+        Q[si(3, 1, 1)] = s2 * fma(ex, x3 * (2.0 / 9.0) - x4 * (1.0 / 36.0), R5 * (1.0 / 3.0));
+        Q[si(3, 1, 2)] = s2 * ex * (x2 * (2.0 / 3.0) - x3 * (1.0 / 3.0) + x4 * (1.0 / 24.0));
+        Q[si(3, 2, 2)] = s2 * fma(ex, x * (8.0 / 3.0) - x2 * (4.0 / 3.0) + x3 * (2.0 / 3.0), R5);
+    }
+}
+
+// Discretise one step (transition into a step whose predecessor is dt earlier).
+// Returns 0, or a nonzero code when the model has no device discretisation for dt.
+template <int D>
+PS_HD int discretize(const ModelParams<D>& p, double dt, double (&F)[D * D], double (&Q)[ns(D)]) {
+    if (dt == p.udt) {
+#pragma unroll
+        for (int i = 0; i < D * D; ++i) F[i] = p.Fu[i];
+#pragma unroll
+        for (int i = 0; i < ns(D); ++i) Q[i] = p.Qu[i];
+        return 0;
+    }
+    if (dt == 0.0) {
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+            for (int j = 0; j < D; ++j) F[i * D + j] = (i == j) ? 1.0 : 0.0;
+#pragma unroll
+        for (int i = 0; i < ns(D); ++i) Q[i] = 0.0;
+        return 0;
+    }
+    if constexpr (D <= 3) {
+        if (p.closed) {
+            matern_closed<D>(p.lam, p.s2, dt, F, Q);
+            return 0;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < D * D; ++i) F[i] = 0.0;
+#pragma unroll
+    for (int i = 0; i < ns(D); ++i) Q[i] = 0.0;
+    return 1;
+}
+
+// ------------------------------------------------------------------ filter fold
+// a <- a (x) e_k, where e_k is the raw filter element of step k built from
+// (F, Q, y_k, mask_k) (Eqs. (6), (8) PAPER.md:97-112 for a missing y
+// for an observed y).  Because J_k = u u^T / S_k has rank one, the operator
+// reduces to a Kalman step conditioned on the chain's
+// entry state: predict C- = F C F^T + Q, then a rank-one update (no solve).
+// For the global first step pass F = 0, Q = P_inf (Eq. (7) PAPER.md:103-107 and
+// reading Z1: the observed first element is the KF update of N(0, P_inf)).
+template <int D>
+PS_HD void fold_step(FAgg<D>& a, const double (&F)[D * D], const double (&Q)[ns(D)],
+                     const ModelParams<D>& p, bool obs, double yk) {
+    double FA[D * D], Fb[D], T[D * D], Cm[ns(D)];
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        double sb = 0.0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            double sa = 0.0, sc = 0.0;
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+                sa = fma(F[i * D + k], a.A[k * D + j], sa);
+                sc = fma(F[i * D + k], a.C[si(D, k, j)], sc);
+            }
+            FA[i * D + j] = sa;
+            T[i * D + j] = sc;
+            sb = fma(F[i * D + j], a.b[j], sb);
+        }
+        Fb[i] = sb;
+    }
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = i; j < D; ++j) {
+            double s = Q[si(D, i, j)];
+#pragma unroll
+            for (int k = 0; k < D; ++k) s = fma(T[i * D + k], F[j * D + k], s);
+            Cm[si(D, i, j)] = s;
+        }
+    if (obs) {
+        double HC[D], w[D], hb, S;
+        if (p.h_unit) {
+#pragma unroll
+            for (int i = 0; i < D; ++i) { HC[i] = Cm[si(D, i, 0)]; w[i] = FA[i]; }
+            hb = Fb[0];
+            S = Cm[0] + p.r;
+        } else {
+            hb = 0.0; S = p.r;
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+                double s = 0.0, ww = 0.0;
+#pragma unroll
+                for (int j = 0; j < D; ++j) {
+                    s = fma(Cm[si(D, i, j)], p.H[j], s);
+                    ww = fma(p.H[j], FA[j * D + i], ww);
+                }
+                HC[i] = s; w[i] = ww;
+                hb = fma(p.H[i], Fb[i], hb);
+            }
+#pragma unroll
+            for (int i = 0; i < D; ++i) S = fma(p.H[i], HC[i], S);
+        }
+        const double iS = 1.0 / S;
+        const double v = yk - hb;
+        const double vs = v * iS;
+        double Kc[D];
+#pragma unroll
+        for (int i = 0; i < D; ++i) Kc[i] = HC[i] * iS;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+#pragma unroll
+            for (int j = 0; j < D; ++j) a.A[i * D + j] = fma(-Kc[i], w[j], FA[i * D + j]);
+            a.b[i] = fma(HC[i], vs, Fb[i]);
+            a.eta[i] = fma(w[i], vs, a.eta[i]);
+        }
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+            for (int j = i; j < D; ++j) {
+                a.C[si(D, i, j)] = fma(-Kc[i], HC[j], Cm[si(D, i, j)]);
+                a.J[si(D, i, j)] = fma(w[i] * iS, w[j], a.J[si(D, i, j)]);
+            }
+    } else {
+#pragma unroll
+        for (int i = 0; i < D * D; ++i) a.A[i] = FA[i];
+#pragma unroll
+        for (int i = 0; i < D; ++i) a.b[i] = Fb[i];
+#pragma unroll
+        for (int i = 0; i < ns(D); ++i) a.C[i] = Cm[i];
+    }
+}
+
+// ------------------------------------------------------------------ general filtering operator
+// (A,b,C,eta,J)_i (x) (A,b,C,eta,J)_j, with solves against
+// (I + C_i J_j) and (I + J_j C_i) (never explicit inverses).
+template <int D>
+PS_HD bool combine(const FAgg<D>& ei, const FAgg<D>& ej, FAgg<D>& out) {
+    constexpr int NX = 2 * D + 1, NY = D + 1;
+    double M[D * D], MT[D * D], X[D * NX], Y[D * NY];
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+            double s = (r == c) ? 1.0 : 0.0, st = s;
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+                s = fma(ei.C[si(D, r, k)], ej.J[si(D, k, c)], s);     // (I + C_i J_j)
+                st = fma(ej.J[si(D, r, k)], ei.C[si(D, k, c)], st);   // (I + J_j C_i)
+            }
+            M[r * D + c] = s;
+            MT[r * D + c] = st;
+        }
+        // X rhs = [A_i | b_i + C_i eta_j | C_i]
+#pragma unroll
+        for (int c = 0; c < D; ++c) X[r * NX + c] = ei.A[r * D + c];
+        double s = ei.b[r];
+#pragma unroll
+        for (int k = 0; k < D; ++k) s = fma(ei.C[si(D, r, k)], ej.eta[k], s);
+        X[r * NX + D] = s;
+#pragma unroll
+        for (int c = 0; c < D; ++c) X[r * NX + D + 1 + c] = ei.C[si(D, r, c)];
+        // Y rhs = [J_j A_i | eta_j - J_j b_i]
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+            double u = 0.0;
+#pragma unroll
+            for (int k = 0; k < D; ++k) u = fma(ej.J[si(D, r, k)], ei.A[k * D + c], u);
+            Y[r * NY + c] = u;
+        }
+        double e = ej.eta[r];
+#pragma unroll
+        for (int k = 0; k < D; ++k) e = fma(-ej.J[si(D, r, k)], ei.b[k], e);
+        Y[r * NY + D] = e;
+    }
+    bool ok = gauss_solve<D, NX>(M, X);
+    ok = gauss_solve<D, NY>(MT, Y) && ok;
+    // A_ij = A_j X_A ; b_ij = A_j X_b + b_j ; C_ij = A_j X_C A_j^T + C_j
+    double AX[D * D];
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+        double sb = ej.b[r];
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+            double sa = 0.0, sc = 0.0;
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+                sa = fma(ej.A[r * D + k], X[k * NX + c], sa);
+                sc = fma(ej.A[r * D + k], X[k * NX + D + 1 + c], sc);
+            }
+            out.A[r * D + c] = sa;
+            AX[r * D + c] = sc;
+        }
+#pragma unroll
+        for (int k = 0; k < D; ++k) sb = fma(ej.A[r * D + k], X[k * NX + D], sb);
+        out.b[r] = sb;
+    }
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+        for (int c = r; c < D; ++c) {
+            double s = ej.C[si(D, r, c)];
+#pragma unroll
+            for (int k = 0; k < D; ++k) s = fma(AX[r * D + k], ej.A[c * D + k], s);
+            out.C[si(D, r, c)] = s;
+        }
+    // eta_ij = A_i^T Y_eta + eta_i ; J_ij = A_i^T Y_J + J_i
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+        double se = ei.eta[r];
+#pragma unroll
+        for (int k = 0; k < D; ++k) se = fma(ei.A[k * D + r], Y[k * NY + D], se);
+        out.eta[r] = se;
+#pragma unroll
+        for (int c = r; c < D; ++c) {
+            double s = ei.J[si(D, r, c)];
+#pragma unroll
+            for (int k = 0; k < D; ++k) s = fma(ei.A[k * D + r], Y[k * NY + c], s);
+            out.J[si(D, r, c)] = s;
+        }
+    }
+    return ok;
+}
+
+// Collapsed global prefix (0, x, P, 0, 0) (x) aggregate (A, b, C, eta, J):
+// x' = A (I + P J)^-1 (x + P eta) + b,  P' = A (I + P J)^-1 P A^T + C.
+template <int D>
+PS_HD bool apply_prefix(const Gauss<D>& g, const FAgg<D>& a, Gauss<D>& out) {
+    constexpr int NX = D + 1;
+    double M[D * D], X[D * NX];
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+        double s0 = g.x[r];
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+            double s = (r == c) ? 1.0 : 0.0;
+#pragma unroll
+            for (int k = 0; k < D; ++k) s = fma(g.P[si(D, r, k)], a.J[si(D, k, c)], s);
+            M[r * D + c] = s;
+            X[r * NX + c] = g.P[si(D, r, c)];
+            s0 = fma(g.P[si(D, r, c)], a.eta[c], s0);
+        }
+        X[r * NX + D] = s0;
+    }
+    const bool ok = gauss_solve<D, NX>(M, X);
+    double AX[D * D];
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+        double sx = a.b[r];
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+            double s = 0.0;
+#pragma unroll
+            for (int k = 0; k < D; ++k) s = fma(a.A[r * D + k], X[k * NX + c], s);
+            AX[r * D + c] = s;
+        }
+#pragma unroll
+        for (int k = 0; k < D; ++k) sx = fma(a.A[r * D + k], X[k * NX + D], sx);
+        out.x[r] = sx;
+    }
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+        for (int c = r; c < D; ++c) {
+            double s = a.C[si(D, r, c)];
+#pragma unroll
+            for (int k = 0; k < D; ++k) s = fma(AX[r * D + k], a.A[c * D + k], s);
+            out.P[si(D, r, c)] = s;
+        }
+    return ok;
+}
+
+// ------------------------------------------------------------------ smoothing operator
+// (E,g,L)_i (x) (E,g,L)_j = (E_i E_j, E_i g_j + g_i, E_i L_j E_i^T + L_i), i earlier.
+template <int D>
+PS_HD void combine(const SAgg<D>& ei, const SAgg<D>& ej, SAgg<D>& out) {
+    double EL[D * D];
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+        double sg = ei.g[r];
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+            double se = 0.0, sl = 0.0;
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+                se = fma(ei.E[r * D + k], ej.E[k * D + c], se);
+                sl = fma(ei.E[r * D + k], ej.L[si(D, k, c)], sl);
+            }
+            out.E[r * D + c] = se;
+            EL[r * D + c] = sl;
+            sg = fma(ei.E[r * D + c], ej.g[c], sg);
+        }
+        out.g[r] = sg;
+    }
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+        for (int c = r; c < D; ++c) {
+            double s = ei.L[si(D, r, c)];
+#pragma unroll
+            for (int k = 0; k < D; ++k) s = fma(EL[r * D + k], ei.E[c * D + k], s);
+            out.L[si(D, r, c)] = s;
+        }
+}
+
+// Aggregate (E, g, L) (x) collapsed global suffix (0, m, P) = (0, E m + g, E P E^T + L).
+template <int D>
+PS_HD void apply_suffix(const SAgg<D>& a, const Gauss<D>& s, Gauss<D>& out) {
+    double EP[D * D];
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+        double sx = a.g[r];
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+            double t = 0.0;
+#pragma unroll
+            for (int k = 0; k < D; ++k) t = fma(a.E[r * D + k], s.P[si(D, k, c)], t);
+            EP[r * D + c] = t;
+            sx = fma(a.E[r * D + c], s.x[c], sx);
+        }
+        out.x[r] = sx;
+    }
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+        for (int c = r; c < D; ++c) {
+            double t = a.L[si(D, r, c)];
+#pragma unroll
+            for (int k = 0; k < D; ++k) t = fma(EP[r * D + k], a.E[c * D + k], t);
+            out.P[si(D, r, c)] = t;
+        }
+}
+
+// ------------------------------------------------------------------ Kalman step (supplement PAPER.md:304-315)
+// Predict: xm = F x, FP = F P, Pm = FP F^T + Q.
+template <int D>
+PS_HD void kf_predict(const double (&x)[D], const double (&P)[ns(D)], const double (&F)[D * D],
+                      const double (&Q)[ns(D)], double (&xm)[D], double (&FP)[D * D], double (&Pm)[ns(D)]) {
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        double sx = 0.0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            double s = 0.0;
+#pragma unroll
+            for (int k = 0; k < D; ++k) s = fma(F[i * D + k], P[si(D, k, j)], s);
+            FP[i * D + j] = s;
+            sx = fma(F[i * D + j], x[j], sx);
+        }
+        xm[i] = sx;
+    }
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = i; j < D; ++j) {
+            double s = Q[si(D, i, j)];
+#pragma unroll
+            for (int k = 0; k < D; ++k) s = fma(FP[i * D + k], F[j * D + k], s);
+            Pm[si(D, i, j)] = s;
+        }
+}
+
+// ------------------------------------------------------------------ chain smoother aggregate
+// The ordered product (x)_s of the smoother elements of steps k0..k1 is the
+// Gaussian conditional p(x_k0 | x_{k1+1}, y_1:k1) (each element is
+// p(x_k | x_{k+1}, y_1:k), reading Z2; Markov property).  With the filtered
+// entry moments (x0, P0), the cross-covariance Sm = Cov(x_k0, x_{k1+1} | y_1:k1)
+// and the predicted (xm, Pm) of step k1+1 it is
+//   E = Sm Pm^-1,  g = x0 - E xm,  L = P0 - E Sm^T.
+template <int D>
+PS_HD bool chain_smoother_agg(const double (&x0)[D], const double (&P0)[ns(D)], const double (&Sm)[D * D],
+                              const double (&xm)[D], const double (&Pm)[ns(D)], SAgg<D>& out) {
+    double Lo[D * D], id[D], Et[D * D];
+    const bool ok = ldlt<D>(Pm, Lo, id);
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) Et[i * D + j] = Sm[j * D + i];
+    ldlt_solve<D, D>(Lo, id, Et);  // Et = Pm^-1 Sm^T = E^T
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        double s = x0[i];
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            out.E[i * D + j] = Et[j * D + i];
+            s = fma(-Et[j * D + i], xm[j], s);
+        }
+        out.g[i] = s;
+    }
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = i; j < D; ++j) {
+            double s = P0[si(D, i, j)];
+#pragma unroll
+            for (int k = 0; k < D; ++k) s = fma(-Et[k * D + i], Sm[j * D + k], s);
+            out.L[si(D, i, j)] = s;
+        }
+    return ok;
+}
+
+// ------------------------------------------------------------------ RTS step
+// Given the filtered (x, P) at k, the predicted (xm, Pm) at k+1, FP = F P, and the
+// smoothed (ms, Ps) at k+1, overwrite (ms, Ps) with the smoothed moments at k.
+// G_k = P F^T Pm^-1 via an LDL^T solve of Pm G_k^T = F P.
+template <int D>
+PS_HD bool rts_step(const double (&x)[D], const double (&P)[ns(D)], const double (&xm)[D],
+                    const double (&Pm)[ns(D)], const double (&FP)[D * D], double (&ms)[D],
+                    double (&Ps)[ns(D)]) {
+    double Lo[D * D], id[D], Gt[D * D];
+    const bool ok = ldlt<D>(Pm, Lo, id);
+#pragma unroll
+    for (int i = 0; i < D * D; ++i) Gt[i] = FP[i];
+    ldlt_solve<D, D>(Lo, id, Gt);   // Gt = G^T, G[i][j] = Gt[j][i]
+    double dm[D], T[D * D];
+#pragma unroll
+    for (int i = 0; i < D; ++i) dm[i] = ms[i] - xm[i];
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        double s = x[i];
+#pragma unroll
+        for (int j = 0; j < D; ++j) s = fma(Gt[j * D + i], dm[j], s);
+        ms[i] = s;
+    }
+    // T = G (Ps - Pm)
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            double s = 0.0;
+#pragma unroll
+            for (int k = 0; k < D; ++k) s = fma(Gt[k * D + i], Ps[si(D, k, j)] - Pm[si(D, k, j)], s);
+            T[i * D + j] = s;
+        }
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = i; j < D; ++j) {
+            double s = P[si(D, i, j)];
+#pragma unroll
+            for (int k = 0; k < D; ++k) s = fma(T[i * D + k], Gt[k * D + j], s);
+            Ps[si(D, i, j)] = s;
+        }
+    return ok;
+}
+
+}  // namespace pssgp

@@ -1,0 +1,177 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by
+element, on seeded synthetic inputs.  Tolerances (north_star, BASELINE.json;
+measures = SURVEY.md §8(c) reading Z14):
+    mean: normwise   max|dm| / max|m_ref|      <= 1e-8
+    var : elementwise max|dv / v_ref|           <= 1e-8
+    nll : |dNLL| / |NLL_ref|                   <= 1e-9
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+import paper_2102_09964_b200 as P
+from paper_2102_09964_b200 import _native
+
+pytestmark = pytest.mark.gpu
+
+MEAN_TOL, VAR_TOL, NLL_TOL = 1e-8, 1e-8, 1e-9
+
+
+def to_dev(w, dev="cuda:0"):
+    return (torch.from_numpy(w.t).to(dev), torch.from_numpy(w.y).to(dev), torch.from_numpy(w.mask).to(dev))
+
+
+def run_gpu(w, **kw):
+    m = P.Model(w.components, w.noise_var, uniform_dt=w.uniform_dt, **kw)
+    t, y, mk = to_dev(w)
+    mean, var, nll = m.posterior(t, y, mk)
+    m.check()
+    return mean.cpu().numpy(), var.cpu().numpy(), float(nll.cpu()[0]), m
+
+
+def errors(g, o):
+    mean, var, nll = g
+    em = np.max(np.abs(mean - o["mean"])) / max(np.max(np.abs(o["mean"])), 1e-300)
+    ev = np.max(np.abs(var - o["var"]) / np.abs(o["var"]))
+    scale = abs(o["nll"]) if abs(o["nll"]) > 1e-12 else 1.0
+    en = abs(nll - o["nll"]) / scale
+    return em, ev, en
+
+
+def assert_parity(w, o=None, **kw):
+    if o is None:
+        o = oracle.posterior(w)
+    mean, var, nll, m = run_gpu(w, **kw)
+    if w.mask.sum() == 0:
+        assert np.max(np.abs(mean)) == 0.0 and nll == 0.0
+        np.testing.assert_allclose(var, o["var"], rtol=VAR_TOL)
+        return m
+    em, ev, en = errors((mean, var, nll), o)
+    assert em <= MEAN_TOL and ev <= VAR_TOL and en <= NLL_TOL, (em, ev, en)
+    return m
+
+
+def test_config1_full(cuda_device):
+    assert_parity(synth.config1())
+
+
+@pytest.mark.parametrize("kind", ["matern12", "matern32", "matern52"])
+@pytest.mark.parametrize("N", [1, 2, 3, 31, 33, 257, 1000, 4099, 30011])
+def test_random_sizes(cuda_device, kind, N):
+    w = synth.random_problem(N % 97, N, kind=kind, p_missing=0.3, ties=min(3, N // 10))
+    assert_parity(w)
+
+
+@pytest.mark.parametrize("chain_len", [1, 2, 5, 16, 17])
+def test_small_chains_many_blocks(cuda_device, chain_len):
+    """Tiny chains -> hundreds of CTAs and multi-pass single-CTA carry scans."""
+    w = synth.random_problem(5, 70001, kind="matern52", p_missing=0.2, ties=4, dt_scale=0.01)
+    assert_parity(w, chain_len=chain_len)
+
+
+@pytest.mark.parametrize("p_missing,first_missing", [(0.0, None), (1.0, None), (0.5, True), (0.5, False), (0.97, True)])
+def test_missing_patterns(cuda_device, p_missing, first_missing):
+    w = synth.random_problem(8, 3001, kind="matern32", p_missing=p_missing, first_missing=first_missing)
+    assert_parity(w)
+
+
+def test_uniform_fast_path(cuda_device):
+    w = synth.metric_workload(2 ** 16, uniform=True)
+    assert_parity(w)
+
+
+def test_large_gaps_and_far_field(cuda_device):
+    """Large gaps (dt >> lengthscale) and isolated observations: prior reversion."""
+    w = synth.random_problem(12, 5000, kind="matern52", p_missing=0.6, dt_scale=0.8, lengthscale=0.3)
+    assert_parity(w)
+
+
+def test_config2_full(cuda_device):
+    w = synth.config2()
+    assert_parity(w)
+
+
+@pytest.mark.slow
+def test_metric_full_size(cuda_device):
+    """Headline configuration (N = 2^24, bench.py's launch configuration)."""
+    w = synth.metric_workload(2 ** 24)
+    assert_parity(w)
+
+
+def test_nll_only_matches_posterior(cuda_device):
+    w = synth.random_problem(2, 20000, kind="matern52", p_missing=0.1)
+    m = P.Model(w.components, w.noise_var)
+    t, y, mk = to_dev(w)
+    _, _, nll_a = m.posterior(t, y, mk)
+    nll_b = m.nll(t, y, mk)
+    m.check()
+    assert float(nll_a.cpu()[0]) == float(nll_b.cpu()[0])
+
+
+def test_deterministic(cuda_device):
+    w = synth.random_problem(3, 100000, kind="matern52", p_missing=0.1)
+    m = P.Model(w.components, w.noise_var)
+    t, y, mk = to_dev(w)
+    a = [x.clone() for x in m.posterior(t, y, mk)]
+    b = m.posterior(t, y, mk)
+    for u, v in zip(a, b):
+        assert torch.equal(u, v)
+
+
+def test_host_api_matches_device(cuda_device):
+    w = synth.random_problem(4, 50000, kind="matern32", p_missing=0.2)
+    m = P.Model(w.components, w.noise_var)
+    t, y, mk = to_dev(w)
+    mean, var, nll = m.posterior(t, y, mk)
+    hm, hv, hn = m.posterior_host(w.t, w.y, w.mask)
+    np.testing.assert_array_equal(hm, mean.cpu().numpy())
+    np.testing.assert_array_equal(hv, var.cpu().numpy())
+    assert hn[0] == float(nll.cpu()[0])
+
+
+def test_input_errors(cuda_device):
+    w = synth.random_problem(6, 5000, kind="matern52", p_missing=0.2)
+    m = P.Model(w.components, w.noise_var)
+    t = w.t.copy(); t[3001] = t[3000] - 1e-6
+    tt, y, mk = to_dev(w)
+    tt = torch.from_numpy(t).cuda()
+    m.posterior(tt, y, mk)
+    with pytest.raises(P.PssgpError) as e:
+        m.check()
+    assert e.value.status == _native.PSSGP_E_INPUT and e.value.index == 3001
+    yb = w.y.copy(); obs = np.nonzero(w.mask)[0]; yb[obs[100]] = np.nan
+    m.posterior(to_dev(w)[0], torch.from_numpy(yb).cuda(), mk)
+    with pytest.raises(P.PssgpError) as e:
+        m.check()
+    assert e.value.status == _native.PSSGP_E_INPUT and e.value.index == obs[100]
+    m.posterior(*to_dev(w))
+    m.check()                                             # error latch was cleared
+
+
+def test_unsupported_irregular_dt(cuda_device):
+    w = synth.random_problem(6, 500, kind="matern52")
+    m = P.Model([synth.Component("rbf", 1.0, 0.5, order=3)], 0.1, uniform_dt=0.01)
+    m.posterior(*to_dev(w))
+    with pytest.raises(P.PssgpError) as e:
+        m.check()
+    assert e.value.status == _native.PSSGP_E_UNSUPPORTED
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_virtual_sharding(cuda_device, world):
+    """Time-sharded 3-phase protocol run shard by shard on one GPU (no kernel waits
+    on another), exchanging aggregates through device memory; must match the
+    unsharded path."""
+    w = synth.random_problem(9, 40003, kind="matern52", p_missing=0.2, ties=3)
+    ref_mean, ref_var, ref_nll, _ = run_gpu(w)
+    from paper_2102_09964_b200 import sharded
+    mean, var, nll = sharded.run_virtual(w.components, w.noise_var, w.t, w.y, w.mask, world)
+    em = np.max(np.abs(mean - ref_mean)) / np.max(np.abs(ref_mean))
+    ev = np.max(np.abs(var - ref_var) / ref_var)
+    assert em < 1e-11 and ev < 1e-11
+    assert abs(nll - ref_nll) < 1e-11 * abs(ref_nll)
+    o = oracle.posterior(w)
+    em, ev, en = errors((mean, var, nll), o)
+    assert em <= MEAN_TOL and ev <= VAR_TOL and en <= NLL_TOL

@@ -1,0 +1,117 @@
+"""CPU-only tests of the C-ABI library (no GPU): the shared library loads and
+exports every symbol include/pssgp.h declares, host-side model construction
+matches the oracle's SSM through basis-invariant quantities, and the
+discretisation the kernels run (pssgp_debug_discretize calls the same
+__host__ __device__ function) matches the oracle's Van Loan on the library's
+own model matrices.
+"""
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from oracle import ssm as ossm
+
+import paper_2102_09964_b200 as P
+from paper_2102_09964_b200 import _native
+
+HEADER = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "pssgp.h")
+
+
+def header_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(pssgp_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = _native.lib()
+    names = header_functions()
+    assert len(names) >= 19
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) == set(_native.SIGNATURES)  # the binding covers the whole ABI
+
+
+def test_create_errors():
+    with pytest.raises(P.PssgpError) as e:
+        P.pssgp_create([synth.Component("matern52", 1.0, 0.5)], -1.0)
+    assert e.value.status == _native.PSSGP_E_ARG
+    with pytest.raises(P.PssgpError) as e:
+        P.pssgp_create([synth.Component("matern52", 0.0, 0.5)], 0.1)
+    assert e.value.status == _native.PSSGP_E_ARG
+
+
+def _lib_ssm(h):
+    s = P.pssgp_get_ssm(h)
+    return ossm.SSM(s["G"], np.zeros((s["G"].shape[0], 1)), 0.0, s["H"], s["Pinf"], Wmat=s["W"]), s
+
+
+@pytest.mark.parametrize("kind", ["matern12", "matern32", "matern52"])
+def test_matern_model_reconstructs_kernel(kind):
+    comp = synth.Component(kind, 1.7, 0.6)
+    m = P.Model([comp], 0.1)
+    lm, s = _lib_ssm(m.h)
+    taus = np.linspace(0, 3.0, 40)
+    np.testing.assert_allclose(ossm.ssm_kernel(lm, taus), ossm.kernel_value(comp, taus), atol=1e-12 * 1.7)
+    # stationarity of the library's model: G P + P G^T + W = 0
+    res = s["G"] @ s["Pinf"] + s["Pinf"] @ s["G"].T + s["W"]
+    assert np.max(np.abs(res)) < 1e-12 * np.max(np.abs(s["W"]))
+
+
+def test_rbf_and_sum_models():
+    comp = synth.Component("rbf", 1.0, 0.5, order=3)
+    m = P.Model([comp], 0.1, uniform_dt=synth.H_FINE)
+    lm, s = _lib_ssm(m.h)
+    om = ossm.build([comp])
+    taus = np.linspace(0, 2.0, 30)
+    np.testing.assert_allclose(ossm.ssm_kernel(lm, taus), ossm.ssm_kernel(om, taus), rtol=1e-9, atol=1e-12)
+    comps = [synth.Component("periodic", 4.0, 1.0, period=1.0, order=6), synth.Component("matern32", 10.0, 20.0)]
+    with pytest.raises(P.PssgpError):   # d = 16 not compiled yet in this build -> E_UNSUPPORTED
+        P.Model(comps, 0.09, uniform_dt=1 / 52)
+
+
+@pytest.mark.parametrize("kind", ["matern12", "matern32", "matern52"])
+@pytest.mark.parametrize("dt", [0.0, 1e-9, 2.4e-7, 1.22e-4, 1e-3, 0.02, 0.3, 1.0, 2.5, 8.0, 40.0])
+def test_closed_form_discretisation_vs_oracle(kind, dt):
+    comp = synth.Component(kind, 1.3, 0.5)
+    m = P.Model([comp], 0.1)
+    lm, s = _lib_ssm(m.h)
+    F, Q = m.discretize(dt)
+    Fo, Qo = oracle.discretize(lm, dt)
+    assert np.max(np.abs(F - Fo)) <= 2e-14 * max(1.0, np.max(np.abs(Fo)))
+    qs = np.max(np.abs(s["Pinf"]))
+    assert np.max(np.abs(Q - Qo)) <= 1e-14 * qs
+    big = np.abs(Qo) > 1e-3 * max(np.max(np.abs(Qo)), 1e-300)
+    if big.any():
+        assert np.max(np.abs(Q - Qo)[big] / np.abs(Qo)[big]) < 1e-10
+
+
+def test_uniform_dt_table_vs_oracle():
+    for comp, dt in [(synth.Component("matern52", 1.0, 0.5), synth.H_FINE),
+                     (synth.Component("rbf", 1.0, 0.5, order=3), synth.H_FINE),
+                     (synth.Component("rbf", 1.0, 1.5, order=2), 0.01),
+                     (synth.Component("matern32", 2.0, 0.3), 0.05)]:
+        m = P.Model([comp], 0.1, uniform_dt=dt)
+        lm, s = _lib_ssm(m.h)
+        F, Q = m.discretize(dt)
+        Fo, Qo = oracle.discretize(lm, dt)
+        assert np.max(np.abs(F - Fo)) <= 1e-13 * max(1.0, np.max(np.abs(Fo)))
+        assert np.max(np.abs(Q - Qo)) <= 1e-12 * max(np.max(np.abs(Qo)), 1e-300)
+
+
+def test_irregular_dt_unsupported_for_non_matern():
+    m = P.Model([synth.Component("rbf", 1.0, 0.5, order=2)], 0.1, uniform_dt=0.01)
+    with pytest.raises(P.PssgpError) as e:
+        m.discretize(0.02)
+    assert e.value.status == _native.PSSGP_E_UNSUPPORTED
+
+
+def test_aggregate_bytes():
+    m = P.Model([synth.Component("matern52", 1.0, 0.5)], 0.1)
+    assert P.pssgp_aggregate_bytes(m.h, 0) == 27 * 8
+    assert P.pssgp_aggregate_bytes(m.h, 1) == 18 * 8
