@@ -430,7 +430,7 @@ pssgp_status pssgp_check(pssgp_model* m) {
     if (w == ~0ULL) return PSSGP_OK;
     cudaMemset(m->d_err, 0xff, sizeof(unsigned long long));
     const unsigned code = static_cast<unsigned>(w & 0xff);
-    const int64_t idx = static_cast<int64_t>(w >> 8);
+    const int64_t idx = static_cast<int64_t>((w >> 8) & 0xffffffffffffULL);
     const char* what = code == kErrInput ? "invalid input (unsorted/non-finite t or non-finite observed y)"
                        : code == kErrNumeric ? "numerical failure (S <= 0 or non-PD predicted covariance)"
                                              : "no device discretisation for this dt (set uniform_dt)";

@@ -37,11 +37,14 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kWin = 16;                // staging window (steps) per chain
 constexpr int kCarryThreads = 256;      // single-CTA scan kernels
 
-// error word: (index << 8) | code, atomicMin keeps the first failing index
+// error word: (class << 56) | (index << 8) | code; atomicMin keeps data errors
+// (input / unsupported dt, class 0) ahead of their numerical consequences
+// (class 1), then the first failing index.
 enum : unsigned { kErrInput = 2, kErrNumeric = 3, kErrUnsupported = 6 };
 
 __device__ __forceinline__ void raise_error(unsigned long long* err, int64_t gidx, unsigned code) {
-    const unsigned long long w = (static_cast<unsigned long long>(gidx) << 8) | code;
+    const unsigned long long cls = (code == kErrNumeric) ? 1ULL : 0ULL;
+    const unsigned long long w = (cls << 56) | ((static_cast<unsigned long long>(gidx) & 0xffffffffffffULL) << 8) | code;
     if (w < *reinterpret_cast<volatile unsigned long long*>(err)) atomicMin(err, w);
 }
 
@@ -344,7 +347,9 @@ __global__ void __launch_bounds__(kThreads, 3) k_filter_apply(const KParams<D> p
     for (int i = 0; i < D; ++i) x[i] = cur.x[i];
 #pragma unroll
     for (int i = 0; i < ns(D); ++i) P[i] = cur.P[i];
-    double x0[D], P0[ns(D)], Sg[D * D];      // entry state and cross-covariance for the smoother aggregate
+    // chain-entry moments E[x_k0 | y_1:k], Cov(x_k0 | y_1:k) and cross-covariance
+    // Cov(x_k0, x_k | y_1:k), carried along the chain for its smoother aggregate
+    double x0[D], P0[ns(D)], Sg[D * D];
     double quad = 0.0, prodm = 1.0;
     long long prode = 0;
     int nobs = 0;
@@ -441,6 +446,13 @@ __global__ void __launch_bounds__(kThreads, 3) k_filter_apply(const KParams<D> p
                         for (int i = 0; i < D; ++i)
 #pragma unroll
                             for (int j = 0; j < D; ++j) Sg[i * D + j] = fma(-SH[i] * iS, HP[j], Sm[i * D + j]);
+                        // entry moments conditioned on y_1:k: E[x_k0 | .] += SH v/S, Cov -= SH SH^T / S
+#pragma unroll
+                        for (int i = 0; i < D; ++i) {
+                            x0[i] = fma(SH[i], vs, x0[i]);
+#pragma unroll
+                            for (int j = i; j < D; ++j) P0[si(D, i, j)] = fma(-SH[i] * iS, SH[j], P0[si(D, i, j)]);
+                        }
                     }
                     // NLL term 0.5 (log 2 pi S + v^2 / S): log of a running product (exponent kept apart)
                     quad = fma(v, vs, quad);

@@ -641,8 +641,9 @@ PS_HD void kf_predict(const double (&x)[D], const double (&P)[ns(D)], const doub
 // ------------------------------------------------------------------ chain smoother aggregate
 // The ordered product (x)_s of the smoother elements of steps k0..k1 is the
 // Gaussian conditional p(x_k0 | x_{k1+1}, y_1:k1) (each element is
-// p(x_k | x_{k+1}, y_1:k), reading Z2; Markov property).  With the filtered
-// entry moments (x0, P0), the cross-covariance Sm = Cov(x_k0, x_{k1+1} | y_1:k1)
+// p(x_k | x_{k+1}, y_1:k), reading Z2; Markov property).  With the chain-entry
+// moments conditioned on the whole chain, x0 = E[x_k0 | y_1:k1] and
+// P0 = Cov(x_k0 | y_1:k1), the cross-covariance Sm = Cov(x_k0, x_{k1+1} | y_1:k1)
 // and the predicted (xm, Pm) of step k1+1 it is
 //   E = Sm Pm^-1,  g = x0 - E xm,  L = P0 - E Sm^T.
 template <int D>
