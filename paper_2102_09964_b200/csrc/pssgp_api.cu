@@ -30,6 +30,7 @@ struct pssgp_model {
     int d = 0;
     ph::Ssm ssm;                 // balanced host model (long double)
     bool closed = false;         // standalone Matern closed form
+    int mode = kTable;           // DiscMode of the kernels (kClosed / kTable / kMixed)
     double lam = 0.0, s2 = 0.0, r = 0.0;
     double udt = 0.0;
     std::vector<double> Fu, Qu;  // F(udt), Q(udt) row-major d x d
@@ -144,9 +145,9 @@ pssgp_status ensure_device(pssgp_model* m) {
 template <int D>
 int occupancy() {
     int a = 0, b = 0, c = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_filter_reduce<D>, kThreads, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_filter_apply<D>, kThreads, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k_smoother_apply<D>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_filter_reduce<D, kClosed>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_filter_apply<D, kClosed>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k_smoother_apply<D, kClosed>, kThreads, 0);
     return std::max(1, std::min(a, std::min(b, c)));
 }
 
@@ -212,6 +213,14 @@ pssgp_status setup(pssgp_model* m, const Plan& pl, KParams<D>& p) {
     return PSSGP_OK;
 }
 
+// launch kernel template KERN<D, mode> with the model's discretisation mode
+#define LAUNCH_MODE(m, KERN, grid, block, s, p)                                  \
+    do {                                                                         \
+        if ((m)->mode == kClosed) KERN<D, kClosed><<<grid, block, 0, s>>>(p);    \
+        else if ((m)->mode == kMixed) KERN<D, kMixed><<<grid, block, 0, s>>>(p); \
+        else KERN<D, kTable><<<grid, block, 0, s>>>(p);                          \
+    } while (0)
+
 #define LAUNCH_CHECK(m, where)                                    \
     do {                                                          \
         cudaError_t e_ = cudaGetLastError();                      \
@@ -221,7 +230,7 @@ pssgp_status setup(pssgp_model* m, const Plan& pl, KParams<D>& p) {
 template <int D>
 pssgp_status phase_filter_reduce(pssgp_model* m, KParams<D>& p, cudaStream_t s) {
     ProfScope ps(m, S_K1, s);
-    k_filter_reduce<D><<<p.nb, kThreads, 0, s>>>(p);
+    LAUNCH_MODE(m, k_filter_reduce, p.nb, kThreads, s, p);
     LAUNCH_CHECK(m, "k_filter_reduce");
     return PSSGP_OK;
 }
@@ -235,7 +244,7 @@ pssgp_status phase_filter_apply(pssgp_model* m, KParams<D>& p, cudaStream_t s) {
     }
     {
         ProfScope ps(m, S_K3, s);
-        k_filter_apply<D><<<p.nb, kThreads, 0, s>>>(p);
+        LAUNCH_MODE(m, k_filter_apply, p.nb, kThreads, s, p);
         LAUNCH_CHECK(m, "k_filter_apply");
     }
     return PSSGP_OK;
@@ -250,7 +259,7 @@ pssgp_status phase_smoother(pssgp_model* m, KParams<D>& p, cudaStream_t s) {
     }
     {
         ProfScope ps(m, S_K5, s);
-        k_smoother_apply<D><<<p.nb, kThreads, 0, s>>>(p);
+        LAUNCH_MODE(m, k_smoother_apply, p.nb, kThreads, s, p);
         LAUNCH_CHECK(m, "k_smoother_apply");
     }
     return PSSGP_OK;
@@ -380,6 +389,7 @@ pssgp_status pssgp_create(const pssgp_component* comps, int n_comps, double nois
         m->Qu.resize(Q.size());
         for (size_t i = 0; i < F.size(); ++i) { m->Fu[i] = static_cast<double>(F[i]); m->Qu[i] = static_cast<double>(Q[i]); }
     }
+    m->mode = m->closed ? (m->udt > 0.0 ? kMixed : kClosed) : kTable;
     *out = m;
     return PSSGP_OK;
 }

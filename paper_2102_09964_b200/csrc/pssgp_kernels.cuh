@@ -157,7 +157,7 @@ __device__ __forceinline__ void stage_in(StageIn& s, const double* __restrict__ 
 }
 
 // ------------------------------------------------------------------ K1: fold chains
-template <int D>
+template <int D, int MODE>
 __global__ void __launch_bounds__(kThreads, 3) k_filter_reduce(const KParams<D> p) {
     __shared__ StageIn st[kWarps];
     __shared__ FAgg<D> wagg[kWarps];
@@ -171,31 +171,42 @@ __global__ void __launch_bounds__(kThreads, 3) k_filter_reduce(const KParams<D> 
     FAgg<D> a;
     set_identity(a);
     double tprev = 0.0;
-    if (kb < p.n && (kb > 0 || p.k0 > 0)) tprev = __ldg(p.t + kb - 1);
+    // first step of the chain, peeled (the only place the global first element,
+    // F = 0 / Q = P_inf (Eq. (7)), can occur)
+    if (kb < ke) {
+        if (kb > 0 || p.k0 > 0) tprev = __ldg(p.t + kb - 1);
+        const double tk = __ldg(p.t + kb);
+        const bool obs = __ldg(p.mask + kb) != 0;
+        const double yk = obs ? __ldg(p.y + kb) : 0.0;
+        const int64_t g = p.k0 + kb;
+        double F[D * D], Q[ns(D)];
+        const double dt = tk - tprev;
+        if (g == 0) {
+#pragma unroll
+            for (int i = 0; i < D * D; ++i) F[i] = 0.0;
+#pragma unroll
+            for (int i = 0; i < ns(D); ++i) Q[i] = p.m.Pinf[i];
+        } else if (disc<D, MODE>(p.m, dt, F, Q)) {
+            raise_error(p.err, g, kErrUnsupported);
+        }
+        if ((g > 0 && !(dt >= 0.0)) || !isfinite(tk) || (obs && !isfinite(yk))) raise_error(p.err, g, kErrInput);
+        fold_step<D>(a, F, Q, p.m, obs, yk);
+        tprev = tk;
+    }
 
     for (int64_t j0 = 0; j0 < p.K; j0 += kWin) {
         stage_in(st[wid], p.t, p.y, p.mask, wbase, p.K, p.n, j0, lane, true);
 #pragma unroll 1
-        for (int jj = 0; jj < kWin; ++jj) {
+        for (int jj = (j0 == 0) ? 1 : 0; jj < kWin; ++jj) {
             const int64_t k = kb + j0 + jj;
             if (k < ke) {
                 const double tk = st[wid].t[lane][jj];
                 const bool obs = st[wid].m[lane][jj] != 0;
                 const double yk = st[wid].y[lane][jj];
-                const int64_t g = p.k0 + k;
                 double F[D * D], Q[ns(D)];
-                if (g == 0) {
-#pragma unroll
-                    for (int i = 0; i < D * D; ++i) F[i] = 0.0;
-#pragma unroll
-                    for (int i = 0; i < ns(D); ++i) Q[i] = p.m.Pinf[i];
-                    if (!isfinite(tk)) raise_error(p.err, g, kErrInput);
-                } else {
-                    const double dt = tk - tprev;
-                    if (!(dt >= 0.0) || !isfinite(tk)) raise_error(p.err, g, kErrInput);
-                    if (discretize<D>(p.m, dt, F, Q)) raise_error(p.err, g, kErrUnsupported);
-                }
-                if (obs && !isfinite(yk)) raise_error(p.err, g, kErrInput);
+                const double dt = tk - tprev;
+                if (disc<D, MODE>(p.m, dt, F, Q)) raise_error(p.err, p.k0 + k, kErrUnsupported);
+                if (!(dt >= 0.0) || !isfinite(tk) || (obs && !isfinite(yk))) raise_error(p.err, p.k0 + k, kErrInput);
                 fold_step<D>(a, F, Q, p.m, obs, yk);
                 tprev = tk;
             }
@@ -290,8 +301,45 @@ __global__ void __launch_bounds__(kCarryThreads, 1) k_filter_carry(const KParams
     }
 }
 
-// ------------------------------------------------------------------ K3: Kalman rescan
+// observation-row terms of a predicted (xm, Pm): HP = Pm H^T, S = H Pm H^T + r, hx = H xm
 template <int D>
+__device__ __forceinline__ void obs_terms(const ModelParams<D>& m, const double (&xm)[D], const double (&Pm)[ns(D)],
+                                          double (&HP)[D], double& S, double& hx) {
+    if (m.h_unit) {
+#pragma unroll
+        for (int i = 0; i < D; ++i) HP[i] = Pm[si(D, i, 0)];
+        S = Pm[0] + m.r;
+        hx = xm[0];
+    } else {
+        S = m.r; hx = 0.0;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            double s2 = 0.0;
+#pragma unroll
+            for (int j = 0; j < D; ++j) s2 = fma(Pm[si(D, i, j)], m.H[j], s2);
+            HP[i] = s2;
+            hx = fma(m.H[i], xm[i], hx);
+        }
+#pragma unroll
+        for (int i = 0; i < D; ++i) S = fma(m.H[i], HP[i], S);
+    }
+}
+
+// NLL term 0.5 (log 2 pi S + v^2/S): v^2/S summed, S multiplied into a running
+// product whose binary exponent is kept apart (one log per chain).
+__device__ __forceinline__ void nll_accumulate(bool obs, double v, double vs, double S, double& quad, double& prodm,
+                                               long long& prode, int& nobs) {
+    quad = fma(v, vs, quad);
+    prodm *= obs ? S : 1.0;
+    long long bits = __double_as_longlong(prodm);
+    prode += ((bits >> 52) & 0x7ff) - 1023;
+    bits = (bits & ~(0x7ffLL << 52)) | (1023LL << 52);
+    prodm = __longlong_as_double(bits);
+    nobs += obs ? 1 : 0;
+}
+
+// ------------------------------------------------------------------ K3: Kalman rescan
+template <int D, int MODE>
 __global__ void __launch_bounds__(kThreads, 3) k_filter_apply(const KParams<D> p) {
     __shared__ StageIn st[kWarps];
     __shared__ FAgg<D> tot[kWarps];
@@ -307,200 +355,163 @@ __global__ void __launch_bounds__(kThreads, 3) k_filter_apply(const KParams<D> p
     const int64_t ke = min(kb + p.K, p.n);
 
     // ---- carry into this chain: block carry (x) exclusive scan of chain aggregates
-    FAgg<D> a;
-    load_soa(a, p.chain_f, nch, c);
+    Gauss<D> cur;
+    {
+        FAgg<D> a;
+        load_soa(a, p.chain_f, nch, c);
 #pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        FAgg<D> o;
-        shfl_up_all(o, a, off);
-        if (lane >= off) {
-            FAgg<D> r;
-            combine(o, a, r);
-            a = r;
+        for (int off = 1; off < 32; off <<= 1) {
+            FAgg<D> o;
+            shfl_up_all(o, a, off);
+            if (lane >= off) {
+                FAgg<D> r;
+                combine(o, a, r);
+                a = r;
+            }
         }
-    }
-    if (lane == 31) tot[wid] = a;
-    FAgg<D> ex;
-    shfl_up_all(ex, a, 1);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        Gauss<D> acc;
-        load_aos(acc, p.fcarry + static_cast<int64_t>(blockIdx.x) * CN(D));
-        for (int w = 0; w < kWarps; ++w) {
-            wcar[w] = acc;
+        if (lane == 31) tot[wid] = a;
+        FAgg<D> ex;
+        shfl_up_all(ex, a, 1);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            Gauss<D> acc;
+            load_aos(acc, p.fcarry + static_cast<int64_t>(blockIdx.x) * CN(D));
+            for (int w = 0; w < kWarps; ++w) {
+                wcar[w] = acc;
+                Gauss<D> r2;
+                apply_prefix(acc, tot[w], r2);
+                acc = r2;
+            }
+        }
+        __syncthreads();
+        cur = wcar[wid];
+        if (lane > 0) {
             Gauss<D> r2;
-            apply_prefix(acc, tot[w], r2);
-            acc = r2;
+            apply_prefix(cur, ex, r2);
+            cur = r2;
         }
-    }
-    __syncthreads();
-    Gauss<D> cur = wcar[wid];
-    if (lane > 0) {
-        Gauss<D> r2;
-        apply_prefix(cur, ex, r2);
-        cur = r2;
     }
 
-    // ---- Kalman filter over the chain (supplement PAPER.md:285-315)
+    // ---- Kalman filter over the chain (supplement PAPER.md:285-315), carrying the
+    // chain-entry moments E[x_k0 | y_1:k], Cov(x_k0 | y_1:k) and the cross-covariance
+    // Cov(x_k0, x_k | y_1:k) for the chain's smoother aggregate.
     double x[D], P[ns(D)];
 #pragma unroll
     for (int i = 0; i < D; ++i) x[i] = cur.x[i];
 #pragma unroll
     for (int i = 0; i < ns(D); ++i) P[i] = cur.P[i];
-    // chain-entry moments E[x_k0 | y_1:k], Cov(x_k0 | y_1:k) and cross-covariance
-    // Cov(x_k0, x_k | y_1:k), carried along the chain for its smoother aggregate
     double x0[D], P0[ns(D)], Sg[D * D];
     double quad = 0.0, prodm = 1.0;
     long long prode = 0;
     int nobs = 0;
     double tprev = 0.0;
-    if (kb < p.n && (kb > 0 || p.k0 > 0)) tprev = __ldg(p.t + kb - 1);
-    SAgg<D> sag;
-    set_identity(sag);
-    bool sag_done = false;
+    // ---- first step of the chain (peeled: global first element, entry moments)
+    if (kb < ke) {
+        if (kb > 0 || p.k0 > 0) tprev = __ldg(p.t + kb - 1);
+        const double tk = __ldg(p.t + kb);
+        const bool obs = __ldg(p.mask + kb) != 0;
+        const double yk = obs ? __ldg(p.y + kb) : 0.0;
+        const int64_t g = p.k0 + kb;
+        double xm[D], Pm[ns(D)];
+        if (g == 0) {
+#pragma unroll
+            for (int i = 0; i < D; ++i) xm[i] = 0.0;
+#pragma unroll
+            for (int i = 0; i < ns(D); ++i) Pm[i] = p.m.Pinf[i];
+        } else {
+            double F[D * D], Q[ns(D)], FP[D * D];
+            disc<D, MODE>(p.m, tk - tprev, F, Q);
+            kf_predict<D>(x, P, F, Q, xm, FP, Pm);
+        }
+        tprev = tk;
+        double HP[D], S, hx;
+        obs_terms<D>(p.m, xm, Pm, HP, S, hx);
+        if (obs && !(S > 0.0 && S < INFINITY)) raise_error(p.err, g, kErrNumeric);
+        const double iS = obs ? rcp(S) : 0.0;
+        const double v = obs ? (yk - hx) : 0.0;
+        const double vs = v * iS;
+#pragma unroll
+        for (int i = 0; i < D; ++i) x[i] = fma(HP[i], vs, xm[i]);
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+            for (int j = i; j < D; ++j) P[si(D, i, j)] = fma(-HP[i] * iS, HP[j], Pm[si(D, i, j)]);
+#pragma unroll
+        for (int i = 0; i < D; ++i) x0[i] = x[i];
+#pragma unroll
+        for (int i = 0; i < ns(D); ++i) P0[i] = P[i];
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+            for (int j = 0; j < D; ++j) Sg[i * D + j] = P[si(D, i, j)];
+        nll_accumulate(obs, v, vs, S, quad, prodm, prode, nobs);
+        if (p.store_state) {
+            double* o = p.xp + (wg * p.K * CN(D)) * 32 + lane;
+#pragma unroll
+            for (int i = 0; i < D; ++i) o[i * 32] = x[i];
+#pragma unroll
+            for (int i = 0; i < ns(D); ++i) o[(D + i) * 32] = P[i];
+        }
+    }
 
     for (int64_t j0 = 0; j0 < p.K; j0 += kWin) {
         stage_in(st[wid], p.t, p.y, p.mask, wbase, p.K, p.n, j0, lane, true);
 #pragma unroll 1
-        for (int jj = 0; jj < kWin; ++jj) {
+        for (int jj = (j0 == 0) ? 1 : 0; jj < kWin; ++jj) {
             const int64_t k = kb + j0 + jj;
             if (k < ke) {
                 const double tk = st[wid].t[lane][jj];
                 const bool obs = st[wid].m[lane][jj] != 0;
                 const double yk = st[wid].y[lane][jj];
-                const int64_t g = p.k0 + k;
                 double xm[D], Pm[ns(D)], FP[D * D], F[D * D], Q[ns(D)];
-                if (g == 0) {
-#pragma unroll
-                    for (int i = 0; i < D; ++i) xm[i] = 0.0;
-#pragma unroll
-                    for (int i = 0; i < ns(D); ++i) Pm[i] = p.m.Pinf[i];
-#pragma unroll
-                    for (int i = 0; i < D * D; ++i) F[i] = 0.0;
-                } else {
-                    discretize<D>(p.m, tk - tprev, F, Q);
-                    kf_predict<D>(x, P, F, Q, xm, FP, Pm);
-                }
+                disc<D, MODE>(p.m, tk - tprev, F, Q);
+                kf_predict<D>(x, P, F, Q, xm, FP, Pm);
                 tprev = tk;
-                const bool first = (k == kb);
-                // cross-covariance prediction Sigma- = Sigma F^T (k > kb)
-                double Sm[D * D];
-                if (!first) {
+                // observation update (branchless: missing y -> 1/S = 0, v = 0)
+                double HP[D], S, hx;
+                obs_terms<D>(p.m, xm, Pm, HP, S, hx);
+                if (obs && !(S > 0.0 && S < INFINITY)) raise_error(p.err, p.k0 + k, kErrNumeric);
+                const double iS = obs ? rcp(S) : 0.0;
+                const double v = obs ? (yk - hx) : 0.0;
+                const double vs = v * iS;
 #pragma unroll
-                    for (int i = 0; i < D; ++i)
+                for (int i = 0; i < D; ++i) x[i] = fma(HP[i], vs, xm[i]);
 #pragma unroll
-                        for (int j = 0; j < D; ++j) {
-                            double s = 0.0;
+                for (int i = 0; i < D; ++i)
 #pragma unroll
-                            for (int l = 0; l < D; ++l) s = fma(Sg[i * D + l], F[j * D + l], s);
-                            Sm[i * D + j] = s;
-                        }
-                    if (g == p.nglob - 1 && p.store_state) {
-                        // smoother aggregate over kb..g-1 (next = g), then (x) terminal after the update
-                        if (!chain_smoother_agg<D>(x0, P0, Sm, xm, Pm, sag)) raise_error(p.err, g, kErrNumeric);
+                    for (int j = i; j < D; ++j) P[si(D, i, j)] = fma(-HP[i] * iS, HP[j], Pm[si(D, i, j)]);
+                // Sigma- = Sigma F^T, then the rank-one update by y_k of the
+                // cross-covariance and of the chain-entry moments
+                double Sm[D * D], SH[D];
+#pragma unroll
+                for (int i = 0; i < D; ++i)
+#pragma unroll
+                    for (int j = 0; j < D; ++j) {
+                        double s2 = 0.0;
+#pragma unroll
+                        for (int l = 0; l < D; ++l) s2 = fma(Sg[i * D + l], F[j * D + l], s2);
+                        Sm[i * D + j] = s2;
+                    }
+#pragma unroll
+                for (int i = 0; i < D; ++i) {
+                    if (p.m.h_unit) SH[i] = Sm[i * D];
+                    else {
+                        double s2 = 0.0;
+#pragma unroll
+                        for (int j = 0; j < D; ++j) s2 = fma(Sm[i * D + j], p.m.H[j], s2);
+                        SH[i] = s2;
                     }
                 }
-                if (obs) {
-                    double HP[D], S, hx;
-                    if (p.m.h_unit) {
 #pragma unroll
-                        for (int i = 0; i < D; ++i) HP[i] = Pm[si(D, i, 0)];
-                        S = Pm[0] + p.m.r;
-                        hx = xm[0];
-                    } else {
-                        S = p.m.r; hx = 0.0;
+                for (int i = 0; i < D; ++i) {
+                    const double si_ = SH[i] * iS;
 #pragma unroll
-                        for (int i = 0; i < D; ++i) {
-                            double s = 0.0;
+                    for (int j = 0; j < D; ++j) Sg[i * D + j] = fma(-si_, HP[j], Sm[i * D + j]);
+                    x0[i] = fma(SH[i], vs, x0[i]);
 #pragma unroll
-                            for (int j = 0; j < D; ++j) s = fma(Pm[si(D, i, j)], p.m.H[j], s);
-                            HP[i] = s;
-                            hx = fma(p.m.H[i], xm[i], hx);
-                        }
-#pragma unroll
-                        for (int i = 0; i < D; ++i) S = fma(p.m.H[i], HP[i], S);
-                    }
-                    if (!(S > 0.0) || !isfinite(S)) raise_error(p.err, g, kErrNumeric);
-                    const double iS = 1.0 / S;
-                    const double v = yk - hx;
-                    const double vs = v * iS;
-#pragma unroll
-                    for (int i = 0; i < D; ++i) x[i] = fma(HP[i], vs, xm[i]);
-#pragma unroll
-                    for (int i = 0; i < D; ++i)
-#pragma unroll
-                        for (int j = i; j < D; ++j) P[si(D, i, j)] = fma(-HP[i] * iS, HP[j], Pm[si(D, i, j)]);
-                    if (!first) {
-                        double SH[D];
-#pragma unroll
-                        for (int i = 0; i < D; ++i) {
-                            if (p.m.h_unit) SH[i] = Sm[i * D];
-                            else {
-                                double s = 0.0;
-#pragma unroll
-                                for (int j = 0; j < D; ++j) s = fma(Sm[i * D + j], p.m.H[j], s);
-                                SH[i] = s;
-                            }
-                        }
-#pragma unroll
-                        for (int i = 0; i < D; ++i)
-#pragma unroll
-                            for (int j = 0; j < D; ++j) Sg[i * D + j] = fma(-SH[i] * iS, HP[j], Sm[i * D + j]);
-                        // entry moments conditioned on y_1:k: E[x_k0 | .] += SH v/S, Cov -= SH SH^T / S
-#pragma unroll
-                        for (int i = 0; i < D; ++i) {
-                            x0[i] = fma(SH[i], vs, x0[i]);
-#pragma unroll
-                            for (int j = i; j < D; ++j) P0[si(D, i, j)] = fma(-SH[i] * iS, SH[j], P0[si(D, i, j)]);
-                        }
-                    }
-                    // NLL term 0.5 (log 2 pi S + v^2 / S): log of a running product (exponent kept apart)
-                    quad = fma(v, vs, quad);
-                    prodm *= S;
-                    {
-                        long long bits = __double_as_longlong(prodm);
-                        prode += ((bits >> 52) & 0x7ff) - 1023;
-                        bits = (bits & ~(0x7ffLL << 52)) | (1023LL << 52);
-                        prodm = __longlong_as_double(bits);
-                    }
-                    ++nobs;
-                } else {
-#pragma unroll
-                    for (int i = 0; i < D; ++i) x[i] = xm[i];
-#pragma unroll
-                    for (int i = 0; i < ns(D); ++i) P[i] = Pm[i];
-                    if (!first) {
-#pragma unroll
-                        for (int i = 0; i < D * D; ++i) Sg[i] = Sm[i];
-                    }
+                    for (int j = i; j < D; ++j) P0[si(D, i, j)] = fma(-si_, SH[j], P0[si(D, i, j)]);
                 }
-                if (first) {
-#pragma unroll
-                    for (int i = 0; i < D; ++i) x0[i] = x[i];
-#pragma unroll
-                    for (int i = 0; i < ns(D); ++i) P0[i] = P[i];
-#pragma unroll
-                    for (int i = 0; i < D; ++i)
-#pragma unroll
-                        for (int j = 0; j < D; ++j) Sg[i * D + j] = P[si(D, i, j)];
-                }
-                if (g == p.nglob - 1 && p.store_state) {
-                    // terminal element (0, xbar_N, P_N)
-                    Gauss<D> term, res;
-#pragma unroll
-                    for (int i = 0; i < D; ++i) term.x[i] = x[i];
-#pragma unroll
-                    for (int i = 0; i < ns(D); ++i) term.P[i] = P[i];
-                    if (first) res = term;
-                    else apply_suffix(sag, term, res);
-#pragma unroll
-                    for (int i = 0; i < D * D; ++i) sag.E[i] = 0.0;
-#pragma unroll
-                    for (int i = 0; i < D; ++i) sag.g[i] = res.x[i];
-#pragma unroll
-                    for (int i = 0; i < ns(D); ++i) sag.L[i] = res.P[i];
-                    sag_done = true;
-                }
+                nll_accumulate(obs, v, vs, S, quad, prodm, prode, nobs);
                 if (p.store_state) {
                     double* o = p.xp + ((wg * p.K + (k - kb)) * CN(D)) * 32 + lane;
 #pragma unroll
@@ -513,23 +524,35 @@ __global__ void __launch_bounds__(kThreads, 3) k_filter_apply(const KParams<D> p
         __syncwarp();
     }
 
-    // ---- chain smoother aggregate: peek one step past the chain (prediction only)
+    // ---- chain smoother aggregate
     if (p.store_state) {
-        if (ke > kb && !sag_done) {
-            const int64_t g1 = p.k0 + ke;   // global index of the next step
-            if (g1 < p.nglob) {
+        SAgg<D> sag;
+        set_identity(sag);
+        if (ke > kb) {
+            if (p.k0 + ke == p.nglob) {
+                // chain ending with the terminal element (0, xbar_N, P_N): the entry
+                // moments conditioned on all data are the smoothed moments -> (0, m^s_k0, P^s_k0)
+#pragma unroll
+                for (int i = 0; i < D * D; ++i) sag.E[i] = 0.0;
+#pragma unroll
+                for (int i = 0; i < D; ++i) sag.g[i] = x0[i];
+#pragma unroll
+                for (int i = 0; i < ns(D); ++i) sag.L[i] = P0[i];
+            } else {
+                // peek one step past the chain (prediction only)
+                const int64_t g1 = p.k0 + ke;
                 const double tn = __ldg(p.t + ke);
                 double F[D * D], Q[ns(D)], xm[D], Pm[ns(D)], FP[D * D], Sm[D * D];
-                discretize<D>(p.m, tn - tprev, F, Q);
+                disc<D, MODE>(p.m, tn - tprev, F, Q);
                 kf_predict<D>(x, P, F, Q, xm, FP, Pm);
 #pragma unroll
                 for (int i = 0; i < D; ++i)
 #pragma unroll
                     for (int j = 0; j < D; ++j) {
-                        double s = 0.0;
+                        double s2 = 0.0;
 #pragma unroll
-                        for (int l = 0; l < D; ++l) s = fma(Sg[i * D + l], F[j * D + l], s);
-                        Sm[i * D + j] = s;
+                        for (int l = 0; l < D; ++l) s2 = fma(Sg[i * D + l], F[j * D + l], s2);
+                        Sm[i * D + j] = s2;
                     }
                 if (!chain_smoother_agg<D>(x0, P0, Sm, xm, Pm, sag)) raise_error(p.err, g1, kErrNumeric);
             }
@@ -558,9 +581,9 @@ __global__ void __launch_bounds__(kThreads, 3) k_filter_apply(const KParams<D> p
     if (lane == 0) nred[wid] = nl;
     __syncthreads();
     if (threadIdx.x == 0) {
-        double s = 0.0;
-        for (int w = 0; w < kWarps; ++w) s += nred[w];
-        p.nll_block[blockIdx.x] = s;
+        double s2 = 0.0;
+        for (int w = 0; w < kWarps; ++w) s2 += nred[w];
+        p.nll_block[blockIdx.x] = s2;
         if (p.store_state) {
             SAgg<D> acc = stot[0];
             for (int w = 1; w < kWarps; ++w) {
@@ -635,12 +658,32 @@ __global__ void __launch_bounds__(kCarryThreads, 1) k_smoother_carry(const KPara
 }
 
 // ------------------------------------------------------------------ K5: RTS rescan
+// f-space projection: mean = H m^s, var = H P^s H^T
+template <int D>
+__device__ __forceinline__ void project(const ModelParams<D>& m, const double (&ms)[D], const double (&Ps)[ns(D)],
+                                        double& mo, double& vo) {
+    if (m.h_unit) {
+        mo = ms[0];
+        vo = Ps[0];
+    } else {
+        mo = 0.0; vo = 0.0;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            mo = fma(m.H[i], ms[i], mo);
+            double s2 = 0.0;
+#pragma unroll
+            for (int j = 0; j < D; ++j) s2 = fma(Ps[si(D, i, j)], m.H[j], s2);
+            vo = fma(m.H[i], s2, vo);
+        }
+    }
+}
+
 struct StageOut {
     double t[32][kWin + 1];   // staged t; each lane overwrites its own slot with the mean
     double b[32][kWin + 1];   // variance
 };
 
-template <int D>
+template <int D, int MODE>
 __global__ void __launch_bounds__(kThreads, 3) k_smoother_apply(const KParams<D> p) {
     __shared__ StageOut so[kWarps];
     __shared__ SAgg<D> tot[kWarps];
@@ -654,52 +697,89 @@ __global__ void __launch_bounds__(kThreads, 3) k_smoother_apply(const KParams<D>
     const int64_t ke = min(kb + p.K, p.n);
 
     // ---- carry: exclusive reverse scan of chain smoother aggregates (x) block carry
-    SAgg<D> a;
-    load_soa(a, p.chain_s, nch, c);
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        SAgg<D> o;
-        shfl_down_all(o, a, off);
-        if (lane + off < 32) {
-            SAgg<D> r;
-            combine(a, o, r);
-            a = r;
-        }
-    }
-    if (lane == 0) tot[wid] = a;
-    SAgg<D> ex;
-    shfl_down_all(ex, a, 1);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        Gauss<D> acc;
-        load_aos(acc, p.scarry + static_cast<int64_t>(blockIdx.x) * CN(D));
-        wcar[kWarps] = acc;
-        for (int w = kWarps - 1; w >= 0; --w) {
-            wcar[w + 1] = acc;
-            Gauss<D> r2;
-            apply_suffix(tot[w], acc, r2);
-            acc = r2;
-        }
-    }
-    __syncthreads();
-    Gauss<D> cur = wcar[wid + 1];
-    if (lane < 31) {
-        Gauss<D> r2;
-        apply_suffix(ex, cur, r2);
-        cur = r2;
-    }
     double ms[D], Ps[ns(D)];
+    {
+        SAgg<D> a;
+        load_soa(a, p.chain_s, nch, c);
 #pragma unroll
-    for (int i = 0; i < D; ++i) ms[i] = cur.x[i];
+        for (int off = 1; off < 32; off <<= 1) {
+            SAgg<D> o;
+            shfl_down_all(o, a, off);
+            if (lane + off < 32) {
+                SAgg<D> r;
+                combine(a, o, r);
+                a = r;
+            }
+        }
+        if (lane == 0) tot[wid] = a;
+        SAgg<D> ex;
+        shfl_down_all(ex, a, 1);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            Gauss<D> acc;
+            load_aos(acc, p.scarry + static_cast<int64_t>(blockIdx.x) * CN(D));
+            wcar[kWarps] = acc;
+            for (int w = kWarps - 1; w >= 0; --w) {
+                wcar[w + 1] = acc;
+                Gauss<D> r2;
+                apply_suffix(tot[w], acc, r2);
+                acc = r2;
+            }
+        }
+        __syncthreads();
+        Gauss<D> cur = wcar[wid + 1];
+        if (lane < 31) {
+            Gauss<D> r2;
+            apply_suffix(ex, cur, r2);
+            cur = r2;
+        }
 #pragma unroll
-    for (int i = 0; i < ns(D); ++i) Ps[i] = cur.P[i];
+        for (int i = 0; i < D; ++i) ms[i] = cur.x[i];
+#pragma unroll
+        for (int i = 0; i < ns(D); ++i) Ps[i] = cur.P[i];
+    }
 
-    // ---- RTS over the chain, last step first
+    // ---- RTS over the chain, last step first; the filtered
+    // (xbar, P) of the next step down is prefetched one step ahead.
+    const double* xpw = p.xp + (wg * p.K * CN(D)) * 32 + lane;
+    double nx[CN(D)];
     double tnext = 0.0;
-    if (ke > kb && p.k0 + ke < p.nglob) tnext = __ldg(p.t + ke);
+    // last step of the chain, peeled (the only place the terminal element can occur);
+    // its outputs are stored directly (one scalar store per chain)
+    if (ke > kb) {
+        const int64_t k = ke - 1;
+        const double* src = xpw + ((k - kb) * CN(D)) * 32;
+        double x[D], P[ns(D)];
+#pragma unroll
+        for (int i = 0; i < D; ++i) x[i] = src[i * 32];
+#pragma unroll
+        for (int i = 0; i < ns(D); ++i) P[i] = src[(D + i) * 32];
+        if (k > kb) {
+            const double* s1 = xpw + ((k - 1 - kb) * CN(D)) * 32;
+#pragma unroll
+            for (int i = 0; i < CN(D); ++i) nx[i] = s1[i * 32];
+        }
+        const double tk = __ldg(p.t + k);
+        if (p.k0 + k == p.nglob - 1) {
+#pragma unroll
+            for (int i = 0; i < D; ++i) ms[i] = x[i];
+#pragma unroll
+            for (int i = 0; i < ns(D); ++i) Ps[i] = P[i];
+        } else {
+            const double tn = __ldg(p.t + ke);
+            double F[D * D], Q[ns(D)], xm[D], Pm[ns(D)], FP[D * D];
+            disc<D, MODE>(p.m, tn - tk, F, Q);
+            kf_predict<D>(x, P, F, Q, xm, FP, Pm);
+            if (!rts_step<D>(x, P, xm, Pm, FP, ms, Ps)) raise_error(p.err, p.k0 + k, kErrNumeric);
+        }
+        tnext = tk;
+        double mo, vo;
+        project<D>(p.m, ms, Ps, mo, vo);
+        if (p.mean) p.mean[k] = mo;
+        if (p.var) p.var[k] = vo;
+    }
     const int64_t jtop = ((p.K - 1) / kWin) * kWin;
     for (int64_t j0 = jtop; j0 >= 0; j0 -= kWin) {
-        // stage t for this window
         {
             constexpr int RPI = 32 / kWin;
             const int col = lane % kWin, rsub = lane / kWin;
@@ -715,42 +795,25 @@ __global__ void __launch_bounds__(kThreads, 3) k_smoother_apply(const KParams<D>
 #pragma unroll 1
         for (int jj = kWin - 1; jj >= 0; --jj) {
             const int64_t k = kb + j0 + jj;
-            if (k < ke) {
+            if (k < ke - 1) {
                 const double tk = so[wid].t[lane][jj];
-                const int64_t g = p.k0 + k;
                 double x[D], P[ns(D)];
-                const double* src = p.xp + ((wg * p.K + (k - kb)) * CN(D)) * 32 + lane;
 #pragma unroll
-                for (int i = 0; i < D; ++i) x[i] = src[i * 32];
+                for (int i = 0; i < D; ++i) x[i] = nx[i];
 #pragma unroll
-                for (int i = 0; i < ns(D); ++i) P[i] = src[(D + i) * 32];
-                if (g == p.nglob - 1) {
+                for (int i = 0; i < ns(D); ++i) P[i] = nx[D + i];
+                if (k > kb) {
+                    const double* src = xpw + ((k - 1 - kb) * CN(D)) * 32;
 #pragma unroll
-                    for (int i = 0; i < D; ++i) ms[i] = x[i];
-#pragma unroll
-                    for (int i = 0; i < ns(D); ++i) Ps[i] = P[i];
-                } else {
-                    double F[D * D], Q[ns(D)], xm[D], Pm[ns(D)], FP[D * D];
-                    discretize<D>(p.m, tnext - tk, F, Q);
-                    kf_predict<D>(x, P, F, Q, xm, FP, Pm);
-                    if (!rts_step<D>(x, P, xm, Pm, FP, ms, Ps)) raise_error(p.err, g, kErrNumeric);
+                    for (int i = 0; i < CN(D); ++i) nx[i] = src[i * 32];
                 }
+                double F[D * D], Q[ns(D)], xm[D], Pm[ns(D)], FP[D * D];
+                disc<D, MODE>(p.m, tnext - tk, F, Q);
+                kf_predict<D>(x, P, F, Q, xm, FP, Pm);
+                if (!rts_step<D>(x, P, xm, Pm, FP, ms, Ps)) raise_error(p.err, p.k0 + k, kErrNumeric);
                 tnext = tk;
                 double mo, vo;
-                if (p.m.h_unit) {
-                    mo = ms[0];
-                    vo = Ps[0];
-                } else {
-                    mo = 0.0; vo = 0.0;
-#pragma unroll
-                    for (int i = 0; i < D; ++i) {
-                        mo = fma(p.m.H[i], ms[i], mo);
-                        double s = 0.0;
-#pragma unroll
-                        for (int j = 0; j < D; ++j) s = fma(Ps[si(D, i, j)], p.m.H[j], s);
-                        vo = fma(p.m.H[i], s, vo);
-                    }
-                }
+                project<D>(p.m, ms, Ps, mo, vo);
                 so[wid].t[lane][jj] = mo;
                 so[wid].b[lane][jj] = vo;
             }
@@ -764,7 +827,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_smoother_apply(const KParams<D>
                 const int r = r0 + rsub;
                 const int64_t j = j0 + col;
                 const int64_t idx = wbase + r * p.K + j;
-                if ((j < p.K) && (idx < p.n)) {
+                const int64_t last = min(wbase + (r + 1) * p.K, p.n) - 1;   // row r's peeled step
+                if ((j < p.K) && (idx < last)) {
                     if (p.mean) p.mean[idx] = so[wid].t[r][col];
                     if (p.var) p.var[idx] = so[wid].b[r][col];
                 }

@@ -37,6 +37,78 @@ PS_CX int FN(int D) { return D * D + 2 * D + 2 * ns(D); }  // filter aggregate d
 PS_CX int SN(int D) { return D * D + D + ns(D); }          // smoother aggregate doubles
 PS_CX int CN(int D) { return D + ns(D); }                  // (mean, cov) pair doubles
 
+// ------------------------------------------------------------------ branch-free scalar math
+// Constants live in a table (device: __constant__, host: constexpr) so the
+// kernels read them as constant-bank operands instead of re-materialising
+// 64-bit literals with uniform-register moves.
+struct MathConsts {
+    double expc[14];   // 1/k!, k = 0..13 (Taylor of e^r on |r| <= ln2/2, error < 5e-18)
+    double inv[32];    // 1/n, n = 0..31 (inv[0] unused)
+    double q52[9];     // Matern-5/2 Q polynomial coefficients
+};
+#define PS_MATH_CONSTS                                                                         \
+    {{1.0, 1.0, 1.0 / 2, 1.0 / 6, 1.0 / 24, 1.0 / 120, 1.0 / 720, 1.0 / 5040, 1.0 / 40320,     \
+      1.0 / 362880, 1.0 / 3628800, 1.0 / 39916800, 1.0 / 479001600, 1.0 / 6227020800.0},        \
+     {0.0, 1.0, 1.0 / 2, 1.0 / 3, 1.0 / 4, 1.0 / 5, 1.0 / 6, 1.0 / 7, 1.0 / 8, 1.0 / 9, 1.0 / 10, \
+      1.0 / 11, 1.0 / 12, 1.0 / 13, 1.0 / 14, 1.0 / 15, 1.0 / 16, 1.0 / 17, 1.0 / 18, 1.0 / 19,   \
+      1.0 / 20, 1.0 / 21, 1.0 / 22, 1.0 / 23, 1.0 / 24, 1.0 / 25, 1.0 / 26, 1.0 / 27, 1.0 / 28,   \
+      1.0 / 29, 1.0 / 30, 1.0 / 31},                                                          \
+     {1.0 / 24, 1.0 / 9, 1.0 / 18, 1.0 / 3, 2.0 / 9, 1.0 / 36, 2.0 / 3, 8.0 / 3, 4.0 / 3}}
+#if defined(__CUDACC__)
+static __constant__ MathConsts d_mc = PS_MATH_CONSTS;
+#endif
+static constexpr MathConsts h_mc = PS_MATH_CONSTS;
+PS_HD const MathConsts& mc() {
+#if defined(__CUDA_ARCH__)
+    return d_mc;
+#else
+    return h_mc;
+#endif
+}
+
+// Reciprocal of a positive normal double, branch-free: scale into [1, 2) by
+// exponent-field arithmetic, fp32 hardware reciprocal as the seed (~2^-23),
+// two Newton steps in fp64 (error squared each: < 2^-90), scale back.
+// Host: plain division.
+PS_HD double rcp(double a) {
+#if defined(__CUDA_ARCH__)
+    const long long bits = __double_as_longlong(a);
+    const long long ex = bits & 0x7ff0000000000000LL;
+    const double m = __longlong_as_double((bits & ~0x7ff0000000000000LL) | 0x3ff0000000000000LL);  // [1, 2)
+    float rf;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rf) : "f"(__double2float_rn(m)));
+    double r = static_cast<double>(rf);
+    double e = fma(-m, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-m, r, 1.0);
+    r = fma(r, e, r);                                                     // 1/m in (0.5, 1]
+    // 1/a = r * 2^-(E-1023): subtract the exponent field (result stays normal for normal a
+    // with E in (1, 2046))
+    return __longlong_as_double(__double_as_longlong(r) - (ex - 0x3ff0000000000000LL));
+#else
+    return 1.0 / a;
+#endif
+}
+
+// e^{-z} for z >= 0, branch-free: n = rint(z / ln2), r = n ln2 - z (Cody-Waite),
+// Taylor-13 of e^r, times 2^-n by exponent arithmetic.  z is clamped to 708
+// (e^-708 ~ 3e-308: below every quantity the kernels combine it with).
+PS_HD double exp_neg(double z) {
+#if defined(__CUDA_ARCH__)
+    const MathConsts& C = mc();
+    z = fmin(fmax(z, 0.0), 708.0);
+    const double n = rint(z * 1.4426950408889634);
+    const double r = fma(n, 1.9082149292705877e-10, fma(n, 0.6931471803691238, -z));
+    double pz = C.expc[13];
+#pragma unroll
+    for (int k = 12; k >= 0; --k) pz = fma(pz, r, C.expc[k]);
+    const long long ni = static_cast<long long>(n);
+    return __longlong_as_double(__double_as_longlong(pz) - (ni << 52));
+#else
+    return std::exp(-z);
+#endif
+}
+
 // Model constants the kernels need (kernel parameter, i.e. constant bank).
 template <int D>
 struct ModelParams {
@@ -144,7 +216,7 @@ PS_HD bool gauss_solve(double (&M)[D * D], double (&R)[D * NR]) {
         }
         const double piv = M[c * D + c];
         ok = ok && (piv != 0.0);
-        const double ip = 1.0 / piv;
+        const double ip = rcp(piv);
 #pragma unroll
         for (int r = c + 1; r < D; ++r) {
             const double f = M[r * D + c] * ip;
@@ -181,7 +253,7 @@ PS_HD bool ldlt(const double (&S)[ns(D)], double (&Lo)[D * D], double (&id)[D]) 
         for (int k = 0; k < j; ++k) d = fma(-Lo[j * D + k] * dd[k], Lo[j * D + k], d);
         ok = ok && (d > 0.0);
         dd[j] = d;
-        id[j] = 1.0 / d;
+        id[j] = rcp(d);
 #pragma unroll
         for (int i = j + 1; i < D; ++i) {
             double s = S[si(D, i, j)];
@@ -223,28 +295,30 @@ PS_HD void ldlt_solve(const double (&Lo)[D * D], const double (&id)[D], double (
 // 1 - e^{-x} sum_{n<m} x^n/n! above (cancellation <= ~20x there).
 template <int M>
 PS_HD double inc_gamma_tail(double x, double emx) {
-    double lead = emx;  // e^{-x} x^M / M!
+    const MathConsts& C = mc();
+    double xm = x;
 #pragma unroll
-    for (int n = 1; n <= M; ++n) lead *= x / n;
+    for (int n = 1; n < M; ++n) xm *= x;
+    const double lead = emx * xm * C.expc[M];  // e^{-x} x^M / M!
     if (x <= 0.015625) {
         double s = 1.0;
 #pragma unroll
-        for (int j = 7; j >= 1; --j) s = fma(s * x, 1.0 / (M + j), 1.0);
+        for (int j = 7; j >= 1; --j) s = fma(s * x, C.inv[M + j], 1.0);
         return lead * s;
     } else if (x <= 0.5) {
         double s = 1.0;
 #pragma unroll
-        for (int j = 13; j >= 1; --j) s = fma(s * x, 1.0 / (M + j), 1.0);
+        for (int j = 13; j >= 1; --j) s = fma(s * x, C.inv[M + j], 1.0);
         return lead * s;
     } else if (x <= 2.0) {
         double s = 1.0;
 #pragma unroll
-        for (int j = 22; j >= 1; --j) s = fma(s * x, 1.0 / (M + j), 1.0);
+        for (int j = 22; j >= 1; --j) s = fma(s * x, C.inv[M + j], 1.0);
         return lead * s;
     } else {
         double p = 1.0, term = 1.0;
 #pragma unroll
-        for (int n = 1; n < M; ++n) { term *= x / n; p += term; }
+        for (int n = 1; n < M; ++n) { term *= x * C.inv[n]; p += term; }
         return fma(-emx, p, 1.0);
     }
 }
@@ -255,67 +329,81 @@ PS_HD double inc_gamma_tail(double x, double emx) {
 // tools/derive_matern.py).  x = 2 z.
 template <int D>
 PS_HD void matern_closed(double lam, double s2, double dt, double (&F)[D * D], double (&Q)[ns(D)]) {
+    const MathConsts& C = mc();
     const double z = lam * dt;
-    const double e = exp(-z);
+    const double e = exp_neg(z);
     const double x = 2.0 * z;
     const double ex = e * e;  // e^{-x}
     if constexpr (D == 1) {
         F[0] = e;
-        Q[0] = -s2 * expm1(-x);
+        Q[0] = s2 * inc_gamma_tail<1>(x, ex);
     } else if constexpr (D == 2) {
         F[0] = e * (1.0 + z); F[1] = e * z;
         F[2] = -e * z;        F[3] = e * (1.0 - z);
         const double R3 = inc_gamma_tail<3>(x, ex);
+        const double se = s2 * ex;
         Q[si(2, 0, 0)] = s2 * R3;
-        Q[si(2, 0, 1)] = s2 * ex * (0.5 * x * x);
-        Q[si(2, 1, 1)] = s2 * fma(2.0 * x, ex, R3);
+        Q[si(2, 0, 1)] = se * (0.5 * x * x);
+        Q[si(2, 1, 1)] = fma(se, 2.0 * x, s2 * R3);
     } else if constexpr (D == 3) {
         const double z2 = z * z;
-        F[0] = e * (1.0 + z + 0.5 * z2); F[1] = e * (z + z2);          F[2] = e * (0.5 * z2);
-        F[3] = e * (-0.5 * z2);          F[4] = e * (1.0 + z - z2);    F[5] = e * (z - 0.5 * z2);
-        F[6] = e * (0.5 * z2 - z);       F[7] = e * (z2 - 3.0 * z);    F[8] = e * (1.0 - 2.0 * z + 0.5 * z2);
-        const double R5 = inc_gamma_tail<5>(x, ex);
+        const double hz2 = 0.5 * z2;
+        F[0] = e * (1.0 + z + hz2); F[1] = e * (z + z2);       F[2] = e * hz2;
+        F[3] = -e * hz2;            F[4] = e * (1.0 + z - z2); F[5] = e * (z - hz2);
+        F[6] = e * (hz2 - z);       F[7] = e * fma(-3.0, z, z2); F[8] = e * (1.0 - 2.0 * z + hz2);
+        const double R5 = s2 * inc_gamma_tail<5>(x, ex);
+        const double se = s2 * ex;
         const double x2 = x * x, x3 = x2 * x, x4 = x2 * x2;
-        Q[si(3, 0, 0)] = s2 * R5;
-        Q[si(3, 0, 1)] = s2 * ex * (x4 * (1.0 / 24.0));
-        Q[si(3, 0, 2)] = s2 * fma(ex, x3 * (1.0 / 9.0) - x4 * (1.0 / 18.0), -R5 * (1.0 / 3.0));
-        Q[si(3, 1, 1)] = s2 * fma(ex, x3 * (2.0 / 9.0) - x4 * (1.0 / 36.0), R5 * (1.0 / 3.0));
-        Q[si(3, 1, 2)] = s2 * ex * (x2 * (2.0 / 3.0) - x3 * (1.0 / 3.0) + x4 * (1.0 / 24.0));
-        Q[si(3, 2, 2)] = s2 * fma(ex, x * (8.0 / 3.0) - x2 * (4.0 / 3.0) + x3 * (2.0 / 3.0), R5);
+        Q[si(3, 0, 0)] = R5;
+        Q[si(3, 0, 1)] = se * (x4 * C.q52[0]);
+        Q[si(3, 0, 2)] = fma(se, fma(x3, C.q52[1], -x4 * C.q52[2]), -R5 * C.q52[3]);
+        Q[si(3, 1, 1)] = fma(se, fma(x3, C.q52[4], -x4 * C.q52[5]), R5 * C.q52[3]);
+        Q[si(3, 1, 2)] = se * fma(x4, C.q52[0], fma(x2, C.q52[6], -x3 * C.q52[3]));
+        Q[si(3, 2, 2)] = fma(se, fma(x, C.q52[7], fma(x3, C.q52[6], -x2 * C.q52[8])), R5);
     }
 }
 
 // Discretise one step (transition into a step whose predecessor is dt earlier).
 // Returns 0, or a nonzero code when the model has no device discretisation for dt.
-template <int D>
-PS_HD int discretize(const ModelParams<D>& p, double dt, double (&F)[D * D], double (&Q)[ns(D)]) {
-    if (dt == p.udt) {
-#pragma unroll
-        for (int i = 0; i < D * D; ++i) F[i] = p.Fu[i];
-#pragma unroll
-        for (int i = 0; i < ns(D); ++i) Q[i] = p.Qu[i];
+// MODE (compile time): kClosed = Matern closed form only (dt = 0 gives F = I,
+// Q = 0 exactly), kTable = the host-precomputed pair for dt == udt (dt = 0 ->
+// I, 0; anything else unsupported), kMixed = table for dt == udt else closed.
+enum DiscMode : int { kClosed = 0, kTable = 1, kMixed = 2 };
+
+template <int D, int MODE>
+PS_HD int disc(const ModelParams<D>& p, double dt, double (&F)[D * D], double (&Q)[ns(D)]) {
+    if constexpr (MODE == kClosed) {
+        if constexpr (D <= 3) matern_closed<D>(p.lam, p.s2, dt, F, Q);
         return 0;
-    }
-    if (dt == 0.0) {
+    } else {
+        if (dt == p.udt) {
 #pragma unroll
-        for (int i = 0; i < D; ++i)
+            for (int i = 0; i < D * D; ++i) F[i] = p.Fu[i];
 #pragma unroll
-            for (int j = 0; j < D; ++j) F[i * D + j] = (i == j) ? 1.0 : 0.0;
-#pragma unroll
-        for (int i = 0; i < ns(D); ++i) Q[i] = 0.0;
-        return 0;
-    }
-    if constexpr (D <= 3) {
-        if (p.closed) {
-            matern_closed<D>(p.lam, p.s2, dt, F, Q);
+            for (int i = 0; i < ns(D); ++i) Q[i] = p.Qu[i];
             return 0;
         }
+        if constexpr (MODE == kMixed && D <= 3) {
+            matern_closed<D>(p.lam, p.s2, dt, F, Q);
+            return 0;
+        } else {
+            const bool zero = (dt == 0.0);
+#pragma unroll
+            for (int i = 0; i < D; ++i)
+#pragma unroll
+                for (int j = 0; j < D; ++j) F[i * D + j] = (zero && i == j) ? 1.0 : 0.0;
+#pragma unroll
+            for (int i = 0; i < ns(D); ++i) Q[i] = 0.0;
+            return zero ? 0 : 1;
+        }
     }
-#pragma unroll
-    for (int i = 0; i < D * D; ++i) F[i] = 0.0;
-#pragma unroll
-    for (int i = 0; i < ns(D); ++i) Q[i] = 0.0;
-    return 1;
+}
+
+// Host-side dispatcher used by pssgp_debug_discretize.
+template <int D>
+PS_HD int discretize(const ModelParams<D>& p, double dt, double (&F)[D * D], double (&Q)[ns(D)]) {
+    if (p.closed) return p.udt > 0.0 ? disc<D, kMixed>(p, dt, F, Q) : disc<D, kClosed>(p, dt, F, Q);
+    return disc<D, kTable>(p, dt, F, Q);
 }
 
 // ------------------------------------------------------------------ filter fold
@@ -356,57 +444,48 @@ PS_HD void fold_step(FAgg<D>& a, const double (&F)[D * D], const double (&Q)[ns(
             for (int k = 0; k < D; ++k) s = fma(T[i * D + k], F[j * D + k], s);
             Cm[si(D, i, j)] = s;
         }
-    if (obs) {
-        double HC[D], w[D], hb, S;
-        if (p.h_unit) {
+    // observation update; branchless: a missing y (Eqs. (6), (8)) is the same
+    // formulas with 1/S and the innovation set to zero (A = F A, b = F b, C = C-)
+    double HC[D], w[D], hb, S;
+    if (p.h_unit) {
 #pragma unroll
-            for (int i = 0; i < D; ++i) { HC[i] = Cm[si(D, i, 0)]; w[i] = FA[i]; }
-            hb = Fb[0];
-            S = Cm[0] + p.r;
-        } else {
-            hb = 0.0; S = p.r;
-#pragma unroll
-            for (int i = 0; i < D; ++i) {
-                double s = 0.0, ww = 0.0;
-#pragma unroll
-                for (int j = 0; j < D; ++j) {
-                    s = fma(Cm[si(D, i, j)], p.H[j], s);
-                    ww = fma(p.H[j], FA[j * D + i], ww);
-                }
-                HC[i] = s; w[i] = ww;
-                hb = fma(p.H[i], Fb[i], hb);
-            }
-#pragma unroll
-            for (int i = 0; i < D; ++i) S = fma(p.H[i], HC[i], S);
-        }
-        const double iS = 1.0 / S;
-        const double v = yk - hb;
-        const double vs = v * iS;
-        double Kc[D];
-#pragma unroll
-        for (int i = 0; i < D; ++i) Kc[i] = HC[i] * iS;
+        for (int i = 0; i < D; ++i) { HC[i] = Cm[si(D, i, 0)]; w[i] = FA[i]; }
+        hb = Fb[0];
+        S = Cm[0] + p.r;
+    } else {
+        hb = 0.0; S = p.r;
 #pragma unroll
         for (int i = 0; i < D; ++i) {
+            double s = 0.0, ww = 0.0;
 #pragma unroll
-            for (int j = 0; j < D; ++j) a.A[i * D + j] = fma(-Kc[i], w[j], FA[i * D + j]);
-            a.b[i] = fma(HC[i], vs, Fb[i]);
-            a.eta[i] = fma(w[i], vs, a.eta[i]);
+            for (int j = 0; j < D; ++j) {
+                s = fma(Cm[si(D, i, j)], p.H[j], s);
+                ww = fma(p.H[j], FA[j * D + i], ww);
+            }
+            HC[i] = s; w[i] = ww;
+            hb = fma(p.H[i], Fb[i], hb);
         }
 #pragma unroll
-        for (int i = 0; i < D; ++i)
-#pragma unroll
-            for (int j = i; j < D; ++j) {
-                a.C[si(D, i, j)] = fma(-Kc[i], HC[j], Cm[si(D, i, j)]);
-                a.J[si(D, i, j)] = fma(w[i] * iS, w[j], a.J[si(D, i, j)]);
-            }
-    } else {
-#pragma unroll
-        for (int i = 0; i < D * D; ++i) a.A[i] = FA[i];
-#pragma unroll
-        for (int i = 0; i < D; ++i) a.b[i] = Fb[i];
-#pragma unroll
-        for (int i = 0; i < ns(D); ++i) a.C[i] = Cm[i];
+        for (int i = 0; i < D; ++i) S = fma(p.H[i], HC[i], S);
     }
+    const double iS = obs ? rcp(S) : 0.0;
+    const double v = obs ? (yk - hb) : 0.0;
+    const double vs = v * iS;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        const double Kc = HC[i] * iS;
+#pragma unroll
+        for (int j = 0; j < D; ++j) a.A[i * D + j] = fma(-Kc, w[j], FA[i * D + j]);
+        a.b[i] = fma(HC[i], vs, Fb[i]);
+        a.eta[i] = fma(w[i], vs, a.eta[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = i; j < D; ++j) {
+            a.C[si(D, i, j)] = fma(-HC[i] * iS, HC[j], Cm[si(D, i, j)]);
+            a.J[si(D, i, j)] = fma(w[i] * iS, w[j], a.J[si(D, i, j)]);
+        }
 }
 
 // ------------------------------------------------------------------ general filtering operator
