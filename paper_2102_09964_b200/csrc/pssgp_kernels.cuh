@@ -32,6 +32,9 @@
 
 namespace pssgp {
 
+#ifndef PSSGP_MINB
+#define PSSGP_MINB 3                    // resident CTAs per SM the main kernels are register-capped for
+#endif
 constexpr int kThreads = 128;           // threads per CTA (4 warps)
 constexpr int kWarps = kThreads / 32;
 constexpr int kWin = 16;                // staging window (steps) per chain
@@ -124,42 +127,48 @@ __device__ __forceinline__ void store_aos(const T& a, double* base) {
     for (int i = 0; i < n; ++i) base[i] = s[i];
 }
 
-// ------------------------------------------------------------------ coalesced staging
-// A warp's 32 chains are 32 contiguous segments of K steps.  A window of kWin
-// steps of all 32 chains is loaded row by row (each row = kWin consecutive
-// steps of one chain, 2 rows per warp instruction) into padded shared memory,
-// then each lane reads its own row (conflict-free: row stride kWin+1 doubles).
-struct StageIn {
-    double t[32][kWin + 1];
-    double y[32][kWin + 1];
-    unsigned char m[32][kWin + 4];
+// ------------------------------------------------------------------ asynchronous staging
+// A warp's 32 chains are 32 contiguous segments of K steps.  Windows of kWinA
+// steps of t and y for all 32 chains are copied global -> shared with cp.async
+// (8-byte copies, 8 lanes per 64-byte row segment) into a TRANSPOSED, padded
+// layout [step][chain] so that each lane later reads its own chain
+// conflict-free; two buffers per warp so the copy of window w+1 overlaps the
+// arithmetic of window w.  Out-of-range elements are zero-filled (src-size 0).
+// The observation mask is prefetched one step ahead into a register instead.
+constexpr int kWinA = 8;
+struct AsyncStage {
+    double t[2][kWinA][33];
+    double y[2][kWinA][33];
 };
 
-__device__ __forceinline__ void stage_in(StageIn& s, const double* __restrict__ t, const double* __restrict__ y,
-                                         const uint8_t* __restrict__ mask, int64_t wbase, int64_t K,
-                                         int64_t n, int64_t j0, int lane, bool with_y) {
-    constexpr int RPI = 32 / kWin;
-    const int col = lane % kWin, rsub = lane / kWin;
-#pragma unroll 4
-    for (int r0 = 0; r0 < 32; r0 += RPI) {
-        const int r = r0 + rsub;
-        const int64_t j = j0 + col;
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, int src_bytes) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ void issue_window(AsyncStage& s, int buf, const double* __restrict__ t,
+                                             const double* __restrict__ y, int64_t wbase, int64_t K, int64_t n,
+                                             int64_t j0, int lane) {
+    const int col = lane & (kWinA - 1), rb = lane / kWinA;
+    const int64_t j = j0 + col;
+#pragma unroll
+    for (int i = 0; i < 32 / (32 / kWinA); ++i) {
+        const int r = rb + (32 / kWinA) * i;
         const int64_t idx = wbase + r * K + j;
         const bool ok = (j < K) && (idx < n);
-        s.t[r][col] = ok ? __ldg(t + idx) : 0.0;
-        if (with_y) {
-            const unsigned char mk = ok ? __ldg(mask + idx) : (unsigned char)0;
-            s.m[r][col] = mk;
-            s.y[r][col] = (ok && mk) ? __ldg(y + idx) : 0.0;
-        }
+        cp_async8(&s.t[buf][col][r], ok ? t + idx : t, ok ? 8 : 0);
+        cp_async8(&s.y[buf][col][r], ok ? y + idx : y, ok ? 8 : 0);
     }
-    __syncwarp();
+    cp_async_commit();
 }
 
 // ------------------------------------------------------------------ K1: fold chains
 template <int D, int MODE>
-__global__ void __launch_bounds__(kThreads, 3) k_filter_reduce(const KParams<D> p) {
-    __shared__ StageIn st[kWarps];
+__global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_reduce(const KParams<D> p) {
+    __shared__ AsyncStage st[kWarps];
     __shared__ FAgg<D> wagg[kWarps];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t c = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
@@ -194,15 +203,24 @@ __global__ void __launch_bounds__(kThreads, 3) k_filter_reduce(const KParams<D> 
         tprev = tk;
     }
 
-    for (int64_t j0 = 0; j0 < p.K; j0 += kWin) {
-        stage_in(st[wid], p.t, p.y, p.mask, wbase, p.K, p.n, j0, lane, true);
+    const int64_t nwin = (p.K + kWinA - 1) / kWinA;
+    issue_window(st[wid], 0, p.t, p.y, wbase, p.K, p.n, 0, lane);
+    unsigned char mk = (kb + 1 < ke) ? __ldg(p.mask + kb + 1) : 0;   // mask of the next step
+    for (int64_t w = 0; w < nwin; ++w) {
+        const int64_t j0 = w * kWinA;
+        const int buf = static_cast<int>(w & 1);
+        if (w + 1 < nwin) issue_window(st[wid], buf ^ 1, p.t, p.y, wbase, p.K, p.n, j0 + kWinA, lane);
+        else cp_async_commit();
+        cp_async_wait<1>();
+        __syncwarp();
 #pragma unroll 1
-        for (int jj = (j0 == 0) ? 1 : 0; jj < kWin; ++jj) {
+        for (int jj = (w == 0) ? 1 : 0; jj < kWinA; ++jj) {
             const int64_t k = kb + j0 + jj;
             if (k < ke) {
-                const double tk = st[wid].t[lane][jj];
-                const bool obs = st[wid].m[lane][jj] != 0;
-                const double yk = st[wid].y[lane][jj];
+                const double tk = st[wid].t[buf][jj][lane];
+                const bool obs = mk != 0;
+                const double yk = obs ? st[wid].y[buf][jj][lane] : 0.0;
+                mk = (k + 1 < ke) ? __ldg(p.mask + k + 1) : 0;
                 double F[D * D], Q[ns(D)];
                 const double dt = tk - tprev;
                 if (disc<D, MODE>(p.m, dt, F, Q)) raise_error(p.err, p.k0 + k, kErrUnsupported);
@@ -340,8 +358,8 @@ __device__ __forceinline__ void nll_accumulate(bool obs, double v, double vs, do
 
 // ------------------------------------------------------------------ K3: Kalman rescan
 template <int D, int MODE>
-__global__ void __launch_bounds__(kThreads, 3) k_filter_apply(const KParams<D> p) {
-    __shared__ StageIn st[kWarps];
+__global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KParams<D> p) {
+    __shared__ AsyncStage st[kWarps];
     __shared__ FAgg<D> tot[kWarps];
     __shared__ Gauss<D> wcar[kWarps];
     __shared__ SAgg<D> stot[kWarps];
@@ -454,15 +472,24 @@ __global__ void __launch_bounds__(kThreads, 3) k_filter_apply(const KParams<D> p
         }
     }
 
-    for (int64_t j0 = 0; j0 < p.K; j0 += kWin) {
-        stage_in(st[wid], p.t, p.y, p.mask, wbase, p.K, p.n, j0, lane, true);
+    const int64_t nwin = (p.K + kWinA - 1) / kWinA;
+    issue_window(st[wid], 0, p.t, p.y, wbase, p.K, p.n, 0, lane);
+    unsigned char mk = (kb + 1 < ke) ? __ldg(p.mask + kb + 1) : 0;   // mask of the next step
+    for (int64_t w = 0; w < nwin; ++w) {
+        const int64_t j0 = w * kWinA;
+        const int buf = static_cast<int>(w & 1);
+        if (w + 1 < nwin) issue_window(st[wid], buf ^ 1, p.t, p.y, wbase, p.K, p.n, j0 + kWinA, lane);
+        else cp_async_commit();
+        cp_async_wait<1>();
+        __syncwarp();
 #pragma unroll 1
-        for (int jj = (j0 == 0) ? 1 : 0; jj < kWin; ++jj) {
+        for (int jj = (w == 0) ? 1 : 0; jj < kWinA; ++jj) {
             const int64_t k = kb + j0 + jj;
             if (k < ke) {
-                const double tk = st[wid].t[lane][jj];
-                const bool obs = st[wid].m[lane][jj] != 0;
-                const double yk = st[wid].y[lane][jj];
+                const double tk = st[wid].t[buf][jj][lane];
+                const bool obs = mk != 0;
+                const double yk = obs ? st[wid].y[buf][jj][lane] : 0.0;
+                mk = (k + 1 < ke) ? __ldg(p.mask + k + 1) : 0;
                 double xm[D], Pm[ns(D)], FP[D * D], F[D * D], Q[ns(D)];
                 disc<D, MODE>(p.m, tk - tprev, F, Q);
                 kf_predict<D>(x, P, F, Q, xm, FP, Pm);
@@ -684,7 +711,7 @@ struct StageOut {
 };
 
 template <int D, int MODE>
-__global__ void __launch_bounds__(kThreads, 3) k_smoother_apply(const KParams<D> p) {
+__global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_smoother_apply(const KParams<D> p) {
     __shared__ StageOut so[kWarps];
     __shared__ SAgg<D> tot[kWarps];
     __shared__ Gauss<D> wcar[kWarps + 1];
