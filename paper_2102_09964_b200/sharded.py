@@ -95,14 +95,23 @@ class DeviceShard:
         return self.mean, self.var
 
 
-def nccl_exchange(x):
-    """all_gather of a 1-D device tensor into [world, len] (rank order)."""
+def torch_exchange(x):
+    """all_gather of a 1-D tensor into [world, len] in rank order (NCCL: one
+    all_gather_into_tensor over NVLink; gloo: list all_gather, for CPU tests)."""
     import torch
     import torch.distributed as dist
     world = dist.get_world_size()
-    out = torch.empty((world,) + tuple(x.shape), dtype=x.dtype, device=x.device)
-    dist.all_gather_into_tensor(out, x.contiguous())
-    return out
+    x = x.contiguous()
+    if dist.get_backend() == "nccl":
+        out = torch.empty((world,) + tuple(x.shape), dtype=x.dtype, device=x.device)
+        dist.all_gather_into_tensor(out, x)
+        return out
+    parts = [torch.empty_like(x) for _ in range(world)]
+    dist.all_gather(parts, x)
+    return torch.stack(parts)
+
+
+nccl_exchange = torch_exchange
 
 
 def chunk_inputs(t: np.ndarray, y: np.ndarray, mask: np.ndarray, k0: int, n: int, device):
