@@ -31,10 +31,27 @@ sys.path.insert(0, ROOT)
 
 METRIC = "time-steps/s (filter+smoother+NLL, fp64) Matern-5/2 N=2^24"
 UNIT = "time-steps/s"
-# algorithmic bytes per time step moved by each kernel at d = 3
+# algorithmic bytes per time step moved by each kernel at d = 3 (DESIGN.md §6 "Roofline")
 ALG_BYTES = {"k_filter_reduce": 17, "k_filter_apply": 17 + 72, "k_smoother_apply": 8 + 72 + 16}
-# executed fp64 operations per time step of each kernel (DFMA = 2 flops), DESIGN.md ledger
+# fp64 flops per time step of each kernel (DFMA = 2), Matern-5/2 closed-form path, from the ncu
+# SASS counts of the committed profile (tools/fp64_flops.py)
+FLOPS_PER_STEP = {"k_filter_reduce": 350.2, "k_filter_apply": 359.1, "k_smoother_apply": 423.5}
+# fp64 peak derived in DESIGN.md §6: 148 SM x 64 FMA/clk x 2 flop x 1.965 GHz
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
 THROTTLE_BAD = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+
+
+def ncu_traffic(kernel: str):
+    """dram read+write bytes per launch of `kernel` from the latest committed ncu summary."""
+    import csv
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "ncu_full_*_summary.csv")))
+    for f in reversed(files):
+        for row in csv.DictReader(open(f)):
+            if kernel in row["Kernel Name"]:
+                return (float(row["dram__bytes_read.sum"]) + float(row["dram__bytes_write.sum"])) * 1e9, \
+                    os.path.relpath(f, ROOT)
+    return None, None
 
 
 def parse():
@@ -200,25 +217,31 @@ def main():
     model.check()
     torch.cuda.synchronize()
 
-    clocks = ClockSampler(local)
-    clocks.start()
-    P.pssgp_profile_enable(model.h, True)
-    P.pssgp_profile_read(model.h)  # reset
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    ev0.record(stream)
-    for _ in range(args.steps):
-        step()
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    ms_total = ev0.elapsed_time(ev1)
-    prof = P.pssgp_profile_read(model.h)
-    P.pssgp_profile_enable(model.h, False)
-    clk = clocks.stop()
+    def timed_region():
+        clocks = ClockSampler(local)
+        clocks.start()
+        P.pssgp_profile_enable(model.h, True)
+        P.pssgp_profile_read(model.h)  # reset
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        ms = ev0.elapsed_time(ev1)
+        prof_ = P.pssgp_profile_read(model.h)
+        P.pssgp_profile_enable(model.h, False)
+        return ms, prof_, clocks.stop()
+
+    ms_total, prof, clk = timed_region()
+    if set(clk.get("reasons", [])) & THROTTLE_BAD:      # rejected run: measure once more
+        ms_total, prof, clk = timed_region()
+        clk["remeasured"] = True
     model.check()
     if dist:
         tt_ = torch.tensor([ms_total], dtype=torch.float64, device=dev)
@@ -264,17 +287,32 @@ def main():
     dom_ms, dom_launches = kern[dom]
     per_launch_ms = dom_ms / dom_launches
     alg_b = ALG_BYTES.get(dom, 0) * n_local
-    achieved = alg_b / (per_launch_ms * 1e-3) / 1e9
+    hbm_gbs = alg_b / (per_launch_ms * 1e-3) / 1e9
+    flops = FLOPS_PER_STEP.get(dom, 0.0) * n_local if model.state_dim == 3 and not args.uniform else None
     plan = model.plan(n_local)
     launches = int(sum(v[1] for v in kern.values()))
-    roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": pk.get("hbm_gbs"), "unit": "GB/s",
-            "frac": achieved / pk.get("hbm_gbs"), "traffic": None,
-            "avg_launch_ms": per_launch_ms,
-            "share_of_step": dom_ms / ms_total,
-            "per_kernel_ms_per_step": {k: v[0] / args.steps for k, v in kern.items()},
-            "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if not pk.get("_fallback") else "fallback",
-            "path_alg_bytes_per_step": 41 + 16 * 9,
-            "path_hbm_frac": (41 + 16 * 9) * N / (ms_step * 1e-3) / 1e9 / pk.get("hbm_gbs")}
+    traffic, traffic_src = ncu_traffic(dom)
+    if flops:
+        achieved_tf = flops / (per_launch_ms * 1e-3) / 1e12
+        roof = {"bound": "alu", "kernel": dom, "achieved": achieved_tf, "peak": FP64_PEAK_TFLOPS,
+                "unit": "TFLOP/s", "frac": achieved_tf / FP64_PEAK_TFLOPS, "traffic": traffic,
+                "peak_source": "fp64 pipe: 148 SM x 64 FMA/clk x 2 x 1.965 GHz (DESIGN.md §6)",
+                "flops_per_step": FLOPS_PER_STEP.get(dom)}
+    else:
+        roof = {"bound": "hbm", "kernel": dom, "achieved": hbm_gbs, "peak": pk.get("hbm_gbs"), "unit": "GB/s",
+                "frac": hbm_gbs / pk.get("hbm_gbs"), "traffic": traffic}
+    roof.update({
+        "traffic_source": traffic_src,
+        "alg_bytes_per_launch": alg_b,
+        "hbm": {"achieved_gbs": hbm_gbs, "peak_gbs": pk.get("hbm_gbs"), "frac": hbm_gbs / pk.get("hbm_gbs"),
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if not pk.get("_fallback") else "fallback"},
+        "avg_launch_ms": per_launch_ms,
+        "share_of_step": dom_ms / ms_total,
+        "per_kernel_ms_per_step": {k: v[0] / args.steps for k, v in kern.items()},
+        "path_alg_bytes_per_step": 41 + 16 * 9,
+        "path_hbm_frac": (41 + 16 * 9) * N / (ms_step * 1e-3) / 1e9 / pk.get("hbm_gbs"),
+        "path_fp64_frac": (sum(FLOPS_PER_STEP.values()) * N / (ms_step * 1e-3) / 1e12 / FP64_PEAK_TFLOPS)
+        if flops else None})
     cpu = None
     if not args.no_cpu_baseline:
         cpu = cpu_baseline(w, args.cpu_sample)

@@ -12,7 +12,7 @@ import subprocess
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(_HERE)
-LIB_PATH = os.environ.get("PSSGP_LIB") or os.path.join(_HERE, "libpssgp.so")
+LIB_PATH = os.path.abspath(os.environ.get("PSSGP_LIB") or os.path.join(_HERE, "libpssgp.so"))
 CSRC = os.path.join(_HERE, "csrc")
 HEADER = os.path.join(ROOT, "include", "pssgp.h")
 

@@ -32,9 +32,13 @@
 
 namespace pssgp {
 
+#ifndef PSSGP_UNROLL
+#define PSSGP_UNROLL 1                  // step-loop unroll (lets ptxas interleave consecutive steps)
+#endif
 #ifndef PSSGP_MINB
 #define PSSGP_MINB 3                    // resident CTAs per SM the main kernels are register-capped for
 #endif
+constexpr int kUnroll = PSSGP_UNROLL;
 constexpr int kThreads = 128;           // threads per CTA (4 warps)
 constexpr int kWarps = kThreads / 32;
 constexpr int kWin = 16;                // staging window (steps) per chain
@@ -149,7 +153,8 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-__device__ __forceinline__ void issue_window(AsyncStage& s, int buf, const double* __restrict__ t,
+template <bool WITH_Y = true>
+__device__ __forceinline__ void issue_copies(double (*ts)[33], double (*ys)[33], const double* __restrict__ t,
                                              const double* __restrict__ y, int64_t wbase, int64_t K, int64_t n,
                                              int64_t j0, int lane) {
     const int col = lane & (kWinA - 1), rb = lane / kWinA;
@@ -158,11 +163,17 @@ __device__ __forceinline__ void issue_window(AsyncStage& s, int buf, const doubl
     for (int i = 0; i < 32 / (32 / kWinA); ++i) {
         const int r = rb + (32 / kWinA) * i;
         const int64_t idx = wbase + r * K + j;
-        const bool ok = (j < K) && (idx < n);
-        cp_async8(&s.t[buf][col][r], ok ? t + idx : t, ok ? 8 : 0);
-        cp_async8(&s.y[buf][col][r], ok ? y + idx : y, ok ? 8 : 0);
+        const bool ok = (j >= 0) && (j < K) && (idx < n);
+        cp_async8(&ts[col][r], ok ? t + idx : t, ok ? 8 : 0);
+        if (WITH_Y) cp_async8(&ys[col][r], ok ? y + idx : y, ok ? 8 : 0);
     }
     cp_async_commit();
+}
+
+__device__ __forceinline__ void issue_window(AsyncStage& s, int buf, const double* __restrict__ t,
+                                             const double* __restrict__ y, int64_t wbase, int64_t K, int64_t n,
+                                             int64_t j0, int lane) {
+    issue_copies<true>(s.t[buf], s.y[buf], t, y, wbase, K, n, j0, lane);
 }
 
 // ------------------------------------------------------------------ K1: fold chains
@@ -213,7 +224,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_reduce(const KP
         else cp_async_commit();
         cp_async_wait<1>();
         __syncwarp();
-#pragma unroll 1
+#pragma unroll kUnroll
         for (int jj = (w == 0) ? 1 : 0; jj < kWinA; ++jj) {
             const int64_t k = kb + j0 + jj;
             if (k < ke) {
@@ -482,7 +493,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
         else cp_async_commit();
         cp_async_wait<1>();
         __syncwarp();
-#pragma unroll 1
+#pragma unroll kUnroll
         for (int jj = (w == 0) ? 1 : 0; jj < kWinA; ++jj) {
             const int64_t k = kb + j0 + jj;
             if (k < ke) {
@@ -706,8 +717,9 @@ __device__ __forceinline__ void project(const ModelParams<D>& m, const double (&
 }
 
 struct StageOut {
-    double t[32][kWin + 1];   // staged t; each lane overwrites its own slot with the mean
-    double b[32][kWin + 1];   // variance
+    double t[2][kWinA][33];   // double-buffered t, transposed [step][chain]
+    double m[kWinA][33];      // mean of the current window, transposed
+    double v[kWinA][33];      // variance
 };
 
 template <int D, int MODE>
@@ -805,25 +817,20 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_smoother_apply(const K
         if (p.mean) p.mean[k] = mo;
         if (p.var) p.var[k] = vo;
     }
-    const int64_t jtop = ((p.K - 1) / kWin) * kWin;
-    for (int64_t j0 = jtop; j0 >= 0; j0 -= kWin) {
-        {
-            constexpr int RPI = 32 / kWin;
-            const int col = lane % kWin, rsub = lane / kWin;
-#pragma unroll 4
-            for (int r0 = 0; r0 < 32; r0 += RPI) {
-                const int r = r0 + rsub;
-                const int64_t j = j0 + col;
-                const int64_t idx = wbase + r * p.K + j;
-                so[wid].t[r][col] = ((j < p.K) && (idx < p.n)) ? __ldg(p.t + idx) : 0.0;
-            }
-            __syncwarp();
-        }
-#pragma unroll 1
-        for (int jj = kWin - 1; jj >= 0; --jj) {
+    const int64_t nwin = (p.K + kWinA - 1) / kWinA;
+    issue_copies<false>(so[wid].t[(nwin - 1) & 1], nullptr, p.t, nullptr, wbase, p.K, p.n, (nwin - 1) * kWinA, lane);
+    for (int64_t w = nwin - 1; w >= 0; --w) {
+        const int64_t j0 = w * kWinA;
+        const int buf = static_cast<int>(w & 1);
+        if (w > 0) issue_copies<false>(so[wid].t[buf ^ 1], nullptr, p.t, nullptr, wbase, p.K, p.n, j0 - kWinA, lane);
+        else cp_async_commit();
+        cp_async_wait<1>();
+        __syncwarp();
+#pragma unroll kUnroll
+        for (int jj = kWinA - 1; jj >= 0; --jj) {
             const int64_t k = kb + j0 + jj;
             if (k < ke - 1) {
-                const double tk = so[wid].t[lane][jj];
+                const double tk = so[wid].t[buf][jj][lane];
                 double x[D], P[ns(D)];
 #pragma unroll
                 for (int i = 0; i < D; ++i) x[i] = nx[i];
@@ -841,27 +848,26 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_smoother_apply(const K
                 tnext = tk;
                 double mo, vo;
                 project<D>(p.m, ms, Ps, mo, vo);
-                so[wid].t[lane][jj] = mo;
-                so[wid].b[lane][jj] = vo;
+                so[wid].m[jj][lane] = mo;
+                so[wid].v[jj][lane] = vo;
             }
         }
         __syncwarp();
         {
-            constexpr int RPI = 32 / kWin;
-            const int col = lane % kWin, rsub = lane / kWin;
-#pragma unroll 4
-            for (int r0 = 0; r0 < 32; r0 += RPI) {
-                const int r = r0 + rsub;
-                const int64_t j = j0 + col;
+            const int col = lane & (kWinA - 1), rb = lane / kWinA;
+            const int64_t j = j0 + col;
+#pragma unroll
+            for (int i = 0; i < 32 / (32 / kWinA); ++i) {
+                const int r = rb + (32 / kWinA) * i;
                 const int64_t idx = wbase + r * p.K + j;
                 const int64_t last = min(wbase + (r + 1) * p.K, p.n) - 1;   // row r's peeled step
                 if ((j < p.K) && (idx < last)) {
-                    if (p.mean) p.mean[idx] = so[wid].t[r][col];
-                    if (p.var) p.var[idx] = so[wid].b[r][col];
+                    if (p.mean) p.mean[idx] = so[wid].m[col][r];
+                    if (p.var) p.var[idx] = so[wid].v[col][r];
                 }
             }
-            __syncwarp();
         }
+        __syncwarp();
     }
 }
 

@@ -18,6 +18,10 @@
 #include <cstdint>
 #include <cmath>
 
+#ifndef PSSGP_ESTRIN
+#define PSSGP_ESTRIN 1
+#endif
+
 #if defined(__CUDACC__)
 #define PS_HD __host__ __device__ __forceinline__
 #define PS_CX __host__ __device__ constexpr
@@ -99,9 +103,21 @@ PS_HD double exp_neg(double z) {
     z = fmin(fmax(z, 0.0), 708.0);
     const double n = rint(z * 1.4426950408889634);
     const double r = fma(n, 1.9082149292705877e-10, fma(n, 0.6931471803691238, -z));
+#if PSSGP_ESTRIN
+    // Estrin scheme: dependency depth 5 instead of 13
+    const double r2 = r * r, r4 = r2 * r2, r8 = r4 * r4;
+    const double p01 = fma(C.expc[1], r, C.expc[0]), p23 = fma(C.expc[3], r, C.expc[2]);
+    const double p45 = fma(C.expc[5], r, C.expc[4]), p67 = fma(C.expc[7], r, C.expc[6]);
+    const double p89 = fma(C.expc[9], r, C.expc[8]), pab = fma(C.expc[11], r, C.expc[10]);
+    const double pcd = fma(C.expc[13], r, C.expc[12]);
+    const double q03 = fma(p23, r2, p01), q47 = fma(p67, r2, p45), q8b = fma(pab, r2, p89);
+    const double q07 = fma(q47, r4, q03), q8d = fma(pcd, r4, q8b);
+    const double pz = fma(q8d, r8, q07);
+#else
     double pz = C.expc[13];
 #pragma unroll
     for (int k = 12; k >= 0; --k) pz = fma(pz, r, C.expc[k]);
+#endif
     const long long ni = static_cast<long long>(n);
     return __longlong_as_double(__double_as_longlong(pz) - (ni << 52));
 #else
