@@ -100,6 +100,13 @@ PS_HD double rcp(double a) {
 PS_HD double exp_neg(double z) {
 #if defined(__CUDA_ARCH__)
     const MathConsts& C = mc();
+    if (z < 0.015625) {
+        // |z| < 2^-6: Taylor-9 of e^{-z} directly (truncation < 4e-22 relative), no range reduction
+        double pz = C.expc[9];
+#pragma unroll
+        for (int k = 8; k >= 0; --k) pz = fma(pz, -z, C.expc[k]);
+        return pz;
+    }
     z = fmin(fmax(z, 0.0), 708.0);
     const double n = rint(z * 1.4426950408889634);
     const double r = fma(n, 1.9082149292705877e-10, fma(n, 0.6931471803691238, -z));
@@ -733,6 +740,55 @@ PS_HD void kf_predict(const double (&x)[D], const double (&P)[ns(D)], const doub
         }
 }
 
+// ------------------------------------------------------------------ SPD solve
+// Solve S X = R for symmetric positive-definite packed S.  D <= 3: cofactor
+// (adjugate) inverse with ONE reciprocal (short dependency chain; relative
+// error ~ cond(S) eps, cond(P-) ~ 2e4 on the metric workload); larger D: LDL^T.
+template <int D, int NR>
+PS_HD bool spd_solve(const double (&S)[ns(D)], double (&R)[D * NR]) {
+    if constexpr (D == 1) {
+        const bool ok = S[0] > 0.0;
+        const double i0 = rcp(S[0]);
+#pragma unroll
+        for (int k = 0; k < NR; ++k) R[k] *= i0;
+        return ok;
+    } else if constexpr (D == 2) {
+        const double a = S[0], b = S[1], d = S[2];
+        const double det = fma(a, d, -b * b);
+        const bool ok = (a > 0.0) && (det > 0.0);
+        const double id = rcp(det);
+        const double i00 = d * id, i01 = -b * id, i11 = a * id;
+#pragma unroll
+        for (int k = 0; k < NR; ++k) {
+            const double r0 = R[k], r1 = R[NR + k];
+            R[k] = fma(i00, r0, i01 * r1);
+            R[NR + k] = fma(i01, r0, i11 * r1);
+        }
+        return ok;
+    } else if constexpr (D == 3) {
+        const double a = S[0], b = S[1], c = S[2], d = S[3], e = S[4], f = S[5];
+        const double A00 = fma(d, f, -e * e), A01 = fma(c, e, -b * f), A02 = fma(b, e, -c * d);
+        const double A11 = fma(a, f, -c * c), A12 = fma(b, c, -a * e), A22 = fma(a, d, -b * b);
+        const double det = fma(a, A00, fma(b, A01, c * A02));
+        const bool ok = (a > 0.0) && (A22 > 0.0) && (det > 0.0);
+        const double id = rcp(det);
+        const double i00 = A00 * id, i01 = A01 * id, i02 = A02 * id, i11 = A11 * id, i12 = A12 * id, i22 = A22 * id;
+#pragma unroll
+        for (int k = 0; k < NR; ++k) {
+            const double r0 = R[k], r1 = R[NR + k], r2 = R[2 * NR + k];
+            R[k] = fma(i00, r0, fma(i01, r1, i02 * r2));
+            R[NR + k] = fma(i01, r0, fma(i11, r1, i12 * r2));
+            R[2 * NR + k] = fma(i02, r0, fma(i12, r1, i22 * r2));
+        }
+        return ok;
+    } else {
+        double Lo[D * D], id[D];
+        const bool ok = ldlt<D>(S, Lo, id);
+        ldlt_solve<D, NR>(Lo, id, R);
+        return ok;
+    }
+}
+
 // ------------------------------------------------------------------ chain smoother aggregate
 // The ordered product (x)_s of the smoother elements of steps k0..k1 is the
 // Gaussian conditional p(x_k0 | x_{k1+1}, y_1:k1) (each element is
@@ -744,13 +800,12 @@ PS_HD void kf_predict(const double (&x)[D], const double (&P)[ns(D)], const doub
 template <int D>
 PS_HD bool chain_smoother_agg(const double (&x0)[D], const double (&P0)[ns(D)], const double (&Sm)[D * D],
                               const double (&xm)[D], const double (&Pm)[ns(D)], SAgg<D>& out) {
-    double Lo[D * D], id[D], Et[D * D];
-    const bool ok = ldlt<D>(Pm, Lo, id);
+    double Et[D * D];
 #pragma unroll
     for (int i = 0; i < D; ++i)
 #pragma unroll
         for (int j = 0; j < D; ++j) Et[i * D + j] = Sm[j * D + i];
-    ldlt_solve<D, D>(Lo, id, Et);  // Et = Pm^-1 Sm^T = E^T
+    const bool ok = spd_solve<D, D>(Pm, Et);  // Et = Pm^-1 Sm^T = E^T
 #pragma unroll
     for (int i = 0; i < D; ++i) {
         double s = x0[i];
@@ -781,11 +836,10 @@ template <int D>
 PS_HD bool rts_step(const double (&x)[D], const double (&P)[ns(D)], const double (&xm)[D],
                     const double (&Pm)[ns(D)], const double (&FP)[D * D], double (&ms)[D],
                     double (&Ps)[ns(D)]) {
-    double Lo[D * D], id[D], Gt[D * D];
-    const bool ok = ldlt<D>(Pm, Lo, id);
+    double Gt[D * D];
 #pragma unroll
     for (int i = 0; i < D * D; ++i) Gt[i] = FP[i];
-    ldlt_solve<D, D>(Lo, id, Gt);   // Gt = G^T, G[i][j] = Gt[j][i]
+    const bool ok = spd_solve<D, D>(Pm, Gt);   // Gt = Pm^-1 F P = G^T, G[i][j] = Gt[j][i]
     double dm[D], T[D * D];
 #pragma unroll
     for (int i = 0; i < D; ++i) dm[i] = ms[i] - xm[i];
@@ -797,13 +851,16 @@ PS_HD bool rts_step(const double (&x)[D], const double (&P)[ns(D)], const double
         ms[i] = s;
     }
     // T = G (Ps - Pm)
+    double dP[ns(D)];
+#pragma unroll
+    for (int i = 0; i < ns(D); ++i) dP[i] = Ps[i] - Pm[i];
 #pragma unroll
     for (int i = 0; i < D; ++i)
 #pragma unroll
         for (int j = 0; j < D; ++j) {
-            double s = 0.0;
+            double s = Gt[i] * dP[si(D, 0, j)];
 #pragma unroll
-            for (int k = 0; k < D; ++k) s = fma(Gt[k * D + i], Ps[si(D, k, j)] - Pm[si(D, k, j)], s);
+            for (int k = 1; k < D; ++k) s = fma(Gt[k * D + i], dP[si(D, k, j)], s);
             T[i * D + j] = s;
         }
 #pragma unroll
