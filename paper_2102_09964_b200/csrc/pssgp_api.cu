@@ -20,8 +20,8 @@ namespace {
 
 constexpr int kMaxD = 3;              // compiled state dimensions: 1, 2, 3
 constexpr int kSlots = 7;
-const char* kSlotNames[kSlots] = {"k_filter_reduce", "k_filter_carry", "k_filter_apply",
-                                  "k_smoother_carry", "k_smoother_apply", "k_nll_sum", "k_reduce_blocks"};
+const char* kSlotNames[kSlots] = {"k_filter_reduce", "(unused)", "k_filter_apply",
+                                  "(unused)", "k_smoother_apply", "k_nll_sum", "k_reduce_blocks"};
 enum Slot { S_K1 = 0, S_K2, S_K3, S_K4, S_K5, S_K6, S_RED };
 
 }  // namespace
@@ -237,31 +237,17 @@ pssgp_status phase_filter_reduce(pssgp_model* m, KParams<D>& p, cudaStream_t s) 
 
 template <int D>
 pssgp_status phase_filter_apply(pssgp_model* m, KParams<D>& p, cudaStream_t s) {
-    {
-        ProfScope ps(m, S_K2, s);
-        k_filter_carry<D><<<1, kCarryThreads, 0, s>>>(p);
-        LAUNCH_CHECK(m, "k_filter_carry");
-    }
-    {
-        ProfScope ps(m, S_K3, s);
-        LAUNCH_MODE(m, k_filter_apply, p.nb, kThreads, s, p);
-        LAUNCH_CHECK(m, "k_filter_apply");
-    }
+    ProfScope ps(m, S_K3, s);
+    LAUNCH_MODE(m, k_filter_apply, p.nb, kThreads, s, p);
+    LAUNCH_CHECK(m, "k_filter_apply");
     return PSSGP_OK;
 }
 
 template <int D>
 pssgp_status phase_smoother(pssgp_model* m, KParams<D>& p, cudaStream_t s) {
-    {
-        ProfScope ps(m, S_K4, s);
-        k_smoother_carry<D><<<1, kCarryThreads, 0, s>>>(p);
-        LAUNCH_CHECK(m, "k_smoother_carry");
-    }
-    {
-        ProfScope ps(m, S_K5, s);
-        LAUNCH_MODE(m, k_smoother_apply, p.nb, kThreads, s, p);
-        LAUNCH_CHECK(m, "k_smoother_apply");
-    }
+    ProfScope ps(m, S_K5, s);
+    LAUNCH_MODE(m, k_smoother_apply, p.nb, kThreads, s, p);
+    LAUNCH_CHECK(m, "k_smoother_apply");
     return PSSGP_OK;
 }
 
@@ -300,8 +286,12 @@ pssgp_status run_posterior(pssgp_model* m, int64_t N, const double* t, const dou
     p.store_state = smooth ? 1 : 0;
     if ((st = phase_filter_reduce<D>(m, p, s))) return st;
     if ((st = phase_filter_apply<D>(m, p, s))) return st;
-    if (nll && (st = nll_sum(m, p.nll_block, p.nb, nll, s))) return st;
-    if (smooth && (st = phase_smoother<D>(m, p, s))) return st;
+    if (smooth) {
+        p.nll_out = nll;                       // K5's CTA 0 sums the NLL partials
+        if ((st = phase_smoother<D>(m, p, s))) return st;
+    } else if (nll && (st = nll_sum(m, p.nll_block, p.nb, nll, s))) {
+        return st;
+    }
     return PSSGP_OK;
 }
 

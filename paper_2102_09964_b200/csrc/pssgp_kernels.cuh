@@ -7,14 +7,15 @@
 //   k_filter_reduce   (K1)  per chain: discretise + build + fold filter elements
 //                           (rank-one fold, PAPER.md:116-121 with J_k = u u^T / S)
 //                           -> chain aggregate; CTA tree-reduce -> block aggregate.
-//   k_filter_carry    (K2)  1 CTA: scan of block aggregates (general operator)
-//                           -> collapsed global prefix (xbar, P) entering each CTA.
+//   (K2)                    folded into K3's prologue: each CTA reduces the block
+//                           aggregates of all earlier CTAs -> collapsed prefix (xbar, P).
 //   k_filter_apply    (K3)  per CTA: scan of its chain aggregates, then per chain
 //                           the Kalman recursion from the carry (Prop. 1 proof order,
 //                           PAPER.md:326-330): writes (xbar_k, P_k), NLL partials,
 //                           and the chain's smoother aggregate (E, g, L) from the
 //                           cross-covariance Cov(x_k0, x_k1+1 | y_1:k1).
-//   k_smoother_carry  (K4)  1 CTA: reverse scan of block smoother aggregates.
+//   (K4)                    folded into K5's prologue (block smoother aggregates of
+//                           all later CTAs), which also sums the NLL partials.
 //   k_smoother_apply  (K5)  per CTA: reverse scan of chain smoother aggregates, then
 //                           per chain the RTS recursion (Prop. 2 proof order,
 //                           PAPER.md:431-435) -> mean = H m^s, var = H P^s H^T.
@@ -269,65 +270,76 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_reduce(const KP
     }
 }
 
-// ------------------------------------------------------------------ K2: block carries (1 CTA)
-template <int D>
-__global__ void __launch_bounds__(kCarryThreads, 1) k_filter_carry(const KParams<D> p) {
-    constexpr int NW = kCarryThreads / 32;
-    __shared__ FAgg<D> tot[NW];
-    __shared__ Gauss<D> wcar[NW + 1];
+// ------------------------------------------------------------------ CTA-wide ordered reductions
+// Ordered product blocks[lo] (x) ... (x) blocks[hi-1] of aggregates (AoS, NA
+// doubles each) by one CTA of kThreads: contiguous runs per thread, ordered
+// warp trees, then the warp totals in order.  Result valid in thread 0.
+// wred: shared scratch of kWarps aggregates.  Used by K3/K5 to build the
+// collapsed carry entering the CTA from the block aggregates of all earlier
+// (K3) / later (K5) CTAs: the block scan is thus spread over every SM instead
+// of a separate single-CTA kernel.
+template <typename Agg>
+__device__ __forceinline__ Agg cta_reduce_range(const double* __restrict__ blocks, int lo, int hi, Agg* wred) {
+    constexpr int NA = sizeof(Agg) / sizeof(double);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    Gauss<D> R;
-    set_zero(R);
-    if (threadIdx.x == 0) {
-        // sharded: fold the aggregates of ranks 0..rank-1 into the incoming carry
-        for (int g = 0; g < p.rank && p.in_filt; ++g) {
-            FAgg<D> ag;
-            load_aos(ag, p.in_filt + static_cast<int64_t>(g) * FN(D));
-            Gauss<D> r2;
-            apply_prefix(R, ag, r2);
-            R = r2;
+    const int cnt = max(hi - lo, 0);
+    const int per = (cnt + kThreads - 1) / kThreads;
+    const int b0 = lo + min(static_cast<int>(threadIdx.x) * per, cnt), b1 = min(b0 + per, lo + cnt);
+    Agg a;
+    set_identity(a);
+    for (int b = b0; b < b1; ++b) {
+        Agg e;
+        load_aos(e, blocks + static_cast<int64_t>(b) * NA);
+        if (b == b0) {
+            a = e;
+        } else {
+            Agg r;
+            combine(a, e, r);
+            a = r;
         }
-        wcar[NW] = R;
+    }
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        Agg o;
+        shfl_down_all(o, a, off);
+        if ((lane & (2 * off - 1)) == 0 && (threadIdx.x + off) * per < cnt) {
+            Agg r;
+            combine(a, o, r);
+            a = r;
+        }
+    }
+    if (lane == 0) wred[wid] = a;
+    __syncthreads();
+    Agg acc = wred[0];
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < kWarps && w * 32 * per < cnt; ++w) {
+            Agg r;
+            combine(acc, wred[w], r);
+            acc = r;
+        }
     }
     __syncthreads();
-    R = wcar[NW];
-    for (int base = 0; base < p.nb; base += kCarryThreads) {
-        const int b = base + threadIdx.x;
-        FAgg<D> a;
-        if (b < p.nb) load_aos(a, p.block_f + static_cast<int64_t>(b) * FN(D));
-        else set_identity(a);
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            FAgg<D> o;
-            shfl_up_all(o, a, off);
-            if (lane >= off) {
-                FAgg<D> r;
-                combine(o, a, r);
-                a = r;
-            }
-        }
-        if (lane == 31) tot[wid] = a;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            Gauss<D> acc = R;
-            for (int w = 0; w < NW; ++w) {
-                wcar[w] = acc;
-                Gauss<D> r2;
-                apply_prefix(acc, tot[w], r2);
-                acc = r2;
-            }
-            wcar[NW] = acc;
-        }
-        __syncthreads();
-        if (b < p.nb) {
-            Gauss<D> pre;
-            apply_prefix(wcar[wid], a, pre);             // global prefix through block b
-            if (b + 1 < p.nb) store_aos(pre, p.fcarry + static_cast<int64_t>(b + 1) * CN(D));
-        }
-        if (b == 0) store_aos(R, p.fcarry);
-        R = wcar[NW];
-        __syncthreads();
+    return acc;
+}
+
+// Deterministic fixed-order sum of parts[0, n) by one CTA; result valid in thread 0.
+__device__ __forceinline__ double cta_sum(const double* __restrict__ parts, int n, double* red) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int per = (n + kThreads - 1) / kThreads;
+    double s = 0.0;
+    for (int i = 0; i < per; ++i) {
+        const int b = threadIdx.x * per + i;
+        if (b < n) s += parts[b];
     }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
+    if (lane == 0) red[wid] = s;
+    __syncthreads();
+    double tsum = 0.0;
+    if (threadIdx.x == 0)
+        for (int w = 0; w < kWarps; ++w) tsum += red[w];
+    __syncthreads();
+    return tsum;
 }
 
 // observation-row terms of a predicted (xm, Pm): HP = Pm H^T, S = H Pm H^T + r, hx = H xm
@@ -383,8 +395,31 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
     const int64_t kb = c * p.K;
     const int64_t ke = min(kb + p.K, p.n);
 
-    // ---- carry into this chain: block carry (x) exclusive scan of chain aggregates
+    // ---- collapsed prefix entering this CTA: incoming carry of earlier ranks (sharded)
+    // (x) ordered product of the block aggregates of CTAs 0..blockIdx-1
     Gauss<D> cur;
+    {
+        const FAgg<D> before = cta_reduce_range<FAgg<D>>(p.block_f, 0, blockIdx.x, tot);
+        if (threadIdx.x == 0) {
+            Gauss<D> R;
+            set_zero(R);
+            for (int g = 0; g < p.rank && p.in_filt; ++g) {
+                FAgg<D> ag;
+                load_aos(ag, p.in_filt + static_cast<int64_t>(g) * FN(D));
+                Gauss<D> r2;
+                apply_prefix(R, ag, r2);
+                R = r2;
+            }
+            if (blockIdx.x > 0) {
+                Gauss<D> r2;
+                apply_prefix(R, before, r2);
+                R = r2;
+            }
+            wcar[0] = R;
+        }
+        __syncthreads();
+    }
+    // ---- carry into this chain: CTA carry (x) exclusive scan of chain aggregates
     {
         FAgg<D> a;
         load_soa(a, p.chain_f, nch, c);
@@ -403,8 +438,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
         shfl_up_all(ex, a, 1);
         __syncthreads();
         if (threadIdx.x == 0) {
-            Gauss<D> acc;
-            load_aos(acc, p.fcarry + static_cast<int64_t>(blockIdx.x) * CN(D));
+            Gauss<D> acc = wcar[0];
             for (int w = 0; w < kWarps; ++w) {
                 wcar[w] = acc;
                 Gauss<D> r2;
@@ -634,67 +668,6 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
     }
 }
 
-// ------------------------------------------------------------------ K4: block smoother carries (1 CTA)
-template <int D>
-__global__ void __launch_bounds__(kCarryThreads, 1) k_smoother_carry(const KParams<D> p) {
-    constexpr int NW = kCarryThreads / 32;
-    __shared__ SAgg<D> tot[NW];
-    __shared__ Gauss<D> wcar[NW + 1];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    Gauss<D> R;
-    set_zero(R);
-    if (threadIdx.x == 0) {
-        for (int g = p.world - 1; g > p.rank && p.in_smooth; --g) {
-            SAgg<D> ag;
-            load_aos(ag, p.in_smooth + static_cast<int64_t>(g) * SN(D));
-            Gauss<D> r2;
-            apply_suffix(ag, R, r2);
-            R = r2;
-        }
-        wcar[0] = R;
-    }
-    __syncthreads();
-    R = wcar[0];
-    const int nchunk = (p.nb + kCarryThreads - 1) / kCarryThreads;
-    for (int ci = nchunk - 1; ci >= 0; --ci) {
-        const int b = ci * kCarryThreads + threadIdx.x;
-        SAgg<D> a;
-        if (b < p.nb) load_aos(a, p.block_s + static_cast<int64_t>(b) * SN(D));
-        else set_identity(a);
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            SAgg<D> o;
-            shfl_down_all(o, a, off);
-            if (lane + off < 32) {
-                SAgg<D> r;
-                combine(a, o, r);
-                a = r;
-            }
-        }
-        if (lane == 0) tot[wid] = a;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            Gauss<D> acc = R;
-            wcar[NW] = acc;
-            for (int w = NW - 1; w >= 0; --w) {
-                Gauss<D> r2;
-                apply_suffix(tot[w], acc, r2);
-                acc = r2;
-                wcar[w] = acc;
-            }
-        }
-        __syncthreads();
-        if (b < p.nb) {
-            Gauss<D> suf;
-            apply_suffix(a, wcar[wid + 1], suf);        // smoothed state at the first step of block b
-            if (b >= 1) store_aos(suf, p.scarry + static_cast<int64_t>(b - 1) * CN(D));
-            if (b == p.nb - 1) store_aos(R, p.scarry + static_cast<int64_t>(b) * CN(D));
-        }
-        R = wcar[0];
-        __syncthreads();
-    }
-}
-
 // ------------------------------------------------------------------ K5: RTS rescan
 // f-space projection: mean = H m^s, var = H P^s H^T
 template <int D>
@@ -735,8 +708,35 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_smoother_apply(const K
     const int64_t kb = c * p.K;
     const int64_t ke = min(kb + p.K, p.n);
 
-    // ---- carry: exclusive reverse scan of chain smoother aggregates (x) block carry
+    // ---- NLL: fixed-order sum of the per-CTA partials written by K3 (CTA 0 only)
+    if (blockIdx.x == 0 && p.nll_out) {
+        const double v = cta_sum(p.nll_block, p.nb, reinterpret_cast<double*>(tot));
+        if (threadIdx.x == 0) *p.nll_out = v;
+    }
+    // ---- collapsed suffix after this CTA: ordered product of the block aggregates of
+    // CTAs blockIdx+1..nb-1 (x) incoming carry of later ranks (sharded)
     double ms[D], Ps[ns(D)];
+    {
+        const SAgg<D> after = cta_reduce_range<SAgg<D>>(p.block_s, blockIdx.x + 1, p.nb, tot);
+        if (threadIdx.x == 0) {
+            Gauss<D> R;
+            set_zero(R);
+            for (int g = p.world - 1; g > p.rank && p.in_smooth; --g) {
+                SAgg<D> ag;
+                load_aos(ag, p.in_smooth + static_cast<int64_t>(g) * SN(D));
+                Gauss<D> r2;
+                apply_suffix(ag, R, r2);
+                R = r2;
+            }
+            if (blockIdx.x + 1 < p.nb) {
+                Gauss<D> r2;
+                apply_suffix(after, R, r2);
+                R = r2;
+            }
+            wcar[kWarps] = R;
+        }
+        __syncthreads();
+    }
     {
         SAgg<D> a;
         load_soa(a, p.chain_s, nch, c);
@@ -755,9 +755,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_smoother_apply(const K
         shfl_down_all(ex, a, 1);
         __syncthreads();
         if (threadIdx.x == 0) {
-            Gauss<D> acc;
-            load_aos(acc, p.scarry + static_cast<int64_t>(blockIdx.x) * CN(D));
-            wcar[kWarps] = acc;
+            Gauss<D> acc = wcar[kWarps];
             for (int w = kWarps - 1; w >= 0; --w) {
                 wcar[w + 1] = acc;
                 Gauss<D> r2;
