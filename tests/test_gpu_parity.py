@@ -175,3 +175,19 @@ def test_virtual_sharding(cuda_device, world):
     o = oracle.posterior(w)
     em, ev, en = errors((mean, var, nll), o)
     assert em <= MEAN_TOL and ev <= VAR_TOL and en <= NLL_TOL
+
+
+def test_misaligned_mask_pointer(cuda_device):
+    """A mask view starting at an odd byte address takes the register-prefetch path."""
+    w = synth.random_problem(14, 9001, kind="matern52", p_missing=0.3)
+    o = oracle.posterior(w)
+    m = P.Model(w.components, w.noise_var)
+    t, y, _ = to_dev(w)
+    big = torch.zeros(w.N + 1, dtype=torch.uint8, device="cuda:0")
+    big[1:] = torch.from_numpy(w.mask).cuda()
+    mk = big[1:]
+    assert mk.data_ptr() % 4 != 0
+    mean, var, nll = m.posterior(t, y, mk)
+    m.check()
+    em, ev, en = errors((mean.cpu().numpy(), var.cpu().numpy(), float(nll.cpu()[0])), o)
+    assert em <= MEAN_TOL and ev <= VAR_TOL and en <= NLL_TOL
