@@ -81,9 +81,11 @@ typedef struct {
 typedef struct {
     int balance;              /* 1 (default): Osborne balancing, Eq. (9) */
     int device;               /* CUDA device ordinal used for workspace (default: current) */
-    double uniform_dt;        /* > 0: steps with t[k]-t[k-1] == uniform_dt exactly use F, Q
-                                 precomputed on the host (fp64 result of an extended-precision
-                                 Van Loan); 0 = none.  Required (> 0) for non-Matern models. */
+    double uniform_dt;        /* > 0: steps with |t[k]-t[k-1] - uniform_dt| <= 1e-12 uniform_dt
+                                 (time-stamp rounding) use F, Q precomputed on the host (fp64
+                                 result of an extended-precision Van Loan); 0 = none.  Required
+                                 (> 0) for non-Matern models; their other steps (except dt = 0)
+                                 fail with PSSGP_E_UNSUPPORTED. */
     int64_t chain_len;        /* steps per thread chain (0 = automatic)                   */
     int blocks_per_sm;        /* CTAs per SM for the one-wave grid (0 = automatic)        */
 } pssgp_options;

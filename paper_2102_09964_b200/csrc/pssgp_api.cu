@@ -12,16 +12,19 @@
 #include "../../include/pssgp.h"
 #include "host_model.hpp"
 #include "pssgp_kernels.cuh"
+#include "pssgp_wide.cuh"
 
 using namespace pssgp;
 namespace ph = pssgp_host;
 
 namespace {
 
-constexpr int kMaxD = 3;              // compiled state dimensions: 1, 2, 3
+constexpr int kMaxD = 3;              // thread-per-chain path: d = 1, 2, 3
+// warp-per-chain path (pssgp_wide.cuh), uniform-dt models: these d are compiled
+#define PSSGP_WIDE_DIMS(X) X(4) X(5) X(6) X(8) X(10) X(12) X(14) X(16) X(18) X(20)
 constexpr int kSlots = 7;
-const char* kSlotNames[kSlots] = {"k_filter_reduce", "(unused)", "k_filter_apply",
-                                  "(unused)", "k_smoother_apply", "k_nll_sum", "k_reduce_blocks"};
+const char* kSlotNames[kSlots] = {"k_filter_reduce", "k_filter_scan", "k_filter_apply",
+                                  "k_smoother_scan", "k_smoother_apply", "k_nll_sum", "k_reduce_blocks"};
 enum Slot { S_K1 = 0, S_K2, S_K3, S_K4, S_K5, S_K6, S_RED };
 
 }  // namespace
@@ -44,6 +47,8 @@ struct pssgp_model {
     size_t ws_bytes = 0;
     unsigned long long* d_err = nullptr;  // separate small allocation
     double* d_scalar = nullptr;           // scratch nll scalar
+    double* d_model = nullptr;            // wide path: F, Q, Pinf, H, r, udt (device copy)
+    int wocc = 0;                         // wide path: resident CTAs / SM
     char* io = nullptr;                   // e2e device buffers
     size_t io_bytes = 0;
     cudaStream_t last_stream = nullptr;
@@ -317,6 +322,278 @@ pssgp_status debug_disc(const pssgp_model* m, double dt, double* F, double* Q) {
 
 }  // namespace
 
+
+// ========================================================================== wide path (d >= 4)
+namespace {
+
+bool wide_supported(int d) {
+    switch (d) {
+#define X(DD) case DD: return true;
+        PSSGP_WIDE_DIMS(X)
+#undef X
+        default: return false;
+    }
+}
+
+template <int D>
+void wide_set_smem_attrs() {
+    using namespace pssgp::wide;
+    static bool done = false;
+    if (done) return;
+    cudaFuncSetAttribute(kw_filter_fold<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K1Smem<D>));
+    cudaFuncSetAttribute(kw_filter_apply<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K3Smem<D>));
+    cudaFuncSetAttribute(kw_smoother_apply<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K5Smem<D>));
+    cudaFuncSetAttribute(kw_scan_filter<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(ScanSmemF<D>));
+    cudaFuncSetAttribute(kw_scan_smoother<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(ScanSmemS<D>));
+    done = true;
+}
+
+struct WPlan {
+    int64_t K = 0;
+    int nch = 0, nb = 0;
+};
+
+template <int D>
+WPlan make_wplan(pssgp_model* m, int64_t n) {
+    using namespace pssgp::wide;
+    wide_set_smem_attrs<D>();
+    if (m->wocc == 0) {
+        int a = 0, b = 0, c = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, kw_filter_fold<D>, 32 * kWWarps, sizeof(K1Smem<D>));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kw_filter_apply<D>, 32 * kWWarps, sizeof(K3Smem<D>));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, kw_smoother_apply<D>, 32 * kWWarps, sizeof(K5Smem<D>));
+        m->wocc = std::max(1, std::min(a, std::min(b, c)));
+    }
+    const int64_t target = static_cast<int64_t>(m->sm_count) * m->wocc * kWWarps;
+    WPlan pl;
+    pl.K = m->forced_K > 0 ? m->forced_K : std::max<int64_t>(16, (n + target - 1) / target);
+    pl.nch = static_cast<int>(std::max<int64_t>(1, (n + pl.K - 1) / pl.K));
+    pl.nb = (pl.nch + kWWarps - 1) / kWWarps;
+    return pl;
+}
+
+template <int D>
+pssgp_status wide_setup(pssgp_model* m, const WPlan& pl, pssgp::wide::WParams& p) {
+    using namespace pssgp::wide;
+    const size_t nch = static_cast<size_t>(pl.nch);
+    const size_t need = (2 * nch * FNW(D) + nch * pl.K * CNW(D) + 2 * nch * SNW(D) + nch + 64) * sizeof(double);
+    if (need > m->ws_bytes) {
+        if (m->ws) cudaFree(m->ws);
+        m->ws = nullptr;
+        m->ws_bytes = 0;
+        if (cudaMalloc(&m->ws, need) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(m, PSSGP_E_NOMEM, "cudaMalloc(workspace) failed");
+        }
+        m->ws_bytes = need;
+    }
+    if (!m->d_model) {
+        std::vector<double> h(MODW(D), 0.0);
+        for (int i = 0; i < D * D; ++i) {
+            h[i] = m->udt > 0.0 ? m->Fu[i] : 0.0;
+            h[D * D + i] = m->udt > 0.0 ? m->Qu[i] : 0.0;
+            h[2 * D * D + i] = static_cast<double>(m->ssm.Pinf[i]);
+        }
+        for (int i = 0; i < D; ++i) h[3 * D * D + i] = static_cast<double>(m->ssm.H[i]);
+        h[3 * D * D + D] = m->r;
+        h[3 * D * D + D + 1] = m->udt > 0.0 ? m->udt : -1.0;
+        if (cudaMalloc(&m->d_model, h.size() * sizeof(double)) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(m, PSSGP_E_NOMEM, "cudaMalloc(model)");
+        }
+        cudaMemcpy(m->d_model, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice);
+    }
+    std::memset(&p, 0, sizeof(p));
+    double* w = reinterpret_cast<double*>(m->ws);
+    p.fagg = w; w += nch * FNW(D);
+    p.fbuf = w; w += nch * FNW(D);
+    p.xp = w; w += nch * pl.K * CNW(D);
+    p.sagg = w; w += nch * SNW(D);
+    p.sbuf = w; w += nch * SNW(D);
+    p.nll_chain = w;
+    p.K = pl.K;
+    p.nch = pl.nch;
+    p.model = m->d_model;
+    p.err = m->d_err;
+    p.rank = 0;
+    p.world = 1;
+    p.store_state = 1;
+    return PSSGP_OK;
+}
+
+// Kogge-Stone levels with ping-pong buffers; returns the buffer holding the inclusive scan
+template <int D>
+double* wide_scan_f(pssgp_model* m, pssgp::wide::WParams& p, cudaStream_t s, pssgp_status& st) {
+    using namespace pssgp::wide;
+    ProfScope ps(m, S_K2, s);
+    double* in = p.fagg;
+    double* out = p.fbuf;
+    for (int off = 1; off < p.nch; off <<= 1) {
+        kw_scan_filter<D><<<p.nch, 32, sizeof(ScanSmemF<D>), s>>>(in, out, p.nch, off, p.err);
+        std::swap(in, out);
+    }
+    cudaError_t e = cudaGetLastError();
+    st = (e == cudaSuccess) ? PSSGP_OK : cuda_fail(m, e, "kw_scan_filter");
+    return in;
+}
+
+template <int D>
+double* wide_scan_s(pssgp_model* m, pssgp::wide::WParams& p, cudaStream_t s, pssgp_status& st) {
+    using namespace pssgp::wide;
+    ProfScope ps(m, S_K4, s);
+    double* in = p.sagg;
+    double* out = p.sbuf;
+    for (int off = 1; off < p.nch; off <<= 1) {
+        kw_scan_smoother<D><<<p.nch, 32, sizeof(ScanSmemS<D>), s>>>(in, out, p.nch, off);
+        std::swap(in, out);
+    }
+    cudaError_t e = cudaGetLastError();
+    st = (e == cudaSuccess) ? PSSGP_OK : cuda_fail(m, e, "kw_scan_smoother");
+    return in;
+}
+
+template <int D>
+pssgp_status wide_fold(pssgp_model* m, pssgp::wide::WParams& p, int nb, cudaStream_t s) {
+    using namespace pssgp::wide;
+    ProfScope ps(m, S_K1, s);
+    kw_filter_fold<D><<<nb, 32 * kWWarps, sizeof(K1Smem<D>), s>>>(p);
+    LAUNCH_CHECK(m, "kw_filter_fold");
+    return PSSGP_OK;
+}
+
+template <int D>
+pssgp_status wide_fapply(pssgp_model* m, pssgp::wide::WParams& p, int nb, cudaStream_t s) {
+    using namespace pssgp::wide;
+    ProfScope ps(m, S_K3, s);
+    kw_filter_apply<D><<<nb, 32 * kWWarps, sizeof(K3Smem<D>), s>>>(p);
+    LAUNCH_CHECK(m, "kw_filter_apply");
+    return PSSGP_OK;
+}
+
+template <int D>
+pssgp_status wide_sapply(pssgp_model* m, pssgp::wide::WParams& p, int nb, cudaStream_t s) {
+    using namespace pssgp::wide;
+    ProfScope ps(m, S_K5, s);
+    kw_smoother_apply<D><<<nb, 32 * kWWarps, sizeof(K5Smem<D>), s>>>(p);
+    LAUNCH_CHECK(m, "kw_smoother_apply");
+    return PSSGP_OK;
+}
+
+template <int D>
+pssgp_status wide_posterior(pssgp_model* m, int64_t N, const double* t, const double* y, const uint8_t* mask,
+                            double* mean, double* var, double* nll, cudaStream_t s, bool smooth) {
+    if (N == 0) {
+        if (nll && cudaMemsetAsync(nll, 0, sizeof(double), s) != cudaSuccess) return fail(m, PSSGP_E_CUDA, "memset");
+        return PSSGP_OK;
+    }
+    const WPlan pl = make_wplan<D>(m, N);
+    pssgp::wide::WParams p;
+    pssgp_status st = wide_setup<D>(m, pl, p);
+    if (st) return st;
+    p.t = t; p.y = y; p.mask = mask;
+    p.n = N; p.k0 = 0; p.nglob = N;
+    p.mean = mean; p.var = var;
+    p.store_state = smooth ? 1 : 0;
+    if ((st = wide_fold<D>(m, p, pl.nb, s))) return st;
+    p.fagg = wide_scan_f<D>(m, p, s, st);
+    if (st) return st;
+    if ((st = wide_fapply<D>(m, p, pl.nb, s))) return st;
+    if (smooth) {
+        p.sagg = wide_scan_s<D>(m, p, s, st);
+        if (st) return st;
+        p.nll_out = nll;
+        return wide_sapply<D>(m, p, pl.nb, s);
+    }
+    if (nll) return nll_sum(m, p.nll_chain, p.nch, nll, s);
+    return PSSGP_OK;
+}
+
+pssgp_status wide_posterior_dispatch(pssgp_model* m, int64_t N, const double* t, const double* y,
+                                     const uint8_t* mask, double* mean, double* var, double* nll, cudaStream_t s,
+                                     bool smooth) {
+    switch (m->d) {
+#define X(DD) case DD: return wide_posterior<DD>(m, N, t, y, mask, mean, var, nll, s, smooth);
+        PSSGP_WIDE_DIMS(X)
+#undef X
+        default: return fail(m, PSSGP_E_UNSUPPORTED, "state dimension not compiled");
+    }
+}
+
+// ---- sharded wide phases
+template <int D>
+pssgp_status wide_shard_reduce(pssgp_model* m, int64_t k0, int64_t n, int64_t Ng, const double* t, const double* y,
+                               const uint8_t* mask, void* out, cudaStream_t s) {
+    const WPlan pl = make_wplan<D>(m, n);
+    pssgp::wide::WParams p;
+    pssgp_status st = wide_setup<D>(m, pl, p);
+    if (st) return st;
+    p.t = t; p.y = y; p.mask = mask; p.n = n; p.k0 = k0; p.nglob = Ng;
+    if ((st = wide_fold<D>(m, p, pl.nb, s))) return st;
+    double* inc = wide_scan_f<D>(m, p, s, st);
+    if (st) return st;
+    cudaMemcpyAsync(out, inc + static_cast<int64_t>(pl.nch - 1) * pssgp::wide::FNW(D),
+                    pssgp::wide::FNW(D) * sizeof(double), cudaMemcpyDeviceToDevice, s);
+    return PSSGP_OK;
+}
+
+int ks_levels(int nch) {
+    int l = 0;
+    for (int off = 1; off < nch; off <<= 1) ++l;
+    return l;
+}
+
+template <int D>
+pssgp_status wide_shard_fapply(pssgp_model* m, int64_t k0, int64_t n, int64_t Ng, const double* t, const double* y,
+                               const uint8_t* mask, const void* all, int rank, int world, void* sout, double* nllp,
+                               cudaStream_t s) {
+    const WPlan pl = make_wplan<D>(m, n);
+    pssgp::wide::WParams p;
+    pssgp_status st = wide_setup<D>(m, pl, p);
+    if (st) return st;
+    p.t = t; p.y = y; p.mask = mask; p.n = n; p.k0 = k0; p.nglob = Ng;
+    p.in_filt = static_cast<const double*>(all);
+    p.rank = rank; p.world = world;
+    if (ks_levels(pl.nch) & 1) p.fagg = p.fbuf;          // where the reduce phase left the scan
+    if ((st = wide_fapply<D>(m, p, pl.nb, s))) return st;
+    if (nllp && (st = nll_sum(m, p.nll_chain, p.nch, nllp, s))) return st;
+    double* inc = wide_scan_s<D>(m, p, s, st);
+    if (st) return st;
+    cudaMemcpyAsync(sout, inc, pssgp::wide::SNW(D) * sizeof(double), cudaMemcpyDeviceToDevice, s);
+    return PSSGP_OK;
+}
+
+template <int D>
+pssgp_status wide_shard_sapply(pssgp_model* m, int64_t k0, int64_t n, int64_t Ng, const double* t, const void* all,
+                               int rank, int world, double* mean, double* var, cudaStream_t s) {
+    const WPlan pl = make_wplan<D>(m, n);
+    pssgp::wide::WParams p;
+    pssgp_status st = wide_setup<D>(m, pl, p);
+    if (st) return st;
+    p.t = t; p.n = n; p.k0 = k0; p.nglob = Ng;
+    p.in_smooth = static_cast<const double*>(all);
+    p.rank = rank; p.world = world;
+    p.mean = mean; p.var = var;
+    if (ks_levels(pl.nch) & 1) p.sagg = p.sbuf;
+    return wide_sapply<D>(m, p, pl.nb, s);
+}
+
+#define DISPATCH_WIDE(m, FN, ...)                                                  \
+    switch ((m)->d) {                                                              \
+        case 4: return FN<4>(__VA_ARGS__);                                         \
+        case 5: return FN<5>(__VA_ARGS__);                                         \
+        case 6: return FN<6>(__VA_ARGS__);                                         \
+        case 8: return FN<8>(__VA_ARGS__);                                         \
+        case 10: return FN<10>(__VA_ARGS__);                                       \
+        case 12: return FN<12>(__VA_ARGS__);                                       \
+        case 14: return FN<14>(__VA_ARGS__);                                       \
+        case 16: return FN<16>(__VA_ARGS__);                                       \
+        case 18: return FN<18>(__VA_ARGS__);                                       \
+        case 20: return FN<20>(__VA_ARGS__);                                       \
+        default: return fail((m), PSSGP_E_UNSUPPORTED, "state dimension not compiled"); \
+    }
+
+}  // namespace
+
 // ========================================================================== C ABI
 extern "C" {
 
@@ -367,7 +644,7 @@ pssgp_status pssgp_create(const pssgp_component* comps, int n_comps, double nois
     }
     m->ssm = parts.size() == 1 ? parts[0] : ph::block_sum(parts);
     m->d = m->ssm.d;
-    if (m->d > kMaxD) {
+    if (m->d > kMaxD && !wide_supported(m->d)) {
         delete m;
         return PSSGP_E_UNSUPPORTED;
     }
@@ -389,6 +666,7 @@ void pssgp_destroy(pssgp_model* m) {
     if (m->ws) cudaFree(m->ws);
     if (m->io) cudaFree(m->io);
     if (m->d_err) cudaFree(m->d_err);
+    if (m->d_model) cudaFree(m->d_model);
     for (int s = 0; s < kSlots; ++s)
         for (auto& pr : m->ev[s]) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
     for (auto e : m->ev_pool) cudaEventDestroy(e);
@@ -405,6 +683,7 @@ pssgp_status pssgp_posterior(pssgp_model* m, int64_t N, const double* t, const d
     auto s = static_cast<cudaStream_t>(stream);
     m->last_stream = s;
     const bool smooth = (mean != nullptr) || (var != nullptr);
+    if (m->d > kMaxD) return wide_posterior_dispatch(m, N, t, y, mask, mean, var, nll, s, smooth);
     DISPATCH_D(m, run_posterior<D_>(m, N, t, y, mask, mean, var, nll, s, smooth));
 }
 
@@ -416,6 +695,7 @@ pssgp_status pssgp_nll(pssgp_model* m, int64_t N, const double* t, const double*
     if ((st = ensure_device(m))) return st;
     auto s = static_cast<cudaStream_t>(stream);
     m->last_stream = s;
+    if (m->d > kMaxD) return wide_posterior_dispatch(m, N, t, y, mask, nullptr, nullptr, nll, s, false);
     DISPATCH_D(m, run_posterior<D_>(m, N, t, y, mask, nullptr, nullptr, nll, s, false));
 }
 
@@ -499,6 +779,15 @@ pssgp_status pssgp_get_ssm(const pssgp_model* m, double* G, double* W, double* H
 pssgp_status pssgp_debug_discretize(const pssgp_model* m, double dt, double* F, double* Q) {
     if (!m || !F || !Q) return PSSGP_E_ARG;
     pssgp_model* mm = const_cast<pssgp_model*>(m);
+    if (m->d > kMaxD) {   // mirrors wide::wdisc_kind
+        const int d = m->d;
+        const bool tab = (m->udt > 0.0 && std::fabs(dt - m->udt) <= 1e-12 * m->udt), zero = (dt == 0.0);
+        for (int i = 0; i < d * d; ++i) {
+            F[i] = tab ? m->Fu[i] : ((zero && i % (d + 1) == 0) ? 1.0 : 0.0);
+            Q[i] = tab ? m->Qu[i] : 0.0;
+        }
+        return (tab || zero) ? PSSGP_OK : PSSGP_E_UNSUPPORTED;
+    }
     DISPATCH_D(mm, debug_disc<D_>(m, dt, F, Q));
 }
 
@@ -512,7 +801,20 @@ pssgp_status pssgp_plan(pssgp_model* m, int64_t N, int64_t* chain_len, int64_t* 
         case 1: pl = make_plan<1>(m, N); break;
         case 2: pl = make_plan<2>(m, N); break;
         case 3: pl = make_plan<3>(m, N); break;
-        default: return PSSGP_E_UNSUPPORTED;
+        default: {
+            WPlan wp;
+            switch (m->d) {
+#define X(DD) case DD: wp = make_wplan<DD>(m, N); break;
+                PSSGP_WIDE_DIMS(X)
+#undef X
+                default: return PSSGP_E_UNSUPPORTED;
+            }
+            if (chain_len) *chain_len = wp.K;
+            if (n_chains) *n_chains = wp.nch;
+            if (n_blocks) *n_blocks = wp.nb;
+            if (threads_per_block) *threads_per_block = 32 * pssgp::wide::kWWarps;
+            return PSSGP_OK;
+        }
     }
     if (chain_len) *chain_len = pl.K;
     if (n_chains) *n_chains = pl.nch;
@@ -553,8 +855,12 @@ const char* pssgp_profile_name(int slot) { return (slot >= 0 && slot < kSlots) ?
 size_t pssgp_aggregate_bytes(const pssgp_model* m, int which) {
     if (!m) return 0;
     const int d = m->d;
-    const int fn = d * d + 2 * d + d * (d + 1);
-    const int sn = d * d + d + d * (d + 1) / 2;
+    int fn = d * d + 2 * d + d * (d + 1);
+    int sn = d * d + d + d * (d + 1) / 2;
+    if (d > kMaxD) {                 // wide path stores full matrices
+        fn = 3 * d * d + 2 * d;
+        sn = 2 * d * d + d;
+    }
     return static_cast<size_t>(which == 0 ? fn : sn) * sizeof(double);
 }
 
@@ -637,6 +943,7 @@ pssgp_status pssgp_shard_filter_reduce(pssgp_model* m, int64_t k0, int64_t n, in
     auto s = static_cast<cudaStream_t>(stream);
     m->last_stream = s;
     m->sh_k0 = k0; m->sh_n = n; m->sh_N = N_global;
+    if (m->d > kMaxD) { DISPATCH_WIDE(m, wide_shard_reduce, m, k0, n, N_global, t, y, mask, filt_agg_out, s); }
     DISPATCH_D(m, shard_reduce<D_>(m, k0, n, N_global, t, y, mask, filt_agg_out, s));
 }
 
@@ -651,6 +958,10 @@ pssgp_status pssgp_shard_filter_apply(pssgp_model* m, int64_t k0, int64_t n, int
         return fail(m, PSSGP_E_ARG, "shard phases called with different chunk arguments");
     auto s = static_cast<cudaStream_t>(stream);
     m->last_stream = s;
+    if (m->d > kMaxD) {
+        DISPATCH_WIDE(m, wide_shard_fapply, m, k0, n, N_global, t, y, mask, all_filt_aggs, rank, world,
+                      smooth_agg_out, nll_partial, s);
+    }
     DISPATCH_D(m, shard_fapply<D_>(m, k0, n, N_global, t, y, mask, all_filt_aggs, rank, world, smooth_agg_out,
                                    nll_partial, s));
 }
@@ -665,6 +976,9 @@ pssgp_status pssgp_shard_smoother_apply(pssgp_model* m, int64_t k0, int64_t n, i
         return fail(m, PSSGP_E_ARG, "shard phases called with different chunk arguments");
     auto s = static_cast<cudaStream_t>(stream);
     m->last_stream = s;
+    if (m->d > kMaxD) {
+        DISPATCH_WIDE(m, wide_shard_sapply, m, k0, n, N_global, t, all_smooth_aggs, rank, world, mean, var, s);
+    }
     DISPATCH_D(m, shard_sapply<D_>(m, k0, n, N_global, t, all_smooth_aggs, rank, world, mean, var, s));
 }
 

@@ -399,7 +399,7 @@ PS_HD int disc(const ModelParams<D>& p, double dt, double (&F)[D * D], double (&
         if constexpr (D <= 3) matern_closed<D>(p.lam, p.s2, dt, F, Q);
         return 0;
     } else {
-        if (dt == p.udt) {
+        if (fabs(dt - p.udt) <= 1e-12 * p.udt) {   // uniform step up to time-stamp rounding
 #pragma unroll
             for (int i = 0; i < D * D; ++i) F[i] = p.Fu[i];
 #pragma unroll

@@ -1,0 +1,980 @@
+// pssgp_wide.cuh — warp-per-chain kernels for larger state dimensions (4 <= D <= 32).
+//
+// Thread-per-chain (pssgp_kernels.cuh) keeps a whole filter aggregate in registers,
+// which stops working past d = 3 (d = 6: 90 doubles, d = 16: 560).  Here one WARP
+// owns one chain; every matrix of the chain lives in shared memory (full D x D,
+// row stride D+1) and the 32 lanes split each matrix operation over its output
+// elements.  Same three-pass structure as the d <= 3 path (PAPER.md:116-123 fold,
+// 326-330 Kalman rescan, 431-435 RTS rescan), but the carries come from
+// Kogge-Stone scans over the chain aggregates in which each general operator
+// (x)_f / (x)_s is evaluated cooperatively by one warp (Gauss-Jordan with
+// partial pivoting for (I + C_i J_j)^-1).
+//
+// Discretisation: uniform-dt models (F, Q precomputed on the host, copied once to
+// device memory); dt == 0 -> (I, 0); any other dt -> PSSGP_E_UNSUPPORTED.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "pssgp_kernels.cuh"
+
+namespace pssgp {
+namespace wide {
+
+constexpr int kWWarps = 4;                       // chains (warps) per CTA in the chain kernels
+
+PS_CX int LD(int D) { return D + 1; }            // padded row stride of a shared matrix
+PS_CX int FNW(int D) { return 3 * D * D + 2 * D; } // full filter aggregate: A, b, C, eta, J
+PS_CX int SNW(int D) { return 2 * D * D + D; }     // full smoother aggregate: E, g, L
+PS_CX int CNW(int D) { return D + D * (D + 1) / 2; } // filtered (x, P packed upper)
+PS_CX int MODW(int D) { return 3 * D * D + D + 2; }  // model: F, Q, Pinf, H, r, udt
+
+struct WParams {
+    const double* t;
+    const double* y;
+    const uint8_t* mask;
+    int64_t n, k0, nglob, K;
+    int nch;                    // chains (= warps) of this launch plan
+    const double* model;        // MODW doubles
+    double* fagg;               // [nch][FNW] chain filter aggregates, then their inclusive scan
+    double* fbuf;               // [nch][FNW] ping-pong
+    double* xp;                 // [nch][K][CNW] filtered moments
+    double* sagg;               // [nch][SNW]
+    double* sbuf;               // [nch][SNW]
+    double* nll_chain;          // [nch]
+    double* mean;
+    double* var;
+    double* nll_out;
+    const double* in_filt;      // sharded inputs (nullable), D-specific packing = FNW / SNW
+    const double* in_smooth;
+    int rank, world;
+    unsigned long long* err;
+    int store_state;
+};
+
+// ------------------------------------------------------------------ shared-memory model
+template <int D>
+struct SModel {
+    double F[D][LD(D)];
+    double Q[D][LD(D)];
+    double Pinf[D][LD(D)];
+    double H[D];
+    double r, udt;
+};
+
+template <int D>
+__device__ __forceinline__ void load_model(SModel<D>& sm, const double* __restrict__ g) {
+    for (int e = threadIdx.x; e < D * D; e += blockDim.x) {
+        const int i = e / D, j = e - (e / D) * D;
+        sm.F[i][j] = g[e];
+        sm.Q[i][j] = g[D * D + e];
+        sm.Pinf[i][j] = g[2 * D * D + e];
+    }
+    for (int i = threadIdx.x; i < D; i += blockDim.x) sm.H[i] = g[3 * D * D + i];
+    if (threadIdx.x == 0) {
+        sm.r = g[3 * D * D + D];
+        sm.udt = g[3 * D * D + D + 1];
+    }
+}
+
+// ------------------------------------------------------------------ warp matrix primitives
+// Out = A B (+ Cadd);  TA/TB: use A^T / B^T.  All D x D, shared, stride LD(D).
+template <int D, bool TA = false, bool TB = false>
+__device__ __forceinline__ void wmm(double (*Out)[LD(D)], const double (*A)[LD(D)], const double (*B)[LD(D)],
+                                    const double (*Cadd)[LD(D)], int lane) {
+    for (int e = lane; e < D * D; e += 32) {
+        const int i = e / D, j = e - (e / D) * D;
+        double s = Cadd ? Cadd[i][j] : 0.0;
+#pragma unroll 8
+        for (int k = 0; k < D; ++k) s = fma(TA ? A[k][i] : A[i][k], TB ? B[j][k] : B[k][j], s);
+        Out[i][j] = s;
+    }
+}
+
+// out = A v (TA: A^T v)
+template <int D, bool TA = false>
+__device__ __forceinline__ void wmv(double* out, const double (*A)[LD(D)], const double* v, int lane) {
+    for (int i = lane; i < D; i += 32) {
+        double s = 0.0;
+#pragma unroll 8
+        for (int k = 0; k < D; ++k) s = fma(TA ? A[k][i] : A[i][k], v[k], s);
+        out[i] = s;
+    }
+}
+
+// warp sum of a per-lane partial
+__device__ __forceinline__ double wsum(double v) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    return v;
+}
+
+// dot(a, b) over D elements in shared memory, result in every lane
+template <int D>
+__device__ __forceinline__ double wdot(const double* a, const double* b, int lane) {
+    double s = 0.0;
+    for (int i = lane; i < D; i += 32) s = fma(a[i], b[i], s);
+    return wsum(s);
+}
+
+// In-place inverse of a general D x D shared matrix by Gauss-Jordan with partial
+// pivoting (W: D x 2D scratch, stride 2D+1).  Returns false on a zero pivot.
+template <int D>
+__device__ bool winverse(double (*M)[LD(D)], double (*W)[2 * D + 1], int lane) {
+    for (int e = lane; e < D * 2 * D; e += 32) {
+        const int i = e / (2 * D), j = e - (e / (2 * D)) * (2 * D);
+        W[i][j] = (j < D) ? M[i][j] : ((j - D == i) ? 1.0 : 0.0);
+    }
+    __syncwarp();
+    bool ok = true;
+    for (int c = 0; c < D; ++c) {
+        // pivot: argmax |W[r][c]|, r >= c
+        double best = -1.0;
+        int br = c;
+        for (int r = c + lane; r < D; r += 32) {
+            const double v = fabs(W[r][c]);
+            if (v > best) { best = v; br = r; }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, best, off);
+            const int orr = __shfl_xor_sync(0xffffffffu, br, off);
+            if (ob > best || (ob == best && orr < br)) { best = ob; br = orr; }
+        }
+        ok = ok && (best > 0.0);
+        if (br != c) {
+            for (int j = lane; j < 2 * D; j += 32) {
+                const double u = W[c][j];
+                W[c][j] = W[br][j];
+                W[br][j] = u;
+            }
+        }
+        __syncwarp();
+        const double ip = 1.0 / W[c][c];
+        __syncwarp();
+        for (int j = lane; j < 2 * D; j += 32) W[c][j] *= ip;
+        __syncwarp();
+        // eliminate column c from every other row (factors read before the row is updated)
+        for (int e = lane; e < D * 2 * D; e += 32) {
+            const int i = e / (2 * D), j = e - (e / (2 * D)) * (2 * D);
+            if (i != c && j != c) W[i][j] = fma(-W[i][c], W[c][j], W[i][j]);
+        }
+        __syncwarp();
+        for (int i = lane; i < D; i += 32)
+            if (i != c) W[i][c] = 0.0;
+        __syncwarp();
+    }
+    for (int e = lane; e < D * D; e += 32) {
+        const int i = e / D, j = e - (e / D) * D;
+        M[i][j] = W[i][D + j];
+    }
+    __syncwarp();
+    return ok;
+}
+
+// ------------------------------------------------------------------ shared aggregates
+template <int D>
+struct SF {   // filter aggregate in shared memory
+    double A[D][LD(D)];
+    double C[D][LD(D)];
+    double J[D][LD(D)];
+    double b[D];
+    double eta[D];
+};
+template <int D>
+struct SS {   // smoother aggregate
+    double E[D][LD(D)];
+    double L[D][LD(D)];
+    double g[D];
+};
+
+// global (row-major, full) <-> shared
+template <int D>
+__device__ __forceinline__ void gload(SF<D>& a, const double* __restrict__ g, int lane) {
+    for (int e = lane; e < D * D; e += 32) {
+        const int i = e / D, j = e - (e / D) * D;
+        a.A[i][j] = g[e];
+        a.C[i][j] = g[D * D + D + e];
+        a.J[i][j] = g[2 * D * D + 2 * D + e];
+    }
+    for (int i = lane; i < D; i += 32) {
+        a.b[i] = g[D * D + i];
+        a.eta[i] = g[2 * D * D + D + i];
+    }
+    __syncwarp();
+}
+template <int D>
+__device__ __forceinline__ void gstore(const SF<D>& a, double* __restrict__ g, int lane) {
+    for (int e = lane; e < D * D; e += 32) {
+        const int i = e / D, j = e - (e / D) * D;
+        g[e] = a.A[i][j];
+        g[D * D + D + e] = a.C[i][j];
+        g[2 * D * D + 2 * D + e] = a.J[i][j];
+    }
+    for (int i = lane; i < D; i += 32) {
+        g[D * D + i] = a.b[i];
+        g[2 * D * D + D + i] = a.eta[i];
+    }
+}
+template <int D>
+__device__ __forceinline__ void gload(SS<D>& a, const double* __restrict__ g, int lane) {
+    for (int e = lane; e < D * D; e += 32) {
+        const int i = e / D, j = e - (e / D) * D;
+        a.E[i][j] = g[e];
+        a.L[i][j] = g[D * D + D + e];
+    }
+    for (int i = lane; i < D; i += 32) a.g[i] = g[D * D + i];
+    __syncwarp();
+}
+template <int D>
+__device__ __forceinline__ void gstore(const SS<D>& a, double* __restrict__ g, int lane) {
+    for (int e = lane; e < D * D; e += 32) {
+        const int i = e / D, j = e - (e / D) * D;
+        g[e] = a.E[i][j];
+        g[D * D + D + e] = a.L[i][j];
+    }
+    for (int i = lane; i < D; i += 32) g[D * D + i] = a.g[i];
+}
+template <int D>
+__device__ __forceinline__ void set_identity(SF<D>& a, int lane) {
+    for (int e = lane; e < D * D; e += 32) {
+        const int i = e / D, j = e - (e / D) * D;
+        a.A[i][j] = (i == j) ? 1.0 : 0.0;
+        a.C[i][j] = 0.0;
+        a.J[i][j] = 0.0;
+    }
+    for (int i = lane; i < D; i += 32) { a.b[i] = 0.0; a.eta[i] = 0.0; }
+    __syncwarp();
+}
+template <int D>
+__device__ __forceinline__ void set_identity(SS<D>& a, int lane) {
+    for (int e = lane; e < D * D; e += 32) {
+        const int i = e / D, j = e - (e / D) * D;
+        a.E[i][j] = (i == j) ? 1.0 : 0.0;
+        a.L[i][j] = 0.0;
+    }
+    for (int i = lane; i < D; i += 32) a.g[i] = 0.0;
+    __syncwarp();
+}
+
+// scratch for the general filtering operator
+template <int D>
+struct SCombF {
+    double M[D][LD(D)];
+    double T1[D][LD(D)];
+    double T2[D][LD(D)];
+    double W[D][2 * D + 1];
+    double v1[D], v2[D];
+};
+
+// out = ei (x) ej, with Minv = (I + C_i J_j)^-1 and
+// (I + J_j C_i)^-1 = Minv^T.  out may alias ej but not ei.
+template <int D>
+__device__ bool wcombine(const SF<D>& ei, SF<D>& ej, SF<D>& out, SCombF<D>& s, int lane) {
+    // M = I + C_i J_j
+    for (int e = lane; e < D * D; e += 32) {
+        const int i = e / D, j = e - (e / D) * D;
+        double acc = (i == j) ? 1.0 : 0.0;
+        for (int k = 0; k < D; ++k) acc = fma(ei.C[i][k], ej.J[k][j], acc);
+        s.M[i][j] = acc;
+    }
+    __syncwarp();
+    const bool ok = winverse<D>(s.M, s.W, lane);
+    // v1 = b_i + C_i eta_j ; v2 = eta_j - J_j b_i
+    for (int i = lane; i < D; i += 32) {
+        double a1 = ei.b[i], a2 = ej.eta[i];
+        for (int k = 0; k < D; ++k) {
+            a1 = fma(ei.C[i][k], ej.eta[k], a1);
+            a2 = fma(-ej.J[i][k], ei.b[k], a2);
+        }
+        s.v1[i] = a1;
+        s.v2[i] = a2;
+    }
+    __syncwarp();
+    // T1 = A_j Minv
+    wmm<D>(s.T1, ej.A, s.M, nullptr, lane);
+    __syncwarp();
+    // b_out = T1 v1 + b_j ; eta_out = A_i^T Minv^T v2 + eta_i  (= (Minv A_i)^T v2)
+    // T2 = Minv A_i (needed for J and eta)
+    wmm<D>(s.T2, s.M, ei.A, nullptr, lane);
+    __syncwarp();
+    double nb[(D + 31) / 32], ne[(D + 31) / 32];
+    for (int i = lane, q = 0; i < D; i += 32, ++q) {
+        double a1 = ej.b[i], a2 = ei.eta[i];
+        for (int k = 0; k < D; ++k) {
+            a1 = fma(s.T1[i][k], s.v1[k], a1);
+            a2 = fma(s.T2[k][i], s.v2[k], a2);
+        }
+        nb[q] = a1;
+        ne[q] = a2;
+    }
+    __syncwarp();
+    // J_out = A_i^T Minv^T J_j A_i + J_i = T2^T J_j A_i + J_i  -> M (free) = J_j A_i first
+    wmm<D>(s.M, ej.J, ei.A, nullptr, lane);
+    __syncwarp();
+    double* ojv = &out.J[0][0];
+    (void)ojv;
+    // compute new J into W (as D x D block) to allow out aliasing ej
+    for (int e = lane; e < D * D; e += 32) {
+        const int i = e / D, j = e - (e / D) * D;
+        double acc = ei.J[i][j];
+        for (int k = 0; k < D; ++k) acc = fma(s.T2[k][i], s.M[k][j], acc);
+        s.W[i][j] = acc;
+    }
+    __syncwarp();
+    // A_out = T1 A_i ; C_out = T1 C_i A_j^T + C_j   (M := T1 C_i)
+    wmm<D>(s.M, s.T1, ei.C, nullptr, lane);
+    __syncwarp();
+    for (int e = lane; e < D * D; e += 32) {
+        const int i = e / D, j = e - (e / D) * D;
+        double aa = 0.0, cc = ej.C[i][j];
+        for (int k = 0; k < D; ++k) {
+            aa = fma(s.T1[i][k], ei.A[k][j], aa);
+            cc = fma(s.M[i][k], ej.A[j][k], cc);
+        }
+        s.T2[i][j] = aa;     // T2 no longer needed
+        s.W[i][D + j] = cc;
+    }
+    __syncwarp();
+    for (int e = lane; e < D * D; e += 32) {
+        const int i = e / D, j = e - (e / D) * D;
+        out.A[i][j] = s.T2[i][j];
+        out.J[i][j] = 0.5 * (s.W[i][j] + s.W[j][i]);
+        out.C[i][j] = 0.5 * (s.W[i][D + j] + s.W[j][D + i]);
+    }
+    for (int i = lane, q = 0; i < D; i += 32, ++q) {
+        out.b[i] = nb[q];
+        out.eta[i] = ne[q];
+    }
+    __syncwarp();
+    return ok;
+}
+
+// out = ei (x)_s ej = (E_i E_j, E_i g_j + g_i, E_i L_j E_i^T + L_i); out may alias ej.
+template <int D>
+__device__ void wcombine(const SS<D>& ei, SS<D>& ej, SS<D>& out, SCombF<D>& s, int lane) {
+    wmm<D>(s.T1, ei.E, ej.L, nullptr, lane);        // E_i L_j
+    wmm<D>(s.T2, ei.E, ej.E, nullptr, lane);        // E_i E_j
+    for (int i = lane; i < D; i += 32) {
+        double a = ei.g[i];
+        for (int k = 0; k < D; ++k) a = fma(ei.E[i][k], ej.g[k], a);
+        s.v1[i] = a;
+    }
+    __syncwarp();
+    for (int e = lane; e < D * D; e += 32) {
+        const int i = e / D, j = e - (e / D) * D;
+        double a = ei.L[i][j];
+        for (int k = 0; k < D; ++k) a = fma(s.T1[i][k], ei.E[j][k], a);
+        s.M[i][j] = a;
+    }
+    __syncwarp();
+    for (int e = lane; e < D * D; e += 32) {
+        const int i = e / D, j = e - (e / D) * D;
+        out.E[i][j] = s.T2[i][j];
+        out.L[i][j] = 0.5 * (s.M[i][j] + s.M[j][i]);
+    }
+    for (int i = lane; i < D; i += 32) out.g[i] = s.v1[i];
+    __syncwarp();
+}
+
+// collapsed prefix (0, x, P, 0, 0) (x) a  ->  (x', P') written into (x, P)
+template <int D>
+__device__ bool wapply_prefix(double* x, double (*P)[LD(D)], const SF<D>& a, SCombF<D>& s, int lane) {
+    for (int e = lane; e < D * D; e += 32) {
+        const int i = e / D, j = e - (e / D) * D;
+        double acc = (i == j) ? 1.0 : 0.0;
+        for (int k = 0; k < D; ++k) acc = fma(P[i][k], a.J[k][j], acc);
+        s.M[i][j] = acc;
+    }
+    __syncwarp();
+    const bool ok = winverse<D>(s.M, s.W, lane);
+    for (int i = lane; i < D; i += 32) {
+        double acc = x[i];
+        for (int k = 0; k < D; ++k) acc = fma(P[i][k], a.eta[k], acc);
+        s.v1[i] = acc;
+    }
+    __syncwarp();
+    wmm<D>(s.T1, a.A, s.M, nullptr, lane);          // A Minv
+    __syncwarp();
+    wmm<D>(s.T2, s.T1, P, nullptr, lane);           // A Minv P
+    __syncwarp();
+    for (int i = lane; i < D; i += 32) {
+        double acc = a.b[i];
+        for (int k = 0; k < D; ++k) acc = fma(s.T1[i][k], s.v1[k], acc);
+        s.v2[i] = acc;
+    }
+    for (int e = lane; e < D * D; e += 32) {
+        const int i = e / D, j = e - (e / D) * D;
+        double acc = a.C[i][j];
+        for (int k = 0; k < D; ++k) acc = fma(s.T2[i][k], a.A[j][k], acc);
+        s.M[i][j] = acc;
+    }
+    __syncwarp();
+    for (int e = lane; e < D * D; e += 32) {
+        const int i = e / D, j = e - (e / D) * D;
+        P[i][j] = 0.5 * (s.M[i][j] + s.M[j][i]);
+    }
+    for (int i = lane; i < D; i += 32) x[i] = s.v2[i];
+    __syncwarp();
+    return ok;
+}
+
+// a (x)_s collapsed suffix (0, m, P) -> (E m + g, E P E^T + L) written into (m, P)
+template <int D>
+__device__ void wapply_suffix(const SS<D>& a, double* m, double (*P)[LD(D)], SCombF<D>& s, int lane) {
+    wmm<D>(s.T1, a.E, P, nullptr, lane);
+    for (int i = lane; i < D; i += 32) {
+        double acc = a.g[i];
+        for (int k = 0; k < D; ++k) acc = fma(a.E[i][k], m[k], acc);
+        s.v1[i] = acc;
+    }
+    __syncwarp();
+    for (int e = lane; e < D * D; e += 32) {
+        const int i = e / D, j = e - (e / D) * D;
+        double acc = a.L[i][j];
+        for (int k = 0; k < D; ++k) acc = fma(s.T1[i][k], a.E[j][k], acc);
+        s.M[i][j] = acc;
+    }
+    __syncwarp();
+    for (int e = lane; e < D * D; e += 32) {
+        const int i = e / D, j = e - (e / D) * D;
+        P[i][j] = 0.5 * (s.M[i][j] + s.M[j][i]);
+    }
+    for (int i = lane; i < D; i += 32) m[i] = s.v1[i];
+    __syncwarp();
+}
+
+// ------------------------------------------------------------------ discretisation (table)
+// returns 0 (F, Q valid in fz / via model), 1 = dt == 0 (identity), 2 = unsupported
+__device__ __forceinline__ int wdisc_kind(double dt, double udt) {
+    if (fabs(dt - udt) <= 1e-12 * udt) return 0;   // uniform step up to time-stamp rounding
+    if (dt == 0.0) return 1;
+    return 2;
+}
+
+// ------------------------------------------------------------------ K1w: fold
+template <int D>
+struct K1Smem {
+    SModel<D> m;
+    struct PerWarp {
+        SF<D> a;
+        double FA[D][LD(D)];
+        double T[D][LD(D)];
+        double Cm[D][LD(D)];
+        double Fb[D], HC[D], w[D];
+    } w[kWWarps];
+};
+
+template <int D>
+__global__ void __launch_bounds__(32 * kWWarps) kw_filter_fold(const WParams p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    K1Smem<D>& sh = *reinterpret_cast<K1Smem<D>*>(smem_raw);
+    load_model<D>(sh.m, p.model);
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int c = blockIdx.x * kWWarps + wid;
+    if (c >= p.nch) return;
+    auto& W = sh.w[wid];
+    set_identity<D>(W.a, lane);
+    const int64_t kb = static_cast<int64_t>(c) * p.K;
+    const int64_t ke = min(kb + p.K, p.n);
+    const SModel<D>& M = sh.m;
+    double tprev = (kb < p.n && (kb > 0 || p.k0 > 0)) ? __ldg(p.t + kb - 1) : 0.0;
+    for (int64_t k = kb; k < ke; ++k) {
+        const double tk = __ldg(p.t + k);
+        const bool obs = __ldg(p.mask + k) != 0;
+        const double yk = obs ? __ldg(p.y + k) : 0.0;
+        const int64_t g = p.k0 + k;
+        int kind = 0;
+        if (g == 0) kind = 3;                                   // F = 0, Q = P_inf
+        else kind = wdisc_kind(tk - tprev, M.udt);
+        if (lane == 0) {
+            if (g > 0 && !(tk - tprev >= 0.0)) raise_error(p.err, g, kErrInput);
+            if (!isfinite(tk) || (obs && !isfinite(yk))) raise_error(p.err, g, kErrInput);
+            if (kind == 2) raise_error(p.err, g, kErrUnsupported);
+        }
+        tprev = tk;
+        // FA = F A, T = F C, Fb = F b
+        for (int e = lane; e < D * D; e += 32) {
+            const int i = e / D, j = e - (e / D) * D;
+            double fa = 0.0, tt = 0.0;
+            if (kind == 0) {
+                for (int q = 0; q < D; ++q) {
+                    fa = fma(M.F[i][q], W.a.A[q][j], fa);
+                    tt = fma(M.F[i][q], W.a.C[q][j], tt);
+                }
+            } else if (kind == 1) {
+                fa = W.a.A[i][j];
+                tt = W.a.C[i][j];
+            }
+            W.FA[i][j] = fa;
+            W.T[i][j] = tt;
+        }
+        for (int i = lane; i < D; i += 32) {
+            double s = 0.0;
+            if (kind == 0)
+                for (int q = 0; q < D; ++q) s = fma(M.F[i][q], W.a.b[q], s);
+            else if (kind == 1)
+                s = W.a.b[i];
+            W.Fb[i] = s;
+        }
+        __syncwarp();
+        // Cm = T F^T + Q  (kind 3: P_inf; kind 1: T)
+        for (int e = lane; e < D * D; e += 32) {
+            const int i = e / D, j = e - (e / D) * D;
+            double s;
+            if (kind == 0) {
+                s = M.Q[i][j];
+                for (int q = 0; q < D; ++q) s = fma(W.T[i][q], M.F[j][q], s);
+            } else if (kind == 1) {
+                s = W.T[i][j];
+            } else {
+                s = M.Pinf[i][j];
+            }
+            W.Cm[i][j] = s;
+        }
+        __syncwarp();
+        // HC = Cm H^T ; w = (H FA)^T
+        for (int i = lane; i < D; i += 32) {
+            double hc = 0.0, ww = 0.0;
+            for (int q = 0; q < D; ++q) {
+                hc = fma(W.Cm[i][q], M.H[q], hc);
+                ww = fma(M.H[q], W.FA[q][i], ww);
+            }
+            W.HC[i] = hc;
+            W.w[i] = ww;
+        }
+        __syncwarp();
+        const double S = wdot<D>(M.H, W.HC, lane) + M.r;
+        const double hb = wdot<D>(M.H, W.Fb, lane);
+        const double iS = obs ? 1.0 / S : 0.0;
+        const double vs = obs ? (yk - hb) * iS : 0.0;
+        for (int e = lane; e < D * D; e += 32) {
+            const int i = e / D, j = e - (e / D) * D;
+            const double Ki = W.HC[i] * iS;
+            W.a.A[i][j] = fma(-Ki, W.w[j], W.FA[i][j]);
+            W.a.C[i][j] = fma(-Ki, W.HC[j], W.Cm[i][j]);
+            W.a.J[i][j] = fma(W.w[i] * iS, W.w[j], W.a.J[i][j]);
+        }
+        for (int i = lane; i < D; i += 32) {
+            W.a.b[i] = fma(W.HC[i], vs, W.Fb[i]);
+            W.a.eta[i] = fma(W.w[i], vs, W.a.eta[i]);
+        }
+        __syncwarp();
+    }
+    gstore<D>(W.a, p.fagg + static_cast<int64_t>(c) * FNW(D), lane);
+}
+
+// ------------------------------------------------------------------ Kogge-Stone scan levels (1 warp per element)
+template <int D>
+struct ScanSmemF {
+    SF<D> a, b;
+    SCombF<D> s;
+};
+template <int D>
+__global__ void __launch_bounds__(32) kw_scan_filter(const double* __restrict__ in, double* __restrict__ out, int nch,
+                                                     int off, unsigned long long* err) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    ScanSmemF<D>& sh = *reinterpret_cast<ScanSmemF<D>*>(smem_raw);
+    const int lane = threadIdx.x;
+    const int c = blockIdx.x;
+    if (c >= off) {
+        gload<D>(sh.a, in + static_cast<int64_t>(c - off) * FNW(D), lane);
+        gload<D>(sh.b, in + static_cast<int64_t>(c) * FNW(D), lane);
+        if (!wcombine<D>(sh.a, sh.b, sh.b, sh.s, lane) && lane == 0) raise_error(err, c, kErrNumeric);
+        gstore<D>(sh.b, out + static_cast<int64_t>(c) * FNW(D), lane);
+    } else {
+        for (int e = lane; e < FNW(D); e += 32) out[static_cast<int64_t>(c) * FNW(D) + e] = in[static_cast<int64_t>(c) * FNW(D) + e];
+    }
+}
+
+template <int D>
+struct ScanSmemS {
+    SS<D> a, b;
+    SCombF<D> s;
+};
+template <int D>
+__global__ void __launch_bounds__(32) kw_scan_smoother(const double* __restrict__ in, double* __restrict__ out,
+                                                       int nch, int off) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    ScanSmemS<D>& sh = *reinterpret_cast<ScanSmemS<D>*>(smem_raw);
+    const int lane = threadIdx.x;
+    const int c = blockIdx.x;
+    if (c + off < nch) {
+        gload<D>(sh.a, in + static_cast<int64_t>(c) * SNW(D), lane);
+        gload<D>(sh.b, in + static_cast<int64_t>(c + off) * SNW(D), lane);
+        wcombine<D>(sh.a, sh.b, sh.b, sh.s, lane);
+        gstore<D>(sh.b, out + static_cast<int64_t>(c) * SNW(D), lane);
+    } else {
+        for (int e = lane; e < SNW(D); e += 32) out[static_cast<int64_t>(c) * SNW(D) + e] = in[static_cast<int64_t>(c) * SNW(D) + e];
+    }
+}
+
+// ------------------------------------------------------------------ K3w: Kalman rescan
+template <int D>
+struct K3Smem {
+    SModel<D> m;
+    struct PerWarp {
+        SF<D> a;                      // scanned prefix of the previous chain (carry source)
+        SCombF<D> s;
+        double P[D][LD(D)], Pm[D][LD(D)], FP[D][LD(D)];
+        double Sg[D][LD(D)], Sm[D][LD(D)], P0[D][LD(D)];
+        double x[D], xm[D], x0[D], HP[D], SH[D];
+    } w[kWWarps];
+};
+
+template <int D>
+__global__ void __launch_bounds__(32 * kWWarps) kw_filter_apply(const WParams p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    K3Smem<D>& sh = *reinterpret_cast<K3Smem<D>*>(smem_raw);
+    load_model<D>(sh.m, p.model);
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int c = blockIdx.x * kWWarps + wid;
+    if (c >= p.nch) return;
+    auto& W = sh.w[wid];
+    const SModel<D>& M = sh.m;
+    // ---- carry (x, P) entering the chain: incoming (sharded) (x) inclusive scan up to chain c-1
+    for (int e = lane; e < D * D; e += 32) W.P[e / D][e % D] = 0.0;
+    for (int i = lane; i < D; i += 32) W.x[i] = 0.0;
+    __syncwarp();
+    for (int g = 0; g < p.rank && p.in_filt; ++g) {
+        gload<D>(W.a, p.in_filt + static_cast<int64_t>(g) * FNW(D), lane);
+        wapply_prefix<D>(W.x, W.P, W.a, W.s, lane);
+    }
+    if (c > 0) {
+        gload<D>(W.a, p.fagg + static_cast<int64_t>(c - 1) * FNW(D), lane);
+        if (!wapply_prefix<D>(W.x, W.P, W.a, W.s, lane) && lane == 0) raise_error(p.err, p.k0, kErrNumeric);
+    }
+    const int64_t kb = static_cast<int64_t>(c) * p.K;
+    const int64_t ke = min(kb + p.K, p.n);
+    double tprev = (kb < p.n && (kb > 0 || p.k0 > 0)) ? __ldg(p.t + kb - 1) : 0.0;
+    double quad = 0.0, logs = 0.0;
+    int nobs = 0;
+    double* xpc = p.xp + static_cast<int64_t>(c) * p.K * CNW(D);
+    for (int64_t k = kb; k < ke; ++k) {
+        const double tk = __ldg(p.t + k);
+        const bool obs = __ldg(p.mask + k) != 0;
+        const double yk = obs ? __ldg(p.y + k) : 0.0;
+        const int64_t g = p.k0 + k;
+        const int kind = (g == 0) ? 3 : wdisc_kind(tk - tprev, M.udt);
+        const bool first = (k == kb);
+        tprev = tk;
+        // predict: xm = F x, FP = F P, Pm = FP F^T + Q ; Sm = Sg F^T
+        for (int e = lane; e < D * D; e += 32) {
+            const int i = e / D, j = e - (e / D) * D;
+            double fp = 0.0, sm = 0.0;
+            if (kind == 0) {
+                for (int q = 0; q < D; ++q) {
+                    fp = fma(M.F[i][q], W.P[q][j], fp);
+                    sm = fma(W.Sg[i][q], M.F[j][q], sm);
+                }
+            } else if (kind == 1) {
+                fp = W.P[i][j];
+                sm = W.Sg[i][j];
+            }
+            W.FP[i][j] = fp;
+            W.Sm[i][j] = sm;
+        }
+        for (int i = lane; i < D; i += 32) {
+            double s = 0.0;
+            if (kind == 0)
+                for (int q = 0; q < D; ++q) s = fma(M.F[i][q], W.x[q], s);
+            else if (kind == 1)
+                s = W.x[i];
+            W.xm[i] = s;
+        }
+        __syncwarp();
+        for (int e = lane; e < D * D; e += 32) {
+            const int i = e / D, j = e - (e / D) * D;
+            double s;
+            if (kind == 0) {
+                s = M.Q[i][j];
+                for (int q = 0; q < D; ++q) s = fma(W.FP[i][q], M.F[j][q], s);
+            } else if (kind == 1) {
+                s = W.FP[i][j];
+            } else {
+                s = M.Pinf[i][j];
+            }
+            W.Pm[i][j] = s;
+        }
+        __syncwarp();
+        for (int i = lane; i < D; i += 32) {
+            double hp = 0.0, sh_ = 0.0;
+            for (int q = 0; q < D; ++q) {
+                hp = fma(W.Pm[i][q], M.H[q], hp);
+                sh_ = fma(W.Sm[i][q], M.H[q], sh_);
+            }
+            W.HP[i] = hp;
+            W.SH[i] = sh_;
+        }
+        __syncwarp();
+        const double S = wdot<D>(M.H, W.HP, lane) + M.r;
+        const double hx = wdot<D>(M.H, W.xm, lane);
+        if (lane == 0 && obs && !(S > 0.0 && S < INFINITY)) raise_error(p.err, g, kErrNumeric);
+        const double iS = obs ? 1.0 / S : 0.0;
+        const double v = obs ? (yk - hx) : 0.0;
+        const double vs = v * iS;
+        for (int e = lane; e < D * D; e += 32) {
+            const int i = e / D, j = e - (e / D) * D;
+            const double Pn = fma(-W.HP[i] * iS, W.HP[j], W.Pm[i][j]);
+            W.P[i][j] = Pn;
+            if (first) {
+                W.P0[i][j] = Pn;
+                W.Sg[i][j] = Pn;
+            } else {
+                W.Sg[i][j] = fma(-W.SH[i] * iS, W.HP[j], W.Sm[i][j]);
+                W.P0[i][j] = fma(-W.SH[i] * iS, W.SH[j], W.P0[i][j]);
+            }
+        }
+        for (int i = lane; i < D; i += 32) {
+            const double xn = fma(W.HP[i], vs, W.xm[i]);
+            W.x[i] = xn;
+            W.x0[i] = first ? xn : fma(W.SH[i], vs, W.x0[i]);
+        }
+        if (obs) {
+            quad = fma(v, vs, quad);
+            logs += log(S);
+            ++nobs;
+        }
+        __syncwarp();
+        if (p.store_state) {
+            double* o = xpc + (k - kb) * CNW(D);
+            for (int i = lane; i < D; i += 32) o[i] = W.x[i];
+            for (int e = lane; e < D * D; e += 32) {
+                const int i = e / D, j = e - (e / D) * D;
+                if (j >= i) o[D + si(D, i, j)] = W.P[i][j];
+            }
+        }
+    }
+    if (lane == 0) {
+        p.nll_chain[c] = nobs ? 0.5 * (quad + logs + nobs * 1.8378770664093453) : 0.0;
+    }
+    if (!p.store_state) return;
+    // ---- chain smoother aggregate (E, g, L), as in the d <= 3 path
+    SS<D>* sagg = reinterpret_cast<SS<D>*>(&W.a);   // reuse the carry scratch
+    if (ke <= kb) {
+        set_identity<D>(*sagg, lane);
+    } else if (p.k0 + ke == p.nglob) {
+        for (int e = lane; e < D * D; e += 32) {
+            const int i = e / D, j = e - (e / D) * D;
+            sagg->E[i][j] = 0.0;
+            sagg->L[i][j] = W.P0[i][j];
+        }
+        for (int i = lane; i < D; i += 32) sagg->g[i] = W.x0[i];
+        __syncwarp();
+    } else {
+        const double tn = __ldg(p.t + ke);
+        const int kind = wdisc_kind(tn - tprev, M.udt);
+        // Pm, xm of the next step; Sm = Sg F^T
+        for (int e = lane; e < D * D; e += 32) {
+            const int i = e / D, j = e - (e / D) * D;
+            double fp = 0.0, sm = 0.0;
+            if (kind == 0) {
+                for (int q = 0; q < D; ++q) {
+                    fp = fma(M.F[i][q], W.P[q][j], fp);
+                    sm = fma(W.Sg[i][q], M.F[j][q], sm);
+                }
+            } else {
+                fp = W.P[i][j];
+                sm = W.Sg[i][j];
+            }
+            W.FP[i][j] = fp;
+            W.Sm[i][j] = sm;
+        }
+        for (int i = lane; i < D; i += 32) {
+            double s = 0.0;
+            if (kind == 0)
+                for (int q = 0; q < D; ++q) s = fma(M.F[i][q], W.x[q], s);
+            else
+                s = W.x[i];
+            W.xm[i] = s;
+        }
+        __syncwarp();
+        for (int e = lane; e < D * D; e += 32) {
+            const int i = e / D, j = e - (e / D) * D;
+            double s = (kind == 0) ? M.Q[i][j] : 0.0;
+            if (kind == 0)
+                for (int q = 0; q < D; ++q) s = fma(W.FP[i][q], M.F[j][q], s);
+            else
+                s = W.FP[i][j];
+            W.Pm[i][j] = s;
+        }
+        __syncwarp();
+        // E = Sm Pm^-1 : invert Pm (into W.FP via winverse on a copy)
+        for (int e = lane; e < D * D; e += 32) W.FP[e / D][e % D] = W.Pm[e / D][e % D];
+        __syncwarp();
+        if (!winverse<D>(W.FP, W.s.W, lane) && lane == 0) raise_error(p.err, p.k0 + ke, kErrNumeric);
+        wmm<D>(sagg->E, W.Sm, W.FP, nullptr, lane);
+        __syncwarp();
+        for (int i = lane; i < D; i += 32) {
+            double a = W.x0[i];
+            for (int q = 0; q < D; ++q) a = fma(-sagg->E[i][q], W.xm[q], a);
+            sagg->g[i] = a;
+        }
+        for (int e = lane; e < D * D; e += 32) {
+            const int i = e / D, j = e - (e / D) * D;
+            double a = W.P0[i][j];
+            for (int q = 0; q < D; ++q) a = fma(-sagg->E[i][q], W.Sm[j][q], a);
+            W.Pm[i][j] = a;
+        }
+        __syncwarp();
+        for (int e = lane; e < D * D; e += 32) {
+            const int i = e / D, j = e - (e / D) * D;
+            sagg->L[i][j] = 0.5 * (W.Pm[i][j] + W.Pm[j][i]);
+        }
+        __syncwarp();
+    }
+    gstore<D>(*sagg, p.sagg + static_cast<int64_t>(c) * SNW(D), lane);
+}
+
+// ------------------------------------------------------------------ K5w: RTS rescan
+template <int D>
+struct K5Smem {
+    SModel<D> m;
+    struct PerWarp {
+        SS<D> a;
+        SCombF<D> s;
+        double P[D][LD(D)], Pm[D][LD(D)], FP[D][LD(D)], G[D][LD(D)], T[D][LD(D)];
+        double Ps[D][LD(D)];
+        double x[D], xm[D], ms[D], dm[D];
+    } w[kWWarps];
+};
+
+template <int D>
+__global__ void __launch_bounds__(32 * kWWarps) kw_smoother_apply(const WParams p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    K5Smem<D>& sh = *reinterpret_cast<K5Smem<D>*>(smem_raw);
+    load_model<D>(sh.m, p.model);
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int c = blockIdx.x * kWWarps + wid;
+    // NLL: fixed-order sum of the chain partials (CTA 0, warp 0)
+    if (blockIdx.x == 0 && wid == 0 && p.nll_out) {
+        double s = 0.0;
+        const int per = (p.nch + 31) / 32;
+        for (int i = 0; i < per; ++i) {
+            const int q = lane * per + i;
+            if (q < p.nch) s += p.nll_chain[q];
+        }
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
+        if (lane == 0) *p.nll_out = s;
+    }
+    if (c >= p.nch) return;
+    auto& W = sh.w[wid];
+    const SModel<D>& M = sh.m;
+    // ---- carry: collapsed suffix after the chain = incoming (sharded) then scanned suffix of c+1
+    for (int e = lane; e < D * D; e += 32) W.Ps[e / D][e % D] = 0.0;
+    for (int i = lane; i < D; i += 32) W.ms[i] = 0.0;
+    __syncwarp();
+    for (int g = p.world - 1; g > p.rank && p.in_smooth; --g) {
+        gload<D>(W.a, p.in_smooth + static_cast<int64_t>(g) * SNW(D), lane);
+        wapply_suffix<D>(W.a, W.ms, W.Ps, W.s, lane);
+    }
+    if (c + 1 < p.nch) {
+        gload<D>(W.a, p.sagg + static_cast<int64_t>(c + 1) * SNW(D), lane);
+        wapply_suffix<D>(W.a, W.ms, W.Ps, W.s, lane);
+    }
+    const int64_t kb = static_cast<int64_t>(c) * p.K;
+    const int64_t ke = min(kb + p.K, p.n);
+    const double* xpc = p.xp + static_cast<int64_t>(c) * p.K * CNW(D);
+    double tnext = (ke > kb && p.k0 + ke < p.nglob) ? __ldg(p.t + ke) : 0.0;
+    for (int64_t k = ke - 1; k >= kb; --k) {
+        const double tk = __ldg(p.t + k);
+        const int64_t g = p.k0 + k;
+        const double* src = xpc + (k - kb) * CNW(D);
+        for (int i = lane; i < D; i += 32) W.x[i] = src[i];
+        for (int e = lane; e < D * D; e += 32) {
+            const int i = e / D, j = e - (e / D) * D;
+            W.P[i][j] = src[D + si(D, i, j)];
+        }
+        __syncwarp();
+        if (g == p.nglob - 1) {
+            for (int e = lane; e < D * D; e += 32) W.Ps[e / D][e % D] = W.P[e / D][e % D];
+            for (int i = lane; i < D; i += 32) W.ms[i] = W.x[i];
+            __syncwarp();
+        } else {
+            const int kind = wdisc_kind(tnext - tk, M.udt);
+            for (int e = lane; e < D * D; e += 32) {
+                const int i = e / D, j = e - (e / D) * D;
+                double fp = 0.0;
+                if (kind == 0)
+                    for (int q = 0; q < D; ++q) fp = fma(M.F[i][q], W.P[q][j], fp);
+                else
+                    fp = W.P[i][j];
+                W.FP[i][j] = fp;
+            }
+            for (int i = lane; i < D; i += 32) {
+                double s = 0.0;
+                if (kind == 0)
+                    for (int q = 0; q < D; ++q) s = fma(M.F[i][q], W.x[q], s);
+                else
+                    s = W.x[i];
+                W.xm[i] = s;
+            }
+            __syncwarp();
+            for (int e = lane; e < D * D; e += 32) {
+                const int i = e / D, j = e - (e / D) * D;
+                double s;
+                if (kind == 0) {
+                    s = M.Q[i][j];
+                    for (int q = 0; q < D; ++q) s = fma(W.FP[i][q], M.F[j][q], s);
+                } else {
+                    s = W.FP[i][j];
+                }
+                W.Pm[i][j] = s;
+                W.T[i][j] = s;
+            }
+            __syncwarp();
+            // G = P F^T Pm^-1 = (Pm^-1 F P)^T
+            if (!winverse<D>(W.T, W.s.W, lane) && lane == 0) raise_error(p.err, g, kErrNumeric);
+            wmm<D, true, false>(W.G, W.FP, W.T, nullptr, lane);   // G = (F P)^T Pm^-1 = P F^T Pm^-1
+            __syncwarp();
+            // ms = x + G (ms - xm)
+            for (int i = lane; i < D; i += 32) W.dm[i] = W.ms[i] - W.xm[i];
+            __syncwarp();
+            for (int i = lane; i < D; i += 32) {
+                double s = W.x[i];
+                for (int q = 0; q < D; ++q) s = fma(W.G[i][q], W.dm[q], s);
+                W.xm[i] = s;
+            }
+            // T = G (Ps - Pm)
+            for (int e = lane; e < D * D; e += 32) {
+                const int i = e / D, j = e - (e / D) * D;
+                double s = 0.0;
+                for (int q = 0; q < D; ++q) s = fma(W.G[i][q], W.Ps[q][j] - W.Pm[q][j], s);
+                W.T[i][j] = s;
+            }
+            __syncwarp();
+            for (int e = lane; e < D * D; e += 32) {
+                const int i = e / D, j = e - (e / D) * D;
+                double s = W.P[i][j];
+                for (int q = 0; q < D; ++q) s = fma(W.T[i][q], W.G[j][q], s);
+                W.FP[i][j] = s;
+            }
+            __syncwarp();
+            for (int e = lane; e < D * D; e += 32) {
+                const int i = e / D, j = e - (e / D) * D;
+                W.Ps[i][j] = 0.5 * (W.FP[i][j] + W.FP[j][i]);
+            }
+            for (int i = lane; i < D; i += 32) W.ms[i] = W.xm[i];
+            __syncwarp();
+        }
+        tnext = tk;
+        if (lane == 0) {
+            double mo = 0.0, vo = 0.0;
+            for (int i = 0; i < D; ++i) {
+                mo = fma(M.H[i], W.ms[i], mo);
+                double s2 = 0.0;
+                for (int j = 0; j < D; ++j) s2 = fma(W.Ps[i][j], M.H[j], s2);
+                vo = fma(M.H[i], s2, vo);
+            }
+            if (p.mean) p.mean[k] = mo;
+            if (p.var) p.var[k] = vo;
+        }
+        __syncwarp();
+    }
+}
+
+}  // namespace wide
+}  // namespace pssgp

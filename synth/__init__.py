@@ -140,15 +140,17 @@ def co2_like(t: np.ndarray) -> np.ndarray:
 
 
 def config4(n: int = 2 ** 24, harmonics: int = 6) -> Workload:
-    """C4: Periodic(J=6) + Matern-3/2 trend, weekly cadence, uniform dt = 1/52."""
-    t = np.arange(n, dtype=np.float64) / 52.0
+    """C4: Periodic(J=6) + Matern-3/2 trend, weekly cadence.  The
+    time unit is the WEEK so the grid t_k = k is exactly uniform (dt = 1): period
+    52 weeks, trend lengthscale 20 years = 1040 weeks."""
+    t = np.arange(n, dtype=np.float64)
     mask = (np.arange(n) % 16 != 15).astype(np.uint8)
-    y = _noisy(co2_like(t), 0.3)
+    y = _noisy(co2_like(t / 52.0), 0.3)
     y = (y - y.mean()) / y.std()
     y = _apply_mask(y, mask)
-    comps = [Component("periodic", 4.0, 1.0, period=1.0, order=harmonics),
-             Component("matern32", 10.0, 20.0)]
-    return Workload("C4", comps, 0.09, t, y, mask, uniform_dt=1.0 / 52.0)
+    comps = [Component("periodic", 4.0, 1.0, period=52.0, order=harmonics),
+             Component("matern32", 10.0, 20.0 * 52.0)]
+    return Workload("C4", comps, 0.09, t, y, mask, uniform_dt=1.0)
 
 
 def random_problem(seed: int, n: int, kind: str = "matern52", p_missing: float = 0.3,

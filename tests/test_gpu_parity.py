@@ -191,3 +191,62 @@ def test_misaligned_mask_pointer(cuda_device):
     m.check()
     em, ev, en = errors((mean.cpu().numpy(), var.cpu().numpy(), float(nll.cpu()[0])), o)
     assert em <= MEAN_TOL and ev <= VAR_TOL and en <= NLL_TOL
+
+
+# ------------------------------------------------------------------ warp-per-chain path (d >= 4, uniform dt)
+def _uniform(components, noise_var, n, dt, p_missing=1 / 16, seed=0, f=None):
+    t = np.arange(n, dtype=np.float64) * dt
+    rng = np.random.default_rng(seed)
+    mask = (rng.random(n) >= p_missing).astype(np.uint8)
+    base = synth.sinusoid(t) if f is None else f(t)
+    y = base + np.sqrt(noise_var) * rng.standard_normal(n)
+    y[mask == 0] = np.nan
+    return synth.Workload("uniform", components, noise_var, t, y, mask, uniform_dt=dt)
+
+
+@pytest.mark.parametrize("n", [1, 7, 300, 4097])
+def test_wide_rbf6(cuda_device, n):
+    """C3-shaped: RBF Taylor order 6 (d = 6), uniform dt = h, 1/16 missing."""
+    w = _uniform([synth.Component("rbf", 1.0, 0.5, order=6)], 0.01, n, synth.H_FINE * 64)
+    assert_parity(w)
+
+
+def test_wide_config3_shape(cuda_device):
+    w = synth.config3(n=2 ** 15)
+    assert_parity(w)
+
+
+@pytest.mark.parametrize("n", [5, 2000])
+def test_wide_config4_shape(cuda_device, n):
+    """C4-shaped: periodic J = 6 (d = 14) + Matern-3/2 trend (d = 2) = d 16, weekly cadence."""
+    w = synth.config4(n=n)
+    assert_parity(w)
+
+
+@pytest.mark.parametrize("comps,dt", [
+    ([synth.Component("matern32", 1.0, 0.7), synth.Component("matern32", 0.5, 3.0)], 0.01),   # d = 4
+    ([synth.Component("matern32", 1.0, 0.7), synth.Component("matern52", 0.5, 3.0)], 0.02),   # d = 5
+    ([synth.Component("periodic", 1.0, 1.0, period=0.5, order=3), synth.Component("matern32", 1.0, 2.0)], 0.01),  # d = 10
+])
+def test_wide_sums(cuda_device, comps, dt):
+    w = _uniform(comps, 0.05, 3001, dt, p_missing=0.3, seed=3)
+    assert_parity(w)
+
+
+def test_wide_ties_and_small_chains(cuda_device):
+    w = _uniform([synth.Component("rbf", 1.0, 0.8, order=4)], 0.02, 5003, 0.01, p_missing=0.25, seed=5)
+    w.t[100:103] = w.t[100]           # exact ties (dt = 0)
+    w.t[103:] = w.t[103:] - 3 * 0.01  # keep the remaining steps uniform
+    w.uniform_dt = 0.01
+    assert_parity(w, chain_len=3)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_wide_virtual_sharding(cuda_device, world):
+    w = _uniform([synth.Component("rbf", 1.0, 0.5, order=6)], 0.01, 6001, 0.002, p_missing=0.2, seed=9)
+    ref_mean, ref_var, ref_nll, _ = run_gpu(w)
+    from paper_2102_09964_b200 import sharded
+    mean, var, nll = sharded.run_virtual(w.components, w.noise_var, w.t, w.y, w.mask, world, uniform_dt=w.uniform_dt)
+    assert np.max(np.abs(mean - ref_mean)) / np.max(np.abs(ref_mean)) < 1e-10
+    assert np.max(np.abs(var - ref_var) / ref_var) < 1e-10
+    assert abs(nll - ref_nll) < 1e-10 * abs(ref_nll)

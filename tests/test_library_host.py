@@ -71,8 +71,19 @@ def test_rbf_and_sum_models():
     taus = np.linspace(0, 2.0, 30)
     np.testing.assert_allclose(ossm.ssm_kernel(lm, taus), ossm.ssm_kernel(om, taus), rtol=1e-9, atol=1e-12)
     comps = [synth.Component("periodic", 4.0, 1.0, period=1.0, order=6), synth.Component("matern32", 10.0, 20.0)]
-    with pytest.raises(P.PssgpError):   # d = 16 not compiled yet in this build -> E_UNSUPPORTED
-        P.Model(comps, 0.09, uniform_dt=1 / 52)
+    m = P.Model(comps, 0.09, uniform_dt=1 / 52)          # C4: d = 16, warp-per-chain path
+    assert m.state_dim == 16
+    lm, s = _lib_ssm(m.h)
+    om = ossm.build(comps)
+    taus = np.linspace(0, 3.0, 31)
+    np.testing.assert_allclose(ossm.ssm_kernel(lm, taus), ossm.ssm_kernel(om, taus), rtol=1e-10, atol=1e-12)
+    F, Q = m.discretize(1 / 52)
+    Fo, Qo = oracle.discretize(lm, 1 / 52)
+    assert np.max(np.abs(F - Fo)) < 1e-13 and np.max(np.abs(Q - Qo)) < 1e-13 * np.max(np.abs(Qo))
+    with pytest.raises(P.PssgpError):
+        m.discretize(0.5 / 52)                            # irregular dt: no device discretisation
+    with pytest.raises(P.PssgpError):                     # d = 7 is not compiled
+        P.Model([synth.Component("rbf", 1.0, 0.5, order=7)], 0.1, uniform_dt=0.01)
 
 
 @pytest.mark.parametrize("kind", ["matern12", "matern32", "matern52"])
@@ -95,6 +106,7 @@ def test_uniform_dt_table_vs_oracle():
     for comp, dt in [(synth.Component("matern52", 1.0, 0.5), synth.H_FINE),
                      (synth.Component("rbf", 1.0, 0.5, order=3), synth.H_FINE),
                      (synth.Component("rbf", 1.0, 1.5, order=2), 0.01),
+                     (synth.Component("rbf", 1.0, 0.5, order=6), synth.H_FINE),
                      (synth.Component("matern32", 2.0, 0.3), 0.05)]:
         m = P.Model([comp], 0.1, uniform_dt=dt)
         lm, s = _lib_ssm(m.h)
@@ -115,3 +127,6 @@ def test_aggregate_bytes():
     m = P.Model([synth.Component("matern52", 1.0, 0.5)], 0.1)
     assert P.pssgp_aggregate_bytes(m.h, 0) == 27 * 8
     assert P.pssgp_aggregate_bytes(m.h, 1) == 18 * 8
+    m = P.Model([synth.Component("rbf", 1.0, 0.5, order=6)], 0.1, uniform_dt=0.01)
+    assert P.pssgp_aggregate_bytes(m.h, 0) == (3 * 36 + 12) * 8     # wide path: full matrices
+    assert P.pssgp_aggregate_bytes(m.h, 1) == (2 * 36 + 6) * 8
