@@ -63,6 +63,8 @@ def parse():
     ap.add_argument("--N", type=int, default=2 ** 24)
     ap.add_argument("--uniform", action="store_true", help="uniform dt (secondary row)")
     ap.add_argument("--kind", default="matern52")
+    ap.add_argument("--config", default="metric", choices=["metric", "c2", "c3", "c4", "c5"],
+                    help="workload (default: the BASELINE metric); c3/c4 are the d = 6 / d = 16 rows")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=2 ** 21)
     ap.add_argument("--chain-len", type=int, default=0)
@@ -139,12 +141,24 @@ def cpu_baseline(w, sample: int):
                       f"{dt:.2f} s on {os.cpu_count()} host cores (1 used)"}
 
 
+def make_workload(args):
+    import synth
+    if args.config == "c2":
+        return synth.config2()
+    if args.config == "c3":
+        return synth.config3(n=args.N if args.N != 2 ** 24 else 2 ** 22)
+    if args.config == "c4":
+        return synth.config4(n=args.N)
+    if args.config == "c5":
+        return synth.metric_workload(2 ** 27 if args.N == 2 ** 24 else args.N)
+    return synth.metric_workload(args.N, uniform=args.uniform, kind=args.kind)
+
+
 def run_reference(args, rank: int):
     """--impl reference: the CPU oracle as the reference arm (rank 0 only)."""
     if rank != 0:
         return
-    import synth
-    w = synth.metric_workload(args.N, uniform=args.uniform, kind=args.kind)
+    w = make_workload(args)
     import oracle
     m = oracle.ssm.build(w.components)
     n = min(2 ** 19, w.N)
@@ -187,7 +201,7 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
 
-    w = synth.metric_workload(args.N, uniform=args.uniform, kind=args.kind)
+    w = make_workload(args)
     model = P.Model(w.components, w.noise_var, uniform_dt=w.uniform_dt, chain_len=args.chain_len,
                     blocks_per_sm=args.blocks_per_sm, device=local)
     N = w.N
@@ -288,7 +302,8 @@ def main():
     per_launch_ms = dom_ms / dom_launches
     alg_b = ALG_BYTES.get(dom, 0) * n_local
     hbm_gbs = alg_b / (per_launch_ms * 1e-3) / 1e9
-    flops = FLOPS_PER_STEP.get(dom, 0.0) * n_local if model.state_dim == 3 and not args.uniform else None
+    flops = (FLOPS_PER_STEP.get(dom, 0.0) * n_local
+             if model.state_dim == 3 and not args.uniform and args.config in ("metric", "c2", "c5") else None)
     plan = model.plan(n_local)
     launches = int(sum(v[1] for v in kern.values()))
     traffic, traffic_src = ncu_traffic(dom)
@@ -316,7 +331,9 @@ def main():
     cpu = None
     if not args.no_cpu_baseline:
         cpu = cpu_baseline(w, args.cpu_sample)
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+    metric = METRIC if args.config == "metric" and not args.uniform else \
+        f"time-steps/s (filter+smoother+NLL, fp64) {w.name} N={N}"
+    line = {"metric": metric, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": w.name, "N": N, "state_dim": model.state_dim, "chain_len": plan["chain_len"],
