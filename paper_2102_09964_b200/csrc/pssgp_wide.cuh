@@ -79,16 +79,120 @@ __device__ __forceinline__ void load_model(SModel<D>& sm, const double* __restri
 
 // ------------------------------------------------------------------ warp matrix primitives
 // Out = A B (+ Cadd);  TA/TB: use A^T / B^T.  All D x D, shared, stride LD(D).
+// D = 16 / 8: register-blocked, each lane owns an RB x CB output block (32 blocks),
+// so per k it loads RB + CB operands for RB*CB FMAs; other D: one output per lane-step.
+template <int D>
+struct Blk {
+    static constexpr bool ok = (D == 16 || D == 8);
+    static constexpr int RB = (D == 16) ? 2 : 1;
+    static constexpr int CB = (D == 16) ? 4 : 2;
+};
+
 template <int D, bool TA = false, bool TB = false>
 __device__ __forceinline__ void wmm(double (*Out)[LD(D)], const double (*A)[LD(D)], const double (*B)[LD(D)],
                                     const double (*Cadd)[LD(D)], int lane) {
-    for (int e = lane; e < D * D; e += 32) {
-        const int i = e / D, j = e - (e / D) * D;
-        double s = Cadd ? Cadd[i][j] : 0.0;
+    if constexpr (Blk<D>::ok) {
+        constexpr int RB = Blk<D>::RB, CB = Blk<D>::CB, NCB = D / CB;
+        const int i0 = (lane / NCB) * RB, j0 = (lane % NCB) * CB;
+        double acc[RB][CB];
+#pragma unroll
+        for (int r = 0; r < RB; ++r)
+#pragma unroll
+            for (int c = 0; c < CB; ++c) acc[r][c] = Cadd ? Cadd[i0 + r][j0 + c] : 0.0;
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            double a[RB], b[CB];
+#pragma unroll
+            for (int r = 0; r < RB; ++r) a[r] = TA ? A[k][i0 + r] : A[i0 + r][k];
+#pragma unroll
+            for (int c = 0; c < CB; ++c) b[c] = TB ? B[j0 + c][k] : B[k][j0 + c];
+#pragma unroll
+            for (int r = 0; r < RB; ++r)
+#pragma unroll
+                for (int c = 0; c < CB; ++c) acc[r][c] = fma(a[r], b[c], acc[r][c]);
+        }
+#pragma unroll
+        for (int r = 0; r < RB; ++r)
+#pragma unroll
+            for (int c = 0; c < CB; ++c) Out[i0 + r][j0 + c] = acc[r][c];
+    } else {
+        for (int e = lane; e < D * D; e += 32) {
+            const int i = e / D, j = e - (e / D) * D;
+            double s = Cadd ? Cadd[i][j] : 0.0;
 #pragma unroll 8
-        for (int k = 0; k < D; ++k) s = fma(TA ? A[k][i] : A[i][k], TB ? B[j][k] : B[k][j], s);
-        Out[i][j] = s;
+            for (int k = 0; k < D; ++k) s = fma(TA ? A[k][i] : A[i][k], TB ? B[j][k] : B[k][j], s);
+            Out[i][j] = s;
+        }
     }
+}
+
+// Cholesky factor of an SPD shared matrix (lower triangle of Lm, reciprocal of the
+// diagonal in Li; left-looking Crout, lanes over the rows of each column, D
+// warp-synchronous rounds; dot products split over two accumulators).
+template <int D>
+__device__ bool wcholesky(const double (*S)[LD(D)], double (*Lm)[LD(D)], double* Li, int lane) {
+    bool ok = true;
+    for (int j = 0; j < D; ++j) {
+        double d0 = S[j][j], d1 = 0.0;
+        int k = 0;
+        for (; k + 1 < j; k += 2) {
+            d0 = fma(-Lm[j][k], Lm[j][k], d0);
+            d1 = fma(-Lm[j][k + 1], Lm[j][k + 1], d1);
+        }
+        if (k < j) d0 = fma(-Lm[j][k], Lm[j][k], d0);
+        const double d = d0 + d1;
+        ok = ok && (d > 0.0);
+        const double il = rsqrt(d);
+        for (int i = j + 1 + lane; i < D; i += 32) {
+            double t0 = S[i][j], t1 = 0.0;
+            int q = 0;
+            for (; q + 1 < j; q += 2) {
+                t0 = fma(-Lm[i][q], Lm[j][q], t0);
+                t1 = fma(-Lm[i][q + 1], Lm[j][q + 1], t1);
+            }
+            if (q < j) t0 = fma(-Lm[i][q], Lm[j][q], t0);
+            Lm[i][j] = (t0 + t1) * il;
+        }
+        if (lane == 0) {
+            Lm[j][j] = d * il;
+            Li[j] = il;
+        }
+        __syncwarp();
+    }
+    return ok;
+}
+
+// X[:, j] = S^-1 R[:, j] for j < D with S = Lm Lm^T: lane j solves column j
+// (forward then backward substitution, vector in registers).  X may alias R.
+template <int D>
+__device__ __forceinline__ void wchol_solve(const double (*Lm)[LD(D)], const double* Li, const double (*R)[LD(D)],
+                                            double (*X)[LD(D)], int lane) {
+    if (lane < D) {
+        double z[D];
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            double s0 = R[i][lane], s1 = 0.0;
+#pragma unroll
+            for (int k = 0; k < i; ++k) {
+                if (k & 1) s1 = fma(-Lm[i][k], z[k], s1);
+                else s0 = fma(-Lm[i][k], z[k], s0);
+            }
+            z[i] = (s0 + s1) * Li[i];
+        }
+#pragma unroll
+        for (int i = D - 1; i >= 0; --i) {
+            double s0 = z[i], s1 = 0.0;
+#pragma unroll
+            for (int k = i + 1; k < D; ++k) {
+                if (k & 1) s1 = fma(-Lm[k][i], z[k], s1);
+                else s0 = fma(-Lm[k][i], z[k], s0);
+            }
+            z[i] = (s0 + s1) * Li[i];
+        }
+#pragma unroll
+        for (int i = 0; i < D; ++i) X[i][lane] = z[i];
+    }
+    __syncwarp();
 }
 
 // out = A v (TA: A^T v)
@@ -419,9 +523,17 @@ __device__ bool wapply_prefix(double* x, double (*P)[LD(D)], const SF<D>& a, SCo
     return ok;
 }
 
-// a (x)_s collapsed suffix (0, m, P) -> (E m + g, E P E^T + L) written into (m, P)
+// scratch of the suffix application (no inverse needed)
 template <int D>
-__device__ void wapply_suffix(const SS<D>& a, double* m, double (*P)[LD(D)], SCombF<D>& s, int lane) {
+struct SSufScratch {
+    double M[D][LD(D)];
+    double T1[D][LD(D)];
+    double v1[D];
+};
+
+// a (x)_s collapsed suffix (0, m, P) -> (E m + g, E P E^T + L) written into (m, P)
+template <int D, typename Scratch>
+__device__ void wapply_suffix(const SS<D>& a, double* m, double (*P)[LD(D)], Scratch& s, int lane) {
     wmm<D>(s.T1, a.E, P, nullptr, lane);
     for (int i = lane; i < D; i += 32) {
         double acc = a.g[i];
@@ -494,44 +606,24 @@ __global__ void __launch_bounds__(32 * kWWarps) kw_filter_fold(const WParams p) 
             if (kind == 2) raise_error(p.err, g, kErrUnsupported);
         }
         tprev = tk;
-        // FA = F A, T = F C, Fb = F b
-        for (int e = lane; e < D * D; e += 32) {
-            const int i = e / D, j = e - (e / D) * D;
-            double fa = 0.0, tt = 0.0;
-            if (kind == 0) {
-                for (int q = 0; q < D; ++q) {
-                    fa = fma(M.F[i][q], W.a.A[q][j], fa);
-                    tt = fma(M.F[i][q], W.a.C[q][j], tt);
-                }
-            } else if (kind == 1) {
-                fa = W.a.A[i][j];
-                tt = W.a.C[i][j];
-            }
-            W.FA[i][j] = fa;
-            W.T[i][j] = tt;
-        }
-        for (int i = lane; i < D; i += 32) {
-            double s = 0.0;
-            if (kind == 0)
+        // FA = F A, T = F C, Fb = F b, Cm = T F^T + Q   (kind 1: F = I, Q = 0; kind 3: F = 0, Q = P_inf)
+        if (kind == 0) {
+            wmm<D>(W.FA, M.F, W.a.A, nullptr, lane);
+            wmm<D>(W.T, M.F, W.a.C, nullptr, lane);
+            for (int i = lane; i < D; i += 32) {
+                double s = 0.0;
                 for (int q = 0; q < D; ++q) s = fma(M.F[i][q], W.a.b[q], s);
-            else if (kind == 1)
-                s = W.a.b[i];
-            W.Fb[i] = s;
-        }
-        __syncwarp();
-        // Cm = T F^T + Q  (kind 3: P_inf; kind 1: T)
-        for (int e = lane; e < D * D; e += 32) {
-            const int i = e / D, j = e - (e / D) * D;
-            double s;
-            if (kind == 0) {
-                s = M.Q[i][j];
-                for (int q = 0; q < D; ++q) s = fma(W.T[i][q], M.F[j][q], s);
-            } else if (kind == 1) {
-                s = W.T[i][j];
-            } else {
-                s = M.Pinf[i][j];
+                W.Fb[i] = s;
             }
-            W.Cm[i][j] = s;
+            __syncwarp();
+            wmm<D, false, true>(W.Cm, W.T, M.F, M.Q, lane);
+        } else {
+            for (int e = lane; e < D * D; e += 32) {
+                const int i = e / D, j = e - (e / D) * D;
+                W.FA[i][j] = (kind == 1) ? W.a.A[i][j] : 0.0;
+                W.Cm[i][j] = (kind == 1) ? W.a.C[i][j] : M.Pinf[i][j];
+            }
+            for (int i = lane; i < D; i += 32) W.Fb[i] = (kind == 1) ? W.a.b[i] : 0.0;
         }
         __syncwarp();
         // HC = Cm H^T ; w = (H FA)^T
@@ -615,11 +707,20 @@ template <int D>
 struct K3Smem {
     SModel<D> m;
     struct PerWarp {
-        SF<D> a;                      // scanned prefix of the previous chain (carry source)
-        SCombF<D> s;
-        double P[D][LD(D)], Pm[D][LD(D)], FP[D][LD(D)];
-        double Sg[D][LD(D)], Sm[D][LD(D)], P0[D][LD(D)];
-        double x[D], xm[D], x0[D], HP[D], SH[D];
+        double P[D][LD(D)];
+        double x[D];
+        union {
+            struct {                  // carry phase
+                SF<D> a;
+                SCombF<D> s;
+            } c;
+            struct {                  // step phase (+ chain smoother aggregate)
+                double Sg[D][LD(D)], P0[D][LD(D)], Sm[D][LD(D)], Pm[D][LD(D)], FP[D][LD(D)];
+                double xm[D], x0[D], HP[D], SH[D];
+                double W2[D][2 * D + 1];
+                SS<D> sagg;
+            } st;
+        } u;
     } w[kWWarps];
 };
 
@@ -639,12 +740,12 @@ __global__ void __launch_bounds__(32 * kWWarps) kw_filter_apply(const WParams p)
     for (int i = lane; i < D; i += 32) W.x[i] = 0.0;
     __syncwarp();
     for (int g = 0; g < p.rank && p.in_filt; ++g) {
-        gload<D>(W.a, p.in_filt + static_cast<int64_t>(g) * FNW(D), lane);
-        wapply_prefix<D>(W.x, W.P, W.a, W.s, lane);
+        gload<D>(W.u.c.a, p.in_filt + static_cast<int64_t>(g) * FNW(D), lane);
+        wapply_prefix<D>(W.x, W.P, W.u.c.a, W.u.c.s, lane);
     }
     if (c > 0) {
-        gload<D>(W.a, p.fagg + static_cast<int64_t>(c - 1) * FNW(D), lane);
-        if (!wapply_prefix<D>(W.x, W.P, W.a, W.s, lane) && lane == 0) raise_error(p.err, p.k0, kErrNumeric);
+        gload<D>(W.u.c.a, p.fagg + static_cast<int64_t>(c - 1) * FNW(D), lane);
+        if (!wapply_prefix<D>(W.x, W.P, W.u.c.a, W.u.c.s, lane) && lane == 0) raise_error(p.err, p.k0, kErrNumeric);
     }
     const int64_t kb = static_cast<int64_t>(c) * p.K;
     const int64_t ke = min(kb + p.K, p.n);
@@ -661,76 +762,57 @@ __global__ void __launch_bounds__(32 * kWWarps) kw_filter_apply(const WParams p)
         const bool first = (k == kb);
         tprev = tk;
         // predict: xm = F x, FP = F P, Pm = FP F^T + Q ; Sm = Sg F^T
-        for (int e = lane; e < D * D; e += 32) {
-            const int i = e / D, j = e - (e / D) * D;
-            double fp = 0.0, sm = 0.0;
-            if (kind == 0) {
-                for (int q = 0; q < D; ++q) {
-                    fp = fma(M.F[i][q], W.P[q][j], fp);
-                    sm = fma(W.Sg[i][q], M.F[j][q], sm);
-                }
-            } else if (kind == 1) {
-                fp = W.P[i][j];
-                sm = W.Sg[i][j];
-            }
-            W.FP[i][j] = fp;
-            W.Sm[i][j] = sm;
-        }
-        for (int i = lane; i < D; i += 32) {
-            double s = 0.0;
-            if (kind == 0)
+        if (kind == 0) {
+            wmm<D>(W.u.st.FP, M.F, W.P, nullptr, lane);
+            if (!first) wmm<D, false, true>(W.u.st.Sm, W.u.st.Sg, M.F, nullptr, lane);
+            for (int i = lane; i < D; i += 32) {
+                double s = 0.0;
                 for (int q = 0; q < D; ++q) s = fma(M.F[i][q], W.x[q], s);
-            else if (kind == 1)
-                s = W.x[i];
-            W.xm[i] = s;
-        }
-        __syncwarp();
-        for (int e = lane; e < D * D; e += 32) {
-            const int i = e / D, j = e - (e / D) * D;
-            double s;
-            if (kind == 0) {
-                s = M.Q[i][j];
-                for (int q = 0; q < D; ++q) s = fma(W.FP[i][q], M.F[j][q], s);
-            } else if (kind == 1) {
-                s = W.FP[i][j];
-            } else {
-                s = M.Pinf[i][j];
+                W.u.st.xm[i] = s;
             }
-            W.Pm[i][j] = s;
+            __syncwarp();
+            wmm<D, false, true>(W.u.st.Pm, W.u.st.FP, M.F, M.Q, lane);
+        } else {
+            for (int e = lane; e < D * D; e += 32) {
+                const int i = e / D, j = e - (e / D) * D;
+                W.u.st.Sm[i][j] = (kind == 1) ? W.u.st.Sg[i][j] : 0.0;
+                W.u.st.Pm[i][j] = (kind == 1) ? W.P[i][j] : M.Pinf[i][j];
+            }
+            for (int i = lane; i < D; i += 32) W.u.st.xm[i] = (kind == 1) ? W.x[i] : 0.0;
         }
         __syncwarp();
         for (int i = lane; i < D; i += 32) {
             double hp = 0.0, sh_ = 0.0;
             for (int q = 0; q < D; ++q) {
-                hp = fma(W.Pm[i][q], M.H[q], hp);
-                sh_ = fma(W.Sm[i][q], M.H[q], sh_);
+                hp = fma(W.u.st.Pm[i][q], M.H[q], hp);
+                sh_ = fma(W.u.st.Sm[i][q], M.H[q], sh_);
             }
-            W.HP[i] = hp;
-            W.SH[i] = sh_;
+            W.u.st.HP[i] = hp;
+            W.u.st.SH[i] = sh_;
         }
         __syncwarp();
-        const double S = wdot<D>(M.H, W.HP, lane) + M.r;
-        const double hx = wdot<D>(M.H, W.xm, lane);
+        const double S = wdot<D>(M.H, W.u.st.HP, lane) + M.r;
+        const double hx = wdot<D>(M.H, W.u.st.xm, lane);
         if (lane == 0 && obs && !(S > 0.0 && S < INFINITY)) raise_error(p.err, g, kErrNumeric);
         const double iS = obs ? 1.0 / S : 0.0;
         const double v = obs ? (yk - hx) : 0.0;
         const double vs = v * iS;
         for (int e = lane; e < D * D; e += 32) {
             const int i = e / D, j = e - (e / D) * D;
-            const double Pn = fma(-W.HP[i] * iS, W.HP[j], W.Pm[i][j]);
+            const double Pn = fma(-W.u.st.HP[i] * iS, W.u.st.HP[j], W.u.st.Pm[i][j]);
             W.P[i][j] = Pn;
             if (first) {
-                W.P0[i][j] = Pn;
-                W.Sg[i][j] = Pn;
+                W.u.st.P0[i][j] = Pn;
+                W.u.st.Sg[i][j] = Pn;
             } else {
-                W.Sg[i][j] = fma(-W.SH[i] * iS, W.HP[j], W.Sm[i][j]);
-                W.P0[i][j] = fma(-W.SH[i] * iS, W.SH[j], W.P0[i][j]);
+                W.u.st.Sg[i][j] = fma(-W.u.st.SH[i] * iS, W.u.st.HP[j], W.u.st.Sm[i][j]);
+                W.u.st.P0[i][j] = fma(-W.u.st.SH[i] * iS, W.u.st.SH[j], W.u.st.P0[i][j]);
             }
         }
         for (int i = lane; i < D; i += 32) {
-            const double xn = fma(W.HP[i], vs, W.xm[i]);
+            const double xn = fma(W.u.st.HP[i], vs, W.u.st.xm[i]);
             W.x[i] = xn;
-            W.x0[i] = first ? xn : fma(W.SH[i], vs, W.x0[i]);
+            W.u.st.x0[i] = first ? xn : fma(W.u.st.SH[i], vs, W.u.st.x0[i]);
         }
         if (obs) {
             quad = fma(v, vs, quad);
@@ -752,16 +834,16 @@ __global__ void __launch_bounds__(32 * kWWarps) kw_filter_apply(const WParams p)
     }
     if (!p.store_state) return;
     // ---- chain smoother aggregate (E, g, L), as in the d <= 3 path
-    SS<D>* sagg = reinterpret_cast<SS<D>*>(&W.a);   // reuse the carry scratch
+    SS<D>* sagg = &W.u.st.sagg;
     if (ke <= kb) {
         set_identity<D>(*sagg, lane);
     } else if (p.k0 + ke == p.nglob) {
         for (int e = lane; e < D * D; e += 32) {
             const int i = e / D, j = e - (e / D) * D;
             sagg->E[i][j] = 0.0;
-            sagg->L[i][j] = W.P0[i][j];
+            sagg->L[i][j] = W.u.st.P0[i][j];
         }
-        for (int i = lane; i < D; i += 32) sagg->g[i] = W.x0[i];
+        for (int i = lane; i < D; i += 32) sagg->g[i] = W.u.st.x0[i];
         __syncwarp();
     } else {
         const double tn = __ldg(p.t + ke);
@@ -773,14 +855,14 @@ __global__ void __launch_bounds__(32 * kWWarps) kw_filter_apply(const WParams p)
             if (kind == 0) {
                 for (int q = 0; q < D; ++q) {
                     fp = fma(M.F[i][q], W.P[q][j], fp);
-                    sm = fma(W.Sg[i][q], M.F[j][q], sm);
+                    sm = fma(W.u.st.Sg[i][q], M.F[j][q], sm);
                 }
             } else {
                 fp = W.P[i][j];
-                sm = W.Sg[i][j];
+                sm = W.u.st.Sg[i][j];
             }
-            W.FP[i][j] = fp;
-            W.Sm[i][j] = sm;
+            W.u.st.FP[i][j] = fp;
+            W.u.st.Sm[i][j] = sm;
         }
         for (int i = lane; i < D; i += 32) {
             double s = 0.0;
@@ -788,40 +870,40 @@ __global__ void __launch_bounds__(32 * kWWarps) kw_filter_apply(const WParams p)
                 for (int q = 0; q < D; ++q) s = fma(M.F[i][q], W.x[q], s);
             else
                 s = W.x[i];
-            W.xm[i] = s;
+            W.u.st.xm[i] = s;
         }
         __syncwarp();
         for (int e = lane; e < D * D; e += 32) {
             const int i = e / D, j = e - (e / D) * D;
             double s = (kind == 0) ? M.Q[i][j] : 0.0;
             if (kind == 0)
-                for (int q = 0; q < D; ++q) s = fma(W.FP[i][q], M.F[j][q], s);
+                for (int q = 0; q < D; ++q) s = fma(W.u.st.FP[i][q], M.F[j][q], s);
             else
-                s = W.FP[i][j];
-            W.Pm[i][j] = s;
+                s = W.u.st.FP[i][j];
+            W.u.st.Pm[i][j] = s;
         }
         __syncwarp();
-        // E = Sm Pm^-1 : invert Pm (into W.FP via winverse on a copy)
-        for (int e = lane; e < D * D; e += 32) W.FP[e / D][e % D] = W.Pm[e / D][e % D];
+        // E = Sm Pm^-1 : invert Pm (into W.u.st.FP via winverse on a copy)
+        for (int e = lane; e < D * D; e += 32) W.u.st.FP[e / D][e % D] = W.u.st.Pm[e / D][e % D];
         __syncwarp();
-        if (!winverse<D>(W.FP, W.s.W, lane) && lane == 0) raise_error(p.err, p.k0 + ke, kErrNumeric);
-        wmm<D>(sagg->E, W.Sm, W.FP, nullptr, lane);
+        if (!winverse<D>(W.u.st.FP, W.u.st.W2, lane) && lane == 0) raise_error(p.err, p.k0 + ke, kErrNumeric);
+        wmm<D>(sagg->E, W.u.st.Sm, W.u.st.FP, nullptr, lane);
         __syncwarp();
         for (int i = lane; i < D; i += 32) {
-            double a = W.x0[i];
-            for (int q = 0; q < D; ++q) a = fma(-sagg->E[i][q], W.xm[q], a);
+            double a = W.u.st.x0[i];
+            for (int q = 0; q < D; ++q) a = fma(-sagg->E[i][q], W.u.st.xm[q], a);
             sagg->g[i] = a;
         }
         for (int e = lane; e < D * D; e += 32) {
             const int i = e / D, j = e - (e / D) * D;
-            double a = W.P0[i][j];
-            for (int q = 0; q < D; ++q) a = fma(-sagg->E[i][q], W.Sm[j][q], a);
-            W.Pm[i][j] = a;
+            double a = W.u.st.P0[i][j];
+            for (int q = 0; q < D; ++q) a = fma(-sagg->E[i][q], W.u.st.Sm[j][q], a);
+            W.u.st.Pm[i][j] = a;
         }
         __syncwarp();
         for (int e = lane; e < D * D; e += 32) {
             const int i = e / D, j = e - (e / D) * D;
-            sagg->L[i][j] = 0.5 * (W.Pm[i][j] + W.Pm[j][i]);
+            sagg->L[i][j] = 0.5 * (W.u.st.Pm[i][j] + W.u.st.Pm[j][i]);
         }
         __syncwarp();
     }
@@ -833,11 +915,18 @@ template <int D>
 struct K5Smem {
     SModel<D> m;
     struct PerWarp {
-        SS<D> a;
-        SCombF<D> s;
-        double P[D][LD(D)], Pm[D][LD(D)], FP[D][LD(D)], G[D][LD(D)], T[D][LD(D)];
         double Ps[D][LD(D)];
-        double x[D], xm[D], ms[D], dm[D];
+        double ms[D];
+        union {
+            struct {                  // carry phase
+                SS<D> a;
+                SSufScratch<D> s;
+            } c;
+            struct {                  // step phase
+                double P[D][LD(D)], Pm[D][LD(D)], FP[D][LD(D)], G[D][LD(D)], T[D][LD(D)];
+                double x[D], xm[D], dm[D], Li[D];
+            } st;
+        } u;
     } w[kWWarps];
 };
 
@@ -868,12 +957,12 @@ __global__ void __launch_bounds__(32 * kWWarps) kw_smoother_apply(const WParams 
     for (int i = lane; i < D; i += 32) W.ms[i] = 0.0;
     __syncwarp();
     for (int g = p.world - 1; g > p.rank && p.in_smooth; --g) {
-        gload<D>(W.a, p.in_smooth + static_cast<int64_t>(g) * SNW(D), lane);
-        wapply_suffix<D>(W.a, W.ms, W.Ps, W.s, lane);
+        gload<D>(W.u.c.a, p.in_smooth + static_cast<int64_t>(g) * SNW(D), lane);
+        wapply_suffix<D>(W.u.c.a, W.ms, W.Ps, W.u.c.s, lane);
     }
     if (c + 1 < p.nch) {
-        gload<D>(W.a, p.sagg + static_cast<int64_t>(c + 1) * SNW(D), lane);
-        wapply_suffix<D>(W.a, W.ms, W.Ps, W.s, lane);
+        gload<D>(W.u.c.a, p.sagg + static_cast<int64_t>(c + 1) * SNW(D), lane);
+        wapply_suffix<D>(W.u.c.a, W.ms, W.Ps, W.u.c.s, lane);
     }
     const int64_t kb = static_cast<int64_t>(c) * p.K;
     const int64_t ke = min(kb + p.K, p.n);
@@ -883,81 +972,62 @@ __global__ void __launch_bounds__(32 * kWWarps) kw_smoother_apply(const WParams 
         const double tk = __ldg(p.t + k);
         const int64_t g = p.k0 + k;
         const double* src = xpc + (k - kb) * CNW(D);
-        for (int i = lane; i < D; i += 32) W.x[i] = src[i];
+        for (int i = lane; i < D; i += 32) W.u.st.x[i] = src[i];
         for (int e = lane; e < D * D; e += 32) {
             const int i = e / D, j = e - (e / D) * D;
-            W.P[i][j] = src[D + si(D, i, j)];
+            W.u.st.P[i][j] = src[D + si(D, i, j)];
         }
         __syncwarp();
         if (g == p.nglob - 1) {
-            for (int e = lane; e < D * D; e += 32) W.Ps[e / D][e % D] = W.P[e / D][e % D];
-            for (int i = lane; i < D; i += 32) W.ms[i] = W.x[i];
+            for (int e = lane; e < D * D; e += 32) W.Ps[e / D][e % D] = W.u.st.P[e / D][e % D];
+            for (int i = lane; i < D; i += 32) W.ms[i] = W.u.st.x[i];
             __syncwarp();
         } else {
             const int kind = wdisc_kind(tnext - tk, M.udt);
-            for (int e = lane; e < D * D; e += 32) {
-                const int i = e / D, j = e - (e / D) * D;
-                double fp = 0.0;
-                if (kind == 0)
-                    for (int q = 0; q < D; ++q) fp = fma(M.F[i][q], W.P[q][j], fp);
-                else
-                    fp = W.P[i][j];
-                W.FP[i][j] = fp;
-            }
-            for (int i = lane; i < D; i += 32) {
-                double s = 0.0;
-                if (kind == 0)
-                    for (int q = 0; q < D; ++q) s = fma(M.F[i][q], W.x[q], s);
-                else
-                    s = W.x[i];
-                W.xm[i] = s;
-            }
-            __syncwarp();
-            for (int e = lane; e < D * D; e += 32) {
-                const int i = e / D, j = e - (e / D) * D;
-                double s;
-                if (kind == 0) {
-                    s = M.Q[i][j];
-                    for (int q = 0; q < D; ++q) s = fma(W.FP[i][q], M.F[j][q], s);
-                } else {
-                    s = W.FP[i][j];
+            if (kind == 0) {
+                wmm<D>(W.u.st.FP, M.F, W.u.st.P, nullptr, lane);                       // F P
+                for (int i = lane; i < D; i += 32) {
+                    double s2 = 0.0;
+                    for (int q = 0; q < D; ++q) s2 = fma(M.F[i][q], W.u.st.x[q], s2);
+                    W.u.st.xm[i] = s2;
                 }
-                W.Pm[i][j] = s;
-                W.T[i][j] = s;
+                __syncwarp();
+                wmm<D, false, true>(W.u.st.Pm, W.u.st.FP, M.F, M.Q, lane);             // F P F^T + Q
+            } else {
+                for (int e = lane; e < D * D; e += 32) {
+                    const int i = e / D, j = e - (e / D) * D;
+                    W.u.st.FP[i][j] = W.u.st.P[i][j];
+                    W.u.st.Pm[i][j] = W.u.st.P[i][j];
+                }
+                for (int i = lane; i < D; i += 32) W.u.st.xm[i] = W.u.st.x[i];
             }
             __syncwarp();
-            // G = P F^T Pm^-1 = (Pm^-1 F P)^T
-            if (!winverse<D>(W.T, W.s.W, lane) && lane == 0) raise_error(p.err, g, kErrNumeric);
-            wmm<D, true, false>(W.G, W.FP, W.T, nullptr, lane);   // G = (F P)^T Pm^-1 = P F^T Pm^-1
-            __syncwarp();
-            // ms = x + G (ms - xm)
-            for (int i = lane; i < D; i += 32) W.dm[i] = W.ms[i] - W.xm[i];
+            // X = Pm^-1 F P (so G = P F^T Pm^-1 = X^T) by Cholesky, lanes over right-hand sides
+            if (!wcholesky<D>(W.u.st.Pm, W.u.st.T, W.u.st.Li, lane) && lane == 0) raise_error(p.err, g, kErrNumeric);
+            wchol_solve<D>(W.u.st.T, W.u.st.Li, W.u.st.FP, W.u.st.G, lane);                  // W.u.st.G holds X (not G)
+            // ms = x + X^T (ms - xm)
+            for (int i = lane; i < D; i += 32) W.u.st.dm[i] = W.ms[i] - W.u.st.xm[i];
             __syncwarp();
             for (int i = lane; i < D; i += 32) {
-                double s = W.x[i];
-                for (int q = 0; q < D; ++q) s = fma(W.G[i][q], W.dm[q], s);
-                W.xm[i] = s;
+                double s2 = W.u.st.x[i];
+                for (int q = 0; q < D; ++q) s2 = fma(W.u.st.G[q][i], W.u.st.dm[q], s2);
+                W.u.st.xm[i] = s2;
             }
-            // T = G (Ps - Pm)
+            // Ps = P + X^T (Ps - Pm) X
             for (int e = lane; e < D * D; e += 32) {
                 const int i = e / D, j = e - (e / D) * D;
-                double s = 0.0;
-                for (int q = 0; q < D; ++q) s = fma(W.G[i][q], W.Ps[q][j] - W.Pm[q][j], s);
-                W.T[i][j] = s;
+                W.u.st.Pm[i][j] = W.Ps[i][j] - W.u.st.Pm[i][j];
             }
+            __syncwarp();
+            wmm<D>(W.u.st.T, W.u.st.Pm, W.u.st.G, nullptr, lane);                 // (Ps - Pm) X
+            __syncwarp();
+            wmm<D, true, false>(W.u.st.FP, W.u.st.G, W.u.st.T, W.u.st.P, lane);        // P + X^T (Ps - Pm) X
             __syncwarp();
             for (int e = lane; e < D * D; e += 32) {
                 const int i = e / D, j = e - (e / D) * D;
-                double s = W.P[i][j];
-                for (int q = 0; q < D; ++q) s = fma(W.T[i][q], W.G[j][q], s);
-                W.FP[i][j] = s;
+                W.Ps[i][j] = 0.5 * (W.u.st.FP[i][j] + W.u.st.FP[j][i]);
             }
-            __syncwarp();
-            for (int e = lane; e < D * D; e += 32) {
-                const int i = e / D, j = e - (e / D) * D;
-                W.Ps[i][j] = 0.5 * (W.FP[i][j] + W.FP[j][i]);
-            }
-            for (int i = lane; i < D; i += 32) W.ms[i] = W.xm[i];
+            for (int i = lane; i < D; i += 32) W.ms[i] = W.u.st.xm[i];
             __syncwarp();
         }
         tnext = tk;
