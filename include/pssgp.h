@@ -64,18 +64,24 @@ typedef enum {
     PSSGP_MATERN32 = 2,       /* d = 2, exact                                                  */
     PSSGP_MATERN52 = 3,       /* d = 3, exact                                                  */
     PSSGP_RBF_TAYLOR = 4,     /* d = order, Taylor approximation of 1/S(w) */
-    PSSGP_PERIODIC = 5        /* d = 2 (order + 1) harmonic oscillators        */
+    PSSGP_PERIODIC = 5,       /* d = 2 (order + 1) harmonic oscillators        */
+    PSSGP_QUASIPERIODIC = 6   /* periodic(order) x Matern-(mat_nu2/2): d = 2 (order + 1) m,
+                                 m = (mat_nu2 + 1) / 2 (CO2 model) */
 } pssgp_kind;
 
 /* One additive component of the covariance (sum of components = block-diagonal
  * state).  variance = sigma^2 > 0, lengthscale > 0, period > 0
- * (periodic only), order >= 1 (RBF Taylor order / periodic harmonics J). */
+ * (periodic, quasi-periodic), order >= 1 (RBF Taylor order / periodic harmonics J).
+ * Quasi-periodic only: mat_lengthscale > 0 and mat_nu2 in {1, 3, 5} describe the
+ * Matern factor (unit variance; the product's variance is `variance`). */
 typedef struct {
     int kind;                 /* pssgp_kind */
     double variance;
     double lengthscale;
     double period;
     int order;
+    double mat_lengthscale;
+    int mat_nu2;
 } pssgp_component;
 
 typedef struct {

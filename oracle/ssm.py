@@ -122,6 +122,21 @@ def periodic(J: int, variance: float, lengthscale: float, period: float) -> SSM:
     return SSM(G, np.zeros((n, 1)), 0.0, H, Pinf)
 
 
+def quasiperiodic(J: int, variance: float, lengthscale: float, period: float, mat_nu2: int,
+                  mat_lengthscale: float) -> SSM:
+    """Product C_per(tau) C_mat(tau): Kronecker-sum drift
+    G = G_p (x) I + I (x) G_m, P_inf = P_p (x) P_m, L q L^T = P_p (x) W_m, H = H_p (x) H_m,
+    so that H e^{G tau} P_inf H^T = k_per(tau) k_mat(tau)."""
+    per = periodic(J, variance, lengthscale, period)
+    mat = matern(mat_nu2, 1.0, mat_lengthscale)
+    Ip, Im = np.eye(per.n), np.eye(mat.n)
+    G = np.kron(per.G, Im) + np.kron(Ip, mat.G)
+    P = np.kron(per.Pinf, mat.Pinf)
+    W = np.kron(per.Pinf, mat.W)
+    H = np.kron(per.H, mat.H)
+    return SSM(G, np.zeros((G.shape[0], 1)), 0.0, H, P, Wmat=W)
+
+
 def osborne(G: np.ndarray, max_sweeps: int = 100) -> np.ndarray:
     """Osborne balancing with powers of two (reading Z6): returns
     the diagonal of D such that D^-1 G D has comparable off-diagonal row and
@@ -194,6 +209,8 @@ def build(components, balance_model: bool = True) -> SSM:
             m.Pinf = lyapunov_vec(m.G, m.W)
         elif kind == "periodic":
             m = periodic(c.order, c.variance, c.lengthscale, c.period)
+        elif kind == "quasiperiodic":
+            m = quasiperiodic(c.order, c.variance, c.lengthscale, c.period, c.mat_nu2, c.mat_lengthscale)
         else:
             raise ValueError(kind)
         parts.append(m)
@@ -219,6 +236,11 @@ def kernel_value(c, tau: np.ndarray) -> np.ndarray:
         return s2 * np.exp(-0.5 * tau ** 2 / ell ** 2)
     if c.kind == "periodic":
         return s2 * np.exp(-2.0 * np.sin(np.pi * tau / c.period) ** 2 / ell ** 2)
+    if c.kind == "quasiperiodic":
+        per = s2 * np.exp(-2.0 * np.sin(np.pi * tau / c.period) ** 2 / ell ** 2)
+        a = math.sqrt(c.mat_nu2) * tau / c.mat_lengthscale
+        mat = {1: np.exp(-a), 3: (1.0 + a) * np.exp(-a), 5: (1.0 + a + a * a / 3.0) * np.exp(-a)}[c.mat_nu2]
+        return per * mat
     raise ValueError(c.kind)
 
 

@@ -59,7 +59,8 @@ def pssgp_create(components: Sequence, noise_var: float, uniform_dt: float = 0.0
     for i, c in enumerate(components):
         kind = KINDS[c.kind] if isinstance(c.kind, str) else int(c.kind)
         arr[i] = Component(kind, float(c.variance), float(c.lengthscale), float(getattr(c, "period", 1.0)),
-                           int(getattr(c, "order", 0)))
+                           int(getattr(c, "order", 0)), float(getattr(c, "mat_lengthscale", 1.0)),
+                           int(getattr(c, "mat_nu2", 3)))
     opt = Options(1 if balance else 0, int(device), float(uniform_dt), int(chain_len), int(blocks_per_sm))
     h = ctypes.c_void_p()
     st = lib().pssgp_create(arr, n, float(noise_var), ctypes.byref(opt), ctypes.byref(h))

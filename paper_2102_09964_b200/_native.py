@@ -21,7 +21,7 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
 
 PSSGP_OK, PSSGP_E_ARG, PSSGP_E_INPUT, PSSGP_E_NUMERIC, PSSGP_E_CUDA, PSSGP_E_NOMEM, PSSGP_E_UNSUPPORTED = range(7)
 STATUS_NAMES = {0: "OK", 1: "E_ARG", 2: "E_INPUT", 3: "E_NUMERIC", 4: "E_CUDA", 5: "E_NOMEM", 6: "E_UNSUPPORTED"}
-KINDS = {"matern12": 1, "matern32": 2, "matern52": 3, "rbf": 4, "periodic": 5}
+KINDS = {"matern12": 1, "matern32": 2, "matern52": 3, "rbf": 4, "periodic": 5, "quasiperiodic": 6}
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -48,7 +48,8 @@ class PssgpError(RuntimeError):
 
 class Component(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int), ("variance", ctypes.c_double), ("lengthscale", ctypes.c_double),
-                ("period", ctypes.c_double), ("order", ctypes.c_int)]
+                ("period", ctypes.c_double), ("order", ctypes.c_int), ("mat_lengthscale", ctypes.c_double),
+                ("mat_nu2", ctypes.c_int)]
 
 
 class Options(ctypes.Structure):

@@ -292,6 +292,32 @@ inline Ssm periodic(int J, ld s2, ld ell, ld period) {
     return m;
 }
 
+// Quasi-periodic product C_per(tau) C_mat(tau):
+// Kronecker-sum drift G = G_p (x) I_m + I_p (x) G_m, P_inf = P_p (x) P_m,
+// W = P_p (x) W_m, H = H_p (x) H_m  (e^{(A (+) B) t} = e^{A t} (x) e^{B t}).
+inline Ssm kron_product(const Ssm& p, const Ssm& q) {
+    Ssm m;
+    const int a = p.d, b = q.d, n = a * b;
+    m.d = n;
+    m.G = zeros(n); m.W = zeros(n); m.Pinf = zeros(n);
+    m.H.assign(n, 0.0L);
+    m.Dbal.assign(n, 1.0L);
+    for (int i = 0; i < a; ++i)
+        for (int k = 0; k < b; ++k) {
+            const int r = i * b + k;
+            m.H[r] = p.H[i] * q.H[k];
+            m.Dbal[r] = p.Dbal[i] * q.Dbal[k];
+            for (int j = 0; j < a; ++j)
+                for (int l = 0; l < b; ++l) {
+                    const int c = j * b + l;
+                    m.G[r * n + c] = p.G[i * a + j] * (k == l ? 1.0L : 0.0L) + (i == j ? 1.0L : 0.0L) * q.G[k * b + l];
+                    m.Pinf[r * n + c] = p.Pinf[i * a + j] * q.Pinf[k * b + l];
+                    m.W[r * n + c] = p.Pinf[i * a + j] * q.W[k * b + l];
+                }
+        }
+    return m;
+}
+
 inline Ssm block_sum(const std::vector<Ssm>& parts) {
     Ssm m;
     int n = 0;

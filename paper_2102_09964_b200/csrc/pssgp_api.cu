@@ -636,6 +636,16 @@ pssgp_status pssgp_create(const pssgp_component* comps, int n_comps, double nois
         } else if (k.kind == PSSGP_PERIODIC) {
             if (k.order < 0 || k.order > 32 || !(k.period > 0.0)) { delete m; return PSSGP_E_ARG; }
             part = ph::periodic(k.order, k.variance, k.lengthscale, k.period);
+        } else if (k.kind == PSSGP_QUASIPERIODIC) {
+            if (k.order < 0 || k.order > 16 || !(k.period > 0.0) || !(k.mat_lengthscale > 0.0) ||
+                (k.mat_nu2 != 1 && k.mat_nu2 != 3 && k.mat_nu2 != 5)) {
+                delete m;
+                return PSSGP_E_ARG;
+            }
+            ph::ld lam;
+            const ph::Ssm per = ph::periodic(k.order, k.variance, k.lengthscale, k.period);
+            const ph::Ssm mat = ph::matern((k.mat_nu2 + 1) / 2, 1.0L, k.mat_lengthscale, &lam);
+            part = ph::kron_product(per, mat);
         } else {
             delete m;
             return PSSGP_E_UNSUPPORTED;

@@ -31,11 +31,13 @@ SEED_NOISE, SEED_JITTER, SEED_MASK = 0, 1, 2
 @dataclass
 class Component:
     """One additive covariance component (kind names follow SPEC.md:109)."""
-    kind: str                    # 'matern12' | 'matern32' | 'matern52' | 'rbf' | 'periodic'
+    kind: str                    # 'matern12' | 'matern32' | 'matern52' | 'rbf' | 'periodic' | 'quasiperiodic'
     variance: float = 1.0
     lengthscale: float = 1.0
     period: float = 1.0
     order: int = 0               # RBF Taylor order / periodic harmonics J
+    mat_lengthscale: float = 1.0  # quasi-periodic: lengthscale of the Matern factor
+    mat_nu2: int = 3             # quasi-periodic: 2 nu of the Matern factor
 
 
 @dataclass
@@ -151,6 +153,20 @@ def config4(n: int = 2 ** 24, harmonics: int = 6) -> Workload:
     comps = [Component("periodic", 4.0, 1.0, period=52.0, order=harmonics),
              Component("matern32", 10.0, 20.0 * 52.0)]
     return Workload("C4", comps, 0.09, t, y, mask, uniform_dt=1.0)
+
+
+def co2_product(n: int = 3192, order: int = 2) -> Workload:
+    """The paper's CO2 model C_Per x C_Mat + C_Mat: quasi-periodic
+    (J harmonics x Matern-3/2) + Matern-3/2 trend, d = 4 (J + 1) + 2 = 10 / 14 / 18 for
+    J = 1 / 2 / 3; weekly grid in weeks (exact uniform dt = 1), 1/16 missing."""
+    t = np.arange(n, dtype=np.float64)
+    mask = (np.arange(n) % 16 != 15).astype(np.uint8)
+    y = _noisy(co2_like(t / 52.0), 0.3)
+    y = (y - y.mean()) / y.std()
+    y = _apply_mask(y, mask)
+    comps = [Component("quasiperiodic", 2.0, 1.0, period=52.0, order=order, mat_lengthscale=300.0, mat_nu2=3),
+             Component("matern32", 10.0, 1040.0)]
+    return Workload(f"co2_product_J{order}", comps, 0.09, t, y, mask, uniform_dt=1.0)
 
 
 def random_problem(seed: int, n: int, kind: str = "matern52", p_missing: float = 0.3,

@@ -250,3 +250,11 @@ def test_wide_virtual_sharding(cuda_device, world):
     assert np.max(np.abs(mean - ref_mean)) / np.max(np.abs(ref_mean)) < 1e-10
     assert np.max(np.abs(var - ref_var) / ref_var) < 1e-10
     assert abs(nll - ref_nll) < 1e-10 * abs(ref_nll)
+
+
+@pytest.mark.parametrize("order", [1, 2, 3])
+def test_co2_product_model(cuda_device, order):
+    """NEXT row f3: the paper's CO2 model C_Per x C_Mat + C_Mat, n_x = 10/14/18,
+    N = 3192 weekly points (the dataset size of PAPER.md:224)."""
+    w = synth.co2_product(n=3192, order=order)
+    assert_parity(w)

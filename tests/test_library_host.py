@@ -130,3 +130,14 @@ def test_aggregate_bytes():
     m = P.Model([synth.Component("rbf", 1.0, 0.5, order=6)], 0.1, uniform_dt=0.01)
     assert P.pssgp_aggregate_bytes(m.h, 0) == (3 * 36 + 12) * 8     # wide path: full matrices
     assert P.pssgp_aggregate_bytes(m.h, 1) == (2 * 36 + 6) * 8
+
+
+def test_quasiperiodic_model_matches_oracle():
+    for J in (1, 2, 3):
+        w = synth.co2_product(n=10, order=J)
+        m = P.Model(w.components, w.noise_var, uniform_dt=1.0)
+        assert m.state_dim == 4 * (J + 1) + 2
+        lm, s = _lib_ssm(m.h)
+        om = ossm.build(w.components)
+        taus = np.linspace(0, 200.0, 41)
+        np.testing.assert_allclose(ossm.ssm_kernel(lm, taus), ossm.ssm_kernel(om, taus), rtol=1e-10, atol=1e-12)

@@ -323,3 +323,38 @@ def test_input_errors():
     with pytest.raises(oracle.OracleError) as e:
         oracle.kf_rts(ssm.build(w.components), w.noise_var, t, w.y, w.mask)
     assert e.value.status == 2 and e.value.index == 20
+
+
+def test_quasiperiodic_kronecker_reconstruction():
+    """Quasi-periodic product: the Kronecker SSM reproduces
+    k_per(tau) * k_mat(tau) up to the periodic truncation, and n_x = 10 / 14 / 18 for the
+    CO2 model C_Per x C_Mat + C_Mat with J = 1 / 2 / 3."""
+    for J, nx in [(1, 10), (2, 14), (3, 18)]:
+        w = synth.co2_product(n=10, order=J)
+        m = ssm.build(w.components)
+        assert m.n == nx
+    comp = synth.Component("quasiperiodic", 2.0, 1.0, period=1.0, order=8, mat_lengthscale=3.0, mat_nu2=3)
+    m = ssm.build([comp])
+    taus = np.linspace(0, 4.0, 81)
+    np.testing.assert_allclose(ssm.ssm_kernel(m, taus), ssm.kernel_value(comp, taus), atol=2.0 * 1e-7)
+    # stationarity of the product model: G P + P G^T + W = 0
+    assert np.max(np.abs(m.G @ m.Pinf + m.Pinf @ m.G.T + m.W)) < 1e-12 * np.max(np.abs(m.W))
+
+
+def test_lemma1_quasiperiodic_ssm_kernel():
+    """Dense GP with the SSM-implied kernel pins the oracle on the product model."""
+    w = synth.co2_product(n=400, order=1)
+    m = ssm.build(w.components)
+    o = oracle.kf_rts(m, w.noise_var, w.t, w.y, w.mask)
+    lags = np.unique(np.abs(w.t[:, None] - w.t[None, :]))
+    kv = ssm.ssm_kernel(m, lags)
+
+    def kf(tau):
+        tau = np.abs(np.asarray(tau))
+        if tau.ndim == 1 and tau.shape[0] == 1 and tau[0] == 0.0:
+            return ssm.ssm_kernel(m, tau)
+        return kv[np.searchsorted(lags, tau)]
+    mean, var, nll = dense_gp.dense_gp(kf, w.t, w.y, w.mask, w.noise_var)
+    assert rel_err(o["mean"], mean) < 1e-8
+    assert var_err(o["var"], var) < 1e-8
+    assert abs(o["nll"] - nll) / abs(nll) < 1e-9
