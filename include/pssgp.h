@@ -129,6 +129,30 @@ pssgp_status pssgp_posterior_host(pssgp_model* m, int64_t N, const double* t, co
                                   const uint8_t* mask, double* mean, double* var, double* nll,
                                   void* stream);
 
+/* Merge sorted training times t_train[n_train] (with y_train) and sorted test
+ * times t_test[n_test] into one sorted grid (pipeline stage 4,
+ * P:171; test points = missing observations, supplement P:255): t_out, y_out
+ * (0 at test points), mask_out (1 train / 0 test) of n_train + n_test entries,
+ * and test_index[j] = position of test time j in the grid.  Training first on
+ * ties.  Device arrays, caller-owned.  Unsorted / non-finite times are reported
+ * by pssgp_check as PSSGP_E_INPUT (index n_train + j for test time j). */
+pssgp_status pssgp_merge_grid(pssgp_model* m, int64_t n_train, const double* t_train, const double* y_train,
+                              int64_t n_test, const double* t_test, double* t_out, double* y_out,
+                              uint8_t* mask_out, int64_t* test_index, void* stream);
+
+/* mean_test[j] = mean[test_index[j]], var_test[j] = var[test_index[j]] (either
+ * output may be NULL).  Device arrays. */
+pssgp_status pssgp_gather(pssgp_model* m, int64_t n_test, const int64_t* test_index, const double* mean,
+                          const double* var, double* mean_test, double* var_test, void* stream);
+
+/* The paper's prediction pipeline in one call: merge (handle-
+ * owned grid buffers), filter + smoother + NLL on the merged grid, gather the
+ * test outputs.  nll (device scalar, nullable) is the training NLL (test points
+ * are missing observations and do not contribute). */
+pssgp_status pssgp_predict(pssgp_model* m, int64_t n_train, const double* t_train, const double* y_train,
+                           int64_t n_test, const double* t_test, double* mean_test, double* var_test,
+                           double* nll, void* stream);
+
 /* Synchronise the handle's last stream and return the first device-detected
  * error (PSSGP_E_INPUT / PSSGP_E_NUMERIC / PSSGP_E_UNSUPPORTED) since the last
  * pssgp_check, or PSSGP_OK.  Clears the latched error. */

@@ -24,7 +24,8 @@ __all__ = ["Model", "PssgpError", "build", "lib", "pssgp_create", "pssgp_destroy
            "pssgp_nll", "pssgp_posterior_host", "pssgp_check", "pssgp_error_index", "pssgp_last_error",
            "pssgp_state_dim", "pssgp_get_ssm", "pssgp_debug_discretize", "pssgp_plan",
            "pssgp_aggregate_bytes", "pssgp_shard_filter_reduce", "pssgp_shard_filter_apply",
-           "pssgp_shard_smoother_apply", "pssgp_profile_enable", "pssgp_profile_read", "pssgp_profile_name"]
+           "pssgp_shard_smoother_apply", "pssgp_profile_enable", "pssgp_profile_read", "pssgp_profile_name",
+           "pssgp_merge_grid", "pssgp_gather", "pssgp_predict"]
 
 
 def _ptr(x) -> Optional[int]:
@@ -97,6 +98,22 @@ def pssgp_posterior_host(h, N, t: np.ndarray, y: np.ndarray, mask: np.ndarray, m
         return a.ctypes.data
     _raise(h, lib().pssgp_posterior_host(h, int(N), hp(t), hp(y), hp(mask), hp(mean), hp(var), hp(nll),
                                          _stream_ptr(stream)))
+
+
+def pssgp_merge_grid(h, n_train, t_train, y_train, n_test, t_test, t_out, y_out, mask_out, test_index,
+                     stream=None) -> None:
+    _raise(h, lib().pssgp_merge_grid(h, int(n_train), _ptr(t_train), _ptr(y_train), int(n_test), _ptr(t_test),
+                                     _ptr(t_out), _ptr(y_out), _ptr(mask_out), _ptr(test_index), _stream_ptr(stream)))
+
+
+def pssgp_gather(h, n_test, test_index, mean, var, mean_test, var_test, stream=None) -> None:
+    _raise(h, lib().pssgp_gather(h, int(n_test), _ptr(test_index), _ptr(mean), _ptr(var), _ptr(mean_test),
+                                 _ptr(var_test), _stream_ptr(stream)))
+
+
+def pssgp_predict(h, n_train, t_train, y_train, n_test, t_test, mean_test, var_test, nll, stream=None) -> None:
+    _raise(h, lib().pssgp_predict(h, int(n_train), _ptr(t_train), _ptr(y_train), int(n_test), _ptr(t_test),
+                                  _ptr(mean_test), _ptr(var_test), _ptr(nll), _stream_ptr(stream)))
 
 
 def pssgp_check(h) -> None:
@@ -224,6 +241,17 @@ class Model:
         nll = np.zeros(1) if nll is None else nll
         pssgp_posterior_host(self.h, N, t, y, mask, mean, var, nll)
         return mean, var, nll
+
+    def predict(self, t_train, y_train, t_test, stream=None):
+        """Merge test times (missing observations) into the training grid on the
+        device, run filter + smoother + NLL, return (mean_test, var_test, nll)."""
+        import torch
+        mt = torch.empty(int(t_test.shape[0]), dtype=torch.float64, device=t_train.device)
+        vt = torch.empty_like(mt)
+        nll = torch.zeros(1, dtype=torch.float64, device=t_train.device)
+        pssgp_predict(self.h, int(t_train.shape[0]), t_train, y_train, int(t_test.shape[0]), t_test, mt, vt, nll,
+                      stream)
+        return mt, vt, nll
 
     def check(self):
         pssgp_check(self.h)

@@ -51,6 +51,8 @@ struct pssgp_model {
     int wocc = 0;                         // wide path: resident CTAs / SM
     char* io = nullptr;                   // e2e device buffers
     size_t io_bytes = 0;
+    char* mg = nullptr;                   // pssgp_predict merged-grid buffers
+    size_t mg_bytes = 0;
     cudaStream_t last_stream = nullptr;
     int64_t err_index = -1;
     std::string last_err;
@@ -675,6 +677,7 @@ void pssgp_destroy(pssgp_model* m) {
     if (!m) return;
     if (m->ws) cudaFree(m->ws);
     if (m->io) cudaFree(m->io);
+    if (m->mg) cudaFree(m->mg);
     if (m->d_err) cudaFree(m->d_err);
     if (m->d_model) cudaFree(m->d_model);
     for (int s = 0; s < kSlots; ++s)
@@ -707,6 +710,67 @@ pssgp_status pssgp_nll(pssgp_model* m, int64_t N, const double* t, const double*
     m->last_stream = s;
     if (m->d > kMaxD) return wide_posterior_dispatch(m, N, t, y, mask, nullptr, nullptr, nll, s, false);
     DISPATCH_D(m, run_posterior<D_>(m, N, t, y, mask, nullptr, nullptr, nll, s, false));
+}
+
+pssgp_status pssgp_merge_grid(pssgp_model* m, int64_t n_train, const double* t_train, const double* y_train,
+                              int64_t n_test, const double* t_test, double* t_out, double* y_out,
+                              uint8_t* mask_out, int64_t* test_index, void* stream) {
+    if (!m) return PSSGP_E_ARG;
+    if (n_train < 0 || n_test < 0 || (n_train > 0 && (!t_train || !y_train)) || (n_test > 0 && (!t_test || !test_index)) ||
+        (n_train + n_test > 0 && (!t_out || !y_out || !mask_out)))
+        return fail(m, PSSGP_E_ARG, "bad merge arguments");
+    pssgp_status st = ensure_device(m);
+    if (st) return st;
+    auto s = static_cast<cudaStream_t>(stream);
+    m->last_stream = s;
+    const int64_t tot = n_train + n_test;
+    if (tot == 0) return PSSGP_OK;
+    const int64_t blocks = (tot + 255) / 256;
+    k_merge<<<static_cast<unsigned>(blocks), 256, 0, s>>>(n_train, t_train, y_train, n_test, t_test, t_out, y_out,
+                                                         mask_out, test_index, m->d_err);
+    LAUNCH_CHECK(m, "k_merge");
+    return PSSGP_OK;
+}
+
+pssgp_status pssgp_gather(pssgp_model* m, int64_t n_test, const int64_t* test_index, const double* mean,
+                          const double* var, double* mean_test, double* var_test, void* stream) {
+    if (!m) return PSSGP_E_ARG;
+    if (n_test < 0 || (n_test > 0 && !test_index)) return fail(m, PSSGP_E_ARG, "bad gather arguments");
+    if (n_test == 0) return PSSGP_OK;
+    auto s = static_cast<cudaStream_t>(stream);
+    k_gather<<<static_cast<unsigned>((n_test + 255) / 256), 256, 0, s>>>(n_test, test_index, mean, var, mean_test,
+                                                                          var_test);
+    LAUNCH_CHECK(m, "k_gather");
+    return PSSGP_OK;
+}
+
+pssgp_status pssgp_predict(pssgp_model* m, int64_t n_train, const double* t_train, const double* y_train,
+                           int64_t n_test, const double* t_test, double* mean_test, double* var_test, double* nll,
+                           void* stream) {
+    if (!m) return PSSGP_E_ARG;
+    pssgp_status st = ensure_device(m);
+    if (st) return st;
+    const size_t tot = static_cast<size_t>(n_train + n_test);
+    const size_t need = tot * (8 + 8 + 8 + 8 + 1) + static_cast<size_t>(n_test) * 8 + 64;
+    if (need > m->mg_bytes) {
+        if (m->mg) cudaFree(m->mg);
+        m->mg = nullptr;
+        m->mg_bytes = 0;
+        if (cudaMalloc(&m->mg, need) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(m, PSSGP_E_NOMEM, "cudaMalloc(merge buffers)");
+        }
+        m->mg_bytes = need;
+    }
+    double* tg = reinterpret_cast<double*>(m->mg);
+    double* yg = tg + tot;
+    double* mean = yg + tot;
+    double* var = mean + tot;
+    int64_t* idx = reinterpret_cast<int64_t*>(var + tot);
+    uint8_t* mk = reinterpret_cast<uint8_t*>(idx + n_test);
+    if ((st = pssgp_merge_grid(m, n_train, t_train, y_train, n_test, t_test, tg, yg, mk, idx, stream))) return st;
+    if ((st = pssgp_posterior(m, static_cast<int64_t>(tot), tg, yg, mk, mean, var, nll, stream))) return st;
+    return pssgp_gather(m, n_test, idx, mean, var, mean_test, var_test, stream);
 }
 
 pssgp_status pssgp_check(pssgp_model* m) {

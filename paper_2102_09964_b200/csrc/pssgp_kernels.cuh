@@ -933,3 +933,57 @@ __global__ void __launch_bounds__(kCarryThreads, 1) k_reduce_blocks(const double
 }
 
 }  // namespace pssgp
+
+namespace pssgp {
+// ------------------------------------------------------------------ test-time merge (stage 4)
+// Rank-based parallel merge of sorted training times (observed) and sorted test
+// times (missing): a training time goes to i + #{test < t_i}, a test time to
+// j + #{train <= s_j} (training first on ties, reading Z12), each rank by binary
+// search — span O(log(N + M)), work O((N + M) log).  Unsorted input -> error.
+__device__ __forceinline__ int64_t count_less(const double* __restrict__ a, int64_t n, double v, bool or_equal) {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        const double x = __ldg(a + mid);
+        if (or_equal ? (x <= v) : (x < v)) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(256) k_merge(int64_t n_tr, const double* __restrict__ t_tr,
+                                               const double* __restrict__ y_tr, int64_t n_te,
+                                               const double* __restrict__ t_te, double* __restrict__ t_out,
+                                               double* __restrict__ y_out, uint8_t* __restrict__ m_out,
+                                               int64_t* __restrict__ test_index, unsigned long long* err) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n_tr) {
+        const double v = __ldg(t_tr + i);
+        if (!isfinite(v) || (i > 0 && !(__ldg(t_tr + i - 1) <= v))) raise_error(err, i, kErrInput);
+        const int64_t dst = i + count_less(t_te, n_te, v, false);
+        t_out[dst] = v;
+        y_out[dst] = __ldg(y_tr + i);
+        m_out[dst] = 1;
+    } else if (i < n_tr + n_te) {
+        const int64_t j = i - n_tr;
+        const double v = __ldg(t_te + j);
+        if (!isfinite(v) || (j > 0 && !(__ldg(t_te + j - 1) <= v))) raise_error(err, n_tr + j, kErrInput);
+        const int64_t dst = j + count_less(t_tr, n_tr, v, true);
+        t_out[dst] = v;
+        y_out[dst] = 0.0;
+        m_out[dst] = 0;
+        test_index[j] = dst;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_gather(int64_t n_te, const int64_t* __restrict__ test_index,
+                                                const double* __restrict__ mean, const double* __restrict__ var,
+                                                double* __restrict__ mean_te, double* __restrict__ var_te) {
+    const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j < n_te) {
+        const int64_t k = __ldg(test_index + j);
+        if (mean_te) mean_te[j] = __ldg(mean + k);
+        if (var_te) var_te[j] = __ldg(var + k);
+    }
+}
+}  // namespace pssgp

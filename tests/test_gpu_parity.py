@@ -258,3 +258,39 @@ def test_co2_product_model(cuda_device, order):
     N = 3192 weekly points (the dataset size of PAPER.md:224)."""
     w = synth.co2_product(n=3192, order=order)
     assert_parity(w)
+
+
+def test_merge_grid_and_predict(cuda_device):
+    """NEXT row f4: device merge equals the stable sorted union (training
+    first on ties), and pssgp_predict equals the oracle on the merged grid."""
+    rng = np.random.default_rng(21)
+    t_tr = np.sort(rng.uniform(0, 4, 5000))
+    t_te = np.sort(np.concatenate([rng.uniform(-0.5, 4.5, 1500), t_tr[::97]]))   # includes exact ties
+    y_tr = synth.sinusoid(t_tr) + 0.1 * rng.standard_normal(t_tr.shape[0])
+    comps = [synth.Component("matern52", 1.0, 0.5)]
+    m = P.Model(comps, 0.01)
+    dev = "cuda:0"
+    T, Y, TE = (torch.from_numpy(a).to(dev) for a in (t_tr, y_tr, t_te))
+    n = t_tr.shape[0] + t_te.shape[0]
+    tg = torch.empty(n, dtype=torch.float64, device=dev); yg = torch.empty_like(tg)
+    mk = torch.empty(n, dtype=torch.uint8, device=dev); idx = torch.empty(t_te.shape[0], dtype=torch.int64, device=dev)
+    P.pssgp_merge_grid(m.h, t_tr.shape[0], T, Y, t_te.shape[0], TE, tg, yg, mk, idx)
+    m.check()
+    t_ref, m_ref, order = synth.merged_grid(t_tr, t_te)
+    np.testing.assert_array_equal(tg.cpu().numpy(), t_ref)
+    np.testing.assert_array_equal(mk.cpu().numpy(), m_ref)
+    pos = np.empty(n, np.int64); pos[order] = np.arange(n)
+    np.testing.assert_array_equal(idx.cpu().numpy(), pos[t_tr.shape[0]:])
+    mt, vt, nll = m.predict(T, Y, TE)
+    m.check()
+    y_ref = np.concatenate([y_tr, np.full(t_te.shape[0], np.nan)])[order]
+    o = oracle.posterior(synth.Workload("merged", comps, 0.01, t_ref, y_ref, m_ref))
+    om, ov = o["mean"][pos[t_tr.shape[0]:]], o["var"][pos[t_tr.shape[0]:]]
+    assert np.max(np.abs(mt.cpu().numpy() - om)) / np.max(np.abs(om)) < MEAN_TOL
+    assert np.max(np.abs(vt.cpu().numpy() - ov) / ov) < VAR_TOL
+    assert abs(float(nll.cpu()[0]) - o["nll"]) < NLL_TOL * abs(o["nll"])
+    tb = T.clone(); tb[10] = tb[9] - 1.0                                 # unsorted training times
+    P.pssgp_merge_grid(m.h, t_tr.shape[0], tb, Y, t_te.shape[0], TE, tg, yg, mk, idx)
+    with pytest.raises(P.PssgpError) as e:
+        m.check()
+    assert e.value.status == _native.PSSGP_E_INPUT and e.value.index == 10
