@@ -153,6 +153,20 @@ pssgp_status pssgp_predict(pssgp_model* m, int64_t n_train, const double* t_trai
                            int64_t n_test, const double* t_test, double* mean_test, double* var_test,
                            double* nll, void* stream);
 
+/* Batched independent problems: nseg series concatenated
+ * along the time axis, series b = steps [offsets[b], offsets[b+1]) (offsets: device
+ * int64[nseg + 1], offsets[0] = 0, offsets[nseg] = N, non-decreasing; empty series
+ * allowed).  Times must be non-decreasing within a series; each series restarts
+ * from the stationary prior (its first element is Eq. (7)'s).  Per-series Matern
+ * hyper-parameters variance[b], lengthscale[b], noise_var[b] (device fp64 arrays;
+ * NULL = the model's value).  Outputs mean[N], var[N] (device) and nll[nseg]
+ * (device, per-series NLL, fixed-order sums).  Only single-component Matern
+ * models (closed-form discretisation) -> else PSSGP_E_UNSUPPORTED. */
+pssgp_status pssgp_posterior_batched(pssgp_model* m, int nseg, const int64_t* offsets, const double* variance,
+                                     const double* lengthscale, const double* noise_var, int64_t N,
+                                     const double* t, const double* y, const uint8_t* mask, double* mean,
+                                     double* var, double* nll, void* stream);
+
 /* Synchronise the handle's last stream and return the first device-detected
  * error (PSSGP_E_INPUT / PSSGP_E_NUMERIC / PSSGP_E_UNSUPPORTED) since the last
  * pssgp_check, or PSSGP_OK.  Clears the latched error. */

@@ -25,7 +25,7 @@ __all__ = ["Model", "PssgpError", "build", "lib", "pssgp_create", "pssgp_destroy
            "pssgp_state_dim", "pssgp_get_ssm", "pssgp_debug_discretize", "pssgp_plan",
            "pssgp_aggregate_bytes", "pssgp_shard_filter_reduce", "pssgp_shard_filter_apply",
            "pssgp_shard_smoother_apply", "pssgp_profile_enable", "pssgp_profile_read", "pssgp_profile_name",
-           "pssgp_merge_grid", "pssgp_gather", "pssgp_predict"]
+           "pssgp_merge_grid", "pssgp_gather", "pssgp_predict", "pssgp_posterior_batched"]
 
 
 def _ptr(x) -> Optional[int]:
@@ -114,6 +114,13 @@ def pssgp_gather(h, n_test, test_index, mean, var, mean_test, var_test, stream=N
 def pssgp_predict(h, n_train, t_train, y_train, n_test, t_test, mean_test, var_test, nll, stream=None) -> None:
     _raise(h, lib().pssgp_predict(h, int(n_train), _ptr(t_train), _ptr(y_train), int(n_test), _ptr(t_test),
                                   _ptr(mean_test), _ptr(var_test), _ptr(nll), _stream_ptr(stream)))
+
+
+def pssgp_posterior_batched(h, nseg, offsets, variance, lengthscale, noise_var, N, t, y, mask, mean, var, nll,
+                            stream=None) -> None:
+    _raise(h, lib().pssgp_posterior_batched(h, int(nseg), _ptr(offsets), _ptr(variance), _ptr(lengthscale),
+                                            _ptr(noise_var), int(N), _ptr(t), _ptr(y), _ptr(mask), _ptr(mean),
+                                            _ptr(var), _ptr(nll), _stream_ptr(stream)))
 
 
 def pssgp_check(h) -> None:

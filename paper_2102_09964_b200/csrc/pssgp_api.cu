@@ -13,6 +13,7 @@
 #include "host_model.hpp"
 #include "pssgp_kernels.cuh"
 #include "pssgp_wide.cuh"
+#include "pssgp_batch.cuh"
 
 using namespace pssgp;
 namespace ph = pssgp_host;
@@ -53,6 +54,8 @@ struct pssgp_model {
     size_t io_bytes = 0;
     char* mg = nullptr;                   // pssgp_predict merged-grid buffers
     size_t mg_bytes = 0;
+    double* bt = nullptr;                 // batched: per-step NLL terms
+    size_t bt_bytes = 0;
     cudaStream_t last_stream = nullptr;
     int64_t err_index = -1;
     std::string last_err;
@@ -678,6 +681,7 @@ void pssgp_destroy(pssgp_model* m) {
     if (m->ws) cudaFree(m->ws);
     if (m->io) cudaFree(m->io);
     if (m->mg) cudaFree(m->mg);
+    if (m->bt) cudaFree(m->bt);
     if (m->d_err) cudaFree(m->d_err);
     if (m->d_model) cudaFree(m->d_model);
     for (int s = 0; s < kSlots; ++s)
@@ -754,6 +758,7 @@ pssgp_status pssgp_predict(pssgp_model* m, int64_t n_train, const double* t_trai
     const size_t need = tot * (8 + 8 + 8 + 8 + 1) + static_cast<size_t>(n_test) * 8 + 64;
     if (need > m->mg_bytes) {
         if (m->mg) cudaFree(m->mg);
+    if (m->bt) cudaFree(m->bt);
         m->mg = nullptr;
         m->mg_bytes = 0;
         if (cudaMalloc(&m->mg, need) != cudaSuccess) {
@@ -771,6 +776,68 @@ pssgp_status pssgp_predict(pssgp_model* m, int64_t n_train, const double* t_trai
     if ((st = pssgp_merge_grid(m, n_train, t_train, y_train, n_test, t_test, tg, yg, mk, idx, stream))) return st;
     if ((st = pssgp_posterior(m, static_cast<int64_t>(tot), tg, yg, mk, mean, var, nll, stream))) return st;
     return pssgp_gather(m, n_test, idx, mean, var, mean_test, var_test, stream);
+}
+
+pssgp_status pssgp_posterior_batched(pssgp_model* m, int nseg, const int64_t* offsets, const double* variance,
+                                     const double* lengthscale, const double* noise_var, int64_t N,
+                                     const double* t, const double* y, const uint8_t* mask, double* mean,
+                                     double* var, double* nll, void* stream) {
+    pssgp_status st = check_args(m, N, t, y, mask);
+    if (st) return st;
+    if (nseg < 1 || !offsets || !nll) return fail(m, PSSGP_E_ARG, "bad batched arguments");
+    if (!m->closed) return fail(m, PSSGP_E_UNSUPPORTED, "batched mode needs a single closed-form Matern model");
+    if ((st = ensure_device(m))) return st;
+    auto s = static_cast<cudaStream_t>(stream);
+    m->last_stream = s;
+    const size_t need = static_cast<size_t>(std::max<int64_t>(N, 1)) * sizeof(double);
+    if (need > m->bt_bytes) {
+        if (m->bt) cudaFree(m->bt);
+        m->bt = nullptr;
+        m->bt_bytes = 0;
+        if (cudaMalloc(&m->bt, need) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(m, PSSGP_E_NOMEM, "cudaMalloc(batched)");
+        }
+        m->bt_bytes = need;
+    }
+    pssgp::batch::BParams q;
+    q.off = offsets;
+    q.nseg = nseg;
+    q.var = variance;
+    q.ell = lengthscale;
+    q.noise = noise_var;
+    q.sqrt2nu = std::sqrt(2.0 * m->d - 1.0);
+    q.nll_step = m->bt;
+    q.nll_seg = nll;
+    if (N > 0) {
+        switch (m->d) {
+#define BATCH_RUN(DD)                                                                                   \
+    case DD: {                                                                                          \
+        const Plan pl = make_plan<DD>(m, N);                                                            \
+        KParams<DD> p;                                                                                  \
+        if ((st = setup<DD>(m, pl, p))) return st;                                                      \
+        p.t = t; p.y = y; p.mask = mask; p.n = N; p.k0 = 0; p.nglob = N; p.mean = mean; p.var = var;    \
+        { ProfScope ps(m, S_K1, s); pssgp::batch::k_batch_filter_reduce<DD><<<pl.nb, kThreads, 0, s>>>(p, q); } \
+        LAUNCH_CHECK(m, "k_batch_filter_reduce");                                                       \
+        { ProfScope ps(m, S_K3, s); pssgp::batch::k_batch_filter_apply<DD><<<pl.nb, kThreads, 0, s>>>(p, q); } \
+        LAUNCH_CHECK(m, "k_batch_filter_apply");                                                        \
+        { ProfScope ps(m, S_K5, s); pssgp::batch::k_batch_smoother_apply<DD><<<pl.nb, kThreads, 0, s>>>(p, q); } \
+        LAUNCH_CHECK(m, "k_batch_smoother_apply");                                                      \
+        break;                                                                                          \
+    }
+            BATCH_RUN(1) BATCH_RUN(2) BATCH_RUN(3)
+#undef BATCH_RUN
+            default: return fail(m, PSSGP_E_UNSUPPORTED, "state dimension");
+        }
+    } else {
+        cudaMemsetAsync(m->bt, 0, sizeof(double), s);
+    }
+    {
+        ProfScope ps(m, S_K6, s);
+        pssgp::batch::k_batch_nll<<<(nseg + 3) / 4, 128, 0, s>>>(q);
+    }
+    LAUNCH_CHECK(m, "k_batch_nll");
+    return PSSGP_OK;
 }
 
 pssgp_status pssgp_check(pssgp_model* m) {

@@ -1,0 +1,329 @@
+// pssgp_batch.cuh — batched independent problems (NEXT row f2).
+//
+// B independent series, concatenated along the time axis (offsets[b]..offsets[b+1]),
+// each with its own Matern hyper-parameters (sigma_b^2, ell_b, sigma_n,b^2): the
+// multi-start / HMC workloads of PAPER.md:206, 224 in one launch.  No new algebra
+// is needed: the first element of every series has A = 0 (Eq. (7)), so the forward
+// scan's carry cannot cross a series start, and the terminal element of every series
+// has E = 0, so the reverse scan's carry cannot cross a series end — the three-pass
+// kernels of pssgp_kernels.cuh apply unchanged to the concatenation, with
+//   * series starts handled like the global first step (F = 0, Q = P_inf,b),
+//   * series ends like the global terminal (chain smoother aggregate (0, m^s, P^s),
+//     RTS reset m^s = xbar, P^s = P),
+//   * per-series discretisation (lambda_b, sigma_b^2) and noise r_b,
+//   * per-step NLL terms reduced per series in fixed order (deterministic).
+// Closed-form Matern models (d <= 3) only; per-step work is the d <= 3 path's.
+#pragma once
+#include "pssgp_kernels.cuh"
+
+namespace pssgp {
+namespace batch {
+
+struct BParams {
+    const int64_t* off;     // [nseg + 1] series offsets (global step indices), off[0] = 0, off[nseg] = N
+    int nseg;
+    const double* var;      // [nseg] sigma_b^2 (nullable: model's)
+    const double* ell;      // [nseg] lengthscale (nullable: model's)
+    const double* noise;    // [nseg] sigma_n,b^2 (nullable: model's)
+    double sqrt2nu;         // sqrt(2 nu) of the model's Matern order
+    double* nll_step;       // [N] per-step NLL terms
+    double* nll_seg;        // [nseg] per-series NLL
+};
+
+struct Seg {
+    int b;
+    int64_t start, end;     // [start, end)
+    double lam, s2, r, pscale;
+};
+
+template <int D>
+__device__ __forceinline__ void seg_load(Seg& s, const KParams<D>& p, const BParams& q, int b) {
+    s.b = b;
+    s.start = __ldg(q.off + b);
+    s.end = __ldg(q.off + b + 1);
+    s.s2 = q.var ? __ldg(q.var + b) : p.m.s2;
+    s.lam = q.ell ? q.sqrt2nu / __ldg(q.ell + b) : p.m.lam;
+    s.r = q.noise ? __ldg(q.noise + b) : p.m.r;
+    s.pscale = s.s2 / p.m.s2;           // P_inf is proportional to sigma^2 in the lambda basis
+}
+
+// series containing global step k (largest b with off[b] <= k)
+__device__ __forceinline__ int seg_find(const BParams& q, int64_t k) {
+    int lo = 0, hi = q.nseg - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (__ldg(q.off + mid) <= k) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+template <int D>
+__device__ __forceinline__ void seg_first(const KParams<D>& p, const Seg& s, double (&F)[D * D], double (&Q)[ns(D)]) {
+#pragma unroll
+    for (int i = 0; i < D * D; ++i) F[i] = 0.0;
+#pragma unroll
+    for (int i = 0; i < ns(D); ++i) Q[i] = p.m.Pinf[i] * s.pscale;
+}
+
+// ------------------------------------------------------------------ K1b: fold
+template <int D>
+__global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_filter_reduce(const KParams<D> p, const BParams q) {
+    __shared__ FAgg<D> wagg[kWarps];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t c = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
+    const int64_t nch = static_cast<int64_t>(p.nb) * kThreads;
+    const int64_t kb = c * p.K;
+    const int64_t ke = min(kb + p.K, p.n);
+    FAgg<D> a;
+    set_identity(a);
+    ModelParams<D> mp = p.m;
+    Seg s;
+    if (kb < ke) seg_load(s, p, q, seg_find(q, kb));
+    double tprev = (kb > 0 && kb < ke) ? __ldg(p.t + kb - 1) : 0.0;
+#pragma unroll 1
+    for (int64_t k = kb; k < ke; ++k) {
+        while (k >= s.end) seg_load(s, p, q, s.b + 1);
+        const double tk = __ldg(p.t + k);
+        const bool obs = __ldg(p.mask + k) != 0;
+        const double yk = obs ? __ldg(p.y + k) : 0.0;
+        double F[D * D], Q[ns(D)];
+        if (k == s.start) {
+            seg_first(p, s, F, Q);
+        } else {
+            if (!(tk - tprev >= 0.0)) raise_error(p.err, k, kErrInput);
+            matern_closed<D>(s.lam, s.s2, tk - tprev, F, Q);
+        }
+        if (!isfinite(tk) || (obs && !isfinite(yk))) raise_error(p.err, k, kErrInput);
+        mp.r = s.r;
+        fold_step<D>(a, F, Q, mp, obs, yk);
+        tprev = tk;
+    }
+    store_soa(a, p.chain_f, nch, c);
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        FAgg<D> o;
+        shfl_down_all(o, a, off);
+        if ((lane & (2 * off - 1)) == 0) {
+            FAgg<D> r;
+            combine(a, o, r);
+            a = r;
+        }
+    }
+    if (lane == 0) wagg[wid] = a;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        FAgg<D> acc = wagg[0];
+        for (int w = 1; w < kWarps; ++w) {
+            FAgg<D> r;
+            combine(acc, wagg[w], r);
+            acc = r;
+        }
+        store_aos(acc, p.block_f + static_cast<int64_t>(blockIdx.x) * FN(D));
+    }
+}
+
+// ------------------------------------------------------------------ K3b: Kalman rescan
+template <int D>
+__global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_filter_apply(const KParams<D> p, const BParams q) {
+    __shared__ FAgg<D> tot[kWarps];
+    __shared__ Gauss<D> wcar[kWarps];
+    __shared__ SAgg<D> stot[kWarps];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t c = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
+    const int64_t nch = static_cast<int64_t>(p.nb) * kThreads;
+    const int64_t wg = static_cast<int64_t>(blockIdx.x) * kWarps + wid;
+    const int64_t kb = c * p.K;
+    const int64_t ke = min(kb + p.K, p.n);
+    const Gauss<D> cur = filter_chain_carry<D>(p, tot, wcar, c, nch, lane, wid);
+    double x[D], P[ns(D)], x0[D], P0[ns(D)], Sg[D * D];
+#pragma unroll
+    for (int i = 0; i < D; ++i) x[i] = cur.x[i];
+#pragma unroll
+    for (int i = 0; i < ns(D); ++i) P[i] = cur.P[i];
+    ModelParams<D> mp = p.m;
+    Seg s;
+    if (kb < ke) seg_load(s, p, q, seg_find(q, kb));
+    double tprev = (kb > 0 && kb < ke) ? __ldg(p.t + kb - 1) : 0.0;
+    SAgg<D> sag;
+    set_identity(sag);
+    bool sag_done = false;
+#pragma unroll 1
+    for (int64_t k = kb; k < ke; ++k) {
+        while (k >= s.end) seg_load(s, p, q, s.b + 1);
+        const double tk = __ldg(p.t + k);
+        const bool obs = __ldg(p.mask + k) != 0;
+        const double yk = obs ? __ldg(p.y + k) : 0.0;
+        const bool first = (k == kb);
+        double F[D * D], Q[ns(D)], xm[D], Pm[ns(D)], FP[D * D];
+        if (k == s.start) seg_first(p, s, F, Q);
+        else matern_closed<D>(s.lam, s.s2, tk - tprev, F, Q);
+        kf_predict<D>(x, P, F, Q, xm, FP, Pm);
+        tprev = tk;
+        mp.r = s.r;
+        double HP[D], S, hx;
+        obs_terms<D>(mp, xm, Pm, HP, S, hx);
+        if (obs && !(S > 0.0 && S < INFINITY)) raise_error(p.err, k, kErrNumeric);
+        const double iS = obs ? rcp(S) : 0.0;
+        const double v = obs ? (yk - hx) : 0.0;
+        const double vs = v * iS;
+#pragma unroll
+        for (int i = 0; i < D; ++i) x[i] = fma(HP[i], vs, xm[i]);
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+            for (int j = i; j < D; ++j) P[si(D, i, j)] = fma(-HP[i] * iS, HP[j], Pm[si(D, i, j)]);
+        if (first) {
+#pragma unroll
+            for (int i = 0; i < D; ++i) x0[i] = x[i];
+#pragma unroll
+            for (int i = 0; i < ns(D); ++i) P0[i] = P[i];
+#pragma unroll
+            for (int i = 0; i < D; ++i)
+#pragma unroll
+                for (int j = 0; j < D; ++j) Sg[i * D + j] = P[si(D, i, j)];
+        } else {
+            double Sm[D * D], SH[D];
+#pragma unroll
+            for (int i = 0; i < D; ++i)
+#pragma unroll
+                for (int j = 0; j < D; ++j) {
+                    double s2 = 0.0;
+#pragma unroll
+                    for (int l = 0; l < D; ++l) s2 = fma(Sg[i * D + l], F[j * D + l], s2);
+                    Sm[i * D + j] = s2;
+                }
+#pragma unroll
+            for (int i = 0; i < D; ++i) SH[i] = Sm[i * D];          // H = e_0 (lambda basis)
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+                const double si_ = SH[i] * iS;
+#pragma unroll
+                for (int j = 0; j < D; ++j) Sg[i * D + j] = fma(-si_, HP[j], Sm[i * D + j]);
+                x0[i] = fma(SH[i], vs, x0[i]);
+#pragma unroll
+                for (int j = i; j < D; ++j) P0[si(D, i, j)] = fma(-si_, SH[j], P0[si(D, i, j)]);
+            }
+        }
+        q.nll_step[k] = obs ? 0.5 * (log(S) + 1.8378770664093453 + v * vs) : 0.0;
+        if (k == s.end - 1 && !sag_done) {
+            // first series end in this chain: the chain's smoother aggregate is the collapsed
+            // (0, m^s_k0, P^s_k0) of that series (terminal element)
+#pragma unroll
+            for (int i = 0; i < D * D; ++i) sag.E[i] = 0.0;
+#pragma unroll
+            for (int i = 0; i < D; ++i) sag.g[i] = x0[i];
+#pragma unroll
+            for (int i = 0; i < ns(D); ++i) sag.L[i] = P0[i];
+            sag_done = true;
+        }
+        double* o = p.xp + ((wg * p.K + (k - kb)) * CN(D)) * 32 + lane;
+#pragma unroll
+        for (int i = 0; i < D; ++i) o[i * 32] = x[i];
+#pragma unroll
+        for (int i = 0; i < ns(D); ++i) o[(D + i) * 32] = P[i];
+    }
+    if (ke > kb && !sag_done) {
+        // the next step exists and belongs to the same series (a series end would have set sag)
+        const double tn = __ldg(p.t + ke);
+        double F[D * D], Q[ns(D)], xm[D], Pm[ns(D)], FP[D * D], Sm[D * D];
+        matern_closed<D>(s.lam, s.s2, tn - tprev, F, Q);
+        kf_predict<D>(x, P, F, Q, xm, FP, Pm);
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                double s2 = 0.0;
+#pragma unroll
+                for (int l = 0; l < D; ++l) s2 = fma(Sg[i * D + l], F[j * D + l], s2);
+                Sm[i * D + j] = s2;
+            }
+        if (!chain_smoother_agg<D>(x0, P0, Sm, xm, Pm, sag)) raise_error(p.err, ke, kErrNumeric);
+    }
+    store_soa(sag, p.chain_s, nch, c);
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        SAgg<D> o;
+        shfl_down_all(o, sag, off);
+        if ((lane & (2 * off - 1)) == 0) {
+            SAgg<D> r;
+            combine(sag, o, r);
+            sag = r;
+        }
+    }
+    if (lane == 0) stot[wid] = sag;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        SAgg<D> acc = stot[0];
+        for (int w = 1; w < kWarps; ++w) {
+            SAgg<D> r;
+            combine(acc, stot[w], r);
+            acc = r;
+        }
+        store_aos(acc, p.block_s + static_cast<int64_t>(blockIdx.x) * SN(D));
+    }
+}
+
+// ------------------------------------------------------------------ K5b: RTS rescan
+template <int D>
+__global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_smoother_apply(const KParams<D> p, const BParams q) {
+    __shared__ SAgg<D> tot[kWarps];
+    __shared__ Gauss<D> wcar[kWarps + 1];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t c = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
+    const int64_t nch = static_cast<int64_t>(p.nb) * kThreads;
+    const int64_t wg = static_cast<int64_t>(blockIdx.x) * kWarps + wid;
+    const int64_t kb = c * p.K;
+    const int64_t ke = min(kb + p.K, p.n);
+    const Gauss<D> cur = smoother_chain_carry<D>(p, tot, wcar, c, nch, lane, wid);
+    double ms[D], Ps[ns(D)];
+#pragma unroll
+    for (int i = 0; i < D; ++i) ms[i] = cur.x[i];
+#pragma unroll
+    for (int i = 0; i < ns(D); ++i) Ps[i] = cur.P[i];
+    if (ke <= kb) return;
+    Seg s;
+    seg_load(s, p, q, seg_find(q, ke - 1));
+    double tnext = (ke < p.n) ? __ldg(p.t + ke) : 0.0;
+#pragma unroll 1
+    for (int64_t k = ke - 1; k >= kb; --k) {
+        while (k < s.start) seg_load(s, p, q, s.b - 1);
+        const double tk = __ldg(p.t + k);
+        const double* src = p.xp + ((wg * p.K + (k - kb)) * CN(D)) * 32 + lane;
+        double x[D], P[ns(D)];
+#pragma unroll
+        for (int i = 0; i < D; ++i) x[i] = src[i * 32];
+#pragma unroll
+        for (int i = 0; i < ns(D); ++i) P[i] = src[(D + i) * 32];
+        if (k == s.end - 1) {
+#pragma unroll
+            for (int i = 0; i < D; ++i) ms[i] = x[i];
+#pragma unroll
+            for (int i = 0; i < ns(D); ++i) Ps[i] = P[i];
+        } else {
+            double F[D * D], Q[ns(D)], xm[D], Pm[ns(D)], FP[D * D];
+            matern_closed<D>(s.lam, s.s2, tnext - tk, F, Q);
+            kf_predict<D>(x, P, F, Q, xm, FP, Pm);
+            if (!rts_step<D>(x, P, xm, Pm, FP, ms, Ps)) raise_error(p.err, k, kErrNumeric);
+        }
+        tnext = tk;
+        if (p.mean) p.mean[k] = ms[0];
+        if (p.var) p.var[k] = Ps[0];
+    }
+}
+
+// ------------------------------------------------------------------ per-series NLL (1 warp per series)
+__global__ void __launch_bounds__(128) k_batch_nll(const BParams q) {
+    const int lane = threadIdx.x & 31;
+    const int b = blockIdx.x * 4 + (threadIdx.x >> 5);
+    if (b >= q.nseg) return;
+    const int64_t a0 = __ldg(q.off + b), a1 = __ldg(q.off + b + 1);
+    double s = 0.0;
+    for (int64_t k = a0 + lane; k < a1; k += 32) s += q.nll_step[k];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
+    if (lane == 0) q.nll_seg[b] = s;
+}
+
+}  // namespace batch
+}  // namespace pssgp

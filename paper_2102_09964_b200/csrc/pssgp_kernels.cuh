@@ -379,22 +379,11 @@ __device__ __forceinline__ void nll_accumulate(bool obs, double v, double vs, do
     nobs += obs ? 1 : 0;
 }
 
-// ------------------------------------------------------------------ K3: Kalman rescan
-template <int D, int MODE>
-__global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KParams<D> p) {
-    __shared__ AsyncStage st[kWarps];
-    __shared__ FAgg<D> tot[kWarps];
-    __shared__ Gauss<D> wcar[kWarps];
-    __shared__ SAgg<D> stot[kWarps];
-    __shared__ double nred[kWarps];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int64_t c = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
-    const int64_t nch = static_cast<int64_t>(p.nb) * kThreads;
-    const int64_t wg = static_cast<int64_t>(blockIdx.x) * kWarps + wid;
-    const int64_t wbase = wg * 32 * p.K;
-    const int64_t kb = c * p.K;
-    const int64_t ke = min(kb + p.K, p.n);
-
+// Collapsed global prefix (xbar, P) entering chain c (the block scan spread over
+// CTAs + the CTA's chain scan); shared scratch tot[kWarps], wcar[kWarps].
+template <int D>
+__device__ __forceinline__ Gauss<D> filter_chain_carry(const KParams<D>& p, FAgg<D>* tot, Gauss<D>* wcar, int64_t c,
+                                                       int64_t nch, int lane, int wid) {
     // ---- collapsed prefix entering this CTA: incoming carry of earlier ranks (sharded)
     // (x) ordered product of the block aggregates of CTAs 0..blockIdx-1
     Gauss<D> cur;
@@ -454,6 +443,27 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
             cur = r2;
         }
     }
+
+    return cur;
+}
+
+// ------------------------------------------------------------------ K3: Kalman rescan
+template <int D, int MODE>
+__global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KParams<D> p) {
+    __shared__ AsyncStage st[kWarps];
+    __shared__ FAgg<D> tot[kWarps];
+    __shared__ Gauss<D> wcar[kWarps];
+    __shared__ SAgg<D> stot[kWarps];
+    __shared__ double nred[kWarps];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t c = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
+    const int64_t nch = static_cast<int64_t>(p.nb) * kThreads;
+    const int64_t wg = static_cast<int64_t>(blockIdx.x) * kWarps + wid;
+    const int64_t wbase = wg * 32 * p.K;
+    const int64_t kb = c * p.K;
+    const int64_t ke = min(kb + p.K, p.n);
+
+    const Gauss<D> cur = filter_chain_carry<D>(p, tot, wcar, c, nch, lane, wid);
 
     // ---- Kalman filter over the chain (supplement PAPER.md:285-315), carrying the
     // chain-entry moments E[x_k0 | y_1:k], Cov(x_k0 | y_1:k) and the cross-covariance
@@ -668,54 +678,14 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
     }
 }
 
-// ------------------------------------------------------------------ K5: RTS rescan
-// f-space projection (PAPER.md:283): mean = H m^s, var = H P^s H^T
+// Collapsed global suffix (m^s, P^s) after chain c (smoothed state at the first
+// step of chain c+1); shared scratch tot[kWarps], wcar[kWarps + 1].
 template <int D>
-__device__ __forceinline__ void project(const ModelParams<D>& m, const double (&ms)[D], const double (&Ps)[ns(D)],
-                                        double& mo, double& vo) {
-    if (m.h_unit) {
-        mo = ms[0];
-        vo = Ps[0];
-    } else {
-        mo = 0.0; vo = 0.0;
-#pragma unroll
-        for (int i = 0; i < D; ++i) {
-            mo = fma(m.H[i], ms[i], mo);
-            double s2 = 0.0;
-#pragma unroll
-            for (int j = 0; j < D; ++j) s2 = fma(Ps[si(D, i, j)], m.H[j], s2);
-            vo = fma(m.H[i], s2, vo);
-        }
-    }
-}
-
-struct StageOut {
-    double t[2][kWinA][33];   // double-buffered t, transposed [step][chain]
-    double m[kWinA][33];      // mean of the current window, transposed
-    double v[kWinA][33];      // variance
-};
-
-template <int D, int MODE>
-__global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_smoother_apply(const KParams<D> p) {
-    __shared__ StageOut so[kWarps];
-    __shared__ SAgg<D> tot[kWarps];
-    __shared__ Gauss<D> wcar[kWarps + 1];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int64_t c = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
-    const int64_t nch = static_cast<int64_t>(p.nb) * kThreads;
-    const int64_t wg = static_cast<int64_t>(blockIdx.x) * kWarps + wid;
-    const int64_t wbase = wg * 32 * p.K;
-    const int64_t kb = c * p.K;
-    const int64_t ke = min(kb + p.K, p.n);
-
-    // ---- NLL: fixed-order sum of the per-CTA partials written by K3 (CTA 0 only)
-    if (blockIdx.x == 0 && p.nll_out) {
-        const double v = cta_sum(p.nll_block, p.nb, reinterpret_cast<double*>(tot));
-        if (threadIdx.x == 0) *p.nll_out = v;
-    }
+__device__ __forceinline__ Gauss<D> smoother_chain_carry(const KParams<D>& p, SAgg<D>* tot, Gauss<D>* wcar,
+                                                         int64_t c, int64_t nch, int lane, int wid) {
+    Gauss<D> res;
     // ---- collapsed suffix after this CTA: ordered product of the block aggregates of
     // CTAs blockIdx+1..nb-1 (x) incoming carry of later ranks (sharded)
-    double ms[D], Ps[ns(D)];
     {
         const SAgg<D> after = cta_reduce_range<SAgg<D>>(p.block_s, blockIdx.x + 1, p.nb, tot);
         if (threadIdx.x == 0) {
@@ -770,6 +740,60 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_smoother_apply(const K
             apply_suffix(ex, cur, r2);
             cur = r2;
         }
+        res = cur;
+    }
+
+    return res;
+}
+
+// ------------------------------------------------------------------ K5: RTS rescan
+// f-space projection (PAPER.md:283): mean = H m^s, var = H P^s H^T
+template <int D>
+__device__ __forceinline__ void project(const ModelParams<D>& m, const double (&ms)[D], const double (&Ps)[ns(D)],
+                                        double& mo, double& vo) {
+    if (m.h_unit) {
+        mo = ms[0];
+        vo = Ps[0];
+    } else {
+        mo = 0.0; vo = 0.0;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            mo = fma(m.H[i], ms[i], mo);
+            double s2 = 0.0;
+#pragma unroll
+            for (int j = 0; j < D; ++j) s2 = fma(Ps[si(D, i, j)], m.H[j], s2);
+            vo = fma(m.H[i], s2, vo);
+        }
+    }
+}
+
+struct StageOut {
+    double t[2][kWinA][33];   // double-buffered t, transposed [step][chain]
+    double m[kWinA][33];      // mean of the current window, transposed
+    double v[kWinA][33];      // variance
+};
+
+template <int D, int MODE>
+__global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_smoother_apply(const KParams<D> p) {
+    __shared__ StageOut so[kWarps];
+    __shared__ SAgg<D> tot[kWarps];
+    __shared__ Gauss<D> wcar[kWarps + 1];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t c = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
+    const int64_t nch = static_cast<int64_t>(p.nb) * kThreads;
+    const int64_t wg = static_cast<int64_t>(blockIdx.x) * kWarps + wid;
+    const int64_t wbase = wg * 32 * p.K;
+    const int64_t kb = c * p.K;
+    const int64_t ke = min(kb + p.K, p.n);
+
+    // ---- NLL: fixed-order sum of the per-CTA partials written by K3 (CTA 0 only)
+    if (blockIdx.x == 0 && p.nll_out) {
+        const double v = cta_sum(p.nll_block, p.nb, reinterpret_cast<double*>(tot));
+        if (threadIdx.x == 0) *p.nll_out = v;
+    }
+    double ms[D], Ps[ns(D)];
+    {
+        const Gauss<D> cur = smoother_chain_carry<D>(p, tot, wcar, c, nch, lane, wid);
 #pragma unroll
         for (int i = 0; i < D; ++i) ms[i] = cur.x[i];
 #pragma unroll

@@ -294,3 +294,44 @@ def test_merge_grid_and_predict(cuda_device):
     with pytest.raises(P.PssgpError) as e:
         m.check()
     assert e.value.status == _native.PSSGP_E_INPUT and e.value.index == 10
+
+
+@pytest.mark.parametrize("kind", ["matern32", "matern52"])
+def test_batched_series(cuda_device, kind):
+    """NEXT row f2: independent series with their own hyper-parameters in one launch
+    (incl. empty and 1-point series, series spanning many chains); each equals the
+    oracle on that series alone, NLL per series."""
+    rng = np.random.default_rng(31)
+    lens = [0, 1, 2, 37, 3200, 0, 5000, 777, 1, 12000, 300]
+    ws = []
+    for b, n in enumerate(lens):
+        ws.append(synth.random_problem(100 + b, n, kind=kind, p_missing=0.2, ties=min(2, n // 10),
+                                       lengthscale=float(rng.uniform(0.2, 2.0)), variance=float(rng.uniform(0.5, 3.0)),
+                                       noise_var=float(rng.uniform(0.01, 0.3))) if n > 0 else None)
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    cat = lambda f, dt: np.concatenate([f(w) if w is not None else np.zeros(0, dt) for w in ws])  # noqa: E731
+    t = cat(lambda w: w.t, np.float64); y = cat(lambda w: w.y, np.float64); mk = cat(lambda w: w.mask, np.uint8)
+    var_b = np.array([w.components[0].variance if w else 1.0 for w in ws])
+    ell_b = np.array([w.components[0].lengthscale if w else 1.0 for w in ws])
+    r_b = np.array([w.noise_var if w else 0.1 for w in ws])
+    m = P.Model([synth.Component(kind, 1.0, 1.0)], 0.1, chain_len=64)
+    dev = "cuda:0"
+    T, Y, MK = (torch.from_numpy(a).to(dev) for a in (t, y, mk))
+    OFF, VB, EB, RB = (torch.from_numpy(a).to(dev) for a in (off, var_b, ell_b, r_b))
+    N = t.shape[0]
+    mean = torch.empty(N, dtype=torch.float64, device=dev); var = torch.empty_like(mean)
+    nll = torch.empty(len(lens), dtype=torch.float64, device=dev)
+    P.pssgp_posterior_batched(m.h, len(lens), OFF, VB, EB, RB, N, T, Y, MK, mean, var, nll)
+    m.check()
+    mean, var, nll = mean.cpu().numpy(), var.cpu().numpy(), nll.cpu().numpy()
+    for b, w in enumerate(ws):
+        if w is None:
+            assert nll[b] == 0.0
+            continue
+        o = oracle.posterior(w)
+        sl = slice(off[b], off[b + 1])
+        if w.mask.sum():
+            em, ev, en = errors((mean[sl], var[sl], nll[b]), o)
+            assert em <= MEAN_TOL and ev <= VAR_TOL and en <= NLL_TOL, (b, em, ev, en)
+        else:
+            np.testing.assert_allclose(var[sl], o["var"], rtol=VAR_TOL)
