@@ -63,7 +63,7 @@ def parse():
     ap.add_argument("--N", type=int, default=2 ** 24)
     ap.add_argument("--uniform", action="store_true", help="uniform dt (secondary row)")
     ap.add_argument("--kind", default="matern52")
-    ap.add_argument("--config", default="metric", choices=["metric", "c2", "c3", "c4", "c5"],
+    ap.add_argument("--config", default="metric", choices=["metric", "c2", "c3", "c4", "c5", "batched"],
                     help="workload (default: the BASELINE metric); c3/c4 are the d = 6 / d = 16 rows")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=2 ** 21)
@@ -151,6 +151,8 @@ def make_workload(args):
         return synth.config4(n=args.N)
     if args.config == "c5":
         return synth.metric_workload(2 ** 27 if args.N == 2 ** 24 else args.N)
+    if args.config == "batched":
+        return synth.metric_workload(3200 * 4, kind="matern52")
     return synth.metric_workload(args.N, uniform=args.uniform, kind=args.kind)
 
 
@@ -207,7 +209,27 @@ def main():
     N = w.N
     stream = torch.cuda.current_stream()
 
-    if world == 1:
+    if args.config == "batched":
+        # f2: B series of 3,200 points (the sunspot N of PAPER.md:206), each with its own
+        # hyper-parameters (multi-start / HMC shape), one launch
+        B = max(1, args.N // 3200)
+        rng = np.random.default_rng(0)
+        lens = np.full(B, 3200, np.int64)
+        off = torch.from_numpy(np.concatenate([[0], np.cumsum(lens)])).to(dev)
+        VB = torch.from_numpy(rng.uniform(0.5, 2.0, B)).to(dev)
+        EB = torch.from_numpy(rng.uniform(0.2, 1.0, B)).to(dev)
+        RB = torch.from_numpy(rng.uniform(0.005, 0.05, B)).to(dev)
+        N = int(lens.sum())
+        tb = np.tile(w.t[:3200] - w.t[0], B); yb = np.tile(w.y[:3200], B); mb = np.tile(w.mask[:3200], B)
+        t = torch.from_numpy(tb).to(dev); y = torch.from_numpy(yb).to(dev); mk = torch.from_numpy(mb).to(dev)
+        mean = torch.empty(N, dtype=torch.float64, device=dev)
+        var = torch.empty_like(mean)
+        nllb = torch.empty(B, dtype=torch.float64, device=dev)
+
+        def step():
+            P.pssgp_posterior_batched(model.h, B, off, VB, EB, RB, N, t, y, mk, mean, var, nllb, stream)
+        n_local = N
+    elif world == 1:
         t = torch.from_numpy(w.t).to(dev)
         y = torch.from_numpy(w.y).to(dev)
         mk = torch.from_numpy(w.mask).to(dev)
@@ -266,7 +288,7 @@ def main():
 
     # ---- e2e through the public host API (pinned buffers, copies inside the timed region)
     e2e = None
-    if world == 1:
+    if world == 1 and args.config != "batched":
         th = torch.from_numpy(w.t).pin_memory()
         yh = torch.from_numpy(w.y).pin_memory()
         mh = torch.from_numpy(w.mask).pin_memory()
@@ -332,7 +354,7 @@ def main():
     if not args.no_cpu_baseline:
         cpu = cpu_baseline(w, args.cpu_sample)
     metric = METRIC if args.config == "metric" and not args.uniform else \
-        f"time-steps/s (filter+smoother+NLL, fp64) {w.name} N={N}"
+        f"time-steps/s (filter+smoother+NLL, fp64) {w.name if args.config != 'batched' else 'batched Matern-5/2 series of 3200'} N={N}"
     line = {"metric": metric, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
