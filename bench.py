@@ -32,7 +32,8 @@ sys.path.insert(0, ROOT)
 METRIC = "time-steps/s (filter+smoother+NLL, fp64) Matern-5/2 N=2^24"
 UNIT = "time-steps/s"
 # algorithmic bytes per time step moved by each kernel at d = 3 (DESIGN.md §6 "Roofline")
-ALG_BYTES = {"k_filter_reduce": 17, "k_filter_apply": 17 + 72, "k_smoother_apply": 8 + 72 + 16}
+ALG_BYTES = {"k_filter_reduce": 17, "k_filter_apply": 17 + 72, "k_smoother_apply": 8 + 72 + 16,
+             "k_grad_fold": 17 + 72}
 # fp64 flops per time step of each kernel (DFMA = 2), Matern-5/2 closed-form path, from the ncu
 # SASS counts of the committed profile (tools/fp64_flops.py)
 FLOPS_PER_STEP = {"k_filter_reduce": 350.2, "k_filter_apply": 359.1, "k_smoother_apply": 423.5}
@@ -63,7 +64,7 @@ def parse():
     ap.add_argument("--N", type=int, default=2 ** 24)
     ap.add_argument("--uniform", action="store_true", help="uniform dt (secondary row)")
     ap.add_argument("--kind", default="matern52")
-    ap.add_argument("--config", default="metric", choices=["metric", "c2", "c3", "c4", "c5", "batched"],
+    ap.add_argument("--config", default="metric", choices=["metric", "c2", "c3", "c4", "c5", "batched", "grad"],
                     help="workload (default: the BASELINE metric); c3/c4 are the d = 6 / d = 16 rows")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=2 ** 21)
@@ -153,6 +154,8 @@ def make_workload(args):
         return synth.metric_workload(2 ** 27 if args.N == 2 ** 24 else args.N)
     if args.config == "batched":
         return synth.metric_workload(3200 * 4, kind="matern52")
+    if args.config == "grad":
+        return synth.metric_workload(args.N)
     return synth.metric_workload(args.N, uniform=args.uniform, kind=args.kind)
 
 
@@ -229,6 +232,17 @@ def main():
         def step():
             P.pssgp_posterior_batched(model.h, B, off, VB, EB, RB, N, t, y, mk, mean, var, nllb, stream)
         n_local = N
+    elif args.config == "grad":
+        # f1: NLL + d NLL / d (log s2, log ell, log r) on the metric grid (one L-BFGS / HMC evaluation)
+        t = torch.from_numpy(w.t).to(dev)
+        y = torch.from_numpy(w.y).to(dev)
+        mk = torch.from_numpy(w.mask).to(dev)
+        nll = torch.zeros(1, dtype=torch.float64, device=dev)
+        gr = torch.zeros(3, dtype=torch.float64, device=dev)
+
+        def step():
+            P.pssgp_nll_grad(model.h, N, t, y, mk, nll, gr, stream)
+        n_local = N
     elif world == 1:
         t = torch.from_numpy(w.t).to(dev)
         y = torch.from_numpy(w.y).to(dev)
@@ -288,7 +302,7 @@ def main():
 
     # ---- e2e through the public host API (pinned buffers, copies inside the timed region)
     e2e = None
-    if world == 1 and args.config != "batched":
+    if world == 1 and args.config not in ("batched", "grad"):
         th = torch.from_numpy(w.t).pin_memory()
         yh = torch.from_numpy(w.y).pin_memory()
         mh = torch.from_numpy(w.mask).pin_memory()
@@ -353,8 +367,28 @@ def main():
     cpu = None
     if not args.no_cpu_baseline:
         cpu = cpu_baseline(w, args.cpu_sample)
-    metric = METRIC if args.config == "metric" and not args.uniform else \
-        f"time-steps/s (filter+smoother+NLL, fp64) {w.name if args.config != 'batched' else 'batched Matern-5/2 series of 3200'} N={N}"
+    if args.config == "metric" and not args.uniform:
+        metric = METRIC
+    elif args.config == "grad":
+        metric = f"time-steps/s (NLL + 3-parameter gradient, fp64) {w.name} N={N}"
+    else:
+        metric = (f"time-steps/s (filter+smoother+NLL, fp64) "
+                  f"{w.name if args.config != 'batched' else 'batched Matern-5/2 series of 3200'} N={N}")
+    extra = {}
+    if args.config == "grad":
+        # latency of one NLL+gradient evaluation at the sunspot size N = 3,200 (Table 1)
+        n1 = 3200
+        t1, y1, m1 = t[:n1].contiguous(), y[:n1].contiguous(), mk[:n1].contiguous()
+        for _ in range(5):
+            P.pssgp_nll_grad(model.h, n1, t1, y1, m1, nll, gr, stream)
+        torch.cuda.synchronize()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for _ in range(200):
+            P.pssgp_nll_grad(model.h, n1, t1, y1, m1, nll, gr, stream)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        extra["latency_n3200_ms"] = a0.elapsed_time(a1) / 200
     line = {"metric": metric, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -362,7 +396,7 @@ def main():
                        "ctas": plan["n_blocks"], "threads_per_cta": plan["threads"],
                        "l2": "no flush: working set (1.8 GB) >> 126 MB L2",
                        "parallelism": f"time-sharded x{world}" if world > 1 else "single GPU"},
-            "clocks": clk, "e2e": e2e, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu}
+            "clocks": clk, "e2e": e2e, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu, **extra}
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()

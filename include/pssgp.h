@@ -121,6 +121,17 @@ pssgp_status pssgp_posterior(pssgp_model* m, int64_t N, const double* t, const d
 pssgp_status pssgp_nll(pssgp_model* m, int64_t N, const double* t, const double* y,
                        const uint8_t* mask, double* nll, void* stream);
 
+/* NLL and its exact gradient with respect to theta = (log sigma^2, log ell,
+ * log sigma_n^2) of a SINGLE-component Matern model (the hyper-parameter
+ * gradient the paper obtains by automatic differentiation, PAPER.md:77, 157,
+ * 173).  Forward-mode tangents of the Kalman recursion (supplement
+ * PAPER.md:304-315) are composed as affine maps per thread chain and reduced
+ * in time order (pssgp_grad.cuh).
+ * nll: device scalar or NULL; grad: device array of 3 doubles, written in the
+ * order above.  N = 0 -> nll = 0, grad = 0.  Other models -> PSSGP_E_UNSUPPORTED. */
+pssgp_status pssgp_nll_grad(pssgp_model* m, int64_t N, const double* t, const double* y,
+                            const uint8_t* mask, double* nll, double* grad, void* stream);
+
 /* End-to-end variant on HOST arrays (pinned memory recommended): copies the
  * inputs to handle-owned device buffers, runs pssgp_posterior, copies mean,
  * var (nullable) and *nll (nullable) back, and synchronises the stream.

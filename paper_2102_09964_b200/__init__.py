@@ -21,7 +21,7 @@ import numpy as np
 from ._native import (KINDS, STATUS_NAMES, Component, Options, PssgpError, build, lib)  # noqa: F401
 
 __all__ = ["Model", "PssgpError", "build", "lib", "pssgp_create", "pssgp_destroy", "pssgp_posterior",
-           "pssgp_nll", "pssgp_posterior_host", "pssgp_check", "pssgp_error_index", "pssgp_last_error",
+           "pssgp_nll", "pssgp_nll_grad", "pssgp_posterior_host", "pssgp_check", "pssgp_error_index", "pssgp_last_error",
            "pssgp_state_dim", "pssgp_get_ssm", "pssgp_debug_discretize", "pssgp_plan",
            "pssgp_aggregate_bytes", "pssgp_shard_filter_reduce", "pssgp_shard_filter_apply",
            "pssgp_shard_smoother_apply", "pssgp_profile_enable", "pssgp_profile_read", "pssgp_profile_name",
@@ -85,6 +85,11 @@ def pssgp_posterior(h, N, t, y, mask, mean, var, nll, stream=None) -> None:
 
 def pssgp_nll(h, N, t, y, mask, nll, stream=None) -> None:
     _raise(h, lib().pssgp_nll(h, int(N), _ptr(t), _ptr(y), _ptr(mask), _ptr(nll), _stream_ptr(stream)))
+
+
+def pssgp_nll_grad(h, N, t, y, mask, nll, grad, stream=None) -> None:
+    _raise(h, lib().pssgp_nll_grad(h, int(N), _ptr(t), _ptr(y), _ptr(mask), _ptr(nll), _ptr(grad),
+                                   _stream_ptr(stream)))
 
 
 def pssgp_posterior_host(h, N, t: np.ndarray, y: np.ndarray, mask: np.ndarray, mean: Optional[np.ndarray],
@@ -240,6 +245,15 @@ class Model:
         nll = out if out is not None else torch.zeros(1, dtype=torch.float64, device=t.device)
         pssgp_nll(self.h, N, t, y, mask, nll, stream)
         return nll
+
+    def nll_grad(self, t, y, mask, stream=None):
+        """(nll[1], grad[3]) with grad = d NLL / d (log sigma^2, log ell, log sigma_n^2)."""
+        import torch
+        N = int(t.shape[0])
+        nll = torch.zeros(1, dtype=torch.float64, device=t.device)
+        grad = torch.zeros(3, dtype=torch.float64, device=t.device)
+        pssgp_nll_grad(self.h, N, t, y, mask, nll, grad, stream)
+        return nll, grad
 
     def posterior_host(self, t: np.ndarray, y: np.ndarray, mask: np.ndarray, mean=None, var=None, nll=None):
         N = int(t.shape[0])

@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstddef>
 #include <cstring>
 #include <new>
 #include <string>
@@ -14,6 +15,7 @@
 #include "pssgp_kernels.cuh"
 #include "pssgp_wide.cuh"
 #include "pssgp_batch.cuh"
+#include "pssgp_grad.cuh"
 
 using namespace pssgp;
 namespace ph = pssgp_host;
@@ -23,10 +25,11 @@ namespace {
 constexpr int kMaxD = 3;              // thread-per-chain path: d = 1, 2, 3
 // warp-per-chain path (pssgp_wide.cuh), uniform-dt models: these d are compiled
 #define PSSGP_WIDE_DIMS(X) X(4) X(5) X(6) X(8) X(10) X(12) X(14) X(16) X(18) X(20)
-constexpr int kSlots = 7;
+constexpr int kSlots = 8;
 const char* kSlotNames[kSlots] = {"k_filter_reduce", "k_filter_scan", "k_filter_apply",
-                                  "k_smoother_scan", "k_smoother_apply", "k_nll_sum", "k_reduce_blocks"};
-enum Slot { S_K1 = 0, S_K2, S_K3, S_K4, S_K5, S_K6, S_RED };
+                                  "k_smoother_scan", "k_smoother_apply", "k_nll_sum", "k_reduce_blocks",
+                                  "k_grad_fold"};
+enum Slot { S_K1 = 0, S_K2, S_K3, S_K4, S_K5, S_K6, S_RED, S_GRAD };
 
 }  // namespace
 
@@ -303,6 +306,54 @@ pssgp_status run_posterior(pssgp_model* m, int64_t N, const double* t, const dou
         return st;
     }
     return PSSGP_OK;
+}
+
+// NLL gradient (f1): primal filter storing (xbar, P), then one tangent fold + ordered
+// block reduction per parameter (pssgp_grad.cuh).
+template <int D, int PAR>
+pssgp_status grad_param(pssgp_model* m, KParams<D>& p, double* blocks, double* out, double* grad, cudaStream_t s) {
+    {
+        ProfScope ps(m, S_GRAD, s);
+        k_grad_fold<D, PAR><<<p.nb, kThreads, 0, s>>>(p, blocks);
+        LAUNCH_CHECK(m, "k_grad_fold");
+    }
+    {
+        ProfScope ps(m, S_RED, s);
+        k_reduce_blocks<D, TAgg<D>><<<1, kCarryThreads, 0, s>>>(blocks, p.nb, out);
+        LAUNCH_CHECK(m, "k_reduce_blocks(grad)");
+    }
+    cudaError_t e = cudaMemcpyAsync(grad + PAR, out + offsetof(TAgg<D>, a) / sizeof(double), sizeof(double),
+                                    cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(m, e, "cudaMemcpyAsync(grad)");
+    return PSSGP_OK;
+}
+
+template <int D>
+pssgp_status run_grad(pssgp_model* m, int64_t N, const double* t, const double* y, const uint8_t* mask,
+                      double* nll, double* grad, cudaStream_t s) {
+    if (N == 0) {
+        cudaError_t e = cudaMemsetAsync(grad, 0, 3 * sizeof(double), s);
+        if (e == cudaSuccess && nll) e = cudaMemsetAsync(nll, 0, sizeof(double), s);
+        if (e != cudaSuccess) return cuda_fail(m, e, "cudaMemsetAsync");
+        return PSSGP_OK;
+    }
+    const Plan pl = make_plan<D>(m, N);
+    KParams<D> p;
+    pssgp_status st = setup<D>(m, pl, p);
+    if (st) return st;
+    p.t = t; p.y = y; p.mask = mask;
+    p.n = N; p.k0 = 0; p.nglob = N;
+    p.store_state = 1;
+    if ((st = phase_filter_reduce<D>(m, p, s))) return st;
+    if ((st = phase_filter_apply<D>(m, p, s))) return st;
+    if (nll && (st = nll_sum(m, p.nll_block, p.nb, nll, s))) return st;
+    // block tangent aggregates reuse the smoother-aggregate region (not read on this path)
+    static_assert(sizeof(TAgg<D>) / sizeof(double) <= kThreads * SN(D), "grad scratch");
+    double* blocks = p.chain_s;
+    double* out = p.chain_s + static_cast<size_t>(pl.nb) * (sizeof(TAgg<D>) / sizeof(double));
+    if ((st = grad_param<D, 0>(m, p, blocks, out, grad, s))) return st;
+    if ((st = grad_param<D, 1>(m, p, blocks, out, grad, s))) return st;
+    return grad_param<D, 2>(m, p, blocks, out, grad, s);
 }
 
 template <int D>
@@ -714,6 +765,19 @@ pssgp_status pssgp_nll(pssgp_model* m, int64_t N, const double* t, const double*
     m->last_stream = s;
     if (m->d > kMaxD) return wide_posterior_dispatch(m, N, t, y, mask, nullptr, nullptr, nll, s, false);
     DISPATCH_D(m, run_posterior<D_>(m, N, t, y, mask, nullptr, nullptr, nll, s, false));
+}
+
+pssgp_status pssgp_nll_grad(pssgp_model* m, int64_t N, const double* t, const double* y, const uint8_t* mask,
+                            double* nll, double* grad, void* stream) {
+    pssgp_status st = check_args(m, N, t, y, mask);
+    if (st) return st;
+    if (!grad) return fail(m, PSSGP_E_ARG, "grad is NULL");
+    if (!m->closed || m->d > kMaxD)
+        return fail(m, PSSGP_E_UNSUPPORTED, "gradient needs a single closed-form Matern component");
+    if ((st = ensure_device(m))) return st;
+    auto s = static_cast<cudaStream_t>(stream);
+    m->last_stream = s;
+    DISPATCH_D(m, run_grad<D_>(m, N, t, y, mask, nll, grad, s));
 }
 
 pssgp_status pssgp_merge_grid(pssgp_model* m, int64_t n_train, const double* t_train, const double* y_train,
