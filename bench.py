@@ -66,6 +66,7 @@ def parse():
     ap.add_argument("--kind", default="matern52")
     ap.add_argument("--config", default="metric", choices=["metric", "c2", "c3", "c4", "c5", "batched", "grad"],
                     help="workload (default: the BASELINE metric); c3/c4 are the d = 6 / d = 16 rows")
+    ap.add_argument("--irregular", action="store_true", help="c3/c4 on a jittered grid (device Pade discretisation)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=2 ** 21)
     ap.add_argument("--chain-len", type=int, default=0)
@@ -147,9 +148,9 @@ def make_workload(args):
     if args.config == "c2":
         return synth.config2()
     if args.config == "c3":
-        return synth.config3(n=args.N if args.N != 2 ** 24 else 2 ** 22)
+        return synth.config3(n=args.N if args.N != 2 ** 24 else 2 ** 22, irregular=args.irregular)
     if args.config == "c4":
-        return synth.config4(n=args.N)
+        return synth.config4(n=args.N, irregular=args.irregular)
     if args.config == "c5":
         return synth.metric_workload(2 ** 27 if args.N == 2 ** 24 else args.N)
     if args.config == "batched":

@@ -89,9 +89,15 @@ typedef struct {
     int device;               /* CUDA device ordinal used for workspace (default: current) */
     double uniform_dt;        /* > 0: steps with |t[k]-t[k-1] - uniform_dt| <= 1e-12 uniform_dt
                                  (time-stamp rounding) use F, Q precomputed on the host (fp64
-                                 result of an extended-precision Van Loan); 0 = none.  Required
-                                 (> 0) for non-Matern models; their other steps (except dt = 0)
-                                 fail with PSSGP_E_UNSUPPORTED. */
+                                 result of an extended-precision Van Loan); 0 = none.
+                                 Non-Matern models (no closed form):
+                                   > 0 -> only dt = uniform_dt or 0 allowed, other steps fail
+                                          with PSSGP_E_UNSUPPORTED (pure uniform grids);
+                                   = 0 -> any dt: per-step F = expm(G dt) by [7/7] Pade
+                                          scaling and squaring on the device and
+                                          Q = P_inf - F P_inf F^T (north_star discretisation
+                                          kernel; d > 3 stores (F, Q) per step in a
+                                          handle-owned buffer of N 2 d (d+1) doubles). */
     int64_t chain_len;        /* steps per thread chain (0 = automatic)                   */
     int blocks_per_sm;        /* CTAs per SM for the one-wave grid (0 = automatic)        */
 } pssgp_options;

@@ -25,11 +25,11 @@ namespace {
 constexpr int kMaxD = 3;              // thread-per-chain path: d = 1, 2, 3
 // warp-per-chain path (pssgp_wide.cuh), uniform-dt models: these d are compiled
 #define PSSGP_WIDE_DIMS(X) X(4) X(5) X(6) X(8) X(10) X(12) X(14) X(16) X(18) X(20)
-constexpr int kSlots = 8;
+constexpr int kSlots = 9;
 const char* kSlotNames[kSlots] = {"k_filter_reduce", "k_filter_scan", "k_filter_apply",
                                   "k_smoother_scan", "k_smoother_apply", "k_nll_sum", "k_reduce_blocks",
-                                  "k_grad_fold"};
-enum Slot { S_K1 = 0, S_K2, S_K3, S_K4, S_K5, S_K6, S_RED, S_GRAD };
+                                  "k_grad_fold", "k_discretize"};
+enum Slot { S_K1 = 0, S_K2, S_K3, S_K4, S_K5, S_K6, S_RED, S_GRAD, S_DISC };
 
 }  // namespace
 
@@ -59,6 +59,8 @@ struct pssgp_model {
     size_t mg_bytes = 0;
     double* bt = nullptr;                 // batched: per-step NLL terms
     size_t bt_bytes = 0;
+    double* fq = nullptr;                 // wide path, kPade mode: per-step (F, Q)
+    size_t fq_bytes = 0;
     cudaStream_t last_stream = nullptr;
     int64_t err_index = -1;
     std::string last_err;
@@ -131,6 +133,7 @@ void fill_params(const pssgp_model* m, ModelParams<D>& p) {
     p.s2 = m->s2;
     p.closed = m->closed ? 1 : 0;
     p.udt = m->udt > 0.0 ? m->udt : -1.0;  // -1 never equals a valid dt >= 0
+    for (int i = 0; i < D * D; ++i) p.G[i] = static_cast<double>(m->ssm.G[i]);
     if (m->udt > 0.0) {
         for (int i = 0; i < D * D; ++i) p.Fu[i] = m->Fu[i];
         for (int i = 0; i < D; ++i)
@@ -231,6 +234,7 @@ pssgp_status setup(pssgp_model* m, const Plan& pl, KParams<D>& p) {
     do {                                                                         \
         if ((m)->mode == kClosed) KERN<D, kClosed><<<grid, block, 0, s>>>(p);    \
         else if ((m)->mode == kMixed) KERN<D, kMixed><<<grid, block, 0, s>>>(p); \
+        else if ((m)->mode == kPade) KERN<D, kPade><<<grid, block, 0, s>>>(p);   \
         else KERN<D, kTable><<<grid, block, 0, s>>>(p);                          \
     } while (0)
 
@@ -401,6 +405,7 @@ void wide_set_smem_attrs() {
     cudaFuncSetAttribute(kw_smoother_apply<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K5Smem<D>));
     cudaFuncSetAttribute(kw_scan_filter<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(ScanSmemF<D>));
     cudaFuncSetAttribute(kw_scan_smoother<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(ScanSmemS<D>));
+    cudaFuncSetAttribute(kw_discretize<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(KDSmem<D>));
     done = true;
 }
 
@@ -453,6 +458,7 @@ pssgp_status wide_setup(pssgp_model* m, const WPlan& pl, pssgp::wide::WParams& p
         for (int i = 0; i < D; ++i) h[3 * D * D + i] = static_cast<double>(m->ssm.H[i]);
         h[3 * D * D + D] = m->r;
         h[3 * D * D + D + 1] = m->udt > 0.0 ? m->udt : -1.0;
+        for (int i = 0; i < D * D; ++i) h[3 * D * D + D + 2 + i] = static_cast<double>(m->ssm.G[i]);
         if (cudaMalloc(&m->d_model, h.size() * sizeof(double)) != cudaSuccess) {
             cudaGetLastError();
             return fail(m, PSSGP_E_NOMEM, "cudaMalloc(model)");
@@ -474,6 +480,38 @@ pssgp_status wide_setup(pssgp_model* m, const WPlan& pl, pssgp::wide::WParams& p
     p.rank = 0;
     p.world = 1;
     p.store_state = 1;
+    return PSSGP_OK;
+}
+
+// kPade mode (no closed form, no uniform step): per-step (F, Q) for local steps
+// [0, n] (step n = the successor read by the smoother when it exists globally)
+template <int D>
+pssgp_status wide_prepare(pssgp_model* m, pssgp::wide::WParams& p, cudaStream_t s) {
+    using namespace pssgp::wide;
+    p.fq = nullptr;
+    if (m->mode != kPade || p.n == 0) return PSSGP_OK;
+    const int64_t nfq = p.n + ((p.k0 + p.n < p.nglob) ? 1 : 0);
+    const size_t need = static_cast<size_t>(nfq) * FQW(D) * sizeof(double);
+    if (need > m->fq_bytes) {
+        if (m->fq) cudaFree(m->fq);
+        m->fq = nullptr;
+        m->fq_bytes = 0;
+        if (cudaMalloc(&m->fq, need) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(m, PSSGP_E_NOMEM, "cudaMalloc(per-step F, Q) failed");
+        }
+        m->fq_bytes = need;
+    }
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kw_discretize<D>, 32 * kWWarps, sizeof(KDSmem<D>));
+    const int64_t want = (nfq + kWWarps - 1) / kWWarps;
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(m->sm_count) * std::max(1, occ))));
+    {
+        ProfScope ps(m, S_DISC, s);
+        kw_discretize<D><<<grid, 32 * kWWarps, sizeof(KDSmem<D>), s>>>(p.t, nfq, p.k0, m->d_model, m->fq, p.err);
+        LAUNCH_CHECK(m, "kw_discretize");
+    }
+    p.fq = m->fq;
     return PSSGP_OK;
 }
 
@@ -550,6 +588,7 @@ pssgp_status wide_posterior(pssgp_model* m, int64_t N, const double* t, const do
     p.n = N; p.k0 = 0; p.nglob = N;
     p.mean = mean; p.var = var;
     p.store_state = smooth ? 1 : 0;
+    if ((st = wide_prepare<D>(m, p, s))) return st;
     if ((st = wide_fold<D>(m, p, pl.nb, s))) return st;
     p.fagg = wide_scan_f<D>(m, p, s, st);
     if (st) return st;
@@ -584,6 +623,7 @@ pssgp_status wide_shard_reduce(pssgp_model* m, int64_t k0, int64_t n, int64_t Ng
     pssgp_status st = wide_setup<D>(m, pl, p);
     if (st) return st;
     p.t = t; p.y = y; p.mask = mask; p.n = n; p.k0 = k0; p.nglob = Ng;
+    if ((st = wide_prepare<D>(m, p, s))) return st;
     if ((st = wide_fold<D>(m, p, pl.nb, s))) return st;
     double* inc = wide_scan_f<D>(m, p, s, st);
     if (st) return st;
@@ -610,6 +650,7 @@ pssgp_status wide_shard_fapply(pssgp_model* m, int64_t k0, int64_t n, int64_t Ng
     p.in_filt = static_cast<const double*>(all);
     p.rank = rank; p.world = world;
     if (ks_levels(pl.nch) & 1) p.fagg = p.fbuf;          // where the reduce phase left the scan
+    if ((st = wide_prepare<D>(m, p, s))) return st;
     if ((st = wide_fapply<D>(m, p, pl.nb, s))) return st;
     if (nllp && (st = nll_sum(m, p.nll_chain, p.nch, nllp, s))) return st;
     double* inc = wide_scan_s<D>(m, p, s, st);
@@ -630,6 +671,7 @@ pssgp_status wide_shard_sapply(pssgp_model* m, int64_t k0, int64_t n, int64_t Ng
     p.rank = rank; p.world = world;
     p.mean = mean; p.var = var;
     if (ks_levels(pl.nch) & 1) p.sagg = p.sbuf;
+    if ((st = wide_prepare<D>(m, p, s))) return st;
     return wide_sapply<D>(m, p, pl.nb, s);
 }
 
@@ -722,7 +764,7 @@ pssgp_status pssgp_create(const pssgp_component* comps, int n_comps, double nois
         m->Qu.resize(Q.size());
         for (size_t i = 0; i < F.size(); ++i) { m->Fu[i] = static_cast<double>(F[i]); m->Qu[i] = static_cast<double>(Q[i]); }
     }
-    m->mode = m->closed ? (m->udt > 0.0 ? kMixed : kClosed) : kTable;
+    m->mode = m->closed ? (m->udt > 0.0 ? kMixed : kClosed) : (m->udt > 0.0 ? kTable : kPade);
     *out = m;
     return PSSGP_OK;
 }
@@ -733,6 +775,7 @@ void pssgp_destroy(pssgp_model* m) {
     if (m->io) cudaFree(m->io);
     if (m->mg) cudaFree(m->mg);
     if (m->bt) cudaFree(m->bt);
+    if (m->fq) cudaFree(m->fq);
     if (m->d_err) cudaFree(m->d_err);
     if (m->d_model) cudaFree(m->d_model);
     for (int s = 0; s < kSlots; ++s)
@@ -823,6 +866,7 @@ pssgp_status pssgp_predict(pssgp_model* m, int64_t n_train, const double* t_trai
     if (need > m->mg_bytes) {
         if (m->mg) cudaFree(m->mg);
     if (m->bt) cudaFree(m->bt);
+    if (m->fq) cudaFree(m->fq);
         m->mg = nullptr;
         m->mg_bytes = 0;
         if (cudaMalloc(&m->mg, need) != cudaSuccess) {
@@ -856,6 +900,7 @@ pssgp_status pssgp_posterior_batched(pssgp_model* m, int nseg, const int64_t* of
     const size_t need = static_cast<size_t>(std::max<int64_t>(N, 1)) * sizeof(double);
     if (need > m->bt_bytes) {
         if (m->bt) cudaFree(m->bt);
+    if (m->fq) cudaFree(m->fq);
         m->bt = nullptr;
         m->bt_bytes = 0;
         if (cudaMalloc(&m->bt, need) != cudaSuccess) {

@@ -143,6 +143,7 @@ struct ModelParams {
     double udt;           // uniform dt (> 0) for which Fu, Qu are valid, else 0
     double Fu[D * D];     // F(udt)
     double Qu[ns(D)];     // Q(udt)
+    double G[D * D];      // continuous drift (balanced coordinates), kPade mode
     int closed;           // 1: Matern closed form of order D available in the lambda-scaled basis
     int h_unit;           // 1: H == e_0
 };
@@ -390,8 +391,76 @@ PS_HD void matern_closed(double lam, double s2, double dt, double (&F)[D * D], d
 // Returns 0, or a nonzero code when the model has no device discretisation for dt.
 // MODE (compile time): kClosed = Matern closed form only (dt = 0 gives F = I,
 // Q = 0 exactly), kTable = the host-precomputed pair for dt == udt (dt = 0 ->
-// I, 0; anything else unsupported), kMixed = table for dt == udt else closed.
-enum DiscMode : int { kClosed = 0, kTable = 1, kMixed = 2 };
+// I, 0; anything else unsupported), kMixed = table for dt == udt else closed,
+// kPade = any model, any dt: F = expm(G dt) by scaling and squaring with the
+// [7/7] Pade approximant, Q = P_inf - F P_inf F^T (Lyapunov form of the stationary
+// model; north_star "per-step small-matrix expm via scaling-and-squaring Pade").
+enum DiscMode : int { kClosed = 0, kTable = 1, kMixed = 2, kPade = 3 };
+
+// F = expm(G dt), D x D row-major.  Higham (2005): the [7/7] Pade approximant is
+// accurate to unit roundoff for ||A||_1 <= theta_7 = 0.9504; A = G dt / 2^s with the
+// smallest such s, then s squarings.  (V - U) F = V + U by pivoted elimination.
+template <int D>
+PS_HD void expm_pade7(const double (&G)[D * D], double dt, double (&F)[D * D]) {
+    double nrm = 0.0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        double c = 0.0;
+#pragma unroll
+        for (int i = 0; i < D; ++i) c += fabs(G[i * D + j]);
+        nrm = fmax(nrm, c);
+    }
+    nrm *= fabs(dt);
+    int s = 0;
+    if (nrm > 0.9504) {
+        int e;
+        frexp(nrm / 0.9504, &e);   // nrm / theta = f 2^e, f in [0.5, 1)  ->  2^e >= nrm / theta
+        s = e;
+    }
+    const double sc = ldexp(dt, -s);
+    double A[D * D], A2[D * D], A4[D * D], A6[D * D];
+#pragma unroll
+    for (int i = 0; i < D * D; ++i) A[i] = G[i] * sc;
+    auto mm = [](const double (&X)[D * D], const double (&Y)[D * D], double (&Z)[D * D]) {
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                double acc = 0.0;
+#pragma unroll
+                for (int k = 0; k < D; ++k) acc = fma(X[i * D + k], Y[k * D + j], acc);
+                Z[i * D + j] = acc;
+            }
+    };
+    mm(A, A, A2);
+    mm(A2, A2, A4);
+    mm(A4, A2, A6);
+    constexpr double b0 = 17297280.0, b1 = 8648640.0, b2 = 1995840.0, b3 = 277200.0, b4 = 25200.0,
+                     b5 = 1512.0, b6 = 56.0, b7 = 1.0;
+    double T[D * D], U[D * D], V[D * D];
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            const int e = i * D + j;
+            const double id = (i == j) ? 1.0 : 0.0;
+            T[e] = fma(b7, A6[e], fma(b5, A4[e], fma(b3, A2[e], b1 * id)));
+            V[e] = fma(b6, A6[e], fma(b4, A4[e], fma(b2, A2[e], b0 * id)));
+        }
+    mm(A, T, U);
+#pragma unroll
+    for (int e = 0; e < D * D; ++e) {
+        T[e] = V[e] - U[e];
+        F[e] = V[e] + U[e];
+    }
+    gauss_solve<D, D>(T, F);
+    for (int q = 0; q < s; ++q) {
+        double Fs[D * D];
+        mm(F, F, Fs);
+#pragma unroll
+        for (int e = 0; e < D * D; ++e) F[e] = Fs[e];
+    }
+}
 
 template <int D, int MODE>
 PS_HD int disc(const ModelParams<D>& p, double dt, double (&F)[D * D], double (&Q)[ns(D)]) {
@@ -408,6 +477,38 @@ PS_HD int disc(const ModelParams<D>& p, double dt, double (&F)[D * D], double (&
         }
         if constexpr (MODE == kMixed && D <= 3) {
             matern_closed<D>(p.lam, p.s2, dt, F, Q);
+            return 0;
+        } else if constexpr (MODE == kPade) {
+            if (dt == 0.0) {   // exact I, 0 on ties (reading Z13)
+#pragma unroll
+                for (int i = 0; i < D; ++i)
+#pragma unroll
+                    for (int j = 0; j < D; ++j) F[i * D + j] = (i == j) ? 1.0 : 0.0;
+#pragma unroll
+                for (int i = 0; i < ns(D); ++i) Q[i] = 0.0;
+                return 0;
+            }
+            expm_pade7<D>(p.G, dt, F);
+            // Q = P_inf - F P_inf F^T
+            double FP[D * D];
+#pragma unroll
+            for (int i = 0; i < D; ++i)
+#pragma unroll
+                for (int j = 0; j < D; ++j) {
+                    double acc = 0.0;
+#pragma unroll
+                    for (int k = 0; k < D; ++k) acc = fma(F[i * D + k], p.Pinf[si(D, k, j)], acc);
+                    FP[i * D + j] = acc;
+                }
+#pragma unroll
+            for (int i = 0; i < D; ++i)
+#pragma unroll
+                for (int j = i; j < D; ++j) {
+                    double acc = p.Pinf[si(D, i, j)];
+#pragma unroll
+                    for (int k = 0; k < D; ++k) acc = fma(-FP[i * D + k], F[j * D + k], acc);
+                    Q[si(D, i, j)] = acc;
+                }
             return 0;
         } else {
             const bool zero = (dt == 0.0);
@@ -426,7 +527,7 @@ PS_HD int disc(const ModelParams<D>& p, double dt, double (&F)[D * D], double (&
 template <int D>
 PS_HD int discretize(const ModelParams<D>& p, double dt, double (&F)[D * D], double (&Q)[ns(D)]) {
     if (p.closed) return p.udt > 0.0 ? disc<D, kMixed>(p, dt, F, Q) : disc<D, kClosed>(p, dt, F, Q);
-    return disc<D, kTable>(p, dt, F, Q);
+    return p.udt > 0.0 ? disc<D, kTable>(p, dt, F, Q) : disc<D, kPade>(p, dt, F, Q);
 }
 
 // ------------------------------------------------------------------ filter fold

@@ -27,7 +27,8 @@ PS_CX int LD(int D) { return D + 1; }            // padded row stride of a share
 PS_CX int FNW(int D) { return 3 * D * D + 2 * D; } // full filter aggregate: A, b, C, eta, J
 PS_CX int SNW(int D) { return 2 * D * D + D; }     // full smoother aggregate: E, g, L
 PS_CX int CNW(int D) { return D + D * (D + 1) / 2; } // filtered (x, P packed upper)
-PS_CX int MODW(int D) { return 3 * D * D + D + 2; }  // model: F, Q, Pinf, H, r, udt
+PS_CX int MODW(int D) { return 4 * D * D + D + 2; }  // model: F, Q, Pinf, H, r, udt, G
+PS_CX int FQW(int D) { return 2 * D * LD(D); }     // per-step F, Q (rows of stride LD) in kPade mode
 
 struct WParams {
     const double* t;
@@ -50,6 +51,7 @@ struct WParams {
     int rank, world;
     unsigned long long* err;
     int store_state;
+    const double* fq;           // per-step (F, Q) [n(+1)][FQW] from kw_discretize (irregular dt), else NULL
 };
 
 // ------------------------------------------------------------------ shared-memory model
@@ -558,10 +560,127 @@ __device__ void wapply_suffix(const SS<D>& a, double* m, double (*P)[LD(D)], Scr
 
 // ------------------------------------------------------------------ discretisation (table)
 // returns 0 (F, Q valid in fz / via model), 1 = dt == 0 (identity), 2 = unsupported
-__device__ __forceinline__ int wdisc_kind(double dt, double udt) {
+__device__ __forceinline__ int wdisc_kind(double dt, double udt, bool stream = false) {
+    if (stream) return dt == 0.0 ? 1 : 0;           // per-step (F, Q) from kw_discretize
     if (fabs(dt - udt) <= 1e-12 * udt) return 0;   // uniform step up to time-stamp rounding
     if (dt == 0.0) return 1;
     return 2;
+}
+
+// (F, Q) used for local step k: the model's table, or the per-step pair of kw_discretize
+template <int D>
+struct FQp {
+    const double (*F)[LD(D)];
+    const double (*Q)[LD(D)];
+};
+template <int D>
+__device__ __forceinline__ FQp<D> wfq(const WParams& p, const SModel<D>& M, int64_t k) {
+    if (p.fq) {
+        const double (*b)[LD(D)] = reinterpret_cast<const double (*)[LD(D)]>(p.fq + k * FQW(D));
+        return {b, b + D};
+    }
+    return {M.F, M.Q};
+}
+
+// ------------------------------------------------------------------ KDw: per-step discretisation
+// One warp per step (grid-stride): F = expm(G dt) by scaling and squaring with the
+// [7/7] Pade approximant (Higham 2005, theta_7 = 0.9504), Q = P_inf - F P_inf^T F^T
+// (Lyapunov form of the stationary model).  Writes fq[k] for local steps
+// k in [0, nfq) with a predecessor (global index > 0) and dt != 0.
+template <int D>
+struct KDSmem {
+    double G[D][LD(D)];
+    double Pinf[D][LD(D)];
+    double gnorm;
+    struct PerWarp {
+        double A[D][LD(D)], A2[D][LD(D)], A4[D][LD(D)], A6[D][LD(D)], T[D][LD(D)], U[D][LD(D)];
+        double W2[D][2 * D + 1];
+    } w[kWWarps];
+};
+
+template <int D>
+__global__ void __launch_bounds__(32 * kWWarps) kw_discretize(const double* __restrict__ t, int64_t nfq, int64_t k0,
+                                                               const double* __restrict__ model, double* fq,
+                                                               unsigned long long* err) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    KDSmem<D>& sh = *reinterpret_cast<KDSmem<D>*>(smem_raw);
+    for (int e = threadIdx.x; e < D * D; e += blockDim.x) {
+        const int i = e / D, j = e - (e / D) * D;
+        sh.G[i][j] = model[3 * D * D + D + 2 + e];
+        sh.Pinf[i][j] = model[2 * D * D + e];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double nrm = 0.0;
+        for (int j = 0; j < D; ++j) {
+            double c = 0.0;
+            for (int i = 0; i < D; ++i) c += fabs(sh.G[i][j]);
+            nrm = fmax(nrm, c);
+        }
+        sh.gnorm = nrm;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    auto& W = sh.w[wid];
+    constexpr double b0 = 17297280.0, b1 = 8648640.0, b2 = 1995840.0, b3 = 277200.0, b4 = 25200.0,
+                     b5 = 1512.0, b6 = 56.0, b7 = 1.0;
+    const int64_t nw = static_cast<int64_t>(gridDim.x) * kWWarps;
+    for (int64_t k = static_cast<int64_t>(blockIdx.x) * kWWarps + wid; k < nfq; k += nw) {
+        if (k0 + k == 0) continue;
+        const double dt = __ldg(t + k) - __ldg(t + k - 1);
+        if (dt == 0.0 || !(dt == dt)) continue;
+        const double nrm = sh.gnorm * fabs(dt);
+        int s = 0;
+        if (nrm > 0.9504) frexp(nrm / 0.9504, &s);
+        const double sc = ldexp(dt, -s);
+        for (int e = lane; e < D * D; e += 32) W.A[e / D][e % D] = sh.G[e / D][e % D] * sc;
+        __syncwarp();
+        wmm<D>(W.A2, W.A, W.A, nullptr, lane);
+        __syncwarp();
+        wmm<D>(W.A4, W.A2, W.A2, nullptr, lane);
+        __syncwarp();
+        wmm<D>(W.A6, W.A4, W.A2, nullptr, lane);
+        __syncwarp();
+        for (int e = lane; e < D * D; e += 32) {
+            const int i = e / D, j = e - (e / D) * D;
+            const double id = (i == j) ? 1.0 : 0.0;
+            W.T[i][j] = fma(b7, W.A6[i][j], fma(b5, W.A4[i][j], fma(b3, W.A2[i][j], b1 * id)));
+            W.U[i][j] = fma(b6, W.A6[i][j], fma(b4, W.A4[i][j], fma(b2, W.A2[i][j], b0 * id)));  // V
+        }
+        __syncwarp();
+        wmm<D>(W.A6, W.A, W.T, nullptr, lane);                     // U = A T  (A6 reused)
+        __syncwarp();
+        for (int e = lane; e < D * D; e += 32) {
+            const int i = e / D, j = e - (e / D) * D;
+            W.A2[i][j] = W.U[i][j] - W.A6[i][j];                   // V - U
+            W.A4[i][j] = W.U[i][j] + W.A6[i][j];                   // V + U
+        }
+        __syncwarp();
+        if (!winverse<D>(W.A2, W.W2, lane) && lane == 0) raise_error(err, k0 + k, kErrNumeric);
+        wmm<D>(W.A, W.A2, W.A4, nullptr, lane);                    // F = (V - U)^-1 (V + U)
+        __syncwarp();
+        double (*F)[LD(D)] = W.A;
+        double (*Fs)[LD(D)] = W.T;
+        for (int q = 0; q < s; ++q) {
+            wmm<D>(Fs, F, F, nullptr, lane);
+            __syncwarp();
+            double (*tmp)[LD(D)] = F; F = Fs; Fs = tmp;
+        }
+        // Q = P_inf - (F P_inf) F^T
+        wmm<D>(W.U, F, sh.Pinf, nullptr, lane);
+        __syncwarp();
+        for (int e = lane; e < D * D; e += 32) W.U[e / D][e % D] = -W.U[e / D][e % D];
+        __syncwarp();
+        wmm<D, false, true>(W.A6, W.U, F, sh.Pinf, lane);
+        __syncwarp();
+        double* o = fq + k * FQW(D);
+        for (int e = lane; e < D * D; e += 32) {
+            const int i = e / D, j = e - (e / D) * D;
+            o[i * LD(D) + j] = F[i][j];
+            o[(D + i) * LD(D) + j] = 0.5 * (W.A6[i][j] + W.A6[j][i]);
+        }
+        __syncwarp();
+    }
 }
 
 // ------------------------------------------------------------------ K1w: fold
@@ -599,7 +718,8 @@ __global__ void __launch_bounds__(32 * kWWarps) kw_filter_fold(const WParams p) 
         const int64_t g = p.k0 + k;
         int kind = 0;
         if (g == 0) kind = 3;                                   // F = 0, Q = P_inf
-        else kind = wdisc_kind(tk - tprev, M.udt);
+        else kind = wdisc_kind(tk - tprev, M.udt, p.fq != nullptr);
+        const FQp<D> fqp = wfq<D>(p, M, k);
         if (lane == 0) {
             if (g > 0 && !(tk - tprev >= 0.0)) raise_error(p.err, g, kErrInput);
             if (!isfinite(tk) || (obs && !isfinite(yk))) raise_error(p.err, g, kErrInput);
@@ -608,15 +728,15 @@ __global__ void __launch_bounds__(32 * kWWarps) kw_filter_fold(const WParams p) 
         tprev = tk;
         // FA = F A, T = F C, Fb = F b, Cm = T F^T + Q   (kind 1: F = I, Q = 0; kind 3: F = 0, Q = P_inf)
         if (kind == 0) {
-            wmm<D>(W.FA, M.F, W.a.A, nullptr, lane);
-            wmm<D>(W.T, M.F, W.a.C, nullptr, lane);
+            wmm<D>(W.FA, fqp.F, W.a.A, nullptr, lane);
+            wmm<D>(W.T, fqp.F, W.a.C, nullptr, lane);
             for (int i = lane; i < D; i += 32) {
                 double s = 0.0;
-                for (int q = 0; q < D; ++q) s = fma(M.F[i][q], W.a.b[q], s);
+                for (int q = 0; q < D; ++q) s = fma(fqp.F[i][q], W.a.b[q], s);
                 W.Fb[i] = s;
             }
             __syncwarp();
-            wmm<D, false, true>(W.Cm, W.T, M.F, M.Q, lane);
+            wmm<D, false, true>(W.Cm, W.T, fqp.F, fqp.Q, lane);
         } else {
             for (int e = lane; e < D * D; e += 32) {
                 const int i = e / D, j = e - (e / D) * D;
@@ -758,20 +878,21 @@ __global__ void __launch_bounds__(32 * kWWarps) kw_filter_apply(const WParams p)
         const bool obs = __ldg(p.mask + k) != 0;
         const double yk = obs ? __ldg(p.y + k) : 0.0;
         const int64_t g = p.k0 + k;
-        const int kind = (g == 0) ? 3 : wdisc_kind(tk - tprev, M.udt);
+        const int kind = (g == 0) ? 3 : wdisc_kind(tk - tprev, M.udt, p.fq != nullptr);
+        const FQp<D> fqp = wfq<D>(p, M, k);
         const bool first = (k == kb);
         tprev = tk;
         // predict: xm = F x, FP = F P, Pm = FP F^T + Q ; Sm = Sg F^T
         if (kind == 0) {
-            wmm<D>(W.u.st.FP, M.F, W.P, nullptr, lane);
-            if (!first) wmm<D, false, true>(W.u.st.Sm, W.u.st.Sg, M.F, nullptr, lane);
+            wmm<D>(W.u.st.FP, fqp.F, W.P, nullptr, lane);
+            if (!first) wmm<D, false, true>(W.u.st.Sm, W.u.st.Sg, fqp.F, nullptr, lane);
             for (int i = lane; i < D; i += 32) {
                 double s = 0.0;
-                for (int q = 0; q < D; ++q) s = fma(M.F[i][q], W.x[q], s);
+                for (int q = 0; q < D; ++q) s = fma(fqp.F[i][q], W.x[q], s);
                 W.u.st.xm[i] = s;
             }
             __syncwarp();
-            wmm<D, false, true>(W.u.st.Pm, W.u.st.FP, M.F, M.Q, lane);
+            wmm<D, false, true>(W.u.st.Pm, W.u.st.FP, fqp.F, fqp.Q, lane);
         } else {
             for (int e = lane; e < D * D; e += 32) {
                 const int i = e / D, j = e - (e / D) * D;
@@ -847,15 +968,16 @@ __global__ void __launch_bounds__(32 * kWWarps) kw_filter_apply(const WParams p)
         __syncwarp();
     } else {
         const double tn = __ldg(p.t + ke);
-        const int kind = wdisc_kind(tn - tprev, M.udt);
+        const int kind = wdisc_kind(tn - tprev, M.udt, p.fq != nullptr);
+        const FQp<D> fqp = wfq<D>(p, M, ke);
         // Pm, xm of the next step; Sm = Sg F^T
         for (int e = lane; e < D * D; e += 32) {
             const int i = e / D, j = e - (e / D) * D;
             double fp = 0.0, sm = 0.0;
             if (kind == 0) {
                 for (int q = 0; q < D; ++q) {
-                    fp = fma(M.F[i][q], W.P[q][j], fp);
-                    sm = fma(W.u.st.Sg[i][q], M.F[j][q], sm);
+                    fp = fma(fqp.F[i][q], W.P[q][j], fp);
+                    sm = fma(W.u.st.Sg[i][q], fqp.F[j][q], sm);
                 }
             } else {
                 fp = W.P[i][j];
@@ -867,7 +989,7 @@ __global__ void __launch_bounds__(32 * kWWarps) kw_filter_apply(const WParams p)
         for (int i = lane; i < D; i += 32) {
             double s = 0.0;
             if (kind == 0)
-                for (int q = 0; q < D; ++q) s = fma(M.F[i][q], W.x[q], s);
+                for (int q = 0; q < D; ++q) s = fma(fqp.F[i][q], W.x[q], s);
             else
                 s = W.x[i];
             W.u.st.xm[i] = s;
@@ -875,9 +997,9 @@ __global__ void __launch_bounds__(32 * kWWarps) kw_filter_apply(const WParams p)
         __syncwarp();
         for (int e = lane; e < D * D; e += 32) {
             const int i = e / D, j = e - (e / D) * D;
-            double s = (kind == 0) ? M.Q[i][j] : 0.0;
+            double s = (kind == 0) ? fqp.Q[i][j] : 0.0;
             if (kind == 0)
-                for (int q = 0; q < D; ++q) s = fma(W.u.st.FP[i][q], M.F[j][q], s);
+                for (int q = 0; q < D; ++q) s = fma(W.u.st.FP[i][q], fqp.F[j][q], s);
             else
                 s = W.u.st.FP[i][j];
             W.u.st.Pm[i][j] = s;
@@ -983,16 +1105,17 @@ __global__ void __launch_bounds__(32 * kWWarps) kw_smoother_apply(const WParams 
             for (int i = lane; i < D; i += 32) W.ms[i] = W.u.st.x[i];
             __syncwarp();
         } else {
-            const int kind = wdisc_kind(tnext - tk, M.udt);
+            const int kind = wdisc_kind(tnext - tk, M.udt, p.fq != nullptr);
+            const FQp<D> fqp = wfq<D>(p, M, k + 1);
             if (kind == 0) {
-                wmm<D>(W.u.st.FP, M.F, W.u.st.P, nullptr, lane);                       // F P
+                wmm<D>(W.u.st.FP, fqp.F, W.u.st.P, nullptr, lane);                     // F P
                 for (int i = lane; i < D; i += 32) {
                     double s2 = 0.0;
-                    for (int q = 0; q < D; ++q) s2 = fma(M.F[i][q], W.u.st.x[q], s2);
+                    for (int q = 0; q < D; ++q) s2 = fma(fqp.F[i][q], W.u.st.x[q], s2);
                     W.u.st.xm[i] = s2;
                 }
                 __syncwarp();
-                wmm<D, false, true>(W.u.st.Pm, W.u.st.FP, M.F, M.Q, lane);             // F P F^T + Q
+                wmm<D, false, true>(W.u.st.Pm, W.u.st.FP, fqp.F, fqp.Q, lane);         // F P F^T + Q
             } else {
                 for (int e = lane; e < D * D; e += 32) {
                     const int i = e / D, j = e - (e / D) * D;

@@ -126,13 +126,14 @@ def metric_workload(n: int = 2 ** 24, uniform: bool = False, kind: str = "matern
                     uniform_dt=H_FINE if uniform else 0.0)
 
 
-def config3(n: int = 2 ** 22, order: int = 6) -> Workload:
-    """C3: RBF Taylor order 6, uniform dt = h, every 16th point missing."""
-    t = np.arange(n, dtype=np.float64) * H_FINE
+def config3(n: int = 2 ** 22, order: int = 6, irregular: bool = False) -> Workload:
+    """C3: RBF Taylor order 6, uniform dt = h, every 16th point missing.
+    irregular=True: the jittered grid of the metric workload instead (device Pade path)."""
+    t = jittered_grid(n) if irregular else np.arange(n, dtype=np.float64) * H_FINE
     mask = (np.arange(n) % 16 != 15).astype(np.uint8)
     y = _apply_mask(_noisy(sinusoid(t), 0.1), mask)
-    return Workload("C3", [Component("rbf", 1.0, 0.5, order=order)], 0.01, t, y, mask,
-                    uniform_dt=H_FINE)
+    return Workload("C3" + ("_irregular" if irregular else ""), [Component("rbf", 1.0, 0.5, order=order)], 0.01,
+                    t, y, mask, uniform_dt=0.0 if irregular else H_FINE)
 
 
 def co2_like(t: np.ndarray) -> np.ndarray:
@@ -141,18 +142,19 @@ def co2_like(t: np.ndarray) -> np.ndarray:
             + 3 * np.sin(2 * np.pi * t) + 0.8 * np.sin(4 * np.pi * t + 1) + 0.3 * np.cos(6 * np.pi * t))
 
 
-def config4(n: int = 2 ** 24, harmonics: int = 6) -> Workload:
+def config4(n: int = 2 ** 24, harmonics: int = 6, irregular: bool = False) -> Workload:
     """C4: Periodic(J=6) + Matern-3/2 trend, weekly cadence.  The
     time unit is the WEEK so the grid t_k = k is exactly uniform (dt = 1): period
     52 weeks, trend lengthscale 20 years = 1040 weeks."""
-    t = np.arange(n, dtype=np.float64)
+    t = jittered_grid(n, h=1.0) if irregular else np.arange(n, dtype=np.float64)
     mask = (np.arange(n) % 16 != 15).astype(np.uint8)
     y = _noisy(co2_like(t / 52.0), 0.3)
     y = (y - y.mean()) / y.std()
     y = _apply_mask(y, mask)
     comps = [Component("periodic", 4.0, 1.0, period=52.0, order=harmonics),
              Component("matern32", 10.0, 20.0 * 52.0)]
-    return Workload("C4", comps, 0.09, t, y, mask, uniform_dt=1.0)
+    return Workload("C4" + ("_irregular" if irregular else ""), comps, 0.09, t, y, mask,
+                    uniform_dt=0.0 if irregular else 1.0)
 
 
 def co2_product(n: int = 3192, order: int = 2) -> Workload:

@@ -335,3 +335,47 @@ def test_batched_series(cuda_device, kind):
             assert em <= MEAN_TOL and ev <= VAR_TOL and en <= NLL_TOL, (b, em, ev, en)
         else:
             np.testing.assert_allclose(var[sl], o["var"], rtol=VAR_TOL)
+
+
+def _irregular(comps, noise_var, n, seed, dt_scale=0.02, p_missing=0.3, ties=3):
+    base = synth.random_problem(seed, n, kind="matern52", p_missing=p_missing, ties=ties, dt_scale=dt_scale,
+                                noise_var=noise_var)
+    return synth.Workload(f"irregular_{seed}_{n}", comps, noise_var, base.t, base.y, base.mask)
+
+
+PADE_MODELS = {
+    "rbf3": [synth.Component("rbf", 1.3, 0.8, order=3)],
+    "m12+m32": [synth.Component("matern12", 1.0, 0.3), synth.Component("matern32", 2.0, 1.5)],
+    "rbf6": [synth.Component("rbf", 1.0, 0.5, order=6)],
+    "per3+m32": [synth.Component("periodic", 1.5, 1.0, period=0.7, order=3), synth.Component("matern32", 1.0, 2.0)],
+    "per6+m32": [synth.Component("periodic", 4.0, 1.0, period=1.0, order=6), synth.Component("matern32", 10.0, 20.0)],
+    "quasi1": [synth.Component("quasiperiodic", 2.0, 1.0, period=0.5, order=1, mat_lengthscale=3.0, mat_nu2=3)],
+}
+
+
+@pytest.mark.parametrize("name", list(PADE_MODELS))
+def test_irregular_pade_models(cuda_device, name):
+    """Irregular time grid for models without a closed form (uniform_dt = 0): per-step
+    expm by [7/7] Pade scaling and squaring on the device (north_star discretisation
+    kernel), thread path for d <= 3 and kw_discretize + warp path above."""
+    comps = PADE_MODELS[name]
+    n = 20011 if name in ("rbf3", "m12+m32", "rbf6") else 4001
+    w = _irregular(comps, 0.05, n, seed=len(name))
+    assert_parity(w)
+
+
+def test_irregular_pade_small_chains_and_sharding(cuda_device):
+    w = _irregular(PADE_MODELS["rbf6"], 0.05, 9001, seed=31, dt_scale=0.01)
+    assert_parity(w, chain_len=3)
+    ref_mean, ref_var, ref_nll, _ = run_gpu(w)
+    from paper_2102_09964_b200 import sharded
+    for world in (2, 3):
+        mean, var, nll = sharded.run_virtual(w.components, w.noise_var, w.t, w.y, w.mask, world)
+        assert np.max(np.abs(mean - ref_mean)) / np.max(np.abs(ref_mean)) < 1e-10
+        assert np.max(np.abs(var - ref_var) / ref_var) < 1e-10
+        assert abs(nll - ref_nll) < 1e-10 * abs(ref_nll)
+    w3 = _irregular(PADE_MODELS["rbf3"], 0.05, 9001, seed=32, dt_scale=0.01)
+    ref_mean, ref_var, ref_nll, _ = run_gpu(w3)
+    mean, var, nll = sharded.run_virtual(w3.components, w3.noise_var, w3.t, w3.y, w3.mask, 3)
+    assert np.max(np.abs(mean - ref_mean)) / np.max(np.abs(ref_mean)) < 1e-10
+    assert abs(nll - ref_nll) < 1e-10 * abs(ref_nll)

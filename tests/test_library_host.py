@@ -141,3 +141,24 @@ def test_quasiperiodic_model_matches_oracle():
         om = ossm.build(w.components)
         taus = np.linspace(0, 200.0, 41)
         np.testing.assert_allclose(ossm.ssm_kernel(lm, taus), ossm.ssm_kernel(om, taus), rtol=1e-10, atol=1e-12)
+
+
+@pytest.mark.parametrize("comps", [
+    [synth.Component("rbf", 1.0, 0.5, order=2)],
+    [synth.Component("rbf", 1.3, 0.8, order=3)],
+    [synth.Component("matern12", 1.0, 0.3), synth.Component("matern32", 2.0, 1.5)],
+    [synth.Component("periodic", 1.5, 1.0, period=0.7, order=0)]])
+@pytest.mark.parametrize("dt", [0.0, 1e-9, 2.4e-7, 1.22e-4, 1e-3, 0.02, 0.3, 1.0, 2.5, 8.0])
+def test_pade_discretisation_vs_oracle(comps, dt):
+    """kPade mode (no closed form, uniform_dt = 0): F = expm(G dt) by [7/7] Pade scaling and
+    squaring, Q = P_inf - F P_inf F^T, host-compiled from the same device source, vs the
+    oracle's Pade-13 + sub-stepped Van Loan."""
+    m = P.Model(comps, 0.1)
+    assert m.state_dim <= 3
+    lm, s = _lib_ssm(m.h)
+    F, Q = m.discretize(dt)
+    Fo, Qo = oracle.discretize(lm, dt)
+    assert np.max(np.abs(F - Fo)) <= 1e-13 * max(1.0, np.max(np.abs(Fo)))
+    assert np.max(np.abs(Q - Qo)) <= 1e-13 * np.max(np.abs(s["Pinf"]))
+    if dt == 0.0:
+        assert np.array_equal(F, np.eye(m.state_dim)) and np.all(Q == 0.0)
