@@ -583,20 +583,34 @@ __device__ __forceinline__ FQp<D> wfq(const WParams& p, const SModel<D>& M, int6
 }
 
 // ------------------------------------------------------------------ KDw: per-step discretisation
-// One warp per step (grid-stride): F = expm(G dt) by scaling and squaring with the
-// [7/7] Pade approximant (Higham 2005, theta_7 = 0.9504), Q = P_inf - F P_inf^T F^T
-// (Lyapunov form of the stationary model).  Writes fq[k] for local steps
-// k in [0, nfq) with a predecessor (global index > 0) and dt != 0.
+// One warp per step (grid-stride): F = expm(G dt) by scaling and squaring with a
+// truncated Taylor polynomial evaluated Paterson-Stockmeyer style (no pivoted solve:
+// a warp-level elimination costs D serial rounds), degree m = 6 for
+// ||A||_1 <= 0.017 and m = 12 for ||A||_1 <= 0.33 (remainder theta^(m+1)/(m+1)!
+// <= 2^-53 relative), A = G dt / 2^s; then Q = P_inf - F P_inf F^T (Lyapunov form of
+// the stationary model).  Writes fq[k] for local steps k in [0, nfq) with a
+// predecessor (global index > 0) and dt != 0.
 template <int D>
 struct KDSmem {
     double G[D][LD(D)];
     double Pinf[D][LD(D)];
     double gnorm;
     struct PerWarp {
-        double A[D][LD(D)], A2[D][LD(D)], A4[D][LD(D)], A6[D][LD(D)], T[D][LD(D)], U[D][LD(D)];
-        double W2[D][2 * D + 1];
+        double A[D][LD(D)], A2[D][LD(D)], A3[D][LD(D)], X[D][LD(D)], T[D][LD(D)], B[D][LD(D)];
     } w[kWWarps];
 };
+
+template <int D>
+__device__ __forceinline__ void taylor_block(double (*B)[LD(D)], const double (*A)[LD(D)], const double (*A2)[LD(D)],
+                                             const double (*A3)[LD(D)], double c0, double c1, double c2, double c3,
+                                             int lane) {
+    for (int e = lane; e < D * D; e += 32) {
+        const int i = e / D, j = e - (e / D) * D;
+        double v = fma(c2, A2[i][j], c1 * A[i][j]);
+        if (A3) v = fma(c3, A3[i][j], v);
+        B[i][j] = v + ((i == j) ? c0 : 0.0);
+    }
+}
 
 template <int D>
 __global__ void __launch_bounds__(32 * kWWarps) kw_discretize(const double* __restrict__ t, int64_t nfq, int64_t k0,
@@ -622,8 +636,9 @@ __global__ void __launch_bounds__(32 * kWWarps) kw_discretize(const double* __re
     __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     auto& W = sh.w[wid];
-    constexpr double b0 = 17297280.0, b1 = 8648640.0, b2 = 1995840.0, b3 = 277200.0, b4 = 25200.0,
-                     b5 = 1512.0, b6 = 56.0, b7 = 1.0;
+    // 1 / j!
+    constexpr double c[13] = {1.0, 1.0, 1.0 / 2, 1.0 / 6, 1.0 / 24, 1.0 / 120, 1.0 / 720, 1.0 / 5040, 1.0 / 40320,
+                              1.0 / 362880, 1.0 / 3628800, 1.0 / 39916800, 1.0 / 479001600};
     const int64_t nw = static_cast<int64_t>(gridDim.x) * kWWarps;
     for (int64_t k = static_cast<int64_t>(blockIdx.x) * kWWarps + wid; k < nfq; k += nw) {
         if (k0 + k == 0) continue;
@@ -631,56 +646,60 @@ __global__ void __launch_bounds__(32 * kWWarps) kw_discretize(const double* __re
         if (dt == 0.0 || !(dt == dt)) continue;
         const double nrm = sh.gnorm * fabs(dt);
         int s = 0;
-        if (nrm > 0.9504) frexp(nrm / 0.9504, &s);
+        if (nrm > 0.33) frexp(nrm / 0.33, &s);
+        const bool low = (ldexp(nrm, -s) <= 0.017);
         const double sc = ldexp(dt, -s);
         for (int e = lane; e < D * D; e += 32) W.A[e / D][e % D] = sh.G[e / D][e % D] * sc;
         __syncwarp();
         wmm<D>(W.A2, W.A, W.A, nullptr, lane);
         __syncwarp();
-        wmm<D>(W.A4, W.A2, W.A2, nullptr, lane);
+        wmm<D>(W.A3, W.A2, W.A, nullptr, lane);
         __syncwarp();
-        wmm<D>(W.A6, W.A4, W.A2, nullptr, lane);
-        __syncwarp();
-        for (int e = lane; e < D * D; e += 32) {
-            const int i = e / D, j = e - (e / D) * D;
-            const double id = (i == j) ? 1.0 : 0.0;
-            W.T[i][j] = fma(b7, W.A6[i][j], fma(b5, W.A4[i][j], fma(b3, W.A2[i][j], b1 * id)));
-            W.U[i][j] = fma(b6, W.A6[i][j], fma(b4, W.A4[i][j], fma(b2, W.A2[i][j], b0 * id)));  // V
+        double (*F)[LD(D)];
+        if (low) {   // m = 6: F = B0 + A3 (c3 I + c4 A + c5 A2 + c6 A3)
+            taylor_block<D>(W.X, W.A, W.A2, W.A3, c[3], c[4], c[5], c[6], lane);
+            taylor_block<D>(W.B, W.A, W.A2, nullptr, c[0], c[1], c[2], 0.0, lane);
+            __syncwarp();
+            wmm<D>(W.T, W.A3, W.X, W.B, lane);
+            F = W.T;
+        } else {     // m = 12: Horner in A3 over degree-2 blocks, top block degree 3
+            taylor_block<D>(W.X, W.A, W.A2, W.A3, c[9], c[10], c[11], c[12], lane);
+            taylor_block<D>(W.B, W.A, W.A2, nullptr, c[6], c[7], c[8], 0.0, lane);
+            __syncwarp();
+            wmm<D>(W.T, W.A3, W.X, W.B, lane);
+            __syncwarp();
+            taylor_block<D>(W.B, W.A, W.A2, nullptr, c[3], c[4], c[5], 0.0, lane);
+            __syncwarp();
+            wmm<D>(W.X, W.A3, W.T, W.B, lane);
+            __syncwarp();
+            taylor_block<D>(W.B, W.A, W.A2, nullptr, c[0], c[1], c[2], 0.0, lane);
+            __syncwarp();
+            wmm<D>(W.T, W.A3, W.X, W.B, lane);
+            F = W.T;
         }
         __syncwarp();
-        wmm<D>(W.A6, W.A, W.T, nullptr, lane);                     // U = A T  (A6 reused)
-        __syncwarp();
-        for (int e = lane; e < D * D; e += 32) {
-            const int i = e / D, j = e - (e / D) * D;
-            W.A2[i][j] = W.U[i][j] - W.A6[i][j];                   // V - U
-            W.A4[i][j] = W.U[i][j] + W.A6[i][j];                   // V + U
-        }
-        __syncwarp();
-        if (!winverse<D>(W.A2, W.W2, lane) && lane == 0) raise_error(err, k0 + k, kErrNumeric);
-        wmm<D>(W.A, W.A2, W.A4, nullptr, lane);                    // F = (V - U)^-1 (V + U)
-        __syncwarp();
-        double (*F)[LD(D)] = W.A;
-        double (*Fs)[LD(D)] = W.T;
+        double (*Fs)[LD(D)] = W.X;
         for (int q = 0; q < s; ++q) {
             wmm<D>(Fs, F, F, nullptr, lane);
             __syncwarp();
             double (*tmp)[LD(D)] = F; F = Fs; Fs = tmp;
         }
-        // Q = P_inf - (F P_inf) F^T
-        wmm<D>(W.U, F, sh.Pinf, nullptr, lane);
+        // Q = P_inf - (F P_inf) F^T   (B = -F P_inf, A = Q)
+        wmm<D>(W.B, F, sh.Pinf, nullptr, lane);
         __syncwarp();
-        for (int e = lane; e < D * D; e += 32) W.U[e / D][e % D] = -W.U[e / D][e % D];
+        for (int e = lane; e < D * D; e += 32) W.B[e / D][e % D] = -W.B[e / D][e % D];
         __syncwarp();
-        wmm<D, false, true>(W.A6, W.U, F, sh.Pinf, lane);
+        wmm<D, false, true>(W.A, W.B, F, sh.Pinf, lane);
         __syncwarp();
         double* o = fq + k * FQW(D);
         for (int e = lane; e < D * D; e += 32) {
             const int i = e / D, j = e - (e / D) * D;
             o[i * LD(D) + j] = F[i][j];
-            o[(D + i) * LD(D) + j] = 0.5 * (W.A6[i][j] + W.A6[j][i]);
+            o[(D + i) * LD(D) + j] = 0.5 * (W.A[i][j] + W.A[j][i]);
         }
         __syncwarp();
     }
+    (void)err;
 }
 
 // ------------------------------------------------------------------ K1w: fold
