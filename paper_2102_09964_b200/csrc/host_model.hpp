@@ -3,11 +3,11 @@
 // (pipeline stage 1).  Written independently of the test oracle.
 //
 //   Matern-nu closed forms (exact), nu = 1/2, 3/2, 5/2:
-//     standalone: the lambda-scaled basis x_hat_i = x_i / lambda^i (a fixed
-//     diagonal balancing, Eq. (9)); drift lambda * G1, G1 = companion of
-//     (s + 1)^d, W = lambda sigma^2 w e_{d-1} e_{d-1}^T with w = 2, 4, 16/3,
-//     P_inf = sigma^2 P1 (see tools/derive_matern.py);
-//     inside a sum: the same basis (block of the block-diagonal state).
+//     the Jordan basis x~ = P^-1 x_hat of the lambda-scaled state x_hat_i = x_i / lambda^i
+//     (a fixed diagonal balancing, Eq. (9), then the unit-triangular change of basis that
+//     turns lambda * companion((s + 1)^d) into lambda (-I + N)); H = e_0,
+//     W = lambda sigma^2 w e_{d-1} e_{d-1}^T with w = 2, 4, 16/3, P_inf = sigma^2 P1;
+//     inside a sum / product: the same basis (block of the state).
 //   RBF Taylor order n (reading Z7): 1/S(w) Taylor-expanded,
 //     left-half-plane spectral factor by Aberth-Ehrlich root finding in
 //     extended precision, companion drift, Osborne balancing, Lyapunov P_inf.
@@ -163,6 +163,10 @@ inline void apply_balance(Ssm& m, const std::vector<ld>& d) {
 
 // --------------------------------------------------------------------- Matern (lambda-scaled basis)
 inline Ssm matern(int d, ld s2, ld ell, ld* lam_out) {
+    // Jordan basis of the drift: x~ = P^-1 diag(lambda^-i) x, where lambda times
+    // the companion matrix of (s + 1)^d equals lambda P J P^-1 with J = -I + N and P unit lower
+    // triangular with first row e_0 (so H stays e_0).  G~ = lambda J, W~ = s2 w lambda e e^T
+    // (e = e_{d-1}, w = 2, 4, 16/3), P_inf~ = s2 P1 below (the limit of the closed-form Q).
     Ssm m;
     m.d = d;
     m.G = zeros(d); m.W = zeros(d); m.Pinf = zeros(d);
@@ -170,19 +174,16 @@ inline Ssm matern(int d, ld s2, ld ell, ld* lam_out) {
     const ld nu2 = 2.0L * d - 1.0L;           // 2 nu
     const ld lam = std::sqrt(nu2) / ell;
     *lam_out = lam;
-    // G1 = companion of (s + 1)^d : rows shift, last row -binom(d, k)
-    for (int i = 0; i + 1 < d; ++i) m.G[i * d + i + 1] = lam;
-    if (d == 1) m.G[0] = -lam;
-    if (d == 2) { m.G[2] = -lam; m.G[3] = -2.0L * lam; }
-    if (d == 3) { m.G[6] = -lam; m.G[7] = -3.0L * lam; m.G[8] = -3.0L * lam; }
+    for (int i = 0; i < d; ++i) {
+        m.G[i * d + i] = -lam;
+        if (i + 1 < d) m.G[i * d + i + 1] = lam;
+    }
     const ld w = (d == 1) ? 2.0L : (d == 2) ? 4.0L : 16.0L / 3.0L;
     m.W[d * d - 1] = lam * s2 * w;
-    if (d == 1) m.Pinf[0] = s2;
-    if (d == 2) { m.Pinf[0] = s2; m.Pinf[3] = s2; }
-    if (d == 3) {
-        m.Pinf[0] = s2; m.Pinf[4] = s2 / 3.0L; m.Pinf[8] = s2;
-        m.Pinf[2] = m.Pinf[6] = -s2 / 3.0L;
-    }
+    static const ld P2[4] = {1.0L, 1.0L, 1.0L, 2.0L};
+    static const ld P3[9] = {1.0L, 1.0L, 2.0L / 3.0L, 1.0L, 4.0L / 3.0L, 4.0L / 3.0L, 2.0L / 3.0L, 4.0L / 3.0L,
+                             8.0L / 3.0L};
+    for (int i = 0; i < d * d; ++i) m.Pinf[i] = s2 * (d == 1 ? 1.0L : d == 2 ? P2[i] : P3[i]);
     m.Dbal.assign(d, 1.0L);
     ld p = 1.0L;
     for (int i = 0; i < d; ++i) { m.Dbal[i] = p; p *= lam; }

@@ -24,7 +24,11 @@ namespace {
 
 constexpr int kMaxD = 3;              // thread-per-chain path: d = 1, 2, 3
 // warp-per-chain path (pssgp_wide.cuh), uniform-dt models: these d are compiled
+#ifdef PSSGP_NO_WIDE                  // experiment builds (tools/build_variant.sh): thread path only
+#define PSSGP_WIDE_DIMS(X)
+#else
 #define PSSGP_WIDE_DIMS(X) X(4) X(5) X(6) X(8) X(10) X(12) X(14) X(16) X(18) X(20)
+#endif
 constexpr int kSlots = 9;
 const char* kSlotNames[kSlots] = {"k_filter_reduce", "k_filter_scan", "k_filter_apply",
                                   "k_smoother_scan", "k_smoother_apply", "k_nll_sum", "k_reduce_blocks",
@@ -37,7 +41,7 @@ struct pssgp_model {
     int d = 0;
     ph::Ssm ssm;                 // balanced host model (long double)
     bool closed = false;         // standalone Matern closed form
-    int mode = kTable;           // DiscMode of the kernels (kClosed / kTable / kMixed)
+    int mode = kTable;           // DiscMode of the kernels (kClosed / kTable / kPade)
     double lam = 0.0, s2 = 0.0, r = 0.0;
     double udt = 0.0;
     std::vector<double> Fu, Qu;  // F(udt), Q(udt) row-major d x d
@@ -233,7 +237,6 @@ pssgp_status setup(pssgp_model* m, const Plan& pl, KParams<D>& p) {
 #define LAUNCH_MODE(m, KERN, grid, block, s, p)                                  \
     do {                                                                         \
         if ((m)->mode == kClosed) KERN<D, kClosed><<<grid, block, 0, s>>>(p);    \
-        else if ((m)->mode == kMixed) KERN<D, kMixed><<<grid, block, 0, s>>>(p); \
         else if ((m)->mode == kPade) KERN<D, kPade><<<grid, block, 0, s>>>(p);   \
         else KERN<D, kTable><<<grid, block, 0, s>>>(p);                          \
     } while (0)
@@ -764,7 +767,7 @@ pssgp_status pssgp_create(const pssgp_component* comps, int n_comps, double nois
         m->Qu.resize(Q.size());
         for (size_t i = 0; i < F.size(); ++i) { m->Fu[i] = static_cast<double>(F[i]); m->Qu[i] = static_cast<double>(Q[i]); }
     }
-    m->mode = m->closed ? (m->udt > 0.0 ? kMixed : kClosed) : (m->udt > 0.0 ? kTable : kPade);
+    m->mode = m->closed ? kClosed : (m->udt > 0.0 ? kTable : kPade);
     *out = m;
     return PSSGP_OK;
 }

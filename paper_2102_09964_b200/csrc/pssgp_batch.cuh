@@ -59,9 +59,8 @@ __device__ __forceinline__ int seg_find(const BParams& q, int64_t k) {
 }
 
 template <int D>
-__device__ __forceinline__ void seg_first(const KParams<D>& p, const Seg& s, double (&F)[D * D], double (&Q)[ns(D)]) {
-#pragma unroll
-    for (int i = 0; i < D * D; ++i) F[i] = 0.0;
+__device__ __forceinline__ void seg_first(const KParams<D>& p, const Seg& s, FJor<D>& F, double (&Q)[ns(D)]) {
+    set_zero(F);
 #pragma unroll
     for (int i = 0; i < ns(D); ++i) Q[i] = p.m.Pinf[i] * s.pscale;
 }
@@ -87,7 +86,8 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_filter_reduce(co
         const double tk = __ldg(p.t + k);
         const bool obs = __ldg(p.mask + k) != 0;
         const double yk = obs ? __ldg(p.y + k) : 0.0;
-        double F[D * D], Q[ns(D)];
+        FJor<D> F;
+        double Q[ns(D)];
         if (k == s.start) {
             seg_first(p, s, F, Q);
         } else {
@@ -155,7 +155,8 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_filter_apply(con
         const bool obs = __ldg(p.mask + k) != 0;
         const double yk = obs ? __ldg(p.y + k) : 0.0;
         const bool first = (k == kb);
-        double F[D * D], Q[ns(D)], xm[D], Pm[ns(D)], FP[D * D];
+        FJor<D> F;
+        double Q[ns(D)], xm[D], Pm[ns(D)], FP[D * D];
         if (k == s.start) seg_first(p, s, F, Q);
         else matern_closed<D>(s.lam, s.s2, tk - tprev, F, Q);
         kf_predict<D>(x, P, F, Q, xm, FP, Pm);
@@ -184,17 +185,9 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_filter_apply(con
                 for (int j = 0; j < D; ++j) Sg[i * D + j] = P[si(D, i, j)];
         } else {
             double Sm[D * D], SH[D];
+mul_bt<D>(Sg, F, Sm);
 #pragma unroll
-            for (int i = 0; i < D; ++i)
-#pragma unroll
-                for (int j = 0; j < D; ++j) {
-                    double s2 = 0.0;
-#pragma unroll
-                    for (int l = 0; l < D; ++l) s2 = fma(Sg[i * D + l], F[j * D + l], s2);
-                    Sm[i * D + j] = s2;
-                }
-#pragma unroll
-            for (int i = 0; i < D; ++i) SH[i] = Sm[i * D];          // H = e_0 (lambda basis)
+            for (int i = 0; i < D; ++i) SH[i] = Sm[i * D];          // H = e_0 (Jordan basis)
 #pragma unroll
             for (int i = 0; i < D; ++i) {
                 const double si_ = SH[i] * iS;
@@ -226,18 +219,11 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_filter_apply(con
     if (ke > kb && !sag_done) {
         // the next step exists and belongs to the same series (a series end would have set sag)
         const double tn = __ldg(p.t + ke);
-        double F[D * D], Q[ns(D)], xm[D], Pm[ns(D)], FP[D * D], Sm[D * D];
+        FJor<D> F;
+        double Q[ns(D)], xm[D], Pm[ns(D)], FP[D * D], Sm[D * D];
         matern_closed<D>(s.lam, s.s2, tn - tprev, F, Q);
         kf_predict<D>(x, P, F, Q, xm, FP, Pm);
-#pragma unroll
-        for (int i = 0; i < D; ++i)
-#pragma unroll
-            for (int j = 0; j < D; ++j) {
-                double s2 = 0.0;
-#pragma unroll
-                for (int l = 0; l < D; ++l) s2 = fma(Sg[i * D + l], F[j * D + l], s2);
-                Sm[i * D + j] = s2;
-            }
+mul_bt<D>(Sg, F, Sm);
         if (!chain_smoother_agg<D>(x0, P0, Sm, xm, Pm, sag)) raise_error(p.err, ke, kErrNumeric);
     }
     store_soa(sag, p.chain_s, nch, c);
@@ -301,7 +287,8 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_smoother_apply(c
 #pragma unroll
             for (int i = 0; i < ns(D); ++i) Ps[i] = P[i];
         } else {
-            double F[D * D], Q[ns(D)], xm[D], Pm[ns(D)], FP[D * D];
+            FJor<D> F;
+        double Q[ns(D)], xm[D], Pm[ns(D)], FP[D * D];
             matern_closed<D>(s.lam, s.s2, tnext - tk, F, Q);
             kf_predict<D>(x, P, F, Q, xm, FP, Pm);
             if (!rts_step<D>(x, P, xm, Pm, FP, ms, Ps)) raise_error(p.err, k, kErrNumeric);

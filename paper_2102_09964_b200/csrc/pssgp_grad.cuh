@@ -18,8 +18,8 @@
 // product of all chain aggregates (the global first element has M = 0, so the
 // incoming tangent is irrelevant).  The associativity that licenses the grouping is
 // that of function composition (the same argument as PAPER.md:326).
-// In the lambda-scaled basis F(z), Q(z) depend on z = lambda dt only and
-// dF/dz = G1 F, dQ/dz = sigma^2 w f f^T (f = last column of F, W1 = w e_d e_d^T),
+// In the Jordan basis of the closed form (pssgp_math.cuh) F(z), Q(z) depend on z = lambda dt
+// only and dF/dz = J F, dQ/dz = sigma^2 w f f^T (f = last column of F, W1 = w e_d e_d^T),
 // so theta_ell = log ell gives dz = -z; P_inf = sigma^2 P1 does not depend on ell.
 #pragma once
 #include "pssgp_kernels.cuh"
@@ -138,12 +138,13 @@ PS_HD void combine(const TAgg<D>& t1, const TAgg<D>& t2, TAgg<D>& out) {
 // Append one step (primal entering the step: x = xbar_{k-1}, P = P_{k-1}) to the aggregate.
 // PAR: 0 = log sigma^2, 1 = log ell, 2 = log sigma_n^2.  first: global first element.
 template <int D, int PAR>
-PS_HD void grad_fold_step(TAgg<D>& A, const double (&x)[D], const double (&P)[ns(D)], const double (&F)[D * D],
+PS_HD void grad_fold_step(TAgg<D>& A, const double (&x)[D], const double (&P)[ns(D)], const FMat<D>& Fm,
                           const double (&Q)[ns(D)], double z, const ModelParams<D>& m, bool first, bool obs,
                           double yk) {
+    const double (&F)[D * D] = Fm.a;
     // primal predict + update quantities
     double FP[D * D], Pm[ns(D)], xm[D];
-    kf_predict<D>(x, P, F, Q, xm, FP, Pm);
+    kf_predict<D>(x, P, Fm, Q, xm, FP, Pm);
     const double S = Pm[0] + m.r;
     const double iS = obs ? rcp(S) : 0.0;
     const double v = obs ? (yk - xm[0]) : 0.0;
@@ -163,20 +164,13 @@ PS_HD void grad_fold_step(TAgg<D>& A, const double (&x)[D], const double (&P)[ns
         for (int i = 0; i < ns(D); ++i) dQ[i] = Q[i];             // Q, P_inf proportional to sigma^2
     } else if constexpr (PAR == 1) {
         if (!first) {
-            // dF = -z G1 F, dQ = -z sigma^2 w f f^T ; G1 = companion of (s + 1)^D
+            // dF = -z J F (Jordan basis: J = -I + N), dQ = -z sigma^2 w f f^T
             const double w = (D == 1) ? 2.0 : (D == 2) ? 4.0 : 16.0 / 3.0;
 #pragma unroll
-            for (int j = 0; j < D; ++j) {
-                double last = 0.0;
+            for (int i = 0; i < D; ++i)
 #pragma unroll
-                for (int k = 0; k < D; ++k) {
-                    const double c = (D == 1) ? -1.0 : (D == 2) ? (k == 0 ? -1.0 : -2.0)
-                                                                : (k == 0 ? -1.0 : -3.0);
-                    last = fma(c, F[k * D + j], last);
-                }
-#pragma unroll
-                for (int i = 0; i < D; ++i) dF[i * D + j] = -z * ((i + 1 < D) ? F[(i + 1) * D + j] : last);
-            }
+                for (int j = 0; j < D; ++j)
+                    dF[i * D + j] = -z * ((i + 1 < D) ? F[(i + 1) * D + j] - F[i * D + j] : -F[i * D + j]);
 #pragma unroll
             for (int i = 0; i < D; ++i)
 #pragma unroll
@@ -303,19 +297,19 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_grad_fold(const KParam
         const double tk = __ldg(p.t + k);
         const bool obs = __ldg(p.mask + k) != 0;
         const double yk = obs ? __ldg(p.y + k) : 0.0;
-        double F[D * D], Q[ns(D)];
+        FJor<D> Fj;
+        double Q[ns(D)];
         const bool first = (k == 0);
         double z = 0.0;
         if (first) {
-#pragma unroll
-            for (int i = 0; i < D * D; ++i) F[i] = 0.0;
+            set_zero(Fj);
 #pragma unroll
             for (int i = 0; i < ns(D); ++i) Q[i] = p.m.Pinf[i];
         } else {
             z = p.m.lam * (tk - tprev);
-            matern_closed<D>(p.m.lam, p.m.s2, tk - tprev, F, Q);
+            matern_closed<D>(p.m.lam, p.m.s2, tk - tprev, Fj, Q);
         }
-        grad_fold_step<D, PAR>(A, x, P, F, Q, z, p.m, first, obs, yk);
+        grad_fold_step<D, PAR>(A, x, P, to_full<D>(Fj), Q, z, p.m, first, obs, yk);
         tprev = tk;
         const double* src = xpw + ((k - kb) * CN(D)) * 32;
 #pragma unroll

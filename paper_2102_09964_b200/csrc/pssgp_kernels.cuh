@@ -40,7 +40,10 @@ namespace pssgp {
 #define PSSGP_MINB 3                    // resident CTAs per SM the main kernels are register-capped for
 #endif
 constexpr int kUnroll = PSSGP_UNROLL;
-constexpr int kThreads = 128;           // threads per CTA (4 warps)
+#ifndef PSSGP_THREADS
+#define PSSGP_THREADS 128               // threads per CTA of the thread-per-chain kernels
+#endif
+constexpr int kThreads = PSSGP_THREADS;
 constexpr int kWarps = kThreads / 32;
 constexpr int kWin = 16;                // staging window (steps) per chain
 constexpr int kCarryThreads = 256;      // single-CTA scan kernels
@@ -200,11 +203,11 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_reduce(const KP
         const bool obs = __ldg(p.mask + kb) != 0;
         const double yk = obs ? __ldg(p.y + kb) : 0.0;
         const int64_t g = p.k0 + kb;
-        double F[D * D], Q[ns(D)];
+        FT_t<D, MODE> F;
+        double Q[ns(D)];
         const double dt = tk - tprev;
         if (g == 0) {
-#pragma unroll
-            for (int i = 0; i < D * D; ++i) F[i] = 0.0;
+set_zero(F);
 #pragma unroll
             for (int i = 0; i < ns(D); ++i) Q[i] = p.m.Pinf[i];
         } else if (disc<D, MODE>(p.m, dt, F, Q)) {
@@ -233,7 +236,8 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_reduce(const KP
                 const bool obs = mk != 0;
                 const double yk = obs ? st[wid].y[buf][jj][lane] : 0.0;
                 mk = (k + 1 < ke) ? __ldg(p.mask + k + 1) : 0;
-                double F[D * D], Q[ns(D)];
+                FT_t<D, MODE> F;
+        double Q[ns(D)];
                 const double dt = tk - tprev;
                 if (disc<D, MODE>(p.m, dt, F, Q)) raise_error(p.err, p.k0 + k, kErrUnsupported);
                 if (!(dt >= 0.0) || !isfinite(tk) || (obs && !isfinite(yk))) raise_error(p.err, p.k0 + k, kErrInput);
@@ -492,7 +496,8 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
 #pragma unroll
             for (int i = 0; i < ns(D); ++i) Pm[i] = p.m.Pinf[i];
         } else {
-            double F[D * D], Q[ns(D)], FP[D * D];
+            FT_t<D, MODE> F;
+            double Q[ns(D)], FP[D * D];
             disc<D, MODE>(p.m, tk - tprev, F, Q);
             kf_predict<D>(x, P, F, Q, xm, FP, Pm);
         }
@@ -545,7 +550,8 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
                 const bool obs = mk != 0;
                 const double yk = obs ? st[wid].y[buf][jj][lane] : 0.0;
                 mk = (k + 1 < ke) ? __ldg(p.mask + k + 1) : 0;
-                double xm[D], Pm[ns(D)], FP[D * D], F[D * D], Q[ns(D)];
+                FT_t<D, MODE> F;
+                double xm[D], Pm[ns(D)], FP[D * D], Q[ns(D)];
                 disc<D, MODE>(p.m, tk - tprev, F, Q);
                 kf_predict<D>(x, P, F, Q, xm, FP, Pm);
                 tprev = tk;
@@ -565,15 +571,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
                 // Sigma- = Sigma F^T, then the rank-one update by y_k of the
                 // cross-covariance and of the chain-entry moments
                 double Sm[D * D], SH[D];
-#pragma unroll
-                for (int i = 0; i < D; ++i)
-#pragma unroll
-                    for (int j = 0; j < D; ++j) {
-                        double s2 = 0.0;
-#pragma unroll
-                        for (int l = 0; l < D; ++l) s2 = fma(Sg[i * D + l], F[j * D + l], s2);
-                        Sm[i * D + j] = s2;
-                    }
+mul_bt<D>(Sg, F, Sm);
 #pragma unroll
                 for (int i = 0; i < D; ++i) {
                     if (p.m.h_unit) SH[i] = Sm[i * D];
@@ -624,18 +622,11 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
                 // peek one step past the chain (prediction only)
                 const int64_t g1 = p.k0 + ke;
                 const double tn = __ldg(p.t + ke);
-                double F[D * D], Q[ns(D)], xm[D], Pm[ns(D)], FP[D * D], Sm[D * D];
+                FT_t<D, MODE> F;
+                double Q[ns(D)], xm[D], Pm[ns(D)], FP[D * D], Sm[D * D];
                 disc<D, MODE>(p.m, tn - tprev, F, Q);
                 kf_predict<D>(x, P, F, Q, xm, FP, Pm);
-#pragma unroll
-                for (int i = 0; i < D; ++i)
-#pragma unroll
-                    for (int j = 0; j < D; ++j) {
-                        double s2 = 0.0;
-#pragma unroll
-                        for (int l = 0; l < D; ++l) s2 = fma(Sg[i * D + l], F[j * D + l], s2);
-                        Sm[i * D + j] = s2;
-                    }
+mul_bt<D>(Sg, F, Sm);
                 if (!chain_smoother_agg<D>(x0, P0, Sm, xm, Pm, sag)) raise_error(p.err, g1, kErrNumeric);
             }
         }
@@ -828,7 +819,8 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_smoother_apply(const K
             for (int i = 0; i < ns(D); ++i) Ps[i] = P[i];
         } else {
             const double tn = __ldg(p.t + ke);
-            double F[D * D], Q[ns(D)], xm[D], Pm[ns(D)], FP[D * D];
+            FT_t<D, MODE> F;
+            double Q[ns(D)], xm[D], Pm[ns(D)], FP[D * D];
             disc<D, MODE>(p.m, tn - tk, F, Q);
             kf_predict<D>(x, P, F, Q, xm, FP, Pm);
             if (!rts_step<D>(x, P, xm, Pm, FP, ms, Ps)) raise_error(p.err, p.k0 + k, kErrNumeric);
@@ -863,7 +855,8 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_smoother_apply(const K
 #pragma unroll
                     for (int i = 0; i < CN(D); ++i) nx[i] = src[i * 32];
                 }
-                double F[D * D], Q[ns(D)], xm[D], Pm[ns(D)], FP[D * D];
+                FT_t<D, MODE> F;
+            double Q[ns(D)], xm[D], Pm[ns(D)], FP[D * D];
                 disc<D, MODE>(p.m, tnext - tk, F, Q);
                 kf_predict<D>(x, P, F, Q, xm, FP, Pm);
                 if (!rts_step<D>(x, P, xm, Pm, FP, ms, Ps)) raise_error(p.err, p.k0 + k, kErrNumeric);

@@ -15,6 +15,7 @@
 //   RTS step               : PAPER.md:422-430
 //   discretisation         : PAPER.md:294-303 (closed forms for Matern)
 #pragma once
+#include <type_traits>
 #include <cstdint>
 #include <cmath>
 
@@ -48,7 +49,6 @@ PS_CX int CN(int D) { return D + ns(D); }                  // (mean, cov) pair d
 struct MathConsts {
     double expc[14];   // 1/k!, k = 0..13 (Taylor of e^r on |r| <= ln2/2, error < 5e-18)
     double inv[32];    // 1/n, n = 0..31 (inv[0] unused)
-    double q52[9];     // Matern-5/2 Q polynomial coefficients
 };
 #define PS_MATH_CONSTS                                                                         \
     {{1.0, 1.0, 1.0 / 2, 1.0 / 6, 1.0 / 24, 1.0 / 120, 1.0 / 720, 1.0 / 5040, 1.0 / 40320,     \
@@ -56,8 +56,7 @@ struct MathConsts {
      {0.0, 1.0, 1.0 / 2, 1.0 / 3, 1.0 / 4, 1.0 / 5, 1.0 / 6, 1.0 / 7, 1.0 / 8, 1.0 / 9, 1.0 / 10, \
       1.0 / 11, 1.0 / 12, 1.0 / 13, 1.0 / 14, 1.0 / 15, 1.0 / 16, 1.0 / 17, 1.0 / 18, 1.0 / 19,   \
       1.0 / 20, 1.0 / 21, 1.0 / 22, 1.0 / 23, 1.0 / 24, 1.0 / 25, 1.0 / 26, 1.0 / 27, 1.0 / 28,   \
-      1.0 / 29, 1.0 / 30, 1.0 / 31},                                                          \
-     {1.0 / 24, 1.0 / 9, 1.0 / 18, 1.0 / 3, 2.0 / 9, 1.0 / 36, 2.0 / 3, 8.0 / 3, 4.0 / 3}}
+      1.0 / 29, 1.0 / 30, 1.0 / 31}}
 #if defined(__CUDACC__)
 static __constant__ MathConsts d_mc = PS_MATH_CONSTS;
 #endif
@@ -97,10 +96,11 @@ PS_HD double rcp(double a) {
 // e^{-z} for z >= 0, branch-free: n = rint(z / ln2), r = n ln2 - z (Cody-Waite),
 // Taylor-13 of e^r, times 2^-n by exponent arithmetic.  z is clamped to 708
 // (e^-708 ~ 3e-308: below every quantity the kernels combine it with).
+template <bool FAST = false>
 PS_HD double exp_neg(double z) {
 #if defined(__CUDA_ARCH__)
     const MathConsts& C = mc();
-    if (z < 0.015625) {
+    if (FAST || z < 0.015625) {   // FAST: caller guarantees 0 <= z < 2^-6
         // |z| < 2^-6: Taylor-9 of e^{-z} directly (truncation < 4e-22 relative), no range reduction
         double pz = C.expc[9];
 #pragma unroll
@@ -317,14 +317,14 @@ PS_HD void ldlt_solve(const double (&Lo)[D * D], const double (&id)[D], double (
 // R_m(x) = e^{-x} sum_{n>=m} x^n / n!  (regularised lower incomplete gamma P(m, x)),
 // evaluated without cancellation: truncated series for x <= 2, complement
 // 1 - e^{-x} sum_{n<m} x^n/n! above (cancellation <= ~20x there).
-template <int M>
+template <int M, bool FAST = false>
 PS_HD double inc_gamma_tail(double x, double emx) {
     const MathConsts& C = mc();
     double xm = x;
 #pragma unroll
     for (int n = 1; n < M; ++n) xm *= x;
     const double lead = emx * xm * C.expc[M];  // e^{-x} x^M / M!
-    if (x <= 0.015625) {
+    if (FAST || x <= 0.015625) {   // FAST: caller guarantees 0 <= x <= 2^-6
         double s = 1.0;
 #pragma unroll
         for (int j = 7; j >= 1; --j) s = fma(s * x, C.inv[M + j], 1.0);
@@ -347,51 +347,109 @@ PS_HD double inc_gamma_tail(double x, double emx) {
     }
 }
 
-// Matern-(2D-1)/2 closed-form F(dt), Q(dt) in the lambda-scaled basis
-// x_hat_i = x_i / lambda^i (a diagonal balancing D = diag(lambda^i), Eq. (9)),
-// where F and Q / sigma^2 depend on z = lambda dt only (sympy derivation in
-// tools/derive_matern.py).  x = 2 z.
+// ------------------------------------------------------------------ transitions
+// A transition matrix F is passed to the step kernels as one of two types with the same
+// interface: F(i, j) reads an element, FT::nz(i, j) is a compile-time "may be nonzero" so
+// the fully unrolled products skip structural zeros.
 template <int D>
-PS_HD void matern_closed(double lam, double s2, double dt, double (&F)[D * D], double (&Q)[ns(D)]) {
+struct FMat {                        // general F (row-major)
+    double a[D * D];
+    PS_HD double operator()(int i, int j) const { return a[i * D + j]; }
+    static PS_HD constexpr bool nz(int, int) { return true; }
+};
+// Closed-form Matern-(2D-1)/2 in the JORDAN basis of its drift: with x_hat_i = x_i / lambda^i
+// the drift is lambda times the companion matrix of (s + 1)^D, which is similar to the single
+// Jordan block J = -I + N (N = ones on the superdiagonal) through a unit lower-triangular P
+// whose first row is e_0 (DESIGN.md §5 "Jordan basis").  In x~ = P^-1 x_hat the observation
+// row stays H = e_0 and
+//     F(z) = e^{-z} (I + z N + z^2/2 N^2 + ...),   z = lambda dt,
+// an upper-triangular Toeplitz matrix: F(i, j) = ec[j - i] = e^{-z} z^(j-i) / (j-i)!.
+template <int D>
+struct FJor {
+    double ec[D];
+    PS_HD double operator()(int i, int j) const { return j >= i ? ec[j - i] : 0.0; }
+    static PS_HD constexpr bool nz(int i, int j) { return j >= i; }
+};
+template <int D>
+PS_HD void set_zero(FMat<D>& f) {
+#pragma unroll
+    for (int i = 0; i < D * D; ++i) f.a[i] = 0.0;
+}
+template <int D>
+PS_HD void set_zero(FJor<D>& f) {
+#pragma unroll
+    for (int i = 0; i < D; ++i) f.ec[i] = 0.0;
+}
+template <int D, class FT>
+PS_HD FMat<D> to_full(const FT& f) {
+    FMat<D> o;
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) o.a[i * D + j] = f(i, j);
+    return o;
+}
+
+// R_m(x) = e^{-x} sum_{n >= m} x^n / n!, m = 1..M, from R_M by R_m = R_{m+1} + e^{-x} x^m / m!
+// (every term positive: no cancellation at any x).  R[m] for m = 1..M (R[0] unused).
+template <int M, bool FAST = false>
+PS_HD void inc_gamma_tails(double x, double emx, double (&R)[M + 1]) {
     const MathConsts& C = mc();
+    R[M] = inc_gamma_tail<M, FAST>(x, emx);
+    double tm = emx * x;                         // e^{-x} x^1 / 1!
+    double t[M + 1];
+    t[1] = tm;
+#pragma unroll
+    for (int m = 2; m < M; ++m) { tm = tm * x * C.inv[m]; t[m] = tm; }
+#pragma unroll
+    for (int m = M - 1; m >= 1; --m) R[m] = R[m + 1] + t[m];
+}
+
+// Matern-(2D-1)/2 closed form in the Jordan basis (above).  With x = 2z and
+// W = sigma^2 w e_{D-1} e_{D-1}^T (w = 2, 4, 16/3), Q(z) = sigma^2 w int_0^z e^{-2u} c(u) c(u)^T du,
+// c(u) = (u^(D-1)/(D-1)!, ..., u, 1), and int_0^z e^{-2u} u^k du = k! / 2^(k+1) R_{k+1}(x), so
+// every entry is a POSITIVE multiple of one R_m (derivation: DESIGN.md §5; pinned against the
+// oracle's Van Loan in tests/test_library_host.py):
+//   D = 1: Q = s2 R1
+//   D = 2: Q00 = s2 R3, Q01 = s2 R2, Q11 = 2 s2 R1
+//   D = 3: Q00 = s2 R5, Q01 = s2 R4, Q02 = 2/3 s2 R3, Q11 = 4/3 s2 R3, Q12 = 4/3 s2 R2, Q22 = 8/3 s2 R1
+// P_inf = lim Q (R_m -> 1).  FAST: the caller guarantees 0 <= z <= 2^-7.
+template <int D, bool FAST = false>
+PS_HD void matern_closed(double lam, double s2, double dt, FJor<D>& F, double (&Q)[ns(D)]) {
     const double z = lam * dt;
-    const double e = exp_neg(z);
+    const double e = exp_neg<FAST>(z);
     const double x = 2.0 * z;
     const double ex = e * e;  // e^{-x}
+    F.ec[0] = e;
+    if constexpr (D >= 2) F.ec[1] = e * z;
+    if constexpr (D >= 3) F.ec[2] = F.ec[1] * (0.5 * z);
     if constexpr (D == 1) {
-        F[0] = e;
-        Q[0] = s2 * inc_gamma_tail<1>(x, ex);
+        Q[0] = s2 * inc_gamma_tail<1, FAST>(x, ex);
     } else if constexpr (D == 2) {
-        F[0] = e * (1.0 + z); F[1] = e * z;
-        F[2] = -e * z;        F[3] = e * (1.0 - z);
-        const double R3 = inc_gamma_tail<3>(x, ex);
-        const double se = s2 * ex;
-        Q[si(2, 0, 0)] = s2 * R3;
-        Q[si(2, 0, 1)] = se * (0.5 * x * x);
-        Q[si(2, 1, 1)] = fma(se, 2.0 * x, s2 * R3);
+        double R[4];
+        inc_gamma_tails<3, FAST>(x, ex, R);
+        Q[si(2, 0, 0)] = s2 * R[3];
+        Q[si(2, 0, 1)] = s2 * R[2];
+        Q[si(2, 1, 1)] = (2.0 * s2) * R[1];
     } else if constexpr (D == 3) {
-        const double z2 = z * z;
-        const double hz2 = 0.5 * z2;
-        F[0] = e * (1.0 + z + hz2); F[1] = e * (z + z2);       F[2] = e * hz2;
-        F[3] = -e * hz2;            F[4] = e * (1.0 + z - z2); F[5] = e * (z - hz2);
-        F[6] = e * (hz2 - z);       F[7] = e * fma(-3.0, z, z2); F[8] = e * (1.0 - 2.0 * z + hz2);
-        const double R5 = s2 * inc_gamma_tail<5>(x, ex);
-        const double se = s2 * ex;
-        const double x2 = x * x, x3 = x2 * x, x4 = x2 * x2;
-        Q[si(3, 0, 0)] = R5;
-        Q[si(3, 0, 1)] = se * (x4 * C.q52[0]);
-        Q[si(3, 0, 2)] = fma(se, fma(x3, C.q52[1], -x4 * C.q52[2]), -R5 * C.q52[3]);
-        Q[si(3, 1, 1)] = fma(se, fma(x3, C.q52[4], -x4 * C.q52[5]), R5 * C.q52[3]);
-        Q[si(3, 1, 2)] = se * fma(x4, C.q52[0], fma(x2, C.q52[6], -x3 * C.q52[3]));
-        Q[si(3, 2, 2)] = fma(se, fma(x, C.q52[7], fma(x3, C.q52[6], -x2 * C.q52[8])), R5);
+        double R[6];
+        inc_gamma_tails<5, FAST>(x, ex, R);
+        const double s43 = s2 * (4.0 / 3.0);
+        Q[si(3, 0, 0)] = s2 * R[5];
+        Q[si(3, 0, 1)] = s2 * R[4];
+        Q[si(3, 0, 2)] = (s2 * (2.0 / 3.0)) * R[3];
+        Q[si(3, 1, 1)] = s43 * R[3];
+        Q[si(3, 1, 2)] = s43 * R[2];
+        Q[si(3, 2, 2)] = (s2 * (8.0 / 3.0)) * R[1];
     }
 }
 
 // Discretise one step (transition into a step whose predecessor is dt earlier).
 // Returns 0, or a nonzero code when the model has no device discretisation for dt.
 // MODE (compile time): kClosed = Matern closed form only (dt = 0 gives F = I,
-// Q = 0 exactly), kTable = the host-precomputed pair for dt == udt (dt = 0 ->
-// I, 0; anything else unsupported), kMixed = table for dt == udt else closed,
+// Q = 0 exactly; any uniform_dt is ignored, the closed form is cheaper than a table
+// lookup), kTable = the host-precomputed pair for dt == udt (dt = 0 -> I, 0; anything
+// else unsupported), kMixed = retired (closed models always use kClosed),
 // kPade = any model, any dt: F = expm(G dt) by scaling and squaring with the
 // [7/7] Pade approximant, Q = P_inf - F P_inf F^T (Lyapunov form of the stationary
 // model; north_star "per-step small-matrix expm via scaling-and-squaring Pade").
@@ -462,12 +520,17 @@ PS_HD void expm_pade7(const double (&G)[D * D], double dt, double (&F)[D * D]) {
     }
 }
 
+// transition type of each mode: Jordan-structured for the Matern closed form
 template <int D, int MODE>
-PS_HD int disc(const ModelParams<D>& p, double dt, double (&F)[D * D], double (&Q)[ns(D)]) {
+using FT_t = typename std::conditional<MODE == kClosed, FJor<D>, FMat<D>>::type;
+
+template <int D, int MODE>
+PS_HD int disc(const ModelParams<D>& p, double dt, FT_t<D, MODE>& Ft, double (&Q)[ns(D)]) {
     if constexpr (MODE == kClosed) {
-        if constexpr (D <= 3) matern_closed<D>(p.lam, p.s2, dt, F, Q);
+        if constexpr (D <= 3) matern_closed<D>(p.lam, p.s2, dt, Ft, Q);
         return 0;
     } else {
+        double (&F)[D * D] = Ft.a;
         if (fabs(dt - p.udt) <= 1e-12 * p.udt) {   // uniform step up to time-stamp rounding
 #pragma unroll
             for (int i = 0; i < D * D; ++i) F[i] = p.Fu[i];
@@ -475,10 +538,7 @@ PS_HD int disc(const ModelParams<D>& p, double dt, double (&F)[D * D], double (&
             for (int i = 0; i < ns(D); ++i) Q[i] = p.Qu[i];
             return 0;
         }
-        if constexpr (MODE == kMixed && D <= 3) {
-            matern_closed<D>(p.lam, p.s2, dt, F, Q);
-            return 0;
-        } else if constexpr (MODE == kPade) {
+        if constexpr (MODE == kPade) {
             if (dt == 0.0) {   // exact I, 0 on ties (reading Z13)
 #pragma unroll
                 for (int i = 0; i < D; ++i)
@@ -526,8 +586,18 @@ PS_HD int disc(const ModelParams<D>& p, double dt, double (&F)[D * D], double (&
 // Host-side dispatcher used by pssgp_debug_discretize.
 template <int D>
 PS_HD int discretize(const ModelParams<D>& p, double dt, double (&F)[D * D], double (&Q)[ns(D)]) {
-    if (p.closed) return p.udt > 0.0 ? disc<D, kMixed>(p, dt, F, Q) : disc<D, kClosed>(p, dt, F, Q);
-    return p.udt > 0.0 ? disc<D, kTable>(p, dt, F, Q) : disc<D, kPade>(p, dt, F, Q);
+    int rc;
+    FMat<D> f;
+    if (p.closed) {
+        FJor<D> fj;
+        rc = disc<D, kClosed>(p, dt, fj, Q);
+        f = to_full<D>(fj);
+    } else {
+        rc = p.udt > 0.0 ? disc<D, kTable>(p, dt, f, Q) : disc<D, kPade>(p, dt, f, Q);
+    }
+#pragma unroll
+    for (int i = 0; i < D * D; ++i) F[i] = f.a[i];
+    return rc;
 }
 
 // ------------------------------------------------------------------ filter fold
@@ -538,8 +608,8 @@ PS_HD int discretize(const ModelParams<D>& p, double dt, double (&F)[D * D], dou
 // entry state: predict C- = F C F^T + Q, then a rank-one update (no solve).
 // For the global first step pass F = 0, Q = P_inf (Eq. (7) PAPER.md:103-107 and
 // reading Z1: the observed first element is the KF update of N(0, P_inf)).
-template <int D>
-PS_HD void fold_step(FAgg<D>& a, const double (&F)[D * D], const double (&Q)[ns(D)],
+template <int D, class FT>
+PS_HD void fold_step(FAgg<D>& a, const FT& F, const double (&Q)[ns(D)],
                      const ModelParams<D>& p, bool obs, double yk) {
     double FA[D * D], Fb[D], T[D * D], Cm[ns(D)];
 #pragma unroll
@@ -550,12 +620,13 @@ PS_HD void fold_step(FAgg<D>& a, const double (&F)[D * D], const double (&Q)[ns(
             double sa = 0.0, sc = 0.0;
 #pragma unroll
             for (int k = 0; k < D; ++k) {
-                sa = fma(F[i * D + k], a.A[k * D + j], sa);
-                sc = fma(F[i * D + k], a.C[si(D, k, j)], sc);
+                if (!FT::nz(i, k)) continue;
+                sa = fma(F(i, k), a.A[k * D + j], sa);
+                sc = fma(F(i, k), a.C[si(D, k, j)], sc);
             }
             FA[i * D + j] = sa;
             T[i * D + j] = sc;
-            sb = fma(F[i * D + j], a.b[j], sb);
+            if (FT::nz(i, j)) sb = fma(F(i, j), a.b[j], sb);
         }
         Fb[i] = sb;
     }
@@ -565,7 +636,8 @@ PS_HD void fold_step(FAgg<D>& a, const double (&F)[D * D], const double (&Q)[ns(
         for (int j = i; j < D; ++j) {
             double s = Q[si(D, i, j)];
 #pragma unroll
-            for (int k = 0; k < D; ++k) s = fma(T[i * D + k], F[j * D + k], s);
+            for (int k = 0; k < D; ++k)
+                if (FT::nz(j, k)) s = fma(T[i * D + k], F(j, k), s);
             Cm[si(D, i, j)] = s;
         }
     // observation update; branchless: a missing y (Eqs. (6), (8)) is the same
@@ -814,8 +886,8 @@ PS_HD void apply_suffix(const SAgg<D>& a, const Gauss<D>& s, Gauss<D>& out) {
 
 // ------------------------------------------------------------------ Kalman step (supplement PAPER.md:304-315)
 // Predict: xm = F x, FP = F P, Pm = FP F^T + Q.
-template <int D>
-PS_HD void kf_predict(const double (&x)[D], const double (&P)[ns(D)], const double (&F)[D * D],
+template <int D, class FT>
+PS_HD void kf_predict(const double (&x)[D], const double (&P)[ns(D)], const FT& F,
                       const double (&Q)[ns(D)], double (&xm)[D], double (&FP)[D * D], double (&Pm)[ns(D)]) {
 #pragma unroll
     for (int i = 0; i < D; ++i) {
@@ -824,9 +896,10 @@ PS_HD void kf_predict(const double (&x)[D], const double (&P)[ns(D)], const doub
         for (int j = 0; j < D; ++j) {
             double s = 0.0;
 #pragma unroll
-            for (int k = 0; k < D; ++k) s = fma(F[i * D + k], P[si(D, k, j)], s);
+            for (int k = 0; k < D; ++k)
+                if (FT::nz(i, k)) s = fma(F(i, k), P[si(D, k, j)], s);
             FP[i * D + j] = s;
-            sx = fma(F[i * D + j], x[j], sx);
+            if (FT::nz(i, j)) sx = fma(F(i, j), x[j], sx);
         }
         xm[i] = sx;
     }
@@ -836,8 +909,24 @@ PS_HD void kf_predict(const double (&x)[D], const double (&P)[ns(D)], const doub
         for (int j = i; j < D; ++j) {
             double s = Q[si(D, i, j)];
 #pragma unroll
-            for (int k = 0; k < D; ++k) s = fma(FP[i * D + k], F[j * D + k], s);
+            for (int k = 0; k < D; ++k)
+                if (FT::nz(j, k)) s = fma(FP[i * D + k], F(j, k), s);
             Pm[si(D, i, j)] = s;
+        }
+}
+
+// Sm = Sg F^T (general Sg)
+template <int D, class FT>
+PS_HD void mul_bt(const double (&Sg)[D * D], const FT& F, double (&Sm)[D * D]) {
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            double s = 0.0;
+#pragma unroll
+            for (int l = 0; l < D; ++l)
+                if (FT::nz(j, l)) s = fma(Sg[i * D + l], F(j, l), s);
+            Sm[i * D + j] = s;
         }
 }
 
