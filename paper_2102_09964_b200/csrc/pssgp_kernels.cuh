@@ -180,6 +180,23 @@ __device__ __forceinline__ void issue_window(AsyncStage& s, int buf, const doubl
     issue_copies<true>(s.t[buf], s.y[buf], t, y, wbase, K, n, j0, lane);
 }
 
+// ------------------------------------------------------------------ mask words
+// The mask bytes of one staging window (kWinA = 8 steps) as one 64-bit word, loaded one
+// window ahead (HBM latency exceeds one step of compute); byte jj = step j0 + jj.  Bytes at
+// or past the chain end are 0.  Vector load when the 8 bytes are aligned and in range.
+static_assert(kWinA == 8, "mask words hold 8 steps");
+__device__ __forceinline__ unsigned long long mask_word(const uint8_t* __restrict__ mask, int64_t pos, int64_t ke) {
+    if (pos >= ke) return 0ull;
+    const uint8_t* a = mask + pos;
+    if ((reinterpret_cast<uintptr_t>(a) & 7) == 0 && pos + 8 <= ke)
+        return __ldg(reinterpret_cast<const unsigned long long*>(a));
+    unsigned long long w = 0ull;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+        if (pos + i < ke) w |= static_cast<unsigned long long>(__ldg(a + i)) << (8 * i);
+    return w;
+}
+
 // ------------------------------------------------------------------ K1: fold chains
 template <int D, int MODE>
 __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_reduce(const KParams<D> p) {
@@ -220,12 +237,14 @@ set_zero(F);
 
     const int64_t nwin = (p.K + kWinA - 1) / kWinA;
     issue_window(st[wid], 0, p.t, p.y, wbase, p.K, p.n, 0, lane);
-    unsigned char mk = (kb + 1 < ke) ? __ldg(p.mask + kb + 1) : 0;   // mask of the next step
+    unsigned long long mnext = mask_word(p.mask, kb, ke);             // mask bytes of window 0
     for (int64_t w = 0; w < nwin; ++w) {
         const int64_t j0 = w * kWinA;
         const int buf = static_cast<int>(w & 1);
         if (w + 1 < nwin) issue_window(st[wid], buf ^ 1, p.t, p.y, wbase, p.K, p.n, j0 + kWinA, lane);
         else cp_async_commit();
+        const unsigned long long mwin = mnext;
+        mnext = mask_word(p.mask, kb + j0 + kWinA, ke);
         cp_async_wait<1>();
         __syncwarp();
 #pragma unroll kUnroll
@@ -233,9 +252,8 @@ set_zero(F);
             const int64_t k = kb + j0 + jj;
             if (k < ke) {
                 const double tk = st[wid].t[buf][jj][lane];
-                const bool obs = mk != 0;
+                const bool obs = ((mwin >> (8 * jj)) & 0xffull) != 0;
                 const double yk = obs ? st[wid].y[buf][jj][lane] : 0.0;
-                mk = (k + 1 < ke) ? __ldg(p.mask + k + 1) : 0;
                 FT_t<D, MODE> F;
         double Q[ns(D)];
                 const double dt = tk - tprev;
@@ -534,12 +552,14 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
 
     const int64_t nwin = (p.K + kWinA - 1) / kWinA;
     issue_window(st[wid], 0, p.t, p.y, wbase, p.K, p.n, 0, lane);
-    unsigned char mk = (kb + 1 < ke) ? __ldg(p.mask + kb + 1) : 0;   // mask of the next step
+    unsigned long long mnext = mask_word(p.mask, kb, ke);             // mask bytes of window 0
     for (int64_t w = 0; w < nwin; ++w) {
         const int64_t j0 = w * kWinA;
         const int buf = static_cast<int>(w & 1);
         if (w + 1 < nwin) issue_window(st[wid], buf ^ 1, p.t, p.y, wbase, p.K, p.n, j0 + kWinA, lane);
         else cp_async_commit();
+        const unsigned long long mwin = mnext;
+        mnext = mask_word(p.mask, kb + j0 + kWinA, ke);
         cp_async_wait<1>();
         __syncwarp();
 #pragma unroll kUnroll
@@ -547,9 +567,8 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
             const int64_t k = kb + j0 + jj;
             if (k < ke) {
                 const double tk = st[wid].t[buf][jj][lane];
-                const bool obs = mk != 0;
+                const bool obs = ((mwin >> (8 * jj)) & 0xffull) != 0;
                 const double yk = obs ? st[wid].y[buf][jj][lane] : 0.0;
-                mk = (k + 1 < ke) ? __ldg(p.mask + k + 1) : 0;
                 FT_t<D, MODE> F;
                 double xm[D], Pm[ns(D)], FP[D * D], Q[ns(D)];
                 disc<D, MODE>(p.m, tk - tprev, F, Q);
