@@ -34,25 +34,41 @@ UNIT = "time-steps/s"
 # algorithmic bytes per time step moved by each kernel at d = 3 (DESIGN.md §6 "Roofline")
 ALG_BYTES = {"k_filter_reduce": 17, "k_filter_apply": 17 + 72, "k_smoother_apply": 8 + 72 + 16,
              "k_grad_fold": 17 + 72}
-# fp64 flops per time step of each kernel (DFMA = 2), Matern-5/2 closed-form path, from the ncu
-# SASS counts of the committed profile (tools/fp64_flops.py)
-FLOPS_PER_STEP = {"k_filter_reduce": 350.2, "k_filter_apply": 359.1, "k_smoother_apply": 423.5}
+# fallback fp64 flops per time step (DFMA = 2) if the committed profile has no SASS counts;
+# normally read from profiles/*/ncu_full_*_summary.csv (flops_per_step())
+FLOPS_PER_STEP = {"k_filter_reduce": 243.3, "k_filter_apply": 255.1, "k_smoother_apply": 327.4}
 # fp64 peak derived in DESIGN.md §6: 148 SM x 64 FMA/clk x 2 flop x 1.965 GHz
 FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
 THROTTLE_BAD = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
 
 
-def ncu_traffic(kernel: str):
-    """dram read+write bytes per launch of `kernel` from the latest committed ncu summary."""
+def _ncu_row(kernel: str):
+    """Row of `kernel` in the latest committed ncu summary (profiles/*/ncu_full_*_summary.csv,
+    written by tools/make_profile_summary.py; DRAM bytes in GB)."""
     import csv
     import glob
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "ncu_full_*_summary.csv")))
     for f in reversed(files):
         for row in csv.DictReader(open(f)):
-            if kernel in row["Kernel Name"]:
-                return (float(row["dram__bytes_read.sum"]) + float(row["dram__bytes_write.sum"])) * 1e9, \
-                    os.path.relpath(f, ROOT)
+            if kernel + "<" in row["Kernel Name"]:
+                return row, os.path.relpath(f, ROOT)
     return None, None
+
+
+def ncu_traffic(kernel: str):
+    """dram read+write bytes per launch of `kernel` from one `ncu --set full` capture."""
+    row, src = _ncu_row(kernel)
+    if row is None:
+        return None, None
+    return (float(row["dram__bytes_read.sum"]) + float(row["dram__bytes_write.sum"])) * 1e9, src
+
+
+def flops_per_step(kernel: str):
+    """Executed fp64 flops per time step (DFMA = 2) from the SASS counts of the committed capture."""
+    row, _ = _ncu_row(kernel)
+    if row is not None and row.get("fp64_flops_per_step"):
+        return float(row["fp64_flops_per_step"])
+    return FLOPS_PER_STEP.get(kernel)
 
 
 def parse():
@@ -339,7 +355,8 @@ def main():
     per_launch_ms = dom_ms / dom_launches
     alg_b = ALG_BYTES.get(dom, 0) * n_local
     hbm_gbs = alg_b / (per_launch_ms * 1e-3) / 1e9
-    flops = (FLOPS_PER_STEP.get(dom, 0.0) * n_local
+    fps = {k: flops_per_step(k) for k in ("k_filter_reduce", "k_filter_apply", "k_smoother_apply")}
+    flops = (fps.get(dom, 0.0) * n_local
              if model.state_dim == 3 and not args.uniform and args.config in ("metric", "c2", "c5") else None)
     plan = model.plan(n_local)
     launches = int(sum(v[1] for v in kern.values()))
@@ -349,7 +366,7 @@ def main():
         roof = {"bound": "alu", "kernel": dom, "achieved": achieved_tf, "peak": FP64_PEAK_TFLOPS,
                 "unit": "TFLOP/s", "frac": achieved_tf / FP64_PEAK_TFLOPS, "traffic": traffic,
                 "peak_source": "fp64 pipe: 148 SM x 64 FMA/clk x 2 x 1.965 GHz (DESIGN.md §6)",
-                "flops_per_step": FLOPS_PER_STEP.get(dom)}
+                "flops_per_step": fps.get(dom)}
     else:
         roof = {"bound": "hbm", "kernel": dom, "achieved": hbm_gbs, "peak": pk.get("hbm_gbs"), "unit": "GB/s",
                 "frac": hbm_gbs / pk.get("hbm_gbs"), "traffic": traffic}
@@ -363,7 +380,7 @@ def main():
         "per_kernel_ms_per_step": {k: v[0] / args.steps for k, v in kern.items()},
         "path_alg_bytes_per_step": 41 + 16 * 9,
         "path_hbm_frac": (41 + 16 * 9) * N / (ms_step * 1e-3) / 1e9 / pk.get("hbm_gbs"),
-        "path_fp64_frac": (sum(FLOPS_PER_STEP.values()) * N / (ms_step * 1e-3) / 1e12 / FP64_PEAK_TFLOPS)
+        "path_fp64_frac": (sum(fps.values()) * N / (ms_step * 1e-3) / 1e12 / FP64_PEAK_TFLOPS)
         if flops else None})
     cpu = None
     if not args.no_cpu_baseline:
