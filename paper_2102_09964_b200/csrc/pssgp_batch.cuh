@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_filter_reduce(co
         }
         if (!isfinite(tk) || (obs && !isfinite(yk))) raise_error(p.err, k, kErrInput);
         mp.r = s.r;
-        fold_step<D>(a, F, Q, mp, obs, yk);
+        fold_step<D, true>(a, F, Q, mp, obs, yk);
         tprev = tk;
     }
     store_soa(a, p.chain_f, nch, c);
@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_filter_apply(con
         tprev = tk;
         mp.r = s.r;
         double HP[D], S, hx;
-        obs_terms<D>(mp, xm, Pm, HP, S, hx);
+        obs_terms<D>(mp, xm, Pm, HP, S, hx, true);
         if (obs && !(S > 0.0 && S < INFINITY)) raise_error(p.err, k, kErrNumeric);
         const double iS = obs ? rcp(S) : 0.0;
         const double v = obs ? (yk - hx) : 0.0;

@@ -231,10 +231,11 @@ set_zero(F);
             raise_error(p.err, g, kErrUnsupported);
         }
         if ((g > 0 && !(dt >= 0.0)) || !isfinite(tk) || (obs && !isfinite(yk))) raise_error(p.err, g, kErrInput);
-        fold_step<D>(a, F, Q, p.m, obs, yk);
+        fold_step<D, MODE == kClosed>(a, F, Q, p.m, obs, yk);
         tprev = tk;
     }
 
+    int ferr_u = -1, ferr_i = -1;
     const int64_t nwin = (p.K + kWinA - 1) / kWinA;
     issue_window(st[wid], 0, p.t, p.y, wbase, p.K, p.n, 0, lane);
     unsigned long long mnext = mask_word(p.mask, kb, ke);             // mask bytes of window 0
@@ -247,24 +248,28 @@ set_zero(F);
         mnext = mask_word(p.mask, kb + j0 + kWinA, ke);
         cp_async_wait<1>();
         __syncwarp();
+        const int jend = static_cast<int>(min(static_cast<int64_t>(kWinA), ke - (kb + j0)));
 #pragma unroll kUnroll
-        for (int jj = (w == 0) ? 1 : 0; jj < kWinA; ++jj) {
-            const int64_t k = kb + j0 + jj;
-            if (k < ke) {
-                const double tk = st[wid].t[buf][jj][lane];
-                const bool obs = ((mwin >> (8 * jj)) & 0xffull) != 0;
-                const double yk = obs ? st[wid].y[buf][jj][lane] : 0.0;
-                FT_t<D, MODE> F;
-        double Q[ns(D)];
-                const double dt = tk - tprev;
-                if (disc<D, MODE>(p.m, dt, F, Q)) raise_error(p.err, p.k0 + k, kErrUnsupported);
-                if (!(dt >= 0.0) || !isfinite(tk) || (obs && !isfinite(yk))) raise_error(p.err, p.k0 + k, kErrInput);
-                fold_step<D>(a, F, Q, p.m, obs, yk);
-                tprev = tk;
-            }
+        for (int jj = (w == 0) ? 1 : 0; jj < jend; ++jj) {
+            const int jl = static_cast<int>(j0) + jj;          // step within the chain
+            const double tk = st[wid].t[buf][jj][lane];
+            const bool obs = ((mwin >> (8 * jj)) & 0xffull) != 0;
+            const double yk = obs ? st[wid].y[buf][jj][lane] : 0.0;
+            FT_t<D, MODE> F;
+            double Q[ns(D)];
+            const double dt = tk - tprev;
+            const bool bad_u = disc<D, MODE>(p.m, dt, F, Q) != 0;
+            const bool bad_i = !(dt >= 0.0) || !isfinite(tk) || (obs && !isfinite(yk));
+            // first failing step of the chain, kept branch-free (reported after the loop)
+            ferr_u = (bad_u && ferr_u < 0) ? jl : ferr_u;
+            ferr_i = (bad_i && ferr_i < 0) ? jl : ferr_i;
+            fold_step<D, MODE == kClosed>(a, F, Q, p.m, obs, yk);
+            tprev = tk;
         }
         __syncwarp();
     }
+    if (ferr_u >= 0) raise_error(p.err, p.k0 + kb + ferr_u, kErrUnsupported);
+    if (ferr_i >= 0) raise_error(p.err, p.k0 + kb + ferr_i, kErrInput);
     store_soa(a, p.chain_f, nch, c);
 
     // CTA tree reduce (ordered): lane 0 of each warp, then warp 0
@@ -367,8 +372,8 @@ __device__ __forceinline__ double cta_sum(const double* __restrict__ parts, int 
 // observation-row terms of a predicted (xm, Pm): HP = Pm H^T, S = H Pm H^T + r, hx = H xm
 template <int D>
 __device__ __forceinline__ void obs_terms(const ModelParams<D>& m, const double (&xm)[D], const double (&Pm)[ns(D)],
-                                          double (&HP)[D], double& S, double& hx) {
-    if (m.h_unit) {
+                                          double (&HP)[D], double& S, double& hx, bool hu_static = false) {
+    if (hu_static || m.h_unit) {
 #pragma unroll
         for (int i = 0; i < D; ++i) HP[i] = Pm[si(D, i, 0)];
         S = Pm[0] + m.r;
@@ -521,7 +526,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
         }
         tprev = tk;
         double HP[D], S, hx;
-        obs_terms<D>(p.m, xm, Pm, HP, S, hx);
+        obs_terms<D>(p.m, xm, Pm, HP, S, hx, MODE == kClosed);
         if (obs && !(S > 0.0 && S < INFINITY)) raise_error(p.err, g, kErrNumeric);
         const double iS = obs ? rcp(S) : 0.0;
         const double v = obs ? (yk - hx) : 0.0;
@@ -550,6 +555,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
         }
     }
 
+    int ferr_n = -1;
     const int64_t nwin = (p.K + kWinA - 1) / kWinA;
     issue_window(st[wid], 0, p.t, p.y, wbase, p.K, p.n, 0, lane);
     unsigned long long mnext = mask_word(p.mask, kb, ke);             // mask bytes of window 0
@@ -562,10 +568,11 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
         mnext = mask_word(p.mask, kb + j0 + kWinA, ke);
         cp_async_wait<1>();
         __syncwarp();
+        const int jend = static_cast<int>(min(static_cast<int64_t>(kWinA), ke - (kb + j0)));
 #pragma unroll kUnroll
-        for (int jj = (w == 0) ? 1 : 0; jj < kWinA; ++jj) {
+        for (int jj = (w == 0) ? 1 : 0; jj < jend; ++jj) {
             const int64_t k = kb + j0 + jj;
-            if (k < ke) {
+            {
                 const double tk = st[wid].t[buf][jj][lane];
                 const bool obs = ((mwin >> (8 * jj)) & 0xffull) != 0;
                 const double yk = obs ? st[wid].y[buf][jj][lane] : 0.0;
@@ -576,8 +583,9 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
                 tprev = tk;
                 // observation update (branchless: missing y -> 1/S = 0, v = 0)
                 double HP[D], S, hx;
-                obs_terms<D>(p.m, xm, Pm, HP, S, hx);
-                if (obs && !(S > 0.0 && S < INFINITY)) raise_error(p.err, p.k0 + k, kErrNumeric);
+                obs_terms<D>(p.m, xm, Pm, HP, S, hx, MODE == kClosed);
+                const bool bad_n = obs && !(S > 0.0 && S < INFINITY);
+                ferr_n = (bad_n && ferr_n < 0) ? static_cast<int>(k - kb) : ferr_n;
                 const double iS = obs ? rcp(S) : 0.0;
                 const double v = obs ? (yk - hx) : 0.0;
                 const double vs = v * iS;
@@ -593,7 +601,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
 mul_bt<D>(Sg, F, Sm);
 #pragma unroll
                 for (int i = 0; i < D; ++i) {
-                    if (p.m.h_unit) SH[i] = Sm[i * D];
+                    if (MODE == kClosed || p.m.h_unit) SH[i] = Sm[i * D];
                     else {
                         double s2 = 0.0;
 #pragma unroll
@@ -622,6 +630,7 @@ mul_bt<D>(Sg, F, Sm);
         }
         __syncwarp();
     }
+    if (ferr_n >= 0) raise_error(p.err, p.k0 + kb + ferr_n, kErrNumeric);
 
     // ---- chain smoother aggregate
     if (p.store_state) {
@@ -760,8 +769,8 @@ __device__ __forceinline__ Gauss<D> smoother_chain_carry(const KParams<D>& p, SA
 // f-space projection: mean = H m^s, var = H P^s H^T
 template <int D>
 __device__ __forceinline__ void project(const ModelParams<D>& m, const double (&ms)[D], const double (&Ps)[ns(D)],
-                                        double& mo, double& vo) {
-    if (m.h_unit) {
+                                        double& mo, double& vo, bool hu_static = false) {
+    if (hu_static || m.h_unit) {
         mo = ms[0];
         vo = Ps[0];
     } else {
@@ -846,10 +855,11 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_smoother_apply(const K
         }
         tnext = tk;
         double mo, vo;
-        project<D>(p.m, ms, Ps, mo, vo);
+        project<D>(p.m, ms, Ps, mo, vo, MODE == kClosed);
         if (p.mean) p.mean[k] = mo;
         if (p.var) p.var[k] = vo;
     }
+    int ferr_n = -1;
     const int64_t nwin = (p.K + kWinA - 1) / kWinA;
     issue_copies<false>(so[wid].t[(nwin - 1) & 1], nullptr, p.t, nullptr, wbase, p.K, p.n, (nwin - 1) * kWinA, lane);
     for (int64_t w = nwin - 1; w >= 0; --w) {
@@ -859,10 +869,11 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_smoother_apply(const K
         else cp_async_commit();
         cp_async_wait<1>();
         __syncwarp();
+        const int jstart = static_cast<int>(min(static_cast<int64_t>(kWinA - 1), ke - 2 - (kb + j0)));
 #pragma unroll kUnroll
-        for (int jj = kWinA - 1; jj >= 0; --jj) {
+        for (int jj = jstart; jj >= 0; --jj) {
             const int64_t k = kb + j0 + jj;
-            if (k < ke - 1) {
+            {
                 const double tk = so[wid].t[buf][jj][lane];
                 double x[D], P[ns(D)];
 #pragma unroll
@@ -878,10 +889,11 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_smoother_apply(const K
             double Q[ns(D)], xm[D], Pm[ns(D)], FP[D * D];
                 disc<D, MODE>(p.m, tnext - tk, F, Q);
                 kf_predict<D>(x, P, F, Q, xm, FP, Pm);
-                if (!rts_step<D>(x, P, xm, Pm, FP, ms, Ps)) raise_error(p.err, p.k0 + k, kErrNumeric);
+                const bool bad_n = !rts_step<D>(x, P, xm, Pm, FP, ms, Ps);
+                ferr_n = bad_n ? static_cast<int>(k - kb) : ferr_n;   // backward: last hit = first index
                 tnext = tk;
                 double mo, vo;
-                project<D>(p.m, ms, Ps, mo, vo);
+                project<D>(p.m, ms, Ps, mo, vo, MODE == kClosed);
                 so[wid].m[jj][lane] = mo;
                 so[wid].v[jj][lane] = vo;
             }
@@ -903,6 +915,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_smoother_apply(const K
         }
         __syncwarp();
     }
+    if (ferr_n >= 0) raise_error(p.err, p.k0 + kb + ferr_n, kErrNumeric);
 }
 
 // ------------------------------------------------------------------ K6: deterministic NLL sum

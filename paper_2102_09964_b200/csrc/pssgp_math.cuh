@@ -608,7 +608,7 @@ PS_HD int discretize(const ModelParams<D>& p, double dt, double (&F)[D * D], dou
 // entry state: predict C- = F C F^T + Q, then a rank-one update (no solve).
 // For the global first step pass F = 0, Q = P_inf (Eq. (7) PAPER.md:103-107 and
 // reading Z1: the observed first element is the KF update of N(0, P_inf)).
-template <int D, class FT>
+template <int D, bool HU = false, class FT>
 PS_HD void fold_step(FAgg<D>& a, const FT& F, const double (&Q)[ns(D)],
                      const ModelParams<D>& p, bool obs, double yk) {
     double FA[D * D], Fb[D], T[D * D], Cm[ns(D)];
@@ -643,7 +643,7 @@ PS_HD void fold_step(FAgg<D>& a, const FT& F, const double (&Q)[ns(D)],
     // observation update; branchless: a missing y (Eqs. (6), (8)) is the same
     // formulas with 1/S and the innovation set to zero (A = F A, b = F b, C = C-)
     double HC[D], w[D], hb, S;
-    if (p.h_unit) {
+    if (HU || p.h_unit) {
 #pragma unroll
         for (int i = 0; i < D; ++i) { HC[i] = Cm[si(D, i, 0)]; w[i] = FA[i]; }
         hb = Fb[0];
