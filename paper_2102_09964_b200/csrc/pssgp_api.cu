@@ -258,7 +258,10 @@ pssgp_status phase_filter_reduce(pssgp_model* m, KParams<D>& p, cudaStream_t s) 
 template <int D>
 pssgp_status phase_filter_apply(pssgp_model* m, KParams<D>& p, cudaStream_t s) {
     ProfScope ps(m, S_K3, s);
-    LAUNCH_MODE(m, k_filter_apply, p.nb, kThreads, s, p);
+    if (p.store_state) LAUNCH_MODE(m, k_filter_apply, p.nb, kThreads, s, p);
+    else if (m->mode == kClosed) k_filter_apply<D, kClosed, false><<<p.nb, kThreads, 0, s>>>(p);
+    else if (m->mode == kPade) k_filter_apply<D, kPade, false><<<p.nb, kThreads, 0, s>>>(p);
+    else k_filter_apply<D, kTable, false><<<p.nb, kThreads, 0, s>>>(p);
     LAUNCH_CHECK(m, "k_filter_apply");
     return PSSGP_OK;
 }

@@ -475,7 +475,8 @@ __device__ __forceinline__ Gauss<D> filter_chain_carry(const KParams<D>& p, FAgg
 }
 
 // ------------------------------------------------------------------ K3: Kalman rescan
-template <int D, int MODE>
+// STORE = false (NLL only): no filtered-state stores, no smoother-aggregate moments.
+template <int D, int MODE, bool STORE = true>
 __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KParams<D> p) {
     __shared__ AsyncStage st[kWarps];
     __shared__ FAgg<D> tot[kWarps];
@@ -546,7 +547,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
 #pragma unroll
             for (int j = 0; j < D; ++j) Sg[i * D + j] = P[si(D, i, j)];
         nll_accumulate(obs, v, vs, S, quad, prodm, prode, nobs);
-        if (p.store_state) {
+        if (STORE) {
             double* o = p.xp + (wg * p.K * CN(D)) * 32 + lane;
 #pragma unroll
             for (int i = 0; i < D; ++i) o[i * 32] = x[i];
@@ -597,8 +598,9 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
                     for (int j = i; j < D; ++j) P[si(D, i, j)] = fma(-HP[i] * iS, HP[j], Pm[si(D, i, j)]);
                 // Sigma- = Sigma F^T, then the rank-one update by y_k of the
                 // cross-covariance and of the chain-entry moments
+                if (STORE) {
                 double Sm[D * D], SH[D];
-mul_bt<D>(Sg, F, Sm);
+                mul_bt<D>(Sg, F, Sm);
 #pragma unroll
                 for (int i = 0; i < D; ++i) {
                     if (MODE == kClosed || p.m.h_unit) SH[i] = Sm[i * D];
@@ -618,8 +620,9 @@ mul_bt<D>(Sg, F, Sm);
 #pragma unroll
                     for (int j = i; j < D; ++j) P0[si(D, i, j)] = fma(-si_, SH[j], P0[si(D, i, j)]);
                 }
+                }
                 nll_accumulate(obs, v, vs, S, quad, prodm, prode, nobs);
-                if (p.store_state) {
+                if (STORE) {
                     double* o = p.xp + ((wg * p.K + (k - kb)) * CN(D)) * 32 + lane;
 #pragma unroll
                     for (int i = 0; i < D; ++i) o[i * 32] = x[i];
@@ -633,7 +636,7 @@ mul_bt<D>(Sg, F, Sm);
     if (ferr_n >= 0) raise_error(p.err, p.k0 + kb + ferr_n, kErrNumeric);
 
     // ---- chain smoother aggregate
-    if (p.store_state) {
+    if (STORE) {
         SAgg<D> sag;
         set_identity(sag);
         if (ke > kb) {
@@ -654,7 +657,7 @@ mul_bt<D>(Sg, F, Sm);
                 double Q[ns(D)], xm[D], Pm[ns(D)], FP[D * D], Sm[D * D];
                 disc<D, MODE>(p.m, tn - tprev, F, Q);
                 kf_predict<D>(x, P, F, Q, xm, FP, Pm);
-mul_bt<D>(Sg, F, Sm);
+                mul_bt<D>(Sg, F, Sm);
                 if (!chain_smoother_agg<D>(x0, P0, Sm, xm, Pm, sag)) raise_error(p.err, g1, kErrNumeric);
             }
         }
@@ -685,7 +688,7 @@ mul_bt<D>(Sg, F, Sm);
         double s2 = 0.0;
         for (int w = 0; w < kWarps; ++w) s2 += nred[w];
         p.nll_block[blockIdx.x] = s2;
-        if (p.store_state) {
+        if (STORE) {
             SAgg<D> acc = stot[0];
             for (int w = 1; w < kWarps; ++w) {
                 SAgg<D> r;
