@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_filter_apply(con
         double Q[ns(D)], xm[D], Pm[ns(D)], FP[D * D];
         if (k == s.start) seg_first(p, s, F, Q);
         else matern_closed<D>(s.lam, s.s2, tk - tprev, F, Q);
-        kf_predict<D>(x, P, F, Q, xm, FP, Pm);
+        kf_predict_pm<D>(x, P, F, Q, xm, Pm);
         tprev = tk;
         mp.r = s.r;
         double HP[D], S, hx;
@@ -222,7 +222,7 @@ mul_bt<D>(Sg, F, Sm);
         FJor<D> F;
         double Q[ns(D)], xm[D], Pm[ns(D)], FP[D * D], Sm[D * D];
         matern_closed<D>(s.lam, s.s2, tn - tprev, F, Q);
-        kf_predict<D>(x, P, F, Q, xm, FP, Pm);
+        kf_predict_pm<D>(x, P, F, Q, xm, Pm);
 mul_bt<D>(Sg, F, Sm);
         if (!chain_smoother_agg<D>(x0, P0, Sm, xm, Pm, sag)) raise_error(p.err, ke, kErrNumeric);
     }

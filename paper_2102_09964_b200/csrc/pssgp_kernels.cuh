@@ -523,7 +523,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
             FT_t<D, MODE> F;
             double Q[ns(D)], FP[D * D];
             disc<D, MODE>(p.m, tk - tprev, F, Q);
-            kf_predict<D>(x, P, F, Q, xm, FP, Pm);
+            kf_predict_pm<D>(x, P, F, Q, xm, Pm);
         }
         tprev = tk;
         double HP[D], S, hx;
@@ -580,7 +580,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
                 FT_t<D, MODE> F;
                 double xm[D], Pm[ns(D)], FP[D * D], Q[ns(D)];
                 disc<D, MODE>(p.m, tk - tprev, F, Q);
-                kf_predict<D>(x, P, F, Q, xm, FP, Pm);
+                kf_predict_pm<D>(x, P, F, Q, xm, Pm);
                 tprev = tk;
                 // observation update (branchless: missing y -> 1/S = 0, v = 0)
                 double HP[D], S, hx;
@@ -656,7 +656,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
                 FT_t<D, MODE> F;
                 double Q[ns(D)], xm[D], Pm[ns(D)], FP[D * D], Sm[D * D];
                 disc<D, MODE>(p.m, tn - tprev, F, Q);
-                kf_predict<D>(x, P, F, Q, xm, FP, Pm);
+                kf_predict_pm<D>(x, P, F, Q, xm, Pm);
                 mul_bt<D>(Sg, F, Sm);
                 if (!chain_smoother_agg<D>(x0, P0, Sm, xm, Pm, sag)) raise_error(p.err, g1, kErrNumeric);
             }

@@ -47,12 +47,16 @@ PS_CX int CN(int D) { return D + ns(D); }                  // (mean, cov) pair d
 // kernels read them as constant-bank operands instead of re-materialising
 // 64-bit literals with uniform-register moves.
 struct MathConsts {
-    double expc[14];   // 1/k!, k = 0..13 (Taylor of e^r on |r| <= ln2/2, error < 5e-18)
+    double expc[28];   // 1/k!, k = 0..27 (Taylor of e^r on |r| <= ln2/2 uses k <= 13; R_m series)
     double inv[32];    // 1/n, n = 0..31 (inv[0] unused)
 };
 #define PS_MATH_CONSTS                                                                         \
-    {{1.0, 1.0, 1.0 / 2, 1.0 / 6, 1.0 / 24, 1.0 / 120, 1.0 / 720, 1.0 / 5040, 1.0 / 40320,     \
-      1.0 / 362880, 1.0 / 3628800, 1.0 / 39916800, 1.0 / 479001600, 1.0 / 6227020800.0},        \
+    {{1.0, 1.0, 0.5, 0.16666666666666666, 0.041666666666666664,  \
+      0.008333333333333333, 0.001388888888888889, 0.0001984126984126984, 2.48015873015873e-05, 2.7557319223985893e-06,  \
+      2.755731922398589e-07, 2.505210838544172e-08, 2.08767569878681e-09, 1.6059043836821613e-10, 1.1470745597729725e-11,  \
+      7.647163731819816e-13, 4.779477332387385e-14, 2.8114572543455206e-15, 1.5619206968586225e-16, 8.22063524662433e-18,  \
+      4.110317623312165e-19, 1.9572941063391263e-20, 8.896791392450574e-22, 3.868170170630684e-23, 1.6117375710961184e-24,  \
+      6.446950284384474e-26, 2.4795962632247976e-27, 9.183689863795546e-29},  \
      {0.0, 1.0, 1.0 / 2, 1.0 / 3, 1.0 / 4, 1.0 / 5, 1.0 / 6, 1.0 / 7, 1.0 / 8, 1.0 / 9, 1.0 / 10, \
       1.0 / 11, 1.0 / 12, 1.0 / 13, 1.0 / 14, 1.0 / 15, 1.0 / 16, 1.0 / 17, 1.0 / 18, 1.0 / 19,   \
       1.0 / 20, 1.0 / 21, 1.0 / 22, 1.0 / 23, 1.0 / 24, 1.0 / 25, 1.0 / 26, 1.0 / 27, 1.0 / 28,   \
@@ -320,24 +324,30 @@ PS_HD void ldlt_solve(const double (&Lo)[D * D], const double (&id)[D], double (
 template <int M, bool FAST = false>
 PS_HD double inc_gamma_tail(double x, double emx) {
     const MathConsts& C = mc();
-    double xm = x;
+    double xm;                                    // x^M
+    if constexpr (M == 5) {
+        const double x2 = x * x;
+        xm = x2 * x2 * x;
+    } else {
+        xm = x;
 #pragma unroll
-    for (int n = 1; n < M; ++n) xm *= x;
-    const double lead = emx * xm * C.expc[M];  // e^{-x} x^M / M!
+        for (int n = 1; n < M; ++n) xm *= x;
+    }
+    const double lead = emx * xm;                 // e^{-x} x^M; series coefficients 1/(M+j)!
     if (FAST || x <= 0.015625) {   // FAST: caller guarantees 0 <= x <= 2^-6
-        double s = 1.0;
+        double s = C.expc[M + 7];
 #pragma unroll
-        for (int j = 7; j >= 1; --j) s = fma(s * x, C.inv[M + j], 1.0);
+        for (int j = 6; j >= 0; --j) s = fma(s, x, C.expc[M + j]);
         return lead * s;
     } else if (x <= 0.5) {
-        double s = 1.0;
+        double s = C.expc[M + 13];
 #pragma unroll
-        for (int j = 13; j >= 1; --j) s = fma(s * x, C.inv[M + j], 1.0);
+        for (int j = 12; j >= 0; --j) s = fma(s, x, C.expc[M + j]);
         return lead * s;
     } else if (x <= 2.0) {
-        double s = 1.0;
+        double s = C.expc[M + 22];
 #pragma unroll
-        for (int j = 22; j >= 1; --j) s = fma(s * x, C.inv[M + j], 1.0);
+        for (int j = 21; j >= 0; --j) s = fma(s, x, C.expc[M + j]);
         return lead * s;
     } else {
         double p = 1.0, term = 1.0;
@@ -366,7 +376,9 @@ struct FMat {                        // general F (row-major)
 // an upper-triangular Toeplitz matrix: F(i, j) = ec[j - i] = e^{-z} z^(j-i) / (j-i)!.
 template <int D>
 struct FJor {
-    double ec[D];
+    double ec[D];      // e^{-z} z^k / k!
+    double e;          // e^{-z}
+    double u[D];       // z^k / k! (u[0] = 1 unused): F = e U
     PS_HD double operator()(int i, int j) const { return j >= i ? ec[j - i] : 0.0; }
     static PS_HD constexpr bool nz(int i, int j) { return j >= i; }
 };
@@ -378,7 +390,57 @@ PS_HD void set_zero(FMat<D>& f) {
 template <int D>
 PS_HD void set_zero(FJor<D>& f) {
 #pragma unroll
-    for (int i = 0; i < D; ++i) f.ec[i] = 0.0;
+    for (int i = 0; i < D; ++i) { f.ec[i] = 0.0; f.u[i] = 0.0; }
+    f.e = 0.0;
+}
+
+// F S F^T + Q for symmetric packed S (packed result).  General F: T = F S, then T F^T.
+template <int D>
+PS_HD void cong_plus(const FMat<D>& F, const double (&S)[ns(D)], const double (&Q)[ns(D)], double (&R)[ns(D)]) {
+    double T[D * D];
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            double t = 0.0;
+#pragma unroll
+            for (int k = 0; k < D; ++k) t = fma(F(i, k), S[si(D, k, j)], t);
+            T[i * D + j] = t;
+        }
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = i; j < D; ++j) {
+            double r = Q[si(D, i, j)];
+#pragma unroll
+            for (int k = 0; k < D; ++k) r = fma(T[i * D + k], F(j, k), r);
+            R[si(D, i, j)] = r;
+        }
+}
+// Jordan F = e U (U unit upper-triangular Toeplitz): e^2 (U S U^T) + Q, the unit diagonal and
+// the structural zeros of U skipped (D = 3: 13 FMA for U S U^T instead of 45).
+template <int D>
+PS_HD void cong_plus(const FJor<D>& F, const double (&S)[ns(D)], const double (&Q)[ns(D)], double (&R)[ns(D)]) {
+    double X[D * D];   // X = U S
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            double t = S[si(D, i, j)];
+#pragma unroll
+            for (int k = i + 1; k < D; ++k) t = fma(F.u[k - i], S[si(D, k, j)], t);
+            X[i * D + j] = t;
+        }
+    const double e2 = F.e * F.e;
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = i; j < D; ++j) {
+            double y = X[i * D + j];
+#pragma unroll
+            for (int l = j + 1; l < D; ++l) y = fma(X[i * D + l], F.u[l - j], y);
+            R[si(D, i, j)] = fma(e2, y, Q[si(D, i, j)]);
+        }
 }
 template <int D, class FT>
 PS_HD FMat<D> to_full(const FT& f) {
@@ -420,9 +482,11 @@ PS_HD void matern_closed(double lam, double s2, double dt, FJor<D>& F, double (&
     const double e = exp_neg<FAST>(z);
     const double x = 2.0 * z;
     const double ex = e * e;  // e^{-x}
+    F.e = e;
+    F.u[0] = 1.0;
     F.ec[0] = e;
-    if constexpr (D >= 2) F.ec[1] = e * z;
-    if constexpr (D >= 3) F.ec[2] = F.ec[1] * (0.5 * z);
+    if constexpr (D >= 2) { F.u[1] = z; F.ec[1] = e * z; }
+    if constexpr (D >= 3) { F.u[2] = 0.5 * z * z; F.ec[2] = e * F.u[2]; }
     if constexpr (D == 1) {
         Q[0] = s2 * inc_gamma_tail<1, FAST>(x, ex);
     } else if constexpr (D == 2) {
@@ -611,35 +675,22 @@ PS_HD int discretize(const ModelParams<D>& p, double dt, double (&F)[D * D], dou
 template <int D, bool HU = false, class FT>
 PS_HD void fold_step(FAgg<D>& a, const FT& F, const double (&Q)[ns(D)],
                      const ModelParams<D>& p, bool obs, double yk) {
-    double FA[D * D], Fb[D], T[D * D], Cm[ns(D)];
+    double FA[D * D], Fb[D], Cm[ns(D)];
 #pragma unroll
     for (int i = 0; i < D; ++i) {
         double sb = 0.0;
 #pragma unroll
         for (int j = 0; j < D; ++j) {
-            double sa = 0.0, sc = 0.0;
+            double sa = 0.0;
 #pragma unroll
-            for (int k = 0; k < D; ++k) {
-                if (!FT::nz(i, k)) continue;
-                sa = fma(F(i, k), a.A[k * D + j], sa);
-                sc = fma(F(i, k), a.C[si(D, k, j)], sc);
-            }
+            for (int k = 0; k < D; ++k)
+                if (FT::nz(i, k)) sa = fma(F(i, k), a.A[k * D + j], sa);
             FA[i * D + j] = sa;
-            T[i * D + j] = sc;
             if (FT::nz(i, j)) sb = fma(F(i, j), a.b[j], sb);
         }
         Fb[i] = sb;
     }
-#pragma unroll
-    for (int i = 0; i < D; ++i)
-#pragma unroll
-        for (int j = i; j < D; ++j) {
-            double s = Q[si(D, i, j)];
-#pragma unroll
-            for (int k = 0; k < D; ++k)
-                if (FT::nz(j, k)) s = fma(T[i * D + k], F(j, k), s);
-            Cm[si(D, i, j)] = s;
-        }
+    cong_plus<D>(F, a.C, Q, Cm);
     // observation update; branchless: a missing y (Eqs. (6), (8)) is the same
     // formulas with 1/S and the innovation set to zero (A = F A, b = F b, C = C-)
     double HC[D], w[D], hb, S;
@@ -913,6 +964,21 @@ PS_HD void kf_predict(const double (&x)[D], const double (&P)[ns(D)], const FT& 
                 if (FT::nz(j, k)) s = fma(FP[i * D + k], F(j, k), s);
             Pm[si(D, i, j)] = s;
         }
+}
+
+// Predict without F P: xm = F x, Pm = F P F^T + Q (the structured congruence for Jordan F).
+template <int D, class FT>
+PS_HD void kf_predict_pm(const double (&x)[D], const double (&P)[ns(D)], const FT& F, const double (&Q)[ns(D)],
+                         double (&xm)[D], double (&Pm)[ns(D)]) {
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        double sx = 0.0;
+#pragma unroll
+        for (int j = 0; j < D; ++j)
+            if (FT::nz(i, j)) sx = fma(F(i, j), x[j], sx);
+        xm[i] = sx;
+    }
+    cong_plus<D>(F, P, Q, Pm);
 }
 
 // Sm = Sg F^T (general Sg)
