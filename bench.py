@@ -361,15 +361,22 @@ def main():
     plan = model.plan(n_local)
     launches = int(sum(v[1] for v in kern.values()))
     traffic, traffic_src = ncu_traffic(dom)
+    # the binding roofline of the dominant kernel is the larger of its two floors:
+    # algorithmic bytes / HBM peak and executed fp64 flops / fp64 peak
+    hbm_frac = hbm_gbs / pk.get("hbm_gbs")
+    alu = None
     if flops:
         achieved_tf = flops / (per_launch_ms * 1e-3) / 1e12
-        roof = {"bound": "alu", "kernel": dom, "achieved": achieved_tf, "peak": FP64_PEAK_TFLOPS,
-                "unit": "TFLOP/s", "frac": achieved_tf / FP64_PEAK_TFLOPS, "traffic": traffic,
-                "peak_source": "fp64 pipe: 148 SM x 64 FMA/clk x 2 x 1.965 GHz (DESIGN.md §6)",
-                "flops_per_step": fps.get(dom)}
+        alu = {"achieved_tflops": achieved_tf, "peak_tflops": FP64_PEAK_TFLOPS,
+               "frac": achieved_tf / FP64_PEAK_TFLOPS, "flops_per_step": fps.get(dom),
+               "peak_source": "fp64 pipe: 148 SM x 64 FMA/clk x 2 x 1.965 GHz (DESIGN.md §6)"}
+    if alu and alu["frac"] > hbm_frac:
+        roof = {"bound": "alu", "kernel": dom, "achieved": alu["achieved_tflops"], "peak": FP64_PEAK_TFLOPS,
+                "unit": "TFLOP/s", "frac": alu["frac"], "traffic": traffic}
     else:
         roof = {"bound": "hbm", "kernel": dom, "achieved": hbm_gbs, "peak": pk.get("hbm_gbs"), "unit": "GB/s",
-                "frac": hbm_gbs / pk.get("hbm_gbs"), "traffic": traffic}
+                "frac": hbm_frac, "traffic": traffic}
+    roof["alu"] = alu
     roof.update({
         "traffic_source": traffic_src,
         "alg_bytes_per_launch": alg_b,

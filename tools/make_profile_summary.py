@@ -1,6 +1,6 @@
 """Build the committed ncu summary for one profiling round from tools/profile_round.sh output.
 
-usage: python tools/make_profile_summary.py gpurun_out/TAG profiles/TAG N
+usage: python tools/make_profile_summary.py gpurun_out/TAG profiles/ROUND N [TAG]
 Writes profiles/TAG/ncu_full_TAG_summary.csv (per hot kernel: duration, DRAM bytes in GB, fp64 pipe
 and issue utilisation, stall ratios, executed fp64 instructions and flops per time step from the
 SASS source page), copies the launch list and the bench line."""
@@ -11,7 +11,7 @@ import shutil
 import sys
 
 src, dst, N = sys.argv[1], sys.argv[2], float(sys.argv[3])
-tag = os.path.basename(dst.rstrip("/"))
+tag = sys.argv[4] if len(sys.argv) > 4 else os.path.basename(src.rstrip("/"))
 os.makedirs(dst, exist_ok=True)
 SCALE = {"byte": 1e-9, "Kbyte": 1e-6, "Mbyte": 1e-3, "Gbyte": 1.0, "Tbyte": 1e3}
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
