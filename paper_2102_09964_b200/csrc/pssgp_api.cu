@@ -318,26 +318,8 @@ pssgp_status run_posterior(pssgp_model* m, int64_t N, const double* t, const dou
     return PSSGP_OK;
 }
 
-// NLL gradient (f1): primal filter storing (xbar, P), then one tangent fold + ordered
-// block reduction per parameter (pssgp_grad.cuh).
-template <int D, int PAR>
-pssgp_status grad_param(pssgp_model* m, KParams<D>& p, double* blocks, double* out, double* grad, cudaStream_t s) {
-    {
-        ProfScope ps(m, S_GRAD, s);
-        k_grad_fold<D, PAR><<<p.nb, kThreads, 0, s>>>(p, blocks);
-        LAUNCH_CHECK(m, "k_grad_fold");
-    }
-    {
-        ProfScope ps(m, S_RED, s);
-        k_reduce_blocks<D, TAgg<D>><<<1, kCarryThreads, 0, s>>>(blocks, p.nb, out);
-        LAUNCH_CHECK(m, "k_reduce_blocks(grad)");
-    }
-    cudaError_t e = cudaMemcpyAsync(grad + PAR, out + offsetof(TAgg<D>, a) / sizeof(double), sizeof(double),
-                                    cudaMemcpyDeviceToDevice, s);
-    if (e != cudaSuccess) return cuda_fail(m, e, "cudaMemcpyAsync(grad)");
-    return PSSGP_OK;
-}
-
+// NLL gradient (f1): primal filter storing (xbar, P), then ONE tangent fold of all three
+// parameter directions + an ordered block reduction (pssgp_grad.cuh).
 template <int D>
 pssgp_status run_grad(pssgp_model* m, int64_t N, const double* t, const double* y, const uint8_t* mask,
                       double* nll, double* grad, cudaStream_t s) {
@@ -358,12 +340,24 @@ pssgp_status run_grad(pssgp_model* m, int64_t N, const double* t, const double* 
     if ((st = phase_filter_apply<D>(m, p, s))) return st;
     if (nll && (st = nll_sum(m, p.nll_block, p.nb, nll, s))) return st;
     // block tangent aggregates reuse the smoother-aggregate region (not read on this path)
-    static_assert(sizeof(TAgg<D>) / sizeof(double) <= kThreads * SN(D), "grad scratch");
+    constexpr size_t NA = sizeof(TAgg3<D>) / sizeof(double);
+    static_assert(NA <= kThreads * SN(D), "grad scratch");
     double* blocks = p.chain_s;
-    double* out = p.chain_s + static_cast<size_t>(pl.nb) * (sizeof(TAgg<D>) / sizeof(double));
-    if ((st = grad_param<D, 0>(m, p, blocks, out, grad, s))) return st;
-    if ((st = grad_param<D, 1>(m, p, blocks, out, grad, s))) return st;
-    return grad_param<D, 2>(m, p, blocks, out, grad, s);
+    double* out = p.chain_s + static_cast<size_t>(pl.nb) * NA;
+    {
+        ProfScope ps(m, S_GRAD, s);
+        k_grad_fold<D><<<p.nb, kThreads, 0, s>>>(p, blocks);
+        LAUNCH_CHECK(m, "k_grad_fold");
+    }
+    {
+        ProfScope ps(m, S_RED, s);
+        k_reduce_blocks<D, TAgg3<D>><<<1, kCarryThreads, 0, s>>>(blocks, p.nb, out);
+        LAUNCH_CHECK(m, "k_reduce_blocks(grad)");
+    }
+    cudaError_t e = cudaMemcpyAsync(grad, out + offsetof(TAgg3<D>, a) / sizeof(double), 3 * sizeof(double),
+                                    cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(m, e, "cudaMemcpyAsync(grad)");
+    return PSSGP_OK;
 }
 
 template <int D>

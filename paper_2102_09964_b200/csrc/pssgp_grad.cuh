@@ -18,6 +18,9 @@
 // product of all chain aggregates (the global first element has M = 0, so the
 // incoming tangent is irrelevant).  The associativity that licenses the grouping is
 // that of function composition (the same argument as PAPER.md:326).
+// The three parameter directions share M, u and also the functional's b and C (they depend
+// only on the primal: b += M^T beta, C += sym(M^T beta u^T) + M^T Gamma M), so one pass folds
+// the 51-double aggregate (M, u, b, C | e_p, N_p, a_p for p = 1..3).
 // In the Jordan basis of the closed form (pssgp_math.cuh) F(z), Q(z) depend on z = lambda dt
 // only and dF/dz = J F, dQ/dz = sigma^2 w f f^T (f = last column of F, W1 = w e_d e_d^T),
 // so theta_ell = log ell gives dz = -z; P_inf = sigma^2 P1 does not depend on ell.
@@ -27,59 +30,103 @@
 namespace pssgp {
 
 template <int D>
-struct TAgg {
+struct TAgg3 {
     double M[D * D];
     double u[D];
-    double e[D];
-    double N[ns(D)];
-    double a;
     double b[D];
     double C[ns(D)];
+    double e[3][D];
+    double N[3][ns(D)];
+    double a[3];
 };
 
 template <int D>
-PS_HD void set_identity(TAgg<D>& t) {
+PS_HD void set_identity(TAgg3<D>& t) {
 #pragma unroll
     for (int i = 0; i < D; ++i) {
 #pragma unroll
         for (int j = 0; j < D; ++j) t.M[i * D + j] = (i == j) ? 1.0 : 0.0;
-        t.u[i] = 0.0; t.e[i] = 0.0; t.b[i] = 0.0;
+        t.u[i] = 0.0; t.b[i] = 0.0;
     }
 #pragma unroll
-    for (int i = 0; i < ns(D); ++i) { t.N[i] = 0.0; t.C[i] = 0.0; }
-    t.a = 0.0;
+    for (int i = 0; i < ns(D); ++i) t.C[i] = 0.0;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+#pragma unroll
+        for (int i = 0; i < D; ++i) t.e[q][i] = 0.0;
+#pragma unroll
+        for (int i = 0; i < ns(D); ++i) t.N[q][i] = 0.0;
+        t.a[q] = 0.0;
+    }
 }
 
 // out = t2 o t1 (t1 earlier in time): map composition + functional pull-back
+//   M = M2 M1, u = u1 + M1^T u2, b = b1 + M1^T b2, C = C1 + sym(M1^T b2 u1^T) + M1^T C2 M1,
+//   a_p = a1_p + a2_p + b2.e1_p + tr(C2 N1_p), e_p = M2 (e1_p + N1_p u2) + e2_p,
+//   N_p = M2 N1_p M2^T + N2_p.
 template <int D>
-PS_HD void combine(const TAgg<D>& t1, const TAgg<D>& t2, TAgg<D>& out) {
-    double Nu[D], MN[D * D], Mb[D];
-    // functional: a = a1 + a2 + b2.e1 + tr(C2 N1); b = b1 + M1^T b2; C = C1 + sym(w u1^T) + M1^T C2 M1, w = M1^T b2
-    double a = t1.a + t2.a;
+PS_HD void combine(const TAgg3<D>& t1, const TAgg3<D>& t2, TAgg3<D>& out) {
+    double Mb[D], Mu[D], C2M[D * D];
 #pragma unroll
     for (int i = 0; i < D; ++i) {
-        a = fma(t2.b[i], t1.e[i], a);
+        double sb = 0.0, su = 0.0;
 #pragma unroll
-        for (int j = 0; j < D; ++j) a = fma(t2.C[si(D, i, j)], t1.N[si(D, j, i)], a);
-    }
-    double C2M[D * D];
-#pragma unroll
-    for (int i = 0; i < D; ++i) {
-        double s = 0.0;
-#pragma unroll
-        for (int k = 0; k < D; ++k) s = fma(t1.M[k * D + i], t2.b[k], s);
-        Mb[i] = s;
+        for (int k = 0; k < D; ++k) {
+            sb = fma(t1.M[k * D + i], t2.b[k], sb);
+            su = fma(t1.M[k * D + i], t2.u[k], su);
+        }
+        Mb[i] = sb;
+        Mu[i] = su;
 #pragma unroll
         for (int j = 0; j < D; ++j) {
             double c = 0.0;
 #pragma unroll
             for (int k = 0; k < D; ++k) c = fma(t2.C[si(D, i, k)], t1.M[k * D + j], c);
-            C2M[i * D + j] = c;                                   // C2 M1
+            C2M[i * D + j] = c;
         }
     }
 #pragma unroll
-    for (int i = 0; i < D; ++i) {
-        out.b[i] = t1.b[i] + Mb[i];
+    for (int q = 0; q < 3; ++q) {
+        double a = t1.a[q] + t2.a[q];
+        double v[D], MN[D * D];
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            a = fma(t2.b[i], t1.e[q][i], a);
+            double s = t1.e[q][i];
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                a = fma(t2.C[si(D, i, j)], t1.N[q][si(D, j, i)], a);
+                s = fma(t1.N[q][si(D, i, j)], t2.u[j], s);
+            }
+            v[i] = s;
+        }
+        out.a[q] = a;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            double s = t2.e[q][i];
+#pragma unroll
+            for (int k = 0; k < D; ++k) s = fma(t2.M[i * D + k], v[k], s);
+            out.e[q][i] = s;
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                double mn = 0.0;
+#pragma unroll
+                for (int k = 0; k < D; ++k) mn = fma(t2.M[i * D + k], t1.N[q][si(D, k, j)], mn);
+                MN[i * D + j] = mn;
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+            for (int j = i; j < D; ++j) {
+                double s = t2.N[q][si(D, i, j)];
+#pragma unroll
+                for (int k = 0; k < D; ++k) s = fma(MN[i * D + k], t2.M[j * D + k], s);
+                out.N[q][si(D, i, j)] = s;
+            }
+    }
+#pragma unroll
+    for (int i = 0; i < D; ++i)
 #pragma unroll
         for (int j = i; j < D; ++j) {
             double c = t1.C[si(D, i, j)] + 0.5 * (Mb[i] * t1.u[j] + t1.u[i] * Mb[j]);
@@ -87,193 +134,223 @@ PS_HD void combine(const TAgg<D>& t1, const TAgg<D>& t2, TAgg<D>& out) {
             for (int k = 0; k < D; ++k) c = fma(t1.M[k * D + i], C2M[k * D + j], c);
             out.C[si(D, i, j)] = c;
         }
-    }
-    out.a = a;
-    // map: M = M2 M1; u = u1 + M1^T u2; e = M2 e1 + M2 N1 u2 + e2; N = M2 N1 M2^T + N2
-#pragma unroll
-    for (int i = 0; i < D; ++i) {
-        double s = 0.0;
-#pragma unroll
-        for (int k = 0; k < D; ++k) s = fma(t1.N[si(D, i, k)], t2.u[k], s);
-        Nu[i] = s;
-    }
-    double M[D * D], u[D], e[D];
-#pragma unroll
-    for (int i = 0; i < D; ++i) {
-        double ue = t1.u[i], ee = t2.e[i];
-#pragma unroll
-        for (int k = 0; k < D; ++k) {
-            ue = fma(t1.M[k * D + i], t2.u[k], ue);
-            ee = fma(t2.M[i * D + k], t1.e[k] + Nu[k], ee);
-        }
-        u[i] = ue;
-        e[i] = ee;
-#pragma unroll
-        for (int j = 0; j < D; ++j) {
-            double m = 0.0, mn = 0.0;
-#pragma unroll
-            for (int k = 0; k < D; ++k) {
-                m = fma(t2.M[i * D + k], t1.M[k * D + j], m);
-                mn = fma(t2.M[i * D + k], t1.N[si(D, k, j)], mn);
-            }
-            M[i * D + j] = m;
-            MN[i * D + j] = mn;
-        }
-    }
+    double M[D * D];
 #pragma unroll
     for (int i = 0; i < D; ++i)
 #pragma unroll
-        for (int j = i; j < D; ++j) {
-            double s = t2.N[si(D, i, j)];
+        for (int j = 0; j < D; ++j) {
+            double m = 0.0;
 #pragma unroll
-            for (int k = 0; k < D; ++k) s = fma(MN[i * D + k], t2.M[j * D + k], s);
-            out.N[si(D, i, j)] = s;
+            for (int k = 0; k < D; ++k) m = fma(t2.M[i * D + k], t1.M[k * D + j], m);
+            M[i * D + j] = m;
         }
 #pragma unroll
     for (int i = 0; i < D * D; ++i) out.M[i] = M[i];
 #pragma unroll
-    for (int i = 0; i < D; ++i) { out.u[i] = u[i]; out.e[i] = e[i]; }
+    for (int i = 0; i < D; ++i) {
+        out.u[i] = t1.u[i] + Mu[i];
+        out.b[i] = t1.b[i] + Mb[i];
+    }
 }
 
-// Append one step (primal entering the step: x = xbar_{k-1}, P = P_{k-1}) to the aggregate.
-// PAR: 0 = log sigma^2, 1 = log ell, 2 = log sigma_n^2.  first: global first element.
-template <int D, int PAR>
-PS_HD void grad_fold_step(TAgg<D>& A, const double (&x)[D], const double (&P)[ns(D)], const FMat<D>& Fm,
-                          const double (&Q)[ns(D)], double z, const ModelParams<D>& m, bool first, bool obs,
-                          double yk) {
+// Append one step (primal entering the step: x = xbar_{k-1}, P = P_{k-1}) to the aggregate,
+// all three parameter directions at once.  first: global first element (F = 0, Q = P_inf).
+template <int D>
+PS_HD void grad_fold_step3(TAgg3<D>& A, const double (&x)[D], const double (&P)[ns(D)], const FMat<D>& Fm,
+                           const double (&Q)[ns(D)], double z, const ModelParams<D>& m, bool first, bool obs,
+                           double yk) {
     const double (&F)[D * D] = Fm.a;
-    // primal predict + update quantities
     double FP[D * D], Pm[ns(D)], xm[D];
     kf_predict<D>(x, P, Fm, Q, xm, FP, Pm);
     const double S = Pm[0] + m.r;
     const double iS = obs ? rcp(S) : 0.0;
     const double v = obs ? (yk - xm[0]) : 0.0;
     const double vs = v * iS;
+    const double c1 = 0.5 * (iS - vs * vs);
     double K[D];
 #pragma unroll
     for (int i = 0; i < D; ++i) K[i] = Pm[si(D, i, 0)] * iS;
-    // parameter derivatives dF, dQ, dr
-    double dF[D * D], dQ[ns(D)];
-    double dr = 0.0;
+    // per-parameter step terms e_k[q], N_k[q], alpha[q]
+    double ek[3][D], Nk[3][ns(D)], alpha[3];
+    // q = 0: log sigma^2 -> dF = 0, dQ = Q (P_inf at the first element), dr = 0: B = Q
+    {
+        double IB[D * D];
 #pragma unroll
-    for (int i = 0; i < D * D; ++i) dF[i] = 0.0;
+        for (int i = 0; i < D; ++i)
 #pragma unroll
-    for (int i = 0; i < ns(D); ++i) dQ[i] = 0.0;
-    if constexpr (PAR == 0) {
+            for (int j = 0; j < D; ++j) IB[i * D + j] = fma(-K[i], Q[si(D, 0, j)], Q[si(D, i, j)]);
 #pragma unroll
-        for (int i = 0; i < ns(D); ++i) dQ[i] = Q[i];             // Q, P_inf proportional to sigma^2
-    } else if constexpr (PAR == 1) {
+        for (int i = 0; i < D; ++i) {
+            ek[0][i] = fma(-K[i], Q[0], Q[si(D, i, 0)]) * vs;
+#pragma unroll
+            for (int j = i; j < D; ++j) Nk[0][si(D, i, j)] = fma(-IB[i * D], K[j], IB[i * D + j]);
+        }
+        alpha[0] = c1 * Q[0];
+    }
+    // q = 1: log ell -> dz = -z: dF = -z J F (J = -I + N), dQ = -z sigma^2 w f f^T, dr = 0
+    {
+        double B[ns(D)], dFx[D];
         if (!first) {
-            // dF = -z J F (Jordan basis: J = -I + N), dQ = -z sigma^2 w f f^T
             const double w = (D == 1) ? 2.0 : (D == 2) ? 4.0 : 16.0 / 3.0;
+            double dF[D * D];
 #pragma unroll
             for (int i = 0; i < D; ++i)
 #pragma unroll
                 for (int j = 0; j < D; ++j)
                     dF[i * D + j] = -z * ((i + 1 < D) ? F[(i + 1) * D + j] - F[i * D + j] : -F[i * D + j]);
+            double X[D * D];
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+                double s = 0.0;
+#pragma unroll
+                for (int k = 0; k < D; ++k) s = fma(dF[i * D + k], x[k], s);
+                dFx[i] = s;
+#pragma unroll
+                for (int j = 0; j < D; ++j) {
+                    double t = 0.0;
+#pragma unroll
+                    for (int k = 0; k < D; ++k) t = fma(dF[i * D + k], FP[j * D + k], t);
+                    X[i * D + j] = t;
+                }
+            }
+            const double zsw = -z * m.s2 * w;
 #pragma unroll
             for (int i = 0; i < D; ++i)
 #pragma unroll
-                for (int j = i; j < D; ++j) dQ[si(D, i, j)] = -z * m.s2 * w * F[i * D + D - 1] * F[j * D + D - 1];
+                for (int j = i; j < D; ++j)
+                    B[si(D, i, j)] = fma(zsw * F[i * D + D - 1], F[j * D + D - 1], X[i * D + j] + X[j * D + i]);
+        } else {
+#pragma unroll
+            for (int i = 0; i < ns(D); ++i) B[i] = 0.0;
+#pragma unroll
+            for (int i = 0; i < D; ++i) dFx[i] = 0.0;
         }
-    } else {
-        dr = m.r;
-    }
-    // B = dF P F^T + F P dF^T + dQ = X + X^T + dQ, X = dF (F P)^T
-    double B[ns(D)], dFx[D];
-    {
-        double X[D * D];
+        double IB[D * D];
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+            for (int j = 0; j < D; ++j) IB[i * D + j] = fma(-K[i], B[si(D, 0, j)], B[si(D, i, j)]);
 #pragma unroll
         for (int i = 0; i < D; ++i) {
-            double s = 0.0;
+            ek[1][i] = fma(-K[i], dFx[0] + B[0] * vs, dFx[i] + B[si(D, i, 0)] * vs);
 #pragma unroll
-            for (int k = 0; k < D; ++k) s = fma(dF[i * D + k], x[k], s);
-            dFx[i] = s;
+            for (int j = i; j < D; ++j) Nk[1][si(D, i, j)] = fma(-IB[i * D], K[j], IB[i * D + j]);
+        }
+        alpha[1] = c1 * B[0] - vs * dFx[0];
+    }
+    // q = 2: log sigma_n^2 -> dr = r: e = -K r v/S, N = K r K^T
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        ek[2][i] = -K[i] * (m.r * vs);
+#pragma unroll
+        for (int j = i; j < D; ++j) Nk[2][si(D, i, j)] = (K[i] * m.r) * K[j];
+    }
+    alpha[2] = c1 * m.r;
+    // functional of this step pulled back through A (g = F^T e_0, h = M^T g, beta = -(v/S) g)
+    double h[D];
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < D; ++k) s = fma(A.M[k * D + i], F[k], s);
+        h[i] = s;
+    }
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        double ge = 0.0, gNg = 0.0;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            ge = fma(F[i], A.e[q][i], ge);
+            double t = 0.0;
+#pragma unroll
+            for (int j = 0; j < D; ++j) t = fma(A.N[q][si(D, i, j)], F[j], t);
+            gNg = fma(F[i], t, gNg);
+        }
+        A.a[q] += alpha[q] - vs * ge + c1 * gNg;
+    }
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = i; j < D; ++j)
+            A.C[si(D, i, j)] += -0.5 * vs * (h[i] * A.u[j] + A.u[i] * h[j]) + c1 * h[i] * h[j];
+#pragma unroll
+    for (int i = 0; i < D; ++i) A.b[i] = fma(-vs, h[i], A.b[i]);
+    // map: Mk = F - K F[0,:], uk = F[0,:]^T v/S; u += M^T uk; e_q = Mk (e_q + N_q uk) + ek_q;
+    // N_q = Mk N_q Mk^T + Nk_q; M = Mk M
+    double Mk[D * D], uk[D];
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        uk[i] = F[i] * vs;
+#pragma unroll
+        for (int j = 0; j < D; ++j) Mk[i * D + j] = fma(-K[i], F[j], F[i * D + j]);
+    }
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        double s = A.u[i];
+#pragma unroll
+        for (int k = 0; k < D; ++k) s = fma(A.M[k * D + i], uk[k], s);
+        A.u[i] = s;
+    }
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        double w[D], MN[D * D];
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            double s = A.e[q][i];
+#pragma unroll
+            for (int j = 0; j < D; ++j) s = fma(A.N[q][si(D, i, j)], uk[j], s);
+            w[i] = s;
+        }
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            double s = ek[q][i];
+#pragma unroll
+            for (int k = 0; k < D; ++k) s = fma(Mk[i * D + k], w[k], s);
+            A.e[q][i] = s;
 #pragma unroll
             for (int j = 0; j < D; ++j) {
                 double t = 0.0;
 #pragma unroll
-                for (int k = 0; k < D; ++k) t = fma(dF[i * D + k], FP[j * D + k], t);
-                X[i * D + j] = t;
+                for (int k = 0; k < D; ++k) t = fma(Mk[i * D + k], A.N[q][si(D, k, j)], t);
+                MN[i * D + j] = t;
             }
         }
 #pragma unroll
         for (int i = 0; i < D; ++i)
 #pragma unroll
-            for (int j = i; j < D; ++j) B[si(D, i, j)] = X[i * D + j] + X[j * D + i] + dQ[si(D, i, j)];
-    }
-    // step element: Mk = (I - K H) F, uk = F^T H^T v/S, ek, Nk
-    double Mk[D * D], uk[D], ek[D], Nk[ns(D)], IB[D * D];
+            for (int j = i; j < D; ++j) {
+                double s = Nk[q][si(D, i, j)];
 #pragma unroll
-    for (int i = 0; i < D; ++i) {
-#pragma unroll
-        for (int j = 0; j < D; ++j) Mk[i * D + j] = fma(-K[i], F[j], F[i * D + j]);
-        uk[i] = F[i] * vs;                                        // F[0][i]: g = F^T e0
+                for (int k = 0; k < D; ++k) s = fma(MN[i * D + k], Mk[j * D + k], s);
+                A.N[q][si(D, i, j)] = s;
+            }
     }
-    // IB = (I - K H) B  (full), then Nk = IB (I - K H)^T + K dr K^T
+    double M[D * D];
 #pragma unroll
     for (int i = 0; i < D; ++i)
 #pragma unroll
-        for (int j = 0; j < D; ++j) IB[i * D + j] = fma(-K[i], B[si(D, 0, j)], B[si(D, i, j)]);
-#pragma unroll
-    for (int i = 0; i < D; ++i) {
-        ek[i] = fma(-K[i], dFx[0] + B[si(D, 0, 0)] * vs, dFx[i] + B[si(D, i, 0)] * vs) - K[i] * dr * vs;
-#pragma unroll
-        for (int j = i; j < D; ++j) Nk[si(D, i, j)] = fma(-IB[i * D], K[j], IB[i * D + j]) + K[i] * dr * K[j];
-    }
-    // functional of this step, pulled back through A: alpha + beta.e + tr(Gamma N); b += M^T beta;
-    // C += sym(M^T beta u^T) + c1 h h^T with g = F[0,:]^T, h = M^T g, beta = -(v/S) g
-    if (obs) {
-        const double c1 = 0.5 * (iS - vs * vs);
-        double h[D];
-#pragma unroll
-        for (int i = 0; i < D; ++i) {
+        for (int j = 0; j < D; ++j) {
             double s = 0.0;
 #pragma unroll
-            for (int k = 0; k < D; ++k) s = fma(A.M[k * D + i], F[k], s);
-            h[i] = s;
+            for (int k = 0; k < D; ++k) s = fma(Mk[i * D + k], A.M[k * D + j], s);
+            M[i * D + j] = s;
         }
-        double ge = 0.0, gNg = 0.0;
 #pragma unroll
-        for (int i = 0; i < D; ++i) {
-            ge = fma(F[i], A.e[i], ge);
-#pragma unroll
-            for (int j = 0; j < D; ++j) gNg = fma(F[i] * A.N[si(D, i, j)], F[j], gNg);
-        }
-        A.a += c1 * (B[0] + dr) - vs * dFx[0] - vs * ge + c1 * gNg;
-#pragma unroll
-        for (int i = 0; i < D; ++i) A.b[i] = fma(-vs, h[i], A.b[i]);
-#pragma unroll
-        for (int i = 0; i < D; ++i)
-#pragma unroll
-            for (int j = i; j < D; ++j)
-                A.C[si(D, i, j)] += -0.5 * vs * (h[i] * A.u[j] + A.u[i] * h[j]) + c1 * h[i] * h[j];
-    }
-    // compose the map: M = Mk M, u = u + M^T uk, e = Mk e + Mk N uk + ek, N = Mk N Mk^T + Nk
-    TAgg<D> step;
-#pragma unroll
-    for (int i = 0; i < D * D; ++i) step.M[i] = Mk[i];
-#pragma unroll
-    for (int i = 0; i < D; ++i) { step.u[i] = uk[i]; step.e[i] = ek[i]; step.b[i] = 0.0; }
-#pragma unroll
-    for (int i = 0; i < ns(D); ++i) { step.N[i] = Nk[i]; step.C[i] = 0.0; }
-    step.a = 0.0;
-    TAgg<D> r;
-    combine(A, step, r);
-    A = r;
+    for (int i = 0; i < D * D; ++i) A.M[i] = M[i];
 }
 
 // ------------------------------------------------------------------ KG: fold tangent aggregates per chain
-// Reads the filtered moments (xbar_k, P_k) written by k_filter_apply (same launch plan).
-template <int D, int PAR>
-__global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_grad_fold(const KParams<D> p, double* block_out) {
-    __shared__ TAgg<D> wagg[kWarps];
+// Reads the filtered moments (xbar_k, P_k) written by k_filter_apply (same launch plan); one
+// pass for all three parameters; 2 CTAs / SM (the 51-double aggregate needs the registers).
+template <int D>
+__global__ void __launch_bounds__(kThreads, 2) k_grad_fold(const KParams<D> p, double* block_out) {
+    __shared__ TAgg3<D> wagg[kWarps];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t c = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
     const int64_t wg = static_cast<int64_t>(blockIdx.x) * kWarps + wid;
     const int64_t kb = c * p.K;
     const int64_t ke = min(kb + p.K, p.n);
-    TAgg<D> A;
+    TAgg3<D> A;
     set_identity(A);
     double x[D], P[ns(D)];
 #pragma unroll
@@ -309,7 +386,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_grad_fold(const KParam
             z = p.m.lam * (tk - tprev);
             matern_closed<D>(p.m.lam, p.m.s2, tk - tprev, Fj, Q);
         }
-        grad_fold_step<D, PAR>(A, x, P, to_full<D>(Fj), Q, z, p.m, first, obs, yk);
+        grad_fold_step3<D>(A, x, P, to_full<D>(Fj), Q, z, p.m, first, obs, yk);
         tprev = tk;
         const double* src = xpw + ((k - kb) * CN(D)) * 32;
 #pragma unroll
@@ -320,10 +397,10 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_grad_fold(const KParam
     // ordered CTA reduction
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
-        TAgg<D> o;
+        TAgg3<D> o;
         shfl_down_all(o, A, off);
         if ((lane & (2 * off - 1)) == 0) {
-            TAgg<D> r;
+            TAgg3<D> r;
             combine(A, o, r);
             A = r;
         }
@@ -331,13 +408,13 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_grad_fold(const KParam
     if (lane == 0) wagg[wid] = A;
     __syncthreads();
     if (threadIdx.x == 0) {
-        TAgg<D> acc = wagg[0];
+        TAgg3<D> acc = wagg[0];
         for (int w = 1; w < kWarps; ++w) {
-            TAgg<D> r;
+            TAgg3<D> r;
             combine(acc, wagg[w], r);
             acc = r;
         }
-        store_aos(acc, block_out + static_cast<int64_t>(blockIdx.x) * (sizeof(TAgg<D>) / sizeof(double)));
+        store_aos(acc, block_out + static_cast<int64_t>(blockIdx.x) * (sizeof(TAgg3<D>) / sizeof(double)));
     }
 }
 
