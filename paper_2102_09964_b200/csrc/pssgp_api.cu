@@ -138,6 +138,8 @@ void fill_params(const pssgp_model* m, ModelParams<D>& p) {
     p.closed = m->closed ? 1 : 0;
     p.udt = m->udt > 0.0 ? m->udt : -1.0;  // -1 never equals a valid dt >= 0
     for (int i = 0; i < D * D; ++i) p.G[i] = static_cast<double>(m->ssm.G[i]);
+    for (int i = 0; i < D; ++i)
+        for (int j = i; j < D; ++j) p.W[si(D, i, j)] = static_cast<double>(m->ssm.W[i * D + j]);
     if (m->udt > 0.0) {
         for (int i = 0; i < D * D; ++i) p.Fu[i] = m->Fu[i];
         for (int i = 0; i < D; ++i)
@@ -459,6 +461,7 @@ pssgp_status wide_setup(pssgp_model* m, const WPlan& pl, pssgp::wide::WParams& p
         h[3 * D * D + D] = m->r;
         h[3 * D * D + D + 1] = m->udt > 0.0 ? m->udt : -1.0;
         for (int i = 0; i < D * D; ++i) h[3 * D * D + D + 2 + i] = static_cast<double>(m->ssm.G[i]);
+        for (int i = 0; i < D * D; ++i) h[4 * D * D + D + 2 + i] = static_cast<double>(m->ssm.W[i]);
         if (cudaMalloc(&m->d_model, h.size() * sizeof(double)) != cudaSuccess) {
             cudaGetLastError();
             return fail(m, PSSGP_E_NOMEM, "cudaMalloc(model)");

@@ -148,6 +148,7 @@ struct ModelParams {
     double Fu[D * D];     // F(udt)
     double Qu[ns(D)];     // Q(udt)
     double G[D * D];      // continuous drift (balanced coordinates), kPade mode
+    double W[ns(D)];      // diffusion L q L^T (balanced coordinates), kPade mode
     int closed;           // 1: Matern closed form of order D available in the lambda-scaled basis
     int h_unit;           // 1: H == e_0
 };
@@ -515,8 +516,9 @@ PS_HD void matern_closed(double lam, double s2, double dt, FJor<D>& F, double (&
 // lookup), kTable = the host-precomputed pair for dt == udt (dt = 0 -> I, 0; anything
 // else unsupported), kMixed = retired (closed models always use kClosed),
 // kPade = any model, any dt: F = expm(G dt) by scaling and squaring with the
-// [7/7] Pade approximant, Q = P_inf - F P_inf F^T (Lyapunov form of the stationary
-// model; north_star "per-step small-matrix expm via scaling-and-squaring Pade").
+// [7/7] Pade approximant and Q by the Taylor series of the Lyapunov ODE on the same scaled
+// step, composed by doubling (taylor_fq; north_star "per-step small-matrix expm via
+// scaling-and-squaring Pade").
 enum DiscMode : int { kClosed = 0, kTable = 1, kMixed = 2, kPade = 3 };
 
 // F = expm(G dt), D x D row-major.  Higham (2005): the [7/7] Pade approximant is
@@ -584,6 +586,99 @@ PS_HD void expm_pade7(const double (&G)[D * D], double dt, double (&F)[D * D]) {
     }
 }
 
+// F = e^{G dt} and Q = int_0^dt e^{Gs} W e^{G^T s} ds together, cancellation-free at every dt
+// (the stationary shortcut P_inf - F P_inf F^T loses the small entries of Q when ||G dt|| << 1,
+// SURVEY A.4): on the scaled step tau = dt / 2^s with ||G tau||_1 <= 1/8,
+//   F_tau = [7/7] Pade of e^A,  Q_tau = sum_{k=1..m} Z_k,  A = G tau,
+//   Z_1 = tau W,  Z_{k+1} = (A Z_k + Z_k A^T) / (k + 1)      (Taylor series of the Lyapunov ODE),
+// m = 12 (truncation (2/8)^m / (m+1)! < 1e-17 relative; m = 7 when ||G dt|| <= 1/100), then s
+// doublings Q <- Q + F Q F^T, F <- F F (the semigroup identity, as Van Loan composes sub-steps).
+template <int D>
+PS_HD void taylor_fq(const double (&G)[D * D], const double (&W)[ns(D)], double dt, double (&F)[D * D],
+                     double (&Q)[ns(D)]) {
+    double nrm = 0.0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        double c = 0.0;
+#pragma unroll
+        for (int i = 0; i < D; ++i) c += fabs(G[i * D + j]);
+        nrm = fmax(nrm, c);
+    }
+    nrm *= fabs(dt);
+    int s = 0;
+    if (nrm > 0.125) {
+        int e;
+        frexp(nrm / 0.125, &e);
+        s = e;
+    }
+    const double tau = ldexp(dt, -s);
+    const int m = (nrm <= 0.01) ? 7 : 12;
+    double A[D * D];
+#pragma unroll
+    for (int i = 0; i < D * D; ++i) A[i] = G[i] * tau;
+    // F on the scaled step: [7/7] Pade (||A||_1 <= 1/8 < theta_7: no further scaling)
+    double T[D * D];
+    expm_pade7<D>(G, tau, F);
+    // Q: Z_1 = tau W, Z_{k+1} = (A Z_k + Z_k A^T) / (k + 1)
+    double Z[ns(D)];
+#pragma unroll
+    for (int i = 0; i < ns(D); ++i) { Z[i] = W[i] * tau; Q[i] = Z[i]; }
+    for (int k = 1; k < m; ++k) {
+        const double ik = 1.0 / (k + 1);
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                double acc = 0.0;
+#pragma unroll
+                for (int l = 0; l < D; ++l) acc = fma(A[i * D + l], Z[si(D, l, j)], acc);
+                T[i * D + j] = acc;                         // Y = A Z
+            }
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+            for (int j = i; j < D; ++j) {
+                Z[si(D, i, j)] = (T[i * D + j] + T[j * D + i]) * ik;
+                Q[si(D, i, j)] += Z[si(D, i, j)];
+            }
+    }
+    // doublings: Q(2t) = Q(t) + F(t) Q(t) F(t)^T, F(2t) = F(t)^2
+    for (int q = 0; q < s; ++q) {
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                double acc = 0.0;
+#pragma unroll
+                for (int l = 0; l < D; ++l) acc = fma(F[i * D + l], Q[si(D, l, j)], acc);
+                T[i * D + j] = acc;                         // F Q
+            }
+        double Qn[ns(D)];
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+            for (int j = i; j < D; ++j) {
+                double acc = Q[si(D, i, j)];
+#pragma unroll
+                for (int l = 0; l < D; ++l) acc = fma(T[i * D + l], F[j * D + l], acc);
+                Qn[si(D, i, j)] = acc;
+            }
+#pragma unroll
+        for (int i = 0; i < ns(D); ++i) Q[i] = Qn[i];
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                double acc = 0.0;
+#pragma unroll
+                for (int l = 0; l < D; ++l) acc = fma(F[i * D + l], F[l * D + j], acc);
+                T[i * D + j] = acc;
+            }
+#pragma unroll
+        for (int i = 0; i < D * D; ++i) F[i] = T[i];
+    }
+}
+
 // transition type of each mode: Jordan-structured for the Matern closed form
 template <int D, int MODE>
 using FT_t = typename std::conditional<MODE == kClosed, FJor<D>, FMat<D>>::type;
@@ -612,27 +707,7 @@ PS_HD int disc(const ModelParams<D>& p, double dt, FT_t<D, MODE>& Ft, double (&Q
                 for (int i = 0; i < ns(D); ++i) Q[i] = 0.0;
                 return 0;
             }
-            expm_pade7<D>(p.G, dt, F);
-            // Q = P_inf - F P_inf F^T
-            double FP[D * D];
-#pragma unroll
-            for (int i = 0; i < D; ++i)
-#pragma unroll
-                for (int j = 0; j < D; ++j) {
-                    double acc = 0.0;
-#pragma unroll
-                    for (int k = 0; k < D; ++k) acc = fma(F[i * D + k], p.Pinf[si(D, k, j)], acc);
-                    FP[i * D + j] = acc;
-                }
-#pragma unroll
-            for (int i = 0; i < D; ++i)
-#pragma unroll
-                for (int j = i; j < D; ++j) {
-                    double acc = p.Pinf[si(D, i, j)];
-#pragma unroll
-                    for (int k = 0; k < D; ++k) acc = fma(-FP[i * D + k], F[j * D + k], acc);
-                    Q[si(D, i, j)] = acc;
-                }
+            taylor_fq<D>(p.G, p.W, dt, F, Q);
             return 0;
         } else {
             const bool zero = (dt == 0.0);

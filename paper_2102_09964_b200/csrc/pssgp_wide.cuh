@@ -27,7 +27,7 @@ PS_CX int LD(int D) { return D + 1; }            // padded row stride of a share
 PS_CX int FNW(int D) { return 3 * D * D + 2 * D; } // full filter aggregate: A, b, C, eta, J
 PS_CX int SNW(int D) { return 2 * D * D + D; }     // full smoother aggregate: E, g, L
 PS_CX int CNW(int D) { return D + D * (D + 1) / 2; } // filtered (x, P packed upper)
-PS_CX int MODW(int D) { return 4 * D * D + D + 2; }  // model: F, Q, Pinf, H, r, udt, G
+PS_CX int MODW(int D) { return 5 * D * D + D + 2; }  // model: F, Q, Pinf, H, r, udt, G, W
 PS_CX int FQW(int D) { return 2 * D * LD(D); }     // per-step F, Q (rows of stride LD) in kPade mode
 
 struct WParams {
@@ -583,17 +583,18 @@ __device__ __forceinline__ FQp<D> wfq(const WParams& p, const SModel<D>& M, int6
 }
 
 // ------------------------------------------------------------------ KDw: per-step discretisation
-// One warp per step (grid-stride): F = expm(G dt) by scaling and squaring with a
-// truncated Taylor polynomial evaluated Paterson-Stockmeyer style (no pivoted solve:
-// a warp-level elimination costs D serial rounds), degree m = 6 for
-// ||A||_1 <= 0.017 and m = 12 for ||A||_1 <= 0.33 (remainder theta^(m+1)/(m+1)!
-// <= 2^-53 relative), A = G dt / 2^s; then Q = P_inf - F P_inf F^T (Lyapunov form of
-// the stationary model).  Writes fq[k] for local steps k in [0, nfq) with a
-// predecessor (global index > 0) and dt != 0.
+// One warp per step (grid-stride).  On the scaled step tau = dt / 2^s with ||G tau||_1 <= 1/8:
+// F_tau by a truncated Taylor polynomial in Paterson-Stockmeyer form (no pivoted solve: a warp
+// elimination costs D serial rounds; degree 6 for ||G dt|| <= 0.017, else 12) and
+// Q_tau = sum_{k=1..m} Z_k, Z_1 = tau W, Z_{k+1} = (A Z_k + Z_k A^T)/(k+1) (Taylor series of the
+// Lyapunov ODE, cancellation-free; m = 7 / 12), then s doublings Q <- Q + F Q F^T, F <- F^2.
+// (The stationary shortcut P_inf - F P_inf F^T loses the small entries of Q on fine grids,
+// SURVEY A.4.)  Writes fq[k] for local steps k in [0, nfq) with a predecessor and dt != 0.
 template <int D>
 struct KDSmem {
     double G[D][LD(D)];
     double Pinf[D][LD(D)];
+    double Wd[D][LD(D)];
     double gnorm;
     struct PerWarp {
         double A[D][LD(D)], A2[D][LD(D)], A3[D][LD(D)], X[D][LD(D)], T[D][LD(D)], B[D][LD(D)];
@@ -622,6 +623,7 @@ __global__ void __launch_bounds__(32 * kWWarps) kw_discretize(const double* __re
         const int i = e / D, j = e - (e / D) * D;
         sh.G[i][j] = model[3 * D * D + D + 2 + e];
         sh.Pinf[i][j] = model[2 * D * D + e];
+        sh.Wd[i][j] = model[4 * D * D + D + 2 + e];
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -646,22 +648,20 @@ __global__ void __launch_bounds__(32 * kWWarps) kw_discretize(const double* __re
         if (dt == 0.0 || !(dt == dt)) continue;
         const double nrm = sh.gnorm * fabs(dt);
         int s = 0;
-        if (nrm > 0.33) frexp(nrm / 0.33, &s);
-        const bool low = (ldexp(nrm, -s) <= 0.017);
-        const double sc = ldexp(dt, -s);
-        for (int e = lane; e < D * D; e += 32) W.A[e / D][e % D] = sh.G[e / D][e % D] * sc;
+        if (nrm > 0.125) frexp(nrm / 0.125, &s);
+        const bool low = (nrm <= 0.017);
+        const double tau = ldexp(dt, -s);
+        for (int e = lane; e < D * D; e += 32) W.A[e / D][e % D] = sh.G[e / D][e % D] * tau;
         __syncwarp();
         wmm<D>(W.A2, W.A, W.A, nullptr, lane);
         __syncwarp();
         wmm<D>(W.A3, W.A2, W.A, nullptr, lane);
         __syncwarp();
-        double (*F)[LD(D)];
         if (low) {   // m = 6: F = B0 + A3 (c3 I + c4 A + c5 A2 + c6 A3)
             taylor_block<D>(W.X, W.A, W.A2, W.A3, c[3], c[4], c[5], c[6], lane);
             taylor_block<D>(W.B, W.A, W.A2, nullptr, c[0], c[1], c[2], 0.0, lane);
             __syncwarp();
             wmm<D>(W.T, W.A3, W.X, W.B, lane);
-            F = W.T;
         } else {     // m = 12: Horner in A3 over degree-2 blocks, top block degree 3
             taylor_block<D>(W.X, W.A, W.A2, W.A3, c[9], c[10], c[11], c[12], lane);
             taylor_block<D>(W.B, W.A, W.A2, nullptr, c[6], c[7], c[8], 0.0, lane);
@@ -675,27 +675,48 @@ __global__ void __launch_bounds__(32 * kWWarps) kw_discretize(const double* __re
             taylor_block<D>(W.B, W.A, W.A2, nullptr, c[0], c[1], c[2], 0.0, lane);
             __syncwarp();
             wmm<D>(W.T, W.A3, W.X, W.B, lane);
-            F = W.T;
         }
         __syncwarp();
-        double (*Fs)[LD(D)] = W.X;
-        for (int q = 0; q < s; ++q) {
-            wmm<D>(Fs, F, F, nullptr, lane);
+        double (*F)[LD(D)] = W.T;
+        // Q_tau: Z = tau W (in A2), Q (in X) accumulates, Y = A Z (in A3)
+        double (*Z)[LD(D)] = W.A2;
+        double (*Qc)[LD(D)] = W.X;
+        for (int e = lane; e < D * D; e += 32) {
+            const int i = e / D, j = e - (e / D) * D;
+            Z[i][j] = sh.Wd[i][j] * tau;
+            Qc[i][j] = Z[i][j];
+        }
+        __syncwarp();
+        const int mq = low ? 7 : 12;
+        for (int kk = 1; kk < mq; ++kk) {
+            wmm<D>(W.A3, W.A, Z, nullptr, lane);
             __syncwarp();
-            double (*tmp)[LD(D)] = F; F = Fs; Fs = tmp;
+            const double ik = 1.0 / (kk + 1);
+            for (int e = lane; e < D * D; e += 32) {
+                const int i = e / D, j = e - (e / D) * D;
+                const double zz = (W.A3[i][j] + W.A3[j][i]) * ik;
+                Z[i][j] = zz;
+                Qc[i][j] += zz;
+            }
+            __syncwarp();
         }
-        // Q = P_inf - (F P_inf) F^T   (B = -F P_inf, A = Q)
-        wmm<D>(W.B, F, sh.Pinf, nullptr, lane);
-        __syncwarp();
-        for (int e = lane; e < D * D; e += 32) W.B[e / D][e % D] = -W.B[e / D][e % D];
-        __syncwarp();
-        wmm<D, false, true>(W.A, W.B, F, sh.Pinf, lane);
-        __syncwarp();
+        // doublings: Q <- Q + F Q F^T, F <- F F   (buffers: B = F Q, A2 / X ping-pong for Q, A3 for F^2)
+        double (*Qn)[LD(D)] = W.A2;
+        double (*Fn)[LD(D)] = W.A3;
+        for (int q = 0; q < s; ++q) {
+            wmm<D>(W.B, F, Qc, nullptr, lane);
+            __syncwarp();
+            wmm<D, false, true>(Qn, W.B, F, Qc, lane);
+            wmm<D>(Fn, F, F, nullptr, lane);
+            __syncwarp();
+            double (*t1)[LD(D)] = Qc; Qc = Qn; Qn = t1;
+            double (*t2)[LD(D)] = F; F = Fn; Fn = t2;
+        }
         double* o = fq + k * FQW(D);
         for (int e = lane; e < D * D; e += 32) {
             const int i = e / D, j = e - (e / D) * D;
             o[i * LD(D) + j] = F[i][j];
-            o[(D + i) * LD(D) + j] = 0.5 * (W.A[i][j] + W.A[j][i]);
+            o[(D + i) * LD(D) + j] = 0.5 * (Qc[i][j] + Qc[j][i]);
         }
         __syncwarp();
     }
