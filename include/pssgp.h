@@ -93,11 +93,12 @@ typedef struct {
                                  Non-Matern models (no closed form):
                                    > 0 -> only dt = uniform_dt or 0 allowed, other steps fail
                                           with PSSGP_E_UNSUPPORTED (pure uniform grids);
-                                   = 0 -> any dt: per-step F = expm(G dt) by [7/7] Pade
-                                          scaling and squaring on the device and
-                                          Q = P_inf - F P_inf F^T (north_star discretisation
-                                          kernel; d > 3 stores (F, Q) per step in a
-                                          handle-owned buffer of N 2 d (d+1) doubles). */
+                                   = 0 -> any dt: per-step F = expm(G dt) by scaling and
+                                          squaring on the device and Q by the Taylor series
+                                          of the Lyapunov ODE on the scaled step composed by
+                                          doubling (north_star discretisation kernel; d > 3
+                                          stores (F, Q) per step in a handle-owned buffer of
+                                          N 2 d (d+1) doubles). */
     int64_t chain_len;        /* steps per thread chain (0 = automatic)                   */
     int blocks_per_sm;        /* CTAs per SM for the one-wave grid (0 = automatic)        */
 } pssgp_options;
