@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_filter_apply(con
         const double yk = obs ? __ldg(p.y + k) : 0.0;
         const bool first = (k == kb);
         FJor<D> F;
-        double Q[ns(D)], xm[D], Pm[ns(D)], FP[D * D];
+        double Q[ns(D)], xm[D], Pm[ns(D)];
         if (k == s.start) seg_first(p, s, F, Q);
         else matern_closed<D>(s.lam, s.s2, tk - tprev, F, Q);
         kf_predict_pm<D>(x, P, F, Q, xm, Pm);
@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_filter_apply(con
                 for (int j = 0; j < D; ++j) Sg[i * D + j] = P[si(D, i, j)];
         } else {
             double Sm[D * D], SH[D];
-mul_bt<D>(Sg, F, Sm);
+        mul_bt<D>(Sg, F, Sm);
 #pragma unroll
             for (int i = 0; i < D; ++i) SH[i] = Sm[i * D];          // H = e_0 (Jordan basis)
 #pragma unroll
@@ -220,10 +220,10 @@ mul_bt<D>(Sg, F, Sm);
         // the next step exists and belongs to the same series (a series end would have set sag)
         const double tn = __ldg(p.t + ke);
         FJor<D> F;
-        double Q[ns(D)], xm[D], Pm[ns(D)], FP[D * D], Sm[D * D];
+        double Q[ns(D)], xm[D], Pm[ns(D)], Sm[D * D];
         matern_closed<D>(s.lam, s.s2, tn - tprev, F, Q);
         kf_predict_pm<D>(x, P, F, Q, xm, Pm);
-mul_bt<D>(Sg, F, Sm);
+        mul_bt<D>(Sg, F, Sm);
         if (!chain_smoother_agg<D>(x0, P0, Sm, xm, Pm, sag)) raise_error(p.err, ke, kErrNumeric);
     }
     store_soa(sag, p.chain_s, nch, c);

@@ -521,7 +521,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
             for (int i = 0; i < ns(D); ++i) Pm[i] = p.m.Pinf[i];
         } else {
             FT_t<D, MODE> F;
-            double Q[ns(D)], FP[D * D];
+            double Q[ns(D)];
             disc<D, MODE>(p.m, tk - tprev, F, Q);
             kf_predict_pm<D>(x, P, F, Q, xm, Pm);
         }
@@ -578,7 +578,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
                 const bool obs = ((mwin >> (8 * jj)) & 0xffull) != 0;
                 const double yk = obs ? st[wid].y[buf][jj][lane] : 0.0;
                 FT_t<D, MODE> F;
-                double xm[D], Pm[ns(D)], FP[D * D], Q[ns(D)];
+                double xm[D], Pm[ns(D)], Q[ns(D)];
                 disc<D, MODE>(p.m, tk - tprev, F, Q);
                 kf_predict_pm<D>(x, P, F, Q, xm, Pm);
                 tprev = tk;
@@ -654,7 +654,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
                 const int64_t g1 = p.k0 + ke;
                 const double tn = __ldg(p.t + ke);
                 FT_t<D, MODE> F;
-                double Q[ns(D)], xm[D], Pm[ns(D)], FP[D * D], Sm[D * D];
+                double Q[ns(D)], xm[D], Pm[ns(D)], Sm[D * D];
                 disc<D, MODE>(p.m, tn - tprev, F, Q);
                 kf_predict_pm<D>(x, P, F, Q, xm, Pm);
                 mul_bt<D>(Sg, F, Sm);

@@ -22,6 +22,9 @@ namespace pssgp {
 namespace wide {
 
 constexpr int kWWarps = 4;                       // chains (warps) per CTA in the chain kernels
+#ifndef PSSGP_WMINB
+#define PSSGP_WMINB 1                            // min resident CTAs/SM the wide chain kernels are built for
+#endif
 
 PS_CX int LD(int D) { return D + 1; }            // padded row stride of a shared matrix
 PS_CX int FNW(int D) { return 3 * D * D + 2 * D; } // full filter aggregate: A, b, C, eta, J
@@ -195,6 +198,46 @@ __device__ __forceinline__ void wchol_solve(const double (*Lm)[LD(D)], const dou
         for (int i = 0; i < D; ++i) X[i][lane] = z[i];
     }
     __syncwarp();
+}
+
+// X = S^-1 R for a symmetric positive-definite shared S (D x D) and shared R (D x D) by
+// Gauss-Jordan elimination on [S | R] held in REGISTERS, one row per lane (lanes < D), the
+// pivot row broadcast by warp shuffles: no shared-memory round trips or warp barriers inside
+// the elimination, fully unrolled (compile-time register indices).  No pivoting: S is SPD
+// (pivots are the Schur complements, positive).  Returns false on a non-positive pivot.
+template <int D>
+__device__ __forceinline__ bool wgj_solve(const double (*S)[LD(D)], const double (*R)[LD(D)], double (*X)[LD(D)],
+                                          int lane) {
+    static_assert(D <= 32, "one row per lane");
+    const int r = lane < D ? lane : D - 1;
+    double a[D], b[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) { a[j] = S[r][j]; b[j] = R[r][j]; }
+    bool ok = true;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        const double piv = __shfl_sync(0xffffffffu, a[j], j);
+        ok = ok && (piv > 0.0);
+        const double ip = 1.0 / piv;
+        const double f = (lane == j) ? 0.0 : a[j] * ip;       // multiplier of this lane's row
+        // pivot row (entries right of the pivot, and the RHS), scaled row update
+#pragma unroll
+        for (int k = j + 1; k < D; ++k) {
+            const double pk = __shfl_sync(0xffffffffu, a[k], j);
+            a[k] = (lane == j) ? a[k] * ip : fma(-f, pk, a[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            const double pk = __shfl_sync(0xffffffffu, b[k], j);
+            b[k] = (lane == j) ? b[k] * ip : fma(-f, pk, b[k]);
+        }
+    }
+    if (lane < D) {
+#pragma unroll
+        for (int k = 0; k < D; ++k) X[lane][k] = b[k];
+    }
+    __syncwarp();
+    return ok;
 }
 
 // out = A v (TA: A^T v)
@@ -737,7 +780,7 @@ struct K1Smem {
 };
 
 template <int D>
-__global__ void __launch_bounds__(32 * kWWarps) kw_filter_fold(const WParams p) {
+__global__ void __launch_bounds__(32 * kWWarps, PSSGP_WMINB) kw_filter_fold(const WParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     K1Smem<D>& sh = *reinterpret_cast<K1Smem<D>*>(smem_raw);
     load_model<D>(sh.m, p.model);
@@ -751,10 +794,15 @@ __global__ void __launch_bounds__(32 * kWWarps) kw_filter_fold(const WParams p) 
     const int64_t ke = min(kb + p.K, p.n);
     const SModel<D>& M = sh.m;
     double tprev = (kb < p.n && (kb > 0 || p.k0 > 0)) ? __ldg(p.t + kb - 1) : 0.0;
+    // (t, mask, y) of the next step prefetched one step ahead (global latency off the step)
+    double tn_ = 0.0, yn_ = 0.0;
+    unsigned char mn_ = 0;
+    if (kb < ke) { tn_ = __ldg(p.t + kb); mn_ = __ldg(p.mask + kb); yn_ = __ldg(p.y + kb); }
     for (int64_t k = kb; k < ke; ++k) {
-        const double tk = __ldg(p.t + k);
-        const bool obs = __ldg(p.mask + k) != 0;
-        const double yk = obs ? __ldg(p.y + k) : 0.0;
+        const double tk = tn_;
+        const bool obs = mn_ != 0;
+        const double yk = obs ? yn_ : 0.0;
+        if (k + 1 < ke) { tn_ = __ldg(p.t + k + 1); mn_ = __ldg(p.mask + k + 1); yn_ = __ldg(p.y + k + 1); }
         const int64_t g = p.k0 + k;
         int kind = 0;
         if (g == 0) kind = 3;                                   // F = 0, Q = P_inf
@@ -885,7 +933,7 @@ struct K3Smem {
 };
 
 template <int D>
-__global__ void __launch_bounds__(32 * kWWarps) kw_filter_apply(const WParams p) {
+__global__ void __launch_bounds__(32 * kWWarps, PSSGP_WMINB) kw_filter_apply(const WParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     K3Smem<D>& sh = *reinterpret_cast<K3Smem<D>*>(smem_raw);
     load_model<D>(sh.m, p.model);
@@ -913,10 +961,14 @@ __global__ void __launch_bounds__(32 * kWWarps) kw_filter_apply(const WParams p)
     double quad = 0.0, logs = 0.0;
     int nobs = 0;
     double* xpc = p.xp + static_cast<int64_t>(c) * p.K * CNW(D);
+    double tn_ = 0.0, yn_ = 0.0;                        // next step's inputs, prefetched
+    unsigned char mn_ = 0;
+    if (kb < ke) { tn_ = __ldg(p.t + kb); mn_ = __ldg(p.mask + kb); yn_ = __ldg(p.y + kb); }
     for (int64_t k = kb; k < ke; ++k) {
-        const double tk = __ldg(p.t + k);
-        const bool obs = __ldg(p.mask + k) != 0;
-        const double yk = obs ? __ldg(p.y + k) : 0.0;
+        const double tk = tn_;
+        const bool obs = mn_ != 0;
+        const double yk = obs ? yn_ : 0.0;
+        if (k + 1 < ke) { tn_ = __ldg(p.t + k + 1); mn_ = __ldg(p.mask + k + 1); yn_ = __ldg(p.y + k + 1); }
         const int64_t g = p.k0 + k;
         const int kind = (g == 0) ? 3 : wdisc_kind(tk - tprev, M.udt, p.fq != nullptr);
         const FQp<D> fqp = wfq<D>(p, M, k);
@@ -1079,6 +1131,7 @@ struct K5Smem {
     struct PerWarp {
         double Ps[D][LD(D)];
         double ms[D];
+        double xst[2][CNW(D)];            // staged packed (xbar, P) records (cp.async)
         union {
             struct {                  // carry phase
                 SS<D> a;
@@ -1093,7 +1146,7 @@ struct K5Smem {
 };
 
 template <int D>
-__global__ void __launch_bounds__(32 * kWWarps) kw_smoother_apply(const WParams p) {
+__global__ void __launch_bounds__(32 * kWWarps, PSSGP_WMINB) kw_smoother_apply(const WParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     K5Smem<D>& sh = *reinterpret_cast<K5Smem<D>*>(smem_raw);
     load_model<D>(sh.m, p.model);
@@ -1130,15 +1183,36 @@ __global__ void __launch_bounds__(32 * kWWarps) kw_smoother_apply(const WParams 
     const int64_t ke = min(kb + p.K, p.n);
     const double* xpc = p.xp + static_cast<int64_t>(c) * p.K * CNW(D);
     double tnext = (ke > kb && p.k0 + ke < p.nglob) ? __ldg(p.t + ke) : 0.0;
+    // the packed (xbar, P) record of the next step down is staged by cp.async one step ahead
+    // (double buffer per warp), t one step ahead in a register
+    double tk_next = 0.0;
+    if (ke > kb) {
+        const double* src = xpc + (ke - 1 - kb) * CNW(D);
+        for (int i = lane; i < CNW(D); i += 32) cp_async8(&W.xst[0][i], src + i, 8);
+        cp_async_commit();
+        tk_next = __ldg(p.t + ke - 1);
+    }
+    int sb = 0;
     for (int64_t k = ke - 1; k >= kb; --k) {
-        const double tk = __ldg(p.t + k);
+        const double tk = tk_next;
         const int64_t g = p.k0 + k;
-        const double* src = xpc + (k - kb) * CNW(D);
-        for (int i = lane; i < D; i += 32) W.u.st.x[i] = src[i];
-        for (int e = lane; e < D * D; e += 32) {
-            const int i = e / D, j = e - (e / D) * D;
-            W.u.st.P[i][j] = src[D + si(D, i, j)];
+        cp_async_wait<0>();
+        __syncwarp();
+        if (k > kb) {
+            const double* src = xpc + (k - 1 - kb) * CNW(D);
+            for (int i = lane; i < CNW(D); i += 32) cp_async8(&W.xst[sb ^ 1][i], src + i, 8);
+            cp_async_commit();
+            tk_next = __ldg(p.t + k - 1);
         }
+        {
+            const double* src = W.xst[sb];
+            for (int i = lane; i < D; i += 32) W.u.st.x[i] = src[i];
+            for (int e = lane; e < D * D; e += 32) {
+                const int i = e / D, j = e - (e / D) * D;
+                W.u.st.P[i][j] = src[D + si(D, i, j)];
+            }
+        }
+        sb ^= 1;
         __syncwarp();
         if (g == p.nglob - 1) {
             for (int e = lane; e < D * D; e += 32) W.Ps[e / D][e % D] = W.u.st.P[e / D][e % D];
@@ -1166,8 +1240,12 @@ __global__ void __launch_bounds__(32 * kWWarps) kw_smoother_apply(const WParams 
             }
             __syncwarp();
             // X = Pm^-1 F P (so G = P F^T Pm^-1 = X^T) by Cholesky, lanes over right-hand sides
+#if PSSGP_WIDE_CHOL
             if (!wcholesky<D>(W.u.st.Pm, W.u.st.T, W.u.st.Li, lane) && lane == 0) raise_error(p.err, g, kErrNumeric);
             wchol_solve<D>(W.u.st.T, W.u.st.Li, W.u.st.FP, W.u.st.G, lane);                  // W.u.st.G holds X (not G)
+#else
+            if (!wgj_solve<D>(W.u.st.Pm, W.u.st.FP, W.u.st.G, lane) && lane == 0) raise_error(p.err, g, kErrNumeric);
+#endif
             // ms = x + X^T (ms - xm)
             for (int i = lane; i < D; i += 32) W.u.st.dm[i] = W.ms[i] - W.u.st.xm[i];
             __syncwarp();
@@ -1194,14 +1272,21 @@ __global__ void __launch_bounds__(32 * kWWarps) kw_smoother_apply(const WParams 
             __syncwarp();
         }
         tnext = tk;
+        // projection mean = H m^s, var = H P^s H^T: lane i owns row i, warp sums
+        double mo = 0.0, vo = 0.0;
+        if (lane < D) {
+            double s2 = 0.0;
+#pragma unroll 4
+            for (int j = 0; j < D; ++j) s2 = fma(W.Ps[lane][j], M.H[j], s2);
+            mo = M.H[lane] * W.ms[lane];
+            vo = M.H[lane] * s2;
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            mo += __shfl_xor_sync(0xffffffffu, mo, off);
+            vo += __shfl_xor_sync(0xffffffffu, vo, off);
+        }
         if (lane == 0) {
-            double mo = 0.0, vo = 0.0;
-            for (int i = 0; i < D; ++i) {
-                mo = fma(M.H[i], W.ms[i], mo);
-                double s2 = 0.0;
-                for (int j = 0; j < D; ++j) s2 = fma(W.Ps[i][j], M.H[j], s2);
-                vo = fma(M.H[i], s2, vo);
-            }
             if (p.mean) p.mean[k] = mo;
             if (p.var) p.var[k] = vo;
         }
