@@ -66,12 +66,16 @@ __device__ __forceinline__ void seg_first(const KParams<D>& p, const Seg& s, FJo
 }
 
 // ------------------------------------------------------------------ K1b: fold
+// Inputs staged like K1 (cp.async windows of t, y in a transposed [step][chain] layout,
+// the window's mask bytes as one word); series starts are global-first-like elements.
 template <int D>
 __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_filter_reduce(const KParams<D> p, const BParams q) {
+    __shared__ AsyncStage st[kWarps];
     __shared__ FAgg<D> wagg[kWarps];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t c = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
     const int64_t nch = static_cast<int64_t>(p.nb) * kThreads;
+    const int64_t wbase = (static_cast<int64_t>(blockIdx.x) * kThreads + wid * 32) * p.K;
     const int64_t kb = c * p.K;
     const int64_t ke = min(kb + p.K, p.n);
     FAgg<D> a;
@@ -80,25 +84,41 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_filter_reduce(co
     Seg s;
     if (kb < ke) seg_load(s, p, q, seg_find(q, kb));
     double tprev = (kb > 0 && kb < ke) ? __ldg(p.t + kb - 1) : 0.0;
+    int ferr = -1;
+    const int64_t nwin = (p.K + kWinA - 1) / kWinA;
+    issue_window(st[wid], 0, p.t, p.y, wbase, p.K, p.n, 0, lane);
+    unsigned long long mnext = mask_word(p.mask, kb, ke);
+    for (int64_t w = 0; w < nwin; ++w) {
+        const int64_t j0 = w * kWinA;
+        const int buf = static_cast<int>(w & 1);
+        if (w + 1 < nwin) issue_window(st[wid], buf ^ 1, p.t, p.y, wbase, p.K, p.n, j0 + kWinA, lane);
+        else cp_async_commit();
+        const unsigned long long mwin = mnext;
+        mnext = mask_word(p.mask, kb + j0 + kWinA, ke);
+        cp_async_wait<1>();
+        __syncwarp();
+        const int jend = static_cast<int>(min(static_cast<int64_t>(kWinA), ke - (kb + j0)));
 #pragma unroll 1
-    for (int64_t k = kb; k < ke; ++k) {
-        while (k >= s.end) seg_load(s, p, q, s.b + 1);
-        const double tk = __ldg(p.t + k);
-        const bool obs = __ldg(p.mask + k) != 0;
-        const double yk = obs ? __ldg(p.y + k) : 0.0;
-        FJor<D> F;
-        double Q[ns(D)];
-        if (k == s.start) {
-            seg_first(p, s, F, Q);
-        } else {
-            if (!(tk - tprev >= 0.0)) raise_error(p.err, k, kErrInput);
-            matern_closed<D>(s.lam, s.s2, tk - tprev, F, Q);
+        for (int jj = 0; jj < jend; ++jj) {
+            const int64_t k = kb + j0 + jj;
+            while (k >= s.end) seg_load(s, p, q, s.b + 1);
+            const double tk = st[wid].t[buf][jj][lane];
+            const bool obs = ((mwin >> (8 * jj)) & 0xffull) != 0;
+            const double yk = obs ? st[wid].y[buf][jj][lane] : 0.0;
+            FJor<D> F;
+            double Q[ns(D)];
+            const bool start = (k == s.start);
+            if (start) seg_first(p, s, F, Q);
+            else matern_closed<D>(s.lam, s.s2, tk - tprev, F, Q);
+            const bool bad = (!start && !(tk - tprev >= 0.0)) || !isfinite(tk) || (obs && !isfinite(yk));
+            ferr = (bad && ferr < 0) ? static_cast<int>(k - kb) : ferr;
+            mp.r = s.r;
+            fold_step<D, true>(a, F, Q, mp, obs, yk);
+            tprev = tk;
         }
-        if (!isfinite(tk) || (obs && !isfinite(yk))) raise_error(p.err, k, kErrInput);
-        mp.r = s.r;
-        fold_step<D, true>(a, F, Q, mp, obs, yk);
-        tprev = tk;
+        __syncwarp();
     }
+    if (ferr >= 0) raise_error(p.err, kb + ferr, kErrInput);
     store_soa(a, p.chain_f, nch, c);
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
@@ -124,8 +144,12 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_filter_reduce(co
 }
 
 // ------------------------------------------------------------------ K3b: Kalman rescan
+// Staged inputs as in K3; the per-step NLL terms go through a transposed shared tile and
+// leave in coalesced stores once per window.
 template <int D>
 __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_filter_apply(const KParams<D> p, const BParams q) {
+    __shared__ AsyncStage st[kWarps];
+    __shared__ double nst[kWarps][kWinA][33];
     __shared__ FAgg<D> tot[kWarps];
     __shared__ Gauss<D> wcar[kWarps];
     __shared__ SAgg<D> stot[kWarps];
@@ -133,6 +157,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_filter_apply(con
     const int64_t c = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
     const int64_t nch = static_cast<int64_t>(p.nb) * kThreads;
     const int64_t wg = static_cast<int64_t>(blockIdx.x) * kWarps + wid;
+    const int64_t wbase = wg * 32 * p.K;
     const int64_t kb = c * p.K;
     const int64_t ke = min(kb + p.K, p.n);
     const Gauss<D> cur = filter_chain_carry<D>(p, tot, wcar, c, nch, lane, wid);
@@ -148,74 +173,105 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_filter_apply(con
     SAgg<D> sag;
     set_identity(sag);
     bool sag_done = false;
+    int ferr = -1;
+    const int64_t nwin = (p.K + kWinA - 1) / kWinA;
+    issue_window(st[wid], 0, p.t, p.y, wbase, p.K, p.n, 0, lane);
+    unsigned long long mnext = mask_word(p.mask, kb, ke);
+    for (int64_t w = 0; w < nwin; ++w) {
+        const int64_t j0 = w * kWinA;
+        const int buf = static_cast<int>(w & 1);
+        if (w + 1 < nwin) issue_window(st[wid], buf ^ 1, p.t, p.y, wbase, p.K, p.n, j0 + kWinA, lane);
+        else cp_async_commit();
+        const unsigned long long mwin = mnext;
+        mnext = mask_word(p.mask, kb + j0 + kWinA, ke);
+        cp_async_wait<1>();
+        __syncwarp();
+        const int jend = static_cast<int>(min(static_cast<int64_t>(kWinA), ke - (kb + j0)));
 #pragma unroll 1
-    for (int64_t k = kb; k < ke; ++k) {
-        while (k >= s.end) seg_load(s, p, q, s.b + 1);
-        const double tk = __ldg(p.t + k);
-        const bool obs = __ldg(p.mask + k) != 0;
-        const double yk = obs ? __ldg(p.y + k) : 0.0;
-        const bool first = (k == kb);
-        FJor<D> F;
-        double Q[ns(D)], xm[D], Pm[ns(D)];
-        if (k == s.start) seg_first(p, s, F, Q);
-        else matern_closed<D>(s.lam, s.s2, tk - tprev, F, Q);
-        kf_predict_pm<D>(x, P, F, Q, xm, Pm);
-        tprev = tk;
-        mp.r = s.r;
-        double HP[D], S, hx;
-        obs_terms<D>(mp, xm, Pm, HP, S, hx, true);
-        if (obs && !(S > 0.0 && S < INFINITY)) raise_error(p.err, k, kErrNumeric);
-        const double iS = obs ? rcp(S) : 0.0;
-        const double v = obs ? (yk - hx) : 0.0;
-        const double vs = v * iS;
+        for (int jj = 0; jj < jend; ++jj) {
+            const int64_t k = kb + j0 + jj;
+            while (k >= s.end) seg_load(s, p, q, s.b + 1);
+            const double tk = st[wid].t[buf][jj][lane];
+            const bool obs = ((mwin >> (8 * jj)) & 0xffull) != 0;
+            const double yk = obs ? st[wid].y[buf][jj][lane] : 0.0;
+            const bool first = (k == kb);
+            FJor<D> F;
+            double Q[ns(D)], xm[D], Pm[ns(D)];
+            if (k == s.start) seg_first(p, s, F, Q);
+            else matern_closed<D>(s.lam, s.s2, tk - tprev, F, Q);
+            kf_predict_pm<D>(x, P, F, Q, xm, Pm);
+            tprev = tk;
+            mp.r = s.r;
+            double HP[D], S, hx;
+            obs_terms<D>(mp, xm, Pm, HP, S, hx, true);
+            const bool bad = obs && !(S > 0.0 && S < INFINITY);
+            ferr = (bad && ferr < 0) ? static_cast<int>(k - kb) : ferr;
+            const double iS = obs ? rcp(S) : 0.0;
+            const double v = obs ? (yk - hx) : 0.0;
+            const double vs = v * iS;
 #pragma unroll
-        for (int i = 0; i < D; ++i) x[i] = fma(HP[i], vs, xm[i]);
-#pragma unroll
-        for (int i = 0; i < D; ++i)
-#pragma unroll
-            for (int j = i; j < D; ++j) P[si(D, i, j)] = fma(-HP[i] * iS, HP[j], Pm[si(D, i, j)]);
-        if (first) {
-#pragma unroll
-            for (int i = 0; i < D; ++i) x0[i] = x[i];
-#pragma unroll
-            for (int i = 0; i < ns(D); ++i) P0[i] = P[i];
+            for (int i = 0; i < D; ++i) x[i] = fma(HP[i], vs, xm[i]);
 #pragma unroll
             for (int i = 0; i < D; ++i)
 #pragma unroll
-                for (int j = 0; j < D; ++j) Sg[i * D + j] = P[si(D, i, j)];
-        } else {
-            double Sm[D * D], SH[D];
-        mul_bt<D>(Sg, F, Sm);
+                for (int j = i; j < D; ++j) P[si(D, i, j)] = fma(-HP[i] * iS, HP[j], Pm[si(D, i, j)]);
+            if (first) {
 #pragma unroll
-            for (int i = 0; i < D; ++i) SH[i] = Sm[i * D];          // H = e_0 (Jordan basis)
+                for (int i = 0; i < D; ++i) x0[i] = x[i];
 #pragma unroll
-            for (int i = 0; i < D; ++i) {
-                const double si_ = SH[i] * iS;
+                for (int i = 0; i < ns(D); ++i) P0[i] = P[i];
 #pragma unroll
-                for (int j = 0; j < D; ++j) Sg[i * D + j] = fma(-si_, HP[j], Sm[i * D + j]);
-                x0[i] = fma(SH[i], vs, x0[i]);
+                for (int i = 0; i < D; ++i)
 #pragma unroll
-                for (int j = i; j < D; ++j) P0[si(D, i, j)] = fma(-si_, SH[j], P0[si(D, i, j)]);
+                    for (int j = 0; j < D; ++j) Sg[i * D + j] = P[si(D, i, j)];
+            } else {
+                double Sm[D * D], SH[D];
+                mul_bt<D>(Sg, F, Sm);
+#pragma unroll
+                for (int i = 0; i < D; ++i) SH[i] = Sm[i * D];          // H = e_0 (Jordan basis)
+#pragma unroll
+                for (int i = 0; i < D; ++i) {
+                    const double si_ = SH[i] * iS;
+#pragma unroll
+                    for (int j = 0; j < D; ++j) Sg[i * D + j] = fma(-si_, HP[j], Sm[i * D + j]);
+                    x0[i] = fma(SH[i], vs, x0[i]);
+#pragma unroll
+                    for (int j = i; j < D; ++j) P0[si(D, i, j)] = fma(-si_, SH[j], P0[si(D, i, j)]);
+                }
+            }
+            nst[wid][jj][lane] = obs ? 0.5 * (log(S) + 1.8378770664093453 + v * vs) : 0.0;
+            if (k == s.end - 1 && !sag_done) {
+                // first series end in this chain: the chain's smoother aggregate is the collapsed
+                // (0, m^s_k0, P^s_k0) of that series (terminal element)
+#pragma unroll
+                for (int i = 0; i < D * D; ++i) sag.E[i] = 0.0;
+#pragma unroll
+                for (int i = 0; i < D; ++i) sag.g[i] = x0[i];
+#pragma unroll
+                for (int i = 0; i < ns(D); ++i) sag.L[i] = P0[i];
+                sag_done = true;
+            }
+            double* o = p.xp + ((wg * p.K + (k - kb)) * CN(D)) * 32 + lane;
+#pragma unroll
+            for (int i = 0; i < D; ++i) o[i * 32] = x[i];
+#pragma unroll
+            for (int i = 0; i < ns(D); ++i) o[(D + i) * 32] = P[i];
+        }
+        __syncwarp();
+        {   // coalesced flush of the window's NLL terms (row r = chain wbase/K + r)
+            const int col = lane & (kWinA - 1), rb = lane / kWinA;
+            const int64_t j = j0 + col;
+#pragma unroll
+            for (int i = 0; i < 32 / (32 / kWinA); ++i) {
+                const int r = rb + (32 / kWinA) * i;
+                const int64_t idx = wbase + r * p.K + j;
+                const int64_t rend = min(wbase + (r + 1) * p.K, p.n);
+                if (j < p.K && idx < rend) q.nll_step[idx] = nst[wid][col][r];
             }
         }
-        q.nll_step[k] = obs ? 0.5 * (log(S) + 1.8378770664093453 + v * vs) : 0.0;
-        if (k == s.end - 1 && !sag_done) {
-            // first series end in this chain: the chain's smoother aggregate is the collapsed
-            // (0, m^s_k0, P^s_k0) of that series (terminal element)
-#pragma unroll
-            for (int i = 0; i < D * D; ++i) sag.E[i] = 0.0;
-#pragma unroll
-            for (int i = 0; i < D; ++i) sag.g[i] = x0[i];
-#pragma unroll
-            for (int i = 0; i < ns(D); ++i) sag.L[i] = P0[i];
-            sag_done = true;
-        }
-        double* o = p.xp + ((wg * p.K + (k - kb)) * CN(D)) * 32 + lane;
-#pragma unroll
-        for (int i = 0; i < D; ++i) o[i * 32] = x[i];
-#pragma unroll
-        for (int i = 0; i < ns(D); ++i) o[(D + i) * 32] = P[i];
+        __syncwarp();
     }
+    if (ferr >= 0) raise_error(p.err, kb + ferr, kErrNumeric);
     if (ke > kb && !sag_done) {
         // the next step exists and belongs to the same series (a series end would have set sag)
         const double tn = __ldg(p.t + ke);
@@ -251,14 +307,18 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_filter_apply(con
 }
 
 // ------------------------------------------------------------------ K5b: RTS rescan
+// t staged in windows and mean/var leaving through a transposed tile (coalesced), the
+// filtered record of the next step down prefetched one step ahead, as in K5.
 template <int D>
 __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_smoother_apply(const KParams<D> p, const BParams q) {
+    __shared__ StageOut so[kWarps];
     __shared__ SAgg<D> tot[kWarps];
     __shared__ Gauss<D> wcar[kWarps + 1];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t c = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
     const int64_t nch = static_cast<int64_t>(p.nb) * kThreads;
     const int64_t wg = static_cast<int64_t>(blockIdx.x) * kWarps + wid;
+    const int64_t wbase = wg * 32 * p.K;
     const int64_t kb = c * p.K;
     const int64_t ke = min(kb + p.K, p.n);
     const Gauss<D> cur = smoother_chain_carry<D>(p, tot, wcar, c, nch, lane, wid);
@@ -267,36 +327,77 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_smoother_apply(c
     for (int i = 0; i < D; ++i) ms[i] = cur.x[i];
 #pragma unroll
     for (int i = 0; i < ns(D); ++i) Ps[i] = cur.P[i];
-    if (ke <= kb) return;
     Seg s;
-    seg_load(s, p, q, seg_find(q, ke - 1));
-    double tnext = (ke < p.n) ? __ldg(p.t + ke) : 0.0;
-#pragma unroll 1
-    for (int64_t k = ke - 1; k >= kb; --k) {
-        while (k < s.start) seg_load(s, p, q, s.b - 1);
-        const double tk = __ldg(p.t + k);
-        const double* src = p.xp + ((wg * p.K + (k - kb)) * CN(D)) * 32 + lane;
-        double x[D], P[ns(D)];
+    if (kb < ke) seg_load(s, p, q, seg_find(q, ke - 1));
+    double tnext = (kb < ke && ke < p.n) ? __ldg(p.t + ke) : 0.0;
+    const double* xpw = p.xp + (wg * p.K * CN(D)) * 32 + lane;
+    double nx[CN(D)];
+    if (kb < ke) {
+        const double* s1 = xpw + ((ke - 1 - kb) * CN(D)) * 32;
 #pragma unroll
-        for (int i = 0; i < D; ++i) x[i] = src[i * 32];
-#pragma unroll
-        for (int i = 0; i < ns(D); ++i) P[i] = src[(D + i) * 32];
-        if (k == s.end - 1) {
-#pragma unroll
-            for (int i = 0; i < D; ++i) ms[i] = x[i];
-#pragma unroll
-            for (int i = 0; i < ns(D); ++i) Ps[i] = P[i];
-        } else {
-            FJor<D> F;
-        double Q[ns(D)], xm[D], Pm[ns(D)], FP[D * D];
-            matern_closed<D>(s.lam, s.s2, tnext - tk, F, Q);
-            kf_predict<D>(x, P, F, Q, xm, FP, Pm);
-            if (!rts_step<D>(x, P, xm, Pm, FP, ms, Ps)) raise_error(p.err, k, kErrNumeric);
-        }
-        tnext = tk;
-        if (p.mean) p.mean[k] = ms[0];
-        if (p.var) p.var[k] = Ps[0];
+        for (int i = 0; i < CN(D); ++i) nx[i] = s1[i * 32];
     }
+    int ferr = -1;
+    const int64_t nwin = (p.K + kWinA - 1) / kWinA;
+    issue_copies<false>(so[wid].t[(nwin - 1) & 1], nullptr, p.t, nullptr, wbase, p.K, p.n, (nwin - 1) * kWinA, lane);
+    for (int64_t w = nwin - 1; w >= 0; --w) {
+        const int64_t j0 = w * kWinA;
+        const int buf = static_cast<int>(w & 1);
+        if (w > 0) issue_copies<false>(so[wid].t[buf ^ 1], nullptr, p.t, nullptr, wbase, p.K, p.n, j0 - kWinA, lane);
+        else cp_async_commit();
+        cp_async_wait<1>();
+        __syncwarp();
+        const int jstart = static_cast<int>(min(static_cast<int64_t>(kWinA - 1), ke - 1 - (kb + j0)));
+#pragma unroll 1
+        for (int jj = jstart; jj >= 0; --jj) {
+            const int64_t k = kb + j0 + jj;
+            while (k < s.start) seg_load(s, p, q, s.b - 1);
+            const double tk = so[wid].t[buf][jj][lane];
+            double x[D], P[ns(D)];
+#pragma unroll
+            for (int i = 0; i < D; ++i) x[i] = nx[i];
+#pragma unroll
+            for (int i = 0; i < ns(D); ++i) P[i] = nx[D + i];
+            if (k > kb) {
+                const double* src = xpw + ((k - 1 - kb) * CN(D)) * 32;
+#pragma unroll
+                for (int i = 0; i < CN(D); ++i) nx[i] = src[i * 32];
+            }
+            if (k == s.end - 1) {   // series end: terminal element
+#pragma unroll
+                for (int i = 0; i < D; ++i) ms[i] = x[i];
+#pragma unroll
+                for (int i = 0; i < ns(D); ++i) Ps[i] = P[i];
+            } else {
+                FJor<D> F;
+                double Q[ns(D)], xm[D], Pm[ns(D)], FP[D * D];
+                matern_closed<D>(s.lam, s.s2, tnext - tk, F, Q);
+                kf_predict<D>(x, P, F, Q, xm, FP, Pm);
+                const bool bad = !rts_step<D>(x, P, xm, Pm, FP, ms, Ps);
+                ferr = bad ? static_cast<int>(k - kb) : ferr;   // backward: last hit = first index
+            }
+            tnext = tk;
+            so[wid].m[jj][lane] = ms[0];
+            so[wid].v[jj][lane] = Ps[0];
+        }
+        __syncwarp();
+        {
+            const int col = lane & (kWinA - 1), rb = lane / kWinA;
+            const int64_t j = j0 + col;
+#pragma unroll
+            for (int i = 0; i < 32 / (32 / kWinA); ++i) {
+                const int r = rb + (32 / kWinA) * i;
+                const int64_t idx = wbase + r * p.K + j;
+                const int64_t rend = min(wbase + (r + 1) * p.K, p.n);
+                if (j < p.K && idx < rend) {
+                    if (p.mean) p.mean[idx] = so[wid].m[col][r];
+                    if (p.var) p.var[idx] = so[wid].v[col][r];
+                }
+            }
+        }
+        __syncwarp();
+    }
+    if (ferr >= 0) raise_error(p.err, kb + ferr, kErrNumeric);
 }
 
 // ------------------------------------------------------------------ per-series NLL (1 warp per series)
