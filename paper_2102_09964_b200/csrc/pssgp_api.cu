@@ -862,14 +862,15 @@ pssgp_status pssgp_predict(pssgp_model* m, int64_t n_train, const double* t_trai
                            int64_t n_test, const double* t_test, double* mean_test, double* var_test, double* nll,
                            void* stream) {
     if (!m) return PSSGP_E_ARG;
+    if (n_train < 0 || n_test < 0) return fail(m, PSSGP_E_ARG, "negative size");
+    if ((n_train > 0 && (!t_train || !y_train)) || (n_test > 0 && (!t_test || !mean_test || !var_test)))
+        return fail(m, PSSGP_E_ARG, "NULL input/output array");
     pssgp_status st = ensure_device(m);
     if (st) return st;
     const size_t tot = static_cast<size_t>(n_train + n_test);
     const size_t need = tot * (8 + 8 + 8 + 8 + 1) + static_cast<size_t>(n_test) * 8 + 64;
     if (need > m->mg_bytes) {
         if (m->mg) cudaFree(m->mg);
-    if (m->bt) cudaFree(m->bt);
-    if (m->fq) cudaFree(m->fq);
         m->mg = nullptr;
         m->mg_bytes = 0;
         if (cudaMalloc(&m->mg, need) != cudaSuccess) {
@@ -903,7 +904,6 @@ pssgp_status pssgp_posterior_batched(pssgp_model* m, int nseg, const int64_t* of
     const size_t need = static_cast<size_t>(std::max<int64_t>(N, 1)) * sizeof(double);
     if (need > m->bt_bytes) {
         if (m->bt) cudaFree(m->bt);
-    if (m->fq) cudaFree(m->fq);
         m->bt = nullptr;
         m->bt_bytes = 0;
         if (cudaMalloc(&m->bt, need) != cudaSuccess) {

@@ -392,3 +392,34 @@ def test_irregular_pade_fine_grids(cuda_device, name, dt_scale):
     comps = PADE_MODELS[name]
     w = _irregular(comps, 0.01, 20011, seed=7, dt_scale=dt_scale)
     assert_parity(w)
+
+
+def test_handle_reuse_across_entry_points(cuda_device):
+    """One handle through predict / batched / posterior with growing sizes (each grows its own
+    handle-owned buffer) gives the same results as fresh handles, and destroys cleanly."""
+    rng = np.random.default_rng(3)
+    comps = [synth.Component("matern52", 1.0, 0.5)]
+    m = P.Model(comps, 0.01)
+    for n_tr, n_te in [(500, 50), (3000, 700)]:
+        t_tr = np.sort(rng.uniform(0, 4, n_tr)); y_tr = synth.sinusoid(t_tr) + 0.1 * rng.standard_normal(n_tr)
+        t_te = np.sort(rng.uniform(0, 4, n_te))
+        d = lambda a: torch.from_numpy(a).cuda()
+        mt, vt, nll = m.predict(d(t_tr), d(y_tr), d(t_te))
+        fresh = P.Model(comps, 0.01)
+        mt2, vt2, nll2 = fresh.predict(d(t_tr), d(y_tr), d(t_te))
+        assert torch.equal(mt, mt2) and torch.equal(vt, vt2) and torch.equal(nll, nll2)
+        B = 3
+        off = torch.tensor([0, n_tr // 3, 2 * n_tr // 3, n_tr], dtype=torch.int64, device="cuda:0")
+        mask = torch.ones(n_tr, dtype=torch.uint8, device="cuda:0")
+        mean = torch.empty(n_tr, dtype=torch.float64, device="cuda:0"); var = torch.empty_like(mean)
+        nllb = torch.empty(B, dtype=torch.float64, device="cuda:0")
+        P.pssgp_posterior_batched(m.h, B, off, None, None, None, n_tr, d(t_tr), d(y_tr), mask, mean, var, nllb)
+        m.check()
+        w = synth.Workload("reuse", comps, 0.01, t_tr, y_tr, np.ones(n_tr, np.uint8))
+        g = m.posterior(d(w.t), d(w.y), d(w.mask))
+        m.check()
+        o = oracle.posterior(w)
+        em, ev, en = errors((g[0].cpu().numpy(), g[1].cpu().numpy(), float(g[2].cpu()[0])), o)
+        assert em <= MEAN_TOL and ev <= VAR_TOL and en <= NLL_TOL
+        fresh.close()
+    m.close()

@@ -168,3 +168,22 @@ def test_pade_discretisation_vs_oracle(comps, dt):
             assert np.max(np.abs(Q - Qo)[big] / np.abs(Qo)[big]) <= 1e-10
     if dt == 0.0:
         assert np.array_equal(F, np.eye(m.state_dim)) and np.all(Q == 0.0)
+
+
+def test_host_side_argument_errors():
+    """Argument validation happens on the host, before any device work (no GPU needed)."""
+    m = P.Model([synth.Component("matern52", 1.0, 0.5)], 0.1)
+    lib = _native.lib()
+    one = np.zeros(4)
+    ptr = one.ctypes.data
+    assert lib.pssgp_nll_grad(m.h, 4, ptr, ptr, ptr, ptr, None, None) == _native.PSSGP_E_ARG     # grad NULL
+    assert lib.pssgp_nll_grad(m.h, -1, ptr, ptr, ptr, ptr, ptr, None) == _native.PSSGP_E_ARG     # N < 0
+    assert lib.pssgp_predict(m.h, -1, ptr, ptr, 1, ptr, ptr, ptr, ptr, None) == _native.PSSGP_E_ARG
+    assert lib.pssgp_predict(m.h, 4, None, ptr, 1, ptr, ptr, ptr, ptr, None) == _native.PSSGP_E_ARG
+    assert lib.pssgp_posterior_batched(m.h, 0, ptr, None, None, None, 4, ptr, ptr, ptr, ptr, ptr, ptr,
+                                       None) == _native.PSSGP_E_ARG                                # nseg < 1
+    r = P.Model([synth.Component("rbf", 1.0, 0.5, order=3)], 0.1, uniform_dt=0.01)
+    assert lib.pssgp_nll_grad(r.h, 4, ptr, ptr, ptr, ptr, ptr, None) == _native.PSSGP_E_UNSUPPORTED
+    assert lib.pssgp_posterior_batched(r.h, 1, ptr, None, None, None, 4, ptr, ptr, ptr, ptr, ptr, ptr,
+                                       None) == _native.PSSGP_E_UNSUPPORTED
+    assert P.pssgp_last_error(r.h) != ""
