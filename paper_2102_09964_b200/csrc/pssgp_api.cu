@@ -921,6 +921,8 @@ pssgp_status pssgp_posterior_batched(pssgp_model* m, int nseg, const int64_t* of
     q.sqrt2nu = std::sqrt(2.0 * m->d - 1.0);
     q.nll_step = m->bt;
     q.nll_seg = nll;
+    pssgp::batch::k_batch_check_offsets<<<(nseg + 256) / 256, 256, 0, s>>>(offsets, nseg, N, m->d_err);
+    LAUNCH_CHECK(m, "k_batch_check_offsets");
     if (N > 0) {
         switch (m->d) {
 #define BATCH_RUN(DD)                                                                                   \
@@ -966,7 +968,8 @@ pssgp_status pssgp_check(pssgp_model* m) {
     const int64_t idx = static_cast<int64_t>((w >> 8) & 0xffffffffffffULL);
     const char* what = code == kErrInput ? "invalid input (unsorted/non-finite t or non-finite observed y)"
                        : code == kErrNumeric ? "numerical failure (S <= 0 or non-PD predicted covariance)"
-                                             : "no device discretisation for this dt (set uniform_dt)";
+                                             : "dt differs from the declared uniform_dt (use uniform_dt = 0 for "
+                                               "per-step device discretisation)";
     return fail(m, static_cast<pssgp_status>(code), std::string(what) + " at step " + std::to_string(idx), idx);
 }
 

@@ -38,9 +38,13 @@ struct Seg {
 
 template <int D>
 __device__ __forceinline__ void seg_load(Seg& s, const KParams<D>& p, const BParams& q, int b) {
+    // out-of-range series (invalid offsets, reported by k_batch_check_offsets) degrade to an
+    // empty/unbounded segment so the step loops always terminate
+    const bool over = b > q.nseg - 1, under = b < 0;
+    b = max(0, min(b, q.nseg - 1));
     s.b = b;
-    s.start = __ldg(q.off + b);
-    s.end = __ldg(q.off + b + 1);
+    s.start = under ? INT64_MIN : __ldg(q.off + b);
+    s.end = over ? INT64_MAX : __ldg(q.off + b + 1);
     s.s2 = q.var ? __ldg(q.var + b) : p.m.s2;
     s.lam = q.ell ? q.sqrt2nu / __ldg(q.ell + b) : p.m.lam;
     s.r = q.noise ? __ldg(q.noise + b) : p.m.r;
@@ -398,6 +402,19 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_smoother_apply(c
         __syncwarp();
     }
     if (ferr >= 0) raise_error(p.err, kb + ferr, kErrNumeric);
+}
+
+// ------------------------------------------------------------------ offsets validation
+// off[0] = 0, off[nseg] = N, non-decreasing; the first violation is reported as an input
+// error at the offending series index.
+__global__ void __launch_bounds__(256) k_batch_check_offsets(const int64_t* __restrict__ off, int nseg, int64_t N,
+                                                             unsigned long long* err) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b > nseg) return;
+    const int64_t o = __ldg(off + b);
+    bool bad = (b == 0 && o != 0) || (b == nseg && o != N) || o < 0 || o > N;
+    if (b > 0) bad = bad || (__ldg(off + b - 1) > o);
+    if (bad) raise_error(err, b, kErrInput);
 }
 
 // ------------------------------------------------------------------ per-series NLL (1 warp per series)

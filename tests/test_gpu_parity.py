@@ -423,3 +423,20 @@ def test_handle_reuse_across_entry_points(cuda_device):
         assert em <= MEAN_TOL and ev <= VAR_TOL and en <= NLL_TOL
         fresh.close()
     m.close()
+
+
+def test_batched_invalid_offsets(cuda_device):
+    """Offsets that do not partition [0, N) are reported (PSSGP_E_INPUT) instead of hanging."""
+    m = P.Model([synth.Component("matern32", 1.0, 0.5)], 0.01)
+    n = 1000
+    t = torch.linspace(0, 1, n, dtype=torch.float64, device="cuda:0")
+    y = torch.zeros(n, dtype=torch.float64, device="cuda:0")
+    mk = torch.ones(n, dtype=torch.uint8, device="cuda:0")
+    mean = torch.empty_like(t); var = torch.empty_like(t)
+    nll = torch.empty(2, dtype=torch.float64, device="cuda:0")
+    for bad in ([0, 600, 900], [0, 700, 300], [5, 500, n]):
+        off = torch.tensor(bad, dtype=torch.int64, device="cuda:0")
+        P.pssgp_posterior_batched(m.h, 2, off, None, None, None, n, t, y, mk, mean, var, nll)
+        with pytest.raises(P.PssgpError) as e:
+            m.check()
+        assert e.value.status == _native.PSSGP_E_INPUT
