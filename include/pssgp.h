@@ -202,10 +202,12 @@ const char* pssgp_last_error(const pssgp_model* m);
 pssgp_status pssgp_get_ssm(const pssgp_model* m, double* G, double* W, double* H,
                            double* Pinf, double* D);
 
-/* The (F, Q) the device code uses for a step of length dt, evaluated on the
- * host by the same __host__ __device__ function the kernels call (closed form
- * for Matern, the precomputed pair for dt == uniform_dt).  F, Q: d*d row-major.
- * Test/introspection only; returns PSSGP_E_UNSUPPORTED where the device would. */
+/* The (F, Q) the device code uses for a step of length dt.  d <= 3: evaluated on
+ * the host by the same __host__ __device__ function the kernels call (closed form
+ * for Matern, the precomputed pair for dt == uniform_dt, the scaled-step series for
+ * uniform_dt = 0).  d > 3 with uniform_dt = 0: ONE step of the device kernel
+ * kw_discretize (needs a GPU).  F, Q: d*d row-major.  Test/introspection only;
+ * returns PSSGP_E_UNSUPPORTED where the device would. */
 pssgp_status pssgp_debug_discretize(const pssgp_model* m, double dt, double* F, double* Q);
 
 /* Launch plan for N steps: steps per chain, number of chains, CTAs, threads/CTA. */

@@ -518,6 +518,36 @@ pssgp_status wide_prepare(pssgp_model* m, pssgp::wide::WParams& p, cudaStream_t 
     return PSSGP_OK;
 }
 
+// One step of kw_discretize on the device (pssgp_debug_discretize for kPade wide models).
+template <int D>
+pssgp_status wide_debug_discretize(pssgp_model* m, double dt, double* F, double* Q) {
+    using namespace pssgp::wide;
+    pssgp_status st = ensure_device(m);
+    if (st) return st;
+    WParams p;
+    if ((st = wide_setup<D>(m, make_wplan<D>(m, 2), p))) return st;
+    double* tbuf = nullptr;
+    if (cudaMalloc(&tbuf, 2 * sizeof(double) + 2 * FQW(D) * sizeof(double)) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(m, PSSGP_E_NOMEM, "cudaMalloc(debug discretize)");
+    }
+    double* fq = tbuf + 2;
+    const double th[2] = {0.0, dt};
+    cudaMemcpy(tbuf, th, sizeof(th), cudaMemcpyHostToDevice);
+    cudaFuncSetAttribute(kw_discretize<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(KDSmem<D>));
+    kw_discretize<D><<<1, 32 * kWWarps, sizeof(KDSmem<D>)>>>(tbuf, 2, 0, m->d_model, fq, m->d_err);
+    std::vector<double> h(FQW(D));
+    cudaError_t e = cudaMemcpy(h.data(), fq + FQW(D), FQW(D) * sizeof(double), cudaMemcpyDeviceToHost);
+    cudaFree(tbuf);
+    if (e != cudaSuccess) return cuda_fail(m, e, "debug discretize");
+    for (int i = 0; i < D; ++i)
+        for (int j = 0; j < D; ++j) {
+            F[i * D + j] = h[i * LD(D) + j];
+            Q[i * D + j] = h[(D + i) * LD(D) + j];
+        }
+    return PSSGP_OK;
+}
+
 // Kogge-Stone levels with ping-pong buffers; returns the buffer holding the inclusive scan
 template <int D>
 double* wide_scan_f(pssgp_model* m, pssgp::wide::WParams& p, cudaStream_t s, pssgp_status& st) {
@@ -1035,6 +1065,15 @@ pssgp_status pssgp_get_ssm(const pssgp_model* m, double* G, double* W, double* H
 pssgp_status pssgp_debug_discretize(const pssgp_model* m, double dt, double* F, double* Q) {
     if (!m || !F || !Q) return PSSGP_E_ARG;
     pssgp_model* mm = const_cast<pssgp_model*>(m);
+    if (m->d > kMaxD && m->mode == kPade && dt != 0.0) {
+        // per-step device discretisation (kw_discretize): run it on the device for one step
+        switch (m->d) {
+#define X(DD) case DD: return wide_debug_discretize<DD>(mm, dt, F, Q);
+            PSSGP_WIDE_DIMS(X)
+#undef X
+            default: return fail(mm, PSSGP_E_UNSUPPORTED, "state dimension not compiled");
+        }
+    }
     if (m->d > kMaxD) {   // mirrors wide::wdisc_kind
         const int d = m->d;
         const bool tab = (m->udt > 0.0 && std::fabs(dt - m->udt) <= 1e-12 * m->udt), zero = (dt == 0.0);

@@ -440,3 +440,40 @@ def test_batched_invalid_offsets(cuda_device):
         with pytest.raises(P.PssgpError) as e:
             m.check()
         assert e.value.status == _native.PSSGP_E_INPUT
+
+
+def _mp_van_loan(G, W, dt, dps=40):
+    """F, Q at 40 digits (mpmath expm of the Van Loan block matrix) — an independent
+    high-precision reference (the fp64 oracle's expm itself carries ~1e-11 error for the
+    non-normal balanced RBF-6 drift at dt ~ 0.3)."""
+    import mpmath as mp
+    mp.mp.dps = dps
+    d = G.shape[0]
+    C = mp.zeros(2 * d, 2 * d)
+    for i in range(d):
+        for j in range(d):
+            C[i, j] = mp.mpf(G[i, j]) * dt
+            C[i, d + j] = mp.mpf(W[i, j]) * dt
+            C[d + i, d + j] = -mp.mpf(G[j, i]) * dt
+    E = mp.expm(C)
+    F = E[0:d, 0:d]
+    Q = E[0:d, d:2 * d] * F.T
+    return np.array(F.tolist(), dtype=float), np.array(Q.tolist(), dtype=float)
+
+
+@pytest.mark.parametrize("name", ["rbf6", "quasi1", "per3+m32"])
+@pytest.mark.parametrize("dt", [1e-9, 2.4e-7, 1.22e-4, 1e-3, 0.02, 0.3, 2.5])
+def test_kw_discretize_vs_high_precision(cuda_device, name, dt):
+    """kw_discretize (d > 3, uniform_dt = 0) for one step against a 40-digit Van Loan: F and Q
+    to ~1e-13 of their scale and, for small steps, every entry of Q above the rounding level of
+    the matrix to relative accuracy (the regime where the stationary shortcut cancels)."""
+    m = P.Model(PADE_MODELS[name], 0.05)
+    assert m.state_dim > 3
+    s = P.pssgp_get_ssm(m.h)
+    F, Q = m.discretize(dt)
+    Fm, Qm = _mp_van_loan(s["G"], s["W"], dt)
+    assert np.max(np.abs(F - Fm)) <= 1e-13 * max(1.0, np.max(np.abs(Fm)))
+    assert np.max(np.abs(Q - Qm)) <= 1e-13 * np.max(np.abs(s["Pinf"]))
+    if dt <= 0.02:
+        big = np.abs(Qm) > 1e-10 * np.max(np.abs(Qm))
+        assert np.max(np.abs(Q - Qm)[big] / np.abs(Qm)[big]) <= 1e-10
