@@ -178,6 +178,9 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_filter_apply(con
     set_identity(sag);
     bool sag_done = false;
     int ferr = -1;
+    double quad = 0.0, prodm = 1.0;
+    long long prode = 0;
+    int nobs = 0;
     const int64_t nwin = (p.K + kWinA - 1) / kWinA;
     issue_window(st[wid], 0, p.t, p.y, wbase, p.K, p.n, 0, lane);
     unsigned long long mnext = mask_word(p.mask, kb, ke);
@@ -243,7 +246,17 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_filter_apply(con
                     for (int j = i; j < D; ++j) P0[si(D, i, j)] = fma(-si_, SH[j], P0[si(D, i, j)]);
                 }
             }
-            nst[wid][jj][lane] = obs ? 0.5 * (log(S) + 1.8378770664093453 + v * vs) : 0.0;
+            // NLL of the (chain, series) segment: running v^2/S sum and S product (one log per
+            // segment, written at the segment's last step; every other step contributes 0)
+            nll_accumulate(obs, v, vs, S, quad, prodm, prode, nobs);
+            double term = 0.0;
+            if (k == s.end - 1 || k == ke - 1) {
+                if (nobs > 0)
+                    term = 0.5 * (quad + log(prodm) + static_cast<double>(prode) * 0.6931471805599453 +
+                                  nobs * 1.8378770664093453);
+                quad = 0.0; prodm = 1.0; prode = 0; nobs = 0;
+            }
+            nst[wid][jj][lane] = term;
             if (k == s.end - 1 && !sag_done) {
                 // first series end in this chain: the chain's smoother aggregate is the collapsed
                 // (0, m^s_k0, P^s_k0) of that series (terminal element)
