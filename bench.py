@@ -232,8 +232,9 @@ def main():
     if args.config == "batched":
         # f2: B series of 3,200 points (the sunspot N of PAPER.md:206), each with its own
         # hyper-parameters (multi-start / HMC shape), one launch
+        # multi-GPU: every rank runs its own batch of independent series (replicas, no collective)
         B = max(1, args.N // 3200)
-        rng = np.random.default_rng(0)
+        rng = np.random.default_rng(rank)
         lens = np.full(B, 3200, np.int64)
         off = torch.from_numpy(np.concatenate([[0], np.cumsum(lens)])).to(dev)
         VB = torch.from_numpy(rng.uniform(0.5, 2.0, B)).to(dev)
@@ -315,7 +316,11 @@ def main():
         dist.all_reduce(tt_, op=dist.ReduceOp.MAX)
         ms_total = float(tt_.item())
     ms_step = ms_total / args.steps
-    value = N / (ms_step * 1e-3)
+    # independent problems per rank (batched series, gradient evaluations): weak scaling, the
+    # job's units are all ranks' steps; the time-sharded posterior: strong scaling over one grid
+    replicas = args.config in ("batched", "grad") and world > 1
+    units = N * world if replicas else N
+    value = units / (ms_step * 1e-3)
 
     # ---- e2e through the public host API (pinned buffers, copies inside the timed region)
     e2e = None
@@ -416,7 +421,8 @@ def main():
         extra["latency_n3200_ms"] = a0.elapsed_time(a1) / 200
     line = {"metric": metric, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "weak" if replicas else "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
             "config": {"workload": w.name, "N": N, "state_dim": model.state_dim, "chain_len": plan["chain_len"],
                        "ctas": plan["n_blocks"], "threads_per_cta": plan["threads"],
                        "l2": "no flush: working set (1.8 GB) >> 126 MB L2",
