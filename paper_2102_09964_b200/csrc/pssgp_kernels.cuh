@@ -239,13 +239,15 @@ set_zero(F);
     const int64_t nwin = (p.K + kWinA - 1) / kWinA;
     issue_window(st[wid], 0, p.t, p.y, wbase, p.K, p.n, 0, lane);
     unsigned long long mnext = mask_word(p.mask, kb, ke);             // mask bytes of window 0
+    unsigned long long mnext2 = mask_word(p.mask, kb + kWinA, ke);     // ... and of window 1 (2 ahead)
     for (int64_t w = 0; w < nwin; ++w) {
         const int64_t j0 = w * kWinA;
         const int buf = static_cast<int>(w & 1);
         if (w + 1 < nwin) issue_window(st[wid], buf ^ 1, p.t, p.y, wbase, p.K, p.n, j0 + kWinA, lane);
         else cp_async_commit();
         const unsigned long long mwin = mnext;
-        mnext = mask_word(p.mask, kb + j0 + kWinA, ke);
+        mnext = mnext2;
+        mnext2 = mask_word(p.mask, kb + j0 + 2 * kWinA, ke);
         cp_async_wait<1>();
         __syncwarp();
         const int jend = static_cast<int>(min(static_cast<int64_t>(kWinA), ke - (kb + j0)));
