@@ -197,6 +197,19 @@ int64_t pssgp_error_index(const pssgp_model* m);
 /* Human-readable description of the last error (static storage of the handle). */
 const char* pssgp_last_error(const pssgp_model* m);
 
+/* Pipelined variant of pssgp_posterior_host for streams of problems: enqueues the host ->
+ * device copies, pssgp_posterior and the device -> host copies on one of two handle-owned
+ * streams (alternating per call) and returns immediately, so one call's device -> host copies
+ * overlap the next call's host -> device copies (PCIe is full duplex); the computes run in call
+ * order.  Host arrays must be PINNED and stay untouched until pssgp_sync returns; the two most
+ * recent calls may be in flight.  Host-detectable errors are returned immediately. */
+pssgp_status pssgp_posterior_host_async(pssgp_model* m, int64_t N, const double* t, const double* y,
+                                        const uint8_t* mask, double* mean, double* var, double* nll);
+
+/* Wait for every pssgp_posterior_host_async call of the handle; returns the first
+ * device-detected error (as pssgp_check). */
+pssgp_status pssgp_sync(pssgp_model* m);
+
 /* Copy the host-side balanced model: G, W = L q L^T, P_inf (d*d row-major),
  * H (d), D (d, balancing diagonal; z = D^-1 x).  Any pointer may be NULL. */
 pssgp_status pssgp_get_ssm(const pssgp_model* m, double* G, double* W, double* H,

@@ -21,7 +21,7 @@ import numpy as np
 from ._native import (KINDS, STATUS_NAMES, Component, Options, PssgpError, build, lib)  # noqa: F401
 
 __all__ = ["Model", "PssgpError", "build", "lib", "pssgp_create", "pssgp_destroy", "pssgp_posterior",
-           "pssgp_nll", "pssgp_nll_grad", "pssgp_posterior_host", "pssgp_check", "pssgp_error_index", "pssgp_last_error",
+           "pssgp_nll", "pssgp_nll_grad", "pssgp_posterior_host_async", "pssgp_sync", "pssgp_posterior_host", "pssgp_check", "pssgp_error_index", "pssgp_last_error",
            "pssgp_state_dim", "pssgp_get_ssm", "pssgp_debug_discretize", "pssgp_plan",
            "pssgp_aggregate_bytes", "pssgp_shard_filter_reduce", "pssgp_shard_filter_apply",
            "pssgp_shard_smoother_apply", "pssgp_profile_enable", "pssgp_profile_read", "pssgp_profile_name",
@@ -103,6 +103,21 @@ def pssgp_posterior_host(h, N, t: np.ndarray, y: np.ndarray, mask: np.ndarray, m
         return a.ctypes.data
     _raise(h, lib().pssgp_posterior_host(h, int(N), hp(t), hp(y), hp(mask), hp(mean), hp(var), hp(nll),
                                          _stream_ptr(stream)))
+
+
+def pssgp_posterior_host_async(h, N, t, y, mask, mean, var, nll) -> None:
+    """Pinned host arrays (torch pin_memory tensors or page-locked numpy); returns immediately."""
+    def hp(a):
+        if a is None:
+            return None
+        if hasattr(a, "data_ptr"):
+            return int(a.data_ptr())
+        return a.ctypes.data
+    _raise(h, lib().pssgp_posterior_host_async(h, int(N), hp(t), hp(y), hp(mask), hp(mean), hp(var), hp(nll)))
+
+
+def pssgp_sync(h) -> None:
+    _raise(h, lib().pssgp_sync(h))
 
 
 def pssgp_merge_grid(h, n_train, t_train, y_train, n_test, t_test, t_out, y_out, mask_out, test_index,

@@ -73,6 +73,8 @@ SIGNATURES = {
     "pssgp_nll_grad": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pssgp_posterior_host": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pssgp_check": (ctypes.c_int, [_vp]),
+    "pssgp_posterior_host_async": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "pssgp_sync": (ctypes.c_int, [_vp]),
     "pssgp_merge_grid": (ctypes.c_int, [_vp, _i64, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pssgp_gather": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pssgp_predict": (ctypes.c_int, [_vp, _i64, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp]),

@@ -65,6 +65,14 @@ struct pssgp_model {
     size_t bt_bytes = 0;
     double* fq = nullptr;                 // wide path, kPade mode: per-step (F, Q)
     size_t fq_bytes = 0;
+    // pipelined host API (pssgp_posterior_host_async): two slots, each with its own stream and
+    // device I/O buffers; computes are chained in call order through acompute
+    char* aio[2] = {nullptr, nullptr};
+    size_t aio_bytes[2] = {0, 0};
+    cudaStream_t astream[2] = {nullptr, nullptr};
+    cudaEvent_t acompute = nullptr;
+    bool acompute_rec = false;
+    int aslot = 0;
     cudaStream_t last_stream = nullptr;
     int64_t err_index = -1;
     std::string last_err;
@@ -809,6 +817,11 @@ void pssgp_destroy(pssgp_model* m) {
     if (m->mg) cudaFree(m->mg);
     if (m->bt) cudaFree(m->bt);
     if (m->fq) cudaFree(m->fq);
+    for (int i = 0; i < 2; ++i) {
+        if (m->aio[i]) cudaFree(m->aio[i]);
+        if (m->astream[i]) cudaStreamDestroy(m->astream[i]);
+    }
+    if (m->acompute) cudaEventDestroy(m->acompute);
     if (m->d_err) cudaFree(m->d_err);
     if (m->d_model) cudaFree(m->d_model);
     for (int s = 0; s < kSlots; ++s)
@@ -1044,6 +1057,68 @@ pssgp_status pssgp_posterior_host(pssgp_model* m, int64_t N, const double* t, co
     m->last_stream = s;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(m, e, "pssgp_posterior_host copies");
+    return pssgp_check(m);
+}
+
+pssgp_status pssgp_posterior_host_async(pssgp_model* m, int64_t N, const double* t, const double* y,
+                                        const uint8_t* mask, double* mean, double* var, double* nll) {
+    pssgp_status st = check_args(m, N, t, y, mask);
+    if (st) return st;
+    if ((st = ensure_device(m))) return st;
+    if (!m->astream[0]) {
+        for (int i = 0; i < 2; ++i)
+            if (cudaStreamCreateWithFlags(&m->astream[i], cudaStreamNonBlocking) != cudaSuccess)
+                return fail(m, PSSGP_E_CUDA, "cudaStreamCreate");
+        if (cudaEventCreateWithFlags(&m->acompute, cudaEventDisableTiming) != cudaSuccess)
+            return fail(m, PSSGP_E_CUDA, "cudaEventCreate");
+    }
+    const int slot = m->aslot;
+    m->aslot ^= 1;
+    cudaStream_t s = m->astream[slot];
+    const size_t nd = static_cast<size_t>(N);
+    const size_t need = nd * (8 + 8 + 8 + 8) + nd + 64;
+    if (need > m->aio_bytes[slot]) {
+        if (m->aio[slot]) cudaFree(m->aio[slot]);      // synchronising: the slot's last call is done
+        m->aio[slot] = nullptr;
+        m->aio_bytes[slot] = 0;
+        if (cudaMalloc(&m->aio[slot], need) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(m, PSSGP_E_NOMEM, "cudaMalloc(async io)");
+        }
+        m->aio_bytes[slot] = need;
+    }
+    double* dnll = reinterpret_cast<double*>(m->aio[slot]);
+    double* dt_ = dnll + 8;
+    double* dy = dt_ + nd;
+    double* dmean = dy + nd;
+    double* dvar = dmean + nd;
+    uint8_t* dmask = reinterpret_cast<uint8_t*>(dvar + nd);
+    if (N > 0) {   // host -> device on this slot's stream (overlaps the other slot's device -> host)
+        cudaMemcpyAsync(dt_, t, nd * 8, cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync(dy, y, nd * 8, cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync(dmask, mask, nd, cudaMemcpyHostToDevice, s);
+    }
+    if (m->acompute_rec) cudaStreamWaitEvent(s, m->acompute, 0);   // computes run in call order
+    st = pssgp_posterior(m, N, dt_, dy, dmask, mean ? dmean : nullptr, var ? dvar : nullptr, nll ? dnll : nullptr,
+                         s);
+    if (st) return st;
+    cudaEventRecord(m->acompute, s);
+    m->acompute_rec = true;
+    if (N > 0 && mean) cudaMemcpyAsync(mean, dmean, nd * 8, cudaMemcpyDeviceToHost, s);
+    if (N > 0 && var) cudaMemcpyAsync(var, dvar, nd * 8, cudaMemcpyDeviceToHost, s);
+    if (nll) cudaMemcpyAsync(nll, dnll, 8, cudaMemcpyDeviceToHost, s);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(m, e, "pssgp_posterior_host_async copies");
+    return PSSGP_OK;
+}
+
+pssgp_status pssgp_sync(pssgp_model* m) {
+    if (!m) return PSSGP_E_ARG;
+    for (int i = 0; i < 2; ++i)
+        if (m->astream[i]) {
+            cudaError_t e = cudaStreamSynchronize(m->astream[i]);
+            if (e != cudaSuccess) return cuda_fail(m, e, "cudaStreamSynchronize(async)");
+        }
     return pssgp_check(m);
 }
 

@@ -477,3 +477,25 @@ def test_kw_discretize_vs_high_precision(cuda_device, name, dt):
     if dt <= 0.02:
         big = np.abs(Qm) > 1e-10 * np.max(np.abs(Qm))
         assert np.max(np.abs(Q - Qm)[big] / np.abs(Qm)[big]) <= 1e-10
+
+
+def test_host_async_pipeline(cuda_device):
+    """pssgp_posterior_host_async: several problems in flight on the two internal slots give the
+    same results as the synchronous host call, for each problem."""
+    m = P.Model([synth.Component("matern52", 1.0, 0.5)], 0.01)
+    ws = [synth.random_problem(40 + i, 5000 + 997 * i, kind="matern52", p_missing=0.2, variance=1.0,
+                               lengthscale=0.5, noise_var=0.01) for i in range(4)]
+    outs = []
+    pinned = []
+    for w in ws:
+        th, yh, mh = (torch.from_numpy(a).pin_memory() for a in (w.t, w.y, w.mask))
+        mo = torch.empty(w.N, dtype=torch.float64).pin_memory()
+        vo = torch.empty_like(mo)
+        no = torch.zeros(1, dtype=torch.float64).pin_memory()
+        pinned.append((th, yh, mh))
+        outs.append((mo, vo, no))
+        P.pssgp_posterior_host_async(m.h, w.N, th, yh, mh, mo, vo, no)
+    P.pssgp_sync(m.h)
+    for w, (mo, vo, no) in zip(ws, outs):
+        mean, var, nll = m.posterior_host(w.t, w.y, w.mask)
+        assert np.array_equal(mo.numpy(), mean) and np.array_equal(vo.numpy(), var) and float(no[0]) == float(nll[0])
