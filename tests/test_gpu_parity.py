@@ -499,3 +499,25 @@ def test_host_async_pipeline(cuda_device):
     for w, (mo, vo, no) in zip(ws, outs):
         mean, var, nll = m.posterior_host(w.t, w.y, w.mask)
         assert np.array_equal(mo.numpy(), mean) and np.array_equal(vo.numpy(), var) and float(no[0]) == float(nll[0])
+
+
+@pytest.mark.parametrize("case", ["table_rbf3", "pade_rbf3", "wide_pade_rbf6", "wide_table_c4"])
+def test_nll_only_all_modes(cuda_device, case):
+    """pssgp_nll (no stored state, no smoother; K3's STORE = false instantiation / the wide
+    NLL-only path) equals the posterior's NLL and the oracle for every discretisation mode."""
+    if case == "table_rbf3":
+        w = _uniform([synth.Component("rbf", 1.3, 0.8, order=3)], 0.05, 9001, 0.01, p_missing=0.2, seed=5)
+    elif case == "pade_rbf3":
+        w = _irregular(PADE_MODELS["rbf3"], 0.05, 9001, seed=6)
+    elif case == "wide_pade_rbf6":
+        w = _irregular(PADE_MODELS["rbf6"], 0.05, 6001, seed=7)
+    else:
+        w = synth.config4(n=4096)
+    m = P.Model(w.components, w.noise_var, uniform_dt=w.uniform_dt)
+    t, y, mk = to_dev(w)
+    _, _, nll_a = m.posterior(t, y, mk)
+    nll_b = m.nll(t, y, mk)
+    m.check()
+    assert abs(float(nll_a.cpu()[0]) - float(nll_b.cpu()[0])) <= 1e-12 * abs(float(nll_a.cpu()[0]))
+    o = oracle.posterior(w, smooth=False)
+    assert abs(float(nll_b.cpu()[0]) - o["nll"]) <= NLL_TOL * abs(o["nll"])
