@@ -12,7 +12,8 @@ the global grid.  The exchange is the paper's associativity (PAPER.md:326,
                      smoother aggregate (E, g, L) and NLL partial -> all_gather
   3. smoother apply: rank g applies the ordered product of smoother aggregates
                      g+1..G-1 (collapsed global suffix), runs the RTS rescan.
-  NLL = fixed-order sum of the gathered partials (deterministic).
+  NLL = fixed-order sum of the gathered partials (deterministic); the partials travel in the
+  same all_gather as the smoother aggregates (two collectives per posterior).
 
 The collectives carry a few hundred bytes (27 + 18 + 1 doubles at d = 3), so
 they are latency-bound; NCCL over NVLink/NVSwitch through torch.distributed.
@@ -50,10 +51,18 @@ def sharded_posterior(backend, exchange: Callable, rank: int, world: int):
     fa = backend.filter_reduce()
     all_fa = exchange(fa)
     sa, nll_part = backend.filter_apply(all_fa)
-    all_sa = exchange(sa)
+    # one collective carries both the smoother aggregate and the NLL partial
+    ns = sa.numel()
+    all_msg = exchange(_cat(sa.reshape(-1), nll_part.reshape(-1)))
+    all_sa = all_msg[:, :ns].contiguous()
+    all_nll = all_msg[:, ns:].contiguous()
     mean, var = backend.smoother_apply(all_sa)
-    all_nll = exchange(nll_part)
     return mean, var, all_nll
+
+
+def _cat(a, b):
+    import torch
+    return torch.cat([a, b])
 
 
 class DeviceShard:
