@@ -269,6 +269,65 @@ PS_HD bool gauss_solve(double (&M)[D * D], double (&R)[D * NR]) {
     return ok;
 }
 
+// Inverse of a small D x D matrix (D <= 3) by the adjugate: cofactors in parallel, one
+// reciprocal of the determinant — a short dependency chain (no pivot search, no
+// compare-and-swap), for the (I + C J) and (I + P J) of the filtering operator, whose
+// eigenvalues are >= 1 (C, J, P positive semi-definite).  Returns false
+// for a zero or non-finite determinant.
+template <int D>
+PS_HD bool inv_small(const double (&M)[D * D], double (&Mi)[D * D]) {
+    static_assert(D <= 3, "adjugate inverse for D <= 3");
+    if constexpr (D == 1) {
+        Mi[0] = rcp(M[0]);
+        return M[0] != 0.0;
+    } else if constexpr (D == 2) {
+        const double det = fma(M[0], M[3], -M[1] * M[2]);
+        const double id = rcp(det);
+        Mi[0] = M[3] * id; Mi[1] = -M[1] * id; Mi[2] = -M[2] * id; Mi[3] = M[0] * id;
+        return det != 0.0 && isfinite(id);
+    } else {
+        const double c00 = fma(M[4], M[8], -M[5] * M[7]);
+        const double c01 = fma(M[5], M[6], -M[3] * M[8]);
+        const double c02 = fma(M[3], M[7], -M[4] * M[6]);
+        const double det = fma(M[0], c00, fma(M[1], c01, M[2] * c02));
+        const double id = rcp(det);
+        Mi[0] = c00 * id;
+        Mi[3] = c01 * id;
+        Mi[6] = c02 * id;
+        Mi[1] = fma(M[2], M[7], -M[1] * M[8]) * id;
+        Mi[4] = fma(M[0], M[8], -M[2] * M[6]) * id;
+        Mi[7] = fma(M[1], M[6], -M[0] * M[7]) * id;
+        Mi[2] = fma(M[1], M[5], -M[2] * M[4]) * id;
+        Mi[5] = fma(M[2], M[3], -M[0] * M[5]) * id;
+        Mi[8] = fma(M[0], M[4], -M[1] * M[3]) * id;
+        return det != 0.0 && isfinite(id);
+    }
+}
+
+// Solve M X = R (R: D x NR row-major, in place): adjugate for D <= 3, pivoted elimination above.
+template <int D, int NR>
+PS_HD bool small_solve(double (&M)[D * D], double (&R)[D * NR]) {
+    if constexpr (D <= 3) {
+        double Mi[D * D];
+        const bool ok = inv_small<D>(M, Mi);
+        double X[D * NR];
+#pragma unroll
+        for (int r = 0; r < D; ++r)
+#pragma unroll
+            for (int c = 0; c < NR; ++c) {
+                double s = 0.0;
+#pragma unroll
+                for (int k = 0; k < D; ++k) s = fma(Mi[r * D + k], R[k * NR + c], s);
+                X[r * NR + c] = s;
+            }
+#pragma unroll
+        for (int i = 0; i < D * NR; ++i) R[i] = X[i];
+        return ok;
+    } else {
+        return gauss_solve<D, NR>(M, R);
+    }
+}
+
 // LDL^T factorisation of a symmetric positive-definite packed matrix.
 // Lo: strictly-lower factor (row-major D x D, only i > j used), id: 1 / d.
 template <int D>
@@ -852,8 +911,13 @@ PS_HD bool combine(const FAgg<D>& ei, const FAgg<D>& ej, FAgg<D>& out) {
         for (int k = 0; k < D; ++k) e = fma(-ej.J[si(D, r, k)], ei.b[k], e);
         Y[r * NY + D] = e;
     }
+#if PSSGP_PIVOTED_COMBINE
     bool ok = gauss_solve<D, NX>(M, X);
     ok = gauss_solve<D, NY>(MT, Y) && ok;
+#else
+    bool ok = small_solve<D, NX>(M, X);
+    ok = small_solve<D, NY>(MT, Y) && ok;
+#endif
     // A_ij = A_j X_A ; b_ij = A_j X_b + b_j ; C_ij = A_j X_C A_j^T + C_j
     double AX[D * D];
 #pragma unroll
@@ -921,7 +985,11 @@ PS_HD bool apply_prefix(const Gauss<D>& g, const FAgg<D>& a, Gauss<D>& out) {
         }
         X[r * NX + D] = s0;
     }
+#if PSSGP_PIVOTED_COMBINE
     const bool ok = gauss_solve<D, NX>(M, X);
+#else
+    const bool ok = small_solve<D, NX>(M, X);
+#endif
     double AX[D * D];
 #pragma unroll
     for (int r = 0; r < D; ++r) {
