@@ -915,8 +915,36 @@ PS_HD bool combine(const FAgg<D>& ei, const FAgg<D>& ej, FAgg<D>& out) {
     bool ok = gauss_solve<D, NX>(M, X);
     ok = gauss_solve<D, NY>(MT, Y) && ok;
 #else
-    bool ok = small_solve<D, NX>(M, X);
-    ok = small_solve<D, NY>(MT, Y) && ok;
+    bool ok;
+    if constexpr (D <= 3) {
+        // (I + J_j C_i) = (I + C_i J_j)^T (C, J symmetric): one inverse serves both solves
+        double Mi[D * D], Xo[D * NX], Yo[D * NY];
+        ok = inv_small<D>(M, Mi);
+#pragma unroll
+        for (int r = 0; r < D; ++r) {
+#pragma unroll
+            for (int c = 0; c < NX; ++c) {
+                double t = 0.0;
+#pragma unroll
+                for (int k = 0; k < D; ++k) t = fma(Mi[r * D + k], X[k * NX + c], t);
+                Xo[r * NX + c] = t;
+            }
+#pragma unroll
+            for (int c = 0; c < NY; ++c) {
+                double t = 0.0;
+#pragma unroll
+                for (int k = 0; k < D; ++k) t = fma(Mi[k * D + r], Y[k * NY + c], t);
+                Yo[r * NY + c] = t;
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < D * NX; ++i) X[i] = Xo[i];
+#pragma unroll
+        for (int i = 0; i < D * NY; ++i) Y[i] = Yo[i];
+    } else {
+        ok = gauss_solve<D, NX>(M, X);
+        ok = gauss_solve<D, NY>(MT, Y) && ok;
+    }
 #endif
     // A_ij = A_j X_A ; b_ij = A_j X_b + b_j ; C_ij = A_j X_C A_j^T + C_j
     double AX[D * D];
