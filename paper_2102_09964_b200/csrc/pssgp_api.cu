@@ -71,6 +71,7 @@ struct pssgp_model {
     size_t aio_bytes[2] = {0, 0};
     cudaStream_t astream[2] = {nullptr, nullptr};
     cudaEvent_t acompute = nullptr;
+    unsigned long long epoch = 0;         // K3 block-carry publication counter (flag = d_err[1])
     bool acompute_rec = false;
     int aslot = 0;
     cudaStream_t last_stream = nullptr;
@@ -168,6 +169,7 @@ pssgp_status ensure_device(pssgp_model* m) {
     e = cudaMalloc(&m->d_err, 2 * sizeof(unsigned long long) + 8 * sizeof(double));
     if (e != cudaSuccess) return fail(m, PSSGP_E_NOMEM, "cudaMalloc(error word)");
     cudaMemset(m->d_err, 0xff, sizeof(unsigned long long));
+    cudaMemset(m->d_err + 1, 0, sizeof(unsigned long long));   // K3 publication flag
     m->d_scalar = reinterpret_cast<double*>(m->d_err + 2);
     return PSSGP_OK;
 }
@@ -237,6 +239,7 @@ pssgp_status setup(pssgp_model* m, const Plan& pl, KParams<D>& p) {
     p.K = pl.K;
     p.nb = pl.nb;
     p.err = m->d_err;
+    p.flag = m->d_err + 1;
     p.rank = 0;
     p.world = 1;
     p.store_state = 1;
@@ -267,6 +270,7 @@ pssgp_status phase_filter_reduce(pssgp_model* m, KParams<D>& p, cudaStream_t s) 
 
 template <int D>
 pssgp_status phase_filter_apply(pssgp_model* m, KParams<D>& p, cudaStream_t s) {
+    p.epoch = ++m->epoch;
     ProfScope ps(m, S_K3, s);
     if (p.store_state) LAUNCH_MODE(m, k_filter_apply, p.nb, kThreads, s, p);
     else if (m->mode == kClosed) k_filter_apply<D, kClosed, false><<<p.nb, kThreads, 0, s>>>(p);
@@ -976,6 +980,7 @@ pssgp_status pssgp_posterior_batched(pssgp_model* m, int nseg, const int64_t* of
         p.t = t; p.y = y; p.mask = mask; p.n = N; p.k0 = 0; p.nglob = N; p.mean = mean; p.var = var;    \
         { ProfScope ps(m, S_K1, s); pssgp::batch::k_batch_filter_reduce<DD><<<pl.nb, kThreads, 0, s>>>(p, q); } \
         LAUNCH_CHECK(m, "k_batch_filter_reduce");                                                       \
+        p.epoch = ++m->epoch;                                                                            \
         { ProfScope ps(m, S_K3, s); pssgp::batch::k_batch_filter_apply<DD><<<pl.nb, kThreads, 0, s>>>(p, q); } \
         LAUNCH_CHECK(m, "k_batch_filter_apply");                                                        \
         { ProfScope ps(m, S_K5, s); pssgp::batch::k_batch_smoother_apply<DD><<<pl.nb, kThreads, 0, s>>>(p, q); } \
@@ -1007,6 +1012,7 @@ pssgp_status pssgp_check(pssgp_model* m) {
     if (e != cudaSuccess) return cuda_fail(m, e, "cudaMemcpy(error word)");
     if (w == ~0ULL) return PSSGP_OK;
     cudaMemset(m->d_err, 0xff, sizeof(unsigned long long));
+    cudaMemset(m->d_err + 1, 0, sizeof(unsigned long long));   // K3 publication flag
     const unsigned code = static_cast<unsigned>(w & 0xff);
     const int64_t idx = static_cast<int64_t>((w >> 8) & 0xffffffffffffULL);
     const char* what = code == kErrInput ? "invalid input (unsorted/non-finite t or non-finite observed y)"

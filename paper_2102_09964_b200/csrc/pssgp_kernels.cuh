@@ -87,6 +87,8 @@ struct KParams {
     double* nll_out;        // nll scalar output (nullable)
     unsigned long long* err;
     int store_state;        // K3: write (xbar, P) and smoother aggregates (0 for NLL-only)
+    unsigned long long* flag;   // K3 block-carry publication word (workspace, zeroed at allocation)
+    unsigned long long epoch;   // this launch's publication value (> every earlier one)
 };
 
 // ------------------------------------------------------------------ warp shuffles of aggregates
@@ -413,34 +415,25 @@ __device__ __forceinline__ void nll_accumulate(bool obs, double v, double vs, do
 template <int D>
 __device__ __forceinline__ Gauss<D> filter_chain_carry(const KParams<D>& p, FAgg<D>* tot, Gauss<D>* wcar, int64_t c,
                                                        int64_t nch, int lane, int wid) {
-    // ---- collapsed prefix entering this CTA: incoming carry of earlier ranks (sharded)
-    // (x) ordered product of the block aggregates of CTAs 0..blockIdx-1
+    // ---- collapsed prefix entering this CTA.  CTA 0 alone scans the block aggregates (an
+    // exclusive scan producing the collapsed carry (x, P) entering every CTA, starting from the
+    // incoming carry of earlier ranks when sharded), writes them to p.fcarry and publishes
+    // p.epoch in p.flag; the other CTAs spin on the flag (all CTAs of the one-wave grid are
+    // co-resident and CTA 0 never waits) while their warps' chain scans below run.  This
+    // replaces a redundant per-CTA reduction of all earlier blocks (~20 dependent operator
+    // levels, throughput-bound across the wave) by one scan of depth ~15 in one CTA.
     Gauss<D> cur;
-    {
-        const FAgg<D> before = cta_reduce_range<FAgg<D>>(p.block_f, 0, blockIdx.x, tot);
-        if (threadIdx.x == 0) {
-            Gauss<D> R;
-            set_zero(R);
-            for (int g = 0; g < p.rank && p.in_filt; ++g) {
-                FAgg<D> ag;
-                load_aos(ag, p.in_filt + static_cast<int64_t>(g) * FN(D));
-                Gauss<D> r2;
-                apply_prefix(R, ag, r2);
-                R = r2;
-            }
-            if (blockIdx.x > 0) {
-                Gauss<D> r2;
-                apply_prefix(R, before, r2);
-                R = r2;
-            }
-            wcar[0] = R;
-        }
-        __syncthreads();
-    }
-    // ---- carry into this chain: CTA carry (x) exclusive scan of chain aggregates
-    {
+    if (blockIdx.x == 0) {
+        const int per = (p.nb + kThreads - 1) / kThreads;
+        const int b0 = min(static_cast<int>(threadIdx.x) * per, p.nb), b1 = min(b0 + per, p.nb);
         FAgg<D> a;
-        load_soa(a, p.chain_f, nch, c);
+        set_identity(a);
+        for (int b = b0; b < b1; ++b) {
+            FAgg<D> e, r;
+            load_aos(e, p.block_f + static_cast<int64_t>(b) * FN(D));
+            combine(a, e, r);
+            a = r;
+        }
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
             FAgg<D> o;
@@ -456,7 +449,71 @@ __device__ __forceinline__ Gauss<D> filter_chain_carry(const KParams<D>& p, FAgg
         shfl_up_all(ex, a, 1);
         __syncthreads();
         if (threadIdx.x == 0) {
-            Gauss<D> acc = wcar[0];
+            Gauss<D> R;
+            set_zero(R);
+            for (int g = 0; g < p.rank && p.in_filt; ++g) {
+                FAgg<D> ag;
+                load_aos(ag, p.in_filt + static_cast<int64_t>(g) * FN(D));
+                Gauss<D> r2;
+                apply_prefix(R, ag, r2);
+                R = r2;
+            }
+            for (int w = 0; w < kWarps; ++w) {
+                wcar[w] = R;
+                Gauss<D> r2;
+                apply_prefix(R, tot[w], r2);
+                R = r2;
+            }
+        }
+        __syncthreads();
+        Gauss<D> C = wcar[wid];
+        if (lane > 0) {
+            Gauss<D> r2;
+            apply_prefix(C, ex, r2);
+            C = r2;
+        }
+        for (int b = b0; b < b1; ++b) {
+            store_aos(C, p.fcarry + static_cast<int64_t>(b) * CN(D));
+            FAgg<D> e;
+            load_aos(e, p.block_f + static_cast<int64_t>(b) * FN(D));
+            Gauss<D> r2;
+            apply_prefix(C, e, r2);
+            C = r2;
+        }
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) atomicExch(p.flag, p.epoch);
+    }
+    // ---- carry into this chain: CTA carry (x) exclusive scan of chain aggregates
+    {
+        FAgg<D> a;
+        load_soa(a, p.chain_f, nch, c);
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            FAgg<D> o;
+            shfl_up_all(o, a, off);
+            if (lane >= off) {
+                FAgg<D> r;
+                combine(o, a, r);
+                a = r;
+            }
+        }
+        FAgg<D> ex;
+        shfl_up_all(ex, a, 1);
+        __syncthreads();                        // CTA 0: its block scan is done with tot / wcar
+        if (lane == 31) tot[wid] = a;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            // wait for CTA 0's publication, then read this CTA's collapsed carry
+            while (atomicAdd(p.flag, 0ull) < p.epoch) __nanosleep(64);
+            __threadfence();
+            Gauss<D> acc;
+            {   // L2 loads (the carry was written by another CTA in this launch)
+                double* d = reinterpret_cast<double*>(&acc);
+                const double* src = p.fcarry + static_cast<int64_t>(blockIdx.x) * CN(D);
+#pragma unroll
+                for (int i = 0; i < CN(D); ++i) d[i] = __ldcg(src + i);
+            }
             for (int w = 0; w < kWarps; ++w) {
                 wcar[w] = acc;
                 Gauss<D> r2;
