@@ -71,7 +71,6 @@ struct pssgp_model {
     size_t aio_bytes[2] = {0, 0};
     cudaStream_t astream[2] = {nullptr, nullptr};
     cudaEvent_t acompute = nullptr;
-    unsigned long long epoch = 0;         // K3 block-carry publication counter (flag = d_err[1])
     bool acompute_rec = false;
     int aslot = 0;
     cudaStream_t last_stream = nullptr;
@@ -270,7 +269,6 @@ pssgp_status phase_filter_reduce(pssgp_model* m, KParams<D>& p, cudaStream_t s) 
 
 template <int D>
 pssgp_status phase_filter_apply(pssgp_model* m, KParams<D>& p, cudaStream_t s) {
-    p.epoch = ++m->epoch;
     ProfScope ps(m, S_K3, s);
     if (p.store_state) LAUNCH_MODE(m, k_filter_apply, p.nb, kThreads, s, p);
     else if (m->mode == kClosed) k_filter_apply<D, kClosed, false><<<p.nb, kThreads, 0, s>>>(p);
@@ -980,7 +978,6 @@ pssgp_status pssgp_posterior_batched(pssgp_model* m, int nseg, const int64_t* of
         p.t = t; p.y = y; p.mask = mask; p.n = N; p.k0 = 0; p.nglob = N; p.mean = mean; p.var = var;    \
         { ProfScope ps(m, S_K1, s); pssgp::batch::k_batch_filter_reduce<DD><<<pl.nb, kThreads, 0, s>>>(p, q); } \
         LAUNCH_CHECK(m, "k_batch_filter_reduce");                                                       \
-        p.epoch = ++m->epoch;                                                                            \
         { ProfScope ps(m, S_K3, s); pssgp::batch::k_batch_filter_apply<DD><<<pl.nb, kThreads, 0, s>>>(p, q); } \
         LAUNCH_CHECK(m, "k_batch_filter_apply");                                                        \
         { ProfScope ps(m, S_K5, s); pssgp::batch::k_batch_smoother_apply<DD><<<pl.nb, kThreads, 0, s>>>(p, q); } \

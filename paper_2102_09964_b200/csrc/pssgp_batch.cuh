@@ -82,6 +82,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_filter_reduce(co
     const int64_t wbase = (static_cast<int64_t>(blockIdx.x) * kThreads + wid * 32) * p.K;
     const int64_t kb = c * p.K;
     const int64_t ke = min(kb + p.K, p.n);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *p.flag = 0ull;   // K3b's carry publication word
     FAgg<D> a;
     set_identity(a);
     ModelParams<D> mp = p.m;

@@ -87,8 +87,8 @@ struct KParams {
     double* nll_out;        // nll scalar output (nullable)
     unsigned long long* err;
     int store_state;        // K3: write (xbar, P) and smoother aggregates (0 for NLL-only)
-    unsigned long long* flag;   // K3 block-carry publication word (workspace, zeroed at allocation)
-    unsigned long long epoch;   // this launch's publication value (> every earlier one)
+    unsigned long long* flag;   // K3 block-carry publication word: reset to 0 by K1, set to 1 by
+                                // K3's CTA 0 (stream-ordered, so CUDA-graph replays are safe)
 };
 
 // ------------------------------------------------------------------ warp shuffles of aggregates
@@ -211,6 +211,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_reduce(const KP
     const int64_t kb = c * p.K;
     const int64_t ke = min(kb + p.K, p.n);
 
+    if (blockIdx.x == 0 && threadIdx.x == 0) *p.flag = 0ull;   // K3's carry publication word
     FAgg<D> a;
     set_identity(a);
     double tprev = 0.0;
@@ -418,7 +419,7 @@ __device__ __forceinline__ Gauss<D> filter_chain_carry(const KParams<D>& p, FAgg
     // ---- collapsed prefix entering this CTA.  CTA 0 alone scans the block aggregates (an
     // exclusive scan producing the collapsed carry (x, P) entering every CTA, starting from the
     // incoming carry of earlier ranks when sharded), writes them to p.fcarry and publishes
-    // p.epoch in p.flag; the other CTAs spin on the flag (all CTAs of the one-wave grid are
+    // 1 in p.flag (K1 of the same posterior reset it to 0); the other CTAs spin on the flag (all CTAs of the one-wave grid are
     // co-resident and CTA 0 never waits) while their warps' chain scans below run.  This
     // replaces a redundant per-CTA reduction of all earlier blocks (~20 dependent operator
     // levels, throughput-bound across the wave) by one scan of depth ~15 in one CTA.
@@ -482,7 +483,7 @@ __device__ __forceinline__ Gauss<D> filter_chain_carry(const KParams<D>& p, FAgg
         }
         __threadfence();
         __syncthreads();
-        if (threadIdx.x == 0) atomicExch(p.flag, p.epoch);
+        if (threadIdx.x == 0) atomicExch(p.flag, 1ull);
     }
     // ---- carry into this chain: CTA carry (x) exclusive scan of chain aggregates
     {
@@ -505,7 +506,7 @@ __device__ __forceinline__ Gauss<D> filter_chain_carry(const KParams<D>& p, FAgg
         __syncthreads();
         if (threadIdx.x == 0) {
             // wait for CTA 0's publication, then read this CTA's collapsed carry
-            while (atomicAdd(p.flag, 0ull) < p.epoch) __nanosleep(64);
+            while (atomicAdd(p.flag, 0ull) == 0ull) __nanosleep(64);
             __threadfence();
             Gauss<D> acc;
             {   // L2 loads (the carry was written by another CTA in this launch)

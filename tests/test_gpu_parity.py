@@ -521,3 +521,31 @@ def test_nll_only_all_modes(cuda_device, case):
     assert abs(float(nll_a.cpu()[0]) - float(nll_b.cpu()[0])) <= 1e-12 * abs(float(nll_a.cpu()[0]))
     o = oracle.posterior(w, smooth=False)
     assert abs(float(nll_b.cpu()[0]) - o["nll"]) <= NLL_TOL * abs(o["nll"])
+
+
+def test_cuda_graph_replay(cuda_device):
+    """pssgp_posterior captured in a CUDA graph and replayed with new data equals a direct call
+    (the K3 carry-publication flag is reset by K1 in stream order, so replays are safe)."""
+    w1 = synth.random_problem(50, 30011, kind="matern52", p_missing=0.2, variance=1.0, lengthscale=0.5,
+                              noise_var=0.01)
+    w2 = synth.random_problem(51, 30011, kind="matern52", p_missing=0.2, variance=1.0, lengthscale=0.5,
+                              noise_var=0.01)
+    m = P.Model(w1.components, w1.noise_var)
+    t, y, mk = to_dev(w1)
+    mean = torch.empty_like(t); var = torch.empty_like(t)
+    nll = torch.zeros(1, dtype=torch.float64, device="cuda:0")
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        m.posterior(t, y, mk, out=(mean, var, nll), stream=s)       # allocate the workspace
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        m.posterior(t, y, mk, out=(mean, var, nll), stream=torch.cuda.current_stream())
+    for w in (w2, w1, w2):
+        t.copy_(torch.from_numpy(w.t)); y.copy_(torch.from_numpy(w.y)); mk.copy_(torch.from_numpy(w.mask))
+        g.replay()
+        torch.cuda.synchronize()
+        ref = P.Model(w.components, w.noise_var).posterior(*to_dev(w))
+        assert torch.equal(mean, ref[0]) and torch.equal(var, ref[1]) and torch.equal(nll, ref[2])
