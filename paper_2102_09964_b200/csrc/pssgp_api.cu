@@ -267,10 +267,13 @@ pssgp_status phase_filter_reduce(pssgp_model* m, KParams<D>& p, cudaStream_t s) 
     return PSSGP_OK;
 }
 
+// sagg = false: filtered-state stores without the smoother-aggregate work (gradient primal pass)
 template <int D>
-pssgp_status phase_filter_apply(pssgp_model* m, KParams<D>& p, cudaStream_t s) {
+pssgp_status phase_filter_apply(pssgp_model* m, KParams<D>& p, cudaStream_t s, bool sagg = true) {
     ProfScope ps(m, S_K3, s);
-    if (p.store_state) LAUNCH_MODE(m, k_filter_apply, p.nb, kThreads, s, p);
+    if (p.store_state && !sagg && m->mode == kClosed)
+        k_filter_apply<D, kClosed, true, false><<<p.nb, kThreads, 0, s>>>(p);
+    else if (p.store_state) LAUNCH_MODE(m, k_filter_apply, p.nb, kThreads, s, p);
     else if (m->mode == kClosed) k_filter_apply<D, kClosed, false><<<p.nb, kThreads, 0, s>>>(p);
     else if (m->mode == kPade) k_filter_apply<D, kPade, false><<<p.nb, kThreads, 0, s>>>(p);
     else k_filter_apply<D, kTable, false><<<p.nb, kThreads, 0, s>>>(p);
@@ -349,7 +352,7 @@ pssgp_status run_grad(pssgp_model* m, int64_t N, const double* t, const double* 
     p.n = N; p.k0 = 0; p.nglob = N;
     p.store_state = 1;
     if ((st = phase_filter_reduce<D>(m, p, s))) return st;
-    if ((st = phase_filter_apply<D>(m, p, s))) return st;
+    if ((st = phase_filter_apply<D>(m, p, s, false))) return st;
     if (nll && (st = nll_sum(m, p.nll_block, p.nb, nll, s))) return st;
     // block tangent aggregates reuse the smoother-aggregate region (not read on this path)
     constexpr size_t NA = sizeof(TAgg3<D>) / sizeof(double);

@@ -535,8 +535,9 @@ __device__ __forceinline__ Gauss<D> filter_chain_carry(const KParams<D>& p, FAgg
 }
 
 // ------------------------------------------------------------------ K3: Kalman rescan
-// STORE = false (NLL only): no filtered-state stores, no smoother-aggregate moments.
-template <int D, int MODE, bool STORE = true>
+// STORE = false (NLL only): no filtered-state stores; SAGG = false: no smoother-aggregate
+// moments / aggregates (NLL only, and the gradient's primal pass which needs only the stores).
+template <int D, int MODE, bool STORE = true, bool SAGG = STORE>
 __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KParams<D> p) {
     __shared__ AsyncStage st[kWarps];
     __shared__ FAgg<D> tot[kWarps];
@@ -658,7 +659,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
                     for (int j = i; j < D; ++j) P[si(D, i, j)] = fma(-HP[i] * iS, HP[j], Pm[si(D, i, j)]);
                 // Sigma- = Sigma F^T, then the rank-one update by y_k of the
                 // cross-covariance and of the chain-entry moments
-                if (STORE) {
+                if (SAGG) {
                 double Sm[D * D], SH[D];
                 mul_bt<D>(Sg, F, Sm);
 #pragma unroll
@@ -696,7 +697,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
     if (ferr_n >= 0) raise_error(p.err, p.k0 + kb + ferr_n, kErrNumeric);
 
     // ---- chain smoother aggregate
-    if (STORE) {
+    if (SAGG) {
         SAgg<D> sag;
         set_identity(sag);
         if (ke > kb) {
@@ -748,7 +749,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
         double s2 = 0.0;
         for (int w = 0; w < kWarps; ++w) s2 += nred[w];
         p.nll_block[blockIdx.x] = s2;
-        if (STORE) {
+        if (SAGG) {
             SAgg<D> acc = stot[0];
             for (int w = 1; w < kWarps; ++w) {
                 SAgg<D> r;
