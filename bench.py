@@ -80,7 +80,7 @@ def parse():
     ap.add_argument("--N", type=int, default=2 ** 24)
     ap.add_argument("--uniform", action="store_true", help="uniform dt (secondary row)")
     ap.add_argument("--kind", default="matern52")
-    ap.add_argument("--config", default="metric", choices=["metric", "c2", "c3", "c4", "c5", "batched", "grad"],
+    ap.add_argument("--config", default="metric", choices=["metric", "c2", "c3", "c4", "c5", "batched", "grad", "gradb"],
                     help="workload (default: the BASELINE metric); c3/c4 are the d = 6 / d = 16 rows")
     ap.add_argument("--irregular", action="store_true", help="c3/c4 on a jittered grid (device Pade discretisation)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -169,7 +169,7 @@ def make_workload(args):
         return synth.config4(n=args.N, irregular=args.irregular)
     if args.config == "c5":
         return synth.metric_workload(2 ** 27 if args.N == 2 ** 24 else args.N)
-    if args.config == "batched":
+    if args.config in ("batched", "gradb"):
         return synth.metric_workload(3200 * 4, kind="matern52")
     if args.config == "grad":
         return synth.metric_workload(args.N)
@@ -229,7 +229,7 @@ def main():
     N = w.N
     stream = torch.cuda.current_stream()
 
-    if args.config == "batched":
+    if args.config in ("batched", "gradb"):
         # f2: B series of 3,200 points (the sunspot N of PAPER.md:206), each with its own
         # hyper-parameters (multi-start / HMC shape), one launch
         # multi-GPU: every rank runs its own batch of independent series (replicas, no collective)
@@ -246,9 +246,15 @@ def main():
         mean = torch.empty(N, dtype=torch.float64, device=dev)
         var = torch.empty_like(mean)
         nllb = torch.empty(B, dtype=torch.float64, device=dev)
+        gb = torch.empty(3 * B, dtype=torch.float64, device=dev)
 
-        def step():
-            P.pssgp_posterior_batched(model.h, B, off, VB, EB, RB, N, t, y, mk, mean, var, nllb, stream)
+        if args.config == "batched":
+            def step():
+                P.pssgp_posterior_batched(model.h, B, off, VB, EB, RB, N, t, y, mk, mean, var, nllb, stream)
+        else:
+            # f1 x f2: per-series NLL + gradient (one multi-start / HMC evaluation of B fits)
+            def step():
+                P.pssgp_nll_grad_batched(model.h, B, off, VB, EB, RB, N, t, y, mk, nllb, gb, stream)
         n_local = N
     elif args.config == "grad":
         # f1: NLL + d NLL / d (log s2, log ell, log r) on the metric grid (one L-BFGS / HMC evaluation)
@@ -318,13 +324,13 @@ def main():
     ms_step = ms_total / args.steps
     # independent problems per rank (batched series, gradient evaluations): weak scaling, the
     # job's units are all ranks' steps; the time-sharded posterior: strong scaling over one grid
-    replicas = args.config in ("batched", "grad") and world > 1
+    replicas = args.config in ("batched", "grad", "gradb") and world > 1
     units = N * world if replicas else N
     value = units / (ms_step * 1e-3)
 
     # ---- e2e through the public host API (pinned buffers, copies inside the timed region)
     e2e = None
-    if world == 1 and args.config not in ("batched", "grad"):
+    if world == 1 and args.config not in ("batched", "grad", "gradb"):
         th = torch.from_numpy(w.t).pin_memory()
         yh = torch.from_numpy(w.y).pin_memory()
         mh = torch.from_numpy(w.mask).pin_memory()
@@ -416,6 +422,8 @@ def main():
         metric = METRIC
     elif args.config == "grad":
         metric = f"time-steps/s (NLL + 3-parameter gradient, fp64) {w.name} N={N}"
+    elif args.config == "gradb":
+        metric = f"time-steps/s (per-series NLL + gradient, fp64) batched Matern-5/2 series of 3200 N={N}"
     else:
         metric = (f"time-steps/s (filter+smoother+NLL, fp64) "
                   f"{w.name if args.config != 'batched' else 'batched Matern-5/2 series of 3200'} N={N}")

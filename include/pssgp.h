@@ -185,6 +185,17 @@ pssgp_status pssgp_posterior_batched(pssgp_model* m, int nseg, const int64_t* of
                                      const double* t, const double* y, const uint8_t* mask, double* mean,
                                      double* var, double* nll, void* stream);
 
+/* Batched NLL + gradient (NEXT rows f1 x f2: the paper's multi-start / HMC workloads,
+ * PAPER.md:206-209, 224): the series and per-series hyper-parameters of
+ * pssgp_posterior_batched; outputs nll[nseg] and grad[3 nseg] (device; grad[3b..3b+2] =
+ * d NLL_b / d (log sigma_b^2, log ell_b, log sigma_n,b^2)).  The tangent aggregates restart
+ * at every series start; series spanning several chains are composed from per-chain pieces
+ * (pssgp_grad.cuh).  Only single-component Matern models -> else PSSGP_E_UNSUPPORTED. */
+pssgp_status pssgp_nll_grad_batched(pssgp_model* m, int nseg, const int64_t* offsets, const double* variance,
+                                    const double* lengthscale, const double* noise_var, int64_t N,
+                                    const double* t, const double* y, const uint8_t* mask, double* nll,
+                                    double* grad, void* stream);
+
 /* Synchronise the handle's last stream and return the first device-detected
  * error (PSSGP_E_INPUT / PSSGP_E_NUMERIC / PSSGP_E_UNSUPPORTED) since the last
  * pssgp_check, or PSSGP_OK.  Clears the latched error. */

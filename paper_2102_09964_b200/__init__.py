@@ -25,7 +25,7 @@ __all__ = ["Model", "PssgpError", "build", "lib", "pssgp_create", "pssgp_destroy
            "pssgp_state_dim", "pssgp_get_ssm", "pssgp_debug_discretize", "pssgp_plan",
            "pssgp_aggregate_bytes", "pssgp_shard_filter_reduce", "pssgp_shard_filter_apply",
            "pssgp_shard_smoother_apply", "pssgp_profile_enable", "pssgp_profile_read", "pssgp_profile_name",
-           "pssgp_merge_grid", "pssgp_gather", "pssgp_predict", "pssgp_posterior_batched"]
+           "pssgp_merge_grid", "pssgp_gather", "pssgp_predict", "pssgp_posterior_batched", "pssgp_nll_grad_batched"]
 
 
 def _ptr(x) -> Optional[int]:
@@ -141,6 +141,13 @@ def pssgp_posterior_batched(h, nseg, offsets, variance, lengthscale, noise_var, 
     _raise(h, lib().pssgp_posterior_batched(h, int(nseg), _ptr(offsets), _ptr(variance), _ptr(lengthscale),
                                             _ptr(noise_var), int(N), _ptr(t), _ptr(y), _ptr(mask), _ptr(mean),
                                             _ptr(var), _ptr(nll), _stream_ptr(stream)))
+
+
+def pssgp_nll_grad_batched(h, nseg, offsets, variance, lengthscale, noise_var, N, t, y, mask, nll, grad,
+                           stream=None) -> None:
+    _raise(h, lib().pssgp_nll_grad_batched(h, int(nseg), _ptr(offsets), _ptr(variance), _ptr(lengthscale),
+                                           _ptr(noise_var), int(N), _ptr(t), _ptr(y), _ptr(mask), _ptr(nll),
+                                           _ptr(grad), _stream_ptr(stream)))
 
 
 def pssgp_check(h) -> None:

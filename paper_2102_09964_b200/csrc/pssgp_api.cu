@@ -63,6 +63,8 @@ struct pssgp_model {
     size_t mg_bytes = 0;
     double* bt = nullptr;                 // batched: per-step NLL terms
     size_t bt_bytes = 0;
+    double* gb = nullptr;                 // batched gradient: head / tail tangent pieces per chain
+    size_t gb_bytes = 0;
     double* fq = nullptr;                 // wide path, kPade mode: per-step (F, Q)
     size_t fq_bytes = 0;
     // pipelined host API (pssgp_posterior_host_async): two slots, each with its own stream and
@@ -822,6 +824,7 @@ void pssgp_destroy(pssgp_model* m) {
     if (m->mg) cudaFree(m->mg);
     if (m->bt) cudaFree(m->bt);
     if (m->fq) cudaFree(m->fq);
+    if (m->gb) cudaFree(m->gb);
     for (int i = 0; i < 2; ++i) {
         if (m->aio[i]) cudaFree(m->aio[i]);
         if (m->astream[i]) cudaStreamDestroy(m->astream[i]);
@@ -993,6 +996,88 @@ pssgp_status pssgp_posterior_batched(pssgp_model* m, int nseg, const int64_t* of
         }
     } else {
         cudaMemsetAsync(m->bt, 0, sizeof(double), s);
+    }
+    {
+        ProfScope ps(m, S_K6, s);
+        pssgp::batch::k_batch_nll<<<(nseg + 3) / 4, 128, 0, s>>>(q);
+    }
+    LAUNCH_CHECK(m, "k_batch_nll");
+    return PSSGP_OK;
+}
+
+pssgp_status pssgp_nll_grad_batched(pssgp_model* m, int nseg, const int64_t* offsets, const double* variance,
+                                    const double* lengthscale, const double* noise_var, int64_t N, const double* t,
+                                    const double* y, const uint8_t* mask, double* nll, double* grad, void* stream) {
+    pssgp_status st = check_args(m, N, t, y, mask);
+    if (st) return st;
+    if (nseg < 1 || !offsets || !nll || !grad) return fail(m, PSSGP_E_ARG, "bad batched-gradient arguments");
+    if (!m->closed || m->d > kMaxD)
+        return fail(m, PSSGP_E_UNSUPPORTED, "batched gradient needs a single closed-form Matern model");
+    if ((st = ensure_device(m))) return st;
+    auto s = static_cast<cudaStream_t>(stream);
+    m->last_stream = s;
+    const size_t need = static_cast<size_t>(std::max<int64_t>(N, 1)) * sizeof(double);
+    if (need > m->bt_bytes) {
+        if (m->bt) cudaFree(m->bt);
+        m->bt = nullptr;
+        m->bt_bytes = 0;
+        if (cudaMalloc(&m->bt, need) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(m, PSSGP_E_NOMEM, "cudaMalloc(batched)");
+        }
+        m->bt_bytes = need;
+    }
+    pssgp::batch::BParams q;
+    q.off = offsets;
+    q.nseg = nseg;
+    q.var = variance;
+    q.ell = lengthscale;
+    q.noise = noise_var;
+    q.sqrt2nu = std::sqrt(2.0 * m->d - 1.0);
+    q.nll_step = m->bt;
+    q.nll_seg = nll;
+    pssgp::batch::k_batch_check_offsets<<<(nseg + 256) / 256, 256, 0, s>>>(offsets, nseg, N, m->d_err);
+    LAUNCH_CHECK(m, "k_batch_check_offsets");
+    if (N == 0) {
+        cudaMemsetAsync(nll, 0, nseg * sizeof(double), s);
+        cudaMemsetAsync(grad, 0, 3 * nseg * sizeof(double), s);
+        return PSSGP_OK;
+    }
+    switch (m->d) {
+#define BGRAD_RUN(DD)                                                                                      \
+    case DD: {                                                                                             \
+        const Plan pl = make_plan<DD>(m, N);                                                               \
+        KParams<DD> p;                                                                                     \
+        if ((st = setup<DD>(m, pl, p))) return st;                                                         \
+        p.t = t; p.y = y; p.mask = mask; p.n = N; p.k0 = 0; p.nglob = N;                                   \
+        const size_t nchp = static_cast<size_t>(pl.nb) * kThreads;                                        \
+        const size_t na = sizeof(TAgg3<DD>) / sizeof(double);                                             \
+        const size_t gneed = 2 * nchp * na * sizeof(double);                                               \
+        if (gneed > m->gb_bytes) {                                                                         \
+            if (m->gb) cudaFree(m->gb);                                                                    \
+            m->gb = nullptr;                                                                               \
+            m->gb_bytes = 0;                                                                               \
+            if (cudaMalloc(&m->gb, gneed) != cudaSuccess) {                                                \
+                cudaGetLastError();                                                                        \
+                return fail(m, PSSGP_E_NOMEM, "cudaMalloc(batched gradient)");                             \
+            }                                                                                              \
+            m->gb_bytes = gneed;                                                                           \
+        }                                                                                                  \
+        double* head = m->gb;                                                                              \
+        double* tail = m->gb + nchp * na;                                                                  \
+        { ProfScope ps(m, S_K1, s); pssgp::batch::k_batch_filter_reduce<DD><<<pl.nb, kThreads, 0, s>>>(p, q); } \
+        LAUNCH_CHECK(m, "k_batch_filter_reduce");                                                          \
+        { ProfScope ps(m, S_K3, s); pssgp::batch::k_batch_filter_apply<DD><<<pl.nb, kThreads, 0, s>>>(p, q); } \
+        LAUNCH_CHECK(m, "k_batch_filter_apply");                                                           \
+        { ProfScope ps(m, S_GRAD, s); k_batch_grad_fold<DD><<<pl.nb, kThreads, 0, s>>>(p, q, head, tail, grad); } \
+        LAUNCH_CHECK(m, "k_batch_grad_fold");                                                              \
+        { ProfScope ps(m, S_RED, s); k_batch_grad_combine<DD><<<(nseg + 127) / 128, 128, 0, s>>>(q, pl.K, head, tail, grad); } \
+        LAUNCH_CHECK(m, "k_batch_grad_combine");                                                           \
+        break;                                                                                             \
+    }
+        BGRAD_RUN(1) BGRAD_RUN(2) BGRAD_RUN(3)
+#undef BGRAD_RUN
+        default: return fail(m, PSSGP_E_UNSUPPORTED, "state dimension");
     }
     {
         ProfScope ps(m, S_K6, s);

@@ -26,6 +26,7 @@
 // so theta_ell = log ell gives dz = -z; P_inf = sigma^2 P1 does not depend on ell.
 #pragma once
 #include "pssgp_kernels.cuh"
+#include "pssgp_batch.cuh"
 
 namespace pssgp {
 
@@ -416,6 +417,115 @@ __global__ void __launch_bounds__(kThreads, 2) k_grad_fold(const KParams<D> p, d
         }
         store_aos(acc, block_out + static_cast<int64_t>(blockIdx.x) * (sizeof(TAgg3<D>) / sizeof(double)));
     }
+}
+
+// ------------------------------------------------------------------ batched gradient (f1 x f2)
+// B independent series with their own (sigma_b^2, ell_b, sigma_n,b^2): the tangent aggregate
+// restarts at every series start (that element has F = 0, so nothing may leak across), a series
+// that lies inside one chain is finished in the fold, and a series spanning chains c1..c2 is the
+// ordered product  tail(c1) o head(c1+1) o ... o head(c2)  of the pieces the fold stores (head =
+// chain start .. first series end in the chain, or the whole chain; tail = last series start in
+// the chain .. chain end), composed by k_batch_grad_combine (one thread per series).
+template <int D>
+__global__ void __launch_bounds__(kThreads, 2) k_batch_grad_fold(const KParams<D> p, const batch::BParams q,
+                                                                 double* head, double* tail, double* grad_seg) {
+    constexpr int NA = sizeof(TAgg3<D>) / sizeof(double);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t c = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
+    const int64_t wg = static_cast<int64_t>(blockIdx.x) * kWarps + wid;
+    const int64_t kb = c * p.K;
+    const int64_t ke = min(kb + p.K, p.n);
+    if (kb >= ke) return;
+    batch::Seg s;
+    batch::seg_load(s, p, q, batch::seg_find(q, kb));
+    ModelParams<D> mp = p.m;
+    TAgg3<D> A;
+    set_identity(A);
+    double x[D], P[ns(D)];
+#pragma unroll
+    for (int i = 0; i < D; ++i) x[i] = 0.0;
+#pragma unroll
+    for (int i = 0; i < ns(D); ++i) P[i] = 0.0;
+    double tprev = 0.0;
+    if (kb > 0) {
+        const int64_t cp = c - 1;
+        const double* src = p.xp + (((cp / 32) * p.K + (p.K - 1)) * CN(D)) * 32 + (cp % 32);
+#pragma unroll
+        for (int i = 0; i < D; ++i) x[i] = src[i * 32];
+#pragma unroll
+        for (int i = 0; i < ns(D); ++i) P[i] = src[(D + i) * 32];
+        tprev = __ldg(p.t + kb - 1);
+    }
+    bool head_done = false;
+    const double* xpw = p.xp + (wg * p.K * CN(D)) * 32 + lane;
+#pragma unroll 1
+    for (int64_t k = kb; k < ke; ++k) {
+        while (k >= s.end) batch::seg_load(s, p, q, s.b + 1);
+        const double tk = __ldg(p.t + k);
+        const bool obs = __ldg(p.mask + k) != 0;
+        const double yk = obs ? __ldg(p.y + k) : 0.0;
+        const bool first = (k == s.start);
+        FJor<D> Fj;
+        double Q[ns(D)];
+        double z = 0.0;
+        if (first) {
+            set_identity(A);                      // a new series: nothing carries over
+            set_zero(Fj);
+#pragma unroll
+            for (int i = 0; i < ns(D); ++i) Q[i] = p.m.Pinf[i] * s.pscale;
+        } else {
+            z = s.lam * (tk - tprev);
+            matern_closed<D>(s.lam, s.s2, tk - tprev, Fj, Q);
+        }
+        mp.r = s.r;
+        mp.s2 = s.s2;
+        grad_fold_step3<D>(A, x, P, to_full<D>(Fj), Q, z, mp, first, obs, yk);
+        tprev = tk;
+        const double* src = xpw + ((k - kb) * CN(D)) * 32;
+#pragma unroll
+        for (int i = 0; i < D; ++i) x[i] = src[i * 32];
+#pragma unroll
+        for (int i = 0; i < ns(D); ++i) P[i] = src[(D + i) * 32];
+        if (k == s.end - 1) {                     // series end inside this chain
+            if (s.start >= kb) {                  // the whole series is in this chain
+#pragma unroll
+                for (int j = 0; j < 3; ++j) grad_seg[3 * s.b + j] = A.a[j];
+            } else if (!head_done) {              // piece chain start .. series end
+                store_aos(A, head + c * NA);
+                head_done = true;
+            }
+            set_identity(A);
+        }
+    }
+    if (s.end > ke) {                             // a series continues past the chain end
+        if (s.start >= kb) store_aos(A, tail + c * NA);       // it started in this chain
+        else if (!head_done) store_aos(A, head + c * NA);     // it runs through the whole chain
+    }
+}
+
+template <int D>
+__global__ void __launch_bounds__(128) k_batch_grad_combine(const batch::BParams q, int64_t K, const double* head,
+                                                            const double* tail, double* grad_seg) {
+    constexpr int NA = sizeof(TAgg3<D>) / sizeof(double);
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= q.nseg) return;
+    const int64_t a0 = __ldg(q.off + b), a1 = __ldg(q.off + b + 1);
+    if (a1 <= a0) {
+        grad_seg[3 * b] = grad_seg[3 * b + 1] = grad_seg[3 * b + 2] = 0.0;
+        return;
+    }
+    const int64_t c1 = a0 / K, c2 = (a1 - 1) / K;
+    if (c1 == c2) return;                         // finished by the fold
+    TAgg3<D> acc;
+    load_aos(acc, tail + c1 * NA);
+    for (int64_t cc = c1 + 1; cc <= c2; ++cc) {
+        TAgg3<D> h, r;
+        load_aos(h, head + cc * NA);
+        combine(acc, h, r);
+        acc = r;
+    }
+#pragma unroll
+    for (int j = 0; j < 3; ++j) grad_seg[3 * b + j] = acc.a[j];
 }
 
 }  // namespace pssgp

@@ -97,3 +97,78 @@ def test_grad_unsupported_model(cuda_device):
     t, y, mk = (torch.from_numpy(a[:64]).to("cuda:0") for a in (w.t, w.y, w.mask))
     with pytest.raises(P.PssgpError):
         m.nll_grad(t, y, mk)
+
+
+def _batched_problem(kind, lens, seed=31):
+    rng = np.random.default_rng(seed)
+    ws = []
+    for b, n in enumerate(lens):
+        ws.append(synth.random_problem(200 + b, n, kind=kind, p_missing=0.2, ties=min(2, n // 10),
+                                       lengthscale=float(rng.uniform(0.2, 2.0)), variance=float(rng.uniform(0.5, 3.0)),
+                                       noise_var=float(rng.uniform(0.01, 0.3))) if n > 0 else None)
+    return ws
+
+
+@pytest.mark.parametrize("kind", ["matern12", "matern32", "matern52"])
+@pytest.mark.parametrize("chain_len", [1, 7, 64, 4096])
+def test_grad_batched(cuda_device, kind, chain_len):
+    """NEXT rows f1 x f2: per-series NLL and gradient w.r.t. each series' own
+    (log sigma_b^2, log ell_b, log sigma_n,b^2), one launch sequence for all series
+    (empty, 1-point, in-chain and chain-spanning series), each against the complex-step
+    oracle on that series alone."""
+    lens = [0, 1, 2, 37, 3200, 0, 5000, 777, 1, 9000, 300]
+    ws = _batched_problem(kind, lens)
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    cat = lambda f, dt: np.concatenate([f(w) if w is not None else np.zeros(0, dt) for w in ws])  # noqa: E731
+    t = cat(lambda w: w.t, np.float64); y = cat(lambda w: w.y, np.float64); mk = cat(lambda w: w.mask, np.uint8)
+    var_b = np.array([w.components[0].variance if w else 1.0 for w in ws])
+    ell_b = np.array([w.components[0].lengthscale if w else 1.0 for w in ws])
+    r_b = np.array([w.noise_var if w else 0.1 for w in ws])
+    m = P.Model([synth.Component(kind, 1.0, 1.0)], 0.1, chain_len=chain_len)
+    dev = "cuda:0"
+    T, Y, MK = (torch.from_numpy(a).to(dev) for a in (t, y, mk))
+    OFF, VB, EB, RB = (torch.from_numpy(a).to(dev) for a in (off, var_b, ell_b, r_b))
+    B = len(lens)
+    nll = torch.empty(B, dtype=torch.float64, device=dev)
+    g = torch.empty(3 * B, dtype=torch.float64, device=dev)
+    P.pssgp_nll_grad_batched(m.h, B, OFF, VB, EB, RB, t.shape[0], T, Y, MK, nll, g)
+    m.check()
+    nll, g = nll.cpu().numpy(), g.cpu().numpy().reshape(B, 3)
+    for b, w in enumerate(ws):
+        if w is None:
+            assert nll[b] == 0.0 and np.all(g[b] == 0.0)
+            continue
+        c = w.components[0]
+        nll_r, g_r = og.kf_nll_grad(c.kind, c.variance, c.lengthscale, w.noise_var, w.t, w.y, w.mask)
+        nobs = int(w.mask.sum())
+        assert abs(nll[b] - nll_r) <= NLL_TOL * max(abs(nll_r), 1.0), (b, nll[b], nll_r)
+        err = np.abs(g[b] - g_r) / (np.abs(g_r) + nobs + 1)
+        assert np.all(err <= GRAD_TOL), (b, g[b], g_r, err)
+
+
+def test_grad_batched_single_series_equals_nll_grad(cuda_device):
+    """One series with the model's own hyper-parameters (null per-series arrays) gives
+    exactly the single-series entry point's result."""
+    w = synth.random_problem(8, 30011, kind="matern52", p_missing=0.15, ties=3)
+    m = P.Model(w.components, w.noise_var)
+    dev = "cuda:0"
+    t, y, mk = (torch.from_numpy(a).to(dev) for a in (w.t, w.y, w.mask))
+    nll1, g1 = m.nll_grad(t, y, mk)
+    off = torch.tensor([0, w.t.shape[0]], dtype=torch.int64, device=dev)
+    nll = torch.empty(1, dtype=torch.float64, device=dev)
+    g = torch.empty(3, dtype=torch.float64, device=dev)
+    P.pssgp_nll_grad_batched(m.h, 1, off, None, None, None, w.t.shape[0], t, y, mk, nll, g)
+    m.check()
+    assert abs(float(nll.cpu()[0]) - float(nll1.cpu()[0])) <= 1e-12 * abs(float(nll1.cpu()[0]))
+    np.testing.assert_allclose(g.cpu().numpy(), g1.cpu().numpy(), rtol=1e-11, atol=1e-9)
+
+
+def test_grad_batched_unsupported_model(cuda_device):
+    w = synth.config3()
+    m = P.Model(w.components, w.noise_var, uniform_dt=w.uniform_dt)
+    n = 64
+    t, y, mk = (torch.from_numpy(a[:n]).to("cuda:0") for a in (w.t, w.y, w.mask))
+    off = torch.tensor([0, n], dtype=torch.int64, device="cuda:0")
+    out = torch.empty(3, dtype=torch.float64, device="cuda:0")
+    with pytest.raises(P.PssgpError):
+        P.pssgp_nll_grad_batched(m.h, 1, off, None, None, None, n, t, y, mk, out[:1], out)
