@@ -32,6 +32,8 @@ sys.path.insert(0, ROOT)
 METRIC = "time-steps/s (filter+smoother+NLL, fp64) Matern-5/2 N=2^24"
 UNIT = "time-steps/s"
 # algorithmic bytes per time step moved by each kernel at d = 3 (DESIGN.md §6 "Roofline")
+# fp32-state path: t, y, mask in fp64 / u8, filtered state 9 floats (36 B), outputs fp64
+ALG_BYTES_F32 = {"k_filter_reduce": 17, "k_filter_apply": 17 + 36, "k_smoother_apply": 8 + 36 + 16}
 ALG_BYTES = {"k_filter_reduce": 17, "k_filter_apply": 17 + 72, "k_smoother_apply": 8 + 72 + 16,
              "k_grad_fold": 17 + 72}
 # fallback fp64 flops per time step (DFMA = 2) if the committed profile has no SASS counts;
@@ -80,7 +82,7 @@ def parse():
     ap.add_argument("--N", type=int, default=2 ** 24)
     ap.add_argument("--uniform", action="store_true", help="uniform dt (secondary row)")
     ap.add_argument("--kind", default="matern52")
-    ap.add_argument("--config", default="metric", choices=["metric", "c2", "c3", "c4", "c5", "batched", "grad", "gradb"],
+    ap.add_argument("--config", default="metric", choices=["metric", "c2", "c3", "c4", "c5", "batched", "grad", "gradb", "f32"],
                     help="workload (default: the BASELINE metric); c3/c4 are the d = 6 / d = 16 rows")
     ap.add_argument("--irregular", action="store_true", help="c3/c4 on a jittered grid (device Pade discretisation)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -167,6 +169,8 @@ def make_workload(args):
         return synth.config3(n=args.N if args.N != 2 ** 24 else 2 ** 22, irregular=args.irregular)
     if args.config == "c4":
         return synth.config4(n=args.N, irregular=args.irregular)
+    if args.config == "f32":
+        return synth.metric_workload(args.N)
     if args.config == "c5":
         return synth.metric_workload(2 ** 27 if args.N == 2 ** 24 else args.N)
     if args.config in ("batched", "gradb"):
@@ -267,6 +271,18 @@ def main():
         def step():
             P.pssgp_nll_grad(model.h, N, t, y, mk, nll, gr, stream)
         n_local = N
+    elif args.config == "f32" and world == 1:
+        # the optional fp32-state path on the metric workload
+        t = torch.from_numpy(w.t).to(dev)
+        y = torch.from_numpy(w.y).to(dev)
+        mk = torch.from_numpy(w.mask).to(dev)
+        mean = torch.empty(N, dtype=torch.float64, device=dev)
+        var = torch.empty_like(mean)
+        nll = torch.zeros(1, dtype=torch.float64, device=dev)
+
+        def step():
+            P.pssgp_posterior_f32(model.h, N, t, y, mk, mean, var, nll, stream)
+        n_local = N
     elif world == 1:
         t = torch.from_numpy(w.t).to(dev)
         y = torch.from_numpy(w.y).to(dev)
@@ -330,7 +346,7 @@ def main():
 
     # ---- e2e through the public host API (pinned buffers, copies inside the timed region)
     e2e = None
-    if world == 1 and args.config not in ("batched", "grad", "gradb"):
+    if world == 1 and args.config not in ("batched", "grad", "gradb", "f32"):
         th = torch.from_numpy(w.t).pin_memory()
         yh = torch.from_numpy(w.y).pin_memory()
         mh = torch.from_numpy(w.mask).pin_memory()
@@ -379,7 +395,7 @@ def main():
     dom = max(kern, key=lambda k: kern[k][0])
     dom_ms, dom_launches = kern[dom]
     per_launch_ms = dom_ms / dom_launches
-    alg_b = ALG_BYTES.get(dom, 0) * n_local
+    alg_b = (ALG_BYTES_F32 if args.config == "f32" else ALG_BYTES).get(dom, 0) * n_local
     hbm_gbs = alg_b / (per_launch_ms * 1e-3) / 1e9
     fps = {k: flops_per_step(k) for k in ("k_filter_reduce", "k_filter_apply", "k_smoother_apply")}
     flops = (fps.get(dom, 0.0) * n_local
@@ -403,6 +419,7 @@ def main():
         roof = {"bound": "hbm", "kernel": dom, "achieved": hbm_gbs, "peak": pk.get("hbm_gbs"), "unit": "GB/s",
                 "frac": hbm_frac, "traffic": traffic}
     roof["alu"] = alu
+    path_b = 41 + 8 * 9 if args.config == "f32" else 41 + 16 * 9
     roof.update({
         "traffic_source": traffic_src,
         "alg_bytes_per_launch": alg_b,
@@ -411,8 +428,8 @@ def main():
         "avg_launch_ms": per_launch_ms,
         "share_of_step": dom_ms / ms_total,
         "per_kernel_ms_per_step": {k: v[0] / args.steps for k, v in kern.items()},
-        "path_alg_bytes_per_step": 41 + 16 * 9,
-        "path_hbm_frac": (41 + 16 * 9) * N / (ms_step * 1e-3) / 1e9 / pk.get("hbm_gbs"),
+        "path_alg_bytes_per_step": path_b,
+        "path_hbm_frac": path_b * N / (ms_step * 1e-3) / 1e9 / pk.get("hbm_gbs"),
         "path_fp64_frac": (sum(fps.values()) * N / (ms_step * 1e-3) / 1e12 / FP64_PEAK_TFLOPS)
         if flops else None})
     cpu = None
@@ -422,6 +439,8 @@ def main():
         metric = METRIC
     elif args.config == "grad":
         metric = f"time-steps/s (NLL + 3-parameter gradient, fp64) {w.name} N={N}"
+    elif args.config == "f32":
+        metric = f"time-steps/s (filter+smoother+NLL, fp32 state) {w.name} N={N}"
     elif args.config == "gradb":
         metric = f"time-steps/s (per-series NLL + gradient, fp64) batched Matern-5/2 series of 3200 N={N}"
     else:
@@ -444,7 +463,8 @@ def main():
         extra["latency_n3200_ms"] = a0.elapsed_time(a1) / 200
     line = {"metric": metric, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "weak" if replicas else "strong", "vs_baseline": None, "dtype": "f64",
+            "scaling": "weak" if replicas else "strong", "vs_baseline": None,
+            "dtype": "f32 (state; f64 times, I/O, NLL sum)" if args.config == "f32" else "f64",
             "data": "synthetic",
             "config": {"workload": w.name, "N": N, "state_dim": model.state_dim, "chain_len": plan["chain_len"],
                        "ctas": plan["n_blocks"], "threads_per_cta": plan["threads"],

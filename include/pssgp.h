@@ -128,6 +128,18 @@ pssgp_status pssgp_posterior(pssgp_model* m, int64_t N, const double* t, const d
 pssgp_status pssgp_nll(pssgp_model* m, int64_t N, const double* t, const double* y,
                        const uint8_t* mask, double* nll, void* stream);
 
+/* Optional fp32 path (north_star "an optional fp32 path must match to 1e-3"):
+ * the same filter / smoother / NLL as pssgp_posterior (Prop. 1-2) with
+ * the state algebra (moments, aggregates, F, Q) and the filtered state in HBM in fp32.  Times,
+ * observations, mean / var outputs and the NLL accumulation stay fp64 (fp32 ulp at t ~ 2048
+ * exceeds the step).  Same arguments, layout, ownership and stream semantics as
+ * pssgp_posterior; mean and var may both be NULL (NLL only: no filtered state stored, no
+ * smoother).  Accuracy ~1e-4 relative on the Matern workloads (tests/test_gpu_f32.py, bar 1e-3).
+ * Single Matern components only (fp32 misses 1e-3 for the d = 16 sum)
+ * -> else PSSGP_E_UNSUPPORTED. */
+pssgp_status pssgp_posterior_f32(pssgp_model* m, int64_t N, const double* t, const double* y,
+                                 const uint8_t* mask, double* mean, double* var, double* nll, void* stream);
+
 /* NLL and its exact gradient with respect to theta = (log sigma^2, log ell,
  * log sigma_n^2) of a SINGLE-component Matern model (the hyper-parameter
  * gradient the paper obtains by automatic differentiation, PAPER.md:77, 157,

@@ -25,7 +25,8 @@ __all__ = ["Model", "PssgpError", "build", "lib", "pssgp_create", "pssgp_destroy
            "pssgp_state_dim", "pssgp_get_ssm", "pssgp_debug_discretize", "pssgp_plan",
            "pssgp_aggregate_bytes", "pssgp_shard_filter_reduce", "pssgp_shard_filter_apply",
            "pssgp_shard_smoother_apply", "pssgp_profile_enable", "pssgp_profile_read", "pssgp_profile_name",
-           "pssgp_merge_grid", "pssgp_gather", "pssgp_predict", "pssgp_posterior_batched", "pssgp_nll_grad_batched"]
+           "pssgp_merge_grid", "pssgp_gather", "pssgp_predict", "pssgp_posterior_batched", "pssgp_nll_grad_batched",
+           "pssgp_posterior_f32"]
 
 
 def _ptr(x) -> Optional[int]:
@@ -81,6 +82,11 @@ def pssgp_state_dim(h: int) -> int:
 def pssgp_posterior(h, N, t, y, mask, mean, var, nll, stream=None) -> None:
     _raise(h, lib().pssgp_posterior(h, int(N), _ptr(t), _ptr(y), _ptr(mask), _ptr(mean), _ptr(var), _ptr(nll),
                                     _stream_ptr(stream)))
+
+
+def pssgp_posterior_f32(h, N, t, y, mask, mean, var, nll, stream=None) -> None:
+    _raise(h, lib().pssgp_posterior_f32(h, int(N), _ptr(t), _ptr(y), _ptr(mask), _ptr(mean), _ptr(var),
+                                        _ptr(nll), _stream_ptr(stream)))
 
 
 def pssgp_nll(h, N, t, y, mask, nll, stream=None) -> None:
@@ -259,6 +265,19 @@ class Model:
         else:
             mean, var, nll = out
         pssgp_posterior(self.h, N, t, y, mask, mean, var, nll, stream)
+        return mean, var, nll
+
+    def posterior_f32(self, t, y, mask, out=None, stream=None, with_nll: bool = True):
+        """The optional fp32-state path (single Matern components): same outputs as posterior()."""
+        import torch
+        N = int(t.shape[0])
+        if out is None:
+            mean = torch.empty(N, dtype=torch.float64, device=t.device)
+            var = torch.empty_like(mean)
+            nll = torch.zeros(1, dtype=torch.float64, device=t.device) if with_nll else None
+        else:
+            mean, var, nll = out
+        pssgp_posterior_f32(self.h, N, t, y, mask, mean, var, nll, stream)
         return mean, var, nll
 
     def nll(self, t, y, mask, out=None, stream=None):

@@ -30,7 +30,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     newest = max(os.path.getmtime(f) for f in srcs + [HEADER])
     if not force and os.path.exists(LIB_PATH) and os.path.getmtime(LIB_PATH) >= newest:
         return LIB_PATH
-    cmd = ["nvcc", *NVCC_FLAGS, "-o", LIB_PATH, os.path.join(CSRC, "pssgp_api.cu")]
+    cmd = ["nvcc", *NVCC_FLAGS, "-o", LIB_PATH, os.path.join(CSRC, "pssgp_api.cu"), os.path.join(CSRC, "pssgp_f32.cu")]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if verbose or res.returncode != 0:
         print(res.stdout, res.stderr)
@@ -71,6 +71,7 @@ SIGNATURES = {
     "pssgp_posterior": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pssgp_nll": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _vp, _vp]),
     "pssgp_nll_grad": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "pssgp_posterior_f32": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pssgp_posterior_host": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pssgp_check": (ctypes.c_int, [_vp]),
     "pssgp_posterior_host_async": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),

@@ -16,6 +16,7 @@
 #include "pssgp_wide.cuh"
 #include "pssgp_batch.cuh"
 #include "pssgp_grad.cuh"
+#include "pssgp_f32.h"
 
 using namespace pssgp;
 namespace ph = pssgp_host;
@@ -50,6 +51,7 @@ struct pssgp_model {
     int blocks_per_sm = 0;
     int sm_count = 0;
     int occ = 0;
+    int occ32 = 0;               // fp32 build (pssgp_posterior_f32): resident CTAs / SM
     // workspace
     char* ws = nullptr;
     size_t ws_bytes = 0;
@@ -862,6 +864,83 @@ pssgp_status pssgp_nll(pssgp_model* m, int64_t N, const double* t, const double*
     m->last_stream = s;
     if (m->d > kMaxD) return wide_posterior_dispatch(m, N, t, y, mask, nullptr, nullptr, nll, s, false);
     DISPATCH_D(m, run_posterior<D_>(m, N, t, y, mask, nullptr, nullptr, nll, s, false));
+}
+
+// Optional fp32 path: the thread-per-chain kernels compiled with fp32 state
+// (pssgp_f32.cu); single Matern components only.
+pssgp_status pssgp_posterior_f32(pssgp_model* m, int64_t N, const double* t, const double* y, const uint8_t* mask,
+                                 double* mean, double* var, double* nll, void* stream) {
+    pssgp_status st = check_args(m, N, t, y, mask);
+    if (st) return st;
+    if (!m->closed || m->d > 3)
+        return fail(m, PSSGP_E_UNSUPPORTED, "the fp32 path covers single Matern components (d <= 3)");
+    if (!mean && !var && !nll) return fail(m, PSSGP_E_ARG, "no output requested");
+    if ((st = ensure_device(m))) return st;
+    auto s = static_cast<cudaStream_t>(stream);
+    m->last_stream = s;
+    if (N == 0) {
+        if (nll) {
+            cudaError_t e = cudaMemsetAsync(nll, 0, sizeof(double), s);
+            if (e != cudaSuccess) return cuda_fail(m, e, "cudaMemsetAsync");
+        }
+        return PSSGP_OK;
+    }
+    if (m->occ32 == 0) m->occ32 = pssgp_f32::occupancy(m->d);
+    const int bps = m->blocks_per_sm > 0 ? m->blocks_per_sm : m->occ32;
+    const int64_t target_chains = static_cast<int64_t>(m->sm_count) * bps * kThreads;
+    int64_t K = m->forced_K > 0 ? m->forced_K : std::max<int64_t>(kWin, (N + target_chains - 1) / target_chains);
+    if (m->forced_K <= 0) K = ((K + kWin - 1) / kWin) * kWin;
+    const int64_t nch = std::max<int64_t>(1, (N + K - 1) / K);
+    pssgp_f32::Run r;
+    std::memset(&r, 0, sizeof(r));
+    r.d = m->d;
+    r.n = N;
+    r.K = K;
+    r.nb = static_cast<int>((nch + kThreads - 1) / kThreads);
+    const size_t need = pssgp_f32::ws_bytes(m->d, K, r.nb);
+    if (need > m->ws_bytes) {
+        if (m->ws) cudaFree(m->ws);
+        m->ws = nullptr;
+        m->ws_bytes = 0;
+        if (cudaMalloc(&m->ws, need) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(m, PSSGP_E_NOMEM, "cudaMalloc(workspace) failed");
+        }
+        m->ws_bytes = need;
+    }
+    r.t = t; r.y = y; r.mask = mask;
+    r.mean = mean; r.var = var; r.nll = nll;
+    r.ws = m->ws;
+    r.err = m->d_err;
+    r.flag = m->d_err + 1;
+    r.lam = m->lam; r.s2 = m->s2; r.r = m->r;
+    switch (m->d) {
+#define F32_PINF(DD)                                              \
+    case DD: {                                                    \
+        ModelParams<DD> mp;                                       \
+        fill_params<DD>(m, mp);                                   \
+        for (int i = 0; i < ns(DD); ++i) r.Pinf[i] = mp.Pinf[i];  \
+        break;                                                    \
+    }
+        F32_PINF(1) F32_PINF(2) F32_PINF(3)
+#undef F32_PINF
+    }
+    r.stream = s;
+    const bool smooth = mean || var;
+    cudaError_t e;
+    { ProfScope ps(m, S_K1, s); e = pssgp_f32::launch(r, 1); }
+    if (e != cudaSuccess) return cuda_fail(m, e, "k_filter_reduce (fp32)");
+    { ProfScope ps(m, S_K3, s); e = pssgp_f32::launch(r, 2); }
+    if (e != cudaSuccess) return cuda_fail(m, e, "k_filter_apply (fp32)");
+    if (smooth) {
+        ProfScope ps(m, S_K5, s);
+        e = pssgp_f32::launch(r, 3);
+    } else {
+        ProfScope ps(m, S_K6, s);
+        e = pssgp_f32::launch(r, 4);
+    }
+    if (e != cudaSuccess) return cuda_fail(m, e, smooth ? "k_smoother_apply (fp32)" : "k_nll_sum (fp32)");
+    return PSSGP_OK;
 }
 
 pssgp_status pssgp_nll_grad(pssgp_model* m, int64_t N, const double* t, const double* y, const uint8_t* mask,

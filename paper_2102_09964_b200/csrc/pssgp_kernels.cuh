@@ -31,7 +31,7 @@
 
 #include "pssgp_math.cuh"
 
-namespace pssgp {
+namespace PSSGP_NS {
 
 #ifndef PSSGP_UNROLL
 #define PSSGP_UNROLL 1                  // step-loop unroll (lets ptxas interleave consecutive steps)
@@ -70,20 +70,20 @@ struct KParams {
     int64_t nglob;          // global number of steps
     int64_t K;              // chain length
     int nb;                 // CTAs of the apply kernels
-    double* chain_f;        // [FN][nb*128]  chain filter aggregates (SoA)
-    double* block_f;        // [nb][FN]
-    double* fcarry;         // [nb][CN]      global prefix entering each CTA
-    double* xp;             // filtered (xbar, P), lane-interleaved [warp][K][CN][32]
-    double* chain_s;        // [SN][nb*128]
-    double* block_s;        // [nb][SN]
-    double* scarry;         // [nb][CN]      global suffix after each CTA
+    real* chain_f;        // [FN][nb*128]  chain filter aggregates (SoA)
+    real* block_f;        // [nb][FN]
+    real* fcarry;         // [nb][CN]      global prefix entering each CTA
+    real* xp;             // filtered (xbar, P), lane-interleaved [warp][K][CN][32]
+    real* chain_s;        // [SN][nb*128]
+    real* block_s;        // [nb][SN]
+    real* scarry;         // [nb][CN]      global suffix after each CTA
     double* nll_block;      // [nb]
     double* mean;
     double* var;
-    const double* in_filt;  // sharded: all ranks' filter aggregates [world][FN] (nullable)
-    const double* in_smooth;// sharded: all ranks' smoother aggregates [world][SN] (nullable)
+    const real* in_filt;  // sharded: all ranks' filter aggregates [world][FN] (nullable)
+    const real* in_smooth;// sharded: all ranks' smoother aggregates [world][SN] (nullable)
     int rank, world;
-    double* out_agg;        // sharded: chunk aggregate output (nullable)
+    real* out_agg;        // sharded: chunk aggregate output (nullable)
     double* nll_out;        // nll scalar output (nullable)
     unsigned long long* err;
     int store_state;        // K3: write (xbar, P) and smoother aggregates (0 for NLL-only)
@@ -94,45 +94,45 @@ struct KParams {
 // ------------------------------------------------------------------ warp shuffles of aggregates
 template <typename T>
 __device__ __forceinline__ void shfl_up_all(T& dst, const T& src, int off) {
-    constexpr int n = sizeof(T) / sizeof(double);
-    const double* s = reinterpret_cast<const double*>(&src);
-    double* d = reinterpret_cast<double*>(&dst);
+    constexpr int n = sizeof(T) / sizeof(real);
+    const real* s = reinterpret_cast<const real*>(&src);
+    real* d = reinterpret_cast<real*>(&dst);
 #pragma unroll
     for (int i = 0; i < n; ++i) d[i] = __shfl_up_sync(0xffffffffu, s[i], off);
 }
 template <typename T>
 __device__ __forceinline__ void shfl_down_all(T& dst, const T& src, int off) {
-    constexpr int n = sizeof(T) / sizeof(double);
-    const double* s = reinterpret_cast<const double*>(&src);
-    double* d = reinterpret_cast<double*>(&dst);
+    constexpr int n = sizeof(T) / sizeof(real);
+    const real* s = reinterpret_cast<const real*>(&src);
+    real* d = reinterpret_cast<real*>(&dst);
 #pragma unroll
     for (int i = 0; i < n; ++i) d[i] = __shfl_down_sync(0xffffffffu, s[i], off);
 }
 template <typename T>
-__device__ __forceinline__ void load_soa(T& a, const double* base, int64_t stride, int64_t idx) {
-    constexpr int n = sizeof(T) / sizeof(double);
-    double* d = reinterpret_cast<double*>(&a);
+__device__ __forceinline__ void load_soa(T& a, const real* base, int64_t stride, int64_t idx) {
+    constexpr int n = sizeof(T) / sizeof(real);
+    real* d = reinterpret_cast<real*>(&a);
 #pragma unroll
     for (int i = 0; i < n; ++i) d[i] = base[i * stride + idx];
 }
 template <typename T>
-__device__ __forceinline__ void store_soa(const T& a, double* base, int64_t stride, int64_t idx) {
-    constexpr int n = sizeof(T) / sizeof(double);
-    const double* s = reinterpret_cast<const double*>(&a);
+__device__ __forceinline__ void store_soa(const T& a, real* base, int64_t stride, int64_t idx) {
+    constexpr int n = sizeof(T) / sizeof(real);
+    const real* s = reinterpret_cast<const real*>(&a);
 #pragma unroll
     for (int i = 0; i < n; ++i) base[i * stride + idx] = s[i];
 }
 template <typename T>
-__device__ __forceinline__ void load_aos(T& a, const double* base) {
-    constexpr int n = sizeof(T) / sizeof(double);
-    double* d = reinterpret_cast<double*>(&a);
+__device__ __forceinline__ void load_aos(T& a, const real* base) {
+    constexpr int n = sizeof(T) / sizeof(real);
+    real* d = reinterpret_cast<real*>(&a);
 #pragma unroll
     for (int i = 0; i < n; ++i) d[i] = base[i];
 }
 template <typename T>
-__device__ __forceinline__ void store_aos(const T& a, double* base) {
-    constexpr int n = sizeof(T) / sizeof(double);
-    const double* s = reinterpret_cast<const double*>(&a);
+__device__ __forceinline__ void store_aos(const T& a, real* base) {
+    constexpr int n = sizeof(T) / sizeof(real);
+    const real* s = reinterpret_cast<const real*>(&a);
 #pragma unroll
     for (int i = 0; i < n; ++i) base[i] = s[i];
 }
@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_reduce(const KP
         const double yk = obs ? __ldg(p.y + kb) : 0.0;
         const int64_t g = p.k0 + kb;
         FT_t<D, MODE> F;
-        double Q[ns(D)];
+        real Q[ns(D)];
         const double dt = tk - tprev;
         if (g == 0) {
 set_zero(F);
@@ -261,7 +261,7 @@ set_zero(F);
             const bool obs = ((mwin >> (8 * jj)) & 0xffull) != 0;
             const double yk = obs ? st[wid].y[buf][jj][lane] : 0.0;
             FT_t<D, MODE> F;
-            double Q[ns(D)];
+            real Q[ns(D)];
             const double dt = tk - tprev;
             const bool bad_u = disc<D, MODE>(p.m, dt, F, Q) != 0;
             const bool bad_i = !(dt >= 0.0) || !isfinite(tk) || (obs && !isfinite(yk));
@@ -304,15 +304,15 @@ set_zero(F);
 
 // ------------------------------------------------------------------ CTA-wide ordered reductions
 // Ordered product blocks[lo] (x) ... (x) blocks[hi-1] of aggregates (AoS, NA
-// doubles each) by one CTA of kThreads: contiguous runs per thread, ordered
+// reals each) by one CTA of kThreads: contiguous runs per thread, ordered
 // warp trees, then the warp totals in order.  Result valid in thread 0.
 // wred: shared scratch of kWarps aggregates.  Used by K3/K5 to build the
 // collapsed carry entering the CTA from the block aggregates of all earlier
 // (K3) / later (K5) CTAs: the block scan is thus spread over every SM instead
 // of a separate single-CTA kernel.
 template <typename Agg>
-__device__ __forceinline__ Agg cta_reduce_range(const double* __restrict__ blocks, int lo, int hi, Agg* wred) {
-    constexpr int NA = sizeof(Agg) / sizeof(double);
+__device__ __forceinline__ Agg cta_reduce_range(const real* __restrict__ blocks, int lo, int hi, Agg* wred) {
+    constexpr int NA = sizeof(Agg) / sizeof(real);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int cnt = max(hi - lo, 0);
     const int per = (cnt + kThreads - 1) / kThreads;
@@ -376,8 +376,8 @@ __device__ __forceinline__ double cta_sum(const double* __restrict__ parts, int 
 
 // observation-row terms of a predicted (xm, Pm): HP = Pm H^T, S = H Pm H^T + r, hx = H xm
 template <int D>
-__device__ __forceinline__ void obs_terms(const ModelParams<D>& m, const double (&xm)[D], const double (&Pm)[ns(D)],
-                                          double (&HP)[D], double& S, double& hx, bool hu_static = false) {
+__device__ __forceinline__ void obs_terms(const ModelParams<D>& m, const real (&xm)[D], const real (&Pm)[ns(D)],
+                                          real (&HP)[D], real& S, real& hx, bool hu_static = false) {
     if (hu_static || m.h_unit) {
 #pragma unroll
         for (int i = 0; i < D; ++i) HP[i] = Pm[si(D, i, 0)];
@@ -387,7 +387,7 @@ __device__ __forceinline__ void obs_terms(const ModelParams<D>& m, const double 
         S = m.r; hx = 0.0;
 #pragma unroll
         for (int i = 0; i < D; ++i) {
-            double s2 = 0.0;
+            real s2 = 0.0;
 #pragma unroll
             for (int j = 0; j < D; ++j) s2 = fma(Pm[si(D, i, j)], m.H[j], s2);
             HP[i] = s2;
@@ -510,8 +510,8 @@ __device__ __forceinline__ Gauss<D> filter_chain_carry(const KParams<D>& p, FAgg
             __threadfence();
             Gauss<D> acc;
             {   // L2 loads (the carry was written by another CTA in this launch)
-                double* d = reinterpret_cast<double*>(&acc);
-                const double* src = p.fcarry + static_cast<int64_t>(blockIdx.x) * CN(D);
+                real* d = reinterpret_cast<real*>(&acc);
+                const real* src = p.fcarry + static_cast<int64_t>(blockIdx.x) * CN(D);
 #pragma unroll
                 for (int i = 0; i < CN(D); ++i) d[i] = __ldcg(src + i);
             }
@@ -557,12 +557,12 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
     // ---- Kalman filter over the chain (supplement PAPER.md:285-315), carrying the
     // chain-entry moments E[x_k0 | y_1:k], Cov(x_k0 | y_1:k) and the cross-covariance
     // Cov(x_k0, x_k | y_1:k) for the chain's smoother aggregate.
-    double x[D], P[ns(D)];
+    real x[D], P[ns(D)];
 #pragma unroll
     for (int i = 0; i < D; ++i) x[i] = cur.x[i];
 #pragma unroll
     for (int i = 0; i < ns(D); ++i) P[i] = cur.P[i];
-    double x0[D], P0[ns(D)], Sg[D * D];
+    real x0[D], P0[ns(D)], Sg[D * D];
     double quad = 0.0, prodm = 1.0;
     long long prode = 0;
     int nobs = 0;
@@ -574,7 +574,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
         const bool obs = __ldg(p.mask + kb) != 0;
         const double yk = obs ? __ldg(p.y + kb) : 0.0;
         const int64_t g = p.k0 + kb;
-        double xm[D], Pm[ns(D)];
+        real xm[D], Pm[ns(D)];
         if (g == 0) {
 #pragma unroll
             for (int i = 0; i < D; ++i) xm[i] = 0.0;
@@ -582,17 +582,17 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
             for (int i = 0; i < ns(D); ++i) Pm[i] = p.m.Pinf[i];
         } else {
             FT_t<D, MODE> F;
-            double Q[ns(D)];
+            real Q[ns(D)];
             disc<D, MODE>(p.m, tk - tprev, F, Q);
             kf_predict_pm<D>(x, P, F, Q, xm, Pm);
         }
         tprev = tk;
-        double HP[D], S, hx;
+        real HP[D], S, hx;
         obs_terms<D>(p.m, xm, Pm, HP, S, hx, MODE == kClosed);
         if (obs && !(S > 0.0 && S < INFINITY)) raise_error(p.err, g, kErrNumeric);
-        const double iS = obs ? rcp(S) : 0.0;
-        const double v = obs ? (yk - hx) : 0.0;
-        const double vs = v * iS;
+        const real iS = obs ? rcp(S) : 0.0;
+        const real v = obs ? (static_cast<real>(yk) - hx) : real(0.0);
+        const real vs = v * iS;
 #pragma unroll
         for (int i = 0; i < D; ++i) x[i] = fma(HP[i], vs, xm[i]);
 #pragma unroll
@@ -609,7 +609,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
             for (int j = 0; j < D; ++j) Sg[i * D + j] = P[si(D, i, j)];
         nll_accumulate(obs, v, vs, S, quad, prodm, prode, nobs);
         if (STORE) {
-            double* o = p.xp + (wg * p.K * CN(D)) * 32 + lane;
+            real* o = p.xp + (wg * p.K * CN(D)) * 32 + lane;
 #pragma unroll
             for (int i = 0; i < D; ++i) o[i * 32] = x[i];
 #pragma unroll
@@ -639,18 +639,18 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
                 const bool obs = ((mwin >> (8 * jj)) & 0xffull) != 0;
                 const double yk = obs ? st[wid].y[buf][jj][lane] : 0.0;
                 FT_t<D, MODE> F;
-                double xm[D], Pm[ns(D)], Q[ns(D)];
+                real xm[D], Pm[ns(D)], Q[ns(D)];
                 disc<D, MODE>(p.m, tk - tprev, F, Q);
                 kf_predict_pm<D>(x, P, F, Q, xm, Pm);
                 tprev = tk;
                 // observation update (branchless: missing y -> 1/S = 0, v = 0)
-                double HP[D], S, hx;
+                real HP[D], S, hx;
                 obs_terms<D>(p.m, xm, Pm, HP, S, hx, MODE == kClosed);
                 const bool bad_n = obs && !(S > 0.0 && S < INFINITY);
                 ferr_n = (bad_n && ferr_n < 0) ? static_cast<int>(k - kb) : ferr_n;
-                const double iS = obs ? rcp(S) : 0.0;
-                const double v = obs ? (yk - hx) : 0.0;
-                const double vs = v * iS;
+                const real iS = obs ? rcp(S) : 0.0;
+                const real v = obs ? (static_cast<real>(yk) - hx) : real(0.0);
+                const real vs = v * iS;
 #pragma unroll
                 for (int i = 0; i < D; ++i) x[i] = fma(HP[i], vs, xm[i]);
 #pragma unroll
@@ -660,13 +660,13 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
                 // Sigma- = Sigma F^T, then the rank-one update by y_k of the
                 // cross-covariance and of the chain-entry moments
                 if (SAGG) {
-                double Sm[D * D], SH[D];
+                real Sm[D * D], SH[D];
                 mul_bt<D>(Sg, F, Sm);
 #pragma unroll
                 for (int i = 0; i < D; ++i) {
                     if (MODE == kClosed || p.m.h_unit) SH[i] = Sm[i * D];
                     else {
-                        double s2 = 0.0;
+                        real s2 = 0.0;
 #pragma unroll
                         for (int j = 0; j < D; ++j) s2 = fma(Sm[i * D + j], p.m.H[j], s2);
                         SH[i] = s2;
@@ -674,7 +674,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
                 }
 #pragma unroll
                 for (int i = 0; i < D; ++i) {
-                    const double si_ = SH[i] * iS;
+                    const real si_ = SH[i] * iS;
 #pragma unroll
                     for (int j = 0; j < D; ++j) Sg[i * D + j] = fma(-si_, HP[j], Sm[i * D + j]);
                     x0[i] = fma(SH[i], vs, x0[i]);
@@ -684,7 +684,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
                 }
                 nll_accumulate(obs, v, vs, S, quad, prodm, prode, nobs);
                 if (STORE) {
-                    double* o = p.xp + ((wg * p.K + (k - kb)) * CN(D)) * 32 + lane;
+                    real* o = p.xp + ((wg * p.K + (k - kb)) * CN(D)) * 32 + lane;
 #pragma unroll
                     for (int i = 0; i < D; ++i) o[i * 32] = x[i];
 #pragma unroll
@@ -715,7 +715,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
                 const int64_t g1 = p.k0 + ke;
                 const double tn = __ldg(p.t + ke);
                 FT_t<D, MODE> F;
-                double Q[ns(D)], xm[D], Pm[ns(D)], Sm[D * D];
+                real Q[ns(D)], xm[D], Pm[ns(D)], Sm[D * D];
                 disc<D, MODE>(p.m, tn - tprev, F, Q);
                 kf_predict_pm<D>(x, P, F, Q, xm, Pm);
                 mul_bt<D>(Sg, F, Sm);
@@ -832,8 +832,8 @@ __device__ __forceinline__ Gauss<D> smoother_chain_carry(const KParams<D>& p, SA
 // ------------------------------------------------------------------ K5: RTS rescan
 // f-space projection: mean = H m^s, var = H P^s H^T
 template <int D>
-__device__ __forceinline__ void project(const ModelParams<D>& m, const double (&ms)[D], const double (&Ps)[ns(D)],
-                                        double& mo, double& vo, bool hu_static = false) {
+__device__ __forceinline__ void project(const ModelParams<D>& m, const real (&ms)[D], const real (&Ps)[ns(D)],
+                                        real& mo, real& vo, bool hu_static = false) {
     if (hu_static || m.h_unit) {
         mo = ms[0];
         vo = Ps[0];
@@ -842,7 +842,7 @@ __device__ __forceinline__ void project(const ModelParams<D>& m, const double (&
 #pragma unroll
         for (int i = 0; i < D; ++i) {
             mo = fma(m.H[i], ms[i], mo);
-            double s2 = 0.0;
+            real s2 = 0.0;
 #pragma unroll
             for (int j = 0; j < D; ++j) s2 = fma(Ps[si(D, i, j)], m.H[j], s2);
             vo = fma(m.H[i], s2, vo);
@@ -859,7 +859,7 @@ struct StageOut {
 template <int D, int MODE>
 __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_smoother_apply(const KParams<D> p) {
     __shared__ StageOut so[kWarps];
-    __shared__ SAgg<D> tot[kWarps];
+    __shared__ __align__(8) SAgg<D> tot[kWarps];   // also the NLL sum scratch (doubles)
     __shared__ Gauss<D> wcar[kWarps + 1];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t c = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
@@ -874,7 +874,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_smoother_apply(const K
         const double v = cta_sum(p.nll_block, p.nb, reinterpret_cast<double*>(tot));
         if (threadIdx.x == 0) *p.nll_out = v;
     }
-    double ms[D], Ps[ns(D)];
+    real ms[D], Ps[ns(D)];
     {
         const Gauss<D> cur = smoother_chain_carry<D>(p, tot, wcar, c, nch, lane, wid);
 #pragma unroll
@@ -885,21 +885,21 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_smoother_apply(const K
 
     // ---- RTS over the chain, last step first; the filtered
     // (xbar, P) of the next step down is prefetched one step ahead.
-    const double* xpw = p.xp + (wg * p.K * CN(D)) * 32 + lane;
-    double nx[CN(D)];
+    const real* xpw = p.xp + (wg * p.K * CN(D)) * 32 + lane;
+    real nx[CN(D)];
     double tnext = 0.0;
     // last step of the chain, peeled (the only place the terminal element can occur);
     // its outputs are stored directly (one scalar store per chain)
     if (ke > kb) {
         const int64_t k = ke - 1;
-        const double* src = xpw + ((k - kb) * CN(D)) * 32;
-        double x[D], P[ns(D)];
+        const real* src = xpw + ((k - kb) * CN(D)) * 32;
+        real x[D], P[ns(D)];
 #pragma unroll
         for (int i = 0; i < D; ++i) x[i] = src[i * 32];
 #pragma unroll
         for (int i = 0; i < ns(D); ++i) P[i] = src[(D + i) * 32];
         if (k > kb) {
-            const double* s1 = xpw + ((k - 1 - kb) * CN(D)) * 32;
+            const real* s1 = xpw + ((k - 1 - kb) * CN(D)) * 32;
 #pragma unroll
             for (int i = 0; i < CN(D); ++i) nx[i] = s1[i * 32];
         }
@@ -912,13 +912,13 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_smoother_apply(const K
         } else {
             const double tn = __ldg(p.t + ke);
             FT_t<D, MODE> F;
-            double Q[ns(D)], xm[D], Pm[ns(D)], FP[D * D];
+            real Q[ns(D)], xm[D], Pm[ns(D)], FP[D * D];
             disc<D, MODE>(p.m, tn - tk, F, Q);
             kf_predict<D>(x, P, F, Q, xm, FP, Pm);
             if (!rts_step<D>(x, P, xm, Pm, FP, ms, Ps)) raise_error(p.err, p.k0 + k, kErrNumeric);
         }
         tnext = tk;
-        double mo, vo;
+        real mo, vo;
         project<D>(p.m, ms, Ps, mo, vo, MODE == kClosed);
         if (p.mean) p.mean[k] = mo;
         if (p.var) p.var[k] = vo;
@@ -939,24 +939,24 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_smoother_apply(const K
             const int64_t k = kb + j0 + jj;
             {
                 const double tk = so[wid].t[buf][jj][lane];
-                double x[D], P[ns(D)];
+                real x[D], P[ns(D)];
 #pragma unroll
                 for (int i = 0; i < D; ++i) x[i] = nx[i];
 #pragma unroll
                 for (int i = 0; i < ns(D); ++i) P[i] = nx[D + i];
                 if (k > kb) {
-                    const double* src = xpw + ((k - 1 - kb) * CN(D)) * 32;
+                    const real* src = xpw + ((k - 1 - kb) * CN(D)) * 32;
 #pragma unroll
                     for (int i = 0; i < CN(D); ++i) nx[i] = src[i * 32];
                 }
                 FT_t<D, MODE> F;
-            double Q[ns(D)], xm[D], Pm[ns(D)], FP[D * D];
+            real Q[ns(D)], xm[D], Pm[ns(D)], FP[D * D];
                 disc<D, MODE>(p.m, tnext - tk, F, Q);
                 kf_predict<D>(x, P, F, Q, xm, FP, Pm);
                 const bool bad_n = !rts_step<D>(x, P, xm, Pm, FP, ms, Ps);
                 ferr_n = bad_n ? static_cast<int>(k - kb) : ferr_n;   // backward: last hit = first index
                 tnext = tk;
-                double mo, vo;
+                real mo, vo;
                 project<D>(p.m, ms, Ps, mo, vo, MODE == kClosed);
                 so[wid].m[jj][lane] = mo;
                 so[wid].v[jj][lane] = vo;
@@ -1004,10 +1004,10 @@ __global__ void __launch_bounds__(256, 1) k_nll_sum(const double* __restrict__ p
 
 // ------------------------------------------------------------------ chunk aggregate reducers (sharded path, 1 CTA)
 template <int D, typename Agg>
-__global__ void __launch_bounds__(kCarryThreads, 1) k_reduce_blocks(const double* __restrict__ blocks, int nb,
-                                                                    double* out) {
+__global__ void __launch_bounds__(kCarryThreads, 1) k_reduce_blocks(const real* __restrict__ blocks, int nb,
+                                                                    real* out) {
     constexpr int NW = kCarryThreads / 32;
-    constexpr int NA = sizeof(Agg) / sizeof(double);
+    constexpr int NA = sizeof(Agg) / sizeof(real);
     __shared__ Agg wred[NW];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int per = (nb + kCarryThreads - 1) / kCarryThreads;
@@ -1045,9 +1045,9 @@ __global__ void __launch_bounds__(kCarryThreads, 1) k_reduce_blocks(const double
     }
 }
 
-}  // namespace pssgp
+}  // namespace PSSGP_NS
 
-namespace pssgp {
+namespace PSSGP_NS {
 // ------------------------------------------------------------------ test-time merge (stage 4)
 // Rank-based parallel merge of sorted training times (observed) and sorted test
 // times (missing): a training time goes to i + #{test < t_i}, a test time to
@@ -1099,4 +1099,4 @@ __global__ void __launch_bounds__(256) k_gather(int64_t n_te, const int64_t* __r
         if (var_te) var_te[j] = __ldg(var + k);
     }
 }
-}  // namespace pssgp
+}  // namespace PSSGP_NS

@@ -1,6 +1,7 @@
 // pssgp_math.cuh — register-resident small-matrix math of the PSSGP hot path.
 //
-// Everything is fp64, fully unrolled at compile time for a state dimension D,
+// Everything is fp64 (the optional fp32 build, pssgp_f32.cu, re-includes this file with
+// real = float for the state algebra), fully unrolled at compile time for a state dimension D,
 // with symmetric matrices (C, J, P, L, Q, P_inf) stored as PACKED UPPER
 // TRIANGLES so that the symmetry the filtering operator needs for
 // associativity (SURVEY.md finding 3) is structural.
@@ -31,24 +32,35 @@
 #define PS_CX constexpr
 #endif
 
-namespace pssgp {
+#ifndef PSSGP_NS
+#define PSSGP_NS pssgp          // the fp64 build; pssgp_f32.cu re-includes with pssgp_f32 / float
+#endif
+#ifndef PSSGP_REAL
+#define PSSGP_REAL double
+#endif
+
+namespace PSSGP_NS {
+
+// scalar type of the state algebra (moments, aggregates, F, Q); times, observations, outputs and
+// the NLL accumulation stay fp64 in every build (fp32 ulp at t ~ 2048 exceeds the step)
+using real = PSSGP_REAL;
 
 PS_CX int ns(int D) { return D * (D + 1) / 2; }
 // packed-upper index of (i, j), any order
 PS_CX int si(int D, int i, int j) {
     return i <= j ? i * (2 * D - i + 1) / 2 + (j - i) : j * (2 * D - j + 1) / 2 + (i - j);
 }
-PS_CX int FN(int D) { return D * D + 2 * D + 2 * ns(D); }  // filter aggregate doubles
-PS_CX int SN(int D) { return D * D + D + ns(D); }          // smoother aggregate doubles
-PS_CX int CN(int D) { return D + ns(D); }                  // (mean, cov) pair doubles
+PS_CX int FN(int D) { return D * D + 2 * D + 2 * ns(D); }  // filter aggregate reals
+PS_CX int SN(int D) { return D * D + D + ns(D); }          // smoother aggregate reals
+PS_CX int CN(int D) { return D + ns(D); }                  // (mean, cov) pair reals
 
 // ------------------------------------------------------------------ branch-free scalar math
 // Constants live in a table (device: __constant__, host: constexpr) so the
 // kernels read them as constant-bank operands instead of re-materialising
 // 64-bit literals with uniform-register moves.
 struct MathConsts {
-    double expc[28];   // 1/k!, k = 0..27 (Taylor of e^r on |r| <= ln2/2 uses k <= 13; R_m series)
-    double inv[32];    // 1/n, n = 0..31 (inv[0] unused)
+    real expc[28];   // 1/k!, k = 0..27 (Taylor of e^r on |r| <= ln2/2 uses k <= 13; R_m series)
+    real inv[32];    // 1/n, n = 0..31 (inv[0] unused)
 };
 #define PS_MATH_CONSTS                                                                         \
     {{1.0, 1.0, 0.5, 0.16666666666666666, 0.041666666666666664,  \
@@ -136,19 +148,38 @@ PS_HD double exp_neg(double z) {
 #endif
 }
 
+// fp32 build (real = float): hardware reciprocal + one Newton step (~1 ulp), hardware exp.
+PS_HD float rcp(float a) {
+#if defined(__CUDA_ARCH__)
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(a));
+    return fmaf(r, fmaf(-a, r, 1.0f), r);
+#else
+    return 1.0f / a;
+#endif
+}
+template <bool FAST = false>
+PS_HD float exp_neg(float z) {
+#if defined(__CUDA_ARCH__)
+    return __expf(-z);
+#else
+    return std::exp(-z);
+#endif
+}
+
 // Model constants the kernels need (kernel parameter, i.e. constant bank).
 template <int D>
 struct ModelParams {
-    double Pinf[ns(D)];   // stationary covariance (balanced coordinates)
-    double H[D];          // observation row (balanced coordinates)
-    double r;             // observation noise variance sigma_n^2 > 0
-    double lam;           // Matern lambda = sqrt(2 nu) / ell (closed form), else 0
-    double s2;            // Matern variance sigma^2
-    double udt;           // uniform dt (> 0) for which Fu, Qu are valid, else 0
-    double Fu[D * D];     // F(udt)
-    double Qu[ns(D)];     // Q(udt)
-    double G[D * D];      // continuous drift (balanced coordinates), kPade mode
-    double W[ns(D)];      // diffusion L q L^T (balanced coordinates), kPade mode
+    real Pinf[ns(D)];   // stationary covariance (balanced coordinates)
+    real H[D];          // observation row (balanced coordinates)
+    real r;             // observation noise variance sigma_n^2 > 0
+    real lam;           // Matern lambda = sqrt(2 nu) / ell (closed form), else 0
+    real s2;            // Matern variance sigma^2
+    real udt;           // uniform dt (> 0) for which Fu, Qu are valid, else 0
+    real Fu[D * D];     // F(udt)
+    real Qu[ns(D)];     // Q(udt)
+    real G[D * D];      // continuous drift (balanced coordinates), kPade mode
+    real W[ns(D)];      // diffusion L q L^T (balanced coordinates), kPade mode
     int closed;           // 1: Matern closed form of order D available in the lambda-scaled basis
     int h_unit;           // 1: H == e_0
 };
@@ -156,24 +187,24 @@ struct ModelParams {
 // ------------------------------------------------------------------ aggregates
 template <int D>
 struct FAgg {  // filter element / aggregate (A, b, C, eta, J)
-    double A[D * D];
-    double b[D];
-    double C[ns(D)];
-    double eta[D];
-    double J[ns(D)];
+    real A[D * D];
+    real b[D];
+    real C[ns(D)];
+    real eta[D];
+    real J[ns(D)];
 };
 
 template <int D>
 struct SAgg {  // smoother element / aggregate (E, g, L)
-    double E[D * D];
-    double g[D];
-    double L[ns(D)];
+    real E[D * D];
+    real g[D];
+    real L[ns(D)];
 };
 
 template <int D>
 struct Gauss {  // (mean, covariance) — a collapsed global prefix (0, x, P, 0, 0) or suffix (0, m, P)
-    double x[D];
-    double P[ns(D)];
+    real x[D];
+    real P[ns(D)];
 };
 
 template <int D>
@@ -210,12 +241,12 @@ PS_HD void set_zero(Gauss<D>& c) {
 }
 
 // flat views for loads / stores / shuffles
-template <int D> PS_HD double* flat(FAgg<D>& a) { return a.A; }
-template <int D> PS_HD const double* flat(const FAgg<D>& a) { return a.A; }
-template <int D> PS_HD double* flat(SAgg<D>& a) { return a.E; }
-template <int D> PS_HD const double* flat(const SAgg<D>& a) { return a.E; }
-template <int D> PS_HD double* flat(Gauss<D>& a) { return a.x; }
-template <int D> PS_HD const double* flat(const Gauss<D>& a) { return a.x; }
+template <int D> PS_HD real* flat(FAgg<D>& a) { return a.A; }
+template <int D> PS_HD const real* flat(const FAgg<D>& a) { return a.A; }
+template <int D> PS_HD real* flat(SAgg<D>& a) { return a.E; }
+template <int D> PS_HD const real* flat(const SAgg<D>& a) { return a.E; }
+template <int D> PS_HD real* flat(Gauss<D>& a) { return a.x; }
+template <int D> PS_HD const real* flat(const Gauss<D>& a) { return a.x; }
 
 // ------------------------------------------------------------------ small dense helpers
 // Gaussian elimination with partial pivoting on [M | R] (M D x D row-major,
@@ -223,7 +254,7 @@ template <int D> PS_HD const double* flat(const Gauss<D>& a) { return a.x; }
 // chosen by compare-and-swap with compile-time indices only (no dynamic
 // register indexing).  Returns false on a zero pivot.
 template <int D, int NR>
-PS_HD bool gauss_solve(double (&M)[D * D], double (&R)[D * NR]) {
+PS_HD bool gauss_solve(real (&M)[D * D], real (&R)[D * NR]) {
     bool ok = true;
 #pragma unroll
     for (int c = 0; c < D; ++c) {
@@ -232,23 +263,23 @@ PS_HD bool gauss_solve(double (&M)[D * D], double (&R)[D * NR]) {
             const bool sw = fabs(M[r * D + c]) > fabs(M[c * D + c]);
 #pragma unroll
             for (int k = c; k < D; ++k) {
-                const double u = M[c * D + k], v = M[r * D + k];
+                const real u = M[c * D + k], v = M[r * D + k];
                 M[c * D + k] = sw ? v : u;
                 M[r * D + k] = sw ? u : v;
             }
 #pragma unroll
             for (int k = 0; k < NR; ++k) {
-                const double u = R[c * NR + k], v = R[r * NR + k];
+                const real u = R[c * NR + k], v = R[r * NR + k];
                 R[c * NR + k] = sw ? v : u;
                 R[r * NR + k] = sw ? u : v;
             }
         }
-        const double piv = M[c * D + c];
+        const real piv = M[c * D + c];
         ok = ok && (piv != 0.0);
-        const double ip = rcp(piv);
+        const real ip = rcp(piv);
 #pragma unroll
         for (int r = c + 1; r < D; ++r) {
-            const double f = M[r * D + c] * ip;
+            const real f = M[r * D + c] * ip;
 #pragma unroll
             for (int k = c + 1; k < D; ++k) M[r * D + k] = fma(-f, M[c * D + k], M[r * D + k]);
 #pragma unroll
@@ -260,7 +291,7 @@ PS_HD bool gauss_solve(double (&M)[D * D], double (&R)[D * NR]) {
     for (int c = D - 1; c >= 0; --c) {
 #pragma unroll
         for (int k = 0; k < NR; ++k) {
-            double s = R[c * NR + k];
+            real s = R[c * NR + k];
 #pragma unroll
             for (int j = c + 1; j < D; ++j) s = fma(-M[c * D + j], R[j * NR + k], s);
             R[c * NR + k] = s * M[c * D + c];
@@ -275,22 +306,22 @@ PS_HD bool gauss_solve(double (&M)[D * D], double (&R)[D * NR]) {
 // eigenvalues are >= 1 (C, J, P positive semi-definite).  Returns false
 // for a zero or non-finite determinant.
 template <int D>
-PS_HD bool inv_small(const double (&M)[D * D], double (&Mi)[D * D]) {
+PS_HD bool inv_small(const real (&M)[D * D], real (&Mi)[D * D]) {
     static_assert(D <= 3, "adjugate inverse for D <= 3");
     if constexpr (D == 1) {
         Mi[0] = rcp(M[0]);
         return M[0] != 0.0;
     } else if constexpr (D == 2) {
-        const double det = fma(M[0], M[3], -M[1] * M[2]);
-        const double id = rcp(det);
+        const real det = fma(M[0], M[3], -M[1] * M[2]);
+        const real id = rcp(det);
         Mi[0] = M[3] * id; Mi[1] = -M[1] * id; Mi[2] = -M[2] * id; Mi[3] = M[0] * id;
         return det != 0.0 && isfinite(id);
     } else {
-        const double c00 = fma(M[4], M[8], -M[5] * M[7]);
-        const double c01 = fma(M[5], M[6], -M[3] * M[8]);
-        const double c02 = fma(M[3], M[7], -M[4] * M[6]);
-        const double det = fma(M[0], c00, fma(M[1], c01, M[2] * c02));
-        const double id = rcp(det);
+        const real c00 = fma(M[4], M[8], -M[5] * M[7]);
+        const real c01 = fma(M[5], M[6], -M[3] * M[8]);
+        const real c02 = fma(M[3], M[7], -M[4] * M[6]);
+        const real det = fma(M[0], c00, fma(M[1], c01, M[2] * c02));
+        const real id = rcp(det);
         Mi[0] = c00 * id;
         Mi[3] = c01 * id;
         Mi[6] = c02 * id;
@@ -306,16 +337,16 @@ PS_HD bool inv_small(const double (&M)[D * D], double (&Mi)[D * D]) {
 
 // Solve M X = R (R: D x NR row-major, in place): adjugate for D <= 3, pivoted elimination above.
 template <int D, int NR>
-PS_HD bool small_solve(double (&M)[D * D], double (&R)[D * NR]) {
+PS_HD bool small_solve(real (&M)[D * D], real (&R)[D * NR]) {
     if constexpr (D <= 3) {
-        double Mi[D * D];
+        real Mi[D * D];
         const bool ok = inv_small<D>(M, Mi);
-        double X[D * NR];
+        real X[D * NR];
 #pragma unroll
         for (int r = 0; r < D; ++r)
 #pragma unroll
             for (int c = 0; c < NR; ++c) {
-                double s = 0.0;
+                real s = 0.0;
 #pragma unroll
                 for (int k = 0; k < D; ++k) s = fma(Mi[r * D + k], R[k * NR + c], s);
                 X[r * NR + c] = s;
@@ -331,12 +362,12 @@ PS_HD bool small_solve(double (&M)[D * D], double (&R)[D * NR]) {
 // LDL^T factorisation of a symmetric positive-definite packed matrix.
 // Lo: strictly-lower factor (row-major D x D, only i > j used), id: 1 / d.
 template <int D>
-PS_HD bool ldlt(const double (&S)[ns(D)], double (&Lo)[D * D], double (&id)[D]) {
-    double dd[D];
+PS_HD bool ldlt(const real (&S)[ns(D)], real (&Lo)[D * D], real (&id)[D]) {
+    real dd[D];
     bool ok = true;
 #pragma unroll
     for (int j = 0; j < D; ++j) {
-        double d = S[si(D, j, j)];
+        real d = S[si(D, j, j)];
 #pragma unroll
         for (int k = 0; k < j; ++k) d = fma(-Lo[j * D + k] * dd[k], Lo[j * D + k], d);
         ok = ok && (d > 0.0);
@@ -344,7 +375,7 @@ PS_HD bool ldlt(const double (&S)[ns(D)], double (&Lo)[D * D], double (&id)[D]) 
         id[j] = rcp(d);
 #pragma unroll
         for (int i = j + 1; i < D; ++i) {
-            double s = S[si(D, i, j)];
+            real s = S[si(D, i, j)];
 #pragma unroll
             for (int k = 0; k < j; ++k) s = fma(-Lo[i * D + k] * dd[k], Lo[j * D + k], s);
             Lo[i * D + j] = s * id[j];
@@ -355,12 +386,12 @@ PS_HD bool ldlt(const double (&S)[ns(D)], double (&Lo)[D * D], double (&id)[D]) 
 
 // Solve S X = R with the LDL^T factors (R: D x NR row-major, in place).
 template <int D, int NR>
-PS_HD void ldlt_solve(const double (&Lo)[D * D], const double (&id)[D], double (&R)[D * NR]) {
+PS_HD void ldlt_solve(const real (&Lo)[D * D], const real (&id)[D], real (&R)[D * NR]) {
 #pragma unroll
     for (int k = 0; k < NR; ++k) {
 #pragma unroll
         for (int i = 1; i < D; ++i) {
-            double s = R[i * NR + k];
+            real s = R[i * NR + k];
 #pragma unroll
             for (int j = 0; j < i; ++j) s = fma(-Lo[i * D + j], R[j * NR + k], s);
             R[i * NR + k] = s;
@@ -369,7 +400,7 @@ PS_HD void ldlt_solve(const double (&Lo)[D * D], const double (&id)[D], double (
         for (int i = 0; i < D; ++i) R[i * NR + k] *= id[i];
 #pragma unroll
         for (int i = D - 2; i >= 0; --i) {
-            double s = R[i * NR + k];
+            real s = R[i * NR + k];
 #pragma unroll
             for (int j = i + 1; j < D; ++j) s = fma(-Lo[j * D + i], R[j * NR + k], s);
             R[i * NR + k] = s;
@@ -382,38 +413,38 @@ PS_HD void ldlt_solve(const double (&Lo)[D * D], const double (&id)[D], double (
 // evaluated without cancellation: truncated series for x <= 2, complement
 // 1 - e^{-x} sum_{n<m} x^n/n! above (cancellation <= ~20x there).
 template <int M, bool FAST = false>
-PS_HD double inc_gamma_tail(double x, double emx) {
+PS_HD real inc_gamma_tail(real x, real emx) {
     const MathConsts& C = mc();
-    double xm;                                    // x^M
+    real xm;                                    // x^M
     if constexpr (M == 5) {
-        const double x2 = x * x;
+        const real x2 = x * x;
         xm = x2 * x2 * x;
     } else {
         xm = x;
 #pragma unroll
         for (int n = 1; n < M; ++n) xm *= x;
     }
-    const double lead = emx * xm;                 // e^{-x} x^M; series coefficients 1/(M+j)!
-    if (FAST || x <= 0.015625) {   // FAST: caller guarantees 0 <= x <= 2^-6
-        double s = C.expc[M + 7];
+    const real lead = emx * xm;                 // e^{-x} x^M; series coefficients 1/(M+j)!
+    if (FAST || x <= real(0.015625)) {   // FAST: caller guarantees 0 <= x <= 2^-6
+        real s = C.expc[M + 7];
 #pragma unroll
         for (int j = 6; j >= 0; --j) s = fma(s, x, C.expc[M + j]);
         return lead * s;
-    } else if (x <= 0.5) {
-        double s = C.expc[M + 13];
+    } else if (x <= real(0.5)) {
+        real s = C.expc[M + 13];
 #pragma unroll
         for (int j = 12; j >= 0; --j) s = fma(s, x, C.expc[M + j]);
         return lead * s;
-    } else if (x <= 2.0) {
-        double s = C.expc[M + 22];
+    } else if (x <= real(2.0)) {
+        real s = C.expc[M + 22];
 #pragma unroll
         for (int j = 21; j >= 0; --j) s = fma(s, x, C.expc[M + j]);
         return lead * s;
     } else {
-        double p = 1.0, term = 1.0;
+        real p = 1.0, term = 1.0;
 #pragma unroll
         for (int n = 1; n < M; ++n) { term *= x * C.inv[n]; p += term; }
-        return fma(-emx, p, 1.0);
+        return fma(-emx, p, real(1.0));
     }
 }
 
@@ -423,8 +454,8 @@ PS_HD double inc_gamma_tail(double x, double emx) {
 // the fully unrolled products skip structural zeros.
 template <int D>
 struct FMat {                        // general F (row-major)
-    double a[D * D];
-    PS_HD double operator()(int i, int j) const { return a[i * D + j]; }
+    real a[D * D];
+    PS_HD real operator()(int i, int j) const { return a[i * D + j]; }
     static PS_HD constexpr bool nz(int, int) { return true; }
 };
 // Closed-form Matern-(2D-1)/2 in the JORDAN basis of its drift: with x_hat_i = x_i / lambda^i
@@ -436,10 +467,10 @@ struct FMat {                        // general F (row-major)
 // an upper-triangular Toeplitz matrix: F(i, j) = ec[j - i] = e^{-z} z^(j-i) / (j-i)!.
 template <int D>
 struct FJor {
-    double ec[D];      // e^{-z} z^k / k!
-    double e;          // e^{-z}
-    double u[D];       // z^k / k! (u[0] = 1 unused): F = e U
-    PS_HD double operator()(int i, int j) const { return j >= i ? ec[j - i] : 0.0; }
+    real ec[D];      // e^{-z} z^k / k!
+    real e;          // e^{-z}
+    real u[D];       // z^k / k! (u[0] = 1 unused): F = e U
+    PS_HD real operator()(int i, int j) const { return j >= i ? ec[j - i] : 0.0; }
     static PS_HD constexpr bool nz(int i, int j) { return j >= i; }
 };
 template <int D>
@@ -456,13 +487,13 @@ PS_HD void set_zero(FJor<D>& f) {
 
 // F S F^T + Q for symmetric packed S (packed result).  General F: T = F S, then T F^T.
 template <int D>
-PS_HD void cong_plus(const FMat<D>& F, const double (&S)[ns(D)], const double (&Q)[ns(D)], double (&R)[ns(D)]) {
-    double T[D * D];
+PS_HD void cong_plus(const FMat<D>& F, const real (&S)[ns(D)], const real (&Q)[ns(D)], real (&R)[ns(D)]) {
+    real T[D * D];
 #pragma unroll
     for (int i = 0; i < D; ++i)
 #pragma unroll
         for (int j = 0; j < D; ++j) {
-            double t = 0.0;
+            real t = 0.0;
 #pragma unroll
             for (int k = 0; k < D; ++k) t = fma(F(i, k), S[si(D, k, j)], t);
             T[i * D + j] = t;
@@ -471,7 +502,7 @@ PS_HD void cong_plus(const FMat<D>& F, const double (&S)[ns(D)], const double (&
     for (int i = 0; i < D; ++i)
 #pragma unroll
         for (int j = i; j < D; ++j) {
-            double r = Q[si(D, i, j)];
+            real r = Q[si(D, i, j)];
 #pragma unroll
             for (int k = 0; k < D; ++k) r = fma(T[i * D + k], F(j, k), r);
             R[si(D, i, j)] = r;
@@ -480,23 +511,23 @@ PS_HD void cong_plus(const FMat<D>& F, const double (&S)[ns(D)], const double (&
 // Jordan F = e U (U unit upper-triangular Toeplitz): e^2 (U S U^T) + Q, the unit diagonal and
 // the structural zeros of U skipped (D = 3: 13 FMA for U S U^T instead of 45).
 template <int D>
-PS_HD void cong_plus(const FJor<D>& F, const double (&S)[ns(D)], const double (&Q)[ns(D)], double (&R)[ns(D)]) {
-    double X[D * D];   // X = U S
+PS_HD void cong_plus(const FJor<D>& F, const real (&S)[ns(D)], const real (&Q)[ns(D)], real (&R)[ns(D)]) {
+    real X[D * D];   // X = U S
 #pragma unroll
     for (int i = 0; i < D; ++i)
 #pragma unroll
         for (int j = 0; j < D; ++j) {
-            double t = S[si(D, i, j)];
+            real t = S[si(D, i, j)];
 #pragma unroll
             for (int k = i + 1; k < D; ++k) t = fma(F.u[k - i], S[si(D, k, j)], t);
             X[i * D + j] = t;
         }
-    const double e2 = F.e * F.e;
+    const real e2 = F.e * F.e;
 #pragma unroll
     for (int i = 0; i < D; ++i)
 #pragma unroll
         for (int j = i; j < D; ++j) {
-            double y = X[i * D + j];
+            real y = X[i * D + j];
 #pragma unroll
             for (int l = j + 1; l < D; ++l) y = fma(X[i * D + l], F.u[l - j], y);
             R[si(D, i, j)] = fma(e2, y, Q[si(D, i, j)]);
@@ -515,11 +546,11 @@ PS_HD FMat<D> to_full(const FT& f) {
 // R_m(x) = e^{-x} sum_{n >= m} x^n / n!, m = 1..M, from R_M by R_m = R_{m+1} + e^{-x} x^m / m!
 // (every term positive: no cancellation at any x).  R[m] for m = 1..M (R[0] unused).
 template <int M, bool FAST = false>
-PS_HD void inc_gamma_tails(double x, double emx, double (&R)[M + 1]) {
+PS_HD void inc_gamma_tails(real x, real emx, real (&R)[M + 1]) {
     const MathConsts& C = mc();
     R[M] = inc_gamma_tail<M, FAST>(x, emx);
-    double tm = emx * x;                         // e^{-x} x^1 / 1!
-    double t[M + 1];
+    real tm = emx * x;                         // e^{-x} x^1 / 1!
+    real t[M + 1];
     t[1] = tm;
 #pragma unroll
     for (int m = 2; m < M; ++m) { tm = tm * x * C.inv[m]; t[m] = tm; }
@@ -537,34 +568,34 @@ PS_HD void inc_gamma_tails(double x, double emx, double (&R)[M + 1]) {
 //   D = 3: Q00 = s2 R5, Q01 = s2 R4, Q02 = 2/3 s2 R3, Q11 = 4/3 s2 R3, Q12 = 4/3 s2 R2, Q22 = 8/3 s2 R1
 // P_inf = lim Q (R_m -> 1).  FAST: the caller guarantees 0 <= z <= 2^-7.
 template <int D, bool FAST = false>
-PS_HD void matern_closed(double lam, double s2, double dt, FJor<D>& F, double (&Q)[ns(D)]) {
-    const double z = lam * dt;
-    const double e = exp_neg<FAST>(z);
-    const double x = 2.0 * z;
-    const double ex = e * e;  // e^{-x}
+PS_HD void matern_closed(real lam, real s2, double dt, FJor<D>& F, real (&Q)[ns(D)]) {
+    const real z = static_cast<real>(lam * dt);
+    const real e = exp_neg<FAST>(z);
+    const real x = real(2.0) * z;
+    const real ex = e * e;  // e^{-x}
     F.e = e;
     F.u[0] = 1.0;
     F.ec[0] = e;
     if constexpr (D >= 2) { F.u[1] = z; F.ec[1] = e * z; }
-    if constexpr (D >= 3) { F.u[2] = 0.5 * z * z; F.ec[2] = e * F.u[2]; }
+    if constexpr (D >= 3) { F.u[2] = real(0.5) * z * z; F.ec[2] = e * F.u[2]; }
     if constexpr (D == 1) {
         Q[0] = s2 * inc_gamma_tail<1, FAST>(x, ex);
     } else if constexpr (D == 2) {
-        double R[4];
+        real R[4];
         inc_gamma_tails<3, FAST>(x, ex, R);
         Q[si(2, 0, 0)] = s2 * R[3];
         Q[si(2, 0, 1)] = s2 * R[2];
-        Q[si(2, 1, 1)] = (2.0 * s2) * R[1];
+        Q[si(2, 1, 1)] = (real(2.0) * s2) * R[1];
     } else if constexpr (D == 3) {
-        double R[6];
+        real R[6];
         inc_gamma_tails<5, FAST>(x, ex, R);
-        const double s43 = s2 * (4.0 / 3.0);
+        const real s43 = s2 * real(4.0 / 3.0);
         Q[si(3, 0, 0)] = s2 * R[5];
         Q[si(3, 0, 1)] = s2 * R[4];
-        Q[si(3, 0, 2)] = (s2 * (2.0 / 3.0)) * R[3];
+        Q[si(3, 0, 2)] = (s2 * real(2.0 / 3.0)) * R[3];
         Q[si(3, 1, 1)] = s43 * R[3];
         Q[si(3, 1, 2)] = s43 * R[2];
-        Q[si(3, 2, 2)] = (s2 * (8.0 / 3.0)) * R[1];
+        Q[si(3, 2, 2)] = (s2 * real(8.0 / 3.0)) * R[1];
     }
 }
 
@@ -584,11 +615,11 @@ enum DiscMode : int { kClosed = 0, kTable = 1, kMixed = 2, kPade = 3 };
 // accurate to unit roundoff for ||A||_1 <= theta_7 = 0.9504; A = G dt / 2^s with the
 // smallest such s, then s squarings.  (V - U) F = V + U by pivoted elimination.
 template <int D>
-PS_HD void expm_pade7(const double (&G)[D * D], double dt, double (&F)[D * D]) {
-    double nrm = 0.0;
+PS_HD void expm_pade7(const real (&G)[D * D], real dt, real (&F)[D * D]) {
+    real nrm = 0.0;
 #pragma unroll
     for (int j = 0; j < D; ++j) {
-        double c = 0.0;
+        real c = 0.0;
 #pragma unroll
         for (int i = 0; i < D; ++i) c += fabs(G[i * D + j]);
         nrm = fmax(nrm, c);
@@ -600,16 +631,16 @@ PS_HD void expm_pade7(const double (&G)[D * D], double dt, double (&F)[D * D]) {
         frexp(nrm / 0.9504, &e);   // nrm / theta = f 2^e, f in [0.5, 1)  ->  2^e >= nrm / theta
         s = e;
     }
-    const double sc = ldexp(dt, -s);
-    double A[D * D], A2[D * D], A4[D * D], A6[D * D];
+    const real sc = ldexp(dt, -s);
+    real A[D * D], A2[D * D], A4[D * D], A6[D * D];
 #pragma unroll
     for (int i = 0; i < D * D; ++i) A[i] = G[i] * sc;
-    auto mm = [](const double (&X)[D * D], const double (&Y)[D * D], double (&Z)[D * D]) {
+    auto mm = [](const real (&X)[D * D], const real (&Y)[D * D], real (&Z)[D * D]) {
 #pragma unroll
         for (int i = 0; i < D; ++i)
 #pragma unroll
             for (int j = 0; j < D; ++j) {
-                double acc = 0.0;
+                real acc = 0.0;
 #pragma unroll
                 for (int k = 0; k < D; ++k) acc = fma(X[i * D + k], Y[k * D + j], acc);
                 Z[i * D + j] = acc;
@@ -618,15 +649,15 @@ PS_HD void expm_pade7(const double (&G)[D * D], double dt, double (&F)[D * D]) {
     mm(A, A, A2);
     mm(A2, A2, A4);
     mm(A4, A2, A6);
-    constexpr double b0 = 17297280.0, b1 = 8648640.0, b2 = 1995840.0, b3 = 277200.0, b4 = 25200.0,
+    constexpr real b0 = 17297280.0, b1 = 8648640.0, b2 = 1995840.0, b3 = 277200.0, b4 = 25200.0,
                      b5 = 1512.0, b6 = 56.0, b7 = 1.0;
-    double T[D * D], U[D * D], V[D * D];
+    real T[D * D], U[D * D], V[D * D];
 #pragma unroll
     for (int i = 0; i < D; ++i)
 #pragma unroll
         for (int j = 0; j < D; ++j) {
             const int e = i * D + j;
-            const double id = (i == j) ? 1.0 : 0.0;
+            const real id = (i == j) ? 1.0 : 0.0;
             T[e] = fma(b7, A6[e], fma(b5, A4[e], fma(b3, A2[e], b1 * id)));
             V[e] = fma(b6, A6[e], fma(b4, A4[e], fma(b2, A2[e], b0 * id)));
         }
@@ -638,7 +669,7 @@ PS_HD void expm_pade7(const double (&G)[D * D], double dt, double (&F)[D * D]) {
     }
     gauss_solve<D, D>(T, F);
     for (int q = 0; q < s; ++q) {
-        double Fs[D * D];
+        real Fs[D * D];
         mm(F, F, Fs);
 #pragma unroll
         for (int e = 0; e < D * D; ++e) F[e] = Fs[e];
@@ -653,12 +684,12 @@ PS_HD void expm_pade7(const double (&G)[D * D], double dt, double (&F)[D * D]) {
 // m = 12 (truncation (2/8)^m / (m+1)! < 1e-17 relative; m = 7 when ||G dt|| <= 1/100), then s
 // doublings Q <- Q + F Q F^T, F <- F F (the semigroup identity, as Van Loan composes sub-steps).
 template <int D>
-PS_HD void taylor_fq(const double (&G)[D * D], const double (&W)[ns(D)], double dt, double (&F)[D * D],
-                     double (&Q)[ns(D)]) {
-    double nrm = 0.0;
+PS_HD void taylor_fq(const real (&G)[D * D], const real (&W)[ns(D)], real dt, real (&F)[D * D],
+                     real (&Q)[ns(D)]) {
+    real nrm = 0.0;
 #pragma unroll
     for (int j = 0; j < D; ++j) {
-        double c = 0.0;
+        real c = 0.0;
 #pragma unroll
         for (int i = 0; i < D; ++i) c += fabs(G[i * D + j]);
         nrm = fmax(nrm, c);
@@ -670,25 +701,25 @@ PS_HD void taylor_fq(const double (&G)[D * D], const double (&W)[ns(D)], double 
         frexp(nrm / 0.125, &e);
         s = e;
     }
-    const double tau = ldexp(dt, -s);
+    const real tau = ldexp(dt, -s);
     const int m = (nrm <= 0.01) ? 7 : 12;
-    double A[D * D];
+    real A[D * D];
 #pragma unroll
     for (int i = 0; i < D * D; ++i) A[i] = G[i] * tau;
     // F on the scaled step: [7/7] Pade (||A||_1 <= 1/8 < theta_7: no further scaling)
-    double T[D * D];
+    real T[D * D];
     expm_pade7<D>(G, tau, F);
     // Q: Z_1 = tau W, Z_{k+1} = (A Z_k + Z_k A^T) / (k + 1)
-    double Z[ns(D)];
+    real Z[ns(D)];
 #pragma unroll
     for (int i = 0; i < ns(D); ++i) { Z[i] = W[i] * tau; Q[i] = Z[i]; }
     for (int k = 1; k < m; ++k) {
-        const double ik = 1.0 / (k + 1);
+        const real ik = 1.0 / (k + 1);
 #pragma unroll
         for (int i = 0; i < D; ++i)
 #pragma unroll
             for (int j = 0; j < D; ++j) {
-                double acc = 0.0;
+                real acc = 0.0;
 #pragma unroll
                 for (int l = 0; l < D; ++l) acc = fma(A[i * D + l], Z[si(D, l, j)], acc);
                 T[i * D + j] = acc;                         // Y = A Z
@@ -707,17 +738,17 @@ PS_HD void taylor_fq(const double (&G)[D * D], const double (&W)[ns(D)], double 
         for (int i = 0; i < D; ++i)
 #pragma unroll
             for (int j = 0; j < D; ++j) {
-                double acc = 0.0;
+                real acc = 0.0;
 #pragma unroll
                 for (int l = 0; l < D; ++l) acc = fma(F[i * D + l], Q[si(D, l, j)], acc);
                 T[i * D + j] = acc;                         // F Q
             }
-        double Qn[ns(D)];
+        real Qn[ns(D)];
 #pragma unroll
         for (int i = 0; i < D; ++i)
 #pragma unroll
             for (int j = i; j < D; ++j) {
-                double acc = Q[si(D, i, j)];
+                real acc = Q[si(D, i, j)];
 #pragma unroll
                 for (int l = 0; l < D; ++l) acc = fma(T[i * D + l], F[j * D + l], acc);
                 Qn[si(D, i, j)] = acc;
@@ -728,7 +759,7 @@ PS_HD void taylor_fq(const double (&G)[D * D], const double (&W)[ns(D)], double 
         for (int i = 0; i < D; ++i)
 #pragma unroll
             for (int j = 0; j < D; ++j) {
-                double acc = 0.0;
+                real acc = 0.0;
 #pragma unroll
                 for (int l = 0; l < D; ++l) acc = fma(F[i * D + l], F[l * D + j], acc);
                 T[i * D + j] = acc;
@@ -743,12 +774,12 @@ template <int D, int MODE>
 using FT_t = typename std::conditional<MODE == kClosed, FJor<D>, FMat<D>>::type;
 
 template <int D, int MODE>
-PS_HD int disc(const ModelParams<D>& p, double dt, FT_t<D, MODE>& Ft, double (&Q)[ns(D)]) {
+PS_HD int disc(const ModelParams<D>& p, double dt, FT_t<D, MODE>& Ft, real (&Q)[ns(D)]) {
     if constexpr (MODE == kClosed) {
         if constexpr (D <= 3) matern_closed<D>(p.lam, p.s2, dt, Ft, Q);
         return 0;
     } else {
-        double (&F)[D * D] = Ft.a;
+        real (&F)[D * D] = Ft.a;
         if (fabs(dt - p.udt) <= 1e-12 * p.udt) {   // uniform step up to time-stamp rounding
 #pragma unroll
             for (int i = 0; i < D * D; ++i) F[i] = p.Fu[i];
@@ -783,7 +814,7 @@ PS_HD int disc(const ModelParams<D>& p, double dt, FT_t<D, MODE>& Ft, double (&Q
 
 // Host-side dispatcher used by pssgp_debug_discretize.
 template <int D>
-PS_HD int discretize(const ModelParams<D>& p, double dt, double (&F)[D * D], double (&Q)[ns(D)]) {
+PS_HD int discretize(const ModelParams<D>& p, double dt, real (&F)[D * D], real (&Q)[ns(D)]) {
     int rc;
     FMat<D> f;
     if (p.closed) {
@@ -807,15 +838,15 @@ PS_HD int discretize(const ModelParams<D>& p, double dt, double (&F)[D * D], dou
 // For the global first step pass F = 0, Q = P_inf (Eq. (7) PAPER.md:103-107 and
 // reading Z1: the observed first element is the KF update of N(0, P_inf)).
 template <int D, bool HU = false, class FT>
-PS_HD void fold_step(FAgg<D>& a, const FT& F, const double (&Q)[ns(D)],
-                     const ModelParams<D>& p, bool obs, double yk) {
-    double FA[D * D], Fb[D], Cm[ns(D)];
+PS_HD void fold_step(FAgg<D>& a, const FT& F, const real (&Q)[ns(D)],
+                     const ModelParams<D>& p, bool obs, real yk) {
+    real FA[D * D], Fb[D], Cm[ns(D)];
 #pragma unroll
     for (int i = 0; i < D; ++i) {
-        double sb = 0.0;
+        real sb = 0.0;
 #pragma unroll
         for (int j = 0; j < D; ++j) {
-            double sa = 0.0;
+            real sa = 0.0;
 #pragma unroll
             for (int k = 0; k < D; ++k)
                 if (FT::nz(i, k)) sa = fma(F(i, k), a.A[k * D + j], sa);
@@ -827,7 +858,7 @@ PS_HD void fold_step(FAgg<D>& a, const FT& F, const double (&Q)[ns(D)],
     cong_plus<D>(F, a.C, Q, Cm);
     // observation update; branchless: a missing y (Eqs. (6), (8)) is the same
     // formulas with 1/S and the innovation set to zero (A = F A, b = F b, C = C-)
-    double HC[D], w[D], hb, S;
+    real HC[D], w[D], hb, S;
     if (HU || p.h_unit) {
 #pragma unroll
         for (int i = 0; i < D; ++i) { HC[i] = Cm[si(D, i, 0)]; w[i] = FA[i]; }
@@ -837,7 +868,7 @@ PS_HD void fold_step(FAgg<D>& a, const FT& F, const double (&Q)[ns(D)],
         hb = 0.0; S = p.r;
 #pragma unroll
         for (int i = 0; i < D; ++i) {
-            double s = 0.0, ww = 0.0;
+            real s = 0.0, ww = 0.0;
 #pragma unroll
             for (int j = 0; j < D; ++j) {
                 s = fma(Cm[si(D, i, j)], p.H[j], s);
@@ -849,12 +880,12 @@ PS_HD void fold_step(FAgg<D>& a, const FT& F, const double (&Q)[ns(D)],
 #pragma unroll
         for (int i = 0; i < D; ++i) S = fma(p.H[i], HC[i], S);
     }
-    const double iS = obs ? rcp(S) : 0.0;
-    const double v = obs ? (yk - hb) : 0.0;
-    const double vs = v * iS;
+    const real iS = obs ? rcp(S) : 0.0;
+    const real v = obs ? (yk - hb) : 0.0;
+    const real vs = v * iS;
 #pragma unroll
     for (int i = 0; i < D; ++i) {
-        const double Kc = HC[i] * iS;
+        const real Kc = HC[i] * iS;
 #pragma unroll
         for (int j = 0; j < D; ++j) a.A[i * D + j] = fma(-Kc, w[j], FA[i * D + j]);
         a.b[i] = fma(HC[i], vs, Fb[i]);
@@ -875,12 +906,12 @@ PS_HD void fold_step(FAgg<D>& a, const FT& F, const double (&Q)[ns(D)],
 template <int D>
 PS_HD bool combine(const FAgg<D>& ei, const FAgg<D>& ej, FAgg<D>& out) {
     constexpr int NX = 2 * D + 1, NY = D + 1;
-    double M[D * D], MT[D * D], X[D * NX], Y[D * NY];
+    real M[D * D], MT[D * D], X[D * NX], Y[D * NY];
 #pragma unroll
     for (int r = 0; r < D; ++r) {
 #pragma unroll
         for (int c = 0; c < D; ++c) {
-            double s = (r == c) ? 1.0 : 0.0, st = s;
+            real s = (r == c) ? 1.0 : 0.0, st = s;
 #pragma unroll
             for (int k = 0; k < D; ++k) {
                 s = fma(ei.C[si(D, r, k)], ej.J[si(D, k, c)], s);     // (I + C_i J_j)
@@ -892,7 +923,7 @@ PS_HD bool combine(const FAgg<D>& ei, const FAgg<D>& ej, FAgg<D>& out) {
         // X rhs = [A_i | b_i + C_i eta_j | C_i]
 #pragma unroll
         for (int c = 0; c < D; ++c) X[r * NX + c] = ei.A[r * D + c];
-        double s = ei.b[r];
+        real s = ei.b[r];
 #pragma unroll
         for (int k = 0; k < D; ++k) s = fma(ei.C[si(D, r, k)], ej.eta[k], s);
         X[r * NX + D] = s;
@@ -901,12 +932,12 @@ PS_HD bool combine(const FAgg<D>& ei, const FAgg<D>& ej, FAgg<D>& out) {
         // Y rhs = [J_j A_i | eta_j - J_j b_i]
 #pragma unroll
         for (int c = 0; c < D; ++c) {
-            double u = 0.0;
+            real u = 0.0;
 #pragma unroll
             for (int k = 0; k < D; ++k) u = fma(ej.J[si(D, r, k)], ei.A[k * D + c], u);
             Y[r * NY + c] = u;
         }
-        double e = ej.eta[r];
+        real e = ej.eta[r];
 #pragma unroll
         for (int k = 0; k < D; ++k) e = fma(-ej.J[si(D, r, k)], ei.b[k], e);
         Y[r * NY + D] = e;
@@ -918,20 +949,20 @@ PS_HD bool combine(const FAgg<D>& ei, const FAgg<D>& ej, FAgg<D>& out) {
     bool ok;
     if constexpr (D <= 3) {
         // (I + J_j C_i) = (I + C_i J_j)^T (C, J symmetric): one inverse serves both solves
-        double Mi[D * D], Xo[D * NX], Yo[D * NY];
+        real Mi[D * D], Xo[D * NX], Yo[D * NY];
         ok = inv_small<D>(M, Mi);
 #pragma unroll
         for (int r = 0; r < D; ++r) {
 #pragma unroll
             for (int c = 0; c < NX; ++c) {
-                double t = 0.0;
+                real t = 0.0;
 #pragma unroll
                 for (int k = 0; k < D; ++k) t = fma(Mi[r * D + k], X[k * NX + c], t);
                 Xo[r * NX + c] = t;
             }
 #pragma unroll
             for (int c = 0; c < NY; ++c) {
-                double t = 0.0;
+                real t = 0.0;
 #pragma unroll
                 for (int k = 0; k < D; ++k) t = fma(Mi[k * D + r], Y[k * NY + c], t);
                 Yo[r * NY + c] = t;
@@ -947,13 +978,13 @@ PS_HD bool combine(const FAgg<D>& ei, const FAgg<D>& ej, FAgg<D>& out) {
     }
 #endif
     // A_ij = A_j X_A ; b_ij = A_j X_b + b_j ; C_ij = A_j X_C A_j^T + C_j
-    double AX[D * D];
+    real AX[D * D];
 #pragma unroll
     for (int r = 0; r < D; ++r) {
-        double sb = ej.b[r];
+        real sb = ej.b[r];
 #pragma unroll
         for (int c = 0; c < D; ++c) {
-            double sa = 0.0, sc = 0.0;
+            real sa = 0.0, sc = 0.0;
 #pragma unroll
             for (int k = 0; k < D; ++k) {
                 sa = fma(ej.A[r * D + k], X[k * NX + c], sa);
@@ -970,7 +1001,7 @@ PS_HD bool combine(const FAgg<D>& ei, const FAgg<D>& ej, FAgg<D>& out) {
     for (int r = 0; r < D; ++r)
 #pragma unroll
         for (int c = r; c < D; ++c) {
-            double s = ej.C[si(D, r, c)];
+            real s = ej.C[si(D, r, c)];
 #pragma unroll
             for (int k = 0; k < D; ++k) s = fma(AX[r * D + k], ej.A[c * D + k], s);
             out.C[si(D, r, c)] = s;
@@ -978,13 +1009,13 @@ PS_HD bool combine(const FAgg<D>& ei, const FAgg<D>& ej, FAgg<D>& out) {
     // eta_ij = A_i^T Y_eta + eta_i ; J_ij = A_i^T Y_J + J_i
 #pragma unroll
     for (int r = 0; r < D; ++r) {
-        double se = ei.eta[r];
+        real se = ei.eta[r];
 #pragma unroll
         for (int k = 0; k < D; ++k) se = fma(ei.A[k * D + r], Y[k * NY + D], se);
         out.eta[r] = se;
 #pragma unroll
         for (int c = r; c < D; ++c) {
-            double s = ei.J[si(D, r, c)];
+            real s = ei.J[si(D, r, c)];
 #pragma unroll
             for (int k = 0; k < D; ++k) s = fma(ei.A[k * D + r], Y[k * NY + c], s);
             out.J[si(D, r, c)] = s;
@@ -998,13 +1029,13 @@ PS_HD bool combine(const FAgg<D>& ei, const FAgg<D>& ej, FAgg<D>& out) {
 template <int D>
 PS_HD bool apply_prefix(const Gauss<D>& g, const FAgg<D>& a, Gauss<D>& out) {
     constexpr int NX = D + 1;
-    double M[D * D], X[D * NX];
+    real M[D * D], X[D * NX];
 #pragma unroll
     for (int r = 0; r < D; ++r) {
-        double s0 = g.x[r];
+        real s0 = g.x[r];
 #pragma unroll
         for (int c = 0; c < D; ++c) {
-            double s = (r == c) ? 1.0 : 0.0;
+            real s = (r == c) ? 1.0 : 0.0;
 #pragma unroll
             for (int k = 0; k < D; ++k) s = fma(g.P[si(D, r, k)], a.J[si(D, k, c)], s);
             M[r * D + c] = s;
@@ -1018,13 +1049,13 @@ PS_HD bool apply_prefix(const Gauss<D>& g, const FAgg<D>& a, Gauss<D>& out) {
 #else
     const bool ok = small_solve<D, NX>(M, X);
 #endif
-    double AX[D * D];
+    real AX[D * D];
 #pragma unroll
     for (int r = 0; r < D; ++r) {
-        double sx = a.b[r];
+        real sx = a.b[r];
 #pragma unroll
         for (int c = 0; c < D; ++c) {
-            double s = 0.0;
+            real s = 0.0;
 #pragma unroll
             for (int k = 0; k < D; ++k) s = fma(a.A[r * D + k], X[k * NX + c], s);
             AX[r * D + c] = s;
@@ -1037,7 +1068,7 @@ PS_HD bool apply_prefix(const Gauss<D>& g, const FAgg<D>& a, Gauss<D>& out) {
     for (int r = 0; r < D; ++r)
 #pragma unroll
         for (int c = r; c < D; ++c) {
-            double s = a.C[si(D, r, c)];
+            real s = a.C[si(D, r, c)];
 #pragma unroll
             for (int k = 0; k < D; ++k) s = fma(AX[r * D + k], a.A[c * D + k], s);
             out.P[si(D, r, c)] = s;
@@ -1049,13 +1080,13 @@ PS_HD bool apply_prefix(const Gauss<D>& g, const FAgg<D>& a, Gauss<D>& out) {
 // (E,g,L)_i (x) (E,g,L)_j = (E_i E_j, E_i g_j + g_i, E_i L_j E_i^T + L_i), i earlier.
 template <int D>
 PS_HD void combine(const SAgg<D>& ei, const SAgg<D>& ej, SAgg<D>& out) {
-    double EL[D * D];
+    real EL[D * D];
 #pragma unroll
     for (int r = 0; r < D; ++r) {
-        double sg = ei.g[r];
+        real sg = ei.g[r];
 #pragma unroll
         for (int c = 0; c < D; ++c) {
-            double se = 0.0, sl = 0.0;
+            real se = 0.0, sl = 0.0;
 #pragma unroll
             for (int k = 0; k < D; ++k) {
                 se = fma(ei.E[r * D + k], ej.E[k * D + c], se);
@@ -1071,7 +1102,7 @@ PS_HD void combine(const SAgg<D>& ei, const SAgg<D>& ej, SAgg<D>& out) {
     for (int r = 0; r < D; ++r)
 #pragma unroll
         for (int c = r; c < D; ++c) {
-            double s = ei.L[si(D, r, c)];
+            real s = ei.L[si(D, r, c)];
 #pragma unroll
             for (int k = 0; k < D; ++k) s = fma(EL[r * D + k], ei.E[c * D + k], s);
             out.L[si(D, r, c)] = s;
@@ -1081,13 +1112,13 @@ PS_HD void combine(const SAgg<D>& ei, const SAgg<D>& ej, SAgg<D>& out) {
 // Aggregate (E, g, L) (x) collapsed global suffix (0, m, P) = (0, E m + g, E P E^T + L).
 template <int D>
 PS_HD void apply_suffix(const SAgg<D>& a, const Gauss<D>& s, Gauss<D>& out) {
-    double EP[D * D];
+    real EP[D * D];
 #pragma unroll
     for (int r = 0; r < D; ++r) {
-        double sx = a.g[r];
+        real sx = a.g[r];
 #pragma unroll
         for (int c = 0; c < D; ++c) {
-            double t = 0.0;
+            real t = 0.0;
 #pragma unroll
             for (int k = 0; k < D; ++k) t = fma(a.E[r * D + k], s.P[si(D, k, c)], t);
             EP[r * D + c] = t;
@@ -1099,7 +1130,7 @@ PS_HD void apply_suffix(const SAgg<D>& a, const Gauss<D>& s, Gauss<D>& out) {
     for (int r = 0; r < D; ++r)
 #pragma unroll
         for (int c = r; c < D; ++c) {
-            double t = a.L[si(D, r, c)];
+            real t = a.L[si(D, r, c)];
 #pragma unroll
             for (int k = 0; k < D; ++k) t = fma(EP[r * D + k], a.E[c * D + k], t);
             out.P[si(D, r, c)] = t;
@@ -1109,14 +1140,14 @@ PS_HD void apply_suffix(const SAgg<D>& a, const Gauss<D>& s, Gauss<D>& out) {
 // ------------------------------------------------------------------ Kalman step (supplement PAPER.md:304-315)
 // Predict: xm = F x, FP = F P, Pm = FP F^T + Q.
 template <int D, class FT>
-PS_HD void kf_predict(const double (&x)[D], const double (&P)[ns(D)], const FT& F,
-                      const double (&Q)[ns(D)], double (&xm)[D], double (&FP)[D * D], double (&Pm)[ns(D)]) {
+PS_HD void kf_predict(const real (&x)[D], const real (&P)[ns(D)], const FT& F,
+                      const real (&Q)[ns(D)], real (&xm)[D], real (&FP)[D * D], real (&Pm)[ns(D)]) {
 #pragma unroll
     for (int i = 0; i < D; ++i) {
-        double sx = 0.0;
+        real sx = 0.0;
 #pragma unroll
         for (int j = 0; j < D; ++j) {
-            double s = 0.0;
+            real s = 0.0;
 #pragma unroll
             for (int k = 0; k < D; ++k)
                 if (FT::nz(i, k)) s = fma(F(i, k), P[si(D, k, j)], s);
@@ -1129,7 +1160,7 @@ PS_HD void kf_predict(const double (&x)[D], const double (&P)[ns(D)], const FT& 
     for (int i = 0; i < D; ++i)
 #pragma unroll
         for (int j = i; j < D; ++j) {
-            double s = Q[si(D, i, j)];
+            real s = Q[si(D, i, j)];
 #pragma unroll
             for (int k = 0; k < D; ++k)
                 if (FT::nz(j, k)) s = fma(FP[i * D + k], F(j, k), s);
@@ -1139,11 +1170,11 @@ PS_HD void kf_predict(const double (&x)[D], const double (&P)[ns(D)], const FT& 
 
 // Predict without F P: xm = F x, Pm = F P F^T + Q (the structured congruence for Jordan F).
 template <int D, class FT>
-PS_HD void kf_predict_pm(const double (&x)[D], const double (&P)[ns(D)], const FT& F, const double (&Q)[ns(D)],
-                         double (&xm)[D], double (&Pm)[ns(D)]) {
+PS_HD void kf_predict_pm(const real (&x)[D], const real (&P)[ns(D)], const FT& F, const real (&Q)[ns(D)],
+                         real (&xm)[D], real (&Pm)[ns(D)]) {
 #pragma unroll
     for (int i = 0; i < D; ++i) {
-        double sx = 0.0;
+        real sx = 0.0;
 #pragma unroll
         for (int j = 0; j < D; ++j)
             if (FT::nz(i, j)) sx = fma(F(i, j), x[j], sx);
@@ -1154,12 +1185,12 @@ PS_HD void kf_predict_pm(const double (&x)[D], const double (&P)[ns(D)], const F
 
 // Sm = Sg F^T (general Sg)
 template <int D, class FT>
-PS_HD void mul_bt(const double (&Sg)[D * D], const FT& F, double (&Sm)[D * D]) {
+PS_HD void mul_bt(const real (&Sg)[D * D], const FT& F, real (&Sm)[D * D]) {
 #pragma unroll
     for (int i = 0; i < D; ++i)
 #pragma unroll
         for (int j = 0; j < D; ++j) {
-            double s = 0.0;
+            real s = 0.0;
 #pragma unroll
             for (int l = 0; l < D; ++l)
                 if (FT::nz(j, l)) s = fma(Sg[i * D + l], F(j, l), s);
@@ -1172,44 +1203,44 @@ PS_HD void mul_bt(const double (&Sg)[D * D], const FT& F, double (&Sm)[D * D]) {
 // (adjugate) inverse with ONE reciprocal (short dependency chain; relative
 // error ~ cond(S) eps, cond(P-) ~ 2e4 on the metric workload); larger D: LDL^T.
 template <int D, int NR>
-PS_HD bool spd_solve(const double (&S)[ns(D)], double (&R)[D * NR]) {
+PS_HD bool spd_solve(const real (&S)[ns(D)], real (&R)[D * NR]) {
     if constexpr (D == 1) {
         const bool ok = S[0] > 0.0;
-        const double i0 = rcp(S[0]);
+        const real i0 = rcp(S[0]);
 #pragma unroll
         for (int k = 0; k < NR; ++k) R[k] *= i0;
         return ok;
     } else if constexpr (D == 2) {
-        const double a = S[0], b = S[1], d = S[2];
-        const double det = fma(a, d, -b * b);
+        const real a = S[0], b = S[1], d = S[2];
+        const real det = fma(a, d, -b * b);
         const bool ok = (a > 0.0) && (det > 0.0);
-        const double id = rcp(det);
-        const double i00 = d * id, i01 = -b * id, i11 = a * id;
+        const real id = rcp(det);
+        const real i00 = d * id, i01 = -b * id, i11 = a * id;
 #pragma unroll
         for (int k = 0; k < NR; ++k) {
-            const double r0 = R[k], r1 = R[NR + k];
+            const real r0 = R[k], r1 = R[NR + k];
             R[k] = fma(i00, r0, i01 * r1);
             R[NR + k] = fma(i01, r0, i11 * r1);
         }
         return ok;
     } else if constexpr (D == 3) {
-        const double a = S[0], b = S[1], c = S[2], d = S[3], e = S[4], f = S[5];
-        const double A00 = fma(d, f, -e * e), A01 = fma(c, e, -b * f), A02 = fma(b, e, -c * d);
-        const double A11 = fma(a, f, -c * c), A12 = fma(b, c, -a * e), A22 = fma(a, d, -b * b);
-        const double det = fma(a, A00, fma(b, A01, c * A02));
+        const real a = S[0], b = S[1], c = S[2], d = S[3], e = S[4], f = S[5];
+        const real A00 = fma(d, f, -e * e), A01 = fma(c, e, -b * f), A02 = fma(b, e, -c * d);
+        const real A11 = fma(a, f, -c * c), A12 = fma(b, c, -a * e), A22 = fma(a, d, -b * b);
+        const real det = fma(a, A00, fma(b, A01, c * A02));
         const bool ok = (a > 0.0) && (A22 > 0.0) && (det > 0.0);
-        const double id = rcp(det);
-        const double i00 = A00 * id, i01 = A01 * id, i02 = A02 * id, i11 = A11 * id, i12 = A12 * id, i22 = A22 * id;
+        const real id = rcp(det);
+        const real i00 = A00 * id, i01 = A01 * id, i02 = A02 * id, i11 = A11 * id, i12 = A12 * id, i22 = A22 * id;
 #pragma unroll
         for (int k = 0; k < NR; ++k) {
-            const double r0 = R[k], r1 = R[NR + k], r2 = R[2 * NR + k];
+            const real r0 = R[k], r1 = R[NR + k], r2 = R[2 * NR + k];
             R[k] = fma(i00, r0, fma(i01, r1, i02 * r2));
             R[NR + k] = fma(i01, r0, fma(i11, r1, i12 * r2));
             R[2 * NR + k] = fma(i02, r0, fma(i12, r1, i22 * r2));
         }
         return ok;
     } else {
-        double Lo[D * D], id[D];
+        real Lo[D * D], id[D];
         const bool ok = ldlt<D>(S, Lo, id);
         ldlt_solve<D, NR>(Lo, id, R);
         return ok;
@@ -1225,9 +1256,9 @@ PS_HD bool spd_solve(const double (&S)[ns(D)], double (&R)[D * NR]) {
 // and the predicted (xm, Pm) of step k1+1 it is
 //   E = Sm Pm^-1,  g = x0 - E xm,  L = P0 - E Sm^T.
 template <int D>
-PS_HD bool chain_smoother_agg(const double (&x0)[D], const double (&P0)[ns(D)], const double (&Sm)[D * D],
-                              const double (&xm)[D], const double (&Pm)[ns(D)], SAgg<D>& out) {
-    double Et[D * D];
+PS_HD bool chain_smoother_agg(const real (&x0)[D], const real (&P0)[ns(D)], const real (&Sm)[D * D],
+                              const real (&xm)[D], const real (&Pm)[ns(D)], SAgg<D>& out) {
+    real Et[D * D];
 #pragma unroll
     for (int i = 0; i < D; ++i)
 #pragma unroll
@@ -1235,7 +1266,7 @@ PS_HD bool chain_smoother_agg(const double (&x0)[D], const double (&P0)[ns(D)], 
     const bool ok = spd_solve<D, D>(Pm, Et);  // Et = Pm^-1 Sm^T = E^T
 #pragma unroll
     for (int i = 0; i < D; ++i) {
-        double s = x0[i];
+        real s = x0[i];
 #pragma unroll
         for (int j = 0; j < D; ++j) {
             out.E[i * D + j] = Et[j * D + i];
@@ -1247,7 +1278,7 @@ PS_HD bool chain_smoother_agg(const double (&x0)[D], const double (&P0)[ns(D)], 
     for (int i = 0; i < D; ++i)
 #pragma unroll
         for (int j = i; j < D; ++j) {
-            double s = P0[si(D, i, j)];
+            real s = P0[si(D, i, j)];
 #pragma unroll
             for (int k = 0; k < D; ++k) s = fma(-Et[k * D + i], Sm[j * D + k], s);
             out.L[si(D, i, j)] = s;
@@ -1260,32 +1291,32 @@ PS_HD bool chain_smoother_agg(const double (&x0)[D], const double (&P0)[ns(D)], 
 // smoothed (ms, Ps) at k+1, overwrite (ms, Ps) with the smoothed moments at k.
 // G_k = P F^T Pm^-1 via an LDL^T solve of Pm G_k^T = F P.
 template <int D>
-PS_HD bool rts_step(const double (&x)[D], const double (&P)[ns(D)], const double (&xm)[D],
-                    const double (&Pm)[ns(D)], const double (&FP)[D * D], double (&ms)[D],
-                    double (&Ps)[ns(D)]) {
-    double Gt[D * D];
+PS_HD bool rts_step(const real (&x)[D], const real (&P)[ns(D)], const real (&xm)[D],
+                    const real (&Pm)[ns(D)], const real (&FP)[D * D], real (&ms)[D],
+                    real (&Ps)[ns(D)]) {
+    real Gt[D * D];
 #pragma unroll
     for (int i = 0; i < D * D; ++i) Gt[i] = FP[i];
     const bool ok = spd_solve<D, D>(Pm, Gt);   // Gt = Pm^-1 F P = G^T, G[i][j] = Gt[j][i]
-    double dm[D], T[D * D];
+    real dm[D], T[D * D];
 #pragma unroll
     for (int i = 0; i < D; ++i) dm[i] = ms[i] - xm[i];
 #pragma unroll
     for (int i = 0; i < D; ++i) {
-        double s = x[i];
+        real s = x[i];
 #pragma unroll
         for (int j = 0; j < D; ++j) s = fma(Gt[j * D + i], dm[j], s);
         ms[i] = s;
     }
     // T = G (Ps - Pm)
-    double dP[ns(D)];
+    real dP[ns(D)];
 #pragma unroll
     for (int i = 0; i < ns(D); ++i) dP[i] = Ps[i] - Pm[i];
 #pragma unroll
     for (int i = 0; i < D; ++i)
 #pragma unroll
         for (int j = 0; j < D; ++j) {
-            double s = Gt[i] * dP[si(D, 0, j)];
+            real s = Gt[i] * dP[si(D, 0, j)];
 #pragma unroll
             for (int k = 1; k < D; ++k) s = fma(Gt[k * D + i], dP[si(D, k, j)], s);
             T[i * D + j] = s;
@@ -1294,7 +1325,7 @@ PS_HD bool rts_step(const double (&x)[D], const double (&P)[ns(D)], const double
     for (int i = 0; i < D; ++i)
 #pragma unroll
         for (int j = i; j < D; ++j) {
-            double s = P[si(D, i, j)];
+            real s = P[si(D, i, j)];
 #pragma unroll
             for (int k = 0; k < D; ++k) s = fma(T[i * D + k], Gt[k * D + j], s);
             Ps[si(D, i, j)] = s;
@@ -1302,4 +1333,4 @@ PS_HD bool rts_step(const double (&x)[D], const double (&P)[ns(D)], const double
     return ok;
 }
 
-}  // namespace pssgp
+}  // namespace PSSGP_NS
