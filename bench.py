@@ -44,12 +44,14 @@ FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
 THROTTLE_BAD = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
 
 
-def _ncu_row(kernel: str):
+def _ncu_row(kernel: str, f32: bool = False):
     """Row of `kernel` in the latest committed ncu summary (profiles/*/ncu_full_*_summary.csv,
-    written by tools/make_profile_summary.py; DRAM bytes in GB)."""
+    written by tools/make_profile_summary.py; DRAM bytes in GB).  Captures of the fp32 build are
+    tagged *f32* and used only for the f32 configuration."""
     import csv
     import glob
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "ncu_full_*_summary.csv")))
+    files = sorted(f for f in glob.glob(os.path.join(ROOT, "profiles", "*", "ncu_full_*_summary.csv"))
+                   if ("f32" in os.path.basename(f)) == f32)
     for f in reversed(files):
         for row in csv.DictReader(open(f)):
             if kernel + "<" in row["Kernel Name"]:
@@ -57,9 +59,9 @@ def _ncu_row(kernel: str):
     return None, None
 
 
-def ncu_traffic(kernel: str):
+def ncu_traffic(kernel: str, f32: bool = False):
     """dram read+write bytes per launch of `kernel` from one `ncu --set full` capture."""
-    row, src = _ncu_row(kernel)
+    row, src = _ncu_row(kernel, f32)
     if row is None:
         return None, None
     return (float(row["dram__bytes_read.sum"]) + float(row["dram__bytes_write.sum"])) * 1e9, src
@@ -400,9 +402,9 @@ def main():
     fps = {k: flops_per_step(k) for k in ("k_filter_reduce", "k_filter_apply", "k_smoother_apply")}
     flops = (fps.get(dom, 0.0) * n_local
              if model.state_dim == 3 and not args.uniform and args.config in ("metric", "c2", "c5") else None)
-    plan = model.plan(n_local)
+    plan = model.plan(n_local, f32=args.config == "f32")
     launches = int(sum(v[1] for v in kern.values()))
-    traffic, traffic_src = ncu_traffic(dom)
+    traffic, traffic_src = ncu_traffic(dom, args.config == "f32")
     # the binding roofline of the dominant kernel is the larger of its two floors:
     # algorithmic bytes / HBM peak and executed fp64 flops / fp64 peak
     hbm_frac = hbm_gbs / pk.get("hbm_gbs")

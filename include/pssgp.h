@@ -249,6 +249,10 @@ pssgp_status pssgp_debug_discretize(const pssgp_model* m, double dt, double* F, 
 /* Launch plan for N steps: steps per chain, number of chains, CTAs, threads/CTA. */
 pssgp_status pssgp_plan(pssgp_model* m, int64_t N, int64_t* chain_len, int64_t* n_chains,
                         int* n_blocks, int* threads_per_block);
+/* The same for pssgp_posterior_f32 (its kernels' occupancy); PSSGP_E_UNSUPPORTED for models
+ * the fp32 path does not cover. */
+pssgp_status pssgp_plan_f32(pssgp_model* m, int64_t N, int64_t* chain_len, int64_t* n_chains,
+                            int* n_blocks, int* threads_per_block);
 
 /* Optional per-kernel timing with CUDA events recorded on the launch stream.
  * pssgp_profile_enable(m, 1) starts recording; pssgp_profile_read synchronises

@@ -26,7 +26,7 @@ __all__ = ["Model", "PssgpError", "build", "lib", "pssgp_create", "pssgp_destroy
            "pssgp_aggregate_bytes", "pssgp_shard_filter_reduce", "pssgp_shard_filter_apply",
            "pssgp_shard_smoother_apply", "pssgp_profile_enable", "pssgp_profile_read", "pssgp_profile_name",
            "pssgp_merge_grid", "pssgp_gather", "pssgp_predict", "pssgp_posterior_batched", "pssgp_nll_grad_batched",
-           "pssgp_posterior_f32"]
+           "pssgp_posterior_f32", "pssgp_plan_f32"]
 
 
 def _ptr(x) -> Optional[int]:
@@ -191,6 +191,13 @@ def pssgp_plan(h, N: int):
     return dict(chain_len=K.value, n_chains=nch.value, n_blocks=nb.value, threads=thr.value)
 
 
+def pssgp_plan_f32(h, N: int):
+    K = ctypes.c_int64(); nch = ctypes.c_int64(); nb = ctypes.c_int(); thr = ctypes.c_int()
+    _raise(h, lib().pssgp_plan_f32(h, int(N), ctypes.byref(K), ctypes.byref(nch), ctypes.byref(nb),
+                                   ctypes.byref(thr)))
+    return dict(chain_len=K.value, n_chains=nch.value, n_blocks=nb.value, threads=thr.value)
+
+
 def pssgp_profile_enable(h, on: bool = True) -> None:
     lib().pssgp_profile_enable(h, 1 if on else 0)
 
@@ -324,5 +331,5 @@ class Model:
     def discretize(self, dt: float):
         return pssgp_debug_discretize(self.h, dt)
 
-    def plan(self, N: int):
-        return pssgp_plan(self.h, N)
+    def plan(self, N: int, f32: bool = False):
+        return pssgp_plan_f32(self.h, N) if f32 else pssgp_plan(self.h, N)

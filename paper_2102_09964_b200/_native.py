@@ -89,6 +89,8 @@ SIGNATURES = {
     "pssgp_debug_discretize": (ctypes.c_int, [_vp, ctypes.c_double, _dp, _dp]),
     "pssgp_plan": (ctypes.c_int, [_vp, _i64, ctypes.POINTER(_i64), ctypes.POINTER(_i64),
                                   ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),
+    "pssgp_plan_f32": (ctypes.c_int, [_vp, _i64, ctypes.POINTER(_i64), ctypes.POINTER(_i64),
+                                  ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),
     "pssgp_profile_enable": (None, [_vp, ctypes.c_int]),
     "pssgp_profile_read": (ctypes.c_int, [_vp, _dp, ctypes.POINTER(_i64), ctypes.c_int]),
     "pssgp_profile_name": (ctypes.c_char_p, [ctypes.c_int]),

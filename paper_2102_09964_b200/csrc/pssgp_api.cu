@@ -867,7 +867,21 @@ pssgp_status pssgp_nll(pssgp_model* m, int64_t N, const double* t, const double*
 }
 
 // Optional fp32 path: the thread-per-chain kernels compiled with fp32 state
-// (pssgp_f32.cu); single Matern components only.
+// (pssgp_f32.cu); single Matern components only.  Same one-wave plan as make_plan with the fp32
+// kernels' occupancy (fewer registers: 4 CTAs / SM at d = 3).
+Plan make_plan_f32(pssgp_model* m, int64_t N) {
+    if (m->occ32 == 0) m->occ32 = pssgp_f32::occupancy(m->d);
+    const int bps = m->blocks_per_sm > 0 ? m->blocks_per_sm : m->occ32;
+    const int64_t target_chains = static_cast<int64_t>(m->sm_count) * bps * kThreads;
+    Plan pl;
+    int64_t K = m->forced_K > 0 ? m->forced_K : std::max<int64_t>(kWin, (N + target_chains - 1) / target_chains);
+    if (m->forced_K <= 0) K = ((K + kWin - 1) / kWin) * kWin;
+    pl.K = K;
+    pl.nch = std::max<int64_t>(1, (N + K - 1) / K);
+    pl.nb = static_cast<int>((pl.nch + kThreads - 1) / kThreads);
+    return pl;
+}
+
 pssgp_status pssgp_posterior_f32(pssgp_model* m, int64_t N, const double* t, const double* y, const uint8_t* mask,
                                  double* mean, double* var, double* nll, void* stream) {
     pssgp_status st = check_args(m, N, t, y, mask);
@@ -885,19 +899,14 @@ pssgp_status pssgp_posterior_f32(pssgp_model* m, int64_t N, const double* t, con
         }
         return PSSGP_OK;
     }
-    if (m->occ32 == 0) m->occ32 = pssgp_f32::occupancy(m->d);
-    const int bps = m->blocks_per_sm > 0 ? m->blocks_per_sm : m->occ32;
-    const int64_t target_chains = static_cast<int64_t>(m->sm_count) * bps * kThreads;
-    int64_t K = m->forced_K > 0 ? m->forced_K : std::max<int64_t>(kWin, (N + target_chains - 1) / target_chains);
-    if (m->forced_K <= 0) K = ((K + kWin - 1) / kWin) * kWin;
-    const int64_t nch = std::max<int64_t>(1, (N + K - 1) / K);
+    const Plan pl = make_plan_f32(m, N);
     pssgp_f32::Run r;
     std::memset(&r, 0, sizeof(r));
     r.d = m->d;
     r.n = N;
-    r.K = K;
-    r.nb = static_cast<int>((nch + kThreads - 1) / kThreads);
-    const size_t need = pssgp_f32::ws_bytes(m->d, K, r.nb);
+    r.K = pl.K;
+    r.nb = pl.nb;
+    const size_t need = pssgp_f32::ws_bytes(m->d, pl.K, r.nb);
     if (need > m->ws_bytes) {
         if (m->ws) cudaFree(m->ws);
         m->ws = nullptr;
@@ -1329,6 +1338,20 @@ pssgp_status pssgp_debug_discretize(const pssgp_model* m, double dt, double* F, 
         return (tab || zero) ? PSSGP_OK : PSSGP_E_UNSUPPORTED;
     }
     DISPATCH_D(mm, debug_disc<D_>(m, dt, F, Q));
+}
+
+pssgp_status pssgp_plan_f32(pssgp_model* m, int64_t N, int64_t* chain_len, int64_t* n_chains, int* n_blocks,
+                            int* threads_per_block) {
+    if (!m || N < 0) return PSSGP_E_ARG;
+    if (!m->closed || m->d > 3) return PSSGP_E_UNSUPPORTED;
+    pssgp_status st = ensure_device(m);
+    if (st) return st;
+    const Plan pl = make_plan_f32(m, N);
+    if (chain_len) *chain_len = pl.K;
+    if (n_chains) *n_chains = pl.nch;
+    if (n_blocks) *n_blocks = pl.nb;
+    if (threads_per_block) *threads_per_block = kThreads;
+    return PSSGP_OK;
 }
 
 pssgp_status pssgp_plan(pssgp_model* m, int64_t N, int64_t* chain_len, int64_t* n_chains, int* n_blocks,
