@@ -197,8 +197,11 @@ Plan make_plan(pssgp_model* m, int64_t n) {
     const int bps = m->blocks_per_sm > 0 ? m->blocks_per_sm : m->occ;
     const int64_t target_chains = static_cast<int64_t>(m->sm_count) * bps * kThreads;
     Plan pl;
-    int64_t K = m->forced_K > 0 ? m->forced_K : std::max<int64_t>(kWin, (n + target_chains - 1) / target_chains);
-    if (m->forced_K <= 0) K = ((K + kWin - 1) / kWin) * kWin;
+    // one wave of chains; K rounded up to whole staging windows, except below one window, where
+    // short chains (down to one step) keep the wave full at small N (the paper's N = 1,200 / 3,200
+    // problems run in ~40 instead of ~70 us: the latency is the scan span, tools/small_n_sweep.py)
+    int64_t K = m->forced_K > 0 ? m->forced_K : std::max<int64_t>(1, (n + target_chains - 1) / target_chains);
+    if (m->forced_K <= 0 && K > kWin / 4) K = ((K + kWin - 1) / kWin) * kWin;
     pl.K = K;
     pl.nch = std::max<int64_t>(1, (n + K - 1) / K);
     pl.nb = static_cast<int>((pl.nch + kThreads - 1) / kThreads);
@@ -874,8 +877,8 @@ Plan make_plan_f32(pssgp_model* m, int64_t N) {
     const int bps = m->blocks_per_sm > 0 ? m->blocks_per_sm : m->occ32;
     const int64_t target_chains = static_cast<int64_t>(m->sm_count) * bps * kThreads;
     Plan pl;
-    int64_t K = m->forced_K > 0 ? m->forced_K : std::max<int64_t>(kWin, (N + target_chains - 1) / target_chains);
-    if (m->forced_K <= 0) K = ((K + kWin - 1) / kWin) * kWin;
+    int64_t K = m->forced_K > 0 ? m->forced_K : std::max<int64_t>(1, (N + target_chains - 1) / target_chains);
+    if (m->forced_K <= 0 && K > kWin / 4) K = ((K + kWin - 1) / kWin) * kWin;
     pl.K = K;
     pl.nch = std::max<int64_t>(1, (N + K - 1) / K);
     pl.nb = static_cast<int>((pl.nch + kThreads - 1) / kThreads);
