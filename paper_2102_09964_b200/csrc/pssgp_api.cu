@@ -298,7 +298,7 @@ pssgp_status phase_smoother(pssgp_model* m, KParams<D>& p, cudaStream_t s) {
 
 pssgp_status nll_sum(pssgp_model* m, const double* parts, int nb, double* out, cudaStream_t s) {
     ProfScope ps(m, S_K6, s);
-    k_nll_sum<<<1, 256, 0, s>>>(parts, nb, out);
+    k_nll_sum<<<1, kThreads, 0, s>>>(parts, nb, out);
     LAUNCH_CHECK(m, "k_nll_sum");
     return PSSGP_OK;
 }
@@ -649,8 +649,8 @@ pssgp_status wide_posterior(pssgp_model* m, int64_t N, const double* t, const do
     if (smooth) {
         p.sagg = wide_scan_s<D>(m, p, s, st);
         if (st) return st;
-        p.nll_out = nll;
-        return wide_sapply<D>(m, p, pl.nb, s);
+        p.nll_out = nullptr;   // summed by k_nll_sum as on the NLL-only path: bit-identical NLL
+        if ((st = wide_sapply<D>(m, p, pl.nb, s))) return st;
     }
     if (nll) return nll_sum(m, p.nll_chain, p.nch, nll, s);
     return PSSGP_OK;

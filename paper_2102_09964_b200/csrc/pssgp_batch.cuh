@@ -381,6 +381,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_smoother_apply(c
 #pragma unroll
                 for (int i = 0; i < CN(D); ++i) nx[i] = src[i * 32];
             }
+            if (PSSGP_K5_PF > 0 && k - PSSGP_K5_PF >= kb) prefetch_state_l2<D>(xpw, lane, k - PSSGP_K5_PF - kb);
             if (k == s.end - 1) {   // series end: terminal element
 #pragma unroll
                 for (int i = 0; i < D; ++i) ms[i] = x[i];

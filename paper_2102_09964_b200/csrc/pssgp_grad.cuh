@@ -28,6 +28,10 @@
 #include "pssgp_kernels.cuh"
 #include "pssgp_batch.cuh"
 
+#ifndef PSSGP_GRAD_PF
+#define PSSGP_GRAD_PF 4   // k_grad_fold: L2 prefetch distance (steps) of the filtered state, 0 = off
+#endif
+
 namespace pssgp {
 
 template <int D>
@@ -389,6 +393,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_grad_fold(const KParams<D> p, d
         }
         grad_fold_step3<D>(A, x, P, to_full<D>(Fj), Q, z, p.m, first, obs, yk);
         tprev = tk;
+        if (PSSGP_GRAD_PF > 0 && k + PSSGP_GRAD_PF < ke) prefetch_state_l2<D>(xpw, lane, k + PSSGP_GRAD_PF - kb);
         const double* src = xpw + ((k - kb) * CN(D)) * 32;
 #pragma unroll
         for (int i = 0; i < D; ++i) x[i] = src[i * 32];
@@ -481,6 +486,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_batch_grad_fold(const KParams<D
         mp.s2 = s.s2;
         grad_fold_step3<D>(A, x, P, to_full<D>(Fj), Q, z, mp, first, obs, yk);
         tprev = tk;
+        if (PSSGP_GRAD_PF > 0 && k + PSSGP_GRAD_PF < ke) prefetch_state_l2<D>(xpw, lane, k + PSSGP_GRAD_PF - kb);
         const double* src = xpw + ((k - kb) * CN(D)) * 32;
 #pragma unroll
         for (int i = 0; i < D; ++i) x[i] = src[i * 32];

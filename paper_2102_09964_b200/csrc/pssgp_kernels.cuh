@@ -47,6 +47,9 @@ constexpr int kThreads = PSSGP_THREADS;
 constexpr int kWarps = kThreads / 32;
 constexpr int kWin = 16;                // staging window (steps) per chain
 constexpr int kCarryThreads = 256;      // single-CTA scan kernels
+#ifndef PSSGP_K5_PF
+#define PSSGP_K5_PF 2                   // K5: L2 prefetch distance (steps) of the filtered state, 0 = off
+#endif
 
 // error word: (class << 56) | (index << 8) | code; atomicMin keeps data errors
 // (input / unsupported dt, class 0) ahead of their numerical consequences
@@ -829,6 +832,18 @@ __device__ __forceinline__ Gauss<D> smoother_chain_carry(const KParams<D>& p, SA
     return res;
 }
 
+// L2 prefetch of a warp's filtered state at chain-relative step kp: the 32 chains' (xbar, P) of
+// one step are one contiguous run of CN * 32 reals in the [warp][K][CN][32] layout, fetched as one
+// 128-byte line per lane into L2 (no registers held, unlike a deeper register prefetch).
+template <int D>
+__device__ __forceinline__ void prefetch_state_l2(const real* xpw, int lane, int64_t kp) {
+    constexpr int kLines = (CN(D) * 32 * static_cast<int>(sizeof(real)) + 127) / 128;
+    if (lane < kLines) {
+        const char* a = reinterpret_cast<const char*>(xpw - lane + (kp * CN(D)) * 32) + lane * 128;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+    }
+}
+
 // ------------------------------------------------------------------ K5: RTS rescan
 // f-space projection: mean = H m^s, var = H P^s H^T
 template <int D>
@@ -949,6 +964,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_smoother_apply(const K
 #pragma unroll
                     for (int i = 0; i < CN(D); ++i) nx[i] = src[i * 32];
                 }
+                if (PSSGP_K5_PF > 0 && k - PSSGP_K5_PF >= kb) prefetch_state_l2<D>(xpw, lane, k - PSSGP_K5_PF - kb);
                 FT_t<D, MODE> F;
             real Q[ns(D)], xm[D], Pm[ns(D)], FP[D * D];
                 disc<D, MODE>(p.m, tnext - tk, F, Q);
@@ -983,23 +999,12 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_smoother_apply(const K
 }
 
 // ------------------------------------------------------------------ K6: deterministic NLL sum
-__global__ void __launch_bounds__(256, 1) k_nll_sum(const double* __restrict__ parts, int nb, double* out) {
-    __shared__ double red[8];
-    const int per = (nb + 255) / 256;
-    double s = 0.0;
-    for (int i = 0; i < per; ++i) {
-        const int b = threadIdx.x * per + i;
-        if (b < nb) s += parts[b];
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double tsum = 0.0;
-        for (int w = 0; w < 8; ++w) tsum += red[w];
-        *out = tsum;
-    }
+// The same fixed-order CTA sum (cta_sum, kThreads threads) as K5's CTA 0 uses, so the NLL-only
+// path returns bit-for-bit the NLL of the full posterior.  Launch <<<1, kThreads>>>.
+__global__ void __launch_bounds__(kThreads, 1) k_nll_sum(const double* __restrict__ parts, int nb, double* out) {
+    __shared__ double red[kWarps];
+    const double v = cta_sum(parts, nb, red);
+    if (threadIdx.x == 0) *out = v;
 }
 
 // ------------------------------------------------------------------ chunk aggregate reducers (sharded path, 1 CTA)
