@@ -427,9 +427,10 @@ def main():
     per_launch_ms = dom_ms / dom_launches
     alg_b = (ALG_BYTES_F32 if args.config == "f32" else ALG_BYTES).get(dom, 0) * n_local
     hbm_gbs = alg_b / (per_launch_ms * 1e-3) / 1e9
-    fps = {k: flops_per_step(k) for k in ("k_filter_reduce", "k_filter_apply", "k_smoother_apply")}
+    fps = {k: flops_per_step(k) for k in ("k_filter_reduce", "k_filter_apply", "k_smoother_apply", "k_grad_fold")}
     flops = (fps.get(dom, 0.0) * n_local
-             if model.state_dim == 3 and not args.uniform and args.config in ("metric", "c2", "c5") else None)
+             if model.state_dim == 3 and not args.uniform and args.config in ("metric", "c2", "c5", "grad")
+             and fps.get(dom) else None)
     plan = model.plan(n_local, f32=args.config == "f32")
     launches = int(sum(v[1] for v in kern.values()))
     traffic, traffic_src = ncu_traffic(dom, args.config == "f32")
@@ -460,7 +461,7 @@ def main():
         "per_kernel_ms_per_step": {k: v[0] / args.steps for k, v in kern.items()},
         "path_alg_bytes_per_step": path_b,
         "path_hbm_frac": path_b * N / (ms_step * 1e-3) / 1e9 / pk.get("hbm_gbs"),
-        "path_fp64_frac": (sum(fps.values()) * N / (ms_step * 1e-3) / 1e12 / FP64_PEAK_TFLOPS)
+        "path_fp64_frac": (sum(fps[k] for k in kern if fps.get(k)) * N / (ms_step * 1e-3) / 1e12 / FP64_PEAK_TFLOPS)
         if flops else None})
     cpu = None
     if not args.no_cpu_baseline:

@@ -47,6 +47,9 @@ constexpr int kThreads = PSSGP_THREADS;
 constexpr int kWarps = kThreads / 32;
 constexpr int kWin = 16;                // staging window (steps) per chain
 constexpr int kCarryThreads = 256;      // single-CTA scan kernels
+#ifndef PSSGP_TY_PF
+#define PSSGP_TY_PF 1                   // K5: L2 prefetch distance (staging windows) of t; 0 = off
+#endif
 #ifndef PSSGP_K5_PF
 #define PSSGP_K5_PF 2                   // K5: L2 prefetch distance (steps) of the filtered state, 0 = off
 #endif
@@ -183,6 +186,16 @@ __device__ __forceinline__ void issue_window(AsyncStage& s, int buf, const doubl
                                              const double* __restrict__ y, int64_t wbase, int64_t K, int64_t n,
                                              int64_t j0, int lane) {
     issue_copies<true>(s.t[buf], s.y[buf], t, y, wbase, K, n, j0, lane);
+}
+
+// L2 prefetch of this lane's chain at chain-relative step j (t, and y when WITH_Y).
+template <bool WITH_Y>
+__device__ __forceinline__ void prefetch_ty_l2(const double* __restrict__ t, const double* __restrict__ y,
+                                               int64_t kb, int64_t j, int64_t ke) {
+    if (kb + j < ke) {
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(t + kb + j));
+        if (WITH_Y) asm volatile("prefetch.global.L2 [%0];" ::"l"(y + kb + j));
+    }
 }
 
 // ------------------------------------------------------------------ mask words
@@ -945,6 +958,8 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_smoother_apply(const K
         const int64_t j0 = w * kWinA;
         const int buf = static_cast<int>(w & 1);
         if (w > 0) issue_copies<false>(so[wid].t[buf ^ 1], nullptr, p.t, nullptr, wbase, p.K, p.n, j0 - kWinA, lane);
+        if (PSSGP_TY_PF > 0 && j0 - (1 + PSSGP_TY_PF) * kWinA >= 0)
+            prefetch_ty_l2<false>(p.t, nullptr, kb, j0 - (1 + PSSGP_TY_PF) * kWinA, ke);
         else cp_async_commit();
         cp_async_wait<1>();
         __syncwarp();
