@@ -123,3 +123,14 @@ def test_f32_input_errors_and_unsupported(cuda_device):
     with pytest.raises(P.PssgpError) as e:
         m3.posterior_f32(t3, y3, k3)
     assert e.value.status == _native.PSSGP_E_UNSUPPORTED
+
+
+def test_f32_empty_and_plan(cuda_device):
+    w = synth.random_problem(3, 100, kind="matern32")
+    m = P.Model(w.components, w.noise_var)
+    e = torch.empty(0, dtype=torch.float64, device="cuda:0")
+    mean, var, nll = m.posterior_f32(e, e, torch.empty(0, dtype=torch.uint8, device="cuda:0"))
+    m.check()
+    assert float(nll.cpu()[0]) == 0.0
+    pl = m.plan(2 ** 24, f32=True)
+    assert pl["chain_len"] * pl["n_chains"] >= 2 ** 24 and pl["threads"] == 128

@@ -172,3 +172,41 @@ def test_grad_batched_unsupported_model(cuda_device):
     out = torch.empty(3, dtype=torch.float64, device="cuda:0")
     with pytest.raises(P.PssgpError):
         P.pssgp_nll_grad_batched(m.h, 1, off, None, None, None, n, t, y, mk, out[:1], out)
+
+
+def test_grad_batched_invalid_offsets_and_missing_series(cuda_device):
+    """Offsets that do not partition [0, N) -> PSSGP_E_INPUT; an all-missing series has NLL 0 and
+    gradient 0 while its neighbours stay exact."""
+    from paper_2102_09964_b200 import _native
+    dev = "cuda:0"
+    m = P.Model([synth.Component("matern32", 1.0, 0.5)], 0.01, chain_len=16)
+    n = 1000
+    t = torch.linspace(0, 1, n, dtype=torch.float64, device=dev)
+    y = torch.zeros(n, dtype=torch.float64, device=dev)
+    mk = torch.ones(n, dtype=torch.uint8, device=dev)
+    nll = torch.empty(2, dtype=torch.float64, device=dev)
+    g = torch.empty(6, dtype=torch.float64, device=dev)
+    for bad in ([0, 600, 900], [0, 700, 300], [5, 500, n]):
+        off = torch.tensor(bad, dtype=torch.int64, device=dev)
+        P.pssgp_nll_grad_batched(m.h, 2, off, None, None, None, n, t, y, mk, nll, g)
+        with pytest.raises(P.PssgpError) as e:
+            m.check()
+        assert e.value.status == _native.PSSGP_E_INPUT
+    ws = _batched_problem("matern32", [700, 500, 900], seed=5)
+    ws[1].mask[:] = 0
+    off = np.array([0, 700, 1200, 2100], np.int64)
+    T, Y, MK = (torch.from_numpy(np.concatenate([getattr(w, a) for w in ws])).to(dev) for a in ("t", "y", "mask"))
+    VB, EB, RB = (torch.tensor([f(w) for w in ws], dtype=torch.float64, device=dev) for f in
+                  (lambda w: w.components[0].variance, lambda w: w.components[0].lengthscale, lambda w: w.noise_var))
+    nll = torch.empty(3, dtype=torch.float64, device=dev)
+    g = torch.empty(9, dtype=torch.float64, device=dev)
+    P.pssgp_nll_grad_batched(m.h, 3, torch.from_numpy(off).to(dev), VB, EB, RB, 2100, T, Y, MK, nll, g)
+    m.check()
+    nll, g = nll.cpu().numpy(), g.cpu().numpy().reshape(3, 3)
+    assert nll[1] == 0.0 and np.all(g[1] == 0.0)
+    for b in (0, 2):
+        w = ws[b]
+        c = w.components[0]
+        nll_r, g_r = og.kf_nll_grad(c.kind, c.variance, c.lengthscale, w.noise_var, w.t, w.y, w.mask)
+        assert abs(nll[b] - nll_r) <= NLL_TOL * max(abs(nll_r), 1.0)
+        assert np.all(np.abs(g[b] - g_r) / (np.abs(g_r) + w.mask.sum() + 1) <= GRAD_TOL)
