@@ -1032,6 +1032,15 @@ pssgp_status pssgp_predict(pssgp_model* m, int64_t n_train, const double* t_trai
     return pssgp_gather(m, n_test, idx, mean, var, mean_test, var_test, stream);
 }
 
+// the launch plan the batched kernels use (same as make_plan<D>; sizes the NLL piece buffers)
+Plan batch_plan(pssgp_model* m, int64_t N) {
+    switch (m->d) {
+        case 1: return make_plan<1>(m, N);
+        case 2: return make_plan<2>(m, N);
+        default: return make_plan<3>(m, N);
+    }
+}
+
 pssgp_status pssgp_posterior_batched(pssgp_model* m, int nseg, const int64_t* offsets, const double* variance,
                                      const double* lengthscale, const double* noise_var, int64_t N,
                                      const double* t, const double* y, const uint8_t* mask, double* mean,
@@ -1043,7 +1052,9 @@ pssgp_status pssgp_posterior_batched(pssgp_model* m, int nseg, const int64_t* of
     if ((st = ensure_device(m))) return st;
     auto s = static_cast<cudaStream_t>(stream);
     m->last_stream = s;
-    const size_t need = static_cast<size_t>(std::max<int64_t>(N, 1)) * sizeof(double);
+    const Plan bpl = batch_plan(m, std::max<int64_t>(N, 1));
+    const size_t nchp = static_cast<size_t>(bpl.nb) * kThreads;
+    const size_t need = 2 * nchp * sizeof(double);   // NLL head / tail pieces per chain
     if (need > m->bt_bytes) {
         if (m->bt) cudaFree(m->bt);
         m->bt = nullptr;
@@ -1061,7 +1072,8 @@ pssgp_status pssgp_posterior_batched(pssgp_model* m, int nseg, const int64_t* of
     q.ell = lengthscale;
     q.noise = noise_var;
     q.sqrt2nu = std::sqrt(2.0 * m->d - 1.0);
-    q.nll_step = m->bt;
+    q.nll_head = m->bt;
+    q.nll_tail = m->bt + nchp;
     q.nll_seg = nll;
     pssgp::batch::k_batch_check_offsets<<<(nseg + 256) / 256, 256, 0, s>>>(offsets, nseg, N, m->d_err);
     LAUNCH_CHECK(m, "k_batch_check_offsets");
@@ -1085,12 +1097,10 @@ pssgp_status pssgp_posterior_batched(pssgp_model* m, int nseg, const int64_t* of
 #undef BATCH_RUN
             default: return fail(m, PSSGP_E_UNSUPPORTED, "state dimension");
         }
-    } else {
-        cudaMemsetAsync(m->bt, 0, sizeof(double), s);
     }
     {
         ProfScope ps(m, S_K6, s);
-        pssgp::batch::k_batch_nll<<<(nseg + 3) / 4, 128, 0, s>>>(q);
+        pssgp::batch::k_batch_nll<<<(nseg + 3) / 4, 128, 0, s>>>(q, bpl.K);
     }
     LAUNCH_CHECK(m, "k_batch_nll");
     return PSSGP_OK;
@@ -1107,7 +1117,9 @@ pssgp_status pssgp_nll_grad_batched(pssgp_model* m, int nseg, const int64_t* off
     if ((st = ensure_device(m))) return st;
     auto s = static_cast<cudaStream_t>(stream);
     m->last_stream = s;
-    const size_t need = static_cast<size_t>(std::max<int64_t>(N, 1)) * sizeof(double);
+    const Plan bpl = batch_plan(m, std::max<int64_t>(N, 1));
+    const size_t nchp = static_cast<size_t>(bpl.nb) * kThreads;
+    const size_t need = 2 * nchp * sizeof(double);   // NLL head / tail pieces per chain
     if (need > m->bt_bytes) {
         if (m->bt) cudaFree(m->bt);
         m->bt = nullptr;
@@ -1125,7 +1137,8 @@ pssgp_status pssgp_nll_grad_batched(pssgp_model* m, int nseg, const int64_t* off
     q.ell = lengthscale;
     q.noise = noise_var;
     q.sqrt2nu = std::sqrt(2.0 * m->d - 1.0);
-    q.nll_step = m->bt;
+    q.nll_head = m->bt;
+    q.nll_tail = m->bt + nchp;
     q.nll_seg = nll;
     pssgp::batch::k_batch_check_offsets<<<(nseg + 256) / 256, 256, 0, s>>>(offsets, nseg, N, m->d_err);
     LAUNCH_CHECK(m, "k_batch_check_offsets");
@@ -1141,9 +1154,9 @@ pssgp_status pssgp_nll_grad_batched(pssgp_model* m, int nseg, const int64_t* off
         KParams<DD> p;                                                                                     \
         if ((st = setup<DD>(m, pl, p))) return st;                                                         \
         p.t = t; p.y = y; p.mask = mask; p.n = N; p.k0 = 0; p.nglob = N;                                   \
-        const size_t nchp = static_cast<size_t>(pl.nb) * kThreads;                                        \
+        const size_t gnch = static_cast<size_t>(pl.nb) * kThreads;                                        \
         const size_t na = sizeof(TAgg3<DD>) / sizeof(double);                                             \
-        const size_t gneed = 2 * nchp * na * sizeof(double);                                               \
+        const size_t gneed = 2 * gnch * na * sizeof(double);                                               \
         if (gneed > m->gb_bytes) {                                                                         \
             if (m->gb) cudaFree(m->gb);                                                                    \
             m->gb = nullptr;                                                                               \
@@ -1155,7 +1168,7 @@ pssgp_status pssgp_nll_grad_batched(pssgp_model* m, int nseg, const int64_t* off
             m->gb_bytes = gneed;                                                                           \
         }                                                                                                  \
         double* head = m->gb;                                                                              \
-        double* tail = m->gb + nchp * na;                                                                  \
+        double* tail = m->gb + gnch * na;                                                                  \
         { ProfScope ps(m, S_K1, s); pssgp::batch::k_batch_filter_reduce<DD><<<pl.nb, kThreads, 0, s>>>(p, q); } \
         LAUNCH_CHECK(m, "k_batch_filter_reduce");                                                          \
         { ProfScope ps(m, S_K3, s); pssgp::batch::k_batch_filter_apply<DD><<<pl.nb, kThreads, 0, s>>>(p, q); } \
@@ -1164,6 +1177,8 @@ pssgp_status pssgp_nll_grad_batched(pssgp_model* m, int nseg, const int64_t* off
         LAUNCH_CHECK(m, "k_batch_grad_fold");                                                              \
         { ProfScope ps(m, S_RED, s); k_batch_grad_combine<DD><<<(nseg + 127) / 128, 128, 0, s>>>(q, pl.K, head, tail, grad); } \
         LAUNCH_CHECK(m, "k_batch_grad_combine");                                                           \
+        { ProfScope ps(m, S_RED, s); k_batch_grad_combine_long<DD><<<nseg, kThreads, 0, s>>>(q, pl.K, head, tail, grad); } \
+        LAUNCH_CHECK(m, "k_batch_grad_combine_long");                                                      \
         break;                                                                                             \
     }
         BGRAD_RUN(1) BGRAD_RUN(2) BGRAD_RUN(3)
@@ -1172,7 +1187,7 @@ pssgp_status pssgp_nll_grad_batched(pssgp_model* m, int nseg, const int64_t* off
     }
     {
         ProfScope ps(m, S_K6, s);
-        pssgp::batch::k_batch_nll<<<(nseg + 3) / 4, 128, 0, s>>>(q);
+        pssgp::batch::k_batch_nll<<<(nseg + 3) / 4, 128, 0, s>>>(q, bpl.K);
     }
     LAUNCH_CHECK(m, "k_batch_nll");
     return PSSGP_OK;

@@ -26,7 +26,10 @@ struct BParams {
     const double* ell;      // [nseg] lengthscale (nullable: model's)
     const double* noise;    // [nseg] sigma_n,b^2 (nullable: model's)
     double sqrt2nu;         // sqrt(2 nu) of the model's Matern order
-    double* nll_step;       // [N] per-step NLL terms
+    double* nll_head;       // [chains] NLL of chain start .. first series end in the chain (or the whole
+                            //          chain) when that series started in an earlier chain
+    double* nll_tail;       // [chains] NLL of the last series start in the chain .. chain end when that
+                            //          series continues past the chain
     double* nll_seg;        // [nseg] per-series NLL
 };
 
@@ -149,12 +152,12 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_filter_reduce(co
 }
 
 // ------------------------------------------------------------------ K3b: Kalman rescan
-// Staged inputs as in K3; the per-step NLL terms go through a transposed shared tile and
-// leave in coalesced stores once per window.
+// Staged inputs as in K3.  NLL per (chain, series) piece: a series inside the chain is written to
+// nll_seg directly, the pieces of series crossing the chain's ends go to nll_head / nll_tail and
+// are summed per series by k_batch_nll (as k_batch_grad_combine composes the gradient pieces).
 template <int D>
 __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_filter_apply(const KParams<D> p, const BParams q) {
     __shared__ AsyncStage st[kWarps];
-    __shared__ double nst[kWarps][kWinA][33];
     __shared__ FAgg<D> tot[kWarps];
     __shared__ Gauss<D> wcar[kWarps];
     __shared__ SAgg<D> stot[kWarps];
@@ -177,7 +180,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_filter_apply(con
     double tprev = (kb > 0 && kb < ke) ? __ldg(p.t + kb - 1) : 0.0;
     SAgg<D> sag;
     set_identity(sag);
-    bool sag_done = false;
+    bool sag_done = false, head_done = false;
     int ferr = -1;
     double quad = 0.0, prodm = 1.0;
     long long prode = 0;
@@ -247,17 +250,15 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_filter_apply(con
                     for (int j = i; j < D; ++j) P0[si(D, i, j)] = fma(-si_, SH[j], P0[si(D, i, j)]);
                 }
             }
-            // NLL of the (chain, series) segment: running v^2/S sum and S product (one log per
-            // segment, written at the segment's last step; every other step contributes 0)
+            // NLL of the (chain, series) piece: running v^2/S sum and S product (one log per piece)
             nll_accumulate(obs, v, vs, S, quad, prodm, prode, nobs);
-            double term = 0.0;
-            if (k == s.end - 1 || k == ke - 1) {
-                if (nobs > 0)
-                    term = 0.5 * (quad + log(prodm) + static_cast<double>(prode) * 0.6931471805599453 +
-                                  nobs * 1.8378770664093453);
+            if (k == s.end - 1) {
+                const double term = nobs > 0 ? 0.5 * (quad + log(prodm) + static_cast<double>(prode) * 0.6931471805599453 +
+                                                      nobs * 1.8378770664093453) : 0.0;
+                if (s.start >= kb) q.nll_seg[s.b] = term;           // the whole series is in this chain
+                else if (!head_done) { q.nll_head[c] = term; head_done = true; }
                 quad = 0.0; prodm = 1.0; prode = 0; nobs = 0;
             }
-            nst[wid][jj][lane] = term;
             if (k == s.end - 1 && !sag_done) {
                 // first series end in this chain: the chain's smoother aggregate is the collapsed
                 // (0, m^s_k0, P^s_k0) of that series (terminal element)
@@ -276,20 +277,14 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_filter_apply(con
             for (int i = 0; i < ns(D); ++i) o[(D + i) * 32] = P[i];
         }
         __syncwarp();
-        {   // coalesced flush of the window's NLL terms (row r = chain wbase/K + r)
-            const int col = lane & (kWinA - 1), rb = lane / kWinA;
-            const int64_t j = j0 + col;
-#pragma unroll
-            for (int i = 0; i < 32 / (32 / kWinA); ++i) {
-                const int r = rb + (32 / kWinA) * i;
-                const int64_t idx = wbase + r * p.K + j;
-                const int64_t rend = min(wbase + (r + 1) * p.K, p.n);
-                if (j < p.K && idx < rend) q.nll_step[idx] = nst[wid][col][r];
-            }
-        }
-        __syncwarp();
     }
     if (ferr >= 0) raise_error(p.err, kb + ferr, kErrNumeric);
+    if (ke > kb && s.end > ke) {                  // a series continues past the chain end
+        const double term = nobs > 0 ? 0.5 * (quad + log(prodm) + static_cast<double>(prode) * 0.6931471805599453 +
+                                              nobs * 1.8378770664093453) : 0.0;
+        if (s.start >= kb) q.nll_tail[c] = term;  // it started in this chain
+        else q.nll_head[c] = term;                // it runs through the whole chain
+    }
     if (ke > kb && !sag_done) {
         // the next step exists and belongs to the same series (a series end would have set sag)
         const double tn = __ldg(p.t + ke);
@@ -433,13 +428,21 @@ __global__ void __launch_bounds__(256) k_batch_check_offsets(const int64_t* __re
 }
 
 // ------------------------------------------------------------------ per-series NLL (1 warp per series)
-__global__ void __launch_bounds__(128) k_batch_nll(const BParams q) {
+// Per-series NLL of series that cross chain boundaries: tail(c1) + head(c1+1) + ... + head(c2)
+// (fixed order, one warp per series); series inside one chain were written by K3b, empty ones get 0.
+__global__ void __launch_bounds__(128) k_batch_nll(const BParams q, int64_t K) {
     const int lane = threadIdx.x & 31;
     const int b = blockIdx.x * 4 + (threadIdx.x >> 5);
     if (b >= q.nseg) return;
     const int64_t a0 = __ldg(q.off + b), a1 = __ldg(q.off + b + 1);
-    double s = 0.0;
-    for (int64_t k = a0 + lane; k < a1; k += 32) s += q.nll_step[k];
+    if (a1 <= a0) {
+        if (lane == 0) q.nll_seg[b] = 0.0;
+        return;
+    }
+    const int64_t c1 = a0 / K, c2 = (a1 - 1) / K;
+    if (c1 == c2) return;
+    double s = lane == 0 ? q.nll_tail[c1] : 0.0;
+    for (int64_t c = c1 + 1 + lane; c <= c2; c += 32) s += q.nll_head[c];
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
     if (lane == 0) q.nll_seg[b] = s;

@@ -430,7 +430,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_grad_fold(const KParams<D> p, d
 // that lies inside one chain is finished in the fold, and a series spanning chains c1..c2 is the
 // ordered product  tail(c1) o head(c1+1) o ... o head(c2)  of the pieces the fold stores (head =
 // chain start .. first series end in the chain, or the whole chain; tail = last series start in
-// the chain .. chain end), composed by k_batch_grad_combine (one thread per series).
+// the chain .. chain end), composed by k_batch_grad_combine (one CTA per series).
 template <int D>
 __global__ void __launch_bounds__(kThreads, 2) k_batch_grad_fold(const KParams<D> p, const batch::BParams q,
                                                                  double* head, double* tail, double* grad_seg) {
@@ -509,6 +509,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_batch_grad_fold(const KParams<D
     }
 }
 
+// A series spanning chains c1..c2 is tail(c1) (x) head(c1+1) (x) ... (x) head(c2).  Short spans
+// (<= kSerialSpan chains): one thread per series composes in order (k_batch_grad_combine); long
+// spans: one CTA per series, the bracket an ordered CTA-wide reduction (k_batch_grad_combine_long,
+// cta_reduce_range: O(chains / kThreads + log) operator levels instead of a serial chain).
+constexpr int64_t kSerialSpan = 64;
+
 template <int D>
 __global__ void __launch_bounds__(128) k_batch_grad_combine(const batch::BParams q, int64_t K, const double* head,
                                                             const double* tail, double* grad_seg) {
@@ -521,7 +527,7 @@ __global__ void __launch_bounds__(128) k_batch_grad_combine(const batch::BParams
         return;
     }
     const int64_t c1 = a0 / K, c2 = (a1 - 1) / K;
-    if (c1 == c2) return;                         // finished by the fold
+    if (c1 == c2 || c2 - c1 > kSerialSpan) return;   // finished by the fold / the long-span kernel
     TAgg3<D> acc;
     load_aos(acc, tail + c1 * NA);
     for (int64_t cc = c1 + 1; cc <= c2; ++cc) {
@@ -532,6 +538,27 @@ __global__ void __launch_bounds__(128) k_batch_grad_combine(const batch::BParams
     }
 #pragma unroll
     for (int j = 0; j < 3; ++j) grad_seg[3 * b + j] = acc.a[j];
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads) k_batch_grad_combine_long(const batch::BParams q, int64_t K,
+                                                                      const double* head, const double* tail,
+                                                                      double* grad_seg) {
+    constexpr int NA = sizeof(TAgg3<D>) / sizeof(double);
+    __shared__ TAgg3<D> wred[kWarps];
+    const int b = blockIdx.x;
+    const int64_t a0 = __ldg(q.off + b), a1 = __ldg(q.off + b + 1);
+    if (a1 <= a0) return;
+    const int64_t c1 = a0 / K, c2 = (a1 - 1) / K;
+    if (c2 - c1 <= kSerialSpan) return;
+    const TAgg3<D> rest = cta_reduce_range<TAgg3<D>>(head, static_cast<int>(c1 + 1), static_cast<int>(c2 + 1), wred);
+    if (threadIdx.x == 0) {
+        TAgg3<D> t, r;
+        load_aos(t, tail + c1 * NA);
+        combine(t, rest, r);
+#pragma unroll
+        for (int j = 0; j < 3; ++j) grad_seg[3 * b + j] = r.a[j];
+    }
 }
 
 }  // namespace pssgp
