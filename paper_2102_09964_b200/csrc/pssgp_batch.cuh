@@ -178,8 +178,6 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_filter_apply(con
     Seg s;
     if (kb < ke) seg_load(s, p, q, seg_find(q, kb));
     double tprev = (kb > 0 && kb < ke) ? __ldg(p.t + kb - 1) : 0.0;
-    SAgg<D> sag;
-    set_identity(sag);
     bool sag_done = false, head_done = false;
     int ferr = -1;
     double quad = 0.0, prodm = 1.0;
@@ -261,13 +259,16 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_filter_apply(con
             }
             if (k == s.end - 1 && !sag_done) {
                 // first series end in this chain: the chain's smoother aggregate is the collapsed
-                // (0, m^s_k0, P^s_k0) of that series (terminal element)
+                // (0, m^s_k0, P^s_k0) of that series (terminal element), stored at
+                // once (not held in registers across the loop)
+                SAgg<D> sag;
 #pragma unroll
                 for (int i = 0; i < D * D; ++i) sag.E[i] = 0.0;
 #pragma unroll
                 for (int i = 0; i < D; ++i) sag.g[i] = x0[i];
 #pragma unroll
                 for (int i = 0; i < ns(D); ++i) sag.L[i] = P0[i];
+                store_soa(sag, p.chain_s, nch, c);
                 sag_done = true;
             }
             double* o = p.xp + ((wg * p.K + (k - kb)) * CN(D)) * 32 + lane;
@@ -285,17 +286,23 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_filter_apply(con
         if (s.start >= kb) q.nll_tail[c] = term;  // it started in this chain
         else q.nll_head[c] = term;                // it runs through the whole chain
     }
-    if (ke > kb && !sag_done) {
-        // the next step exists and belongs to the same series (a series end would have set sag)
-        const double tn = __ldg(p.t + ke);
-        FJor<D> F;
-        double Q[ns(D)], xm[D], Pm[ns(D)], Sm[D * D];
-        matern_closed<D>(s.lam, s.s2, tn - tprev, F, Q);
-        kf_predict_pm<D>(x, P, F, Q, xm, Pm);
-        mul_bt<D>(Sg, F, Sm);
-        if (!chain_smoother_agg<D>(x0, P0, Sm, xm, Pm, sag)) raise_error(p.err, ke, kErrNumeric);
+    SAgg<D> sag;
+    if (sag_done) {
+        load_soa(sag, p.chain_s, nch, c);
+    } else {
+        set_identity(sag);
+        if (ke > kb) {
+            // the next step exists and belongs to the same series (a series end would have set sag)
+            const double tn = __ldg(p.t + ke);
+            FJor<D> F;
+            double Q[ns(D)], xm[D], Pm[ns(D)], Sm[D * D];
+            matern_closed<D>(s.lam, s.s2, tn - tprev, F, Q);
+            kf_predict_pm<D>(x, P, F, Q, xm, Pm);
+            mul_bt<D>(Sg, F, Sm);
+            if (!chain_smoother_agg<D>(x0, P0, Sm, xm, Pm, sag)) raise_error(p.err, ke, kErrNumeric);
+        }
+        store_soa(sag, p.chain_s, nch, c);
     }
-    store_soa(sag, p.chain_s, nch, c);
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
         SAgg<D> o;
@@ -357,6 +364,8 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_smoother_apply(c
         const int64_t j0 = w * kWinA;
         const int buf = static_cast<int>(w & 1);
         if (w > 0) issue_copies<false>(so[wid].t[buf ^ 1], nullptr, p.t, nullptr, wbase, p.K, p.n, j0 - kWinA, lane);
+        if (PSSGP_TY_PF > 0 && j0 - (1 + PSSGP_TY_PF) * kWinA >= 0)
+            prefetch_ty_l2<false>(p.t, nullptr, kb, j0 - (1 + PSSGP_TY_PF) * kWinA, ke);
         else cp_async_commit();
         cp_async_wait<1>();
         __syncwarp();
