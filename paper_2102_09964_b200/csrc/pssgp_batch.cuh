@@ -364,9 +364,9 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_smoother_apply(c
         const int64_t j0 = w * kWinA;
         const int buf = static_cast<int>(w & 1);
         if (w > 0) issue_copies<false>(so[wid].t[buf ^ 1], nullptr, p.t, nullptr, wbase, p.K, p.n, j0 - kWinA, lane);
+        else cp_async_commit();
         if (PSSGP_TY_PF > 0 && j0 - (1 + PSSGP_TY_PF) * kWinA >= 0)
             prefetch_ty_l2<false>(p.t, nullptr, kb, j0 - (1 + PSSGP_TY_PF) * kWinA, ke);
-        else cp_async_commit();
         cp_async_wait<1>();
         __syncwarp();
         const int jstart = static_cast<int>(min(static_cast<int64_t>(kWinA - 1), ke - 1 - (kb + j0)));

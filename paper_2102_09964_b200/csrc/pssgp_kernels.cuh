@@ -48,7 +48,7 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kWin = 16;                // staging window (steps) per chain
 constexpr int kCarryThreads = 256;      // single-CTA scan kernels
 #ifndef PSSGP_TY_PF
-#define PSSGP_TY_PF 1                   // K5: L2 prefetch distance (staging windows) of t; 0 = off
+#define PSSGP_TY_PF 0                   // K5: L2 prefetch distance (staging windows) of t; 0 = off (measured: no gain)
 #endif
 #ifndef PSSGP_K5_PF
 #define PSSGP_K5_PF 2                   // K5: L2 prefetch distance (steps) of the filtered state, 0 = off
@@ -958,9 +958,9 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_smoother_apply(const K
         const int64_t j0 = w * kWinA;
         const int buf = static_cast<int>(w & 1);
         if (w > 0) issue_copies<false>(so[wid].t[buf ^ 1], nullptr, p.t, nullptr, wbase, p.K, p.n, j0 - kWinA, lane);
+        else cp_async_commit();
         if (PSSGP_TY_PF > 0 && j0 - (1 + PSSGP_TY_PF) * kWinA >= 0)
             prefetch_ty_l2<false>(p.t, nullptr, kb, j0 - (1 + PSSGP_TY_PF) * kWinA, ke);
-        else cp_async_commit();
         cp_async_wait<1>();
         __syncwarp();
         const int jstart = static_cast<int>(min(static_cast<int64_t>(kWinA - 1), ke - 2 - (kb + j0)));
