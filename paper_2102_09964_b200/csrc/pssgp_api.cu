@@ -70,12 +70,14 @@ struct pssgp_model {
     double* fq = nullptr;                 // wide path, kPade mode: per-step (F, Q)
     size_t fq_bytes = 0;
     // pipelined host API (pssgp_posterior_host_async): two slots, each with its own stream and
-    // device I/O buffers; computes are chained in call order through acompute
+    // device I/O buffers; inputs, computes (one stream, call order) and outputs on separate streams
     char* aio[2] = {nullptr, nullptr};
     size_t aio_bytes[2] = {0, 0};
-    cudaStream_t astream[2] = {nullptr, nullptr};
-    cudaEvent_t acompute = nullptr;
-    bool acompute_rec = false;
+    cudaStream_t astream[2] = {nullptr, nullptr};   // per slot: host -> device copies
+    cudaStream_t aout[2] = {nullptr, nullptr};      // per slot: device -> host copies
+    cudaStream_t acs = nullptr;                      // computes, in call order
+    cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
+    bool arec[2] = {false, false};                   // the slot has a previous call
     int aslot = 0;
     cudaStream_t last_stream = nullptr;
     int64_t err_index = -1;
@@ -833,8 +835,12 @@ void pssgp_destroy(pssgp_model* m) {
     for (int i = 0; i < 2; ++i) {
         if (m->aio[i]) cudaFree(m->aio[i]);
         if (m->astream[i]) cudaStreamDestroy(m->astream[i]);
+        if (m->aout[i]) cudaStreamDestroy(m->aout[i]);
+        if (m->ev_in[i]) cudaEventDestroy(m->ev_in[i]);
+        if (m->ev_comp[i]) cudaEventDestroy(m->ev_comp[i]);
+        if (m->ev_out[i]) cudaEventDestroy(m->ev_out[i]);
     }
-    if (m->acompute) cudaEventDestroy(m->acompute);
+    if (m->acs) cudaStreamDestroy(m->acs);
     if (m->d_err) cudaFree(m->d_err);
     if (m->d_model) cudaFree(m->d_model);
     for (int s = 0; s < kSlots; ++s)
@@ -1262,16 +1268,20 @@ pssgp_status pssgp_posterior_host_async(pssgp_model* m, int64_t N, const double*
     pssgp_status st = check_args(m, N, t, y, mask);
     if (st) return st;
     if ((st = ensure_device(m))) return st;
-    if (!m->astream[0]) {
-        for (int i = 0; i < 2; ++i)
-            if (cudaStreamCreateWithFlags(&m->astream[i], cudaStreamNonBlocking) != cudaSuccess)
-                return fail(m, PSSGP_E_CUDA, "cudaStreamCreate");
-        if (cudaEventCreateWithFlags(&m->acompute, cudaEventDisableTiming) != cudaSuccess)
-            return fail(m, PSSGP_E_CUDA, "cudaEventCreate");
+    if (!m->acs) {
+        bool ok = cudaStreamCreateWithFlags(&m->acs, cudaStreamNonBlocking) == cudaSuccess;
+        for (int i = 0; i < 2; ++i) {
+            ok = ok && cudaStreamCreateWithFlags(&m->astream[i], cudaStreamNonBlocking) == cudaSuccess;
+            ok = ok && cudaStreamCreateWithFlags(&m->aout[i], cudaStreamNonBlocking) == cudaSuccess;
+            ok = ok && cudaEventCreateWithFlags(&m->ev_in[i], cudaEventDisableTiming) == cudaSuccess;
+            ok = ok && cudaEventCreateWithFlags(&m->ev_comp[i], cudaEventDisableTiming) == cudaSuccess;
+            ok = ok && cudaEventCreateWithFlags(&m->ev_out[i], cudaEventDisableTiming) == cudaSuccess;
+        }
+        if (!ok) return fail(m, PSSGP_E_CUDA, "cudaStreamCreate / cudaEventCreate");
     }
     const int slot = m->aslot;
     m->aslot ^= 1;
-    cudaStream_t s = m->astream[slot];
+    cudaStream_t sin = m->astream[slot], sout = m->aout[slot], sc = m->acs;
     const size_t nd = static_cast<size_t>(N);
     const size_t need = nd * (8 + 8 + 8 + 8) + nd + 64;
     if (need > m->aio_bytes[slot]) {
@@ -1290,20 +1300,30 @@ pssgp_status pssgp_posterior_host_async(pssgp_model* m, int64_t N, const double*
     double* dmean = dy + nd;
     double* dvar = dmean + nd;
     uint8_t* dmask = reinterpret_cast<uint8_t*>(dvar + nd);
-    if (N > 0) {   // host -> device on this slot's stream (overlaps the other slot's device -> host)
-        cudaMemcpyAsync(dt_, t, nd * 8, cudaMemcpyHostToDevice, s);
-        cudaMemcpyAsync(dy, y, nd * 8, cudaMemcpyHostToDevice, s);
-        cudaMemcpyAsync(dmask, mask, nd, cudaMemcpyHostToDevice, s);
+    // host -> device: the slot's input buffers are free once its previous compute has run; the copy
+    // does not wait for that call's device -> host copies (separate stream), so consecutive calls'
+    // inputs stream back to back while earlier outputs drain the other direction
+    if (m->arec[slot]) cudaStreamWaitEvent(sin, m->ev_comp[slot], 0);
+    if (N > 0) {
+        cudaMemcpyAsync(dt_, t, nd * 8, cudaMemcpyHostToDevice, sin);
+        cudaMemcpyAsync(dy, y, nd * 8, cudaMemcpyHostToDevice, sin);
+        cudaMemcpyAsync(dmask, mask, nd, cudaMemcpyHostToDevice, sin);
     }
-    if (m->acompute_rec) cudaStreamWaitEvent(s, m->acompute, 0);   // computes run in call order
+    cudaEventRecord(m->ev_in[slot], sin);
+    // compute (one stream: calls in order, never sharing the GPU): after the inputs, and after the
+    // slot's previous outputs have left (the compute overwrites them)
+    cudaStreamWaitEvent(sc, m->ev_in[slot], 0);
+    if (m->arec[slot]) cudaStreamWaitEvent(sc, m->ev_out[slot], 0);
     st = pssgp_posterior(m, N, dt_, dy, dmask, mean ? dmean : nullptr, var ? dvar : nullptr, nll ? dnll : nullptr,
-                         s);
+                         sc);
     if (st) return st;
-    cudaEventRecord(m->acompute, s);
-    m->acompute_rec = true;
-    if (N > 0 && mean) cudaMemcpyAsync(mean, dmean, nd * 8, cudaMemcpyDeviceToHost, s);
-    if (N > 0 && var) cudaMemcpyAsync(var, dvar, nd * 8, cudaMemcpyDeviceToHost, s);
-    if (nll) cudaMemcpyAsync(nll, dnll, 8, cudaMemcpyDeviceToHost, s);
+    cudaEventRecord(m->ev_comp[slot], sc);
+    cudaStreamWaitEvent(sout, m->ev_comp[slot], 0);
+    if (N > 0 && mean) cudaMemcpyAsync(mean, dmean, nd * 8, cudaMemcpyDeviceToHost, sout);
+    if (N > 0 && var) cudaMemcpyAsync(var, dvar, nd * 8, cudaMemcpyDeviceToHost, sout);
+    if (nll) cudaMemcpyAsync(nll, dnll, 8, cudaMemcpyDeviceToHost, sout);
+    cudaEventRecord(m->ev_out[slot], sout);
+    m->arec[slot] = true;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(m, e, "pssgp_posterior_host_async copies");
     return PSSGP_OK;
@@ -1311,11 +1331,14 @@ pssgp_status pssgp_posterior_host_async(pssgp_model* m, int64_t N, const double*
 
 pssgp_status pssgp_sync(pssgp_model* m) {
     if (!m) return PSSGP_E_ARG;
-    for (int i = 0; i < 2; ++i)
-        if (m->astream[i]) {
-            cudaError_t e = cudaStreamSynchronize(m->astream[i]);
+    for (int i = 0; i < 2; ++i) {
+        if (m->aout[i]) {
+            cudaError_t e = cudaStreamSynchronize(m->aout[i]);
             if (e != cudaSuccess) return cuda_fail(m, e, "cudaStreamSynchronize(async)");
         }
+        if (m->astream[i]) cudaStreamSynchronize(m->astream[i]);
+    }
+    if (m->acs) cudaStreamSynchronize(m->acs);
     return pssgp_check(m);
 }
 

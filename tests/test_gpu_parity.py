@@ -549,3 +549,26 @@ def test_cuda_graph_replay(cuda_device):
         torch.cuda.synchronize()
         ref = P.Model(w.components, w.noise_var).posterior(*to_dev(w))
         assert torch.equal(mean, ref[0]) and torch.equal(var, ref[1]) and torch.equal(nll, ref[2])
+
+
+def test_host_async_slot_reuse(cuda_device):
+    """Six same-size calls: each slot's device buffers are reused while earlier outputs are still
+    draining on the copy-out streams (the input / compute / output event chain)."""
+    m = P.Model([synth.Component("matern32", 1.0, 0.5)], 0.02)
+    n = 200_000
+    ws = [synth.random_problem(70 + i, n, kind="matern32", p_missing=0.2, variance=1.0, lengthscale=0.5,
+                               noise_var=0.02) for i in range(6)]
+    ins, outs = [], []
+    for w in ws:
+        th, yh, mh = (torch.from_numpy(a).pin_memory() for a in (w.t, w.y, w.mask))
+        mo = torch.empty(n, dtype=torch.float64).pin_memory()
+        vo = torch.empty_like(mo)
+        no = torch.zeros(1, dtype=torch.float64).pin_memory()
+        ins.append((th, yh, mh))
+        outs.append((mo, vo, no))
+    for (th, yh, mh), (mo, vo, no) in zip(ins, outs):
+        P.pssgp_posterior_host_async(m.h, n, th, yh, mh, mo, vo, no)
+    P.pssgp_sync(m.h)
+    for w, (mo, vo, no) in zip(ws, outs):
+        mean, var, nll = m.posterior_host(w.t, w.y, w.mask)
+        assert np.array_equal(mo.numpy(), mean) and np.array_equal(vo.numpy(), var) and float(no[0]) == float(nll[0])
