@@ -682,8 +682,9 @@ pssgp_status wide_shard_reduce(pssgp_model* m, int64_t k0, int64_t n, int64_t Ng
     if ((st = wide_fold<D>(m, p, pl.nb, s))) return st;
     double* inc = wide_scan_f<D>(m, p, s, st);
     if (st) return st;
-    cudaMemcpyAsync(out, inc + static_cast<int64_t>(pl.nch - 1) * pssgp::wide::FNW(D),
-                    pssgp::wide::FNW(D) * sizeof(double), cudaMemcpyDeviceToDevice, s);
+    const cudaError_t e = cudaMemcpyAsync(out, inc + static_cast<int64_t>(pl.nch - 1) * pssgp::wide::FNW(D),
+                                          pssgp::wide::FNW(D) * sizeof(double), cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(m, e, "cudaMemcpyAsync(chunk aggregate)");
     return PSSGP_OK;
 }
 
@@ -710,7 +711,8 @@ pssgp_status wide_shard_fapply(pssgp_model* m, int64_t k0, int64_t n, int64_t Ng
     if (nllp && (st = nll_sum(m, p.nll_chain, p.nch, nllp, s))) return st;
     double* inc = wide_scan_s<D>(m, p, s, st);
     if (st) return st;
-    cudaMemcpyAsync(sout, inc, pssgp::wide::SNW(D) * sizeof(double), cudaMemcpyDeviceToDevice, s);
+    const cudaError_t e = cudaMemcpyAsync(sout, inc, pssgp::wide::SNW(D) * sizeof(double), cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(m, e, "cudaMemcpyAsync(chunk smoother aggregate)");
     return PSSGP_OK;
 }
 
@@ -1149,8 +1151,9 @@ pssgp_status pssgp_nll_grad_batched(pssgp_model* m, int nseg, const int64_t* off
     pssgp::batch::k_batch_check_offsets<<<(nseg + 256) / 256, 256, 0, s>>>(offsets, nseg, N, m->d_err);
     LAUNCH_CHECK(m, "k_batch_check_offsets");
     if (N == 0) {
-        cudaMemsetAsync(nll, 0, nseg * sizeof(double), s);
-        cudaMemsetAsync(grad, 0, 3 * nseg * sizeof(double), s);
+        cudaError_t e = cudaMemsetAsync(nll, 0, nseg * sizeof(double), s);
+        if (e == cudaSuccess) e = cudaMemsetAsync(grad, 0, 3 * nseg * sizeof(double), s);
+        if (e != cudaSuccess) return cuda_fail(m, e, "cudaMemsetAsync");
         return PSSGP_OK;
     }
     switch (m->d) {
