@@ -239,6 +239,7 @@ pssgp_status setup(pssgp_model* m, const Plan& pl, KParams<D>& p) {
     p.chain_f = w; w += nchp * FN(D);
     p.block_f = w; w += static_cast<size_t>(pl.nb) * FN(D);
     p.fcarry = w; w += static_cast<size_t>(pl.nb) * CN(D);
+    w += (reinterpret_cast<uintptr_t>(w) >> 3) & 1;   // 16-byte aligned records (paired state loads)
     p.xp = w; w += static_cast<size_t>(pl.nb) * kWarps * pl.K * CN(D) * 32;
     p.chain_s = w; w += nchp * SN(D);
     p.block_s = w; w += static_cast<size_t>(pl.nb) * SN(D);

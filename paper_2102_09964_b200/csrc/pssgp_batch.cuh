@@ -272,10 +272,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_filter_apply(con
                 sag_done = true;
             }
             double* o = p.xp + ((wg * p.K + (k - kb)) * CN(D)) * 32 + lane;
-#pragma unroll
-            for (int i = 0; i < D; ++i) o[i * 32] = x[i];
-#pragma unroll
-            for (int i = 0; i < ns(D); ++i) o[(D + i) * 32] = P[i];
+            st_xP<D>(o, lane, x, P);
         }
         __syncwarp();
     }
@@ -354,8 +351,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_smoother_apply(c
     double nx[CN(D)];
     if (kb < ke) {
         const double* s1 = xpw + ((ke - 1 - kb) * CN(D)) * 32;
-#pragma unroll
-        for (int i = 0; i < CN(D); ++i) nx[i] = s1[i * 32];
+        ld_state<D>(s1, lane, nx);
     }
     int ferr = -1;
     const int64_t nwin = (p.K + kWinA - 1) / kWinA;
@@ -382,8 +378,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_smoother_apply(c
             for (int i = 0; i < ns(D); ++i) P[i] = nx[D + i];
             if (k > kb) {
                 const double* src = xpw + ((k - 1 - kb) * CN(D)) * 32;
-#pragma unroll
-                for (int i = 0; i < CN(D); ++i) nx[i] = src[i * 32];
+                ld_state<D>(src, lane, nx);
             }
             if (PSSGP_K5_PF > 0 && k - PSSGP_K5_PF >= kb) prefetch_state_l2<D>(xpw, lane, k - PSSGP_K5_PF - kb);
             if (k == s.end - 1) {   // series end: terminal element

@@ -51,6 +51,7 @@ cudaError_t launch_d(const Run& r, int phase) {
     p.chain_f = w; w += nchp * FN(D);
     p.block_f = w; w += static_cast<size_t>(r.nb) * FN(D);
     p.fcarry = w; w += static_cast<size_t>(r.nb) * CN(D);
+    w += (reinterpret_cast<uintptr_t>(w) >> 2) & 1;   // 8-byte aligned records (paired state loads)
     p.xp = w; w += static_cast<size_t>(r.nb) * kWarps * r.K * CN(D) * 32;
     p.chain_s = w; w += nchp * SN(D);
     p.block_s = w; w += static_cast<size_t>(r.nb) * SN(D);

@@ -367,10 +367,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_grad_fold(const KParams<D> p, d
         // primal entering the chain = filtered moments of step kb-1 (last step of chain c-1)
         const int64_t cp = c - 1;
         const double* src = p.xp + (((cp / 32) * p.K + (p.K - 1)) * CN(D)) * 32 + (cp % 32);
-#pragma unroll
-        for (int i = 0; i < D; ++i) x[i] = src[i * 32];
-#pragma unroll
-        for (int i = 0; i < ns(D); ++i) P[i] = src[(D + i) * 32];
+        ld_xP<D>(src, static_cast<int>(cp % 32), x, P);
         tprev = __ldg(p.t + kb - 1);
     }
     const double* xpw = p.xp + (wg * p.K * CN(D)) * 32 + lane;
@@ -395,10 +392,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_grad_fold(const KParams<D> p, d
         tprev = tk;
         if (PSSGP_GRAD_PF > 0 && k + PSSGP_GRAD_PF < ke) prefetch_state_l2<D>(xpw, lane, k + PSSGP_GRAD_PF - kb);
         const double* src = xpw + ((k - kb) * CN(D)) * 32;
-#pragma unroll
-        for (int i = 0; i < D; ++i) x[i] = src[i * 32];
-#pragma unroll
-        for (int i = 0; i < ns(D); ++i) P[i] = src[(D + i) * 32];
+        ld_xP<D>(src, lane, x, P);
     }
     // ordered CTA reduction
 #pragma unroll
@@ -455,10 +449,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_batch_grad_fold(const KParams<D
     if (kb > 0) {
         const int64_t cp = c - 1;
         const double* src = p.xp + (((cp / 32) * p.K + (p.K - 1)) * CN(D)) * 32 + (cp % 32);
-#pragma unroll
-        for (int i = 0; i < D; ++i) x[i] = src[i * 32];
-#pragma unroll
-        for (int i = 0; i < ns(D); ++i) P[i] = src[(D + i) * 32];
+        ld_xP<D>(src, static_cast<int>(cp % 32), x, P);
         tprev = __ldg(p.t + kb - 1);
     }
     bool head_done = false;
@@ -488,10 +479,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_batch_grad_fold(const KParams<D
         tprev = tk;
         if (PSSGP_GRAD_PF > 0 && k + PSSGP_GRAD_PF < ke) prefetch_state_l2<D>(xpw, lane, k + PSSGP_GRAD_PF - kb);
         const double* src = xpw + ((k - kb) * CN(D)) * 32;
-#pragma unroll
-        for (int i = 0; i < D; ++i) x[i] = src[i * 32];
-#pragma unroll
-        for (int i = 0; i < ns(D); ++i) P[i] = src[(D + i) * 32];
+        ld_xP<D>(src, lane, x, P);
         if (k == s.end - 1) {                     // series end inside this chain
             if (s.start >= kb) {                  // the whole series is in this chain
 #pragma unroll

@@ -143,6 +143,68 @@ __device__ __forceinline__ void store_aos(const T& a, real* base) {
     for (int i = 0; i < n; ++i) base[i] = s[i];
 }
 
+// ------------------------------------------------------------------ filtered-state record layout
+// xp holds, per (warp, step), one block of CN * 32 reals (the warp's 32 chains).  PSSGP_VEC_STATE = 1:
+// component pairs (2c, 2c+1) of lane l at block + 64 c + 2 l (one 16-byte access per lane for fp64),
+// an odd last component at block + 64 (CN / 2) + l; 0: component i of lane l at block + 32 i + l.
+// Every site passes `at` = block + lane (the lane's component-0 position of the plain layout).
+#ifndef PSSGP_VEC_STATE
+#define PSSGP_VEC_STATE 0
+#endif
+template <typename T> struct Vec2;
+template <> struct Vec2<double> { using type = double2; };
+template <> struct Vec2<float> { using type = float2; };
+
+template <int D>
+__device__ __forceinline__ void ld_state(const real* at, int lane, real (&v)[CN(D)]) {
+    if (PSSGP_VEC_STATE) {
+        using V = typename Vec2<real>::type;
+        const real* blk = at - lane;
+#pragma unroll
+        for (int c = 0; c < CN(D) / 2; ++c) {
+            const V q = *reinterpret_cast<const V*>(blk + 64 * c + 2 * lane);
+            v[2 * c] = q.x;
+            v[2 * c + 1] = q.y;
+        }
+        if (CN(D) & 1) v[CN(D) - 1] = blk[64 * (CN(D) / 2) + lane];
+    } else {
+#pragma unroll
+        for (int i = 0; i < CN(D); ++i) v[i] = at[i * 32];
+    }
+}
+template <int D>
+__device__ __forceinline__ void ld_xP(const real* at, int lane, real (&x)[D], real (&P)[ns(D)]) {
+    real v[CN(D)];
+    ld_state<D>(at, lane, v);
+#pragma unroll
+    for (int i = 0; i < D; ++i) x[i] = v[i];
+#pragma unroll
+    for (int i = 0; i < ns(D); ++i) P[i] = v[D + i];
+}
+template <int D>
+__device__ __forceinline__ void st_xP(real* at, int lane, const real (&x)[D], const real (&P)[ns(D)]) {
+    real v[CN(D)];
+#pragma unroll
+    for (int i = 0; i < D; ++i) v[i] = x[i];
+#pragma unroll
+    for (int i = 0; i < ns(D); ++i) v[D + i] = P[i];
+    if (PSSGP_VEC_STATE) {
+        using V = typename Vec2<real>::type;
+        real* blk = at - lane;
+#pragma unroll
+        for (int c = 0; c < CN(D) / 2; ++c) {
+            V q;
+            q.x = v[2 * c];
+            q.y = v[2 * c + 1];
+            *reinterpret_cast<V*>(blk + 64 * c + 2 * lane) = q;
+        }
+        if (CN(D) & 1) blk[64 * (CN(D) / 2) + lane] = v[CN(D) - 1];
+    } else {
+#pragma unroll
+        for (int i = 0; i < CN(D); ++i) at[i * 32] = v[i];
+    }
+}
+
 // ------------------------------------------------------------------ asynchronous staging
 // A warp's 32 chains are 32 contiguous segments of K steps.  Windows of kWinA
 // steps of t and y for all 32 chains are copied global -> shared with cp.async
@@ -626,10 +688,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
         nll_accumulate(obs, v, vs, S, quad, prodm, prode, nobs);
         if (STORE) {
             real* o = p.xp + (wg * p.K * CN(D)) * 32 + lane;
-#pragma unroll
-            for (int i = 0; i < D; ++i) o[i * 32] = x[i];
-#pragma unroll
-            for (int i = 0; i < ns(D); ++i) o[(D + i) * 32] = P[i];
+            st_xP<D>(o, lane, x, P);
         }
     }
 
@@ -701,10 +760,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
                 nll_accumulate(obs, v, vs, S, quad, prodm, prode, nobs);
                 if (STORE) {
                     real* o = p.xp + ((wg * p.K + (k - kb)) * CN(D)) * 32 + lane;
-#pragma unroll
-                    for (int i = 0; i < D; ++i) o[i * 32] = x[i];
-#pragma unroll
-                    for (int i = 0; i < ns(D); ++i) o[(D + i) * 32] = P[i];
+                    st_xP<D>(o, lane, x, P);
                 }
             }
         }
@@ -922,14 +978,10 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_smoother_apply(const K
         const int64_t k = ke - 1;
         const real* src = xpw + ((k - kb) * CN(D)) * 32;
         real x[D], P[ns(D)];
-#pragma unroll
-        for (int i = 0; i < D; ++i) x[i] = src[i * 32];
-#pragma unroll
-        for (int i = 0; i < ns(D); ++i) P[i] = src[(D + i) * 32];
+        ld_xP<D>(src, lane, x, P);
         if (k > kb) {
             const real* s1 = xpw + ((k - 1 - kb) * CN(D)) * 32;
-#pragma unroll
-            for (int i = 0; i < CN(D); ++i) nx[i] = s1[i * 32];
+            ld_state<D>(s1, lane, nx);
         }
         const double tk = __ldg(p.t + k);
         if (p.k0 + k == p.nglob - 1) {
@@ -976,8 +1028,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_smoother_apply(const K
                 for (int i = 0; i < ns(D); ++i) P[i] = nx[D + i];
                 if (k > kb) {
                     const real* src = xpw + ((k - 1 - kb) * CN(D)) * 32;
-#pragma unroll
-                    for (int i = 0; i < CN(D); ++i) nx[i] = src[i * 32];
+                    ld_state<D>(src, lane, nx);
                 }
                 if (PSSGP_K5_PF > 0 && k - PSSGP_K5_PF >= kb) prefetch_state_l2<D>(xpw, lane, k - PSSGP_K5_PF - kb);
                 FT_t<D, MODE> F;
