@@ -61,6 +61,7 @@ PS_CX int CN(int D) { return D + ns(D); }                  // (mean, cov) pair r
 struct MathConsts {
     real expc[28];   // 1/k!, k = 0..27 (Taylor of e^r on |r| <= ln2/2 uses k <= 13; R_m series)
     real inv[32];    // 1/n, n = 0..31 (inv[0] unused)
+    real qw[4];      // Jordan-basis Q weights 2/3, 4/3, 8/3, 2 (constant-bank operands, not immediates)
 };
 #define PS_MATH_CONSTS                                                                         \
     {{1.0, 1.0, 0.5, 0.16666666666666666, 0.041666666666666664,  \
@@ -72,7 +73,8 @@ struct MathConsts {
      {0.0, 1.0, 1.0 / 2, 1.0 / 3, 1.0 / 4, 1.0 / 5, 1.0 / 6, 1.0 / 7, 1.0 / 8, 1.0 / 9, 1.0 / 10, \
       1.0 / 11, 1.0 / 12, 1.0 / 13, 1.0 / 14, 1.0 / 15, 1.0 / 16, 1.0 / 17, 1.0 / 18, 1.0 / 19,   \
       1.0 / 20, 1.0 / 21, 1.0 / 22, 1.0 / 23, 1.0 / 24, 1.0 / 25, 1.0 / 26, 1.0 / 27, 1.0 / 28,   \
-      1.0 / 29, 1.0 / 30, 1.0 / 31}}
+      1.0 / 29, 1.0 / 30, 1.0 / 31},                                                              \
+     {2.0 / 3.0, 4.0 / 3.0, 8.0 / 3.0, 2.0}}
 #if defined(__CUDACC__)
 static __constant__ MathConsts d_mc = PS_MATH_CONSTS;
 #endif
@@ -585,17 +587,18 @@ PS_HD void matern_closed(real lam, real s2, double dt, FJor<D>& F, real (&Q)[ns(
         inc_gamma_tails<3, FAST>(x, ex, R);
         Q[si(2, 0, 0)] = s2 * R[3];
         Q[si(2, 0, 1)] = s2 * R[2];
-        Q[si(2, 1, 1)] = (real(2.0) * s2) * R[1];
+        Q[si(2, 1, 1)] = (mc().qw[3] * s2) * R[1];
     } else if constexpr (D == 3) {
         real R[6];
         inc_gamma_tails<5, FAST>(x, ex, R);
-        const real s43 = s2 * real(4.0 / 3.0);
+        const MathConsts& C = mc();
+        const real s43 = s2 * C.qw[1];
         Q[si(3, 0, 0)] = s2 * R[5];
         Q[si(3, 0, 1)] = s2 * R[4];
-        Q[si(3, 0, 2)] = (s2 * real(2.0 / 3.0)) * R[3];
+        Q[si(3, 0, 2)] = (s2 * C.qw[0]) * R[3];
         Q[si(3, 1, 1)] = s43 * R[3];
         Q[si(3, 1, 2)] = s43 * R[2];
-        Q[si(3, 2, 2)] = (s2 * real(8.0 / 3.0)) * R[1];
+        Q[si(3, 2, 2)] = (s2 * C.qw[2]) * R[1];
     }
 }
 
