@@ -408,8 +408,13 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_smoother_apply(c
                 const int64_t idx = wbase + r * p.K + j;
                 const int64_t rend = min(wbase + (r + 1) * p.K, p.n);
                 if (j < p.K && idx < rend) {
-                    if (p.mean) p.mean[idx] = so[wid].m[col][r];
-                    if (p.var) p.var[idx] = so[wid].v[col][r];
+                    if (PSSGP_CS_HINTS & 4) {   // streaming stores of the outputs
+                        if (p.mean) __stcs(p.mean + idx, so[wid].m[col][r]);
+                        if (p.var) __stcs(p.var + idx, so[wid].v[col][r]);
+                    } else {
+                        if (p.mean) p.mean[idx] = so[wid].m[col][r];
+                        if (p.var) p.var[idx] = so[wid].v[col][r];
+                    }
                 }
             }
         }

@@ -151,6 +151,9 @@ __device__ __forceinline__ void store_aos(const T& a, real* base) {
 #ifndef PSSGP_VEC_STATE
 #define PSSGP_VEC_STATE 0
 #endif
+#ifndef PSSGP_CS_HINTS
+#define PSSGP_CS_HINTS 1                // bit 0: streaming (evict-first) record stores; bit 1: streaming record loads; bit 2: output stores
+#endif
 template <typename T> struct Vec2;
 template <> struct Vec2<double> { using type = double2; };
 template <> struct Vec2<float> { using type = float2; };
@@ -167,6 +170,9 @@ __device__ __forceinline__ void ld_state(const real* at, int lane, real (&v)[CN(
             v[2 * c + 1] = q.y;
         }
         if (CN(D) & 1) v[CN(D) - 1] = blk[64 * (CN(D) / 2) + lane];
+    } else if (PSSGP_CS_HINTS & 2) {
+#pragma unroll
+        for (int i = 0; i < CN(D); ++i) v[i] = __ldcs(at + i * 32);
     } else {
 #pragma unroll
         for (int i = 0; i < CN(D); ++i) v[i] = at[i * 32];
@@ -199,6 +205,9 @@ __device__ __forceinline__ void st_xP(real* at, int lane, const real (&x)[D], co
             *reinterpret_cast<V*>(blk + 64 * c + 2 * lane) = q;
         }
         if (CN(D) & 1) blk[64 * (CN(D) / 2) + lane] = v[CN(D) - 1];
+    } else if (PSSGP_CS_HINTS & 1) {
+#pragma unroll
+        for (int i = 0; i < CN(D); ++i) __stcs(at + i * 32, v[i]);
     } else {
 #pragma unroll
         for (int i = 0; i < CN(D); ++i) at[i * 32] = v[i];
@@ -1054,8 +1063,13 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_smoother_apply(const K
                 const int64_t idx = wbase + r * p.K + j;
                 const int64_t last = min(wbase + (r + 1) * p.K, p.n) - 1;   // row r's peeled step
                 if ((j < p.K) && (idx < last)) {
-                    if (p.mean) p.mean[idx] = so[wid].m[col][r];
-                    if (p.var) p.var[idx] = so[wid].v[col][r];
+                    if (PSSGP_CS_HINTS & 4) {   // streaming stores of the outputs
+                        if (p.mean) __stcs(p.mean + idx, so[wid].m[col][r]);
+                        if (p.var) __stcs(p.var + idx, so[wid].v[col][r]);
+                    } else {
+                        if (p.mean) p.mean[idx] = so[wid].m[col][r];
+                        if (p.var) p.var[idx] = so[wid].v[col][r];
+                    }
                 }
             }
         }
