@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstddef>
 #include <cstring>
 #include <new>
@@ -426,6 +427,10 @@ void wide_set_smem_attrs() {
     static bool done = false;
     if (done) return;
     cudaFuncSetAttribute(kw_filter_fold<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K1Smem<D>));
+    if constexpr (D <= kGL) {
+        cudaFuncSetAttribute(kw_filter_fold_lpr<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K1LSmem<D>));
+        cudaFuncSetAttribute(kw_filter_fold_lpr<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K1LSmem<D>));
+    }
     cudaFuncSetAttribute(kw_filter_apply<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K3Smem<D>));
     cudaFuncSetAttribute(kw_smoother_apply<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K5Smem<D>));
     cudaFuncSetAttribute(kw_scan_filter<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(ScanSmemF<D>));
@@ -445,6 +450,8 @@ WPlan make_wplan(pssgp_model* m, int64_t n) {
     wide_set_smem_attrs<D>();
     if (m->wocc == 0) {
         int a = 0, b = 0, c = 0;
+        // (the lane-per-row fold of D <= 8 is not part of the plan's occupancy: it is register-
+        // capped at PSSGP_WLPR_MINB CTAs/SM and simply runs the same grid)
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, kw_filter_fold<D>, 32 * kWWarps, sizeof(K1Smem<D>));
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kw_filter_apply<D>, 32 * kWWarps, sizeof(K3Smem<D>));
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, kw_smoother_apply<D>, 32 * kWWarps, sizeof(K5Smem<D>));
@@ -606,6 +613,16 @@ template <int D>
 pssgp_status wide_fold(pssgp_model* m, pssgp::wide::WParams& p, int nb, cudaStream_t s) {
     using namespace pssgp::wide;
     ProfScope ps(m, S_K1, s);
+    if constexpr (D <= kGL) {
+        // lane-per-row fold (D <= 8); PSSGP_WIDE_LPR=0 selects the shared-memory fold (A/B runs)
+        static const bool lpr = [] { const char* e = getenv("PSSGP_WIDE_LPR"); return !(e && e[0] == '0'); }();
+        if (lpr) {
+            if (p.fq) kw_filter_fold_lpr<D, true><<<nb, 32 * kWWarps, sizeof(K1LSmem<D>), s>>>(p);
+            else kw_filter_fold_lpr<D, false><<<nb, 32 * kWWarps, sizeof(K1LSmem<D>), s>>>(p);
+            LAUNCH_CHECK(m, "kw_filter_fold_lpr");
+            return PSSGP_OK;
+        }
+    }
     kw_filter_fold<D><<<nb, 32 * kWWarps, sizeof(K1Smem<D>), s>>>(p);
     LAUNCH_CHECK(m, "kw_filter_fold");
     return PSSGP_OK;

@@ -865,6 +865,175 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WMINB) kw_filter_fold(cons
     gstore<D>(W.a, p.fagg + static_cast<int64_t>(c) * FNW(D), lane);
 }
 
+// ------------------------------------------------------------------ K1w for D <= 8: lane-per-row fold
+// Same grid and output as kw_filter_fold (one warp per chain, fagg[c]), but the chain is split
+// into kQ = 4 consecutive quarters, each folded IN REGISTERS by one 8-lane group: lane r of a
+// group holds column r of A, rows r of C and J (symmetric) and b_r, eta_r.  F and Q are read
+// from shared memory (one address per group: broadcast); the full vectors a step needs (b, HC,
+// w) are gathered by shuffles and F C is transposed through a per-group shared buffer.  The
+// four quarter aggregates are then combined in order with the warp operator (
+// any grouping).  Steps past a quarter's end are identity steps (F = I, Q = 0, y
+// missing), which leave the aggregate unchanged exactly, so all lanes run the same trip count
+// (full-warp shuffles).  Replaces one warp-cooperative shared-memory step per chain (36-64
+// outputs over 32 lanes, ~4,400 cycles at d = 6) by four register steps in parallel.
+constexpr int kQ = 4, kGL = 8;
+template <int D>
+struct K1LSmem {
+    SModel<D> m;
+    double I[D][LD(D)], Z[D][LD(D)];
+    struct PerWarp {
+        SF<D> q[kQ];
+        SCombF<D> s;
+        double U[kQ][D][LD(D)];
+    } w[kWWarps];
+};
+
+#ifndef PSSGP_WLPR_MINB
+#define PSSGP_WLPR_MINB 3                        // resident CTAs/SM the lane-per-row fold is register-capped for
+#endif
+template <int D, bool STREAM>
+__global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_filter_fold_lpr(const WParams p) {
+    static_assert(D <= kGL, "lane-per-row fold holds one row per lane of an 8-lane group");
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    K1LSmem<D>& sh = *reinterpret_cast<K1LSmem<D>*>(smem_raw);
+    load_model<D>(sh.m, p.model);
+    for (int e = threadIdx.x; e < D * D; e += blockDim.x) {
+        const int i = e / D, j = e - (e / D) * D;
+        sh.I[i][j] = (i == j) ? 1.0 : 0.0;
+        sh.Z[i][j] = 0.0;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int c = blockIdx.x * kWWarps + wid;
+    if (c >= p.nch) return;                                     // warp-uniform
+    const int q = lane / kGL, r = lane % kGL, gb = q * kGL;
+    const bool act = r < D;
+    const int rr = act ? r : 0;                                 // row addressed by idle lanes
+    auto& W = sh.w[wid];
+    const SModel<D>& M = sh.m;
+    const int64_t kb = static_cast<int64_t>(c) * p.K;
+    const int64_t ke = min(kb + p.K, p.n);
+    const int64_t Kq = (p.K + kQ - 1) / kQ;
+    const int64_t qb = min(kb + q * Kq, ke), qe = min(qb + Kq, ke);
+
+    double Ac[D], Cr[D], Jr[D], b = 0.0, eta = 0.0;
+#pragma unroll
+    for (int i = 0; i < D; ++i) { Ac[i] = (i == r) ? 1.0 : 0.0; Cr[i] = 0.0; Jr[i] = 0.0; }
+    double tprev = (qb < qe && (qb > 0 || p.k0 > 0)) ? __ldg(p.t + qb - 1) : 0.0;
+    double tn_ = 0.0, yn_ = 0.0;
+    unsigned char mn_ = 0;
+    if (qb < qe) { tn_ = __ldg(p.t + qb); mn_ = __ldg(p.mask + qb); yn_ = __ldg(p.y + qb); }
+    const double hr = act ? M.H[r] : 0.0;
+    for (int64_t j = 0; j < Kq; ++j) {
+        const int64_t k = qb + j;
+        const bool valid = k < qe;
+        const double tk = tn_;
+        const bool obs = valid && mn_ != 0;
+        const double yk = obs ? yn_ : 0.0;
+        if (k + 1 < qe) { tn_ = __ldg(p.t + k + 1); mn_ = __ldg(p.mask + k + 1); yn_ = __ldg(p.y + k + 1); }
+        const int64_t g = p.k0 + k;
+        int kind = 1;                                            // identity step past the quarter's end
+        if (valid) kind = (g == 0) ? 3 : wdisc_kind(tk - tprev, M.udt, STREAM);
+        if (valid && r == 0) {
+            if (g > 0 && !(tk - tprev >= 0.0)) raise_error(p.err, g, kErrInput);
+            if (!isfinite(tk) || (obs && !isfinite(yk))) raise_error(p.err, g, kErrInput);
+            if (kind == 2) raise_error(p.err, g, kErrUnsupported);
+        }
+        if (valid) tprev = tk;
+        const double* Fp;
+        const double* Qp;
+        if (kind == 0) {
+            if (STREAM) { Fp = p.fq + k * FQW(D); Qp = Fp + D * LD(D); }
+            else { Fp = &M.F[0][0]; Qp = &M.Q[0][0]; }
+        } else if (kind == 1) {
+            Fp = &sh.I[0][0]; Qp = &sh.Z[0][0];
+        } else {                                                 // 3 (and 2, reported): F = 0, Q = P_inf
+            Fp = &sh.Z[0][0]; Qp = &M.Pinf[0][0];
+        }
+        // FA column r and U = F C column r (column r of C = row r)
+        double FAc[D], Uc[D];
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            double sa = 0.0, su = 0.0;
+#pragma unroll
+            for (int kk = 0; kk < D; ++kk) {
+                const double f = Fp[i * LD(D) + kk];
+                sa = fma(f, Ac[kk], sa);
+                su = fma(f, Cr[kk], su);
+            }
+            FAc[i] = sa;
+            Uc[i] = su;
+        }
+        // Fb_r = F[r,:] b
+        double Fb = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < D; ++kk) Fb = fma(Fp[rr * LD(D) + kk], __shfl_sync(0xffffffffu, b, gb + kk), Fb);
+        // row r of U through shared; Cm row r = U[r,:] F^T + Q[r,:]
+        if (act) {
+#pragma unroll
+            for (int i = 0; i < D; ++i) W.U[q][i][r] = Uc[i];
+        }
+        __syncwarp();
+        double Ur[D];
+#pragma unroll
+        for (int kk = 0; kk < D; ++kk) Ur[kk] = W.U[q][rr][kk];
+        __syncwarp();
+        double Cm[D];
+        double HC = 0.0, w = 0.0;
+#pragma unroll
+        for (int jj = 0; jj < D; ++jj) {
+            double s = Qp[rr * LD(D) + jj];
+#pragma unroll
+            for (int kk = 0; kk < D; ++kk) s = fma(Ur[kk], Fp[jj * LD(D) + kk], s);
+            Cm[jj] = s;
+            HC = fma(s, M.H[jj], HC);
+            w = fma(M.H[jj], FAc[jj], w);
+        }
+        if (!act) { HC = 0.0; w = 0.0; Fb = 0.0; }
+        double S = hr * HC, hb = hr * Fb;
+#pragma unroll
+        for (int off = kGL / 2; off > 0; off >>= 1) {
+            S += __shfl_xor_sync(0xffffffffu, S, off);
+            hb += __shfl_xor_sync(0xffffffffu, hb, off);
+        }
+        S += M.r;
+        const double iS = obs ? 1.0 / S : 0.0;
+        const double vs = obs ? (yk - hb) * iS : 0.0;
+        const double HCs = HC * iS, ws = w * iS;
+#pragma unroll
+        for (int jj = 0; jj < D; ++jj) {
+            const double HCj = __shfl_sync(0xffffffffu, HC, gb + jj);
+            const double wj = __shfl_sync(0xffffffffu, w, gb + jj);
+            Ac[jj] = fma(-HCj * iS, w, FAc[jj]);
+            Cr[jj] = fma(-HCs, HCj, Cm[jj]);
+            Jr[jj] = fma(ws, wj, Jr[jj]);
+        }
+        b = fma(HC, vs, Fb);
+        eta = fma(w, vs, eta);
+    }
+    // quarter aggregates -> shared, ordered combination, store
+    if (act) {
+        SF<D>& o = W.q[q];
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            o.A[i][r] = Ac[i];
+            o.C[r][i] = Cr[i];
+            o.J[r][i] = Jr[i];
+        }
+        o.b[r] = b;
+        o.eta[r] = eta;
+    }
+    __syncwarp();
+    bool ok = true;
+#pragma unroll 1
+    for (int i = 1; i < kQ; ++i) {
+        ok = wcombine<D>(W.q[i - 1], W.q[i], W.q[i], W.s, lane) && ok;
+        __syncwarp();
+    }
+    if (!ok && lane == 0) raise_error(p.err, p.k0 + kb, kErrNumeric);
+    gstore<D>(W.q[kQ - 1], p.fagg + static_cast<int64_t>(c) * FNW(D), lane);
+}
+
 // ------------------------------------------------------------------ Kogge-Stone scan levels (1 warp per element)
 template <int D>
 struct ScanSmemF {
