@@ -430,6 +430,8 @@ void wide_set_smem_attrs() {
     if constexpr (D <= kGL) {
         cudaFuncSetAttribute(kw_filter_fold_lpr<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K1LSmem<D>));
         cudaFuncSetAttribute(kw_filter_fold_lpr<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K1LSmem<D>));
+        cudaFuncSetAttribute(kw_smoother_apply_lpr<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K5LSmem<D>));
+        cudaFuncSetAttribute(kw_smoother_apply_lpr<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K5LSmem<D>));
     }
     cudaFuncSetAttribute(kw_filter_apply<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K3Smem<D>));
     cudaFuncSetAttribute(kw_smoother_apply<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K5Smem<D>));
@@ -437,6 +439,14 @@ void wide_set_smem_attrs() {
     cudaFuncSetAttribute(kw_scan_smoother<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(ScanSmemS<D>));
     cudaFuncSetAttribute(kw_discretize<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(KDSmem<D>));
     done = true;
+}
+
+// lane-per-row kernels of the wide path for D <= 8 (bit 0: fold, bit 1: RTS rescan, bit 2: RTS
+// rescan also with per-step (F, Q), bit 3: one-wave plan for them on the table path); env
+// PSSGP_WIDE_LPR overrides the default 11 for A/B runs (0 = the shared-memory kernels)
+int wide_lpr_mask() {
+    static const int v = [] { const char* e = getenv("PSSGP_WIDE_LPR"); return e && *e ? atoi(e) : 11; }();
+    return v;
 }
 
 struct WPlan {
@@ -456,6 +466,18 @@ WPlan make_wplan(pssgp_model* m, int64_t n) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kw_filter_apply<D>, 32 * kWWarps, sizeof(K3Smem<D>));
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, kw_smoother_apply<D>, 32 * kWWarps, sizeof(K5Smem<D>));
         m->wocc = std::max(1, std::min(a, std::min(b, c)));
+        if constexpr (D <= kGL) {
+            int l1 = 0, l5 = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l1, kw_filter_fold_lpr<D, false>, 32 * kWWarps, sizeof(K1LSmem<D>));
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l5, kw_smoother_apply_lpr<D, false>, 32 * kWWarps, sizeof(K5LSmem<D>));
+            if (getenv("PSSGP_WIDE_DEBUG"))
+                fprintf(stderr, "wide plan D=%d occupancy: fold %d, apply %d, smoother %d, lpr fold %d, lpr smoother %d\n",
+                        D, a, b, c, l1, l5);
+            // bit 3: on the table (uniform-dt) path, where both lane-per-row kernels run, size the
+            // plan so they run in one wave (C3: 13.8 -> 11.7 ms; on the per-step (F, Q) path the
+            // fewer, longer chains slow the shared-memory rescans: 26.2 -> 28.3 ms, so not there)
+            if ((wide_lpr_mask() & 8) && m->mode != kPade) m->wocc = std::max(1, std::min(m->wocc, std::min(l1, l5)));
+        }
     }
     const int64_t target = static_cast<int64_t>(m->sm_count) * m->wocc * kWWarps;
     WPlan pl;
@@ -615,8 +637,7 @@ pssgp_status wide_fold(pssgp_model* m, pssgp::wide::WParams& p, int nb, cudaStre
     ProfScope ps(m, S_K1, s);
     if constexpr (D <= kGL) {
         // lane-per-row fold (D <= 8); PSSGP_WIDE_LPR=0 selects the shared-memory fold (A/B runs)
-        static const bool lpr = [] { const char* e = getenv("PSSGP_WIDE_LPR"); return !(e && e[0] == '0'); }();
-        if (lpr) {
+        if (wide_lpr_mask() & 1) {
             if (p.fq) kw_filter_fold_lpr<D, true><<<nb, 32 * kWWarps, sizeof(K1LSmem<D>), s>>>(p);
             else kw_filter_fold_lpr<D, false><<<nb, 32 * kWWarps, sizeof(K1LSmem<D>), s>>>(p);
             LAUNCH_CHECK(m, "kw_filter_fold_lpr");
@@ -641,6 +662,16 @@ template <int D>
 pssgp_status wide_sapply(pssgp_model* m, pssgp::wide::WParams& p, int nb, cudaStream_t s) {
     using namespace pssgp::wide;
     ProfScope ps(m, S_K5, s);
+    if constexpr (D <= kGL) {
+        // uniform dt only by default: with per-step (F, Q) read from global memory it measured
+        // slower than the shared-memory kernel (C3 irregular K5w 8.4 -> 11.3 ms); bit 2 forces it
+        if ((wide_lpr_mask() & 2) && (!p.fq || (wide_lpr_mask() & 4))) {
+            if (p.fq) kw_smoother_apply_lpr<D, true><<<nb, 32 * kWWarps, sizeof(K5LSmem<D>), s>>>(p);
+            else kw_smoother_apply_lpr<D, false><<<nb, 32 * kWWarps, sizeof(K5LSmem<D>), s>>>(p);
+            LAUNCH_CHECK(m, "kw_smoother_apply_lpr");
+            return PSSGP_OK;
+        }
+    }
     kw_smoother_apply<D><<<nb, 32 * kWWarps, sizeof(K5Smem<D>), s>>>(p);
     LAUNCH_CHECK(m, "kw_smoother_apply");
     return PSSGP_OK;

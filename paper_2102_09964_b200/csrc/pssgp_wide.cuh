@@ -1463,5 +1463,235 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WMINB) kw_smoother_apply(c
     }
 }
 
+
+// ------------------------------------------------------------------ K5w for D <= 8: lane-per-row RTS
+// Same grid, carries and outputs as kw_smoother_apply; the per-step RTS recursion (PAPER.md:
+// 422-430 / Prop. 2 order) runs in registers with lane r (< D) owning row r of P, P^s
+// and column r of F P and X = P^-_{k+1}^-1 F P (so the gain is X^T).  Matrices a lane needs in
+// full (P^-, P^s, X) go through per-warp shared buffers; every lane factors P^- (Cholesky,
+// upper triangle as the symmetric source of truth) in registers and solves for its own column.
+template <int D>
+struct K5LSmem {
+    K5Smem<D> b;
+    double I[D][LD(D)], Z[D][LD(D)];
+    struct G {
+        double U[D][LD(D)], Pm[D][LD(D)], Ps[D][LD(D)] /* P^s_{k+1} - P^- */, X[D][LD(D)];
+        double dm[D];
+    } g[kWWarps];
+};
+
+template <int D, bool STREAM>
+__global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_smoother_apply_lpr(const WParams p) {
+    static_assert(D <= kGL, "lane-per-row RTS holds one row per lane");
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    K5LSmem<D>& shl = *reinterpret_cast<K5LSmem<D>*>(smem_raw);
+    K5Smem<D>& sh = shl.b;
+    load_model<D>(sh.m, p.model);
+    for (int e = threadIdx.x; e < D * D; e += blockDim.x) {
+        const int i = e / D, j = e - (e / D) * D;
+        shl.I[i][j] = (i == j) ? 1.0 : 0.0;
+        shl.Z[i][j] = 0.0;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int c = blockIdx.x * kWWarps + wid;
+    // NLL: fixed-order sum of the chain partials (CTA 0, warp 0) — as kw_smoother_apply
+    if (blockIdx.x == 0 && wid == 0 && p.nll_out) {
+        double s = 0.0;
+        const int per = (p.nch + 31) / 32;
+        for (int i = 0; i < per; ++i) {
+            const int q = lane * per + i;
+            if (q < p.nch) s += p.nll_chain[q];
+        }
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
+        if (lane == 0) *p.nll_out = s;
+    }
+    if (c >= p.nch) return;
+    auto& W = sh.w[wid];
+    auto& Gs = shl.g[wid];
+    const SModel<D>& M = sh.m;
+    // ---- carry (warp-cooperative, shared layout): collapsed suffix after the chain
+    for (int e = lane; e < D * D; e += 32) W.Ps[e / D][e % D] = 0.0;
+    for (int i = lane; i < D; i += 32) W.ms[i] = 0.0;
+    __syncwarp();
+    for (int g = p.world - 1; g > p.rank && p.in_smooth; --g) {
+        gload<D>(W.u.c.a, p.in_smooth + static_cast<int64_t>(g) * SNW(D), lane);
+        wapply_suffix<D>(W.u.c.a, W.ms, W.Ps, W.u.c.s, lane);
+    }
+    if (c + 1 < p.nch) {
+        gload<D>(W.u.c.a, p.sagg + static_cast<int64_t>(c + 1) * SNW(D), lane);
+        wapply_suffix<D>(W.u.c.a, W.ms, W.Ps, W.u.c.s, lane);
+    }
+    const bool act = lane < D;
+    const int r = act ? lane : 0;
+    double Psr[D], msr = W.ms[r];
+#pragma unroll
+    for (int j = 0; j < D; ++j) Psr[j] = W.Ps[r][j];
+    const double hr = act ? M.H[r] : 0.0;
+    __syncwarp();                                   // W.u (carry scratch) is reused by the staging below
+
+    const int64_t kb = static_cast<int64_t>(c) * p.K;
+    const int64_t ke = min(kb + p.K, p.n);
+    const double* xpc = p.xp + static_cast<int64_t>(c) * p.K * CNW(D);
+    double tnext = (ke > kb && p.k0 + ke < p.nglob) ? __ldg(p.t + ke) : 0.0;
+    double tk_next = 0.0;
+    if (ke > kb) {
+        const double* src = xpc + (ke - 1 - kb) * CNW(D);
+        for (int i = lane; i < CNW(D); i += 32) cp_async8(&W.xst[0][i], src + i, 8);
+        cp_async_commit();
+        tk_next = __ldg(p.t + ke - 1);
+    }
+    int sb = 0;
+    bool bad = false;
+    for (int64_t k = ke - 1; k >= kb; --k) {
+        const double tk = tk_next;
+        const int64_t g = p.k0 + k;
+        cp_async_wait<0>();
+        __syncwarp();
+        if (k > kb) {
+            const double* src = xpc + (k - 1 - kb) * CNW(D);
+            for (int i = lane; i < CNW(D); i += 32) cp_async8(&W.xst[sb ^ 1][i], src + i, 8);
+            cp_async_commit();
+            tk_next = __ldg(p.t + k - 1);
+        }
+        // filtered (xbar_k, row r of P_k) from the staged packed record
+        double xa[D], Pr[D];
+        {
+            const double* src = W.xst[sb];
+#pragma unroll
+            for (int i = 0; i < D; ++i) xa[i] = src[i];
+#pragma unroll
+            for (int j = 0; j < D; ++j) Pr[j] = src[D + si(D, r, j)];
+        }
+        sb ^= 1;
+        if (g == p.nglob - 1) {                     // terminal element: smoothed = filtered
+#pragma unroll
+            for (int j = 0; j < D; ++j) Psr[j] = Pr[j];
+            msr = xa[r];
+        } else {
+            const int kind = wdisc_kind(tnext - tk, M.udt, STREAM);
+            const double* Fp;
+            const double* Qp;
+            if (kind == 0) {
+                if (STREAM) { Fp = p.fq + (k + 1) * FQW(D); Qp = Fp + D * LD(D); }
+                else { Fp = &M.F[0][0]; Qp = &M.Q[0][0]; }
+            } else {                                // dt == 0 (or unsupported, reported by the fold): F = I, Q = 0
+                Fp = &shl.I[0][0]; Qp = &shl.Z[0][0];
+            }
+            // column r of F P (P symmetric: column r = row r); xm_r = F[r,:] xbar
+            double Uc[D], xm = 0.0;
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+                double su = 0.0;
+#pragma unroll
+                for (int q = 0; q < D; ++q) su = fma(Fp[i * LD(D) + q], Pr[q], su);
+                Uc[i] = su;
+            }
+#pragma unroll
+            for (int q = 0; q < D; ++q) xm = fma(Fp[r * LD(D) + q], xa[q], xm);
+            if (act) {
+#pragma unroll
+                for (int i = 0; i < D; ++i) Gs.U[i][r] = Uc[i];
+            }
+            __syncwarp();
+            // row r of P^- = (F P)[r,:] F^T + Q[r,:]
+            double Ur[D];
+#pragma unroll
+            for (int q = 0; q < D; ++q) Ur[q] = Gs.U[r][q];
+            if (act) {
+#pragma unroll
+                for (int j = 0; j < D; ++j) {
+                    double s2 = Qp[r * LD(D) + j];
+#pragma unroll
+                    for (int q = 0; q < D; ++q) s2 = fma(Ur[q], Fp[j * LD(D) + q], s2);
+                    Gs.Pm[r][j] = s2;
+                    Gs.Ps[r][j] = Psr[j] - s2;          // Delta = P^s_{k+1} - P^- (row r)
+                }
+                Gs.dm[r] = msr - xm;
+            }
+            __syncwarp();
+            // Cholesky of P^- (upper triangle) in every lane: L lower, Li = 1 / L_jj
+            double L[D][D], Li[D];
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                double sd = Gs.Pm[j][j];
+#pragma unroll
+                for (int q = 0; q < j; ++q) sd = fma(-L[j][q], L[j][q], sd);
+                bad = bad || !(sd > 0.0);
+                Li[j] = rsqrt(sd);
+#pragma unroll
+                for (int i = j + 1; i < D; ++i) {
+                    double so = Gs.Pm[j][i];
+#pragma unroll
+                    for (int q = 0; q < j; ++q) so = fma(-L[i][q], L[j][q], so);
+                    L[i][j] = so * Li[j];
+                }
+                L[j][j] = sd * Li[j];
+            }
+            // column r of X = P^-^{-1} (F P)
+            double Xc[D];
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+                double z = Uc[i];
+#pragma unroll
+                for (int q = 0; q < i; ++q) z = fma(-L[i][q], Xc[q], z);
+                Xc[i] = z * Li[i];
+            }
+#pragma unroll
+            for (int i = D - 1; i >= 0; --i) {
+                double z = Xc[i];
+#pragma unroll
+                for (int q = i + 1; q < D; ++q) z = fma(-L[q][i], Xc[q], z);
+                Xc[i] = z * Li[i];
+            }
+            // m^s_r = xbar_r + X[:,r] . (m^s_{k+1} - xm);  V = X[:,r]^T (P^s_{k+1} - P^-) (upper triangles)
+            double ms_new = xa[r], V[D];
+#pragma unroll
+            for (int q = 0; q < D; ++q) ms_new = fma(Xc[q], Gs.dm[q], ms_new);
+#pragma unroll
+            for (int bb = 0; bb < D; ++bb) {
+                double v = 0.0;
+#pragma unroll
+                for (int a = 0; a < D; ++a) {
+                    const int lo = a < bb ? a : bb, hi = a < bb ? bb : a;
+                    v = fma(Xc[a], Gs.Ps[lo][hi], v);
+                }
+                V[bb] = v;
+            }
+            if (act) {
+#pragma unroll
+                for (int i = 0; i < D; ++i) Gs.X[i][r] = Xc[i];
+            }
+            __syncwarp();
+            // row r of P^s_k = P[r,:] + V X
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                double s2 = Pr[j];
+#pragma unroll
+                for (int bb = 0; bb < D; ++bb) s2 = fma(V[bb], Gs.X[bb][j], s2);
+                Psr[j] = s2;
+            }
+            msr = ms_new;
+            __syncwarp();                           // Gs buffers are rewritten by the next step
+        }
+        tnext = tk;
+        // projection mean = H m^s, var = H P^s H^T (rows summed over the lanes)
+        double mo = hr * msr, vo = 0.0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) vo = fma(Psr[j], M.H[j], vo);
+        vo *= hr;
+#pragma unroll
+        for (int off = kGL / 2; off > 0; off >>= 1) {
+            mo += __shfl_xor_sync(0xffffffffu, mo, off);
+            vo += __shfl_xor_sync(0xffffffffu, vo, off);
+        }
+        if (lane == 0) {
+            if (p.mean) p.mean[k] = mo;
+            if (p.var) p.var[k] = vo;
+        }
+    }
+    if (bad && lane == 0) raise_error(p.err, p.k0 + kb, kErrNumeric);
+}
+
 }  // namespace wide
 }  // namespace pssgp
