@@ -430,6 +430,8 @@ void wide_set_smem_attrs() {
     if constexpr (D <= kGL) {
         cudaFuncSetAttribute(kw_filter_fold_lpr<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K1LSmem<D>));
         cudaFuncSetAttribute(kw_filter_fold_lpr<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K1LSmem<D>));
+        cudaFuncSetAttribute(kw_filter_apply_lpr<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K3LSmem<D>));
+        cudaFuncSetAttribute(kw_filter_apply_lpr<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K3LSmem<D>));
         cudaFuncSetAttribute(kw_smoother_apply_lpr<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K5LSmem<D>));
         cudaFuncSetAttribute(kw_smoother_apply_lpr<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K5LSmem<D>));
     }
@@ -442,10 +444,10 @@ void wide_set_smem_attrs() {
 }
 
 // lane-per-row kernels of the wide path for D <= 8 (bit 0: fold, bit 1: RTS rescan, bit 2: RTS
-// rescan also with per-step (F, Q), bit 3: one-wave plan for them on the table path); env
-// PSSGP_WIDE_LPR overrides the default 11 for A/B runs (0 = the shared-memory kernels)
+// rescan also with per-step (F, Q), bit 3: one-wave plan for them on the table path, bit 4: Kalman
+// rescan); env PSSGP_WIDE_LPR overrides the default 27 for A/B runs (0 = the shared-memory kernels)
 int wide_lpr_mask() {
-    static const int v = [] { const char* e = getenv("PSSGP_WIDE_LPR"); return e && *e ? atoi(e) : 11; }();
+    static const int v = [] { const char* e = getenv("PSSGP_WIDE_LPR"); return e && *e ? atoi(e) : 27; }();
     return v;
 }
 
@@ -467,9 +469,11 @@ WPlan make_wplan(pssgp_model* m, int64_t n) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, kw_smoother_apply<D>, 32 * kWWarps, sizeof(K5Smem<D>));
         m->wocc = std::max(1, std::min(a, std::min(b, c)));
         if constexpr (D <= kGL) {
-            int l1 = 0, l5 = 0;
+            int l1 = 0, l5 = 0, l3 = 0;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l1, kw_filter_fold_lpr<D, false>, 32 * kWWarps, sizeof(K1LSmem<D>));
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l3, kw_filter_apply_lpr<D, false>, 32 * kWWarps, sizeof(K3LSmem<D>));
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l5, kw_smoother_apply_lpr<D, false>, 32 * kWWarps, sizeof(K5LSmem<D>));
+            if (wide_lpr_mask() & 16) l5 = std::min(l5, l3);
             if (getenv("PSSGP_WIDE_DEBUG"))
                 fprintf(stderr, "wide plan D=%d occupancy: fold %d, apply %d, smoother %d, lpr fold %d, lpr smoother %d\n",
                         D, a, b, c, l1, l5);
@@ -653,6 +657,15 @@ template <int D>
 pssgp_status wide_fapply(pssgp_model* m, pssgp::wide::WParams& p, int nb, cudaStream_t s) {
     using namespace pssgp::wide;
     ProfScope ps(m, S_K3, s);
+    if constexpr (D <= kGL) {
+        // bit 4: lane-per-row Kalman rescan (uniform dt unless bit 2)
+        if ((wide_lpr_mask() & 16) && (!p.fq || (wide_lpr_mask() & 4))) {
+            if (p.fq) kw_filter_apply_lpr<D, true><<<nb, 32 * kWWarps, sizeof(K3LSmem<D>), s>>>(p);
+            else kw_filter_apply_lpr<D, false><<<nb, 32 * kWWarps, sizeof(K3LSmem<D>), s>>>(p);
+            LAUNCH_CHECK(m, "kw_filter_apply_lpr");
+            return PSSGP_OK;
+        }
+    }
     kw_filter_apply<D><<<nb, 32 * kWWarps, sizeof(K3Smem<D>), s>>>(p);
     LAUNCH_CHECK(m, "kw_filter_apply");
     return PSSGP_OK;

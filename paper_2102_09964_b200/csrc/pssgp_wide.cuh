@@ -1101,6 +1101,89 @@ struct K3Smem {
     } w[kWWarps];
 };
 
+// chain smoother aggregate (E, g, L) of K3w from the chain's last filtered moments (W.P, W.x) and
+// the propagated moments (W.u.st.Sg, P0, x0); shared by both K3w kernels
+template <int D>
+__device__ void k3w_chain_sagg(const WParams& p, typename K3Smem<D>::PerWarp& W, const SModel<D>& M, int c,
+                               int64_t kb, int64_t ke, double tprev, int lane) {
+    // ---- chain smoother aggregate (E, g, L), as in the d <= 3 path (DESIGN.md §5)
+    SS<D>* sagg = &W.u.st.sagg;
+    if (ke <= kb) {
+        set_identity<D>(*sagg, lane);
+    } else if (p.k0 + ke == p.nglob) {
+        for (int e = lane; e < D * D; e += 32) {
+            const int i = e / D, j = e - (e / D) * D;
+            sagg->E[i][j] = 0.0;
+            sagg->L[i][j] = W.u.st.P0[i][j];
+        }
+        for (int i = lane; i < D; i += 32) sagg->g[i] = W.u.st.x0[i];
+        __syncwarp();
+    } else {
+        const double tn = __ldg(p.t + ke);
+        const int kind = wdisc_kind(tn - tprev, M.udt, p.fq != nullptr);
+        const FQp<D> fqp = wfq<D>(p, M, ke);
+        // Pm, xm of the next step; Sm = Sg F^T
+        for (int e = lane; e < D * D; e += 32) {
+            const int i = e / D, j = e - (e / D) * D;
+            double fp = 0.0, sm = 0.0;
+            if (kind == 0) {
+                for (int q = 0; q < D; ++q) {
+                    fp = fma(fqp.F[i][q], W.P[q][j], fp);
+                    sm = fma(W.u.st.Sg[i][q], fqp.F[j][q], sm);
+                }
+            } else {
+                fp = W.P[i][j];
+                sm = W.u.st.Sg[i][j];
+            }
+            W.u.st.FP[i][j] = fp;
+            W.u.st.Sm[i][j] = sm;
+        }
+        for (int i = lane; i < D; i += 32) {
+            double s = 0.0;
+            if (kind == 0)
+                for (int q = 0; q < D; ++q) s = fma(fqp.F[i][q], W.x[q], s);
+            else
+                s = W.x[i];
+            W.u.st.xm[i] = s;
+        }
+        __syncwarp();
+        for (int e = lane; e < D * D; e += 32) {
+            const int i = e / D, j = e - (e / D) * D;
+            double s = (kind == 0) ? fqp.Q[i][j] : 0.0;
+            if (kind == 0)
+                for (int q = 0; q < D; ++q) s = fma(W.u.st.FP[i][q], fqp.F[j][q], s);
+            else
+                s = W.u.st.FP[i][j];
+            W.u.st.Pm[i][j] = s;
+        }
+        __syncwarp();
+        // E = Sm Pm^-1 : invert Pm (into W.u.st.FP via winverse on a copy)
+        for (int e = lane; e < D * D; e += 32) W.u.st.FP[e / D][e % D] = W.u.st.Pm[e / D][e % D];
+        __syncwarp();
+        if (!winverse<D>(W.u.st.FP, W.u.st.W2, lane) && lane == 0) raise_error(p.err, p.k0 + ke, kErrNumeric);
+        wmm<D>(sagg->E, W.u.st.Sm, W.u.st.FP, nullptr, lane);
+        __syncwarp();
+        for (int i = lane; i < D; i += 32) {
+            double a = W.u.st.x0[i];
+            for (int q = 0; q < D; ++q) a = fma(-sagg->E[i][q], W.u.st.xm[q], a);
+            sagg->g[i] = a;
+        }
+        for (int e = lane; e < D * D; e += 32) {
+            const int i = e / D, j = e - (e / D) * D;
+            double a = W.u.st.P0[i][j];
+            for (int q = 0; q < D; ++q) a = fma(-sagg->E[i][q], W.u.st.Sm[j][q], a);
+            W.u.st.Pm[i][j] = a;
+        }
+        __syncwarp();
+        for (int e = lane; e < D * D; e += 32) {
+            const int i = e / D, j = e - (e / D) * D;
+            sagg->L[i][j] = 0.5 * (W.u.st.Pm[i][j] + W.u.st.Pm[j][i]);
+        }
+        __syncwarp();
+    }
+    gstore<D>(*sagg, p.sagg + static_cast<int64_t>(c) * SNW(D), lane);
+}
+
 template <int D>
 __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WMINB) kw_filter_apply(const WParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1215,82 +1298,181 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WMINB) kw_filter_apply(con
         p.nll_chain[c] = nobs ? 0.5 * (quad + logs + nobs * 1.8378770664093453) : 0.0;
     }
     if (!p.store_state) return;
-    // ---- chain smoother aggregate (E, g, L), as in the d <= 3 path (DESIGN.md §5)
-    SS<D>* sagg = &W.u.st.sagg;
-    if (ke <= kb) {
-        set_identity<D>(*sagg, lane);
-    } else if (p.k0 + ke == p.nglob) {
-        for (int e = lane; e < D * D; e += 32) {
-            const int i = e / D, j = e - (e / D) * D;
-            sagg->E[i][j] = 0.0;
-            sagg->L[i][j] = W.u.st.P0[i][j];
-        }
-        for (int i = lane; i < D; i += 32) sagg->g[i] = W.u.st.x0[i];
-        __syncwarp();
-    } else {
-        const double tn = __ldg(p.t + ke);
-        const int kind = wdisc_kind(tn - tprev, M.udt, p.fq != nullptr);
-        const FQp<D> fqp = wfq<D>(p, M, ke);
-        // Pm, xm of the next step; Sm = Sg F^T
-        for (int e = lane; e < D * D; e += 32) {
-            const int i = e / D, j = e - (e / D) * D;
-            double fp = 0.0, sm = 0.0;
-            if (kind == 0) {
-                for (int q = 0; q < D; ++q) {
-                    fp = fma(fqp.F[i][q], W.P[q][j], fp);
-                    sm = fma(W.u.st.Sg[i][q], fqp.F[j][q], sm);
-                }
-            } else {
-                fp = W.P[i][j];
-                sm = W.u.st.Sg[i][j];
-            }
-            W.u.st.FP[i][j] = fp;
-            W.u.st.Sm[i][j] = sm;
-        }
-        for (int i = lane; i < D; i += 32) {
-            double s = 0.0;
-            if (kind == 0)
-                for (int q = 0; q < D; ++q) s = fma(fqp.F[i][q], W.x[q], s);
-            else
-                s = W.x[i];
-            W.u.st.xm[i] = s;
-        }
-        __syncwarp();
-        for (int e = lane; e < D * D; e += 32) {
-            const int i = e / D, j = e - (e / D) * D;
-            double s = (kind == 0) ? fqp.Q[i][j] : 0.0;
-            if (kind == 0)
-                for (int q = 0; q < D; ++q) s = fma(W.u.st.FP[i][q], fqp.F[j][q], s);
-            else
-                s = W.u.st.FP[i][j];
-            W.u.st.Pm[i][j] = s;
-        }
-        __syncwarp();
-        // E = Sm Pm^-1 : invert Pm (into W.u.st.FP via winverse on a copy)
-        for (int e = lane; e < D * D; e += 32) W.u.st.FP[e / D][e % D] = W.u.st.Pm[e / D][e % D];
-        __syncwarp();
-        if (!winverse<D>(W.u.st.FP, W.u.st.W2, lane) && lane == 0) raise_error(p.err, p.k0 + ke, kErrNumeric);
-        wmm<D>(sagg->E, W.u.st.Sm, W.u.st.FP, nullptr, lane);
-        __syncwarp();
-        for (int i = lane; i < D; i += 32) {
-            double a = W.u.st.x0[i];
-            for (int q = 0; q < D; ++q) a = fma(-sagg->E[i][q], W.u.st.xm[q], a);
-            sagg->g[i] = a;
-        }
-        for (int e = lane; e < D * D; e += 32) {
-            const int i = e / D, j = e - (e / D) * D;
-            double a = W.u.st.P0[i][j];
-            for (int q = 0; q < D; ++q) a = fma(-sagg->E[i][q], W.u.st.Sm[j][q], a);
-            W.u.st.Pm[i][j] = a;
-        }
-        __syncwarp();
-        for (int e = lane; e < D * D; e += 32) {
-            const int i = e / D, j = e - (e / D) * D;
-            sagg->L[i][j] = 0.5 * (W.u.st.Pm[i][j] + W.u.st.Pm[j][i]);
-        }
-        __syncwarp();
+    k3w_chain_sagg<D>(p, W, M, c, kb, ke, tprev, lane);
+}
+
+// ------------------------------------------------------------------ K3w for D <= 8: lane-per-row Kalman rescan
+// Same grid, carry, outputs and chain smoother aggregate as kw_filter_apply; the step recursion
+// (PAPER.md:285-324 Kalman step from the collapsed carry, Prop. 1 order) runs in registers with
+// lane r (< D) owning row r of P, Sg = Cov(x_k0, x_k), P0 and x_r, x0_r; F P is transposed
+// through a per-warp shared buffer, the full x, HP, SH vectors are gathered by shuffles.  The
+// moments are written back to the shared layout for the chain smoother aggregate.
+template <int D>
+struct K3LSmem {
+    K3Smem<D> b;
+    double I[D][LD(D)], Z[D][LD(D)];
+    double U[kWWarps][D][LD(D)];
+};
+
+template <int D, bool STREAM>
+__global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_filter_apply_lpr(const WParams p) {
+    static_assert(D <= kGL, "lane-per-row rescan holds one row per lane");
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    K3LSmem<D>& shl = *reinterpret_cast<K3LSmem<D>*>(smem_raw);
+    K3Smem<D>& sh = shl.b;
+    load_model<D>(sh.m, p.model);
+    for (int e = threadIdx.x; e < D * D; e += blockDim.x) {
+        const int i = e / D, j = e - (e / D) * D;
+        shl.I[i][j] = (i == j) ? 1.0 : 0.0;
+        shl.Z[i][j] = 0.0;
     }
-    gstore<D>(*sagg, p.sagg + static_cast<int64_t>(c) * SNW(D), lane);
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int c = blockIdx.x * kWWarps + wid;
+    if (c >= p.nch) return;
+    auto& W = sh.w[wid];
+    auto& U = shl.U[wid];
+    const SModel<D>& M = sh.m;
+    // ---- carry (x, P) entering the chain (warp-cooperative, as kw_filter_apply)
+    for (int e = lane; e < D * D; e += 32) W.P[e / D][e % D] = 0.0;
+    for (int i = lane; i < D; i += 32) W.x[i] = 0.0;
+    __syncwarp();
+    for (int g = 0; g < p.rank && p.in_filt; ++g) {
+        gload<D>(W.u.c.a, p.in_filt + static_cast<int64_t>(g) * FNW(D), lane);
+        wapply_prefix<D>(W.x, W.P, W.u.c.a, W.u.c.s, lane);
+    }
+    if (c > 0) {
+        gload<D>(W.u.c.a, p.fagg + static_cast<int64_t>(c - 1) * FNW(D), lane);
+        if (!wapply_prefix<D>(W.x, W.P, W.u.c.a, W.u.c.s, lane) && lane == 0) raise_error(p.err, p.k0, kErrNumeric);
+    }
+    const bool act = lane < D;
+    const int r = act ? lane : 0;
+    double Pr[D], Sgr[D], P0r[D], xr = W.x[r], x0r = 0.0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) { Pr[j] = W.P[r][j]; Sgr[j] = 0.0; P0r[j] = 0.0; }
+    const double hr = act ? M.H[r] : 0.0;
+    __syncwarp();
+
+    const int64_t kb = static_cast<int64_t>(c) * p.K;
+    const int64_t ke = min(kb + p.K, p.n);
+    double tprev = (kb < p.n && (kb > 0 || p.k0 > 0)) ? __ldg(p.t + kb - 1) : 0.0;
+    double quad = 0.0, logs = 0.0;
+    int nobs = 0;
+    bool bad_s = false;
+    int64_t bad_g = 0;
+    double* xpc = p.xp + static_cast<int64_t>(c) * p.K * CNW(D);
+    double tn_ = 0.0, yn_ = 0.0;
+    unsigned char mn_ = 0;
+    if (kb < ke) { tn_ = __ldg(p.t + kb); mn_ = __ldg(p.mask + kb); yn_ = __ldg(p.y + kb); }
+    for (int64_t k = kb; k < ke; ++k) {
+        const double tk = tn_;
+        const bool obs = mn_ != 0;
+        const double yk = obs ? yn_ : 0.0;
+        if (k + 1 < ke) { tn_ = __ldg(p.t + k + 1); mn_ = __ldg(p.mask + k + 1); yn_ = __ldg(p.y + k + 1); }
+        const int64_t g = p.k0 + k;
+        const int kind = (g == 0) ? 3 : wdisc_kind(tk - tprev, M.udt, STREAM);
+        const bool first = (k == kb);
+        tprev = tk;
+        const double* Fp;
+        const double* Qp;
+        if (kind == 0) {
+            if (STREAM) { Fp = p.fq + k * FQW(D); Qp = Fp + D * LD(D); }
+            else { Fp = &M.F[0][0]; Qp = &M.Q[0][0]; }
+        } else if (kind == 1) {
+            Fp = &shl.I[0][0]; Qp = &shl.Z[0][0];
+        } else {                                     // 3 (and 2, reported by the fold): F = 0, Q = P_inf
+            Fp = &shl.Z[0][0]; Qp = &M.Pinf[0][0];
+        }
+        // column r of F P, xm_r = F[r,:] x, row r of Sm = Sg[r,:] F^T
+        double Uc[D], xm = 0.0;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            double su = 0.0;
+#pragma unroll
+            for (int q = 0; q < D; ++q) su = fma(Fp[i * LD(D) + q], Pr[q], su);
+            Uc[i] = su;
+        }
+#pragma unroll
+        for (int q = 0; q < D; ++q) xm = fma(Fp[r * LD(D) + q], __shfl_sync(0xffffffffu, xr, q), xm);
+        if (act) {
+#pragma unroll
+            for (int i = 0; i < D; ++i) U[i][r] = Uc[i];
+        }
+        __syncwarp();
+        double Pm[D], Sm[D], HP = 0.0, SH = 0.0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            double s2 = Qp[r * LD(D) + j], s3 = 0.0;
+#pragma unroll
+            for (int q = 0; q < D; ++q) {
+                const double f = Fp[j * LD(D) + q];
+                s2 = fma(U[r][q], f, s2);
+                s3 = fma(Sgr[q], f, s3);
+            }
+            Pm[j] = s2;
+            Sm[j] = s3;
+            HP = fma(s2, M.H[j], HP);
+            SH = fma(s3, M.H[j], SH);
+        }
+        __syncwarp();                                 // U is rewritten by the next step
+        if (!act) { HP = 0.0; SH = 0.0; }
+        double S = hr * HP, hx = hr * xm;
+#pragma unroll
+        for (int off = kGL / 2; off > 0; off >>= 1) {
+            S += __shfl_xor_sync(0xffffffffu, S, off);
+            hx += __shfl_xor_sync(0xffffffffu, hx, off);
+        }
+        S += M.r;
+        if (obs && !(S > 0.0 && S < INFINITY) && !bad_s) { bad_s = true; bad_g = g; }
+        const double iS = obs ? 1.0 / S : 0.0;
+        const double v = obs ? (yk - hx) : 0.0;
+        const double vs = v * iS;
+        const double HPs = HP * iS, SHs = SH * iS;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            const double HPj = __shfl_sync(0xffffffffu, HP, j);
+            const double SHj = __shfl_sync(0xffffffffu, SH, j);
+            const double Pn = fma(-HPs, HPj, Pm[j]);
+            Pr[j] = Pn;
+            if (first) {
+                P0r[j] = Pn;
+                Sgr[j] = Pn;
+            } else {
+                Sgr[j] = fma(-SHs, HPj, Sm[j]);
+                P0r[j] = fma(-SHs, SHj, P0r[j]);
+            }
+        }
+        xr = fma(HP, vs, xm);
+        x0r = first ? xr : fma(SH, vs, x0r);
+        if (obs) {
+            quad = fma(v, vs, quad);
+            logs += log(S);
+            ++nobs;
+        }
+        if (p.store_state && act) {
+            double* o = xpc + (k - kb) * CNW(D);
+            o[r] = xr;
+#pragma unroll
+            for (int j = 0; j < D; ++j)
+                if (j >= r) o[D + si(D, r, j)] = Pr[j];
+        }
+    }
+    if (bad_s && lane == 0) raise_error(p.err, bad_g, kErrNumeric);
+    if (lane == 0) p.nll_chain[c] = nobs ? 0.5 * (quad + logs + nobs * 1.8378770664093453) : 0.0;
+    if (!p.store_state) return;
+    // moments back to the shared layout for the chain smoother aggregate
+    if (act) {
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            W.P[r][j] = Pr[j];
+            W.u.st.Sg[r][j] = Sgr[j];
+            W.u.st.P0[r][j] = P0r[j];
+        }
+        W.x[r] = xr;
+        W.u.st.x0[r] = x0r;
+    }
+    __syncwarp();
+    k3w_chain_sagg<D>(p, W, M, c, kb, ke, tprev, lane);
 }
 
 // ------------------------------------------------------------------ K5w: RTS rescan
