@@ -443,11 +443,12 @@ void wide_set_smem_attrs() {
     done = true;
 }
 
-// lane-per-row kernels of the wide path for D <= 8 (bit 0: fold, bit 1: RTS rescan, bit 2: RTS
-// rescan also with per-step (F, Q), bit 3: one-wave plan for them on the table path, bit 4: Kalman
-// rescan); env PSSGP_WIDE_LPR overrides the default 27 for A/B runs (0 = the shared-memory kernels)
+// lane-per-row kernels of the wide path for D <= 8 (bit 0: fold, bit 1: RTS rescan, bit 2: both
+// rescans also with per-step (F, Q) staged in shared memory, bit 3: one-wave plan for them on the
+// table path, bit 4: Kalman rescan, bit 5: the one-wave plan also on the per-step (F, Q) path); env
+// PSSGP_WIDE_LPR overrides the default 63 for A/B runs (0 = the shared-memory kernels)
 int wide_lpr_mask() {
-    static const int v = [] { const char* e = getenv("PSSGP_WIDE_LPR"); return e && *e ? atoi(e) : 27; }();
+    static const int v = [] { const char* e = getenv("PSSGP_WIDE_LPR"); return e && *e ? atoi(e) : 63; }();
     return v;
 }
 
@@ -480,7 +481,7 @@ WPlan make_wplan(pssgp_model* m, int64_t n) {
             // bit 3: on the table (uniform-dt) path, where both lane-per-row kernels run, size the
             // plan so they run in one wave (C3: 13.8 -> 11.7 ms; on the per-step (F, Q) path the
             // fewer, longer chains slow the shared-memory rescans: 26.2 -> 28.3 ms, so not there)
-            if ((wide_lpr_mask() & 8) && m->mode != kPade) m->wocc = std::max(1, std::min(m->wocc, std::min(l1, l5)));
+            if ((wide_lpr_mask() & 8) && (m->mode != kPade || (wide_lpr_mask() & 32))) m->wocc = std::max(1, std::min(m->wocc, std::min(l1, l5)));
         }
     }
     const int64_t target = static_cast<int64_t>(m->sm_count) * m->wocc * kWWarps;

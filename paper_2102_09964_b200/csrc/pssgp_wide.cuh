@@ -1312,6 +1312,7 @@ struct K3LSmem {
     K3Smem<D> b;
     double I[D][LD(D)], Z[D][LD(D)];
     double U[kWWarps][D][LD(D)];
+    double fqs[kWWarps][2][FQW(D)];                 // STREAM: per-step (F_k, Q_k) staged one step ahead
 };
 
 template <int D, bool STREAM>
@@ -1364,7 +1365,25 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_filter_apply
     double tn_ = 0.0, yn_ = 0.0;
     unsigned char mn_ = 0;
     if (kb < ke) { tn_ = __ldg(p.t + kb); mn_ = __ldg(p.mask + kb); yn_ = __ldg(p.y + kb); }
+    auto& fqs = shl.fqs[wid];
+    if (STREAM && kb < ke) {
+        const double* src = p.fq + kb * FQW(D);
+        for (int i = lane; i < FQW(D); i += 32) cp_async8(&fqs[0][i], src + i, 8);
+        cp_async_commit();
+    }
     for (int64_t k = kb; k < ke; ++k) {
+        const int fb = static_cast<int>((k - kb) & 1);
+        if (STREAM) {
+            // (F_k, Q_k) staged in slot fb; slot fb^1 was last read before the previous step's
+            // closing __syncwarp, so the copy for k + 1 may start once this one is visible
+            cp_async_wait<0>();
+            __syncwarp();
+            if (k + 1 < ke) {
+                const double* src = p.fq + (k + 1) * FQW(D);
+                for (int i = lane; i < FQW(D); i += 32) cp_async8(&fqs[fb ^ 1][i], src + i, 8);
+                cp_async_commit();
+            }
+        }
         const double tk = tn_;
         const bool obs = mn_ != 0;
         const double yk = obs ? yn_ : 0.0;
@@ -1376,7 +1395,7 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_filter_apply
         const double* Fp;
         const double* Qp;
         if (kind == 0) {
-            if (STREAM) { Fp = p.fq + k * FQW(D); Qp = Fp + D * LD(D); }
+            if (STREAM) { Fp = &fqs[fb][0]; Qp = Fp + D * LD(D); }
             else { Fp = &M.F[0][0]; Qp = &M.Q[0][0]; }
         } else if (kind == 1) {
             Fp = &shl.I[0][0]; Qp = &shl.Z[0][0];
@@ -1659,6 +1678,7 @@ struct K5LSmem {
     struct G {
         double U[D][LD(D)], Pm[D][LD(D)], Ps[D][LD(D)] /* P^s_{k+1} - P^- */, X[D][LD(D)];
         double dm[D];
+        double fqs[2][FQW(D)];                      // STREAM: (F_{k+1}, Q_{k+1}) staged with the record of k
     } g[kWWarps];
 };
 
@@ -1720,6 +1740,10 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_smoother_app
     if (ke > kb) {
         const double* src = xpc + (ke - 1 - kb) * CNW(D);
         for (int i = lane; i < CNW(D); i += 32) cp_async8(&W.xst[0][i], src + i, 8);
+        if (STREAM && p.k0 + ke < p.nglob) {       // F, Q of the transition out of ke - 1 (record ke)
+            const double* fsrc = p.fq + ke * FQW(D);
+            for (int i = lane; i < FQW(D); i += 32) cp_async8(&Gs.fqs[0][i], fsrc + i, 8);
+        }
         cp_async_commit();
         tk_next = __ldg(p.t + ke - 1);
     }
@@ -1733,9 +1757,14 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_smoother_app
         if (k > kb) {
             const double* src = xpc + (k - 1 - kb) * CNW(D);
             for (int i = lane; i < CNW(D); i += 32) cp_async8(&W.xst[sb ^ 1][i], src + i, 8);
+            if (STREAM) {                           // record k: the transition out of k - 1
+                const double* fsrc = p.fq + k * FQW(D);
+                for (int i = lane; i < FQW(D); i += 32) cp_async8(&Gs.fqs[sb ^ 1][i], fsrc + i, 8);
+            }
             cp_async_commit();
             tk_next = __ldg(p.t + k - 1);
         }
+        const int fb = sb;
         // filtered (xbar_k, row r of P_k) from the staged packed record
         double xa[D], Pr[D];
         {
@@ -1755,7 +1784,7 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_smoother_app
             const double* Fp;
             const double* Qp;
             if (kind == 0) {
-                if (STREAM) { Fp = p.fq + (k + 1) * FQW(D); Qp = Fp + D * LD(D); }
+                if (STREAM) { Fp = &Gs.fqs[fb][0]; Qp = Fp + D * LD(D); }
                 else { Fp = &M.F[0][0]; Qp = &M.Q[0][0]; }
             } else {                                // dt == 0 (or unsupported, reported by the fold): F = I, Q = 0
                 Fp = &shl.I[0][0]; Qp = &shl.Z[0][0];

@@ -1,5 +1,6 @@
 """Full-size parity of a BASELINE config on one GPU against the sequential oracle:
 python tools/config_parity.py c3            (RBF-6, N = 2^22, uniform dt)
+python tools/config_parity.py c3i           (RBF-6, N = 2^22, jittered dt: per-step (F, Q) path)
 python tools/config_parity.py c4 [N]        (periodic J=6 + Matern-3/2, d = 16; default N = 2^20)
 python tools/config_parity.py c2            (Matern-5/2, 2^20 + 10^4 test points)"""
 import os
@@ -17,6 +18,8 @@ import paper_2102_09964_b200 as P
 cfg = sys.argv[1]
 if cfg == "c3":
     w = synth.config3()
+elif cfg == "c3i":
+    w = synth.config3(irregular=True)
 elif cfg == "c4":
     w = synth.config4(n=int(sys.argv[2]) if len(sys.argv) > 2 else 2 ** 20)
 elif cfg == "c2":
