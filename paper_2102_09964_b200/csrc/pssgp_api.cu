@@ -445,10 +445,11 @@ void wide_set_smem_attrs() {
 
 // lane-per-row kernels of the wide path for D <= 8 (bit 0: fold, bit 1: RTS rescan, bit 2: both
 // rescans also with per-step (F, Q) staged in shared memory, bit 3: one-wave plan for them on the
-// table path, bit 4: Kalman rescan, bit 5: the one-wave plan also on the per-step (F, Q) path); env
-// PSSGP_WIDE_LPR overrides the default 63 for A/B runs (0 = the shared-memory kernels)
+// table path, bit 4: Kalman rescan, bit 5: the one-wave plan also on the per-step (F, Q) path, bit 6:
+// lane-per-row discretisation); env PSSGP_WIDE_LPR overrides the default 127 for A/B runs (0 = the
+// shared-memory kernels)
 int wide_lpr_mask() {
-    static const int v = [] { const char* e = getenv("PSSGP_WIDE_LPR"); return e && *e ? atoi(e) : 63; }();
+    static const int v = [] { const char* e = getenv("PSSGP_WIDE_LPR"); return e && *e ? atoi(e) : 127; }();
     return v;
 }
 
@@ -561,6 +562,21 @@ pssgp_status wide_prepare(pssgp_model* m, pssgp::wide::WParams& p, cudaStream_t 
             return fail(m, PSSGP_E_NOMEM, "cudaMalloc(per-step F, Q) failed");
         }
         m->fq_bytes = need;
+    }
+    if constexpr (D <= kGL) {
+        if (wide_lpr_mask() & 64) {   // lane-per-row discretisation: one step per 8-lane group
+            int occ = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kw_discretize_lpr<D>, 32 * kWWarps, 0);
+            const int64_t want = (nfq * kGL + 32 * kWWarps - 1) / (32 * kWWarps);
+            const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(m->sm_count) * std::max(1, occ))));
+            {
+                ProfScope ps(m, S_DISC, s);
+                kw_discretize_lpr<D><<<grid, 32 * kWWarps, 0, s>>>(p.t, nfq, p.k0, m->d_model, m->fq);
+                LAUNCH_CHECK(m, "kw_discretize_lpr");
+            }
+            p.fq = m->fq;
+            return PSSGP_OK;
+        }
     }
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kw_discretize<D>, 32 * kWWarps, sizeof(KDSmem<D>));

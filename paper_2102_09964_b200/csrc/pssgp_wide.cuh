@@ -891,6 +891,146 @@ struct K1LSmem {
 #ifndef PSSGP_WLPR_MINB
 #define PSSGP_WLPR_MINB 3                        // resident CTAs/SM the lane-per-row fold is register-capped for
 #endif
+
+// ------------------------------------------------------------------ KDl: lane-per-row discretisation
+// The same algorithm as kw_discretize (Taylor expm of G tau and the Van Loan series of Q_tau, then s
+// squarings: supp. P:294-303) with one step per 8-lane group and row r of every matrix in lane r's
+// registers; products take the other rows by group shuffles.  Four steps per warp, no shared
+// memory, no __syncwarp phases.  The A Z + (A Z)^T symmetrisation is formed as A Z + Z A^T with
+// the same products in the same order (Z symmetric), so it is exactly symmetric as before.
+template <int D>
+__device__ __forceinline__ void g_mm(double (&out)[D], const double (&x)[D], const double (&y)[D], unsigned gm) {
+#pragma unroll
+    for (int j = 0; j < D; ++j) out[j] = 0.0;
+#pragma unroll
+    for (int q = 0; q < D; ++q)
+#pragma unroll
+        for (int j = 0; j < D; ++j) out[j] = fma(x[q], __shfl_sync(gm, y[j], q, kGL), out[j]);
+}
+template <int D>   // row r of X Y^T (+ add)
+__device__ __forceinline__ void g_mmt(double (&out)[D], const double (&x)[D], const double (&y)[D], const double* add,
+                                      unsigned gm) {
+#pragma unroll
+    for (int i = 0; i < D; ++i) out[i] = 0.0;
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) out[i] = fma(x[j], __shfl_sync(gm, y[j], i, kGL), out[i]);
+    if (add) {
+#pragma unroll
+        for (int i = 0; i < D; ++i) out[i] += add[i];
+    }
+}
+
+#ifndef PSSGP_WDISC_MINB
+#define PSSGP_WDISC_MINB 4                       // resident CTAs/SM kw_discretize_lpr is register-capped for (1: 5.31, 4: 5.04, 5: 5.31 ms at C3 irregular)
+#endif
+template <int D>
+__global__ void __launch_bounds__(32 * kWWarps, PSSGP_WDISC_MINB) kw_discretize_lpr(const double* __restrict__ t, int64_t nfq, int64_t k0,
+                                                                   const double* __restrict__ model, double* fq) {
+    static_assert(D <= kGL, "one row per lane of an 8-lane group");
+    const int lane = threadIdx.x & 31, grp = lane / kGL, r0 = lane % kGL;
+    const bool act = r0 < D;
+    const int r = act ? r0 : 0;
+    const unsigned gm = 0xFFu << (grp * kGL);
+    double Gr[D], Wr[D];
+    double gnorm = 0.0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        Gr[j] = __ldg(model + 3 * D * D + D + 2 + r * D + j);
+        Wr[j] = __ldg(model + 4 * D * D + D + 2 + r * D + j);
+        double cs = 0.0;
+        for (int i = 0; i < D; ++i) cs += fabs(__ldg(model + 3 * D * D + D + 2 + i * D + j));
+        gnorm = fmax(gnorm, cs);
+    }
+    constexpr double c[13] = {1.0, 1.0, 1.0 / 2, 1.0 / 6, 1.0 / 24, 1.0 / 120, 1.0 / 720, 1.0 / 5040, 1.0 / 40320,
+                              1.0 / 362880, 1.0 / 3628800, 1.0 / 39916800, 1.0 / 479001600};
+    const int64_t ng = static_cast<int64_t>(gridDim.x) * blockDim.x / kGL;
+    for (int64_t k = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / kGL; k < nfq; k += ng) {
+        if (k0 + k == 0) continue;
+        const double dt = __ldg(t + k) - __ldg(t + k - 1);
+        if (dt == 0.0 || !(dt == dt)) continue;
+        const double nrm = gnorm * fabs(dt);
+        int s = 0;
+        if (nrm > 0.125) frexp(nrm / 0.125, &s);
+        const bool low = (nrm <= 0.017);
+        const double tau = ldexp(dt, -s);
+        double A[D], A2[D], A3[D], X[D], B[D], T[D];
+#pragma unroll
+        for (int j = 0; j < D; ++j) A[j] = Gr[j] * tau;
+        g_mm<D>(A2, A, A, gm);
+        g_mm<D>(A3, A2, A, gm);
+        auto tblock = [&](double (&o)[D], double c0, double c1, double c2, double c3, bool use3) {
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                double v = fma(c2, A2[j], c1 * A[j]);
+                if (use3) v = fma(c3, A3[j], v);
+                o[j] = v + ((j == r) ? c0 : 0.0);
+            }
+        };
+        if (low) {   // m = 6: F = B0 + A3 (c3 I + c4 A + c5 A2 + c6 A3)
+            tblock(X, c[3], c[4], c[5], c[6], true);
+            tblock(B, c[0], c[1], c[2], 0.0, false);
+            g_mm<D>(T, A3, X, gm);
+#pragma unroll
+            for (int j = 0; j < D; ++j) T[j] += B[j];
+        } else {     // m = 12: Horner in A3 over degree-2 blocks, top block degree 3
+            tblock(X, c[9], c[10], c[11], c[12], true);
+            tblock(B, c[6], c[7], c[8], 0.0, false);
+            g_mm<D>(T, A3, X, gm);
+#pragma unroll
+            for (int j = 0; j < D; ++j) T[j] += B[j];
+            tblock(B, c[3], c[4], c[5], 0.0, false);
+            g_mm<D>(X, A3, T, gm);
+#pragma unroll
+            for (int j = 0; j < D; ++j) X[j] += B[j];
+            tblock(B, c[0], c[1], c[2], 0.0, false);
+            g_mm<D>(T, A3, X, gm);
+#pragma unroll
+            for (int j = 0; j < D; ++j) T[j] += B[j];
+        }
+        // Q_tau = sum_k tau^k ... : Z = tau W, Z <- (A Z + Z A^T) / (k + 1), Q += Z
+        double Z[D], Qc[D];
+#pragma unroll
+        for (int j = 0; j < D; ++j) { Z[j] = Wr[j] * tau; Qc[j] = Z[j]; }
+        const int mq = low ? 7 : 12;
+        for (int kk = 1; kk < mq; ++kk) {
+            g_mm<D>(A3, A, Z, gm);
+            g_mmt<D>(X, Z, A, nullptr, gm);
+            const double ik = 1.0 / (kk + 1);
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                Z[j] = (A3[j] + X[j]) * ik;
+                Qc[j] += Z[j];
+            }
+        }
+        // doublings: Q <- Q + F Q F^T, F <- F F   (F in T)
+        for (int q = 0; q < s; ++q) {
+            g_mm<D>(B, T, Qc, gm);
+            g_mmt<D>(A2, B, T, Qc, gm);
+            g_mm<D>(A3, T, T, gm);
+#pragma unroll
+            for (int j = 0; j < D; ++j) { Qc[j] = A2[j]; T[j] = A3[j]; }
+        }
+        // column r of Q (lane j's element r) for the symmetrised output
+        double Qt[D];
+#pragma unroll
+        for (int cc = 0; cc < D; ++cc)
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                const double v = __shfl_sync(gm, Qc[cc], j, kGL);
+                if (cc == r) Qt[j] = v;
+            }
+        if (act) {
+            double* o = fq + k * FQW(D);
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                o[r * LD(D) + j] = T[j];
+                o[(D + r) * LD(D) + j] = 0.5 * (Qc[j] + Qt[j]);
+            }
+        }
+    }
+}
 template <int D, bool STREAM>
 __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_filter_fold_lpr(const WParams p) {
     static_assert(D <= kGL, "lane-per-row fold holds one row per lane of an 8-lane group");
