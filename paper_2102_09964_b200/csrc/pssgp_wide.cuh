@@ -885,6 +885,7 @@ struct K1LSmem {
         SF<D> q[kQ];
         SCombF<D> s;
         double U[kQ][D][LD(D)];
+        double fqs[kQ][2][FQW(D)];                 // STREAM: each quarter's (F_k, Q_k) staged one step ahead
     } w[kWWarps];
 };
 
@@ -1064,8 +1065,23 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_filter_fold_
     unsigned char mn_ = 0;
     if (qb < qe) { tn_ = __ldg(p.t + qb); mn_ = __ldg(p.mask + qb); yn_ = __ldg(p.y + qb); }
     const double hr = act ? M.H[r] : 0.0;
+    auto& fqs = W.fqs[q];
+    if (STREAM) {
+        if (qb < qe)
+            for (int i = r; i < FQW(D); i += kGL) cp_async8(&fqs[0][i], p.fq + qb * FQW(D) + i, 8);
+        cp_async_commit();
+    }
     for (int64_t j = 0; j < Kq; ++j) {
         const int64_t k = qb + j;
+        const int fb = static_cast<int>(j & 1);
+        if (STREAM) {
+            // slot fb holds (F_k, Q_k); slot fb^1 was last read in step j - 1, before this sync
+            cp_async_wait<0>();
+            __syncwarp();
+            if (k + 1 < qe)
+                for (int i = r; i < FQW(D); i += kGL) cp_async8(&fqs[fb ^ 1][i], p.fq + (k + 1) * FQW(D) + i, 8);
+            cp_async_commit();
+        }
         const bool valid = k < qe;
         const double tk = tn_;
         const bool obs = valid && mn_ != 0;
@@ -1083,7 +1099,7 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_filter_fold_
         const double* Fp;
         const double* Qp;
         if (kind == 0) {
-            if (STREAM) { Fp = p.fq + k * FQW(D); Qp = Fp + D * LD(D); }
+            if (STREAM) { Fp = &fqs[fb][0]; Qp = Fp + D * LD(D); }
             else { Fp = &M.F[0][0]; Qp = &M.Q[0][0]; }
         } else if (kind == 1) {
             Fp = &sh.I[0][0]; Qp = &sh.Z[0][0];
