@@ -433,7 +433,9 @@ def main():
              and fps.get(dom) else None)
     plan = model.plan(n_local, f32=args.config == "f32")
     launches = int(sum(v[1] for v in kern.values()))
-    traffic, traffic_src = ncu_traffic(dom, args.config == "f32")
+    # the committed captures of the logical kernels are of the d = 3 thread path: not evidence for
+    # the wide-path (d >= 4) rows, whose kernels carry the same logical names
+    traffic, traffic_src = (ncu_traffic(dom, args.config == "f32") if model.state_dim <= 3 else (None, None))
     # the binding roofline of the dominant kernel is the larger of its two floors:
     # algorithmic bytes / HBM peak and executed fp64 flops / fp64 peak
     hbm_frac = hbm_gbs / pk.get("hbm_gbs")
