@@ -31,48 +31,102 @@ sys.path.insert(0, ROOT)
 
 METRIC = "time-steps/s (filter+smoother+NLL, fp64) Matern-5/2 N=2^24"
 UNIT = "time-steps/s"
-# algorithmic bytes per time step moved by each kernel at d = 3 (DESIGN.md §6 "Roofline")
-# fp32-state path: t, y, mask in fp64 / u8, filtered state 9 floats (36 B), outputs fp64
-ALG_BYTES_F32 = {"k_filter_reduce": 17, "k_filter_apply": 17 + 36, "k_smoother_apply": 8 + 36 + 16}
-ALG_BYTES = {"k_filter_reduce": 17, "k_filter_apply": 17 + 72, "k_smoother_apply": 8 + 72 + 16,
-             "k_grad_fold": 17 + 72}
-# fallback fp64 flops per time step (DFMA = 2) if the committed profile has no SASS counts;
-# normally read from profiles/*/ncu_full_*_summary.csv (flops_per_step())
-FLOPS_PER_STEP = {"k_filter_reduce": 243.3, "k_filter_apply": 255.1, "k_smoother_apply": 327.4}
-# fp64 peak derived in DESIGN.md §6: 148 SM x 64 FMA/clk x 2 flop x 1.965 GHz
-FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
+# fp64 pipe peak derived from the unit counts and clock: 148 SM x 64 DFMA/clk x 2 flop
+# x 1.965 GHz; the roofline uses the DFMA throughput MEASURED live on this GPU (pssgp_measure_fp64_peak)
+FP64_PEAK_DERIVED_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
 THROTTLE_BAD = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+SLOTS = ("k_filter_reduce", "k_filter_scan", "k_filter_apply", "k_smoother_scan", "k_smoother_apply",
+         "k_nll_sum", "k_reduce_blocks", "k_grad_fold", "k_discretize")
 
 
-def _ncu_row(kernel: str, f32: bool = False):
-    """Row of `kernel` in the latest committed ncu summary (profiles/*/ncu_full_*_summary.csv,
-    written by tools/make_profile_summary.py; DRAM bytes in GB).  Captures of the fp32 build are
-    tagged *f32* and used only for the f32 configuration."""
+def state_size(d: int) -> int:
+    """S(d) = d + d(d+1)/2 reals per filtered-state record (x, P packed upper)."""
+    return d + d * (d + 1) // 2
+
+
+def path_alg_bytes(d: int, f32: bool = False) -> int:
+    """Algorithmic bytes per time step of the whole path: t, y, mask in (17), the
+    filtered state written and read once (2 x 8 S), t re-read (8), mean and var out (16)."""
+    return 41 + (8 if f32 else 16) * state_size(d)
+
+
+def alg_bytes(slot: str, d: int, wide_stream: bool = False, f32: bool = False) -> int:
+    """Algorithmic bytes per time step moved by the kernel in profile slot `slot`:
+    K1 reads t, y, mask; K3 reads them and writes the filtered state; K5 reads t and the filtered
+    state and writes mean, var; the gradient fold reads the inputs and the filtered state.  On the
+    wide path with per-step discretisation (irregular dt) each pass also reads the step's (F, Q)
+    record of 2 d (d+1) doubles, which k_discretize writes.  Scans / sums: O(chains), 0 per step."""
+    st = (4 if f32 else 8) * state_size(d)
+    fq = 16 * d * (d + 1) if wide_stream else 0
+    return {"k_filter_reduce": 17 + fq, "k_filter_apply": 17 + st + fq, "k_smoother_apply": 8 + st + 16 + fq,
+            "k_grad_fold": 17 + st, "k_discretize": 8 + 16 * d * (d + 1)}.get(slot, 0)
+
+
+# kernel families behind each profile slot (thread path d <= 3, wide path d >= 4)
+_FAMILY = {"k_filter_reduce": ("k_filter_reduce", "kw_filter_fold"), "k_filter_apply": ("k_filter_apply", "kw_filter_apply"),
+           "k_smoother_apply": ("k_smoother_apply", "kw_smoother_apply"), "k_grad_fold": ("k_grad_fold", "k_grad_fold"),
+           "k_discretize": ("k_discretize", "kw_discretize"), "k_filter_scan": ("", "kw_scan_filter"),
+           "k_smoother_scan": ("", "kw_scan_smoother")}
+
+
+def _ncu_row(slot: str, d: int, cfg_key: str, f32: bool = False):
+    """Row of the kernel behind `slot` at state dimension d in the newest committed ncu summary of
+    this configuration (profiles/*/ncu_full_<tag>_summary.csv from tools/make_profile_summary.py;
+    tags end in _<config key>, e.g. r2a_c3; untagged round-1 captures are the d = 3 metric
+    workload; fp32 captures are tagged f32).  DRAM bytes in GB."""
     import csv
     import glob
-    files = sorted(f for f in glob.glob(os.path.join(ROOT, "profiles", "*", "ncu_full_*_summary.csv"))
-                   if ("f32" in os.path.basename(f)) == f32)
+    fam = _FAMILY.get(slot)
+    if fam is None:
+        return None, None
+    fam = fam[0] if d <= 3 else fam[1]
+    if not fam:
+        return None, None
+
+    def tag_key(f):
+        tag = os.path.basename(f)[len("ncu_full_"):-len("_summary.csv")]
+        if "f32" in tag:
+            return "f32"
+        return tag.split("_", 1)[1] if "_" in tag else "metric"
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "ncu_full_*_summary.csv")))
+    want = "f32" if f32 else cfg_key
     for f in reversed(files):
+        if tag_key(f) != want:
+            continue
         for row in csv.DictReader(open(f)):
-            if kernel + "<" in row["Kernel Name"]:
-                return row, os.path.relpath(f, ROOT)
+            name = row["Kernel Name"]
+            if fam + "<" in name or fam + "_lpr<" in name:
+                targs = name[name.index("<") + 1:]
+                if targs.startswith(f"{d},") or targs.startswith(f"{d}>"):
+                    return row, os.path.relpath(f, ROOT)
     return None, None
 
 
-def ncu_traffic(kernel: str, f32: bool = False):
-    """dram read+write bytes per launch of `kernel` from one `ncu --set full` capture."""
-    row, src = _ncu_row(kernel, f32)
+def ncu_traffic(slot: str, d: int, cfg_key: str, f32: bool = False):
+    """dram read+write bytes per launch of the kernel behind `slot` from one `ncu --set full` capture."""
+    row, src = _ncu_row(slot, d, cfg_key, f32)
     if row is None:
         return None, None
     return (float(row["dram__bytes_read.sum"]) + float(row["dram__bytes_write.sum"])) * 1e9, src
 
 
-def flops_per_step(kernel: str):
+def flops_per_step(slot: str, d: int, cfg_key: str):
     """Executed fp64 flops per time step (DFMA = 2) from the SASS counts of the committed capture."""
-    row, _ = _ncu_row(kernel)
+    row, _ = _ncu_row(slot, d, cfg_key)
     if row is not None and row.get("fp64_flops_per_step"):
         return float(row["fp64_flops_per_step"])
-    return FLOPS_PER_STEP.get(kernel)
+    return None
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
 
 
 def parse():
@@ -92,6 +146,41 @@ def parse():
     ap.add_argument("--chain-len", type=int, default=0)
     ap.add_argument("--blocks-per-sm", type=int, default=0)
     return ap.parse_args()
+
+
+def config_key(args) -> str:
+    """Key of the committed ncu summaries of this workload (profiles/*/ncu_full_<tag>_<key>_summary.csv)."""
+    if args.config == "metric":
+        return "metric_uniform" if args.uniform else "metric"
+    return args.config + ("i" if args.irregular and args.config in ("c3", "c4") else "")
+
+
+def ensure_ranks(args) -> None:
+    """`--gpus N` means N ranks, one per GPU.  Under torchrun (WORLD_SIZE set) WORLD_SIZE must equal
+    N; started directly with N > 1 the script re-launches itself through torch.distributed.run with
+    N local ranks (NCCL), or exits with an error when fewer than N GPUs are visible.  It never
+    falls back to fewer GPUs than asked for."""
+    ws = os.environ.get("WORLD_SIZE")
+    if ws is not None:
+        if int(ws) != args.gpus:
+            sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}; launch one rank per GPU")
+        return
+    if args.gpus <= 1 or args.impl == "reference":
+        return
+    import socket
+    import torch
+    n = torch.cuda.device_count()
+    if n < args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} needs {args.gpus} GPUs, {n} visible; refusing to run "
+                 f"fewer ranks than asked for")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    print("bench.py: launching " + " ".join(cmd), file=sys.stderr, flush=True)
+    os.execv(sys.executable, cmd)
 
 
 # ------------------------------------------------------------------------------ clocks
@@ -188,7 +277,7 @@ def cpu_baseline(w, sample: int):
     return {"value": n / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
             "sample": f"first {n} steps of the same grid, sequential C oracle (KF+RTS+NLL, Van Loan per step), "
                       f"{dt:.2f} s on {ncpu} host cores (1 used)",
-            "all_cores": allc}
+            "cpu_model": cpu_model(), "host_cores": ncpu, "all_cores": allc}
 
 
 def make_workload(args):
@@ -231,7 +320,8 @@ def run_reference(args, rank: int):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": w.name, "N": w.N, "sample_steps": n},
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": f"first {n} steps of {w.name} per step"},
+                             "sample": f"first {n} steps of {w.name} per step", "cpu_model": cpu_model(),
+                             "host_cores": os.cpu_count()},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -239,6 +329,7 @@ def run_reference(args, rank: int):
 # ------------------------------------------------------------------------------ ours
 def main():
     args = parse()
+    ensure_ranks(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -253,9 +344,18 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
+    nccl_info = None
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
+        # communicator check: one all_reduce of ones over NCCL must equal the world size
+        one = torch.ones(1, device=dev)
+        dist.all_reduce(one)
+        nccl_info = {"backend": dist.get_backend(), "comm_nranks": int(one.item()),
+                     "world_size": dist.get_world_size(), "nccl_version": ".".join(map(str, torch.cuda.nccl.version()))}
+        if rank == 0:
+            print(f"bench.py: NCCL communicator of {nccl_info['comm_nranks']} ranks "
+                  f"(NCCL {nccl_info['nccl_version']})", file=sys.stderr, flush=True)
 
     w = make_workload(args)
     model = P.Model(w.components, w.noise_var, uniform_dt=w.uniform_dt, chain_len=args.chain_len,
@@ -419,52 +519,69 @@ def main():
             dist.destroy_process_group()
         return
 
-    # ---- roofline for the dominant kernel
+    # ---- roofline for the dominant kernel: algorithmic bytes / HBM peak or executed
+    # fp64 flops / fp64 peak, whichever floor is larger, from per-kernel CUDA-event times of the
+    # timed region (events recorded by the library on the launch stream)
     pk = peaks()
+    d = model.state_dim
+    f32 = args.config == "f32"
+    wide_stream = d > 3 and w.uniform_dt == 0.0
+    ckey = config_key(args)
+    fp64_peak = P.pssgp_measure_fp64_peak(model.h) if hasattr(P, "pssgp_measure_fp64_peak") else None
+    fp64_src = "measured in this run: DFMA throughput kernel, all SMs (pssgp_measure_fp64_peak)"
+    if not fp64_peak:
+        fp64_peak, fp64_src = FP64_PEAK_DERIVED_TFLOPS, "derived: 148 SM x 64 DFMA/clk x 2 x 1.965 GHz"
     kern = {k: v for k, v in prof.items() if v[1] > 0}
+    per_kernel = {}
+    for k, (kms, kl) in kern.items():
+        b = alg_bytes(k, d, wide_stream, f32) * n_local
+        fl = flops_per_step(k, d, ckey)
+        launch_ms = kms / kl
+        e = {"ms_per_step": kms / args.steps, "launches_per_step": kl / args.steps, "alg_bytes_per_step": alg_bytes(k, d, wide_stream, f32)}
+        if b:
+            e["hbm_frac"] = b / (launch_ms * 1e-3) / 1e9 / pk.get("hbm_gbs")
+        if fl and not f32:
+            e["fp64_flops_per_step"] = fl
+            e["fp64_frac"] = fl * n_local / (launch_ms * 1e-3) / 1e12 / fp64_peak
+        per_kernel[k] = e
     dom = max(kern, key=lambda k: kern[k][0])
     dom_ms, dom_launches = kern[dom]
     per_launch_ms = dom_ms / dom_launches
-    alg_b = (ALG_BYTES_F32 if args.config == "f32" else ALG_BYTES).get(dom, 0) * n_local
+    alg_b = alg_bytes(dom, d, wide_stream, f32) * n_local
     hbm_gbs = alg_b / (per_launch_ms * 1e-3) / 1e9
-    fps = {k: flops_per_step(k) for k in ("k_filter_reduce", "k_filter_apply", "k_smoother_apply", "k_grad_fold")}
-    flops = (fps.get(dom, 0.0) * n_local
-             if model.state_dim == 3 and not args.uniform and args.config in ("metric", "c2", "c5", "grad")
-             and fps.get(dom) else None)
-    plan = model.plan(n_local, f32=args.config == "f32")
+    fl = per_kernel[dom].get("fp64_flops_per_step")
     launches = int(sum(v[1] for v in kern.values()))
-    # the committed captures of the logical kernels are of the d = 3 thread path: not evidence for
-    # the wide-path (d >= 4) rows, whose kernels carry the same logical names
-    traffic, traffic_src = (ncu_traffic(dom, args.config == "f32") if model.state_dim <= 3 else (None, None))
-    # the binding roofline of the dominant kernel is the larger of its two floors:
-    # algorithmic bytes / HBM peak and executed fp64 flops / fp64 peak
+    traffic, traffic_src = ncu_traffic(dom, d, ckey, f32)
     hbm_frac = hbm_gbs / pk.get("hbm_gbs")
     alu = None
-    if flops:
-        achieved_tf = flops / (per_launch_ms * 1e-3) / 1e12
-        alu = {"achieved_tflops": achieved_tf, "peak_tflops": FP64_PEAK_TFLOPS,
-               "frac": achieved_tf / FP64_PEAK_TFLOPS, "flops_per_step": fps.get(dom),
-               "peak_source": "fp64 pipe: 148 SM x 64 FMA/clk x 2 x 1.965 GHz (DESIGN.md §6)"}
+    if fl:
+        achieved_tf = fl * n_local / (per_launch_ms * 1e-3) / 1e12
+        alu = {"achieved_tflops": achieved_tf, "peak_tflops": fp64_peak, "frac": achieved_tf / fp64_peak,
+               "flops_per_step": fl, "peak_source": fp64_src, "peak_derived_tflops": FP64_PEAK_DERIVED_TFLOPS}
     if alu and alu["frac"] > hbm_frac:
-        roof = {"bound": "alu", "kernel": dom, "achieved": alu["achieved_tflops"], "peak": FP64_PEAK_TFLOPS,
+        roof = {"bound": "alu", "kernel": dom, "achieved": alu["achieved_tflops"], "peak": fp64_peak,
                 "unit": "TFLOP/s", "frac": alu["frac"], "traffic": traffic}
     else:
         roof = {"bound": "hbm", "kernel": dom, "achieved": hbm_gbs, "peak": pk.get("hbm_gbs"), "unit": "GB/s",
                 "frac": hbm_frac, "traffic": traffic}
     roof["alu"] = alu
-    path_b = 41 + 8 * 9 if args.config == "f32" else 41 + 16 * 9
+    path_b = path_alg_bytes(d, f32)
+    fl_all = [per_kernel[k].get("fp64_flops_per_step") for k in kern if alg_bytes(k, d) or k == "k_grad_fold"]
+    plan = model.plan(n_local, f32=f32)
     roof.update({
         "traffic_source": traffic_src,
         "alg_bytes_per_launch": alg_b,
-        "hbm": {"achieved_gbs": hbm_gbs, "peak_gbs": pk.get("hbm_gbs"), "frac": hbm_gbs / pk.get("hbm_gbs"),
+        "hbm": {"achieved_gbs": hbm_gbs, "peak_gbs": pk.get("hbm_gbs"), "frac": hbm_frac,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if not pk.get("_fallback") else "fallback"},
         "avg_launch_ms": per_launch_ms,
         "share_of_step": dom_ms / ms_total,
+        "per_kernel": per_kernel,
         "per_kernel_ms_per_step": {k: v[0] / args.steps for k, v in kern.items()},
+        "state_dim": d,
         "path_alg_bytes_per_step": path_b,
         "path_hbm_frac": path_b * N / (ms_step * 1e-3) / 1e9 / pk.get("hbm_gbs"),
-        "path_fp64_frac": (sum(fps[k] for k in kern if fps.get(k)) * N / (ms_step * 1e-3) / 1e12 / FP64_PEAK_TFLOPS)
-        if flops else None})
+        "path_fp64_frac": (sum(fl_all) * N / (ms_step * 1e-3) / 1e12 / fp64_peak)
+        if fl_all and all(fl_all) and not f32 else None})
     cpu = None
     if not args.no_cpu_baseline:
         cpu = cpu_baseline(w, args.cpu_sample)
@@ -501,8 +618,8 @@ def main():
             "data": "synthetic",
             "config": {"workload": w.name, "N": N, "state_dim": model.state_dim, "chain_len": plan["chain_len"],
                        "ctas": plan["n_blocks"], "threads_per_cta": plan["threads"],
-                       "l2": "no flush: working set (1.8 GB) >> 126 MB L2",
-                       "parallelism": f"time-sharded x{world}" if world > 1 else "single GPU"},
+                       "l2": f"no flush: working set ({path_b * N / 1e9:.2f} GB per step) >> 126 MB L2",
+                       "parallelism": f"time-sharded x{world}" if world > 1 else "single GPU", "nccl": nccl_info},
             "clocks": clk, "e2e": e2e, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu, **extra}
     print(json.dumps(line), flush=True)
     if dist:

@@ -263,13 +263,19 @@ void pssgp_profile_enable(pssgp_model* m, int on);
 int pssgp_profile_read(pssgp_model* m, double* ms, int64_t* launches, int cap);
 const char* pssgp_profile_name(int slot);
 
+/* Measurement helper (the fp64 roofline denominator): DFMA throughput of the
+ * handle's device in TFLOP/s (FMA = 2 flop), best of three runs each of two probe kernels (8
+ * independent FMA chains per thread, 8 CTAs of 256 threads per SM; register or constant-bank
+ * addend).  Synchronous (default stream); ~10 ms.  *tflops: host double. */
+pssgp_status pssgp_measure_fp64_peak(pssgp_model* m, double* tflops);
+
 /* ---- Time-sharded path (multi-GPU, one process per GPU).
  * Rank g owns the contiguous chunk [k0, k0 + n) of a global grid of N_global
  * steps.  t points at the chunk's first element and t[-1] (if k0 > 0) and
  * t[n] (if k0 + n < N_global) must be readable (one-point halo each side);
  * y, mask point at the chunk's first element.  Aggregates are opaque byte
  * blobs of pssgp_aggregate_bytes(m, which) bytes (which = 0 filter, 1
- * smoother) in DEVICE memory; the caller all-gathers them (e.g. NCCL) into
+ * smoother + NLL partial) in DEVICE memory; the caller all-gathers them (e.g. NCCL) into
  * arrays ordered by rank.  The three calls must be made in order with the
  * same chunk arguments; the handle keeps the filtered state in between. */
 size_t pssgp_aggregate_bytes(const pssgp_model* m, int which);
@@ -279,18 +285,24 @@ pssgp_status pssgp_shard_filter_reduce(pssgp_model* m, int64_t k0, int64_t n, in
                                        void* filt_agg_out, void* stream);
 
 /* all_filt_aggs: world filter aggregates; the carry into this chunk is the
- * ordered product of ranks 0..rank-1.  Writes this chunk's smoother aggregate
- * and its NLL partial (device scalar). */
+ * ordered product of ranks 0..rank-1 (any grouping P:326).
+ * Writes this chunk's smoother blob (pssgp_aggregate_bytes(m, 1) bytes: the chunk's
+ * smoother aggregate followed by its NLL partial) and, if nll_partial != NULL, the
+ * partial alone (device scalar). */
 pssgp_status pssgp_shard_filter_apply(pssgp_model* m, int64_t k0, int64_t n, int64_t N_global,
                                       const double* t, const double* y, const uint8_t* mask,
                                       const void* all_filt_aggs, int rank, int world,
                                       void* smooth_agg_out, double* nll_partial, void* stream);
 
-/* all_smooth_aggs: world smoother aggregates; the carry into this chunk is the
- * ordered product of ranks rank+1..world-1.  Writes mean[n], var[n]. */
+/* all_smooth_aggs: world smoother blobs in rank order; the carry into this chunk is
+ * the ordered product of ranks rank+1..world-1.  Writes mean[n],
+ * var[n] and, if nll != NULL, the TOTAL NLL of the global grid into the device scalar
+ * *nll: the fixed-order sum over ranks 0..world-1 of the NLL partials carried in the
+ * blobs (deterministic; identical on every rank). */
 pssgp_status pssgp_shard_smoother_apply(pssgp_model* m, int64_t k0, int64_t n, int64_t N_global,
                                         const double* t, const void* all_smooth_aggs, int rank,
-                                        int world, double* mean, double* var, void* stream);
+                                        int world, double* mean, double* var, double* nll,
+                                        void* stream);
 
 #ifdef __cplusplus
 }

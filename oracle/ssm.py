@@ -8,7 +8,7 @@ library's C++ model builder.
     with spectral density q; Matern closed forms are exact.
   * Matern-nu: lambda = sqrt(2 nu)/ell, companion drift,
     q chosen so that H P_inf H^T = sigma^2 (checked against the closed-form
-    P_inf of SURVEY.md §8(c) by tests/test_oracle_ssm.py).
+    P_inf of SURVEY.md §8(c) by tests/test_oracle_pins.py::test_matern_pinf_closed_form).
   * RBF Taylor approximation (reading Z7):
     Taylor-expand 1/S(omega) to order n, take the left-half-plane spectral
     factor a(s) (numpy.roots), G = companion(a), L = e_n,

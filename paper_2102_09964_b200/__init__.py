@@ -26,7 +26,7 @@ __all__ = ["Model", "PssgpError", "build", "lib", "pssgp_create", "pssgp_destroy
            "pssgp_aggregate_bytes", "pssgp_shard_filter_reduce", "pssgp_shard_filter_apply",
            "pssgp_shard_smoother_apply", "pssgp_profile_enable", "pssgp_profile_read", "pssgp_profile_name",
            "pssgp_merge_grid", "pssgp_gather", "pssgp_predict", "pssgp_posterior_batched", "pssgp_nll_grad_batched",
-           "pssgp_posterior_f32", "pssgp_plan_f32"]
+           "pssgp_posterior_f32", "pssgp_plan_f32", "pssgp_measure_fp64_peak"]
 
 
 def _ptr(x) -> Optional[int]:
@@ -228,10 +228,17 @@ def pssgp_shard_filter_apply(h, k0, n, N_global, t_ptr, y_ptr, mask_ptr, all_ptr
                                              int(rank), int(world), sout_ptr, nll_ptr, _stream_ptr(stream)))
 
 
-def pssgp_shard_smoother_apply(h, k0, n, N_global, t_ptr, all_ptr, rank, world, mean_ptr, var_ptr,
+def pssgp_shard_smoother_apply(h, k0, n, N_global, t_ptr, all_ptr, rank, world, mean_ptr, var_ptr, nll_ptr=None,
                                stream=None) -> None:
     _raise(h, lib().pssgp_shard_smoother_apply(h, int(k0), int(n), int(N_global), t_ptr, all_ptr, int(rank),
-                                               int(world), mean_ptr, var_ptr, _stream_ptr(stream)))
+                                               int(world), mean_ptr, var_ptr, nll_ptr, _stream_ptr(stream)))
+
+
+def pssgp_measure_fp64_peak(h) -> float:
+    """DFMA throughput of the handle's device in TFLOP/s (the fp64 roofline denominator)."""
+    out = ctypes.c_double(0.0)
+    _raise(h, lib().pssgp_measure_fp64_peak(h, ctypes.byref(out)))
+    return out.value
 
 
 # ------------------------------------------------------------------------- convenience wrapper

@@ -24,18 +24,49 @@ STATUS_NAMES = {0: "OK", 1: "E_ARG", 2: "E_INPUT", 3: "E_NUMERIC", 4: "E_CUDA", 
 KINDS = {"matern12": 1, "matern32": 2, "matern52": 3, "rbf": 4, "periodic": 5, "quasiperiodic": 6}
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile csrc/*.cu into libpssgp.so for sm_100a with nvcc (in-tree)."""
-    srcs = [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC))]
+def wide_dims():
+    """State dimensions of the warp-per-chain path (csrc/pssgp_dims.h), one object each."""
+    import re
+    txt = open(os.path.join(CSRC, "pssgp_dims.h")).read()
+    line = next(ln for ln in txt.splitlines() if ln.startswith("#define PSSGP_WIDE_DIMS"))
+    return [int(x) for x in re.findall(r"X\((\d+)\)", line)]
+
+
+def build(force: bool = False, verbose: bool = False, jobs: int = 0) -> str:
+    """Compile libpssgp.so for sm_100a with nvcc, in-tree: pssgp_api.cu (C ABI, d <= 3 path),
+    pssgp_f32.cu, and pssgp_wide_inst.cu once per wide state dimension, in parallel, then link."""
+    from concurrent.futures import ThreadPoolExecutor
+    srcs = [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if not f.endswith(".o")]
     newest = max(os.path.getmtime(f) for f in srcs + [HEADER])
     if not force and os.path.exists(LIB_PATH) and os.path.getmtime(LIB_PATH) >= newest:
         return LIB_PATH
-    cmd = ["nvcc", *NVCC_FLAGS, "-o", LIB_PATH, os.path.join(CSRC, "pssgp_api.cu"), os.path.join(CSRC, "pssgp_f32.cu")]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    objdir = os.path.join(_HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
+    cflags = [f for f in NVCC_FLAGS if f != "-shared"] + ["-c"]
+    units = [(os.path.join(CSRC, "pssgp_api.cu"), [], "pssgp_api.o"),
+             (os.path.join(CSRC, "pssgp_f32.cu"), [], "pssgp_f32.o")]
+    units += [(os.path.join(CSRC, "pssgp_wide_inst.cu"), [f"-DPSSGP_WD={d}"], f"pssgp_wide_{d}.o")
+              for d in wide_dims()]
+
+    def compile_one(u):
+        src, defs, obj = u
+        cmd = ["nvcc", *cflags, *defs, "-o", os.path.join(objdir, obj), src]
+        return cmd, subprocess.run(cmd, capture_output=True, text=True)
+
+    with ThreadPoolExecutor(max_workers=jobs or os.cpu_count() or 4) as ex:
+        results = list(ex.map(compile_one, units))
+    for cmd, res in results:
+        if verbose or res.returncode != 0:
+            print(" ".join(cmd), res.stdout, res.stderr)
+        if res.returncode != 0:
+            raise RuntimeError("nvcc failed building libpssgp.so")
+    link = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
+            "-o", LIB_PATH, *[os.path.join(objdir, u[2]) for u in units]]
+    res = subprocess.run(link, capture_output=True, text=True)
     if verbose or res.returncode != 0:
         print(res.stdout, res.stderr)
     if res.returncode != 0:
-        raise RuntimeError("nvcc failed building libpssgp.so")
+        raise RuntimeError("nvcc link of libpssgp.so failed")
     return LIB_PATH
 
 
@@ -95,11 +126,12 @@ SIGNATURES = {
     "pssgp_profile_read": (ctypes.c_int, [_vp, _dp, ctypes.POINTER(_i64), ctypes.c_int]),
     "pssgp_profile_name": (ctypes.c_char_p, [ctypes.c_int]),
     "pssgp_aggregate_bytes": (ctypes.c_size_t, [_vp, ctypes.c_int]),
+    "pssgp_measure_fp64_peak": (ctypes.c_int, [_vp, _dp]),
     "pssgp_shard_filter_reduce": (ctypes.c_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp]),
     "pssgp_shard_filter_apply": (ctypes.c_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, ctypes.c_int,
                                                 ctypes.c_int, _vp, _vp, _vp]),
     "pssgp_shard_smoother_apply": (ctypes.c_int, [_vp, _i64, _i64, _i64, _vp, _vp, ctypes.c_int, ctypes.c_int,
-                                                  _vp, _vp, _vp]),
+                                                  _vp, _vp, _vp, _vp]),
 }
 
 

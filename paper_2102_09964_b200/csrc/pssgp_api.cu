@@ -11,130 +11,54 @@
 #include <string>
 #include <vector>
 
-#include "../../include/pssgp.h"
-#include "host_model.hpp"
+#include "pssgp_internal.hpp"
 #include "pssgp_kernels.cuh"
-#include "pssgp_wide.cuh"
 #include "pssgp_batch.cuh"
 #include "pssgp_grad.cuh"
 #include "pssgp_f32.h"
 
 using namespace pssgp;
+using namespace pssgp_internal;
 namespace ph = pssgp_host;
 
-namespace {
 
-constexpr int kMaxD = 3;              // thread-per-chain path: d = 1, 2, 3
-// warp-per-chain path (pssgp_wide.cuh), uniform-dt models: these d are compiled
-#ifdef PSSGP_NO_WIDE                  // experiment builds (tools/build_variant.sh): thread path only
-#define PSSGP_WIDE_DIMS(X)
-#else
-#define PSSGP_WIDE_DIMS(X) X(4) X(5) X(6) X(8) X(10) X(12) X(14) X(16) X(18) X(20)
-#endif
-constexpr int kSlots = 9;
+
+namespace {
 const char* kSlotNames[kSlots] = {"k_filter_reduce", "k_filter_scan", "k_filter_apply",
                                   "k_smoother_scan", "k_smoother_apply", "k_nll_sum", "k_reduce_blocks",
                                   "k_grad_fold", "k_discretize"};
-enum Slot { S_K1 = 0, S_K2, S_K3, S_K4, S_K5, S_K6, S_RED, S_GRAD, S_DISC };
-
 }  // namespace
 
-struct pssgp_model {
-    int d = 0;
-    ph::Ssm ssm;                 // balanced host model (long double)
-    bool closed = false;         // standalone Matern closed form
-    int mode = kTable;           // DiscMode of the kernels (kClosed / kTable / kPade)
-    double lam = 0.0, s2 = 0.0, r = 0.0;
-    double udt = 0.0;
-    std::vector<double> Fu, Qu;  // F(udt), Q(udt) row-major d x d
-    int device = 0;
-    int64_t forced_K = 0;
-    int blocks_per_sm = 0;
-    int sm_count = 0;
-    int occ = 0;
-    int occ32 = 0;               // fp32 build (pssgp_posterior_f32): resident CTAs / SM
-    // workspace
-    char* ws = nullptr;
-    size_t ws_bytes = 0;
-    unsigned long long* d_err = nullptr;  // separate small allocation
-    double* d_scalar = nullptr;           // scratch nll scalar
-    double* d_model = nullptr;            // wide path: F, Q, Pinf, H, r, udt (device copy)
-    int wocc = 0;                         // wide path: resident CTAs / SM
-    char* io = nullptr;                   // e2e device buffers
-    size_t io_bytes = 0;
-    char* mg = nullptr;                   // pssgp_predict merged-grid buffers
-    size_t mg_bytes = 0;
-    double* bt = nullptr;                 // batched: per-step NLL terms
-    size_t bt_bytes = 0;
-    double* gb = nullptr;                 // batched gradient: head / tail tangent pieces per chain
-    size_t gb_bytes = 0;
-    double* fq = nullptr;                 // wide path, kPade mode: per-step (F, Q)
-    size_t fq_bytes = 0;
-    // pipelined host API (pssgp_posterior_host_async): two slots, each with its own stream and
-    // device I/O buffers; inputs, computes (one stream, call order) and outputs on separate streams
-    char* aio[2] = {nullptr, nullptr};
-    size_t aio_bytes[2] = {0, 0};
-    cudaStream_t astream[2] = {nullptr, nullptr};   // per slot: host -> device copies
-    cudaStream_t aout[2] = {nullptr, nullptr};      // per slot: device -> host copies
-    cudaStream_t acs = nullptr;                      // computes, in call order
-    cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
-    bool arec[2] = {false, false};                   // the slot has a previous call
-    int aslot = 0;
-    cudaStream_t last_stream = nullptr;
-    int64_t err_index = -1;
-    std::string last_err;
-    // sharded plan state
-    int64_t sh_k0 = -1, sh_n = -1, sh_N = -1;
-    // profiling
-    bool prof = false;
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[kSlots];
-    std::vector<cudaEvent_t> ev_pool;
-};
+namespace pssgp_internal {
+pssgp_status ensure_device(pssgp_model* m) {
+    if (m->sm_count > 0) return PSSGP_OK;
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0) return fail(m, PSSGP_E_CUDA, "no CUDA device available");
+    int dev = m->device;
+    if (dev < 0) cudaGetDevice(&dev);
+    m->device = dev;
+    e = cudaDeviceGetAttribute(&m->sm_count, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return cuda_fail(m, e, "cudaDeviceGetAttribute");
+    // word 0: latched error; 1: K3 publication flag; 2: K3 tile ticket; then 8 scratch doubles
+    e = cudaMalloc(&m->d_err, 3 * sizeof(unsigned long long) + 8 * sizeof(double));
+    if (e != cudaSuccess) return fail(m, PSSGP_E_NOMEM, "cudaMalloc(error word)");
+    cudaMemset(m->d_err, 0xff, sizeof(unsigned long long));
+    cudaMemset(m->d_err + 1, 0, 2 * sizeof(unsigned long long));   // K3 publication flag, ticket
+    m->d_scalar = reinterpret_cast<double*>(m->d_err + 3);
+    return PSSGP_OK;
+}
+
+pssgp_status nll_sum(pssgp_model* m, const double* parts, int nb, double* out, cudaStream_t s, int stride) {
+    ProfScope ps(m, S_K6, s);
+    k_nll_sum<<<1, kThreads, 0, s>>>(parts, nb, out, stride);
+    LAUNCH_CHECK(m, "k_nll_sum");
+    return PSSGP_OK;
+}
+}  // namespace pssgp_internal
 
 namespace {
 
-pssgp_status fail(pssgp_model* m, pssgp_status st, const std::string& msg, int64_t idx = -1) {
-    if (m) {
-        m->last_err = msg;
-        m->err_index = idx;
-    }
-    return st;
-}
-
-pssgp_status cuda_fail(pssgp_model* m, cudaError_t e, const char* where) {
-    return fail(m, PSSGP_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
-}
-
-cudaEvent_t get_event(pssgp_model* m) {
-    if (!m->ev_pool.empty()) {
-        cudaEvent_t e = m->ev_pool.back();
-        m->ev_pool.pop_back();
-        return e;
-    }
-    cudaEvent_t e;
-    cudaEventCreate(&e);
-    return e;
-}
-
-struct ProfScope {
-    pssgp_model* m;
-    int slot;
-    cudaStream_t s;
-    cudaEvent_t a = nullptr;
-    ProfScope(pssgp_model* m_, int slot_, cudaStream_t s_) : m(m_), slot(slot_), s(s_) {
-        if (m->prof) {
-            a = get_event(m);
-            cudaEventRecord(a, s);
-        }
-    }
-    ~ProfScope() {
-        if (m->prof) {
-            cudaEvent_t b = get_event(m);
-            cudaEventRecord(b, s);
-            m->ev[slot].emplace_back(a, b);
-        }
-    }
-};
 
 template <int D>
 void fill_params(const pssgp_model* m, ModelParams<D>& p) {
@@ -160,24 +84,6 @@ void fill_params(const pssgp_model* m, ModelParams<D>& p) {
         for (int i = 0; i < D; ++i)
             for (int j = i; j < D; ++j) p.Qu[si(D, i, j)] = m->Qu[i * D + j];
     }
-}
-
-pssgp_status ensure_device(pssgp_model* m) {
-    if (m->sm_count > 0) return PSSGP_OK;
-    int ndev = 0;
-    cudaError_t e = cudaGetDeviceCount(&ndev);
-    if (e != cudaSuccess || ndev == 0) return fail(m, PSSGP_E_CUDA, "no CUDA device available");
-    int dev = m->device;
-    if (dev < 0) cudaGetDevice(&dev);
-    m->device = dev;
-    e = cudaDeviceGetAttribute(&m->sm_count, cudaDevAttrMultiProcessorCount, dev);
-    if (e != cudaSuccess) return cuda_fail(m, e, "cudaDeviceGetAttribute");
-    e = cudaMalloc(&m->d_err, 2 * sizeof(unsigned long long) + 8 * sizeof(double));
-    if (e != cudaSuccess) return fail(m, PSSGP_E_NOMEM, "cudaMalloc(error word)");
-    cudaMemset(m->d_err, 0xff, sizeof(unsigned long long));
-    cudaMemset(m->d_err + 1, 0, sizeof(unsigned long long));   // K3 publication flag
-    m->d_scalar = reinterpret_cast<double*>(m->d_err + 2);
-    return PSSGP_OK;
 }
 
 template <int D>
@@ -264,12 +170,6 @@ pssgp_status setup(pssgp_model* m, const Plan& pl, KParams<D>& p) {
         else KERN<D, kTable><<<grid, block, 0, s>>>(p);                          \
     } while (0)
 
-#define LAUNCH_CHECK(m, where)                                    \
-    do {                                                          \
-        cudaError_t e_ = cudaGetLastError();                      \
-        if (e_ != cudaSuccess) return cuda_fail((m), e_, where);  \
-    } while (0)
-
 template <int D>
 pssgp_status phase_filter_reduce(pssgp_model* m, KParams<D>& p, cudaStream_t s) {
     ProfScope ps(m, S_K1, s);
@@ -297,13 +197,6 @@ pssgp_status phase_smoother(pssgp_model* m, KParams<D>& p, cudaStream_t s) {
     ProfScope ps(m, S_K5, s);
     LAUNCH_MODE(m, k_smoother_apply, p.nb, kThreads, s, p);
     LAUNCH_CHECK(m, "k_smoother_apply");
-    return PSSGP_OK;
-}
-
-pssgp_status nll_sum(pssgp_model* m, const double* parts, int nb, double* out, cudaStream_t s) {
-    ProfScope ps(m, S_K6, s);
-    k_nll_sum<<<1, kThreads, 0, s>>>(parts, nb, out);
-    LAUNCH_CHECK(m, "k_nll_sum");
     return PSSGP_OK;
 }
 
@@ -377,7 +270,7 @@ pssgp_status run_grad(pssgp_model* m, int64_t N, const double* t, const double* 
     }
     {
         ProfScope ps(m, S_RED, s);
-        k_reduce_blocks<D, TAgg3<D>><<<1, kCarryThreads, 0, s>>>(blocks, p.nb, out);
+        k_reduce_blocks<D, TAgg3<D>><<<1, kCarryThreads, 0, s>>>(blocks, p.nb, out, nullptr, 0);
         LAUNCH_CHECK(m, "k_reduce_blocks(grad)");
     }
     cudaError_t e = cudaMemcpyAsync(grad, out + offsetof(TAgg3<D>, a) / sizeof(double), 3 * sizeof(double),
@@ -409,424 +302,6 @@ pssgp_status debug_disc(const pssgp_model* m, double dt, double* F, double* Q) {
 }  // namespace
 
 
-// ========================================================================== wide path (d >= 4)
-namespace {
-
-bool wide_supported(int d) {
-    switch (d) {
-#define X(DD) case DD: return true;
-        PSSGP_WIDE_DIMS(X)
-#undef X
-        default: return false;
-    }
-}
-
-template <int D>
-void wide_set_smem_attrs() {
-    using namespace pssgp::wide;
-    static bool done = false;
-    if (done) return;
-    cudaFuncSetAttribute(kw_filter_fold<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K1Smem<D>));
-    if constexpr (D <= kGL) {
-        cudaFuncSetAttribute(kw_filter_fold_lpr<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K1LSmem<D>));
-        cudaFuncSetAttribute(kw_filter_fold_lpr<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K1LSmem<D>));
-        cudaFuncSetAttribute(kw_filter_apply_lpr<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K3LSmem<D>));
-        cudaFuncSetAttribute(kw_filter_apply_lpr<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K3LSmem<D>));
-        cudaFuncSetAttribute(kw_smoother_apply_lpr<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K5LSmem<D>));
-        cudaFuncSetAttribute(kw_smoother_apply_lpr<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K5LSmem<D>));
-    }
-    cudaFuncSetAttribute(kw_filter_apply<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K3Smem<D>));
-    cudaFuncSetAttribute(kw_smoother_apply<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K5Smem<D>));
-    cudaFuncSetAttribute(kw_scan_filter<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(ScanSmemF<D>));
-    cudaFuncSetAttribute(kw_scan_smoother<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(ScanSmemS<D>));
-    cudaFuncSetAttribute(kw_discretize<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(KDSmem<D>));
-    done = true;
-}
-
-// lane-per-row kernels of the wide path for D <= 8 (bit 0: fold, bit 1: RTS rescan, bit 2: both
-// rescans also with per-step (F, Q) staged in shared memory, bit 3: one-wave plan for them on the
-// table path, bit 4: Kalman rescan, bit 5: the one-wave plan also on the per-step (F, Q) path, bit 6:
-// lane-per-row discretisation); env PSSGP_WIDE_LPR overrides the default 127 for A/B runs (0 = the
-// shared-memory kernels)
-int wide_lpr_mask() {
-    static const int v = [] { const char* e = getenv("PSSGP_WIDE_LPR"); return e && *e ? atoi(e) : 127; }();
-    return v;
-}
-
-struct WPlan {
-    int64_t K = 0;
-    int nch = 0, nb = 0;
-};
-
-template <int D>
-WPlan make_wplan(pssgp_model* m, int64_t n) {
-    using namespace pssgp::wide;
-    wide_set_smem_attrs<D>();
-    if (m->wocc == 0) {
-        int a = 0, b = 0, c = 0;
-        // (the lane-per-row fold of D <= 8 is not part of the plan's occupancy: it is register-
-        // capped at PSSGP_WLPR_MINB CTAs/SM and simply runs the same grid)
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, kw_filter_fold<D>, 32 * kWWarps, sizeof(K1Smem<D>));
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kw_filter_apply<D>, 32 * kWWarps, sizeof(K3Smem<D>));
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, kw_smoother_apply<D>, 32 * kWWarps, sizeof(K5Smem<D>));
-        m->wocc = std::max(1, std::min(a, std::min(b, c)));
-        if constexpr (D <= kGL) {
-            int l1 = 0, l5 = 0, l3 = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l1, kw_filter_fold_lpr<D, false>, 32 * kWWarps, sizeof(K1LSmem<D>));
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l3, kw_filter_apply_lpr<D, false>, 32 * kWWarps, sizeof(K3LSmem<D>));
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l5, kw_smoother_apply_lpr<D, false>, 32 * kWWarps, sizeof(K5LSmem<D>));
-            if (wide_lpr_mask() & 16) l5 = std::min(l5, l3);
-            if (getenv("PSSGP_WIDE_DEBUG"))
-                fprintf(stderr, "wide plan D=%d occupancy: fold %d, apply %d, smoother %d, lpr fold %d, lpr smoother %d\n",
-                        D, a, b, c, l1, l5);
-            // bit 3: on the table (uniform-dt) path, where both lane-per-row kernels run, size the
-            // plan so they run in one wave (C3: 13.8 -> 11.7 ms; on the per-step (F, Q) path the
-            // fewer, longer chains slow the shared-memory rescans: 26.2 -> 28.3 ms, so not there)
-            if ((wide_lpr_mask() & 8) && (m->mode != kPade || (wide_lpr_mask() & 32))) m->wocc = std::max(1, std::min(m->wocc, std::min(l1, l5)));
-        }
-    }
-    const int64_t target = static_cast<int64_t>(m->sm_count) * m->wocc * kWWarps;
-    WPlan pl;
-    pl.K = m->forced_K > 0 ? m->forced_K : std::max<int64_t>(16, (n + target - 1) / target);
-    pl.nch = static_cast<int>(std::max<int64_t>(1, (n + pl.K - 1) / pl.K));
-    pl.nb = (pl.nch + kWWarps - 1) / kWWarps;
-    return pl;
-}
-
-template <int D>
-pssgp_status wide_setup(pssgp_model* m, const WPlan& pl, pssgp::wide::WParams& p) {
-    using namespace pssgp::wide;
-    const size_t nch = static_cast<size_t>(pl.nch);
-    const size_t need = (2 * nch * FNW(D) + nch * pl.K * CNW(D) + 2 * nch * SNW(D) + nch + 64) * sizeof(double);
-    if (need > m->ws_bytes) {
-        if (m->ws) cudaFree(m->ws);
-        m->ws = nullptr;
-        m->ws_bytes = 0;
-        if (cudaMalloc(&m->ws, need) != cudaSuccess) {
-            cudaGetLastError();
-            return fail(m, PSSGP_E_NOMEM, "cudaMalloc(workspace) failed");
-        }
-        m->ws_bytes = need;
-    }
-    if (!m->d_model) {
-        std::vector<double> h(MODW(D), 0.0);
-        for (int i = 0; i < D * D; ++i) {
-            h[i] = m->udt > 0.0 ? m->Fu[i] : 0.0;
-            h[D * D + i] = m->udt > 0.0 ? m->Qu[i] : 0.0;
-            h[2 * D * D + i] = static_cast<double>(m->ssm.Pinf[i]);
-        }
-        for (int i = 0; i < D; ++i) h[3 * D * D + i] = static_cast<double>(m->ssm.H[i]);
-        h[3 * D * D + D] = m->r;
-        h[3 * D * D + D + 1] = m->udt > 0.0 ? m->udt : -1.0;
-        for (int i = 0; i < D * D; ++i) h[3 * D * D + D + 2 + i] = static_cast<double>(m->ssm.G[i]);
-        for (int i = 0; i < D * D; ++i) h[4 * D * D + D + 2 + i] = static_cast<double>(m->ssm.W[i]);
-        if (cudaMalloc(&m->d_model, h.size() * sizeof(double)) != cudaSuccess) {
-            cudaGetLastError();
-            return fail(m, PSSGP_E_NOMEM, "cudaMalloc(model)");
-        }
-        cudaMemcpy(m->d_model, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice);
-    }
-    std::memset(&p, 0, sizeof(p));
-    double* w = reinterpret_cast<double*>(m->ws);
-    p.fagg = w; w += nch * FNW(D);
-    p.fbuf = w; w += nch * FNW(D);
-    p.xp = w; w += nch * pl.K * CNW(D);
-    p.sagg = w; w += nch * SNW(D);
-    p.sbuf = w; w += nch * SNW(D);
-    p.nll_chain = w;
-    p.K = pl.K;
-    p.nch = pl.nch;
-    p.model = m->d_model;
-    p.err = m->d_err;
-    p.rank = 0;
-    p.world = 1;
-    p.store_state = 1;
-    return PSSGP_OK;
-}
-
-// kPade mode (no closed form, no uniform step): per-step (F, Q) for local steps
-// [0, n] (step n = the successor read by the smoother when it exists globally)
-template <int D>
-pssgp_status wide_prepare(pssgp_model* m, pssgp::wide::WParams& p, cudaStream_t s) {
-    using namespace pssgp::wide;
-    p.fq = nullptr;
-    if (m->mode != kPade || p.n == 0) return PSSGP_OK;
-    const int64_t nfq = p.n + ((p.k0 + p.n < p.nglob) ? 1 : 0);
-    const size_t need = static_cast<size_t>(nfq) * FQW(D) * sizeof(double);
-    if (need > m->fq_bytes) {
-        if (m->fq) cudaFree(m->fq);
-        m->fq = nullptr;
-        m->fq_bytes = 0;
-        if (cudaMalloc(&m->fq, need) != cudaSuccess) {
-            cudaGetLastError();
-            return fail(m, PSSGP_E_NOMEM, "cudaMalloc(per-step F, Q) failed");
-        }
-        m->fq_bytes = need;
-    }
-    if constexpr (D <= kGL) {
-        if (wide_lpr_mask() & 64) {   // lane-per-row discretisation: one step per 8-lane group
-            int occ = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kw_discretize_lpr<D>, 32 * kWWarps, 0);
-            const int64_t want = (nfq * kGL + 32 * kWWarps - 1) / (32 * kWWarps);
-            const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(m->sm_count) * std::max(1, occ))));
-            {
-                ProfScope ps(m, S_DISC, s);
-                kw_discretize_lpr<D><<<grid, 32 * kWWarps, 0, s>>>(p.t, nfq, p.k0, m->d_model, m->fq);
-                LAUNCH_CHECK(m, "kw_discretize_lpr");
-            }
-            p.fq = m->fq;
-            return PSSGP_OK;
-        }
-    }
-    int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kw_discretize<D>, 32 * kWWarps, sizeof(KDSmem<D>));
-    const int64_t want = (nfq + kWWarps - 1) / kWWarps;
-    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(m->sm_count) * std::max(1, occ))));
-    {
-        ProfScope ps(m, S_DISC, s);
-        kw_discretize<D><<<grid, 32 * kWWarps, sizeof(KDSmem<D>), s>>>(p.t, nfq, p.k0, m->d_model, m->fq, p.err);
-        LAUNCH_CHECK(m, "kw_discretize");
-    }
-    p.fq = m->fq;
-    return PSSGP_OK;
-}
-
-// One step of kw_discretize on the device (pssgp_debug_discretize for kPade wide models).
-template <int D>
-pssgp_status wide_debug_discretize(pssgp_model* m, double dt, double* F, double* Q) {
-    using namespace pssgp::wide;
-    pssgp_status st = ensure_device(m);
-    if (st) return st;
-    WParams p;
-    if ((st = wide_setup<D>(m, make_wplan<D>(m, 2), p))) return st;
-    double* tbuf = nullptr;
-    if (cudaMalloc(&tbuf, 2 * sizeof(double) + 2 * FQW(D) * sizeof(double)) != cudaSuccess) {
-        cudaGetLastError();
-        return fail(m, PSSGP_E_NOMEM, "cudaMalloc(debug discretize)");
-    }
-    double* fq = tbuf + 2;
-    const double th[2] = {0.0, dt};
-    cudaMemcpy(tbuf, th, sizeof(th), cudaMemcpyHostToDevice);
-    cudaFuncSetAttribute(kw_discretize<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(KDSmem<D>));
-    kw_discretize<D><<<1, 32 * kWWarps, sizeof(KDSmem<D>)>>>(tbuf, 2, 0, m->d_model, fq, m->d_err);
-    std::vector<double> h(FQW(D));
-    cudaError_t e = cudaMemcpy(h.data(), fq + FQW(D), FQW(D) * sizeof(double), cudaMemcpyDeviceToHost);
-    cudaFree(tbuf);
-    if (e != cudaSuccess) return cuda_fail(m, e, "debug discretize");
-    for (int i = 0; i < D; ++i)
-        for (int j = 0; j < D; ++j) {
-            F[i * D + j] = h[i * LD(D) + j];
-            Q[i * D + j] = h[(D + i) * LD(D) + j];
-        }
-    return PSSGP_OK;
-}
-
-// Kogge-Stone levels with ping-pong buffers; returns the buffer holding the inclusive scan
-template <int D>
-double* wide_scan_f(pssgp_model* m, pssgp::wide::WParams& p, cudaStream_t s, pssgp_status& st) {
-    using namespace pssgp::wide;
-    ProfScope ps(m, S_K2, s);
-    double* in = p.fagg;
-    double* out = p.fbuf;
-    for (int off = 1; off < p.nch; off <<= 1) {
-        kw_scan_filter<D><<<p.nch, 32, sizeof(ScanSmemF<D>), s>>>(in, out, p.nch, off, p.err);
-        std::swap(in, out);
-    }
-    cudaError_t e = cudaGetLastError();
-    st = (e == cudaSuccess) ? PSSGP_OK : cuda_fail(m, e, "kw_scan_filter");
-    return in;
-}
-
-template <int D>
-double* wide_scan_s(pssgp_model* m, pssgp::wide::WParams& p, cudaStream_t s, pssgp_status& st) {
-    using namespace pssgp::wide;
-    ProfScope ps(m, S_K4, s);
-    double* in = p.sagg;
-    double* out = p.sbuf;
-    for (int off = 1; off < p.nch; off <<= 1) {
-        kw_scan_smoother<D><<<p.nch, 32, sizeof(ScanSmemS<D>), s>>>(in, out, p.nch, off);
-        std::swap(in, out);
-    }
-    cudaError_t e = cudaGetLastError();
-    st = (e == cudaSuccess) ? PSSGP_OK : cuda_fail(m, e, "kw_scan_smoother");
-    return in;
-}
-
-template <int D>
-pssgp_status wide_fold(pssgp_model* m, pssgp::wide::WParams& p, int nb, cudaStream_t s) {
-    using namespace pssgp::wide;
-    ProfScope ps(m, S_K1, s);
-    if constexpr (D <= kGL) {
-        // lane-per-row fold (D <= 8); PSSGP_WIDE_LPR=0 selects the shared-memory fold (A/B runs)
-        if (wide_lpr_mask() & 1) {
-            if (p.fq) kw_filter_fold_lpr<D, true><<<nb, 32 * kWWarps, sizeof(K1LSmem<D>), s>>>(p);
-            else kw_filter_fold_lpr<D, false><<<nb, 32 * kWWarps, sizeof(K1LSmem<D>), s>>>(p);
-            LAUNCH_CHECK(m, "kw_filter_fold_lpr");
-            return PSSGP_OK;
-        }
-    }
-    kw_filter_fold<D><<<nb, 32 * kWWarps, sizeof(K1Smem<D>), s>>>(p);
-    LAUNCH_CHECK(m, "kw_filter_fold");
-    return PSSGP_OK;
-}
-
-template <int D>
-pssgp_status wide_fapply(pssgp_model* m, pssgp::wide::WParams& p, int nb, cudaStream_t s) {
-    using namespace pssgp::wide;
-    ProfScope ps(m, S_K3, s);
-    if constexpr (D <= kGL) {
-        // bit 4: lane-per-row Kalman rescan (uniform dt unless bit 2)
-        if ((wide_lpr_mask() & 16) && (!p.fq || (wide_lpr_mask() & 4))) {
-            if (p.fq) kw_filter_apply_lpr<D, true><<<nb, 32 * kWWarps, sizeof(K3LSmem<D>), s>>>(p);
-            else kw_filter_apply_lpr<D, false><<<nb, 32 * kWWarps, sizeof(K3LSmem<D>), s>>>(p);
-            LAUNCH_CHECK(m, "kw_filter_apply_lpr");
-            return PSSGP_OK;
-        }
-    }
-    kw_filter_apply<D><<<nb, 32 * kWWarps, sizeof(K3Smem<D>), s>>>(p);
-    LAUNCH_CHECK(m, "kw_filter_apply");
-    return PSSGP_OK;
-}
-
-template <int D>
-pssgp_status wide_sapply(pssgp_model* m, pssgp::wide::WParams& p, int nb, cudaStream_t s) {
-    using namespace pssgp::wide;
-    ProfScope ps(m, S_K5, s);
-    if constexpr (D <= kGL) {
-        // uniform dt only by default: with per-step (F, Q) read from global memory it measured
-        // slower than the shared-memory kernel (C3 irregular K5w 8.4 -> 11.3 ms); bit 2 forces it
-        if ((wide_lpr_mask() & 2) && (!p.fq || (wide_lpr_mask() & 4))) {
-            if (p.fq) kw_smoother_apply_lpr<D, true><<<nb, 32 * kWWarps, sizeof(K5LSmem<D>), s>>>(p);
-            else kw_smoother_apply_lpr<D, false><<<nb, 32 * kWWarps, sizeof(K5LSmem<D>), s>>>(p);
-            LAUNCH_CHECK(m, "kw_smoother_apply_lpr");
-            return PSSGP_OK;
-        }
-    }
-    kw_smoother_apply<D><<<nb, 32 * kWWarps, sizeof(K5Smem<D>), s>>>(p);
-    LAUNCH_CHECK(m, "kw_smoother_apply");
-    return PSSGP_OK;
-}
-
-template <int D>
-pssgp_status wide_posterior(pssgp_model* m, int64_t N, const double* t, const double* y, const uint8_t* mask,
-                            double* mean, double* var, double* nll, cudaStream_t s, bool smooth) {
-    if (N == 0) {
-        if (nll && cudaMemsetAsync(nll, 0, sizeof(double), s) != cudaSuccess) return fail(m, PSSGP_E_CUDA, "memset");
-        return PSSGP_OK;
-    }
-    const WPlan pl = make_wplan<D>(m, N);
-    pssgp::wide::WParams p;
-    pssgp_status st = wide_setup<D>(m, pl, p);
-    if (st) return st;
-    p.t = t; p.y = y; p.mask = mask;
-    p.n = N; p.k0 = 0; p.nglob = N;
-    p.mean = mean; p.var = var;
-    p.store_state = smooth ? 1 : 0;
-    if ((st = wide_prepare<D>(m, p, s))) return st;
-    if ((st = wide_fold<D>(m, p, pl.nb, s))) return st;
-    p.fagg = wide_scan_f<D>(m, p, s, st);
-    if (st) return st;
-    if ((st = wide_fapply<D>(m, p, pl.nb, s))) return st;
-    if (smooth) {
-        p.sagg = wide_scan_s<D>(m, p, s, st);
-        if (st) return st;
-        p.nll_out = nullptr;   // summed by k_nll_sum as on the NLL-only path: bit-identical NLL
-        if ((st = wide_sapply<D>(m, p, pl.nb, s))) return st;
-    }
-    if (nll) return nll_sum(m, p.nll_chain, p.nch, nll, s);
-    return PSSGP_OK;
-}
-
-pssgp_status wide_posterior_dispatch(pssgp_model* m, int64_t N, const double* t, const double* y,
-                                     const uint8_t* mask, double* mean, double* var, double* nll, cudaStream_t s,
-                                     bool smooth) {
-    switch (m->d) {
-#define X(DD) case DD: return wide_posterior<DD>(m, N, t, y, mask, mean, var, nll, s, smooth);
-        PSSGP_WIDE_DIMS(X)
-#undef X
-        default: return fail(m, PSSGP_E_UNSUPPORTED, "state dimension not compiled");
-    }
-}
-
-// ---- sharded wide phases
-template <int D>
-pssgp_status wide_shard_reduce(pssgp_model* m, int64_t k0, int64_t n, int64_t Ng, const double* t, const double* y,
-                               const uint8_t* mask, void* out, cudaStream_t s) {
-    const WPlan pl = make_wplan<D>(m, n);
-    pssgp::wide::WParams p;
-    pssgp_status st = wide_setup<D>(m, pl, p);
-    if (st) return st;
-    p.t = t; p.y = y; p.mask = mask; p.n = n; p.k0 = k0; p.nglob = Ng;
-    if ((st = wide_prepare<D>(m, p, s))) return st;
-    if ((st = wide_fold<D>(m, p, pl.nb, s))) return st;
-    double* inc = wide_scan_f<D>(m, p, s, st);
-    if (st) return st;
-    const cudaError_t e = cudaMemcpyAsync(out, inc + static_cast<int64_t>(pl.nch - 1) * pssgp::wide::FNW(D),
-                                          pssgp::wide::FNW(D) * sizeof(double), cudaMemcpyDeviceToDevice, s);
-    if (e != cudaSuccess) return cuda_fail(m, e, "cudaMemcpyAsync(chunk aggregate)");
-    return PSSGP_OK;
-}
-
-int ks_levels(int nch) {
-    int l = 0;
-    for (int off = 1; off < nch; off <<= 1) ++l;
-    return l;
-}
-
-template <int D>
-pssgp_status wide_shard_fapply(pssgp_model* m, int64_t k0, int64_t n, int64_t Ng, const double* t, const double* y,
-                               const uint8_t* mask, const void* all, int rank, int world, void* sout, double* nllp,
-                               cudaStream_t s) {
-    const WPlan pl = make_wplan<D>(m, n);
-    pssgp::wide::WParams p;
-    pssgp_status st = wide_setup<D>(m, pl, p);
-    if (st) return st;
-    p.t = t; p.y = y; p.mask = mask; p.n = n; p.k0 = k0; p.nglob = Ng;
-    p.in_filt = static_cast<const double*>(all);
-    p.rank = rank; p.world = world;
-    if (ks_levels(pl.nch) & 1) p.fagg = p.fbuf;          // where the reduce phase left the scan
-    if ((st = wide_prepare<D>(m, p, s))) return st;
-    if ((st = wide_fapply<D>(m, p, pl.nb, s))) return st;
-    if (nllp && (st = nll_sum(m, p.nll_chain, p.nch, nllp, s))) return st;
-    double* inc = wide_scan_s<D>(m, p, s, st);
-    if (st) return st;
-    const cudaError_t e = cudaMemcpyAsync(sout, inc, pssgp::wide::SNW(D) * sizeof(double), cudaMemcpyDeviceToDevice, s);
-    if (e != cudaSuccess) return cuda_fail(m, e, "cudaMemcpyAsync(chunk smoother aggregate)");
-    return PSSGP_OK;
-}
-
-template <int D>
-pssgp_status wide_shard_sapply(pssgp_model* m, int64_t k0, int64_t n, int64_t Ng, const double* t, const void* all,
-                               int rank, int world, double* mean, double* var, cudaStream_t s) {
-    const WPlan pl = make_wplan<D>(m, n);
-    pssgp::wide::WParams p;
-    pssgp_status st = wide_setup<D>(m, pl, p);
-    if (st) return st;
-    p.t = t; p.n = n; p.k0 = k0; p.nglob = Ng;
-    p.in_smooth = static_cast<const double*>(all);
-    p.rank = rank; p.world = world;
-    p.mean = mean; p.var = var;
-    if (ks_levels(pl.nch) & 1) p.sagg = p.sbuf;
-    if ((st = wide_prepare<D>(m, p, s))) return st;
-    return wide_sapply<D>(m, p, pl.nb, s);
-}
-
-#define DISPATCH_WIDE(m, FN, ...)                                                  \
-    switch ((m)->d) {                                                              \
-        case 4: return FN<4>(__VA_ARGS__);                                         \
-        case 5: return FN<5>(__VA_ARGS__);                                         \
-        case 6: return FN<6>(__VA_ARGS__);                                         \
-        case 8: return FN<8>(__VA_ARGS__);                                         \
-        case 10: return FN<10>(__VA_ARGS__);                                       \
-        case 12: return FN<12>(__VA_ARGS__);                                       \
-        case 14: return FN<14>(__VA_ARGS__);                                       \
-        case 16: return FN<16>(__VA_ARGS__);                                       \
-        case 18: return FN<18>(__VA_ARGS__);                                       \
-        case 20: return FN<20>(__VA_ARGS__);                                       \
-        default: return fail((m), PSSGP_E_UNSUPPORTED, "state dimension not compiled"); \
-    }
-
-}  // namespace
 
 // ========================================================================== C ABI
 extern "C" {
@@ -888,7 +363,7 @@ pssgp_status pssgp_create(const pssgp_component* comps, int n_comps, double nois
     }
     m->ssm = parts.size() == 1 ? parts[0] : ph::block_sum(parts);
     m->d = m->ssm.d;
-    if (m->d > kMaxD && !wide_supported(m->d)) {
+    if (m->d > kMaxD && !wide_ops_for(m->d)) {
         delete m;
         return PSSGP_E_UNSUPPORTED;
     }
@@ -940,7 +415,7 @@ pssgp_status pssgp_posterior(pssgp_model* m, int64_t N, const double* t, const d
     auto s = static_cast<cudaStream_t>(stream);
     m->last_stream = s;
     const bool smooth = (mean != nullptr) || (var != nullptr);
-    if (m->d > kMaxD) return wide_posterior_dispatch(m, N, t, y, mask, mean, var, nll, s, smooth);
+    if (m->d > kMaxD) return wide_ops_for(m->d)->posterior(m, N, t, y, mask, mean, var, nll, s, smooth);
     DISPATCH_D(m, run_posterior<D_>(m, N, t, y, mask, mean, var, nll, s, smooth));
 }
 
@@ -952,7 +427,7 @@ pssgp_status pssgp_nll(pssgp_model* m, int64_t N, const double* t, const double*
     if ((st = ensure_device(m))) return st;
     auto s = static_cast<cudaStream_t>(stream);
     m->last_stream = s;
-    if (m->d > kMaxD) return wide_posterior_dispatch(m, N, t, y, mask, nullptr, nullptr, nll, s, false);
+    if (m->d > kMaxD) return wide_ops_for(m->d)->posterior(m, N, t, y, mask, nullptr, nullptr, nll, s, false);
     DISPATCH_D(m, run_posterior<D_>(m, N, t, y, mask, nullptr, nullptr, nll, s, false));
 }
 
@@ -1281,6 +756,69 @@ pssgp_status pssgp_nll_grad_batched(pssgp_model* m, int nseg, const int64_t* off
     return PSSGP_OK;
 }
 
+}  // extern "C"
+
+namespace {
+// DFMA throughput probe (pssgp_measure_fp64_peak): 8 independent FMA chains per thread hide the
+// pipe latency; MODE 0 three register operands, MODE 1 a constant-bank addend (the form the
+// closed-form discretisation uses).
+__constant__ double c_fp64_probe[8] = {1.0000001, 0.9999999, 1.0000002, 0.9999998,
+                                       1.0000003, 0.9999997, 1.0000004, 0.9999996};
+template <int MODE>
+__global__ void __launch_bounds__(256) k_fp64_probe(double* out, int iters, double s) {
+    double acc[8], x[8], y[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { acc[i] = threadIdx.x * 1e-3 + i; x[i] = s + i * 1e-7; y[i] = 1e-9 * i - s * 1e-3; }
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = fma(acc[i], x[i], MODE == 0 ? y[i] : c_fp64_probe[i]);
+    }
+    double r = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r += acc[i];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = r;
+}
+}  // namespace
+
+extern "C" {
+
+pssgp_status pssgp_measure_fp64_peak(pssgp_model* m, double* tflops) {
+    if (!m || !tflops) return PSSGP_E_ARG;
+    pssgp_status st = ensure_device(m);
+    if (st) return st;
+    const int blocks = m->sm_count * 8, threads = 256, iters = 4096;
+    double* out = nullptr;
+    if (cudaMalloc(&out, sizeof(double) * blocks * threads) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(m, PSSGP_E_NOMEM, "cudaMalloc(fp64 probe)");
+    }
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    double best = 0.0;
+    for (int rep = 0; rep < 6; ++rep) {
+        const int mode = rep & 1;
+        if (mode == 0) k_fp64_probe<0><<<blocks, threads>>>(out, 16, 1.0);
+        else k_fp64_probe<1><<<blocks, threads>>>(out, 16, 1.0);
+        cudaEventRecord(a);
+        if (mode == 0) k_fp64_probe<0><<<blocks, threads>>>(out, iters, 1.0);
+        else k_fp64_probe<1><<<blocks, threads>>>(out, iters, 1.0);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, a, b);
+        const double flop = 2.0 * blocks * threads * static_cast<double>(iters) * 8;
+        if (ms > 0.f) best = std::max(best, flop / (ms * 1e-3) / 1e12);
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(out);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(m, e, "fp64 probe");
+    *tflops = best;
+    return PSSGP_OK;
+}
+
 pssgp_status pssgp_check(pssgp_model* m) {
     if (!m) return PSSGP_E_ARG;
     if (!m->d_err) return PSSGP_OK;
@@ -1291,7 +829,7 @@ pssgp_status pssgp_check(pssgp_model* m) {
     if (e != cudaSuccess) return cuda_fail(m, e, "cudaMemcpy(error word)");
     if (w == ~0ULL) return PSSGP_OK;
     cudaMemset(m->d_err, 0xff, sizeof(unsigned long long));
-    cudaMemset(m->d_err + 1, 0, sizeof(unsigned long long));   // K3 publication flag
+    cudaMemset(m->d_err + 1, 0, 2 * sizeof(unsigned long long));   // K3 publication flag, ticket
     const unsigned code = static_cast<unsigned>(w & 0xff);
     const int64_t idx = static_cast<int64_t>((w >> 8) & 0xffffffffffffULL);
     const char* what = code == kErrInput ? "invalid input (unsorted/non-finite t or non-finite observed y)"
@@ -1444,12 +982,9 @@ pssgp_status pssgp_debug_discretize(const pssgp_model* m, double dt, double* F, 
     pssgp_model* mm = const_cast<pssgp_model*>(m);
     if (m->d > kMaxD && m->mode == kPade && dt != 0.0) {
         // per-step device discretisation (kw_discretize): run it on the device for one step
-        switch (m->d) {
-#define X(DD) case DD: return wide_debug_discretize<DD>(mm, dt, F, Q);
-            PSSGP_WIDE_DIMS(X)
-#undef X
-            default: return fail(mm, PSSGP_E_UNSUPPORTED, "state dimension not compiled");
-        }
+        const WideOps* ops = wide_ops_for(m->d);
+        if (!ops) return fail(mm, PSSGP_E_UNSUPPORTED, "state dimension not compiled");
+        return ops->debug_disc(mm, dt, F, Q);
     }
     if (m->d > kMaxD) {   // mirrors wide::wdisc_kind
         const int d = m->d;
@@ -1488,17 +1023,9 @@ pssgp_status pssgp_plan(pssgp_model* m, int64_t N, int64_t* chain_len, int64_t* 
         case 2: pl = make_plan<2>(m, N); break;
         case 3: pl = make_plan<3>(m, N); break;
         default: {
-            WPlan wp;
-            switch (m->d) {
-#define X(DD) case DD: wp = make_wplan<DD>(m, N); break;
-                PSSGP_WIDE_DIMS(X)
-#undef X
-                default: return PSSGP_E_UNSUPPORTED;
-            }
-            if (chain_len) *chain_len = wp.K;
-            if (n_chains) *n_chains = wp.nch;
-            if (n_blocks) *n_blocks = wp.nb;
-            if (threads_per_block) *threads_per_block = 32 * pssgp::wide::kWWarps;
+            const WideOps* ops = wide_ops_for(m->d);
+            if (!ops) return PSSGP_E_UNSUPPORTED;
+            ops->plan(m, N, chain_len, n_chains, n_blocks, threads_per_block);
             return PSSGP_OK;
         }
     }
@@ -1547,7 +1074,7 @@ size_t pssgp_aggregate_bytes(const pssgp_model* m, int which) {
         fn = 3 * d * d + 2 * d;
         sn = 2 * d * d + d;
     }
-    return static_cast<size_t>(which == 0 ? fn : sn) * sizeof(double);
+    return static_cast<size_t>(which == 0 ? fn : sn + 1) * sizeof(double);   // smoother blob: + NLL partial
 }
 
 }  // extern "C"
@@ -1573,7 +1100,7 @@ pssgp_status shard_reduce(pssgp_model* m, int64_t k0, int64_t n, int64_t Ng, con
     p.t = t; p.y = y; p.mask = mask;
     if ((st = phase_filter_reduce<D>(m, p, s))) return st;
     ProfScope ps(m, S_RED, s);
-    k_reduce_blocks<D, FAgg<D>><<<1, kCarryThreads, 0, s>>>(p.block_f, p.nb, static_cast<double*>(out));
+    k_reduce_blocks<D, FAgg<D>><<<1, kCarryThreads, 0, s>>>(p.block_f, p.nb, static_cast<double*>(out), p.err, k0);
     LAUNCH_CHECK(m, "k_reduce_blocks(filter)");
     return PSSGP_OK;
 }
@@ -1590,16 +1117,18 @@ pssgp_status shard_fapply(pssgp_model* m, int64_t k0, int64_t n, int64_t Ng, con
     p.in_filt = static_cast<const double*>(all);
     p.rank = rank; p.world = world;
     if ((st = phase_filter_apply<D>(m, p, s))) return st;
+    // the chunk's NLL partial travels in the smoother blob, after the aggregate
+    if ((st = nll_sum(m, p.nll_block, p.nb, static_cast<double*>(sout) + SN(D), s))) return st;
     if (nllp && (st = nll_sum(m, p.nll_block, p.nb, nllp, s))) return st;
     ProfScope ps(m, S_RED, s);
-    k_reduce_blocks<D, SAgg<D>><<<1, kCarryThreads, 0, s>>>(p.block_s, p.nb, static_cast<double*>(sout));
+    k_reduce_blocks<D, SAgg<D>><<<1, kCarryThreads, 0, s>>>(p.block_s, p.nb, static_cast<double*>(sout), nullptr, 0);
     LAUNCH_CHECK(m, "k_reduce_blocks(smoother)");
     return PSSGP_OK;
 }
 
 template <int D>
 pssgp_status shard_sapply(pssgp_model* m, int64_t k0, int64_t n, int64_t Ng, const double* t, const void* all,
-                          int rank, int world, double* mean, double* var, cudaStream_t s) {
+                          int rank, int world, double* mean, double* var, double* nll, cudaStream_t s) {
     KParams<D> p;
     Plan pl;
     pssgp_status st = shard_setup<D>(m, k0, n, Ng, p, pl);
@@ -1608,7 +1137,10 @@ pssgp_status shard_sapply(pssgp_model* m, int64_t k0, int64_t n, int64_t Ng, con
     p.in_smooth = static_cast<const double*>(all);
     p.rank = rank; p.world = world;
     p.mean = mean; p.var = var;
-    return phase_smoother<D>(m, p, s);
+    if ((st = phase_smoother<D>(m, p, s))) return st;
+    // total NLL: fixed-order sum over ranks of the partials carried in the gathered blobs
+    if (nll) return nll_sum(m, static_cast<const double*>(all) + SN(D), world, nll, s, SN(D) + 1);
+    return PSSGP_OK;
 }
 
 pssgp_status shard_args(pssgp_model* m, int64_t k0, int64_t n, int64_t Ng, const double* t) {
@@ -1629,7 +1161,7 @@ pssgp_status pssgp_shard_filter_reduce(pssgp_model* m, int64_t k0, int64_t n, in
     auto s = static_cast<cudaStream_t>(stream);
     m->last_stream = s;
     m->sh_k0 = k0; m->sh_n = n; m->sh_N = N_global;
-    if (m->d > kMaxD) { DISPATCH_WIDE(m, wide_shard_reduce, m, k0, n, N_global, t, y, mask, filt_agg_out, s); }
+    if (m->d > kMaxD) return wide_ops_for(m->d)->shard_reduce(m, k0, n, N_global, t, y, mask, filt_agg_out, s);
     DISPATCH_D(m, shard_reduce<D_>(m, k0, n, N_global, t, y, mask, filt_agg_out, s));
 }
 
@@ -1645,8 +1177,8 @@ pssgp_status pssgp_shard_filter_apply(pssgp_model* m, int64_t k0, int64_t n, int
     auto s = static_cast<cudaStream_t>(stream);
     m->last_stream = s;
     if (m->d > kMaxD) {
-        DISPATCH_WIDE(m, wide_shard_fapply, m, k0, n, N_global, t, y, mask, all_filt_aggs, rank, world,
-                      smooth_agg_out, nll_partial, s);
+        return wide_ops_for(m->d)->shard_fapply(m, k0, n, N_global, t, y, mask, all_filt_aggs, rank, world,
+                                                smooth_agg_out, nll_partial, s);
     }
     DISPATCH_D(m, shard_fapply<D_>(m, k0, n, N_global, t, y, mask, all_filt_aggs, rank, world, smooth_agg_out,
                                    nll_partial, s));
@@ -1654,7 +1186,7 @@ pssgp_status pssgp_shard_filter_apply(pssgp_model* m, int64_t k0, int64_t n, int
 
 pssgp_status pssgp_shard_smoother_apply(pssgp_model* m, int64_t k0, int64_t n, int64_t N_global, const double* t,
                                         const void* all_smooth_aggs, int rank, int world, double* mean, double* var,
-                                        void* stream) {
+                                        double* nll, void* stream) {
     pssgp_status st = shard_args(m, k0, n, N_global, t);
     if (st) return st;
     if (!all_smooth_aggs || rank < 0 || rank >= world) return fail(m, PSSGP_E_ARG, "bad argument");
@@ -1663,9 +1195,9 @@ pssgp_status pssgp_shard_smoother_apply(pssgp_model* m, int64_t k0, int64_t n, i
     auto s = static_cast<cudaStream_t>(stream);
     m->last_stream = s;
     if (m->d > kMaxD) {
-        DISPATCH_WIDE(m, wide_shard_sapply, m, k0, n, N_global, t, all_smooth_aggs, rank, world, mean, var, s);
+        return wide_ops_for(m->d)->shard_sapply(m, k0, n, N_global, t, all_smooth_aggs, rank, world, mean, var, nll, s);
     }
-    DISPATCH_D(m, shard_sapply<D_>(m, k0, n, N_global, t, all_smooth_aggs, rank, world, mean, var, s));
+    DISPATCH_D(m, shard_sapply<D_>(m, k0, n, N_global, t, all_smooth_aggs, rank, world, mean, var, nll, s));
 }
 
 }  // extern "C"

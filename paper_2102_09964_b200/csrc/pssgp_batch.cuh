@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_filter_reduce(co
     const int64_t wbase = (static_cast<int64_t>(blockIdx.x) * kThreads + wid * 32) * p.K;
     const int64_t kb = c * p.K;
     const int64_t ke = min(kb + p.K, p.n);
-    if (blockIdx.x == 0 && threadIdx.x == 0) *p.flag = 0ull;   // K3b's carry publication word
+    if (blockIdx.x == 0 && threadIdx.x == 0) { p.flag[0] = 0ull; p.flag[1] = 0ull; }   // K3b's publication word, ticket
     FAgg<D> a;
     set_identity(a);
     ModelParams<D> mp = p.m;
@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_filter_reduce(co
         shfl_down_all(o, a, off);
         if ((lane & (2 * off - 1)) == 0) {
             FAgg<D> r;
-            combine(a, o, r);
+            if (!combine(a, o, r)) raise_error(p.err, kb, kErrNumeric);
             a = r;
         }
     }
@@ -142,11 +142,13 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_filter_reduce(co
     __syncthreads();
     if (threadIdx.x == 0) {
         FAgg<D> acc = wagg[0];
+        bool ok = true;
         for (int w = 1; w < kWarps; ++w) {
             FAgg<D> r;
-            combine(acc, wagg[w], r);
+            ok = combine(acc, wagg[w], r) && ok;
             acc = r;
         }
+        if (!ok) raise_error(p.err, kb, kErrNumeric);
         store_aos(acc, p.block_f + static_cast<int64_t>(blockIdx.x) * FN(D));
     }
 }
@@ -161,14 +163,16 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_filter_apply(con
     __shared__ FAgg<D> tot[kWarps];
     __shared__ Gauss<D> wcar[kWarps];
     __shared__ SAgg<D> stot[kWarps];
+    __shared__ int s_bid;
+    const int bid = k3_ticket(p.flag, &s_bid);               // logical CTA index (arrival order)
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int64_t c = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
+    const int64_t c = static_cast<int64_t>(bid) * kThreads + threadIdx.x;
     const int64_t nch = static_cast<int64_t>(p.nb) * kThreads;
-    const int64_t wg = static_cast<int64_t>(blockIdx.x) * kWarps + wid;
+    const int64_t wg = static_cast<int64_t>(bid) * kWarps + wid;
     const int64_t wbase = wg * 32 * p.K;
     const int64_t kb = c * p.K;
     const int64_t ke = min(kb + p.K, p.n);
-    const Gauss<D> cur = filter_chain_carry<D>(p, tot, wcar, c, nch, lane, wid);
+    const Gauss<D> cur = filter_chain_carry<D>(p, tot, wcar, c, nch, lane, wid, bid);
     double x[D], P[ns(D)], x0[D], P0[ns(D)], Sg[D * D];
 #pragma unroll
     for (int i = 0; i < D; ++i) x[i] = cur.x[i];
@@ -319,7 +323,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_filter_apply(con
             combine(acc, stot[w], r);
             acc = r;
         }
-        store_aos(acc, p.block_s + static_cast<int64_t>(blockIdx.x) * SN(D));
+        store_aos(acc, p.block_s + static_cast<int64_t>(bid) * SN(D));
     }
 }
 

@@ -74,7 +74,7 @@ cudaError_t launch_d(const Run& r, int phase) {
             p.nll_out = r.nll;
             k_smoother_apply<D, kClosed><<<r.nb, kThreads, 0, r.stream>>>(p);
             break;
-        case 4: k_nll_sum<<<1, kThreads, 0, r.stream>>>(p.nll_block, r.nb, r.nll); break;
+        case 4: k_nll_sum<<<1, kThreads, 0, r.stream>>>(p.nll_block, r.nb, r.nll, 1); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

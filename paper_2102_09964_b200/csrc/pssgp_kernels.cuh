@@ -65,6 +65,19 @@ __device__ __forceinline__ void raise_error(unsigned long long* err, int64_t gid
     if (w < *reinterpret_cast<volatile unsigned long long*>(err)) atomicMin(err, w);
 }
 
+// combine() of the filtering operator reports a singular (I + C_i J_j) (false); the smoothing and
+// tangent operators cannot fail.  Every operator tree ANDs the results into a per-thread flag and
+// latches kErrNumeric once after the tree.
+template <typename Agg>
+__device__ __forceinline__ bool combine_chk(const Agg& a, const Agg& b, Agg& r) {
+    if constexpr (std::is_same_v<decltype(combine(a, b, r)), bool>) {
+        return combine(a, b, r);
+    } else {
+        combine(a, b, r);
+        return true;
+    }
+}
+
 template <int D>
 struct KParams {
     ModelParams<D> m;
@@ -93,9 +106,21 @@ struct KParams {
     double* nll_out;        // nll scalar output (nullable)
     unsigned long long* err;
     int store_state;        // K3: write (xbar, P) and smoother aggregates (0 for NLL-only)
-    unsigned long long* flag;   // K3 block-carry publication word: reset to 0 by K1, set to 1 by
-                                // K3's CTA 0 (stream-ordered, so CUDA-graph replays are safe)
+    unsigned long long* flag;   // flag[0]: K3 block-carry publication word (set to 1 by logical CTA 0);
+                                // flag[1]: K3 tile ticket (logical CTA index = arrival order).  Both reset
+                                // to 0 by K1 (stream-ordered, so CUDA-graph replays are safe).
 };
+
+// K3's logical CTA index: the arrival order of the CTAs (an atomic ticket), so the CTA that scans
+// the block aggregates and publishes every CTA's carry (logical 0) is the first one that ever ran.
+// A CTA spins only after taking a later ticket, i.e. after logical 0 is resident, and logical 0
+// waits on nobody: forward progress needs no co-residency or dispatch-order assumption (other
+// streams, MPS, grids larger than one wave).
+__device__ __forceinline__ int k3_ticket(unsigned long long* flag, int* s_bid) {
+    if (threadIdx.x == 0) *s_bid = static_cast<int>(atomicAdd(flag + 1, 1ull));
+    __syncthreads();
+    return *s_bid;
+}
 
 // ------------------------------------------------------------------ warp shuffles of aggregates
 template <typename T>
@@ -298,7 +323,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_reduce(const KP
     const int64_t kb = c * p.K;
     const int64_t ke = min(kb + p.K, p.n);
 
-    if (blockIdx.x == 0 && threadIdx.x == 0) *p.flag = 0ull;   // K3's carry publication word
+    if (blockIdx.x == 0 && threadIdx.x == 0) { p.flag[0] = 0ull; p.flag[1] = 0ull; }   // K3 publication word, ticket
     FAgg<D> a;
     set_identity(a);
     double tprev = 0.0;
@@ -379,12 +404,14 @@ set_zero(F);
     __syncthreads();
     if (threadIdx.x == 0) {
         FAgg<D> acc = wagg[0];
+        bool ok = true;
 #pragma unroll 1
         for (int w = 1; w < kWarps; ++w) {
             FAgg<D> r;
-            combine(acc, wagg[w], r);
+            ok = combine(acc, wagg[w], r) && ok;
             acc = r;
         }
+        if (!ok) raise_error(p.err, p.k0 + kb, kErrNumeric);
         store_aos(acc, p.block_f + static_cast<int64_t>(blockIdx.x) * FN(D));
     }
 }
@@ -398,7 +425,8 @@ set_zero(F);
 // (K3) / later (K5) CTAs: the block scan is thus spread over every SM instead
 // of a separate single-CTA kernel.
 template <typename Agg>
-__device__ __forceinline__ Agg cta_reduce_range(const real* __restrict__ blocks, int lo, int hi, Agg* wred) {
+__device__ __forceinline__ Agg cta_reduce_range(const real* __restrict__ blocks, int lo, int hi, Agg* wred,
+                                                bool* ok_out = nullptr) {
     constexpr int NA = sizeof(Agg) / sizeof(real);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int cnt = max(hi - lo, 0);
@@ -406,6 +434,7 @@ __device__ __forceinline__ Agg cta_reduce_range(const real* __restrict__ blocks,
     const int b0 = lo + min(static_cast<int>(threadIdx.x) * per, cnt), b1 = min(b0 + per, lo + cnt);
     Agg a;
     set_identity(a);
+    bool ok = true;
     for (int b = b0; b < b1; ++b) {
         Agg e;
         load_aos(e, blocks + static_cast<int64_t>(b) * NA);
@@ -413,7 +442,7 @@ __device__ __forceinline__ Agg cta_reduce_range(const real* __restrict__ blocks,
             a = e;
         } else {
             Agg r;
-            combine(a, e, r);
+            ok = combine_chk(a, e, r) && ok;
             a = r;
         }
     }
@@ -423,7 +452,7 @@ __device__ __forceinline__ Agg cta_reduce_range(const real* __restrict__ blocks,
         shfl_down_all(o, a, off);
         if ((lane & (2 * off - 1)) == 0 && (threadIdx.x + off) * per < cnt) {
             Agg r;
-            combine(a, o, r);
+            ok = combine_chk(a, o, r) && ok;
             a = r;
         }
     }
@@ -433,22 +462,24 @@ __device__ __forceinline__ Agg cta_reduce_range(const real* __restrict__ blocks,
     if (threadIdx.x == 0) {
         for (int w = 1; w < kWarps && w * 32 * per < cnt; ++w) {
             Agg r;
-            combine(acc, wred[w], r);
+            ok = combine_chk(acc, wred[w], r) && ok;
             acc = r;
         }
     }
+    if (ok_out) *ok_out = ok;
     __syncthreads();
     return acc;
 }
 
-// Deterministic fixed-order sum of parts[0, n) by one CTA; result valid in thread 0.
-__device__ __forceinline__ double cta_sum(const double* __restrict__ parts, int n, double* red) {
+// Deterministic fixed-order sum of parts[0, n) (element b at parts[b * stride]) by one CTA; result
+// valid in thread 0.
+__device__ __forceinline__ double cta_sum(const double* __restrict__ parts, int n, double* red, int stride = 1) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int per = (n + kThreads - 1) / kThreads;
     double s = 0.0;
     for (int i = 0; i < per; ++i) {
         const int b = threadIdx.x * per + i;
-        if (b < n) s += parts[b];
+        if (b < n) s += parts[static_cast<int64_t>(b) * stride];
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
@@ -502,16 +533,18 @@ __device__ __forceinline__ void nll_accumulate(bool obs, double v, double vs, do
 // CTAs + the CTA's chain scan); shared scratch tot[kWarps], wcar[kWarps].
 template <int D>
 __device__ __forceinline__ Gauss<D> filter_chain_carry(const KParams<D>& p, FAgg<D>* tot, Gauss<D>* wcar, int64_t c,
-                                                       int64_t nch, int lane, int wid) {
-    // ---- collapsed prefix entering this CTA.  CTA 0 alone scans the block aggregates (an
-    // exclusive scan producing the collapsed carry (x, P) entering every CTA, starting from the
-    // incoming carry of earlier ranks when sharded), writes them to p.fcarry and publishes
-    // 1 in p.flag (K1 of the same posterior reset it to 0); the other CTAs spin on the flag (all CTAs of the one-wave grid are
-    // co-resident and CTA 0 never waits) while their warps' chain scans below run.  This
-    // replaces a redundant per-CTA reduction of all earlier blocks (~20 dependent operator
-    // levels, throughput-bound across the wave) by one scan of depth ~15 in one CTA.
+                                                       int64_t nch, int lane, int wid, int bid) {
+    // ---- collapsed prefix entering this CTA.  Logical CTA 0 (the first to arrive, k3_ticket) alone
+    // scans the block aggregates (an exclusive scan producing the collapsed carry (x, P) entering
+    // every CTA, starting from the incoming carry of earlier ranks when sharded), writes them to
+    // p.fcarry and publishes 1 in p.flag[0] (K1 of the same posterior reset it); the other CTAs run
+    // their warps' chain scans below and then wait for the flag.  Logical CTA 0 waits on nobody and
+    // has started before any CTA that waits, so the wait always ends.  One scan of depth ~15 in one
+    // CTA replaces a redundant per-CTA reduction of all earlier blocks (~20 dependent operator
+    // levels, throughput-bound across the wave).
     Gauss<D> cur;
-    if (blockIdx.x == 0) {
+    bool ok = true;
+    if (bid == 0) {
         const int per = (p.nb + kThreads - 1) / kThreads;
         const int b0 = min(static_cast<int>(threadIdx.x) * per, p.nb), b1 = min(b0 + per, p.nb);
         FAgg<D> a;
@@ -519,7 +552,7 @@ __device__ __forceinline__ Gauss<D> filter_chain_carry(const KParams<D>& p, FAgg
         for (int b = b0; b < b1; ++b) {
             FAgg<D> e, r;
             load_aos(e, p.block_f + static_cast<int64_t>(b) * FN(D));
-            combine(a, e, r);
+            ok = combine(a, e, r) && ok;
             a = r;
         }
 #pragma unroll
@@ -528,7 +561,7 @@ __device__ __forceinline__ Gauss<D> filter_chain_carry(const KParams<D>& p, FAgg
             shfl_up_all(o, a, off);
             if (lane >= off) {
                 FAgg<D> r;
-                combine(o, a, r);
+                ok = combine(o, a, r) && ok;
                 a = r;
             }
         }
@@ -543,13 +576,13 @@ __device__ __forceinline__ Gauss<D> filter_chain_carry(const KParams<D>& p, FAgg
                 FAgg<D> ag;
                 load_aos(ag, p.in_filt + static_cast<int64_t>(g) * FN(D));
                 Gauss<D> r2;
-                apply_prefix(R, ag, r2);
+                ok = apply_prefix(R, ag, r2) && ok;
                 R = r2;
             }
             for (int w = 0; w < kWarps; ++w) {
                 wcar[w] = R;
                 Gauss<D> r2;
-                apply_prefix(R, tot[w], r2);
+                ok = apply_prefix(R, tot[w], r2) && ok;
                 R = r2;
             }
         }
@@ -557,7 +590,7 @@ __device__ __forceinline__ Gauss<D> filter_chain_carry(const KParams<D>& p, FAgg
         Gauss<D> C = wcar[wid];
         if (lane > 0) {
             Gauss<D> r2;
-            apply_prefix(C, ex, r2);
+            ok = apply_prefix(C, ex, r2) && ok;
             C = r2;
         }
         for (int b = b0; b < b1; ++b) {
@@ -565,7 +598,7 @@ __device__ __forceinline__ Gauss<D> filter_chain_carry(const KParams<D>& p, FAgg
             FAgg<D> e;
             load_aos(e, p.block_f + static_cast<int64_t>(b) * FN(D));
             Gauss<D> r2;
-            apply_prefix(C, e, r2);
+            ok = apply_prefix(C, e, r2) && ok;
             C = r2;
         }
         __threadfence();
@@ -582,7 +615,7 @@ __device__ __forceinline__ Gauss<D> filter_chain_carry(const KParams<D>& p, FAgg
             shfl_up_all(o, a, off);
             if (lane >= off) {
                 FAgg<D> r;
-                combine(o, a, r);
+                ok = combine(o, a, r) && ok;
                 a = r;
             }
         }
@@ -593,19 +626,19 @@ __device__ __forceinline__ Gauss<D> filter_chain_carry(const KParams<D>& p, FAgg
         __syncthreads();
         if (threadIdx.x == 0) {
             // wait for CTA 0's publication, then read this CTA's collapsed carry
-            while (atomicAdd(p.flag, 0ull) == 0ull) __nanosleep(64);
+            while (atomicAdd(p.flag, 0ull) == 0ull) __nanosleep(64);   // logical CTA 0 runs (k3_ticket)
             __threadfence();
             Gauss<D> acc;
             {   // L2 loads (the carry was written by another CTA in this launch)
                 real* d = reinterpret_cast<real*>(&acc);
-                const real* src = p.fcarry + static_cast<int64_t>(blockIdx.x) * CN(D);
+                const real* src = p.fcarry + static_cast<int64_t>(bid) * CN(D);
 #pragma unroll
                 for (int i = 0; i < CN(D); ++i) d[i] = __ldcg(src + i);
             }
             for (int w = 0; w < kWarps; ++w) {
                 wcar[w] = acc;
                 Gauss<D> r2;
-                apply_prefix(acc, tot[w], r2);
+                ok = apply_prefix(acc, tot[w], r2) && ok;
                 acc = r2;
             }
         }
@@ -613,10 +646,12 @@ __device__ __forceinline__ Gauss<D> filter_chain_carry(const KParams<D>& p, FAgg
         cur = wcar[wid];
         if (lane > 0) {
             Gauss<D> r2;
-            apply_prefix(cur, ex, r2);
+            ok = apply_prefix(cur, ex, r2) && ok;
             cur = r2;
         }
     }
+    // a singular (I + C_i J_j) anywhere in the carry trees: latched at the CTA's first step
+    if (!ok) raise_error(p.err, p.k0 + static_cast<int64_t>(bid) * kThreads * p.K, kErrNumeric);
 
     return cur;
 }
@@ -631,15 +666,17 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
     __shared__ Gauss<D> wcar[kWarps];
     __shared__ SAgg<D> stot[kWarps];
     __shared__ double nred[kWarps];
+    __shared__ int s_bid;
+    const int bid = k3_ticket(p.flag, &s_bid);               // logical CTA index (arrival order)
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int64_t c = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
+    const int64_t c = static_cast<int64_t>(bid) * kThreads + threadIdx.x;
     const int64_t nch = static_cast<int64_t>(p.nb) * kThreads;
-    const int64_t wg = static_cast<int64_t>(blockIdx.x) * kWarps + wid;
+    const int64_t wg = static_cast<int64_t>(bid) * kWarps + wid;
     const int64_t wbase = wg * 32 * p.K;
     const int64_t kb = c * p.K;
     const int64_t ke = min(kb + p.K, p.n);
 
-    const Gauss<D> cur = filter_chain_carry<D>(p, tot, wcar, c, nch, lane, wid);
+    const Gauss<D> cur = filter_chain_carry<D>(p, tot, wcar, c, nch, lane, wid, bid);
 
     // ---- Kalman filter over the chain (supplement PAPER.md:285-315), carrying the
     // chain-entry moments E[x_k0 | y_1:k], Cov(x_k0 | y_1:k) and the cross-covariance
@@ -829,7 +866,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
     if (threadIdx.x == 0) {
         double s2 = 0.0;
         for (int w = 0; w < kWarps; ++w) s2 += nred[w];
-        p.nll_block[blockIdx.x] = s2;
+        p.nll_block[bid] = s2;
         if (SAGG) {
             SAgg<D> acc = stot[0];
             for (int w = 1; w < kWarps; ++w) {
@@ -837,7 +874,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
                 combine(acc, stot[w], r);
                 acc = r;
             }
-            store_aos(acc, p.block_s + static_cast<int64_t>(blockIdx.x) * SN(D));
+            store_aos(acc, p.block_s + static_cast<int64_t>(bid) * SN(D));
         }
     }
 }
@@ -857,7 +894,7 @@ __device__ __forceinline__ Gauss<D> smoother_chain_carry(const KParams<D>& p, SA
             set_zero(R);
             for (int g = p.world - 1; g > p.rank && p.in_smooth; --g) {
                 SAgg<D> ag;
-                load_aos(ag, p.in_smooth + static_cast<int64_t>(g) * SN(D));
+                load_aos(ag, p.in_smooth + static_cast<int64_t>(g) * (SN(D) + 1));   // blob = aggregate + NLL partial
                 Gauss<D> r2;
                 apply_suffix(ag, R, r2);
                 R = r2;
@@ -1078,19 +1115,24 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_smoother_apply(const K
     if (ferr_n >= 0) raise_error(p.err, p.k0 + kb + ferr_n, kErrNumeric);
 }
 
+#ifndef PSSGP_NO_MISC_KERNELS
 // ------------------------------------------------------------------ K6: deterministic NLL sum
 // The same fixed-order CTA sum (cta_sum, kThreads threads) as K5's CTA 0 uses, so the NLL-only
-// path returns bit-for-bit the NLL of the full posterior.  Launch <<<1, kThreads>>>.
-__global__ void __launch_bounds__(kThreads, 1) k_nll_sum(const double* __restrict__ parts, int nb, double* out) {
+// path returns bit-for-bit the NLL of the full posterior.  Launch <<<1, kThreads>>>.  stride > 1:
+// the partials are spread over gathered per-rank blobs (sharded total NLL).
+__global__ void __launch_bounds__(kThreads, 1) k_nll_sum(const double* __restrict__ parts, int nb, double* out,
+                                                         int stride) {
     __shared__ double red[kWarps];
-    const double v = cta_sum(parts, nb, red);
+    const double v = cta_sum(parts, nb, red, stride);
     if (threadIdx.x == 0) *out = v;
 }
+#endif
 
 // ------------------------------------------------------------------ chunk aggregate reducers (sharded path, 1 CTA)
 template <int D, typename Agg>
 __global__ void __launch_bounds__(kCarryThreads, 1) k_reduce_blocks(const real* __restrict__ blocks, int nb,
-                                                                    real* out) {
+                                                                    real* out, unsigned long long* err,
+                                                                    int64_t err_index) {
     constexpr int NW = kCarryThreads / 32;
     constexpr int NA = sizeof(Agg) / sizeof(real);
     __shared__ Agg wred[NW];
@@ -1098,12 +1140,13 @@ __global__ void __launch_bounds__(kCarryThreads, 1) k_reduce_blocks(const real* 
     const int per = (nb + kCarryThreads - 1) / kCarryThreads;
     Agg a;
     set_identity(a);
+    bool ok = true;
     for (int i = 0; i < per; ++i) {
         const int b = threadIdx.x * per + i;
         if (b < nb) {
             Agg e, r;
             load_aos(e, blocks + static_cast<int64_t>(b) * NA);
-            combine(a, e, r);
+            ok = combine_chk(a, e, r) && ok;
             a = r;
         }
     }
@@ -1113,7 +1156,7 @@ __global__ void __launch_bounds__(kCarryThreads, 1) k_reduce_blocks(const real* 
         shfl_down_all(o, a, off);
         if ((lane & (2 * off - 1)) == 0) {
             Agg r;
-            combine(a, o, r);
+            ok = combine_chk(a, o, r) && ok;
             a = r;
         }
     }
@@ -1123,15 +1166,17 @@ __global__ void __launch_bounds__(kCarryThreads, 1) k_reduce_blocks(const real* 
         Agg acc = wred[0];
         for (int w = 1; w < NW; ++w) {
             Agg r;
-            combine(acc, wred[w], r);
+            ok = combine_chk(acc, wred[w], r) && ok;
             acc = r;
         }
         store_aos(acc, out);
     }
+    if (!ok && err) raise_error(err, err_index, kErrNumeric);
 }
 
 }  // namespace PSSGP_NS
 
+#ifndef PSSGP_NO_MISC_KERNELS
 namespace PSSGP_NS {
 // ------------------------------------------------------------------ test-time merge (stage 4)
 // Rank-based parallel merge of sorted training times (observed) and sorted test
@@ -1185,3 +1230,4 @@ __global__ void __launch_bounds__(256) k_gather(int64_t n_te, const int64_t* __r
     }
 }
 }  // namespace PSSGP_NS
+#endif  // PSSGP_NO_MISC_KERNELS

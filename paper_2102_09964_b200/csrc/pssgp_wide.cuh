@@ -877,7 +877,9 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WMINB) kw_filter_fold(cons
 // (full-warp shuffles).  Replaces one warp-cooperative shared-memory step per chain (36-64
 // outputs over 32 lanes, ~4,400 cycles at d = 6) by four register steps in parallel.
 constexpr int kQ = 4, kGL = 8;
-template <int D>
+// staging slot of one step's (F_k, Q_k) record: only the per-step (STREAM) kernels reserve it
+PS_CX int FQS(int D, bool stream) { return stream ? FQW(D) : 1; }
+template <int D, bool STREAM>
 struct K1LSmem {
     SModel<D> m;
     double I[D][LD(D)], Z[D][LD(D)];
@@ -885,7 +887,7 @@ struct K1LSmem {
         SF<D> q[kQ];
         SCombF<D> s;
         double U[kQ][D][LD(D)];
-        double fqs[kQ][2][FQW(D)];                 // STREAM: each quarter's (F_k, Q_k) staged one step ahead
+        double fqs[kQ][2][FQS(D, STREAM)];         // STREAM: each quarter's (F_k, Q_k) staged one step ahead
     } w[kWWarps];
 };
 
@@ -1040,7 +1042,7 @@ template <int D, bool STREAM>
 __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_filter_fold_lpr(const WParams p) {
     static_assert(D <= kGL, "lane-per-row fold holds one row per lane of an 8-lane group");
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    K1LSmem<D>& sh = *reinterpret_cast<K1LSmem<D>*>(smem_raw);
+    K1LSmem<D, STREAM>& sh = *reinterpret_cast<K1LSmem<D, STREAM>*>(smem_raw);
     load_model<D>(sh.m, p.model);
     for (int e = threadIdx.x; e < D * D; e += blockDim.x) {
         const int i = e / D, j = e - (e / D) * D;
@@ -1361,7 +1363,7 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WMINB) kw_filter_apply(con
     __syncwarp();
     for (int g = 0; g < p.rank && p.in_filt; ++g) {
         gload<D>(W.u.c.a, p.in_filt + static_cast<int64_t>(g) * FNW(D), lane);
-        wapply_prefix<D>(W.x, W.P, W.u.c.a, W.u.c.s, lane);
+        if (!wapply_prefix<D>(W.x, W.P, W.u.c.a, W.u.c.s, lane) && lane == 0) raise_error(p.err, p.k0, kErrNumeric);
     }
     if (c > 0) {
         gload<D>(W.u.c.a, p.fagg + static_cast<int64_t>(c - 1) * FNW(D), lane);
@@ -1467,19 +1469,19 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WMINB) kw_filter_apply(con
 // lane r (< D) owning row r of P, Sg = Cov(x_k0, x_k), P0 and x_r, x0_r; F P is transposed
 // through a per-warp shared buffer, the full x, HP, SH vectors are gathered by shuffles.  The
 // moments are written back to the shared layout for the chain smoother aggregate.
-template <int D>
+template <int D, bool STREAM>
 struct K3LSmem {
     K3Smem<D> b;
     double I[D][LD(D)], Z[D][LD(D)];
     double U[kWWarps][D][LD(D)];
-    double fqs[kWWarps][2][FQW(D)];                 // STREAM: per-step (F_k, Q_k) staged one step ahead
+    double fqs[kWWarps][2][FQS(D, STREAM)];         // STREAM: per-step (F_k, Q_k) staged one step ahead
 };
 
 template <int D, bool STREAM>
 __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_filter_apply_lpr(const WParams p) {
     static_assert(D <= kGL, "lane-per-row rescan holds one row per lane");
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    K3LSmem<D>& shl = *reinterpret_cast<K3LSmem<D>*>(smem_raw);
+    K3LSmem<D, STREAM>& shl = *reinterpret_cast<K3LSmem<D, STREAM>*>(smem_raw);
     K3Smem<D>& sh = shl.b;
     load_model<D>(sh.m, p.model);
     for (int e = threadIdx.x; e < D * D; e += blockDim.x) {
@@ -1500,7 +1502,7 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_filter_apply
     __syncwarp();
     for (int g = 0; g < p.rank && p.in_filt; ++g) {
         gload<D>(W.u.c.a, p.in_filt + static_cast<int64_t>(g) * FNW(D), lane);
-        wapply_prefix<D>(W.x, W.P, W.u.c.a, W.u.c.s, lane);
+        if (!wapply_prefix<D>(W.x, W.P, W.u.c.a, W.u.c.s, lane) && lane == 0) raise_error(p.err, p.k0, kErrNumeric);
     }
     if (c > 0) {
         gload<D>(W.u.c.a, p.fagg + static_cast<int64_t>(c - 1) * FNW(D), lane);
@@ -1702,7 +1704,7 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WMINB) kw_smoother_apply(c
     for (int i = lane; i < D; i += 32) W.ms[i] = 0.0;
     __syncwarp();
     for (int g = p.world - 1; g > p.rank && p.in_smooth; --g) {
-        gload<D>(W.u.c.a, p.in_smooth + static_cast<int64_t>(g) * SNW(D), lane);
+        gload<D>(W.u.c.a, p.in_smooth + static_cast<int64_t>(g) * (SNW(D) + 1), lane);   // blob = aggregate + NLL partial
         wapply_suffix<D>(W.u.c.a, W.ms, W.Ps, W.u.c.s, lane);
     }
     if (c + 1 < p.nch) {
@@ -1831,14 +1833,14 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WMINB) kw_smoother_apply(c
 // and column r of F P and X = P^-_{k+1}^-1 F P (so the gain is X^T).  Matrices a lane needs in
 // full (P^-, P^s, X) go through per-warp shared buffers; every lane factors P^- (Cholesky,
 // upper triangle as the symmetric source of truth) in registers and solves for its own column.
-template <int D>
+template <int D, bool STREAM>
 struct K5LSmem {
     K5Smem<D> b;
     double I[D][LD(D)], Z[D][LD(D)];
     struct G {
         double U[D][LD(D)], Pm[D][LD(D)], Ps[D][LD(D)] /* P^s_{k+1} - P^- */, X[D][LD(D)];
         double dm[D];
-        double fqs[2][FQW(D)];                      // STREAM: (F_{k+1}, Q_{k+1}) staged with the record of k
+        double fqs[2][FQS(D, STREAM)];              // STREAM: (F_{k+1}, Q_{k+1}) staged with the record of k
     } g[kWWarps];
 };
 
@@ -1846,7 +1848,7 @@ template <int D, bool STREAM>
 __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_smoother_apply_lpr(const WParams p) {
     static_assert(D <= kGL, "lane-per-row RTS holds one row per lane");
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    K5LSmem<D>& shl = *reinterpret_cast<K5LSmem<D>*>(smem_raw);
+    K5LSmem<D, STREAM>& shl = *reinterpret_cast<K5LSmem<D, STREAM>*>(smem_raw);
     K5Smem<D>& sh = shl.b;
     load_model<D>(sh.m, p.model);
     for (int e = threadIdx.x; e < D * D; e += blockDim.x) {
@@ -1877,7 +1879,7 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_smoother_app
     for (int i = lane; i < D; i += 32) W.ms[i] = 0.0;
     __syncwarp();
     for (int g = p.world - 1; g > p.rank && p.in_smooth; --g) {
-        gload<D>(W.u.c.a, p.in_smooth + static_cast<int64_t>(g) * SNW(D), lane);
+        gload<D>(W.u.c.a, p.in_smooth + static_cast<int64_t>(g) * (SNW(D) + 1), lane);   // blob = aggregate + NLL partial
         wapply_suffix<D>(W.u.c.a, W.ms, W.Ps, W.u.c.s, lane);
     }
     if (c + 1 < p.nch) {

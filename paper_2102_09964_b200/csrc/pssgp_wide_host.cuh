@@ -1,0 +1,425 @@
+// pssgp_wide_host.cuh — host side of the warp-per-chain path (d >= 4): launch plan, workspace,
+// and the kernel sequences of pssgp_posterior / the sharded phases for one state dimension D.
+// Included only by pssgp_wide_inst.cu (one object per D in pssgp_dims.h).
+#pragma once
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "pssgp_internal.hpp"
+#include "pssgp_wide.cuh"
+
+namespace pssgp_internal {
+namespace widehost {
+using namespace pssgp;
+// ========================================================================== wide path (d >= 4)
+
+// The >48 KB dynamic shared-memory opt-in is a per-device function attribute: set it once per
+// device (bit `device` of a process-wide mask; setting it twice is harmless, so a race only repeats
+// the calls).
+template <int D>
+void wide_set_smem_attrs(int device) {
+    using namespace pssgp::wide;
+    static std::atomic<unsigned long long> done{0ull};
+    const unsigned long long bit = 1ull << (device & 63);
+    if (done.load() & bit) return;
+    cudaFuncSetAttribute(kw_filter_fold<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K1Smem<D>));
+    if constexpr (D <= kGL) {
+        cudaFuncSetAttribute(kw_filter_fold_lpr<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K1LSmem<D, false>));
+        cudaFuncSetAttribute(kw_filter_fold_lpr<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K1LSmem<D, true>));
+        cudaFuncSetAttribute(kw_filter_apply_lpr<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K3LSmem<D, false>));
+        cudaFuncSetAttribute(kw_filter_apply_lpr<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K3LSmem<D, true>));
+        cudaFuncSetAttribute(kw_smoother_apply_lpr<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K5LSmem<D, false>));
+        cudaFuncSetAttribute(kw_smoother_apply_lpr<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K5LSmem<D, true>));
+    }
+    cudaFuncSetAttribute(kw_filter_apply<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K3Smem<D>));
+    cudaFuncSetAttribute(kw_smoother_apply<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K5Smem<D>));
+    cudaFuncSetAttribute(kw_scan_filter<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(ScanSmemF<D>));
+    cudaFuncSetAttribute(kw_scan_smoother<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(ScanSmemS<D>));
+    cudaFuncSetAttribute(kw_discretize<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(KDSmem<D>));
+    done.fetch_or(bit);
+}
+
+// lane-per-row kernels of the wide path for D <= 8 (bit 0: fold, bit 1: RTS rescan, bit 2: both
+// rescans also with per-step (F, Q) staged in shared memory, bit 3: one-wave plan for them on the
+// table path, bit 4: Kalman rescan, bit 5: the one-wave plan also on the per-step (F, Q) path, bit 6:
+// lane-per-row discretisation); env PSSGP_WIDE_LPR overrides the default 127 for A/B runs (0 = the
+// shared-memory kernels)
+inline int wide_lpr_mask() {
+    static const int v = [] { const char* e = getenv("PSSGP_WIDE_LPR"); return e && *e ? atoi(e) : 127; }();
+    return v;
+}
+
+struct WPlan {
+    int64_t K = 0;
+    int nch = 0, nb = 0;
+};
+
+template <int D>
+WPlan make_wplan(pssgp_model* m, int64_t n) {
+    using namespace pssgp::wide;
+    wide_set_smem_attrs<D>(m->device);
+    if (m->wocc == 0) {
+        int a = 0, b = 0, c = 0;
+        // (the lane-per-row fold of D <= 8 is not part of the plan's occupancy: it is register-
+        // capped at PSSGP_WLPR_MINB CTAs/SM and simply runs the same grid)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, kw_filter_fold<D>, 32 * kWWarps, sizeof(K1Smem<D>));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kw_filter_apply<D>, 32 * kWWarps, sizeof(K3Smem<D>));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, kw_smoother_apply<D>, 32 * kWWarps, sizeof(K5Smem<D>));
+        m->wocc = std::max(1, std::min(a, std::min(b, c)));
+        if constexpr (D <= kGL) {
+            int l1 = 0, l5 = 0, l3 = 0;
+            if (m->mode == kPade) {   // per-step (F, Q) variants (their staging buffers cost shared memory)
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l1, kw_filter_fold_lpr<D, true>, 32 * kWWarps, sizeof(K1LSmem<D, true>));
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l3, kw_filter_apply_lpr<D, true>, 32 * kWWarps, sizeof(K3LSmem<D, true>));
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l5, kw_smoother_apply_lpr<D, true>, 32 * kWWarps, sizeof(K5LSmem<D, true>));
+            } else {
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l1, kw_filter_fold_lpr<D, false>, 32 * kWWarps, sizeof(K1LSmem<D, false>));
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l3, kw_filter_apply_lpr<D, false>, 32 * kWWarps, sizeof(K3LSmem<D, false>));
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l5, kw_smoother_apply_lpr<D, false>, 32 * kWWarps, sizeof(K5LSmem<D, false>));
+            }
+            if (wide_lpr_mask() & 16) l5 = std::min(l5, l3);
+            if (getenv("PSSGP_WIDE_DEBUG"))
+                fprintf(stderr, "wide plan D=%d occupancy: fold %d, apply %d, smoother %d, lpr fold %d, lpr smoother %d\n",
+                        D, a, b, c, l1, l5);
+            // bit 3: on the table (uniform-dt) path, where both lane-per-row kernels run, size the
+            // plan so they run in one wave (C3: 13.8 -> 11.7 ms; on the per-step (F, Q) path the
+            // fewer, longer chains slow the shared-memory rescans: 26.2 -> 28.3 ms, so not there)
+            if ((wide_lpr_mask() & 8) && (m->mode != kPade || (wide_lpr_mask() & 32))) m->wocc = std::max(1, std::min(m->wocc, std::min(l1, l5)));
+        }
+    }
+    const int64_t target = static_cast<int64_t>(m->sm_count) * m->wocc * kWWarps;
+    WPlan pl;
+    pl.K = m->forced_K > 0 ? m->forced_K : std::max<int64_t>(16, (n + target - 1) / target);
+    pl.nch = static_cast<int>(std::max<int64_t>(1, (n + pl.K - 1) / pl.K));
+    pl.nb = (pl.nch + kWWarps - 1) / kWWarps;
+    return pl;
+}
+
+template <int D>
+pssgp_status wide_setup(pssgp_model* m, const WPlan& pl, pssgp::wide::WParams& p) {
+    using namespace pssgp::wide;
+    const size_t nch = static_cast<size_t>(pl.nch);
+    const size_t need = (2 * nch * FNW(D) + nch * pl.K * CNW(D) + 2 * nch * SNW(D) + nch + 64) * sizeof(double);
+    if (need > m->ws_bytes) {
+        if (m->ws) cudaFree(m->ws);
+        m->ws = nullptr;
+        m->ws_bytes = 0;
+        if (cudaMalloc(&m->ws, need) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(m, PSSGP_E_NOMEM, "cudaMalloc(workspace) failed");
+        }
+        m->ws_bytes = need;
+    }
+    if (!m->d_model) {
+        std::vector<double> h(MODW(D), 0.0);
+        for (int i = 0; i < D * D; ++i) {
+            h[i] = m->udt > 0.0 ? m->Fu[i] : 0.0;
+            h[D * D + i] = m->udt > 0.0 ? m->Qu[i] : 0.0;
+            h[2 * D * D + i] = static_cast<double>(m->ssm.Pinf[i]);
+        }
+        for (int i = 0; i < D; ++i) h[3 * D * D + i] = static_cast<double>(m->ssm.H[i]);
+        h[3 * D * D + D] = m->r;
+        h[3 * D * D + D + 1] = m->udt > 0.0 ? m->udt : -1.0;
+        for (int i = 0; i < D * D; ++i) h[3 * D * D + D + 2 + i] = static_cast<double>(m->ssm.G[i]);
+        for (int i = 0; i < D * D; ++i) h[4 * D * D + D + 2 + i] = static_cast<double>(m->ssm.W[i]);
+        if (cudaMalloc(&m->d_model, h.size() * sizeof(double)) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(m, PSSGP_E_NOMEM, "cudaMalloc(model)");
+        }
+        cudaMemcpy(m->d_model, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice);
+    }
+    std::memset(&p, 0, sizeof(p));
+    double* w = reinterpret_cast<double*>(m->ws);
+    p.fagg = w; w += nch * FNW(D);
+    p.fbuf = w; w += nch * FNW(D);
+    p.xp = w; w += nch * pl.K * CNW(D);
+    p.sagg = w; w += nch * SNW(D);
+    p.sbuf = w; w += nch * SNW(D);
+    p.nll_chain = w;
+    p.K = pl.K;
+    p.nch = pl.nch;
+    p.model = m->d_model;
+    p.err = m->d_err;
+    p.rank = 0;
+    p.world = 1;
+    p.store_state = 1;
+    return PSSGP_OK;
+}
+
+// kPade mode (no closed form, no uniform step): per-step (F, Q) for local steps
+// [0, n] (step n = the successor read by the smoother when it exists globally)
+template <int D>
+pssgp_status wide_prepare(pssgp_model* m, pssgp::wide::WParams& p, cudaStream_t s) {
+    using namespace pssgp::wide;
+    p.fq = nullptr;
+    if (m->mode != kPade || p.n == 0) return PSSGP_OK;
+    const int64_t nfq = p.n + ((p.k0 + p.n < p.nglob) ? 1 : 0);
+    const size_t need = static_cast<size_t>(nfq) * FQW(D) * sizeof(double);
+    if (need > m->fq_bytes) {
+        if (m->fq) cudaFree(m->fq);
+        m->fq = nullptr;
+        m->fq_bytes = 0;
+        if (cudaMalloc(&m->fq, need) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(m, PSSGP_E_NOMEM, "cudaMalloc(per-step F, Q) failed");
+        }
+        m->fq_bytes = need;
+    }
+    if constexpr (D <= kGL) {
+        if (wide_lpr_mask() & 64) {   // lane-per-row discretisation: one step per 8-lane group
+            int occ = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kw_discretize_lpr<D>, 32 * kWWarps, 0);
+            const int64_t want = (nfq * kGL + 32 * kWWarps - 1) / (32 * kWWarps);
+            const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(m->sm_count) * std::max(1, occ))));
+            {
+                ProfScope ps(m, S_DISC, s);
+                kw_discretize_lpr<D><<<grid, 32 * kWWarps, 0, s>>>(p.t, nfq, p.k0, m->d_model, m->fq);
+                LAUNCH_CHECK(m, "kw_discretize_lpr");
+            }
+            p.fq = m->fq;
+            return PSSGP_OK;
+        }
+    }
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kw_discretize<D>, 32 * kWWarps, sizeof(KDSmem<D>));
+    const int64_t want = (nfq + kWWarps - 1) / kWWarps;
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(m->sm_count) * std::max(1, occ))));
+    {
+        ProfScope ps(m, S_DISC, s);
+        kw_discretize<D><<<grid, 32 * kWWarps, sizeof(KDSmem<D>), s>>>(p.t, nfq, p.k0, m->d_model, m->fq, p.err);
+        LAUNCH_CHECK(m, "kw_discretize");
+    }
+    p.fq = m->fq;
+    return PSSGP_OK;
+}
+
+// One step of kw_discretize on the device (pssgp_debug_discretize for kPade wide models).
+template <int D>
+pssgp_status wide_debug_discretize(pssgp_model* m, double dt, double* F, double* Q) {
+    using namespace pssgp::wide;
+    pssgp_status st = ensure_device(m);
+    if (st) return st;
+    WParams p;
+    if ((st = wide_setup<D>(m, make_wplan<D>(m, 2), p))) return st;
+    double* tbuf = nullptr;
+    if (cudaMalloc(&tbuf, 2 * sizeof(double) + 2 * FQW(D) * sizeof(double)) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(m, PSSGP_E_NOMEM, "cudaMalloc(debug discretize)");
+    }
+    double* fq = tbuf + 2;
+    const double th[2] = {0.0, dt};
+    cudaMemcpy(tbuf, th, sizeof(th), cudaMemcpyHostToDevice);
+    // the same kernel wide_prepare launches for this model (lane-per-row for D <= 8 by default)
+    bool lpr = false;
+    if constexpr (D <= kGL) lpr = (wide_lpr_mask() & 64) != 0;
+    if constexpr (D <= kGL) {
+        if (lpr) kw_discretize_lpr<D><<<1, 32 * kWWarps>>>(tbuf, 2, 0, m->d_model, fq);
+    }
+    if (!lpr) {
+        cudaFuncSetAttribute(kw_discretize<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(KDSmem<D>));
+        kw_discretize<D><<<1, 32 * kWWarps, sizeof(KDSmem<D>)>>>(tbuf, 2, 0, m->d_model, fq, m->d_err);
+    }
+    std::vector<double> h(FQW(D));
+    cudaError_t e = cudaMemcpy(h.data(), fq + FQW(D), FQW(D) * sizeof(double), cudaMemcpyDeviceToHost);
+    cudaFree(tbuf);
+    if (e != cudaSuccess) return cuda_fail(m, e, "debug discretize");
+    for (int i = 0; i < D; ++i)
+        for (int j = 0; j < D; ++j) {
+            F[i * D + j] = h[i * LD(D) + j];
+            Q[i * D + j] = h[(D + i) * LD(D) + j];
+        }
+    return PSSGP_OK;
+}
+
+// Kogge-Stone levels with ping-pong buffers; returns the buffer holding the inclusive scan
+template <int D>
+double* wide_scan_f(pssgp_model* m, pssgp::wide::WParams& p, cudaStream_t s, pssgp_status& st) {
+    using namespace pssgp::wide;
+    ProfScope ps(m, S_K2, s);
+    double* in = p.fagg;
+    double* out = p.fbuf;
+    for (int off = 1; off < p.nch; off <<= 1) {
+        kw_scan_filter<D><<<p.nch, 32, sizeof(ScanSmemF<D>), s>>>(in, out, p.nch, off, p.err);
+        std::swap(in, out);
+    }
+    cudaError_t e = cudaGetLastError();
+    st = (e == cudaSuccess) ? PSSGP_OK : cuda_fail(m, e, "kw_scan_filter");
+    return in;
+}
+
+template <int D>
+double* wide_scan_s(pssgp_model* m, pssgp::wide::WParams& p, cudaStream_t s, pssgp_status& st) {
+    using namespace pssgp::wide;
+    ProfScope ps(m, S_K4, s);
+    double* in = p.sagg;
+    double* out = p.sbuf;
+    for (int off = 1; off < p.nch; off <<= 1) {
+        kw_scan_smoother<D><<<p.nch, 32, sizeof(ScanSmemS<D>), s>>>(in, out, p.nch, off);
+        std::swap(in, out);
+    }
+    cudaError_t e = cudaGetLastError();
+    st = (e == cudaSuccess) ? PSSGP_OK : cuda_fail(m, e, "kw_scan_smoother");
+    return in;
+}
+
+template <int D>
+pssgp_status wide_fold(pssgp_model* m, pssgp::wide::WParams& p, int nb, cudaStream_t s) {
+    using namespace pssgp::wide;
+    ProfScope ps(m, S_K1, s);
+    if constexpr (D <= kGL) {
+        // lane-per-row fold (D <= 8); PSSGP_WIDE_LPR=0 selects the shared-memory fold (A/B runs)
+        if (wide_lpr_mask() & 1) {
+            if (p.fq) kw_filter_fold_lpr<D, true><<<nb, 32 * kWWarps, sizeof(K1LSmem<D, true>), s>>>(p);
+            else kw_filter_fold_lpr<D, false><<<nb, 32 * kWWarps, sizeof(K1LSmem<D, false>), s>>>(p);
+            LAUNCH_CHECK(m, "kw_filter_fold_lpr");
+            return PSSGP_OK;
+        }
+    }
+    kw_filter_fold<D><<<nb, 32 * kWWarps, sizeof(K1Smem<D>), s>>>(p);
+    LAUNCH_CHECK(m, "kw_filter_fold");
+    return PSSGP_OK;
+}
+
+template <int D>
+pssgp_status wide_fapply(pssgp_model* m, pssgp::wide::WParams& p, int nb, cudaStream_t s) {
+    using namespace pssgp::wide;
+    ProfScope ps(m, S_K3, s);
+    if constexpr (D <= kGL) {
+        // bit 4: lane-per-row Kalman rescan (uniform dt unless bit 2)
+        if ((wide_lpr_mask() & 16) && (!p.fq || (wide_lpr_mask() & 4))) {
+            if (p.fq) kw_filter_apply_lpr<D, true><<<nb, 32 * kWWarps, sizeof(K3LSmem<D, true>), s>>>(p);
+            else kw_filter_apply_lpr<D, false><<<nb, 32 * kWWarps, sizeof(K3LSmem<D, false>), s>>>(p);
+            LAUNCH_CHECK(m, "kw_filter_apply_lpr");
+            return PSSGP_OK;
+        }
+    }
+    kw_filter_apply<D><<<nb, 32 * kWWarps, sizeof(K3Smem<D>), s>>>(p);
+    LAUNCH_CHECK(m, "kw_filter_apply");
+    return PSSGP_OK;
+}
+
+template <int D>
+pssgp_status wide_sapply(pssgp_model* m, pssgp::wide::WParams& p, int nb, cudaStream_t s) {
+    using namespace pssgp::wide;
+    ProfScope ps(m, S_K5, s);
+    if constexpr (D <= kGL) {
+        // uniform dt only by default: with per-step (F, Q) read from global memory it measured
+        // slower than the shared-memory kernel (C3 irregular K5w 8.4 -> 11.3 ms); bit 2 forces it
+        if ((wide_lpr_mask() & 2) && (!p.fq || (wide_lpr_mask() & 4))) {
+            if (p.fq) kw_smoother_apply_lpr<D, true><<<nb, 32 * kWWarps, sizeof(K5LSmem<D, true>), s>>>(p);
+            else kw_smoother_apply_lpr<D, false><<<nb, 32 * kWWarps, sizeof(K5LSmem<D, false>), s>>>(p);
+            LAUNCH_CHECK(m, "kw_smoother_apply_lpr");
+            return PSSGP_OK;
+        }
+    }
+    kw_smoother_apply<D><<<nb, 32 * kWWarps, sizeof(K5Smem<D>), s>>>(p);
+    LAUNCH_CHECK(m, "kw_smoother_apply");
+    return PSSGP_OK;
+}
+
+template <int D>
+pssgp_status wide_posterior(pssgp_model* m, int64_t N, const double* t, const double* y, const uint8_t* mask,
+                            double* mean, double* var, double* nll, cudaStream_t s, bool smooth) {
+    if (N == 0) {
+        if (nll && cudaMemsetAsync(nll, 0, sizeof(double), s) != cudaSuccess) return fail(m, PSSGP_E_CUDA, "memset");
+        return PSSGP_OK;
+    }
+    const WPlan pl = make_wplan<D>(m, N);
+    pssgp::wide::WParams p;
+    pssgp_status st = wide_setup<D>(m, pl, p);
+    if (st) return st;
+    p.t = t; p.y = y; p.mask = mask;
+    p.n = N; p.k0 = 0; p.nglob = N;
+    p.mean = mean; p.var = var;
+    p.store_state = smooth ? 1 : 0;
+    if ((st = wide_prepare<D>(m, p, s))) return st;
+    if ((st = wide_fold<D>(m, p, pl.nb, s))) return st;
+    p.fagg = wide_scan_f<D>(m, p, s, st);
+    if (st) return st;
+    if ((st = wide_fapply<D>(m, p, pl.nb, s))) return st;
+    if (smooth) {
+        p.sagg = wide_scan_s<D>(m, p, s, st);
+        if (st) return st;
+        p.nll_out = nullptr;   // summed by k_nll_sum as on the NLL-only path: bit-identical NLL
+        if ((st = wide_sapply<D>(m, p, pl.nb, s))) return st;
+    }
+    if (nll) return nll_sum(m, p.nll_chain, p.nch, nll, s);
+    return PSSGP_OK;
+}
+
+// ---- sharded wide phases
+template <int D>
+pssgp_status wide_shard_reduce(pssgp_model* m, int64_t k0, int64_t n, int64_t Ng, const double* t, const double* y,
+                               const uint8_t* mask, void* out, cudaStream_t s) {
+    const WPlan pl = make_wplan<D>(m, n);
+    pssgp::wide::WParams p;
+    pssgp_status st = wide_setup<D>(m, pl, p);
+    if (st) return st;
+    p.t = t; p.y = y; p.mask = mask; p.n = n; p.k0 = k0; p.nglob = Ng;
+    if ((st = wide_prepare<D>(m, p, s))) return st;
+    if ((st = wide_fold<D>(m, p, pl.nb, s))) return st;
+    double* inc = wide_scan_f<D>(m, p, s, st);
+    if (st) return st;
+    const cudaError_t e = cudaMemcpyAsync(out, inc + static_cast<int64_t>(pl.nch - 1) * pssgp::wide::FNW(D),
+                                          pssgp::wide::FNW(D) * sizeof(double), cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(m, e, "cudaMemcpyAsync(chunk aggregate)");
+    return PSSGP_OK;
+}
+
+inline int ks_levels(int nch) {
+    int l = 0;
+    for (int off = 1; off < nch; off <<= 1) ++l;
+    return l;
+}
+
+template <int D>
+pssgp_status wide_shard_fapply(pssgp_model* m, int64_t k0, int64_t n, int64_t Ng, const double* t, const double* y,
+                               const uint8_t* mask, const void* all, int rank, int world, void* sout, double* nllp,
+                               cudaStream_t s) {
+    const WPlan pl = make_wplan<D>(m, n);
+    pssgp::wide::WParams p;
+    pssgp_status st = wide_setup<D>(m, pl, p);
+    if (st) return st;
+    p.t = t; p.y = y; p.mask = mask; p.n = n; p.k0 = k0; p.nglob = Ng;
+    p.in_filt = static_cast<const double*>(all);
+    p.rank = rank; p.world = world;
+    if (ks_levels(pl.nch) & 1) p.fagg = p.fbuf;          // where the reduce phase left the scan
+    if ((st = wide_prepare<D>(m, p, s))) return st;
+    if ((st = wide_fapply<D>(m, p, pl.nb, s))) return st;
+    // the chunk's NLL partial travels in the smoother blob, after the aggregate
+    double* blob = static_cast<double*>(sout);
+    if ((st = nll_sum(m, p.nll_chain, p.nch, blob + pssgp::wide::SNW(D), s))) return st;
+    if (nllp && (st = nll_sum(m, p.nll_chain, p.nch, nllp, s))) return st;
+    double* inc = wide_scan_s<D>(m, p, s, st);
+    if (st) return st;
+    const cudaError_t e = cudaMemcpyAsync(sout, inc, pssgp::wide::SNW(D) * sizeof(double), cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(m, e, "cudaMemcpyAsync(chunk smoother aggregate)");
+    return PSSGP_OK;
+}
+
+template <int D>
+pssgp_status wide_shard_sapply(pssgp_model* m, int64_t k0, int64_t n, int64_t Ng, const double* t, const void* all,
+                               int rank, int world, double* mean, double* var, double* nll, cudaStream_t s) {
+    const WPlan pl = make_wplan<D>(m, n);
+    pssgp::wide::WParams p;
+    pssgp_status st = wide_setup<D>(m, pl, p);
+    if (st) return st;
+    p.t = t; p.n = n; p.k0 = k0; p.nglob = Ng;
+    p.in_smooth = static_cast<const double*>(all);
+    p.rank = rank; p.world = world;
+    p.mean = mean; p.var = var;
+    if (ks_levels(pl.nch) & 1) p.sagg = p.sbuf;
+    if ((st = wide_prepare<D>(m, p, s))) return st;
+    if ((st = wide_sapply<D>(m, p, pl.nb, s))) return st;
+    // total NLL: fixed-order sum over ranks of the partials carried in the gathered blobs
+    if (nll) return nll_sum(m, static_cast<const double*>(all) + pssgp::wide::SNW(D), world, nll, s,
+                            pssgp::wide::SNW(D) + 1);
+    return PSSGP_OK;
+}
+
+}  // namespace widehost
+}  // namespace pssgp_internal

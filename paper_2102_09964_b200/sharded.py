@@ -8,12 +8,14 @@ the global grid.  The exchange is the paper's associativity (PAPER.md:326,
                      (A, b, C, eta, J)                       -> all_gather
   2. filter apply  : rank g applies the ordered product of aggregates 0..g-1
                      (a collapsed global prefix, A = 0 after rank 0's element
-                     with A_1 = 0, Eq. (7)), runs the Kalman rescan, emits its
-                     smoother aggregate (E, g, L) and NLL partial -> all_gather
+                     with A_1 = 0, Eq. (7)), runs the Kalman rescan, emits ONE
+                     smoother blob = its smoother aggregate (E, g, L) followed by
+                     its NLL partial                        -> all_gather
   3. smoother apply: rank g applies the ordered product of smoother aggregates
-                     g+1..G-1 (collapsed global suffix), runs the RTS rescan.
-  NLL = fixed-order sum of the gathered partials (deterministic); the partials travel in the
-  same all_gather as the smoother aggregates (two collectives per posterior).
+                     g+1..G-1 (collapsed global suffix), runs the RTS rescan; the
+                     library forms the total NLL as the fixed-order sum of the
+                     gathered partials (deterministic, identical on every rank).
+  Two collectives per posterior; the binding does no arithmetic.
 
 The collectives carry a few hundred bytes (27 + 18 + 1 doubles at d = 3), so
 they are latency-bound; NCCL over NVLink/NVSwitch through torch.distributed.
@@ -45,24 +47,16 @@ def split(N: int, world: int) -> List[Tuple[int, int]]:
 def sharded_posterior(backend, exchange: Callable, rank: int, world: int):
     """Backend-agnostic 3-phase protocol.
 
-    backend.filter_reduce() -> agg ; backend.filter_apply(all_aggs) -> (sagg, nll_part)
-    backend.smoother_apply(all_saggs) -> (mean, var) ; exchange(x) -> stacked [world, ...]
+    backend.filter_reduce() -> filter aggregate blob
+    backend.filter_apply(all_filter_blobs) -> smoother blob (aggregate + NLL partial)
+    backend.smoother_apply(all_smoother_blobs) -> (mean, var, total NLL)
+    exchange(x) -> stacked [world, ...] in rank order
     """
     fa = backend.filter_reduce()
     all_fa = exchange(fa)
-    sa, nll_part = backend.filter_apply(all_fa)
-    # one collective carries both the smoother aggregate and the NLL partial
-    ns = sa.numel()
-    all_msg = exchange(_cat(sa.reshape(-1), nll_part.reshape(-1)))
-    all_sa = all_msg[:, :ns].contiguous()
-    all_nll = all_msg[:, ns:].contiguous()
-    mean, var = backend.smoother_apply(all_sa)
-    return mean, var, all_nll
-
-
-def _cat(a, b):
-    import torch
-    return torch.cat([a, b])
+    sb = backend.filter_apply(all_fa)
+    all_sb = exchange(sb)
+    return backend.smoother_apply(all_sb)
 
 
 class DeviceShard:
@@ -78,8 +72,8 @@ class DeviceShard:
         self.fbytes = pssgp_aggregate_bytes(model.h, 0)
         self.sbytes = pssgp_aggregate_bytes(model.h, 1)
         self.fagg = torch.zeros(self.fbytes // 8, dtype=torch.float64, device=dev)
-        self.sagg = torch.zeros(self.sbytes // 8, dtype=torch.float64, device=dev)
-        self.nll = torch.zeros(1, dtype=torch.float64, device=dev)
+        self.sagg = torch.zeros(self.sbytes // 8, dtype=torch.float64, device=dev)   # aggregate + NLL partial
+        self.nll = torch.zeros(1, dtype=torch.float64, device=dev)                    # total NLL (all ranks)
         self.mean = torch.empty(n, dtype=torch.float64, device=dev)
         self.var = torch.empty(n, dtype=torch.float64, device=dev)
 
@@ -94,14 +88,14 @@ class DeviceShard:
     def filter_apply(self, all_fa):
         pssgp_shard_filter_apply(self.m.h, self.k0, self.n, self.N, self._tp(), int(self.y.data_ptr()),
                                  int(self.mask.data_ptr()), int(all_fa.data_ptr()), self.rank, self.world,
-                                 int(self.sagg.data_ptr()), int(self.nll.data_ptr()), self.stream)
-        return self.sagg, self.nll
+                                 int(self.sagg.data_ptr()), None, self.stream)
+        return self.sagg
 
-    def smoother_apply(self, all_sa):
-        pssgp_shard_smoother_apply(self.m.h, self.k0, self.n, self.N, self._tp(), int(all_sa.data_ptr()),
+    def smoother_apply(self, all_sb):
+        pssgp_shard_smoother_apply(self.m.h, self.k0, self.n, self.N, self._tp(), int(all_sb.data_ptr()),
                                    self.rank, self.world, int(self.mean.data_ptr()), int(self.var.data_ptr()),
-                                   self.stream)
-        return self.mean, self.var
+                                   int(self.nll.data_ptr()), self.stream)
+        return self.mean, self.var, self.nll
 
 
 def torch_exchange(x):
@@ -147,12 +141,12 @@ def run_virtual(components: Sequence, noise_var: float, t: np.ndarray, y: np.nda
         tt, yy, mm = chunk_inputs(t, y, mask, k0, n, device)
         shards.append(DeviceShard(m, tt, yy, mm, k0, n, N, g, world))
     fa = torch.stack([s.filter_reduce().clone() for s in shards])
-    outs = [s.filter_apply(fa) for s in shards]
-    sa = torch.stack([o[0].clone() for o in outs])
-    nll = sum(float(o[1].cpu()[0]) for o in outs)
-    res = [s.smoother_apply(sa) for s in shards]
+    sb = torch.stack([s.filter_apply(fa).clone() for s in shards])
+    res = [s.smoother_apply(sb) for s in shards]
     for s in shards:
         s.m.check()
     mean = torch.cat([r[0] for r in res]).cpu().numpy()
     var = torch.cat([r[1] for r in res]).cpu().numpy()
-    return mean, var, nll
+    nlls = [float(r[2].cpu()[0]) for r in res]
+    assert all(v == nlls[0] for v in nlls), "total NLL differs between ranks"
+    return mean, var, nlls[0]

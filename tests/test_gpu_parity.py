@@ -233,6 +233,28 @@ def test_wide_sums(cuda_device, comps, dt):
     assert_parity(w)
 
 
+# every compiled state dimension of the warp-per-chain path (pssgp_dims.h: d = 4 ... 20; north_star
+# "d = 2..~20"): the odd ones added in round 2 on uniform and jittered grids
+_ODD_D = {
+    7: [synth.Component("rbf", 1.0, 0.6, order=7)],
+    9: [synth.Component("periodic", 1.0, 1.0, period=0.5, order=3), synth.Component("matern12", 0.5, 2.0)],
+    11: [synth.Component("periodic", 1.0, 1.0, period=0.5, order=4), synth.Component("matern12", 0.5, 2.0)],
+    13: [synth.Component("periodic", 1.0, 1.0, period=0.5, order=5), synth.Component("matern12", 0.5, 2.0)],
+    15: [synth.Component("periodic", 1.0, 1.0, period=0.5, order=6), synth.Component("matern12", 0.5, 2.0)],
+    17: [synth.Component("periodic", 1.0, 1.0, period=0.5, order=7), synth.Component("matern12", 0.5, 2.0)],
+    19: [synth.Component("periodic", 1.0, 1.0, period=0.5, order=8), synth.Component("matern12", 0.5, 2.0)],
+}
+
+
+@pytest.mark.parametrize("d", sorted(_ODD_D))
+def test_wide_odd_state_dims(cuda_device, d):
+    w = _uniform(_ODD_D[d], 0.05, 2501, 0.01, p_missing=0.25, seed=d)
+    m = assert_parity(w)
+    assert m.state_dim == d
+    wi = _irregular(_ODD_D[d], 0.05, 1201, seed=d)
+    assert_parity(wi)
+
+
 def test_wide_ties_and_small_chains(cuda_device):
     w = _uniform([synth.Component("rbf", 1.0, 0.8, order=4)], 0.02, 5003, 0.01, p_missing=0.25, seed=5)
     w.t[100:103] = w.t[100]           # exact ties (dt = 0)

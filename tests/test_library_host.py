@@ -82,8 +82,13 @@ def test_rbf_and_sum_models():
     assert np.max(np.abs(F - Fo)) < 1e-13 and np.max(np.abs(Q - Qo)) < 1e-13 * np.max(np.abs(Qo))
     with pytest.raises(P.PssgpError):
         m.discretize(0.5 / 52)                            # irregular dt: no device discretisation
-    with pytest.raises(P.PssgpError):                     # d = 7 is not compiled
-        P.Model([synth.Component("rbf", 1.0, 0.5, order=7)], 0.1, uniform_dt=0.01)
+    # every d = 4 ... 20 is compiled (north_star "d = 2..~20"); d = 22 is not
+    for order in (7, 9, 11):
+        assert P.Model([synth.Component("rbf", 1.0, 0.5, order=order)], 0.1, uniform_dt=0.01).state_dim == order
+    assert P.Model([synth.Component("periodic", 1.0, 1.0, period=1.0, order=6),
+                    synth.Component("matern12", 1.0, 1.0)], 0.1).state_dim == 15
+    with pytest.raises(P.PssgpError):
+        P.Model([synth.Component("periodic", 1.0, 1.0, period=1.0, order=10)], 0.1, uniform_dt=0.01)
 
 
 @pytest.mark.parametrize("kind", ["matern12", "matern32", "matern52"])
@@ -126,10 +131,10 @@ def test_irregular_dt_unsupported_for_non_matern():
 def test_aggregate_bytes():
     m = P.Model([synth.Component("matern52", 1.0, 0.5)], 0.1)
     assert P.pssgp_aggregate_bytes(m.h, 0) == 27 * 8
-    assert P.pssgp_aggregate_bytes(m.h, 1) == 18 * 8
+    assert P.pssgp_aggregate_bytes(m.h, 1) == (18 + 1) * 8            # smoother aggregate + NLL partial
     m = P.Model([synth.Component("rbf", 1.0, 0.5, order=6)], 0.1, uniform_dt=0.01)
     assert P.pssgp_aggregate_bytes(m.h, 0) == (3 * 36 + 12) * 8     # wide path: full matrices
-    assert P.pssgp_aggregate_bytes(m.h, 1) == (2 * 36 + 6) * 8
+    assert P.pssgp_aggregate_bytes(m.h, 1) == (2 * 36 + 6 + 1) * 8
 
 
 def test_quasiperiodic_model_matches_oracle():

@@ -132,6 +132,18 @@ def test_rbf_reconstruction_and_coefficients():
     assert abs(m.q - 115505.43) < 0.05
 
 
+def test_rbf_spectral_factor_vs_mpmath_golden():
+    """The oracle's fp64 spectral factor (numpy.roots) and q against the 50-digit construction of
+    reading Z7 written independently by tools/gen_rbf_pins.py (tests/golden/rbf_taylor_pins.json)."""
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "rbf_taylor_pins.json")))
+    for c in gold["cases"]:
+        m = ssm.rbf_taylor(c["order"], c["variance"], c["lengthscale"])
+        a = -m.G[-1, :][::-1]                       # companion last row = -(a_0 .. a_{n-1}), low to high
+        ref = np.array([float(x) for x in c["a_monic_high_to_low"][1:]])
+        np.testing.assert_allclose(a, ref, rtol=1e-11)
+        assert abs(m.q - float(c["q"])) <= 1e-13 * float(c["q"])
+
+
 def test_periodic_reconstruction():
     """Periodic J=6, ell=1: Bessel construction error ~1.3e-6."""
     comp = synth.Component("periodic", 1.0, 1.0, period=1.0, order=6)

@@ -1,7 +1,8 @@
 """Multi-process (world_size 2 and 3, gloo on CPU) test of the time-sharded
 protocol in paper_2102_09964_b200/sharded.py: the exchange order (filter
 aggregates of ranks < g, smoother aggregates of ranks > g), the one-point
-halo of t, the global first / terminal elements and the NLL partial sum.
+halo of t, the global first / terminal elements and the NLL partials carried
+in the smoother blobs.
 
 The per-rank backend here is a MOCK built from the oracle's element algebra
 (oracle/elements.py) — it exercises the protocol and the
@@ -123,13 +124,14 @@ class OracleShard:
         agg = se[0]
         for e in se[1:]:
             agg = el.smoother_combine(agg, e)
-        return self._flat(agg), torch.tensor([nll], dtype=torch.float64)
+        # one blob: the smoother aggregate followed by the NLL partial (as the library's)
+        return torch.cat([self._flat(agg), torch.tensor([nll], dtype=torch.float64)])
 
-    def smoother_apply(self, all_sa):
-        world = all_sa.shape[0]
+    def smoother_apply(self, all_sb):
+        world = all_sb.shape[0]
         carry = None
         for g in range(world - 1, self.rank, -1):
-            a = self._unflat_s(all_sa[g])
+            a = self._unflat_s(all_sb[g][:-1])
             carry = a if carry is None else el.smoother_combine(a, carry)
         acc = carry
         means = np.empty(self.n); vars_ = np.empty(self.n)
@@ -137,7 +139,10 @@ class OracleShard:
             acc = self.se[i] if acc is None else el.smoother_combine(self.se[i], acc)
             means[i] = self.m.H @ acc[1]
             vars_[i] = self.m.H @ acc[2] @ self.m.H
-        return torch.from_numpy(means), torch.from_numpy(vars_)
+        nll = 0.0
+        for g in range(world):                       # fixed-order sum of the gathered partials
+            nll += float(all_sb[g][-1])
+        return torch.from_numpy(means), torch.from_numpy(vars_), torch.tensor([nll], dtype=torch.float64)
 
 
 def _worker(rank, world, port, seed, q):
@@ -151,8 +156,8 @@ def _worker(rank, world, port, seed, q):
         k0, n = sharded.split(w.N, world)[rank]
         be = OracleShard(m, w.noise_var, w.t, w.y, w.mask, k0, n, w.N)
         be.rank = rank
-        mean, var, all_nll = sharded.sharded_posterior(be, sharded.torch_exchange, rank, world)
-        q.put((rank, k0, mean.numpy(), var.numpy(), all_nll.numpy().ravel()))
+        mean, var, nll = sharded.sharded_posterior(be, sharded.torch_exchange, rank, world)
+        q.put((rank, k0, mean.numpy(), var.numpy(), float(nll[0])))
     finally:
         dist.destroy_process_group()
 
@@ -173,8 +178,8 @@ def test_sharded_protocol_gloo(world):
     w = synth.random_problem(17, 301, kind="matern52", p_missing=0.25, ties=2)
     o = oracle.posterior(w)
     mean = np.concatenate([r[2] for r in res]); var = np.concatenate([r[3] for r in res])
-    nll = float(np.sum(res[0][4]))
-    assert all(np.array_equal(r[4], res[0][4]) for r in res)       # every rank sees the same partials
+    nll = res[0][4]
+    assert all(r[4] == nll for r in res)                            # every rank forms the same total
     assert np.max(np.abs(mean - o["mean"])) / np.max(np.abs(o["mean"])) < 1e-9
     assert np.max(np.abs(var - o["var"]) / o["var"]) < 1e-9
     assert abs(nll - o["nll"]) < 1e-9 * abs(o["nll"])

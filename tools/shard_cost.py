@@ -24,7 +24,7 @@ for G in (1, 2, 4, 8):
     all_fa = torch.stack([fa.clone() for _ in range(G)])
     all_fa[:rank] = 0.0
     all_fa[:rank, 0::4] = 0.0
-    sa, nl = sh.filter_apply(all_fa)
+    sa = sh.filter_apply(all_fa)
     all_sa = torch.stack([sa.clone() for _ in range(G)])
     torch.cuda.synchronize()
     e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
