@@ -55,6 +55,8 @@ struct WParams {
     unsigned long long* err;
     int store_state;
     const double* fq;           // per-step (F, Q) [n(+1)][FQW] from kw_discretize (irregular dt), else NULL
+    double* qagg;               // [nch][kQ-1][FNW] quarter prefix filter aggregates (lane-per-row fold, D <= 8)
+    double* sqagg;              // [nch][kQ-1][SNW] smoother aggregates of quarters 1..3 (quarter Kalman rescan)
 };
 
 // ------------------------------------------------------------------ shared-memory model
@@ -1189,6 +1191,9 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_filter_fold_
     bool ok = true;
 #pragma unroll 1
     for (int i = 1; i < kQ; ++i) {
+        // W.q[i - 1] is the prefix q0 (x) ... (x) q_{i-1}: the quarter rescans start from the
+        // chain carry applied to it (kw_filter_apply_q)
+        if (p.qagg) gstore<D>(W.q[i - 1], p.qagg + (static_cast<int64_t>(c) * (kQ - 1) + (i - 1)) * FNW(D), lane);
         ok = wcombine<D>(W.q[i - 1], W.q[i], W.q[i], W.s, lane) && ok;
         __syncwarp();
     }
@@ -2064,6 +2069,592 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_smoother_app
         }
     }
     if (bad && lane == 0) raise_error(p.err, p.k0 + kb, kErrNumeric);
+}
+
+
+// ================================================================== quarter-parallel rescans (D <= 8)
+// The fold (kw_filter_fold_lpr) splits every chain into kQ = 4 quarters [qb, qe) (the split below,
+// identical in all three kernels) and stores the quarter PREFIX aggregates q0, q0 (x) q1,
+// q0 (x) q1 (x) q2 (p.qagg).  The rescans then run the four quarters of a chain at once, one per
+// 8-lane group (lane r of a group owns row r of every matrix, as in the lane-per-row kernels),
+// from per-quarter carries: the filtered state entering quarter q is the chain carry applied to
+// the prefix aggregate of quarters < q (any grouping of the scan), and the
+// smoothed state after quarter q is the chain's suffix carry applied through the smoother
+// aggregates of the later quarters.  All four groups of a warp are busy (the
+// lane-per-row rescans kept one group busy per chain).
+__device__ __forceinline__ void quarter_bounds(int64_t kb, int64_t ke, int64_t K, int q, int64_t& qb, int64_t& qe) {
+    const int64_t Kq = (K + kQ - 1) / kQ;
+    qb = min(kb + q * Kq, ke);
+    qe = min(qb + Kq, ke);
+}
+
+// scratch of a quarter smoother aggregate (the k3w_chain_sagg computation on explicit operands)
+template <int D>
+struct SQScratch {
+    double FP[D][LD(D)], Sm[D][LD(D)], Pm[D][LD(D)], W2[D][2 * D + 1];
+    double xm[D];
+};
+
+// (E, g, L) of the quarter [qb, qe) from its moments at the quarter's last step: filtered (x, P),
+// cross-covariance Sg = Cov(x_qb, x_{qe-1} | y_1:qe-1), entry moments (x0, P0) = E / Cov(x_qb | y_1:qe-1)
+// (DESIGN.md §5 "chain smoother aggregates", reading N1), tprev = t[qe - 1].  Warp-cooperative.
+template <int D>
+__device__ void quarter_sagg(const WParams& p, const SModel<D>& M, const double (*P)[LD(D)], const double* x,
+                             const double (*Sg)[LD(D)], const double (*P0)[LD(D)], const double* x0, int64_t qb,
+                             int64_t qe, double tprev, SS<D>& out, SQScratch<D>& w, int lane) {
+    if (qe <= qb) {
+        set_identity<D>(out, lane);
+        return;
+    }
+    if (p.k0 + qe == p.nglob) {                  // terminal element inside: (0, m^s_qb, P^s_qb) = (0, x0, P0)
+        for (int e = lane; e < D * D; e += 32) {
+            const int i = e / D, j = e - (e / D) * D;
+            out.E[i][j] = 0.0;
+            out.L[i][j] = P0[i][j];
+        }
+        for (int i = lane; i < D; i += 32) out.g[i] = x0[i];
+        __syncwarp();
+        return;
+    }
+    const double tn = __ldg(p.t + qe);
+    const int kind = wdisc_kind(tn - tprev, M.udt, p.fq != nullptr);
+    const FQp<D> fqp = wfq<D>(p, M, qe);
+    for (int e = lane; e < D * D; e += 32) {
+        const int i = e / D, j = e - (e / D) * D;
+        double fp = 0.0, sm = 0.0;
+        if (kind == 0) {
+            for (int q = 0; q < D; ++q) {
+                fp = fma(fqp.F[i][q], P[q][j], fp);
+                sm = fma(Sg[i][q], fqp.F[j][q], sm);
+            }
+        } else {
+            fp = P[i][j];
+            sm = Sg[i][j];
+        }
+        w.FP[i][j] = fp;
+        w.Sm[i][j] = sm;
+    }
+    for (int i = lane; i < D; i += 32) {
+        double s2 = 0.0;
+        if (kind == 0)
+            for (int q = 0; q < D; ++q) s2 = fma(fqp.F[i][q], x[q], s2);
+        else
+            s2 = x[i];
+        w.xm[i] = s2;
+    }
+    __syncwarp();
+    for (int e = lane; e < D * D; e += 32) {
+        const int i = e / D, j = e - (e / D) * D;
+        double s2 = (kind == 0) ? fqp.Q[i][j] : 0.0;
+        if (kind == 0)
+            for (int q = 0; q < D; ++q) s2 = fma(w.FP[i][q], fqp.F[j][q], s2);
+        else
+            s2 = w.FP[i][j];
+        w.Pm[i][j] = s2;
+    }
+    __syncwarp();
+    for (int e = lane; e < D * D; e += 32) w.FP[e / D][e % D] = w.Pm[e / D][e % D];
+    __syncwarp();
+    if (!winverse<D>(w.FP, w.W2, lane) && lane == 0) raise_error(p.err, p.k0 + qe, kErrNumeric);
+    wmm<D>(out.E, w.Sm, w.FP, nullptr, lane);           // E = Sm Pm^-1
+    __syncwarp();
+    for (int i = lane; i < D; i += 32) {
+        double a = x0[i];
+        for (int q = 0; q < D; ++q) a = fma(-out.E[i][q], w.xm[q], a);
+        out.g[i] = a;
+    }
+    for (int e = lane; e < D * D; e += 32) {
+        const int i = e / D, j = e - (e / D) * D;
+        double a = P0[i][j];
+        for (int q = 0; q < D; ++q) a = fma(-out.E[i][q], w.Sm[j][q], a);
+        w.Pm[i][j] = a;
+    }
+    __syncwarp();
+    for (int e = lane; e < D * D; e += 32) {
+        const int i = e / D, j = e - (e / D) * D;
+        out.L[i][j] = 0.5 * (w.Pm[i][j] + w.Pm[j][i]);
+    }
+    __syncwarp();
+}
+
+// ------------------------------------------------------------------ K3q: quarter-parallel Kalman rescan
+template <int D, bool STREAM>
+struct K3QSmem {
+    SModel<D> m;
+    double I[D][LD(D)], Z[D][LD(D)];
+    struct PerWarp {
+        double cx[kQ][D];                          // filtered state entering each quarter
+        double cP[kQ][D][LD(D)];
+        union {
+            struct {                               // carry phase
+                SF<D> a;
+                SCombF<D> s;
+            } c;
+            struct {                               // step phase, one slot per group
+                double U[kQ][D][LD(D)];
+                double fqs[kQ][2][FQS(D, STREAM)];
+            } st;
+            struct {                               // quarter smoother aggregates, one quarter at a time
+                double P[D][LD(D)], Sg[D][LD(D)], P0[D][LD(D)];
+                double x[D], x0[D];
+                SS<D> acc, cur;
+                SQScratch<D> w;
+                SCombF<D> s;
+            } ag;
+        } u;
+    } w[kWWarps];
+};
+
+template <int D, bool STREAM>
+__global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_filter_apply_q(const WParams p) {
+    static_assert(D <= kGL, "one row per lane of an 8-lane group");
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    K3QSmem<D, STREAM>& sh = *reinterpret_cast<K3QSmem<D, STREAM>*>(smem_raw);
+    load_model<D>(sh.m, p.model);
+    for (int e = threadIdx.x; e < D * D; e += blockDim.x) {
+        const int i = e / D, j = e - (e / D) * D;
+        sh.I[i][j] = (i == j) ? 1.0 : 0.0;
+        sh.Z[i][j] = 0.0;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int c = blockIdx.x * kWWarps + wid;
+    if (c >= p.nch) return;                                     // warp-uniform
+    auto& W = sh.w[wid];
+    const SModel<D>& M = sh.m;
+    const int64_t kb = static_cast<int64_t>(c) * p.K;
+    const int64_t ke = min(kb + p.K, p.n);
+    // ---- carries: the chain's (incoming sharded (x) scanned chains < c), then through the quarter
+    // prefix aggregates of the fold
+    for (int e = lane; e < D * D; e += 32) W.cP[0][e / D][e % D] = 0.0;
+    for (int i = lane; i < D; i += 32) W.cx[0][i] = 0.0;
+    __syncwarp();
+    bool ok = true;
+    for (int g = 0; g < p.rank && p.in_filt; ++g) {
+        gload<D>(W.u.c.a, p.in_filt + static_cast<int64_t>(g) * FNW(D), lane);
+        ok = wapply_prefix<D>(W.cx[0], W.cP[0], W.u.c.a, W.u.c.s, lane) && ok;
+    }
+    if (c > 0) {
+        gload<D>(W.u.c.a, p.fagg + static_cast<int64_t>(c - 1) * FNW(D), lane);
+        ok = wapply_prefix<D>(W.cx[0], W.cP[0], W.u.c.a, W.u.c.s, lane) && ok;
+    }
+    for (int q = 1; q < kQ; ++q) {
+        for (int e = lane; e < D * D; e += 32) W.cP[q][e / D][e % D] = W.cP[0][e / D][e % D];
+        for (int i = lane; i < D; i += 32) W.cx[q][i] = W.cx[0][i];
+        __syncwarp();
+        gload<D>(W.u.c.a, p.qagg + (static_cast<int64_t>(c) * (kQ - 1) + (q - 1)) * FNW(D), lane);
+        ok = wapply_prefix<D>(W.cx[q], W.cP[q], W.u.c.a, W.u.c.s, lane) && ok;
+    }
+    if (!ok && lane == 0) raise_error(p.err, p.k0 + kb, kErrNumeric);
+
+    // ---- the four quarters, one per 8-lane group, in registers
+    const int q = lane / kGL, r0 = lane % kGL, gb = q * kGL;
+    const unsigned gm = 0xFFu << gb;
+    const bool act = r0 < D;
+    const int r = act ? r0 : 0;
+    int64_t qb, qe;
+    quarter_bounds(kb, ke, p.K, q, qb, qe);
+    double Pr[D], Sgr[D], P0r[D], xr = W.cx[q][r], x0r = 0.0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) { Pr[j] = W.cP[q][r][j]; Sgr[j] = 0.0; P0r[j] = 0.0; }
+    const double hr = act ? M.H[r] : 0.0;
+    __syncwarp();                                               // W.u is reused by the step phase
+    double tprev = (qb < qe && (qb > 0 || p.k0 > 0)) ? __ldg(p.t + qb - 1) : 0.0;
+    double quad = 0.0, logs = 0.0;
+    int nobs = 0;
+    bool bad_s = false;
+    int64_t bad_g = 0;
+    double* xpc = p.xp + static_cast<int64_t>(c) * p.K * CNW(D);
+    double tn_ = 0.0, yn_ = 0.0;
+    unsigned char mn_ = 0;
+    if (qb < qe) { tn_ = __ldg(p.t + qb); mn_ = __ldg(p.mask + qb); yn_ = __ldg(p.y + qb); }
+    auto& U = W.u.st.U[q];
+    auto& fqs = W.u.st.fqs[q];
+    if (STREAM) {
+        if (qb < qe)
+            for (int i = r0; i < FQW(D); i += kGL) cp_async8(&fqs[0][i], p.fq + qb * FQW(D) + i, 8);
+        cp_async_commit();
+    }
+    for (int64_t k = qb; k < qe; ++k) {
+        const int fb = static_cast<int>((k - qb) & 1);
+        if (STREAM) {
+            // slot fb holds (F_k, Q_k); slot fb^1 was last read in step k - 1, before its closing sync
+            cp_async_wait<0>();
+            __syncwarp(gm);
+            if (k + 1 < qe)
+                for (int i = r0; i < FQW(D); i += kGL) cp_async8(&fqs[fb ^ 1][i], p.fq + (k + 1) * FQW(D) + i, 8);
+            cp_async_commit();
+        }
+        const double tk = tn_;
+        const bool obs = mn_ != 0;
+        const double yk = obs ? yn_ : 0.0;
+        if (k + 1 < qe) { tn_ = __ldg(p.t + k + 1); mn_ = __ldg(p.mask + k + 1); yn_ = __ldg(p.y + k + 1); }
+        const int64_t g = p.k0 + k;
+        const int kind = (g == 0) ? 3 : wdisc_kind(tk - tprev, M.udt, STREAM);
+        const bool first = (k == qb);
+        tprev = tk;
+        const double* Fp;
+        const double* Qp;
+        if (kind == 0) {
+            if (STREAM) { Fp = &fqs[fb][0]; Qp = Fp + D * LD(D); }
+            else { Fp = &M.F[0][0]; Qp = &M.Q[0][0]; }
+        } else if (kind == 1) {
+            Fp = &sh.I[0][0]; Qp = &sh.Z[0][0];
+        } else {                                     // 3 (and 2, reported by the fold): F = 0, Q = P_inf
+            Fp = &sh.Z[0][0]; Qp = &M.Pinf[0][0];
+        }
+        // column r of F P, xm_r = F[r,:] x, row r of Sm = Sg[r,:] F^T
+        double Uc[D], xm = 0.0;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            double su = 0.0;
+#pragma unroll
+            for (int qq = 0; qq < D; ++qq) su = fma(Fp[i * LD(D) + qq], Pr[qq], su);
+            Uc[i] = su;
+        }
+#pragma unroll
+        for (int qq = 0; qq < D; ++qq) xm = fma(Fp[r * LD(D) + qq], __shfl_sync(gm, xr, qq, kGL), xm);
+        if (act) {
+#pragma unroll
+            for (int i = 0; i < D; ++i) U[i][r] = Uc[i];
+        }
+        __syncwarp(gm);
+        double Pm[D], Sm[D], HP = 0.0, SH = 0.0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            double s2 = Qp[r * LD(D) + j], s3 = 0.0;
+#pragma unroll
+            for (int qq = 0; qq < D; ++qq) {
+                const double f = Fp[j * LD(D) + qq];
+                s2 = fma(U[r][qq], f, s2);
+                s3 = fma(Sgr[qq], f, s3);
+            }
+            Pm[j] = s2;
+            Sm[j] = s3;
+            HP = fma(s2, M.H[j], HP);
+            SH = fma(s3, M.H[j], SH);
+        }
+        __syncwarp(gm);                               // U is rewritten by the next step
+        if (!act) { HP = 0.0; SH = 0.0; }
+        double S = hr * HP, hx = hr * xm;
+#pragma unroll
+        for (int off = kGL / 2; off > 0; off >>= 1) {
+            S += __shfl_xor_sync(gm, S, off);
+            hx += __shfl_xor_sync(gm, hx, off);
+        }
+        S += M.r;
+        if (obs && !(S > 0.0 && S < INFINITY) && !bad_s) { bad_s = true; bad_g = g; }
+        const double iS = obs ? 1.0 / S : 0.0;
+        const double v = obs ? (yk - hx) : 0.0;
+        const double vs = v * iS;
+        const double HPs = HP * iS, SHs = SH * iS;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            const double HPj = __shfl_sync(gm, HP, j, kGL);
+            const double SHj = __shfl_sync(gm, SH, j, kGL);
+            const double Pn = fma(-HPs, HPj, Pm[j]);
+            Pr[j] = Pn;
+            if (first) {
+                P0r[j] = Pn;
+                Sgr[j] = Pn;
+            } else {
+                Sgr[j] = fma(-SHs, HPj, Sm[j]);
+                P0r[j] = fma(-SHs, SHj, P0r[j]);
+            }
+        }
+        xr = fma(HP, vs, xm);
+        x0r = first ? xr : fma(SH, vs, x0r);
+        if (obs) {
+            quad = fma(v, vs, quad);
+            logs += log(S);
+            ++nobs;
+        }
+        if (p.store_state && act) {
+            double* o = xpc + (k - kb) * CNW(D);
+            o[r] = xr;
+#pragma unroll
+            for (int j = 0; j < D; ++j)
+                if (j >= r) o[D + si(D, r, j)] = Pr[j];
+        }
+    }
+    __syncwarp();
+    if (bad_s && r0 == 0) raise_error(p.err, bad_g, kErrNumeric);
+    // NLL partial of the chain: the four groups' sums (identical in every lane of a group) in order
+    {
+        double nl = nobs ? 0.5 * (quad + logs + nobs * 1.8378770664093453) : 0.0;
+        double tot = 0.0;
+#pragma unroll
+        for (int qq = 0; qq < kQ; ++qq) tot += __shfl_sync(0xffffffffu, nl, qq * kGL);
+        if (lane == 0) p.nll_chain[c] = tot;
+    }
+    if (!p.store_state) return;
+    // ---- quarter smoother aggregates (E, g, L), combined in time order into the chain's
+    const double tq = tprev;
+    SS<D>* acc = &W.u.ag.acc;
+    SS<D>* cur = &W.u.ag.cur;
+#pragma unroll 1
+    for (int qq = 0; qq < kQ; ++qq) {
+        if (q == qq && act) {
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                W.u.ag.P[r][j] = Pr[j];
+                W.u.ag.Sg[r][j] = Sgr[j];
+                W.u.ag.P0[r][j] = P0r[j];
+            }
+            W.u.ag.x[r] = xr;
+            W.u.ag.x0[r] = x0r;
+        }
+        __syncwarp();
+        int64_t sb, se;
+        quarter_bounds(kb, ke, p.K, qq, sb, se);
+        const double tpq = __shfl_sync(0xffffffffu, tq, qq * kGL);
+        quarter_sagg<D>(p, M, W.u.ag.P, W.u.ag.x, W.u.ag.Sg, W.u.ag.P0, W.u.ag.x0, sb, se, tpq, *cur, W.u.ag.w, lane);
+        if (qq > 0) {
+            gstore<D>(*cur, p.sqagg + (static_cast<int64_t>(c) * (kQ - 1) + (qq - 1)) * SNW(D), lane);
+            __syncwarp();
+            wcombine<D>(*acc, *cur, *cur, W.u.ag.s, lane);   // acc (x) cur, earlier quarter on the left
+        }
+        SS<D>* t = acc; acc = cur; cur = t;
+        __syncwarp();
+    }
+    gstore<D>(*acc, p.sagg + static_cast<int64_t>(c) * SNW(D), lane);
+}
+
+// ------------------------------------------------------------------ K5q: quarter-parallel RTS rescan
+template <int D, bool STREAM>
+struct K5QSmem {
+    SModel<D> m;
+    double I[D][LD(D)], Z[D][LD(D)];
+    struct PerWarp {
+        double cm[kQ][D];                          // smoothed state after each quarter
+        double cP[kQ][D][LD(D)];
+        union {
+            struct {                               // carry phase
+                SS<D> a;
+                SSufScratch<D> s;
+            } c;
+            struct Grp {                           // step phase, one slot per group
+                double xst[2][CNW(D)];             // staged packed (xbar, P) records (cp.async)
+                double U[D][LD(D)], Pm[D][LD(D)], Ps[D][LD(D)] /* P^s_{k+1} - P^- */, X[D][LD(D)];
+                double dm[D];
+                double fqs[2][FQS(D, STREAM)];     // STREAM: (F_{k+1}, Q_{k+1}) staged with record k
+            } g[kQ];
+        } u;
+    } w[kWWarps];
+};
+
+template <int D, bool STREAM>
+__global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_smoother_apply_q(const WParams p) {
+    static_assert(D <= kGL, "one row per lane of an 8-lane group");
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    K5QSmem<D, STREAM>& sh = *reinterpret_cast<K5QSmem<D, STREAM>*>(smem_raw);
+    load_model<D>(sh.m, p.model);
+    for (int e = threadIdx.x; e < D * D; e += blockDim.x) {
+        const int i = e / D, j = e - (e / D) * D;
+        sh.I[i][j] = (i == j) ? 1.0 : 0.0;
+        sh.Z[i][j] = 0.0;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int c = blockIdx.x * kWWarps + wid;
+    if (c >= p.nch) return;
+    auto& W = sh.w[wid];
+    const SModel<D>& M = sh.m;
+    const int64_t kb = static_cast<int64_t>(c) * p.K;
+    const int64_t ke = min(kb + p.K, p.n);
+    // ---- carries: collapsed suffix after the chain (incoming sharded, scanned chains > c), then
+    // back through the smoother aggregates of quarters 3, 2, 1 (kw_filter_apply_q)
+    auto& c3P = W.cP[kQ - 1];
+    for (int e = lane; e < D * D; e += 32) c3P[e / D][e % D] = 0.0;
+    for (int i = lane; i < D; i += 32) W.cm[kQ - 1][i] = 0.0;
+    __syncwarp();
+    for (int g = p.world - 1; g > p.rank && p.in_smooth; --g) {
+        gload<D>(W.u.c.a, p.in_smooth + static_cast<int64_t>(g) * (SNW(D) + 1), lane);   // blob = aggregate + NLL partial
+        wapply_suffix<D>(W.u.c.a, W.cm[kQ - 1], c3P, W.u.c.s, lane);
+    }
+    if (c + 1 < p.nch) {
+        gload<D>(W.u.c.a, p.sagg + static_cast<int64_t>(c + 1) * SNW(D), lane);
+        wapply_suffix<D>(W.u.c.a, W.cm[kQ - 1], c3P, W.u.c.s, lane);
+    }
+    for (int q = kQ - 2; q >= 0; --q) {
+        for (int e = lane; e < D * D; e += 32) W.cP[q][e / D][e % D] = W.cP[q + 1][e / D][e % D];
+        for (int i = lane; i < D; i += 32) W.cm[q][i] = W.cm[q + 1][i];
+        __syncwarp();
+        gload<D>(W.u.c.a, p.sqagg + (static_cast<int64_t>(c) * (kQ - 1) + q) * SNW(D), lane);   // quarter q + 1
+        wapply_suffix<D>(W.u.c.a, W.cm[q], W.cP[q], W.u.c.s, lane);
+    }
+    const int q = lane / kGL, r0 = lane % kGL, gb = q * kGL;
+    const unsigned gm = 0xFFu << gb;
+    const bool act = r0 < D;
+    const int r = act ? r0 : 0;
+    int64_t qb, qe;
+    quarter_bounds(kb, ke, p.K, q, qb, qe);
+    double Psr[D], msr = W.cm[q][r];
+#pragma unroll
+    for (int j = 0; j < D; ++j) Psr[j] = W.cP[q][r][j];
+    const double hr = act ? M.H[r] : 0.0;
+    __syncwarp();                                   // W.u (carry scratch) is reused by the staging below
+    auto& Gs = W.u.g[q];
+    const double* xpc = p.xp + static_cast<int64_t>(c) * p.K * CNW(D);
+    double tnext = (qe > qb && p.k0 + qe < p.nglob) ? __ldg(p.t + qe) : 0.0;
+    double tk_next = 0.0;
+    if (qe > qb) {
+        const double* src = xpc + (qe - 1 - kb) * CNW(D);
+        for (int i = r0; i < CNW(D); i += kGL) cp_async8(&Gs.xst[0][i], src + i, 8);
+        if (STREAM && p.k0 + qe < p.nglob) {        // F, Q of the transition out of qe - 1 (record qe)
+            const double* fsrc = p.fq + qe * FQW(D);
+            for (int i = r0; i < FQW(D); i += kGL) cp_async8(&Gs.fqs[0][i], fsrc + i, 8);
+        }
+        cp_async_commit();
+        tk_next = __ldg(p.t + qe - 1);
+    }
+    int sb = 0;
+    bool bad = false;
+    for (int64_t k = qe - 1; k >= qb; --k) {
+        const double tk = tk_next;
+        const int64_t g = p.k0 + k;
+        cp_async_wait<0>();
+        __syncwarp(gm);
+        if (k > qb) {
+            const double* src = xpc + (k - 1 - kb) * CNW(D);
+            for (int i = r0; i < CNW(D); i += kGL) cp_async8(&Gs.xst[sb ^ 1][i], src + i, 8);
+            if (STREAM) {                           // record k: the transition out of k - 1
+                const double* fsrc = p.fq + k * FQW(D);
+                for (int i = r0; i < FQW(D); i += kGL) cp_async8(&Gs.fqs[sb ^ 1][i], fsrc + i, 8);
+            }
+            cp_async_commit();
+            tk_next = __ldg(p.t + k - 1);
+        }
+        const int fb = sb;
+        double xa[D], Pr[D];
+        {
+            const double* src = Gs.xst[sb];
+#pragma unroll
+            for (int i = 0; i < D; ++i) xa[i] = src[i];
+#pragma unroll
+            for (int j = 0; j < D; ++j) Pr[j] = src[D + si(D, r, j)];
+        }
+        sb ^= 1;
+        if (g == p.nglob - 1) {                     // terminal element: smoothed = filtered
+#pragma unroll
+            for (int j = 0; j < D; ++j) Psr[j] = Pr[j];
+            msr = xa[r];
+        } else {
+            const int kind = wdisc_kind(tnext - tk, M.udt, STREAM);
+            const double* Fp;
+            const double* Qp;
+            if (kind == 0) {
+                if (STREAM) { Fp = &Gs.fqs[fb][0]; Qp = Fp + D * LD(D); }
+                else { Fp = &M.F[0][0]; Qp = &M.Q[0][0]; }
+            } else {                                // dt == 0 (or unsupported, reported by the fold): F = I, Q = 0
+                Fp = &sh.I[0][0]; Qp = &sh.Z[0][0];
+            }
+            double Uc[D], xm = 0.0;
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+                double su = 0.0;
+#pragma unroll
+                for (int qq = 0; qq < D; ++qq) su = fma(Fp[i * LD(D) + qq], Pr[qq], su);
+                Uc[i] = su;
+            }
+#pragma unroll
+            for (int qq = 0; qq < D; ++qq) xm = fma(Fp[r * LD(D) + qq], xa[qq], xm);
+            if (act) {
+#pragma unroll
+                for (int i = 0; i < D; ++i) Gs.U[i][r] = Uc[i];
+            }
+            __syncwarp(gm);
+            double Ur[D];
+#pragma unroll
+            for (int qq = 0; qq < D; ++qq) Ur[qq] = Gs.U[r][qq];
+            if (act) {
+#pragma unroll
+                for (int j = 0; j < D; ++j) {
+                    double s2 = Qp[r * LD(D) + j];
+#pragma unroll
+                    for (int qq = 0; qq < D; ++qq) s2 = fma(Ur[qq], Fp[j * LD(D) + qq], s2);
+                    Gs.Pm[r][j] = s2;
+                    Gs.Ps[r][j] = Psr[j] - s2;          // Delta = P^s_{k+1} - P^- (row r)
+                }
+                Gs.dm[r] = msr - xm;
+            }
+            __syncwarp(gm);
+            double L[D][D], Li[D];
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                double sd = Gs.Pm[j][j];
+#pragma unroll
+                for (int qq = 0; qq < j; ++qq) sd = fma(-L[j][qq], L[j][qq], sd);
+                bad = bad || !(sd > 0.0);
+                Li[j] = rsqrt(sd);
+#pragma unroll
+                for (int i = j + 1; i < D; ++i) {
+                    double so = Gs.Pm[j][i];
+#pragma unroll
+                    for (int qq = 0; qq < j; ++qq) so = fma(-L[i][qq], L[j][qq], so);
+                    L[i][j] = so * Li[j];
+                }
+                L[j][j] = sd * Li[j];
+            }
+            double Xc[D];
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+                double z = Uc[i];
+#pragma unroll
+                for (int qq = 0; qq < i; ++qq) z = fma(-L[i][qq], Xc[qq], z);
+                Xc[i] = z * Li[i];
+            }
+#pragma unroll
+            for (int i = D - 1; i >= 0; --i) {
+                double z = Xc[i];
+#pragma unroll
+                for (int qq = i + 1; qq < D; ++qq) z = fma(-L[qq][i], Xc[qq], z);
+                Xc[i] = z * Li[i];
+            }
+            double ms_new = xa[r], V[D];
+#pragma unroll
+            for (int qq = 0; qq < D; ++qq) ms_new = fma(Xc[qq], Gs.dm[qq], ms_new);
+#pragma unroll
+            for (int bb = 0; bb < D; ++bb) {
+                double v = 0.0;
+#pragma unroll
+                for (int a = 0; a < D; ++a) {
+                    const int lo = a < bb ? a : bb, hi = a < bb ? bb : a;
+                    v = fma(Xc[a], Gs.Ps[lo][hi], v);
+                }
+                V[bb] = v;
+            }
+            if (act) {
+#pragma unroll
+                for (int i = 0; i < D; ++i) Gs.X[i][r] = Xc[i];
+            }
+            __syncwarp(gm);
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                double s2 = Pr[j];
+#pragma unroll
+                for (int bb = 0; bb < D; ++bb) s2 = fma(V[bb], Gs.X[bb][j], s2);
+                Psr[j] = s2;
+            }
+            msr = ms_new;
+            __syncwarp(gm);                         // Gs buffers are rewritten by the next step
+        }
+        tnext = tk;
+        double mo = hr * msr, vo = 0.0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) vo = fma(Psr[j], M.H[j], vo);
+        vo *= hr;
+#pragma unroll
+        for (int off = kGL / 2; off > 0; off >>= 1) {
+            mo += __shfl_xor_sync(gm, mo, off);
+            vo += __shfl_xor_sync(gm, vo, off);
+        }
+        if (r0 == 0) {
+            if (p.mean) p.mean[k] = mo;
+            if (p.var) p.var[k] = vo;
+        }
+    }
+    if (bad && r0 == 0) raise_error(p.err, p.k0 + qb, kErrNumeric);
 }
 
 }  // namespace wide

@@ -34,6 +34,10 @@ void wide_set_smem_attrs(int device) {
         cudaFuncSetAttribute(kw_filter_apply_lpr<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K3LSmem<D, true>));
         cudaFuncSetAttribute(kw_smoother_apply_lpr<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K5LSmem<D, false>));
         cudaFuncSetAttribute(kw_smoother_apply_lpr<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K5LSmem<D, true>));
+        cudaFuncSetAttribute(kw_filter_apply_q<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K3QSmem<D, false>));
+        cudaFuncSetAttribute(kw_filter_apply_q<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K3QSmem<D, true>));
+        cudaFuncSetAttribute(kw_smoother_apply_q<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K5QSmem<D, false>));
+        cudaFuncSetAttribute(kw_smoother_apply_q<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K5QSmem<D, true>));
     }
     cudaFuncSetAttribute(kw_filter_apply<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K3Smem<D>));
     cudaFuncSetAttribute(kw_smoother_apply<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K5Smem<D>));
@@ -46,12 +50,14 @@ void wide_set_smem_attrs(int device) {
 // lane-per-row kernels of the wide path for D <= 8 (bit 0: fold, bit 1: RTS rescan, bit 2: both
 // rescans also with per-step (F, Q) staged in shared memory, bit 3: one-wave plan for them on the
 // table path, bit 4: Kalman rescan, bit 5: the one-wave plan also on the per-step (F, Q) path, bit 6:
-// lane-per-row discretisation); env PSSGP_WIDE_LPR overrides the default 127 for A/B runs (0 = the
-// shared-memory kernels)
+// lane-per-row discretisation, bit 7: quarter-parallel rescans (all four 8-lane groups of a warp
+// busy; needs bit 0, whose fold stores the quarter prefix aggregates)); env PSSGP_WIDE_LPR overrides
+// the default 255 for A/B runs (0 = the shared-memory kernels)
 inline int wide_lpr_mask() {
-    static const int v = [] { const char* e = getenv("PSSGP_WIDE_LPR"); return e && *e ? atoi(e) : 127; }();
+    static const int v = [] { const char* e = getenv("PSSGP_WIDE_LPR"); return e && *e ? atoi(e) : 255; }();
     return v;
 }
+inline bool wide_quarter_rescans() { return (wide_lpr_mask() & 129) == 129; }
 
 struct WPlan {
     int64_t K = 0;
@@ -72,7 +78,17 @@ WPlan make_wplan(pssgp_model* m, int64_t n) {
         m->wocc = std::max(1, std::min(a, std::min(b, c)));
         if constexpr (D <= kGL) {
             int l1 = 0, l5 = 0, l3 = 0;
-            if (m->mode == kPade) {   // per-step (F, Q) variants (their staging buffers cost shared memory)
+            if (wide_quarter_rescans()) {
+                if (m->mode == kPade) {
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l1, kw_filter_fold_lpr<D, true>, 32 * kWWarps, sizeof(K1LSmem<D, true>));
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l3, kw_filter_apply_q<D, true>, 32 * kWWarps, sizeof(K3QSmem<D, true>));
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l5, kw_smoother_apply_q<D, true>, 32 * kWWarps, sizeof(K5QSmem<D, true>));
+                } else {
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l1, kw_filter_fold_lpr<D, false>, 32 * kWWarps, sizeof(K1LSmem<D, false>));
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l3, kw_filter_apply_q<D, false>, 32 * kWWarps, sizeof(K3QSmem<D, false>));
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l5, kw_smoother_apply_q<D, false>, 32 * kWWarps, sizeof(K5QSmem<D, false>));
+                }
+            } else if (m->mode == kPade) {   // per-step (F, Q) variants (their staging buffers cost shared memory)
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l1, kw_filter_fold_lpr<D, true>, 32 * kWWarps, sizeof(K1LSmem<D, true>));
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l3, kw_filter_apply_lpr<D, true>, 32 * kWWarps, sizeof(K3LSmem<D, true>));
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l5, kw_smoother_apply_lpr<D, true>, 32 * kWWarps, sizeof(K5LSmem<D, true>));
@@ -83,12 +99,13 @@ WPlan make_wplan(pssgp_model* m, int64_t n) {
             }
             if (wide_lpr_mask() & 16) l5 = std::min(l5, l3);
             if (getenv("PSSGP_WIDE_DEBUG"))
-                fprintf(stderr, "wide plan D=%d occupancy: fold %d, apply %d, smoother %d, lpr fold %d, lpr smoother %d\n",
-                        D, a, b, c, l1, l5);
+                fprintf(stderr, "wide plan D=%d occupancy: fold %d, apply %d, smoother %d, lpr fold %d, lpr/q apply %d, "
+                        "lpr/q smoother %d\n", D, a, b, c, l1, l3, l5);
             // bit 3: on the table (uniform-dt) path, where both lane-per-row kernels run, size the
             // plan so they run in one wave (C3: 13.8 -> 11.7 ms; on the per-step (F, Q) path the
             // fewer, longer chains slow the shared-memory rescans: 26.2 -> 28.3 ms, so not there)
             if ((wide_lpr_mask() & 8) && (m->mode != kPade || (wide_lpr_mask() & 32))) m->wocc = std::max(1, std::min(m->wocc, std::min(l1, l5)));
+            if (wide_quarter_rescans()) m->wocc = std::max(1, std::min(l1, std::min(l3, l5)));
         }
     }
     const int64_t target = static_cast<int64_t>(m->sm_count) * m->wocc * kWWarps;
@@ -103,7 +120,9 @@ template <int D>
 pssgp_status wide_setup(pssgp_model* m, const WPlan& pl, pssgp::wide::WParams& p) {
     using namespace pssgp::wide;
     const size_t nch = static_cast<size_t>(pl.nch);
-    const size_t need = (2 * nch * FNW(D) + nch * pl.K * CNW(D) + 2 * nch * SNW(D) + nch + 64) * sizeof(double);
+    const bool quarters = D <= kGL && wide_quarter_rescans();
+    const size_t nq = quarters ? nch * (kQ - 1) * (FNW(D) + SNW(D)) : 0;   // quarter prefix / smoother aggregates
+    const size_t need = (2 * nch * FNW(D) + nch * pl.K * CNW(D) + 2 * nch * SNW(D) + nch + nq + 64) * sizeof(double);
     if (need > m->ws_bytes) {
         if (m->ws) cudaFree(m->ws);
         m->ws = nullptr;
@@ -139,7 +158,11 @@ pssgp_status wide_setup(pssgp_model* m, const WPlan& pl, pssgp::wide::WParams& p
     p.xp = w; w += nch * pl.K * CNW(D);
     p.sagg = w; w += nch * SNW(D);
     p.sbuf = w; w += nch * SNW(D);
-    p.nll_chain = w;
+    p.nll_chain = w; w += nch;
+    if (quarters) {
+        p.qagg = w; w += nch * (kQ - 1) * FNW(D);
+        p.sqagg = w;
+    }
     p.K = pl.K;
     p.nch = pl.nch;
     p.model = m->d_model;
@@ -289,6 +312,12 @@ pssgp_status wide_fapply(pssgp_model* m, pssgp::wide::WParams& p, int nb, cudaSt
     using namespace pssgp::wide;
     ProfScope ps(m, S_K3, s);
     if constexpr (D <= kGL) {
+        if (p.qagg) {   // quarter-parallel Kalman rescan (the fold stored the quarter prefix aggregates)
+            if (p.fq) kw_filter_apply_q<D, true><<<nb, 32 * kWWarps, sizeof(K3QSmem<D, true>), s>>>(p);
+            else kw_filter_apply_q<D, false><<<nb, 32 * kWWarps, sizeof(K3QSmem<D, false>), s>>>(p);
+            LAUNCH_CHECK(m, "kw_filter_apply_q");
+            return PSSGP_OK;
+        }
         // bit 4: lane-per-row Kalman rescan (uniform dt unless bit 2)
         if ((wide_lpr_mask() & 16) && (!p.fq || (wide_lpr_mask() & 4))) {
             if (p.fq) kw_filter_apply_lpr<D, true><<<nb, 32 * kWWarps, sizeof(K3LSmem<D, true>), s>>>(p);
@@ -307,6 +336,12 @@ pssgp_status wide_sapply(pssgp_model* m, pssgp::wide::WParams& p, int nb, cudaSt
     using namespace pssgp::wide;
     ProfScope ps(m, S_K5, s);
     if constexpr (D <= kGL) {
+        if (p.sqagg) {  // quarter-parallel RTS rescan (kw_filter_apply_q stored the quarter smoother aggregates)
+            if (p.fq) kw_smoother_apply_q<D, true><<<nb, 32 * kWWarps, sizeof(K5QSmem<D, true>), s>>>(p);
+            else kw_smoother_apply_q<D, false><<<nb, 32 * kWWarps, sizeof(K5QSmem<D, false>), s>>>(p);
+            LAUNCH_CHECK(m, "kw_smoother_apply_q");
+            return PSSGP_OK;
+        }
         // uniform dt only by default: with per-step (F, Q) read from global memory it measured
         // slower than the shared-memory kernel (C3 irregular K5w 8.4 -> 11.3 ms); bit 2 forces it
         if ((wide_lpr_mask() & 2) && (!p.fq || (wide_lpr_mask() & 4))) {

@@ -39,10 +39,13 @@ def _workloads():
 
 
 @pytest.fixture(scope="module")
-def oracle_jobs():
-    """Workloads and their oracle results (futures), all started at once."""
-    ws = {k: f() for k, f in _workloads().items()}
-    ex = ThreadPoolExecutor(max_workers=len(ws))
+def oracle_jobs(request):
+    """Workloads and their oracle results (futures) of the SELECTED tests of this module, all
+    started at once."""
+    names = {"test_config3_full_size": "C3", "test_config4_full_size": "C4", "test_config5_full_size": "C5"}
+    selected = {names[it.name] for it in request.session.items if it.name in names}
+    ws = {k: f() for k, f in _workloads().items() if k in selected}
+    ex = ThreadPoolExecutor(max_workers=max(1, len(ws)))
     futs = {k: ex.submit(oracle.posterior, w) for k, w in ws.items()}
     yield ws, futs
     ex.shutdown(wait=True)
