@@ -106,3 +106,90 @@ def test_kf_complex_step_vs_fd_of_c_oracle():
 
     fd = np.array([richardson(lambda x, j=j: f(j, x), th0[j], 1e-3) for j in range(3)])
     np.testing.assert_allclose(gk, fd, rtol=1e-6, atol=1e-6)
+
+
+# ---------------------------------------------------------------- any SSM (NEXT row f1 widened)
+GENERAL_MODELS = {
+    "rbf4": [synth.Component("rbf", 1.2, 0.7, order=4)],
+    "per3+m32": [synth.Component("periodic", 1.5, 1.0, period=0.7, order=3), synth.Component("matern32", 1.0, 2.0)],
+    "quasi1": [synth.Component("quasiperiodic", 2.0, 1.0, period=0.5, order=1, mat_lengthscale=3.0, mat_nu2=3)],
+    # the paper's CO2 model C_Per x C_Mat + C_Mat, J = 2, d = 14, at time scale 1/52
+    "co2_J2": [synth.Component("quasiperiodic", 2.0, 1.0, period=1.0, order=2, mat_lengthscale=5.0, mat_nu2=3),
+               synth.Component("matern32", 10.0, 20.0)],
+    "rbf3+m12": [synth.Component("rbf", 1.0, 0.5, order=3), synth.Component("matern12", 0.5, 2.0)],
+}
+
+
+def components_at(comps, theta):
+    """The kernel spec at log-hyper-parameters theta (oracle.grad.param_names order)."""
+    out, i = [], 0
+    for c in comps:
+        kw = dict(variance=math.exp(theta[i]), lengthscale=math.exp(theta[i + 1]))
+        i += 2
+        if c.kind in ("periodic", "quasiperiodic"):
+            kw["period"] = math.exp(theta[i]); i += 1
+        if c.kind == "quasiperiodic":
+            kw["mat_lengthscale"] = math.exp(theta[i]); i += 1
+        out.append(synth.Component(c.kind, order=c.order, mat_nu2=c.mat_nu2, **{**dict(period=c.period,
+                                   mat_lengthscale=c.mat_lengthscale), **kw}))
+    return out, math.exp(theta[i])
+
+
+def _general_problem(name, n=240, seed=21):
+    rng = np.random.default_rng(seed)
+    t = np.cumsum(rng.exponential(0.02, n))
+    if name == "co2_J2":
+        t = np.arange(n) / 52.0
+    y = np.sin(2 * np.pi * t) + 0.3 * np.cos(7 * t) + 0.2 * rng.standard_normal(n)
+    mask = (rng.random(n) > 0.15).astype(np.uint8)
+    y[mask == 0] = np.nan
+    return GENERAL_MODELS[name], 0.05, t, y, mask
+
+
+def test_ive_series_vs_scipy():
+    from scipy import special
+    for j in range(0, 9):
+        for a in (1e-3, 0.25, 1.0, 4.0, 25.0):
+            assert abs(og.ive_series(j, a) - special.ive(j, a)) <= 1e-14 * max(special.ive(j, a), 1e-300) + 1e-300
+
+
+@pytest.mark.parametrize("name", list(GENERAL_MODELS))
+def test_general_ssm_matches_builder(name):
+    """The complex-capable construction at the real theta equals oracle.ssm.build."""
+    comps = GENERAL_MODELS[name]
+    G, W, H, P = og.ssm_cs(comps, og.theta0(comps, 0.1))
+    m = ossm.build(comps)
+    for a, b in ((G, m.G), (W, m.W), (P, m.Pinf)):
+        assert np.max(np.abs(a - b)) <= 1e-13 * max(1.0, np.max(np.abs(b)))
+    np.testing.assert_array_equal(H, m.H)
+
+
+@pytest.mark.parametrize("name", list(GENERAL_MODELS))
+def test_general_complex_step_vs_fd_of_c_oracle(name):
+    """Complex-step gradient of any SSM against 4th-order finite differences of the C oracle's NLL
+    (independent code: oracle.ssm.build at the perturbed hyper-parameters + kalman.c)."""
+    comps, r, t, y, mask = _general_problem(name)
+    nll, g = og.kf_nll_grad_general(comps, r, t, y, mask)
+    th0 = og.theta0(comps, r)
+    assert len(og.param_names(comps)) == th0.shape[0] == g.shape[0]
+
+    def f(j, x):
+        th = th0.copy()
+        th[j] = x
+        cs, rr = components_at(comps, th)
+        return oracle.posterior(synth.Workload("g", cs, rr, t, y, mask), smooth=False)["nll"]
+
+    assert abs(nll - f(0, th0[0])) <= 1e-10 * abs(nll)
+    fd = np.array([richardson(lambda x, j=j: f(j, x), th0[j], 1e-3) for j in range(th0.shape[0])])
+    np.testing.assert_allclose(g, fd, rtol=2e-6, atol=2e-6 * (1 + np.max(np.abs(fd))))
+
+
+def test_general_equals_matern_specific():
+    """For one Matern component the general complex step equals kf_nll_grad (3 parameters)."""
+    for kind in KINDS:
+        w = synth.random_problem(15, 250, kind=kind, p_missing=0.2, ties=2)
+        c = w.components[0]
+        n1, g1 = og.kf_nll_grad(kind, c.variance, c.lengthscale, w.noise_var, w.t, w.y, w.mask)
+        n2, g2 = og.kf_nll_grad_general(w.components, w.noise_var, w.t, w.y, w.mask)
+        assert abs(n1 - n2) <= 1e-12 * abs(n1)
+        np.testing.assert_allclose(g2, g1, rtol=1e-11, atol=1e-11 * np.max(np.abs(g1)))
