@@ -140,16 +140,30 @@ pssgp_status pssgp_nll(pssgp_model* m, int64_t N, const double* t, const double*
 pssgp_status pssgp_posterior_f32(pssgp_model* m, int64_t N, const double* t, const double* y,
                                  const uint8_t* mask, double* mean, double* var, double* nll, void* stream);
 
-/* NLL and its exact gradient with respect to theta = (log sigma^2, log ell,
- * log sigma_n^2) of a SINGLE-component Matern model (the hyper-parameter
- * gradient the paper obtains by automatic differentiation, PAPER.md:77, 157,
- * 173).  Forward-mode tangents of the Kalman recursion (supplement
- * PAPER.md:304-315) are composed as affine maps per thread chain and reduced
- * in time order (pssgp_grad.cuh).
- * nll: device scalar or NULL; grad: device array of 3 doubles, written in the
- * order above.  N = 0 -> nll = 0, grad = 0.  Other models -> PSSGP_E_UNSUPPORTED. */
+/* NLL and its exact gradient with respect to the log hyper-parameters theta (the gradient the
+ * paper obtains by automatic differentiation of the parallel filter; its
+ * L-BFGS / HMC workloads).  theta, in this order (pssgp_num_params entries):
+ * for each component in the order given to pssgp_create
+ *     Matern-nu, RBF-Taylor:  log variance, log lengthscale
+ *     periodic:               log variance, log lengthscale, log period
+ *     quasi-periodic:         log variance, log lengthscale, log period, log mat_lengthscale
+ * then log noise_var.  The model basis (balancing matrix D, Eq. (9); the Matern lambda-scaling) is
+ * treated as constant ("D treated as constant"), which leaves the gradient exact.
+ *   - One Matern component (any grid): forward-mode tangents of the Kalman recursion (supplement
+ *     PAPER.md:304-315) composed as affine maps per thread chain (pssgp_grad.cuh).
+ *   - Any other model (sums, RBF, periodic, quasi-periodic products): reverse mode - the adjoint
+ *     of the Kalman recursion is an affine backward recursion whose per-chain maps compose in
+ *     closed form; forward rescan composing them, reverse scan, backward rescan, contraction with
+ *     dF/dtheta, dQ/dtheta (exact Van Loan tangents at the uniform step) and dP_inf/dtheta
+ *     (pssgp_wide.cuh).  Needs options.uniform_dt > 0 (every step of length
+ *     uniform_dt or 0), else PSSGP_E_UNSUPPORTED.
+ * nll: device scalar or NULL; grad: device array of pssgp_num_params(m) doubles.  N = 0 -> nll = 0,
+ * grad = 0. */
 pssgp_status pssgp_nll_grad(pssgp_model* m, int64_t N, const double* t, const double* y,
                             const uint8_t* mask, double* nll, double* grad, void* stream);
+
+/* Number of hyper-parameters of the model (length of pssgp_nll_grad's grad; see its order). */
+int pssgp_num_params(const pssgp_model* m);
 
 /* End-to-end variant on HOST arrays (pinned memory recommended): copies the
  * inputs to handle-owned device buffers, runs pssgp_posterior, copies mean,

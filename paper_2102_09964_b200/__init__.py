@@ -26,7 +26,7 @@ __all__ = ["Model", "PssgpError", "build", "lib", "pssgp_create", "pssgp_destroy
            "pssgp_aggregate_bytes", "pssgp_shard_filter_reduce", "pssgp_shard_filter_apply",
            "pssgp_shard_smoother_apply", "pssgp_profile_enable", "pssgp_profile_read", "pssgp_profile_name",
            "pssgp_merge_grid", "pssgp_gather", "pssgp_predict", "pssgp_posterior_batched", "pssgp_nll_grad_batched",
-           "pssgp_posterior_f32", "pssgp_plan_f32", "pssgp_measure_fp64_peak"]
+           "pssgp_posterior_f32", "pssgp_plan_f32", "pssgp_measure_fp64_peak", "pssgp_num_params"]
 
 
 def _ptr(x) -> Optional[int]:
@@ -234,6 +234,11 @@ def pssgp_shard_smoother_apply(h, k0, n, N_global, t_ptr, all_ptr, rank, world, 
                                                int(world), mean_ptr, var_ptr, nll_ptr, _stream_ptr(stream)))
 
 
+def pssgp_num_params(h) -> int:
+    """Number of log hyper-parameters (length of the pssgp_nll_grad gradient)."""
+    return int(lib().pssgp_num_params(h))
+
+
 def pssgp_measure_fp64_peak(h) -> float:
     """DFMA throughput of the handle's device in TFLOP/s (the fp64 roofline denominator)."""
     out = ctypes.c_double(0.0)
@@ -301,12 +306,18 @@ class Model:
         pssgp_nll(self.h, N, t, y, mask, nll, stream)
         return nll
 
+    @property
+    def num_params(self) -> int:
+        return pssgp_num_params(self.h)
+
     def nll_grad(self, t, y, mask, stream=None):
-        """(nll[1], grad[3]) with grad = d NLL / d (log sigma^2, log ell, log sigma_n^2)."""
+        """(nll[1], grad[num_params]): d NLL / d log hyper-parameters in the order of
+        include/pssgp.h (per component: log variance, log lengthscale[, log period[, log Matern
+        lengthscale]]; then log noise variance)."""
         import torch
         N = int(t.shape[0])
         nll = torch.zeros(1, dtype=torch.float64, device=t.device)
-        grad = torch.zeros(3, dtype=torch.float64, device=t.device)
+        grad = torch.zeros(self.num_params, dtype=torch.float64, device=t.device)
         pssgp_nll_grad(self.h, N, t, y, mask, nll, grad, stream)
         return nll, grad
 

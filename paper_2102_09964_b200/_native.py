@@ -102,6 +102,7 @@ SIGNATURES = {
     "pssgp_posterior": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pssgp_nll": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _vp, _vp]),
     "pssgp_nll_grad": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "pssgp_num_params": (ctypes.c_int, [_vp]),
     "pssgp_posterior_f32": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pssgp_posterior_host": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pssgp_check": (ctypes.c_int, [_vp]),

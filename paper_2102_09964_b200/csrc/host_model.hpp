@@ -400,4 +400,128 @@ inline void van_loan(const Mat& G, const Mat& W, int n, ld dt, Mat& F, Mat& Q) {
         }
 }
 
+// --------------------------------------------------------------------- hyper-parameter derivatives
+// d/d theta_p of (G, W, P_inf) of one component in its final (device) basis, theta = the log
+// hyper-parameters in the order of include/pssgp.h (pssgp_nll_grad).  The basis (balancing D, the
+// Matern lambda-scaling) is held constant: every family below describes the
+// covariance at theta exactly in that fixed basis, so the NLL - which is basis invariant - has the
+// true gradient.  Time-scale parameters (Matern / RBF lengthscale, periodic period, the Matern
+// factor of a product) rescale time, x(t) = x_1(t / tau): G -> G / tau, W -> W / tau, P_inf fixed
+// (for RBF-Taylor: p_ell(s) = p_1(ell s), so the spectral factor scales exactly the same way);
+// variances scale W and P_inf; the periodic lengthscale enters only the Bessel weights
+// q_j^2 = (2 - [j = 0]) s2 I_j(a) e^{-a}, a = ell^-2, with d(I_j e^{-a})/da = (I_{j-1} + I_{j+1})/2 e^{-a}
+// - I_j e^{-a} (I_{-1} = I_1).
+struct ParamDeriv {
+    Mat dG, dW, dP;   // d x d each (zeros where the parameter does not enter)
+};
+
+inline ld bessel_ive_dloga(int j, ld a) {   // d (I_j(a) e^{-a}) / d log a
+    const ld im = bessel_ive(j == 0 ? 1 : j - 1, a), ip = bessel_ive(j + 1, a);
+    return a * (0.5L * (im + ip) - bessel_ive(j, a));
+}
+
+inline Mat periodic_dP_dlogell(int J, ld s2, ld ell) {   // d P_inf / d log ell of periodic(J, s2, ell, .)
+    const int n = 2 * (J + 1);
+    Mat dP = zeros(n);
+    const ld a = 1.0L / (ell * ell);
+    for (int j = 0; j <= J; ++j) {
+        const ld v = (j == 0 ? 1.0L : 2.0L) * s2 * bessel_ive_dloga(j, a) * (-2.0L);   // d log a / d log ell = -2
+        dP[(2 * j) * n + 2 * j] = v;
+        dP[(2 * j + 1) * n + 2 * j + 1] = v;
+    }
+    return dP;
+}
+
+inline Mat scaled(const Mat& A, ld s) {
+    Mat B = A;
+    for (auto& v : B) v *= s;
+    return B;
+}
+
+// Forward-mode tangent of van_loan (same algorithm, same scaling / doubling counts): F, Q and their
+// derivatives along (dG, dW).
+inline void expm_taylor_tangent(const Mat& A, const Mat& dA, int n, Mat& E, Mat& dE) {
+    const ld nr = norm1(A, n);
+    int s = 0;
+    if (nr > 0.5L) s = static_cast<int>(std::ceil(std::log2(nr / 0.5L)));
+    const ld sc = std::ldexp(1.0L, -s);
+    const Mat As = scaled(A, sc), dAs = scaled(dA, sc);
+    E = eye(n);
+    dE = zeros(n);
+    Mat term = eye(n), dterm = zeros(n);
+    for (int k = 1; k <= 30; ++k) {
+        Mat dt1 = matmul(dterm, As, n), dt2 = matmul(term, dAs, n);
+        term = matmul(term, As, n);
+        for (size_t i = 0; i < term.size(); ++i) {
+            term[i] /= k;
+            dterm[i] = (dt1[i] + dt2[i]) / k;
+            E[i] += term[i];
+            dE[i] += dterm[i];
+        }
+    }
+    for (int i = 0; i < s; ++i) {
+        Mat a = matmul(dE, E, n), b = matmul(E, dE, n);
+        for (size_t q = 0; q < a.size(); ++q) dE[q] = a[q] + b[q];
+        E = matmul(E, E, n);
+    }
+}
+
+inline void van_loan_tangent(const Mat& G, const Mat& W, const Mat& dG, const Mat& dW, int n, ld dt, Mat& F, Mat& Q,
+                             Mat& dF, Mat& dQ) {
+    const ld g = norm1(G, n) * std::fabs(dt);
+    int s = 0;
+    if (g > 0.5L) s = static_cast<int>(std::ceil(std::log2(g / 0.5L)));
+    const ld h = std::ldexp(dt, -s);
+    const int m = 2 * n;
+    Mat M = zeros(m), dM = zeros(m);
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+            M[i * m + j] = G[i * n + j] * h;
+            M[i * m + n + j] = W[i * n + j] * h;
+            M[(n + i) * m + n + j] = -G[j * n + i] * h;
+            dM[i * m + j] = dG[i * n + j] * h;
+            dM[i * m + n + j] = dW[i * n + j] * h;
+            dM[(n + i) * m + n + j] = -dG[j * n + i] * h;
+        }
+    Mat E, dE;
+    expm_taylor_tangent(M, dM, m, E, dE);
+    F = zeros(n); Q = zeros(n); dF = zeros(n); dQ = zeros(n);
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+            F[i * n + j] = E[i * m + j];
+            dF[i * n + j] = dE[i * m + j];
+        }
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+            ld acc = 0.0L, dacc = 0.0L;
+            for (int k = 0; k < n; ++k) {
+                acc += E[i * m + n + k] * E[j * m + k];
+                dacc += dE[i * m + n + k] * E[j * m + k] + E[i * m + n + k] * dE[j * m + k];
+            }
+            Q[i * n + j] = acc;
+            dQ[i * n + j] = dacc;
+        }
+    for (int r = 0; r < s; ++r) {
+        // Q <- F Q F^T + Q, F <- F F
+        const Mat Ft = transpose(F, n), dFt = transpose(dF, n);
+        const Mat FQ = matmul(F, Q, n);
+        const Mat a = matmul(matmul(dF, Q, n), Ft, n), b = matmul(matmul(F, dQ, n), Ft, n), c = matmul(FQ, dFt, n);
+        Mat Qn = matmul(FQ, Ft, n);
+        for (size_t i = 0; i < Qn.size(); ++i) {
+            Qn[i] += Q[i];
+            dQ[i] = a[i] + b[i] + c[i] + dQ[i];
+        }
+        Q = Qn;
+        const Mat x1 = matmul(dF, F, n), x2 = matmul(F, dF, n);
+        for (size_t i = 0; i < dF.size(); ++i) dF[i] = x1[i] + x2[i];
+        F = matmul(F, F, n);
+    }
+    for (int i = 0; i < n; ++i)
+        for (int j = i + 1; j < n; ++j) {
+            const ld a = 0.5L * (Q[i * n + j] + Q[j * n + i]), b = 0.5L * (dQ[i * n + j] + dQ[j * n + i]);
+            Q[i * n + j] = Q[j * n + i] = a;
+            dQ[i * n + j] = dQ[j * n + i] = b;
+        }
+}
+
 }  // namespace pssgp_host

@@ -321,6 +321,10 @@ pssgp_status pssgp_create(const pssgp_component* comps, int n_comps, double nois
     m->forced_K = o.chain_len;
     m->blocks_per_sm = o.blocks_per_sm;
     std::vector<ph::Ssm> parts;
+    std::vector<std::vector<ph::ParamDeriv>> cder;   // per component: d(G, W, P_inf)/d theta_p, local basis
+    // variance: W and P_inf scale; time-scale parameter: G, W scale as 1 / tau (host_model.hpp)
+    auto vscale = [](const ph::Ssm& p) { return ph::ParamDeriv{ph::zeros(p.d), p.W, p.Pinf}; };
+    auto tscale = [](const ph::Ssm& p) { return ph::ParamDeriv{ph::scaled(p.G, -1.0L), ph::scaled(p.W, -1.0L), ph::zeros(p.d)}; };
     for (int c = 0; c < n_comps; ++c) {
         const pssgp_component& k = comps[c];
         if (!(k.variance > 0.0) || !std::isfinite(k.variance) || !(k.lengthscale > 0.0) || !std::isfinite(k.lengthscale)) {
@@ -345,6 +349,10 @@ pssgp_status pssgp_create(const pssgp_component* comps, int n_comps, double nois
         } else if (k.kind == PSSGP_PERIODIC) {
             if (k.order < 0 || k.order > 32 || !(k.period > 0.0)) { delete m; return PSSGP_E_ARG; }
             part = ph::periodic(k.order, k.variance, k.lengthscale, k.period);
+            cder.push_back({vscale(part),
+                            ph::ParamDeriv{ph::zeros(part.d), ph::zeros(part.d),
+                                           ph::periodic_dP_dlogell(k.order, k.variance, k.lengthscale)},
+                            tscale(part)});
         } else if (k.kind == PSSGP_QUASIPERIODIC) {
             if (k.order < 0 || k.order > 16 || !(k.period > 0.0) || !(k.mat_lengthscale > 0.0) ||
                 (k.mat_nu2 != 1 && k.mat_nu2 != 3 && k.mat_nu2 != 5)) {
@@ -355,14 +363,46 @@ pssgp_status pssgp_create(const pssgp_component* comps, int n_comps, double nois
             const ph::Ssm per = ph::periodic(k.order, k.variance, k.lengthscale, k.period);
             const ph::Ssm mat = ph::matern((k.mat_nu2 + 1) / 2, 1.0L, k.mat_lengthscale, &lam);
             part = ph::kron_product(per, mat);
+            // log ell: P_p -> dP_p (Bessel weights); log period: -(G_p (x) I); log Matern ell: -(I (x) G_m), -W
+            ph::Ssm per_l = per, per_t = per, mat_0 = mat, per_0 = per, mat_t = mat;
+            per_l.G = ph::zeros(per.d);
+            per_l.Pinf = ph::periodic_dP_dlogell(k.order, k.variance, k.lengthscale);
+            per_t.G = ph::scaled(per.G, -1.0L);
+            per_t.Pinf = ph::zeros(per.d);
+            mat_0.G = ph::zeros(mat.d);
+            per_0.G = ph::zeros(per.d);
+            mat_t.G = ph::scaled(mat.G, -1.0L);
+            const ph::Ssm kl = ph::kron_product(per_l, mat), kp = ph::kron_product(per_t, mat_0),
+                          km = ph::kron_product(per_0, mat_t);
+            cder.push_back({vscale(part), ph::ParamDeriv{ph::zeros(part.d), kl.W, kl.Pinf},
+                            ph::ParamDeriv{kp.G, ph::zeros(part.d), ph::zeros(part.d)},
+                            ph::ParamDeriv{km.G, ph::scaled(part.W, -1.0L), ph::zeros(part.d)}});
         } else {
             delete m;
             return PSSGP_E_UNSUPPORTED;
         }
+        if (k.kind != PSSGP_PERIODIC && k.kind != PSSGP_QUASIPERIODIC) cder.push_back({vscale(part), tscale(part)});
         parts.push_back(part);
     }
     m->ssm = parts.size() == 1 ? parts[0] : ph::block_sum(parts);
     m->d = m->ssm.d;
+    {   // embed the per-component derivatives into the d x d state (block-diagonal sum)
+        int o = 0;
+        for (size_t c = 0; c < parts.size(); ++c) {
+            const int pd = parts[c].d;
+            for (const auto& q : cder[c]) {
+                ph::ParamDeriv g{ph::zeros(m->d), ph::zeros(m->d), ph::zeros(m->d)};
+                for (int i = 0; i < pd; ++i)
+                    for (int j = 0; j < pd; ++j) {
+                        g.dG[(o + i) * m->d + o + j] = q.dG[i * pd + j];
+                        g.dW[(o + i) * m->d + o + j] = q.dW[i * pd + j];
+                        g.dP[(o + i) * m->d + o + j] = q.dP[i * pd + j];
+                    }
+                m->pder.push_back(g);
+            }
+            o += pd;
+        }
+    }
     if (m->d > kMaxD && !wide_ops_for(m->d)) {
         delete m;
         return PSSGP_E_UNSUPPORTED;
@@ -399,6 +439,8 @@ void pssgp_destroy(pssgp_model* m) {
     if (m->acs) cudaStreamDestroy(m->acs);
     if (m->d_err) cudaFree(m->d_err);
     if (m->d_model) cudaFree(m->d_model);
+    if (m->d_gder) cudaFree(m->d_gder);
+    if (m->gw) cudaFree(m->gw);
     for (int s = 0; s < kSlots; ++s)
         for (auto& pr : m->ev[s]) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
     for (auto e : m->ev_pool) cudaEventDestroy(e);
@@ -522,13 +564,20 @@ pssgp_status pssgp_nll_grad(pssgp_model* m, int64_t N, const double* t, const do
     pssgp_status st = check_args(m, N, t, y, mask);
     if (st) return st;
     if (!grad) return fail(m, PSSGP_E_ARG, "grad is NULL");
-    if (!m->closed || m->d > kMaxD)
-        return fail(m, PSSGP_E_UNSUPPORTED, "gradient needs a single closed-form Matern component");
+    if (!m->closed && m->mode != kTable)
+        return fail(m, PSSGP_E_UNSUPPORTED, "the gradient of this model needs a uniform grid (options.uniform_dt > 0)");
     if ((st = ensure_device(m))) return st;
     auto s = static_cast<cudaStream_t>(stream);
     m->last_stream = s;
+    if (!m->closed) {   // any other model on a uniform grid: reverse mode on the warp-per-chain path
+        const WideOps* ops = wide_ops_for(m->d);
+        if (!ops) return fail(m, PSSGP_E_UNSUPPORTED, "state dimension not compiled");
+        return ops->nll_grad(m, N, t, y, mask, nll, grad, s);
+    }
     DISPATCH_D(m, run_grad<D_>(m, N, t, y, mask, nll, grad, s));
 }
+
+int pssgp_num_params(const pssgp_model* m) { return m ? static_cast<int>(m->pder.size()) + 1 : -1; }
 
 pssgp_status pssgp_merge_grid(pssgp_model* m, int64_t n_train, const double* t_train, const double* y_train,
                               int64_t n_test, const double* t_test, double* t_out, double* y_out,

@@ -28,6 +28,10 @@ struct pssgp_model {
     double lam = 0.0, s2 = 0.0, r = 0.0;
     double udt = 0.0;
     std::vector<double> Fu, Qu;  // F(udt), Q(udt) row-major d x d
+    std::vector<pssgp_host::ParamDeriv> pder;   // d(G, W, P_inf) / d theta_p, p < npar - 1 (log noise last)
+    double* d_gder = nullptr;    // device: per parameter dF, dQ (at udt), dP_inf (d x d each)
+    char* gw = nullptr;          // general-model gradient workspace
+    size_t gw_bytes = 0;
     int device = 0;
     int64_t forced_K = 0;
     int blocks_per_sm = 0;
@@ -141,6 +145,8 @@ struct WideOps {
                                  int rank, int world, double* mean, double* var, double* nll,
                                  cudaStream_t s);
     pssgp_status (*debug_disc)(pssgp_model*, double dt, double* F, double* Q);
+    pssgp_status (*nll_grad)(pssgp_model*, int64_t N, const double* t, const double* y, const uint8_t* mask,
+                             double* nll, double* grad, cudaStream_t s);
     void (*plan)(pssgp_model*, int64_t N, int64_t* K, int64_t* nch, int* nb, int* threads);
 };
 template <int D>

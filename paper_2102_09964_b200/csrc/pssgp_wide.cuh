@@ -2657,5 +2657,404 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_smoother_app
     if (bad && r0 == 0) raise_error(p.err, p.k0 + qb, kErrNumeric);
 }
 
+
+// ================================================================== NLL gradient of any model (uniform dt)
+// Reverse mode over the Kalman recursion (supplement PAPER.md:304-315; the paper differentiates the
+// parallel filter by AD).  With the adjoint (b_k, C_k) = d NLL_{>k} / d (x_k, P_k) of
+// the filtered moments, one step k maps it back as an affine map
+//   b_{k-1} = M_k^T b_k + beta_k,  C_{k-1} = M_k^T C_k M_k + sym(M_k^T b_k u_k^T) + Gamma_k,
+//   M_k = (I - K_k h^T) F,  g = F^T h,  u_k = (v/S) g,  beta_k = -u_k,  Gamma_k = c1 g g^T,
+//   c1 = (1/S - v^2/S^2) / 2   (missing y: M_k = F, u = beta = Gamma = 0),
+// and these maps compose in closed form: (M, U, Gamma) with beta = -U always,
+//   Phi_1 o Phi_2 = (M_2 M_1, U_1 + M_1^T U_2, Gamma_1 - sym(M_1^T U_2 U_1^T) + M_1^T Gamma_2 M_1)
+// (Phi_2 applied first, i.e. the later steps).  The forward rescan (kw_grad_forward) composes each
+// chain's map step by step at O(d^2) + one F M product per step, a reverse Kogge-Stone scan
+// (kw_scan_adjoint) gives the adjoint entering every chain from the right, and the backward rescan
+// (kw_grad_backward) runs the adjoint recursion, accumulating with the adjoint before the update
+// (b^-, C^-) of every uniform step
+//   Z += b^- x_{k-1}^T + 2 C^- F P_{k-1},   Cs += C^-,   gr += c1 - (b_k . K)(v/S) + K^T C_k K,
+// and C0 = C^- of the global first step; then d NLL / d theta_p = <dF_p, Z> + <dQ_p, Cs> +
+// <dP_inf_p, C0> (+ r gr for log r) because dF_p, dQ_p are the same at every uniform step
+// (k_grad_contract).  Steps with dt = 0 (F = I, Q = 0) carry the adjoint but have no theta
+// dependence.  DESIGN.md §5c.
+struct GradBufs {
+    double* gagg;      // [nch][SNW]  chain adjoint maps (M, U, Gamma full) -> their reverse scan
+    double* gbuf;      // [nch][SNW]  ping-pong of the scan
+    double* gcar;      // [nch][CNW]  filtered state entering each chain
+    double* gpart;     // [nch][2 D^2 + 1]  per-chain (Z, Cs, gr)
+    double* gc0;       // [D^2]       C^- of the global first step
+};
+PS_CX int GPN(int D) { return 2 * D * D + 1; }
+
+template <int D>
+struct GFwdSmem {
+    SModel<D> m;
+    struct PerWarp {
+        double P[D][LD(D)], M[D][LD(D)], Gam[D][LD(D)];
+        double x[D], U[D];
+        union {
+            struct {
+                SF<D> a;
+                SCombF<D> s;
+            } c;
+            struct {
+                double FP[D][LD(D)], Pm[D][LD(D)], FM[D][LD(D)];
+                double xm[D], HP[D], w[D];
+            } st;
+        } u;
+    } w[kWWarps];
+};
+
+template <int D>
+__global__ void __launch_bounds__(32 * kWWarps) kw_grad_forward(const WParams p, const GradBufs gb) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    GFwdSmem<D>& sh = *reinterpret_cast<GFwdSmem<D>*>(smem_raw);
+    load_model<D>(sh.m, p.model);
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int c = blockIdx.x * kWWarps + wid;
+    if (c >= p.nch) return;
+    auto& W = sh.w[wid];
+    const SModel<D>& M = sh.m;
+    for (int e = lane; e < D * D; e += 32) W.P[e / D][e % D] = 0.0;
+    for (int i = lane; i < D; i += 32) W.x[i] = 0.0;
+    __syncwarp();
+    if (c > 0) {
+        gload<D>(W.u.c.a, p.fagg + static_cast<int64_t>(c - 1) * FNW(D), lane);
+        if (!wapply_prefix<D>(W.x, W.P, W.u.c.a, W.u.c.s, lane) && lane == 0) raise_error(p.err, p.k0, kErrNumeric);
+    }
+    {   // filtered state entering the chain (for the backward rescan's first step)
+        double* o = gb.gcar + static_cast<int64_t>(c) * CNW(D);
+        for (int i = lane; i < D; i += 32) o[i] = W.x[i];
+        for (int e = lane; e < D * D; e += 32) {
+            const int i = e / D, j = e - (e / D) * D;
+            if (j >= i) o[D + si(D, i, j)] = W.P[i][j];
+        }
+    }
+    for (int e = lane; e < D * D; e += 32) {
+        const int i = e / D, j = e - (e / D) * D;
+        W.M[i][j] = (i == j) ? 1.0 : 0.0;
+        W.Gam[i][j] = 0.0;
+    }
+    for (int i = lane; i < D; i += 32) W.U[i] = 0.0;
+    __syncwarp();
+    const int64_t kb = static_cast<int64_t>(c) * p.K;
+    const int64_t ke = min(kb + p.K, p.n);
+    double tprev = (kb < p.n && (kb > 0 || p.k0 > 0)) ? __ldg(p.t + kb - 1) : 0.0;
+    double quad = 0.0, logs = 0.0;
+    int nobs = 0;
+    double* xpc = p.xp + static_cast<int64_t>(c) * p.K * CNW(D);
+    for (int64_t k = kb; k < ke; ++k) {
+        const double tk = __ldg(p.t + k);
+        const bool obs = __ldg(p.mask + k) != 0;
+        const double yk = obs ? __ldg(p.y + k) : 0.0;
+        const int64_t g = p.k0 + k;
+        const int kind = (g == 0) ? 3 : wdisc_kind(tk - tprev, M.udt, false);
+        tprev = tk;
+        if (kind == 0) {
+            wmm<D>(W.u.st.FP, M.F, W.P, nullptr, lane);
+            wmm<D>(W.u.st.FM, M.F, W.M, nullptr, lane);
+            for (int i = lane; i < D; i += 32) {
+                double s2 = 0.0;
+                for (int q = 0; q < D; ++q) s2 = fma(M.F[i][q], W.x[q], s2);
+                W.u.st.xm[i] = s2;
+            }
+            __syncwarp();
+            wmm<D, false, true>(W.u.st.Pm, W.u.st.FP, M.F, M.Q, lane);
+        } else {
+            for (int e = lane; e < D * D; e += 32) {
+                const int i = e / D, j = e - (e / D) * D;
+                W.u.st.FM[i][j] = (kind == 1) ? W.M[i][j] : 0.0;
+                W.u.st.Pm[i][j] = (kind == 1) ? W.P[i][j] : M.Pinf[i][j];
+            }
+            for (int i = lane; i < D; i += 32) W.u.st.xm[i] = (kind == 1) ? W.x[i] : 0.0;
+        }
+        __syncwarp();
+        for (int i = lane; i < D; i += 32) {
+            double hp = 0.0, ww = 0.0;
+            for (int q = 0; q < D; ++q) {
+                hp = fma(W.u.st.Pm[i][q], M.H[q], hp);
+                ww = fma(W.u.st.FM[q][i], M.H[q], ww);
+            }
+            W.u.st.HP[i] = hp;
+            W.u.st.w[i] = ww;
+        }
+        __syncwarp();
+        const double S = wdot<D>(M.H, W.u.st.HP, lane) + M.r;
+        const double hx = wdot<D>(M.H, W.u.st.xm, lane);
+        if (lane == 0 && obs && !(S > 0.0 && S < INFINITY)) raise_error(p.err, g, kErrNumeric);
+        const double iS = obs ? 1.0 / S : 0.0;
+        const double v = obs ? (yk - hx) : 0.0;
+        const double vs = v * iS;
+        const double c1 = obs ? 0.5 * (iS - vs * vs) : 0.0;
+        for (int e = lane; e < D * D; e += 32) {
+            const int i = e / D, j = e - (e / D) * D;
+            const double hpi = W.u.st.HP[i] * iS;
+            W.P[i][j] = fma(-hpi, W.u.st.HP[j], W.u.st.Pm[i][j]);
+            W.M[i][j] = fma(-hpi, W.u.st.w[j], W.u.st.FM[i][j]);
+            const double wi = W.u.st.w[i], wj = W.u.st.w[j];
+            W.Gam[i][j] += fma(c1 * wi, wj, -0.5 * vs * (wi * W.U[j] + W.U[i] * wj));
+        }
+        __syncwarp();
+        for (int i = lane; i < D; i += 32) {
+            W.x[i] = fma(W.u.st.HP[i], vs, W.u.st.xm[i]);
+            W.U[i] = fma(vs, W.u.st.w[i], W.U[i]);
+        }
+        if (obs) {
+            quad = fma(v, vs, quad);
+            logs += log(S);
+            ++nobs;
+        }
+        __syncwarp();
+        double* o = xpc + (k - kb) * CNW(D);
+        for (int i = lane; i < D; i += 32) o[i] = W.x[i];
+        for (int e = lane; e < D * D; e += 32) {
+            const int i = e / D, j = e - (e / D) * D;
+            if (j >= i) o[D + si(D, i, j)] = W.P[i][j];
+        }
+    }
+    if (lane == 0) p.nll_chain[c] = nobs ? 0.5 * (quad + logs + nobs * 1.8378770664093453) : 0.0;
+    double* ga = gb.gagg + static_cast<int64_t>(c) * SNW(D);
+    for (int e = lane; e < D * D; e += 32) {
+        const int i = e / D, j = e - (e / D) * D;
+        ga[e] = W.M[i][j];
+        ga[D * D + D + e] = W.Gam[i][j];
+    }
+    for (int i = lane; i < D; i += 32) ga[D * D + i] = W.U[i];
+}
+
+// One reverse Kogge-Stone level of the chain adjoint maps: out[c] = in[c] o in[c + off] (the later
+// chain's map applied first), or in[c] when c + off >= nch.  One warp per element.
+template <int D>
+struct ScanSmemA {
+    double M1[D][LD(D)], M2[D][LD(D)], G1[D][LD(D)], G2[D][LD(D)], T1[D][LD(D)], T2[D][LD(D)];
+    double U1[D], U2[D], MU[D];
+};
+template <int D>
+__global__ void __launch_bounds__(32) kw_scan_adjoint(const double* __restrict__ in, double* __restrict__ out,
+                                                      int nch, int off) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    ScanSmemA<D>& sh = *reinterpret_cast<ScanSmemA<D>*>(smem_raw);
+    const int lane = threadIdx.x;
+    const int c = blockIdx.x;
+    const double* a = in + static_cast<int64_t>(c) * SNW(D);
+    double* o = out + static_cast<int64_t>(c) * SNW(D);
+    if (c + off >= nch) {
+        for (int e = lane; e < SNW(D); e += 32) o[e] = a[e];
+        return;
+    }
+    const double* b = in + static_cast<int64_t>(c + off) * SNW(D);
+    for (int e = lane; e < D * D; e += 32) {
+        const int i = e / D, j = e - (e / D) * D;
+        sh.M1[i][j] = a[e];
+        sh.G1[i][j] = a[D * D + D + e];
+        sh.M2[i][j] = b[e];
+        sh.G2[i][j] = b[D * D + D + e];
+    }
+    for (int i = lane; i < D; i += 32) {
+        sh.U1[i] = a[D * D + i];
+        sh.U2[i] = b[D * D + i];
+    }
+    __syncwarp();
+    wmm<D>(sh.T1, sh.G2, sh.M1, nullptr, lane);                 // Gamma_2 M_1
+    wmm<D>(sh.T2, sh.M2, sh.M1, nullptr, lane);                 // M_2 M_1
+    for (int i = lane; i < D; i += 32) {
+        double s2 = 0.0;
+        for (int q = 0; q < D; ++q) s2 = fma(sh.M1[q][i], sh.U2[q], s2);
+        sh.MU[i] = s2;                                          // M_1^T U_2
+    }
+    __syncwarp();
+    wmm<D, true, false>(sh.M2, sh.M1, sh.T1, sh.G1, lane);      // Gamma_1 + M_1^T Gamma_2 M_1 (into M2)
+    __syncwarp();
+    for (int e = lane; e < D * D; e += 32) {
+        const int i = e / D, j = e - (e / D) * D;
+        o[e] = sh.T2[i][j];
+        const double gsym = 0.5 * (sh.M2[i][j] + sh.M2[j][i]);
+        o[D * D + D + e] = gsym - 0.5 * (sh.MU[i] * sh.U1[j] + sh.U1[i] * sh.MU[j]);
+    }
+    for (int i = lane; i < D; i += 32) o[D * D + i] = sh.U1[i] + sh.MU[i];
+}
+
+template <int D>
+struct GBwdSmem {
+    SModel<D> m;
+    struct PerWarp {
+        double C[D][LD(D)], Z[D][LD(D)], Cs[D][LD(D)], Pp[D][LD(D)], FP[D][LD(D)], Pm[D][LD(D)], T[D][LD(D)],
+            Cm[D][LD(D)];
+        double b[D], xp[D], xm[D], HP[D], K[D], CK[D], KT[D], Mb[D], bm[D];
+    } w[kWWarps];
+};
+
+template <int D>
+__global__ void __launch_bounds__(32 * kWWarps) kw_grad_backward(const WParams p, const GradBufs gb,
+                                                                  const double* __restrict__ scanned) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    GBwdSmem<D>& sh = *reinterpret_cast<GBwdSmem<D>*>(smem_raw);
+    load_model<D>(sh.m, p.model);
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int c = blockIdx.x * kWWarps + wid;
+    if (c >= p.nch) return;
+    auto& W = sh.w[wid];
+    const SModel<D>& M = sh.m;
+    // adjoint after the chain's last step: (beta, Gamma) = (-U, Gamma) of the scanned maps of c + 1 ...
+    for (int e = lane; e < D * D; e += 32) {
+        const int i = e / D, j = e - (e / D) * D;
+        W.C[i][j] = (c + 1 < p.nch) ? scanned[static_cast<int64_t>(c + 1) * SNW(D) + D * D + D + e] : 0.0;
+        W.Z[i][j] = 0.0;
+        W.Cs[i][j] = 0.0;
+    }
+    for (int i = lane; i < D; i += 32)
+        W.b[i] = (c + 1 < p.nch) ? -scanned[static_cast<int64_t>(c + 1) * SNW(D) + D * D + i] : 0.0;
+    __syncwarp();
+    const int64_t kb = static_cast<int64_t>(c) * p.K;
+    const int64_t ke = min(kb + p.K, p.n);
+    const double* xpc = p.xp + static_cast<int64_t>(c) * p.K * CNW(D);
+    double gr = 0.0;
+    for (int64_t k = ke - 1; k >= kb; --k) {
+        const int64_t g = p.k0 + k;
+        const double tk = __ldg(p.t + k);
+        const int kind = (g == 0) ? 3 : wdisc_kind(tk - __ldg(p.t + k - 1), M.udt, false);
+        const bool obs = __ldg(p.mask + k) != 0;
+        const double yk = obs ? __ldg(p.y + k) : 0.0;
+        if (kind != 3) {   // filtered state of the previous step
+            const double* src = (k > kb) ? xpc + (k - 1 - kb) * CNW(D) : gb.gcar + static_cast<int64_t>(c) * CNW(D);
+            for (int i = lane; i < D; i += 32) W.xp[i] = src[i];
+            for (int e = lane; e < D * D; e += 32) {
+                const int i = e / D, j = e - (e / D) * D;
+                W.Pp[i][j] = src[D + si(D, i, j)];
+            }
+            __syncwarp();
+        }
+        if (kind == 0) {
+            wmm<D>(W.FP, M.F, W.Pp, nullptr, lane);
+            for (int i = lane; i < D; i += 32) {
+                double s2 = 0.0;
+                for (int q = 0; q < D; ++q) s2 = fma(M.F[i][q], W.xp[q], s2);
+                W.xm[i] = s2;
+            }
+            __syncwarp();
+            wmm<D, false, true>(W.Pm, W.FP, M.F, M.Q, lane);
+        } else {
+            for (int e = lane; e < D * D; e += 32) {
+                const int i = e / D, j = e - (e / D) * D;
+                W.Pm[i][j] = (kind == 1) ? W.Pp[i][j] : M.Pinf[i][j];
+            }
+            for (int i = lane; i < D; i += 32) W.xm[i] = (kind == 1) ? W.xp[i] : 0.0;
+        }
+        __syncwarp();
+        if (obs) {
+            for (int i = lane; i < D; i += 32) {
+                double hp = 0.0;
+                for (int q = 0; q < D; ++q) hp = fma(W.Pm[i][q], M.H[q], hp);
+                W.HP[i] = hp;
+            }
+            __syncwarp();
+            const double S = wdot<D>(M.H, W.HP, lane) + M.r;
+            const double v = yk - wdot<D>(M.H, W.xm, lane);
+            const double iS = 1.0 / S, vs = v * iS, c1 = 0.5 * (iS - vs * vs);
+            for (int i = lane; i < D; i += 32) W.K[i] = W.HP[i] * iS;
+            __syncwarp();
+            for (int i = lane; i < D; i += 32) {
+                double s2 = 0.0;
+                for (int q = 0; q < D; ++q) s2 = fma(W.C[i][q], W.K[q], s2);
+                W.CK[i] = s2;
+            }
+            __syncwarp();
+            const double bK = wdot<D>(W.b, W.K, lane), KCK = wdot<D>(W.K, W.CK, lane);
+            gr += c1 - bK * vs + KCK;
+            // (I - K h^T)^T C (I - K h^T) + (v/S) sym(h Mb^T) + c1 h h^T, Mb = (I - K h^T)^T b
+            for (int e = lane; e < D * D; e += 32) {
+                const int i = e / D, j = e - (e / D) * D;
+                W.T[i][j] = fma(-W.CK[i], M.H[j], W.C[i][j]);   // C (I - K h^T)
+            }
+            for (int i = lane; i < D; i += 32) W.Mb[i] = fma(-M.H[i], bK, W.b[i]);
+            __syncwarp();
+            for (int j = lane; j < D; j += 32) {
+                double s2 = 0.0;
+                for (int q = 0; q < D; ++q) s2 = fma(W.K[q], W.T[q][j], s2);
+                W.KT[j] = s2;
+            }
+            __syncwarp();
+            for (int e = lane; e < D * D; e += 32) {
+                const int i = e / D, j = e - (e / D) * D;
+                const double hi = M.H[i], hj = M.H[j];
+                W.Cm[i][j] = fma(-hi, W.KT[j], W.T[i][j]) + 0.5 * vs * (hi * W.Mb[j] + W.Mb[i] * hj) + c1 * hi * hj;
+            }
+            for (int i = lane; i < D; i += 32) W.bm[i] = fma(-vs, M.H[i], W.Mb[i]);
+        } else {
+            for (int e = lane; e < D * D; e += 32) W.Cm[e / D][e % D] = W.C[e / D][e % D];
+            for (int i = lane; i < D; i += 32) W.bm[i] = W.b[i];
+        }
+        __syncwarp();
+        if (kind == 3) {   // the global first step: x^- = 0, P^- = P_inf
+            for (int e = lane; e < D * D; e += 32) gb.gc0[e] = W.Cm[e / D][e % D];
+            break;
+        }
+        if (kind == 0) {
+            wmm<D>(W.T, W.Cm, W.FP, nullptr, lane);                  // C^- F P_{k-1}
+            __syncwarp();
+            for (int e = lane; e < D * D; e += 32) {
+                const int i = e / D, j = e - (e / D) * D;
+                W.Z[i][j] += fma(W.bm[i], W.xp[j], 2.0 * W.T[i][j]);
+                W.Cs[i][j] += W.Cm[i][j];
+            }
+            __syncwarp();
+            wmm<D>(W.T, W.Cm, M.F, nullptr, lane);                   // C^- F
+            for (int i = lane; i < D; i += 32) {
+                double s2 = 0.0;
+                for (int q = 0; q < D; ++q) s2 = fma(M.F[q][i], W.bm[q], s2);
+                W.b[i] = s2;                                          // F^T b^-
+            }
+            __syncwarp();
+            wmm<D, true, false>(W.Pm, M.F, W.T, nullptr, lane);      // F^T C^- F
+            __syncwarp();
+            for (int e = lane; e < D * D; e += 32) {
+                const int i = e / D, j = e - (e / D) * D;
+                W.C[i][j] = 0.5 * (W.Pm[i][j] + W.Pm[j][i]);
+            }
+        } else {
+            for (int e = lane; e < D * D; e += 32) W.C[e / D][e % D] = W.Cm[e / D][e % D];
+            for (int i = lane; i < D; i += 32) W.b[i] = W.bm[i];
+        }
+        __syncwarp();
+    }
+    double* o = gb.gpart + static_cast<int64_t>(c) * GPN(D);
+    for (int e = lane; e < D * D; e += 32) {
+        o[e] = W.Z[e / D][e % D];
+        o[D * D + e] = W.Cs[e / D][e % D];
+    }
+    if (lane == 0) o[2 * D * D] = gr;
+}
+
+// d NLL / d theta_p = <dF_p, Z> + <dQ_p, Cs> + <dP_inf_p, C0>  (p < npar - 1), r gr (log noise):
+// fixed-order sums of the chain partials, then one warp per parameter.  <<<1, 256>>>.
+template <int D>
+__global__ void __launch_bounds__(256) k_grad_contract(const double* __restrict__ gpart, int nch,
+                                                       const double* __restrict__ gc0,
+                                                       const double* __restrict__ gder, int npar, double r,
+                                                       double* grad) {
+    __shared__ double tot[GPN(D)];
+    for (int e = threadIdx.x; e < GPN(D); e += blockDim.x) {
+        double s2 = 0.0;
+        for (int c = 0; c < nch; ++c) s2 += gpart[static_cast<int64_t>(c) * GPN(D) + e];
+        tot[e] = s2;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int pp = wid; pp < npar; pp += blockDim.x / 32) {
+        double acc = 0.0;
+        if (pp < npar - 1) {
+            const double* dd = gder + static_cast<int64_t>(pp) * 3 * D * D;
+            for (int e = lane; e < D * D; e += 32)
+                acc += dd[e] * tot[e] + dd[D * D + e] * tot[D * D + e] + dd[2 * D * D + e] * gc0[e];
+        } else if (lane == 0) {
+            acc = r * tot[2 * D * D];
+        }
+        acc = wsum(acc);
+        if (lane == 0) grad[pp] = acc;
+    }
+}
+
 }  // namespace wide
 }  // namespace pssgp

@@ -44,6 +44,9 @@ void wide_set_smem_attrs(int device) {
     cudaFuncSetAttribute(kw_scan_filter<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(ScanSmemF<D>));
     cudaFuncSetAttribute(kw_scan_smoother<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(ScanSmemS<D>));
     cudaFuncSetAttribute(kw_discretize<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(KDSmem<D>));
+    cudaFuncSetAttribute(kw_grad_forward<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(GFwdSmem<D>));
+    cudaFuncSetAttribute(kw_grad_backward<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(GBwdSmem<D>));
+    cudaFuncSetAttribute(kw_scan_adjoint<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(ScanSmemA<D>));
     done.fetch_or(bit);
 }
 
@@ -453,6 +456,99 @@ pssgp_status wide_shard_sapply(pssgp_model* m, int64_t k0, int64_t n, int64_t Ng
     // total NLL: fixed-order sum over ranks of the partials carried in the gathered blobs
     if (nll) return nll_sum(m, static_cast<const double*>(all) + pssgp::wide::SNW(D), world, nll, s,
                             pssgp::wide::SNW(D) + 1);
+    return PSSGP_OK;
+}
+
+
+// ---- NLL gradient of any model on a uniform grid (pssgp_nll_grad): primal fold +
+// chain scan, forward rescan composing the chain adjoint maps, their reverse scan, backward
+// rescan accumulating (Z, Cs, gr, C0), contraction with the per-parameter dF, dQ, dP_inf.
+template <int D>
+pssgp_status wide_nll_grad(pssgp_model* m, int64_t N, const double* t, const double* y, const uint8_t* mask,
+                           double* nll, double* grad, cudaStream_t s) {
+    using namespace pssgp::wide;
+    const int npar = static_cast<int>(m->pder.size()) + 1;
+    if (m->mode != kTable)
+        return fail(m, PSSGP_E_UNSUPPORTED, "the gradient of this model needs a uniform grid (options.uniform_dt > 0)");
+    if (N == 0) {
+        cudaError_t e = cudaMemsetAsync(grad, 0, npar * sizeof(double), s);
+        if (e == cudaSuccess && nll) e = cudaMemsetAsync(nll, 0, sizeof(double), s);
+        return e == cudaSuccess ? PSSGP_OK : cuda_fail(m, e, "cudaMemsetAsync");
+    }
+    if (!m->d_gder) {   // dF_p, dQ_p at uniform_dt (Van Loan tangent, long double) and dP_inf_p
+        const int d = m->d;
+        std::vector<double> hbuf(static_cast<size_t>(npar - 1) * 3 * d * d);
+        for (int pp = 0; pp + 1 < npar; ++pp) {
+            pssgp_host::Mat F, Q, dF, dQ;
+            pssgp_host::van_loan_tangent(m->ssm.G, m->ssm.W, m->pder[pp].dG, m->pder[pp].dW, d,
+                                         static_cast<pssgp_host::ld>(m->udt), F, Q, dF, dQ);
+            for (int e = 0; e < d * d; ++e) {
+                hbuf[(static_cast<size_t>(pp) * 3 + 0) * d * d + e] = static_cast<double>(dF[e]);
+                hbuf[(static_cast<size_t>(pp) * 3 + 1) * d * d + e] = static_cast<double>(dQ[e]);
+                hbuf[(static_cast<size_t>(pp) * 3 + 2) * d * d + e] = static_cast<double>(m->pder[pp].dP[e]);
+            }
+        }
+        if (cudaMalloc(&m->d_gder, std::max<size_t>(1, hbuf.size()) * sizeof(double)) != cudaSuccess) {
+            cudaGetLastError();
+            m->d_gder = nullptr;
+            return fail(m, PSSGP_E_NOMEM, "cudaMalloc(gradient model)");
+        }
+        if (!hbuf.empty()) cudaMemcpy(m->d_gder, hbuf.data(), hbuf.size() * sizeof(double), cudaMemcpyHostToDevice);
+    }
+    const WPlan pl = make_wplan<D>(m, N);
+    WParams p;
+    pssgp_status st = wide_setup<D>(m, pl, p);
+    if (st) return st;
+    p.t = t; p.y = y; p.mask = mask;
+    p.n = N; p.k0 = 0; p.nglob = N;
+    p.store_state = 1;
+    const size_t nch = static_cast<size_t>(pl.nch);
+    const size_t need = (nch * CNW(D) + nch * GPN(D) + D * D + 8) * sizeof(double);
+    if (need > m->gw_bytes) {
+        if (m->gw) cudaFree(m->gw);
+        m->gw = nullptr;
+        m->gw_bytes = 0;
+        if (cudaMalloc(&m->gw, need) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(m, PSSGP_E_NOMEM, "cudaMalloc(gradient workspace)");
+        }
+        m->gw_bytes = need;
+    }
+    GradBufs gb;
+    gb.gagg = p.sagg;
+    gb.gbuf = p.sbuf;
+    gb.gcar = reinterpret_cast<double*>(m->gw);
+    gb.gpart = gb.gcar + nch * CNW(D);
+    gb.gc0 = gb.gpart + nch * GPN(D);
+    if ((st = wide_fold<D>(m, p, pl.nb, s))) return st;
+    p.fagg = wide_scan_f<D>(m, p, s, st);
+    if (st) return st;
+    {
+        ProfScope ps(m, S_K3, s);
+        kw_grad_forward<D><<<pl.nb, 32 * kWWarps, sizeof(GFwdSmem<D>), s>>>(p, gb);
+        LAUNCH_CHECK(m, "kw_grad_forward");
+    }
+    double* in = gb.gagg;
+    double* out = gb.gbuf;
+    {
+        ProfScope ps(m, S_K4, s);
+        for (int off = 1; off < p.nch; off <<= 1) {
+            kw_scan_adjoint<D><<<p.nch, 32, sizeof(ScanSmemA<D>), s>>>(in, out, p.nch, off);
+            std::swap(in, out);
+        }
+        LAUNCH_CHECK(m, "kw_scan_adjoint");
+    }
+    {
+        ProfScope ps(m, S_GRAD, s);
+        kw_grad_backward<D><<<pl.nb, 32 * kWWarps, sizeof(GBwdSmem<D>), s>>>(p, gb, in);
+        LAUNCH_CHECK(m, "kw_grad_backward");
+    }
+    {
+        ProfScope ps(m, S_RED, s);
+        k_grad_contract<D><<<1, 256, 0, s>>>(gb.gpart, p.nch, gb.gc0, m->d_gder, npar, m->r, grad);
+        LAUNCH_CHECK(m, "k_grad_contract");
+    }
+    if (nll) return nll_sum(m, p.nll_chain, p.nch, nll, s);
     return PSSGP_OK;
 }
 

@@ -2,12 +2,12 @@
 (oracle/grad.py): complex-step sequential filter for N up to a few 10^4 and the
 dense R&W Eq. (5.9) gradient for small N.
 
-Tolerance: each component g_j is a sum of N
-per-step terms of either sign; fp64 rounding of the tangent recursion gives an
-error ~ eps * cond * sum_k |term_k|, so the bar is
-    |g_gpu - g_ref| <= GRAD_TOL * (|g_ref| + N_obs)
-with GRAD_TOL = 1e-10 (per-step terms are O(1) for these workloads; measured
-errors are ~1e-15 relative to |g_ref|, tools/grad_errors.py)."""
+Tolerance: each component g_j is a sum of N per-step terms of either
+sign, so a component can be small against the others; the bar is per component,
+    |g_gpu,j - g_ref,j| <= GRAD_TOL * (|g_ref,j| + 1e-3 max_i |g_ref,i|) + 1e-12
+with GRAD_TOL = 1e-9 (measured errors ~1e-15 relative to |g_ref,j|, tools/grad_errors.py): a
+component is checked to 9 digits unless it is below 1e-3 of the largest, and then to 12 digits of
+the largest."""
 import numpy as np
 import pytest
 import torch
@@ -18,7 +18,7 @@ import paper_2102_09964_b200 as P
 
 pytestmark = pytest.mark.gpu
 
-GRAD_TOL = 1e-10
+GRAD_TOL = 1e-9
 NLL_TOL = 1e-9
 
 
@@ -37,11 +37,16 @@ def assert_grad(w, ref=None, **kw):
         ref = og.kf_nll_grad(c.kind, c.variance, c.lengthscale, w.noise_var, w.t, w.y, w.mask)
     nll_r, g_r = ref
     nll, g = gpu_grad(w, **kw)
-    nobs = int(w.mask.sum())
     assert abs(nll - nll_r) <= NLL_TOL * max(abs(nll_r), 1.0), (nll, nll_r)
-    err = np.abs(g - g_r) / (np.abs(g_r) + nobs + 1)
+    err = grad_err(g, g_r)
     assert np.all(err <= GRAD_TOL), (g, g_r, err)
     return err
+
+
+def grad_err(g, g_r):
+    """Per-component error in units of the bar (see the module docstring)."""
+    scale = np.abs(g_r) + 1e-3 * np.max(np.abs(g_r)) + 1e-12 / GRAD_TOL
+    return np.abs(g - g_r) / scale
 
 
 @pytest.mark.parametrize("kind", ["matern12", "matern32", "matern52"])
@@ -210,3 +215,76 @@ def test_grad_batched_invalid_offsets_and_missing_series(cuda_device):
         nll_r, g_r = og.kf_nll_grad(c.kind, c.variance, c.lengthscale, w.noise_var, w.t, w.y, w.mask)
         assert abs(nll[b] - nll_r) <= NLL_TOL * max(abs(nll_r), 1.0)
         assert np.all(np.abs(g[b] - g_r) / (np.abs(g_r) + w.mask.sum() + 1) <= GRAD_TOL)
+
+
+# ---------------------------------------------------------------- any model (reverse mode, uniform grids)
+GENERAL = {
+    # the paper's CO2 model C_Per x C_Mat + C_Mat, n_x = 10 / 14 / 18, weekly grid
+    "co2_J1": lambda n: synth.co2_product(n=n, order=1),
+    "co2_J2": lambda n: synth.co2_product(n=n, order=2),
+    "co2_J3": lambda n: synth.co2_product(n=n, order=3),
+    # BASELINE C4 shape: periodic J = 6 + Matern-3/2 trend (d = 16), weekly cadence
+    "c4": lambda n: synth.config4(n=n),
+    # C3 shape: RBF Taylor order 6 (d = 6), uniform fine grid
+    "c3": lambda n: synth.config3(n=n),
+    # d <= 3 models other than one Matern component
+    "rbf3": lambda n: _uniform_w([synth.Component("rbf", 1.3, 0.8, order=3)], 0.02, n, 0.01),
+    "m12+m12": lambda n: _uniform_w([synth.Component("matern12", 1.0, 0.3), synth.Component("matern12", 0.5, 3.0)],
+                                    0.05, n, 0.02),
+    "per1+m32_sum": lambda n: _uniform_w([synth.Component("periodic", 1.5, 1.0, period=0.7, order=1),
+                                          synth.Component("matern32", 1.0, 2.0)], 0.05, n, 0.013),
+}
+
+
+def _uniform_w(comps, r, n, dt, seed=4):
+    t = np.arange(n, dtype=np.float64) * dt
+    rng = np.random.default_rng(seed)
+    mask = (rng.random(n) >= 0.15).astype(np.uint8)
+    y = synth.sinusoid(t) + np.sqrt(r) * rng.standard_normal(n)
+    y[mask == 0] = np.nan
+    return synth.Workload("uniform", comps, r, t, y, mask, uniform_dt=dt)
+
+
+def assert_grad_general(w, **kw):
+    nll_r, g_r = og.kf_nll_grad_general(w.components, w.noise_var, w.t, w.y, w.mask)
+    nll, g = gpu_grad(w, **kw)
+    assert g.shape == g_r.shape == (len(og.param_names(w.components)),)
+    assert abs(nll - nll_r) <= NLL_TOL * max(abs(nll_r), 1.0), (nll, nll_r)
+    err = grad_err(g, g_r)
+    assert np.all(err <= GRAD_TOL), (g, g_r, err)
+
+
+@pytest.mark.parametrize("name,n", [("co2_J1", 3192), ("co2_J2", 3192), ("co2_J3", 3192), ("c4", 2000),
+                                    ("c3", 3001), ("rbf3", 2500), ("m12+m12", 2500), ("per1+m32_sum", 2500)])
+def test_grad_general_models(cuda_device, name, n):
+    """f1 widened: the paper's HMC model (CO2 product), the C4 sum,
+    RBF, and d <= 3 sums against the complex-step oracle of any SSM."""
+    assert_grad_general(GENERAL[name](n))
+
+
+@pytest.mark.parametrize("chain_len", [1, 7, 64])
+def test_grad_general_chain_lengths(cuda_device, chain_len):
+    """Many chains: the reverse scan of the chain adjoint maps over several levels."""
+    assert_grad_general(GENERAL["co2_J1"](1500), chain_len=chain_len)
+
+
+def test_grad_general_ties_and_edges(cuda_device):
+    """dt = 0 steps (no theta dependence, adjoint passes through), first point missing, N = 1, 2."""
+    w = GENERAL["per1+m32_sum"](700)
+    w.t[100:104] = w.t[100]
+    w.t[104:] -= 3 * w.uniform_dt
+    w.mask[0] = 0
+    w.y[0] = np.nan
+    assert_grad_general(w, chain_len=5)
+    for n in (1, 2):
+        assert_grad_general(GENERAL["co2_J1"](n))
+
+
+def test_grad_general_needs_uniform_grid(cuda_device):
+    comps = [synth.Component("rbf", 1.0, 0.5, order=4)]
+    w = _uniform_w(comps, 0.02, 100, 0.01)
+    m = P.Model(comps, 0.02)                         # no uniform_dt: per-step device discretisation
+    t, y, mk = (torch.from_numpy(a).to("cuda:0") for a in (w.t, w.y, w.mask))
+    with pytest.raises(P.PssgpError) as e:
+        m.nll_grad(t, y, mk)
+    assert e.value.status == 6                       # PSSGP_E_UNSUPPORTED

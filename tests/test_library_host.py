@@ -187,8 +187,21 @@ def test_host_side_argument_errors():
     assert lib.pssgp_predict(m.h, 4, None, ptr, 1, ptr, ptr, ptr, ptr, None) == _native.PSSGP_E_ARG
     assert lib.pssgp_posterior_batched(m.h, 0, ptr, None, None, None, 4, ptr, ptr, ptr, ptr, ptr, ptr,
                                        None) == _native.PSSGP_E_ARG                                # nseg < 1
-    r = P.Model([synth.Component("rbf", 1.0, 0.5, order=3)], 0.1, uniform_dt=0.01)
+    r = P.Model([synth.Component("rbf", 1.0, 0.5, order=3)], 0.1)      # no uniform grid declared
     assert lib.pssgp_nll_grad(r.h, 4, ptr, ptr, ptr, ptr, ptr, None) == _native.PSSGP_E_UNSUPPORTED
     assert lib.pssgp_posterior_batched(r.h, 1, ptr, None, None, None, 4, ptr, ptr, ptr, ptr, ptr, ptr,
                                        None) == _native.PSSGP_E_UNSUPPORTED
     assert P.pssgp_last_error(r.h) != ""
+
+
+def test_num_params_order():
+    """pssgp_num_params (include/pssgp.h): 2 per Matern / RBF, 3 per periodic, 4 per quasi-periodic,
+    + log noise - the order of oracle.grad.param_names."""
+    from oracle import grad as og
+    for comps in ([synth.Component("matern52", 1.0, 0.5)],
+                  [synth.Component("periodic", 4.0, 1.0, period=1.0, order=6), synth.Component("matern32", 10.0, 20.0)],
+                  [synth.Component("quasiperiodic", 2.0, 1.0, period=52.0, order=2, mat_lengthscale=300.0, mat_nu2=3),
+                   synth.Component("matern32", 10.0, 1040.0)],
+                  [synth.Component("rbf", 1.0, 0.5, order=6)]):
+        m = P.Model(comps, 0.1, uniform_dt=0.01)
+        assert m.num_params == len(og.param_names(comps))
