@@ -96,14 +96,6 @@ def test_grad_nll_equals_posterior_nll(cuda_device):
     assert nll == float(nll2.cpu()[0])
 
 
-def test_grad_unsupported_model(cuda_device):
-    w = synth.config3()
-    m = P.Model(w.components, w.noise_var, uniform_dt=w.uniform_dt)
-    t, y, mk = (torch.from_numpy(a[:64]).to("cuda:0") for a in (w.t, w.y, w.mask))
-    with pytest.raises(P.PssgpError):
-        m.nll_grad(t, y, mk)
-
-
 def _batched_problem(kind, lens, seed=31):
     rng = np.random.default_rng(seed)
     ws = []
@@ -276,8 +268,11 @@ def test_grad_general_ties_and_edges(cuda_device):
     w.mask[0] = 0
     w.y[0] = np.nan
     assert_grad_general(w, chain_len=5)
-    for n in (1, 2):
-        assert_grad_general(GENERAL["co2_J1"](n))
+    for n in (1, 2, 3):
+        w = GENERAL["per1+m32_sum"](n)
+        w.mask[:] = 1
+        w.y = synth.sinusoid(w.t)
+        assert_grad_general(w)
 
 
 def test_grad_general_needs_uniform_grid(cuda_device):
