@@ -23,11 +23,6 @@ namespace ph = pssgp_host;
 
 
 
-namespace {
-const char* kSlotNames[kSlots] = {"k_filter_reduce", "k_filter_scan", "k_filter_apply",
-                                  "k_smoother_scan", "k_smoother_apply", "k_nll_sum", "k_reduce_blocks",
-                                  "k_grad_fold", "k_discretize"};
-}  // namespace
 
 namespace pssgp_internal {
 pssgp_status ensure_device(pssgp_model* m) {
@@ -40,12 +35,13 @@ pssgp_status ensure_device(pssgp_model* m) {
     m->device = dev;
     e = cudaDeviceGetAttribute(&m->sm_count, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) return cuda_fail(m, e, "cudaDeviceGetAttribute");
-    // word 0: latched error; 1: K3 publication flag; 2: K3 tile ticket; then 8 scratch doubles
-    e = cudaMalloc(&m->d_err, 3 * sizeof(unsigned long long) + 8 * sizeof(double));
+    // word 0: latched error; 1..4: K3 publication flag, tile ticket, published-block and finished-CTA
+    // counters (pssgp_kernels.cuh KParams::flag); then 8 scratch doubles
+    e = cudaMalloc(&m->d_err, 8 * sizeof(unsigned long long) + 8 * sizeof(double));
     if (e != cudaSuccess) return fail(m, PSSGP_E_NOMEM, "cudaMalloc(error word)");
     cudaMemset(m->d_err, 0xff, sizeof(unsigned long long));
-    cudaMemset(m->d_err + 1, 0, 2 * sizeof(unsigned long long));   // K3 publication flag, ticket
-    m->d_scalar = reinterpret_cast<double*>(m->d_err + 3);
+    cudaMemset(m->d_err + 1, 0, 7 * sizeof(unsigned long long));
+    m->d_scalar = reinterpret_cast<double*>(m->d_err + 8);
     return PSSGP_OK;
 }
 
@@ -192,6 +188,37 @@ pssgp_status phase_filter_apply(pssgp_model* m, KParams<D>& p, cudaStream_t s, b
     return PSSGP_OK;
 }
 
+// single-pass K1 + K3 (k_filter_fused) instead of two launches: PSSGP_FUSED=1 (A/B)
+bool fused_filter() {
+    static const bool v = [] { const char* e = getenv("PSSGP_FUSED"); return e && *e == '1'; }();
+    return v;
+}
+
+// the cooperative launch needs the whole grid resident (one-wave plans are, forced chain lengths
+// may not be: those take the two-launch path)
+template <int D>
+bool fused_fits(pssgp_model* m, int nb) {
+    int occ = 0;
+    if (m->mode == kClosed) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_filter_fused<D, kClosed>, kThreads, 0);
+    else if (m->mode == kPade) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_filter_fused<D, kPade>, kThreads, 0);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_filter_fused<D, kTable>, kThreads, 0);
+    return nb <= occ * m->sm_count;
+}
+
+template <int D>
+pssgp_status phase_filter_fused(pssgp_model* m, KParams<D>& p, cudaStream_t s) {
+    ProfScope ps(m, S_K3, s);
+    p.fused = 1;
+    void* args[] = {&p};
+    const void* fn = (m->mode == kClosed) ? reinterpret_cast<const void*>(k_filter_fused<D, kClosed>)
+                     : (m->mode == kPade) ? reinterpret_cast<const void*>(k_filter_fused<D, kPade>)
+                                          : reinterpret_cast<const void*>(k_filter_fused<D, kTable>);
+    const cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(p.nb), dim3(kThreads), args, 0, s);
+    p.fused = 0;
+    if (e != cudaSuccess) return cuda_fail(m, e, "k_filter_fused (cooperative launch)");
+    return PSSGP_OK;
+}
+
 template <int D>
 pssgp_status phase_smoother(pssgp_model* m, KParams<D>& p, cudaStream_t s) {
     ProfScope ps(m, S_K5, s);
@@ -226,8 +253,12 @@ pssgp_status run_posterior(pssgp_model* m, int64_t N, const double* t, const dou
     p.n = N; p.k0 = 0; p.nglob = N;
     p.mean = mean; p.var = var;
     p.store_state = smooth ? 1 : 0;
-    if ((st = phase_filter_reduce<D>(m, p, s))) return st;
-    if ((st = phase_filter_apply<D>(m, p, s))) return st;
+    if (smooth && fused_filter() && fused_fits<D>(m, p.nb)) {
+        if ((st = phase_filter_fused<D>(m, p, s))) return st;
+    } else {
+        if ((st = phase_filter_reduce<D>(m, p, s))) return st;
+        if ((st = phase_filter_apply<D>(m, p, s))) return st;
+    }
     if (smooth) {
         p.nll_out = nll;                       // K5's CTA 0 sums the NLL partials
         if ((st = phase_smoother<D>(m, p, s))) return st;
@@ -451,6 +482,7 @@ int pssgp_state_dim(const pssgp_model* m) { return m ? m->d : -1; }
 
 pssgp_status pssgp_posterior(pssgp_model* m, int64_t N, const double* t, const double* y, const uint8_t* mask,
                              double* mean, double* var, double* nll, void* stream) {
+    NvtxCall nvtx_("pssgp_posterior");
     pssgp_status st = check_args(m, N, t, y, mask);
     if (st) return st;
     if ((st = ensure_device(m))) return st;
@@ -463,6 +495,7 @@ pssgp_status pssgp_posterior(pssgp_model* m, int64_t N, const double* t, const d
 
 pssgp_status pssgp_nll(pssgp_model* m, int64_t N, const double* t, const double* y, const uint8_t* mask,
                        double* nll, void* stream) {
+    NvtxCall nvtx_("pssgp_nll");
     pssgp_status st = check_args(m, N, t, y, mask);
     if (st) return st;
     if (!nll) return fail(m, PSSGP_E_ARG, "nll is NULL");
@@ -491,6 +524,7 @@ Plan make_plan_f32(pssgp_model* m, int64_t N) {
 
 pssgp_status pssgp_posterior_f32(pssgp_model* m, int64_t N, const double* t, const double* y, const uint8_t* mask,
                                  double* mean, double* var, double* nll, void* stream) {
+    NvtxCall nvtx_("pssgp_posterior_f32");
     pssgp_status st = check_args(m, N, t, y, mask);
     if (st) return st;
     if (!m->closed || m->d > 3)
@@ -561,6 +595,7 @@ pssgp_status pssgp_posterior_f32(pssgp_model* m, int64_t N, const double* t, con
 
 pssgp_status pssgp_nll_grad(pssgp_model* m, int64_t N, const double* t, const double* y, const uint8_t* mask,
                             double* nll, double* grad, void* stream) {
+    NvtxCall nvtx_("pssgp_nll_grad");
     pssgp_status st = check_args(m, N, t, y, mask);
     if (st) return st;
     if (!grad) return fail(m, PSSGP_E_ARG, "grad is NULL");
@@ -614,6 +649,7 @@ pssgp_status pssgp_gather(pssgp_model* m, int64_t n_test, const int64_t* test_in
 pssgp_status pssgp_predict(pssgp_model* m, int64_t n_train, const double* t_train, const double* y_train,
                            int64_t n_test, const double* t_test, double* mean_test, double* var_test, double* nll,
                            void* stream) {
+    NvtxCall nvtx_("pssgp_predict");
     if (!m) return PSSGP_E_ARG;
     if (n_train < 0 || n_test < 0) return fail(m, PSSGP_E_ARG, "negative size");
     if ((n_train > 0 && (!t_train || !y_train)) || (n_test > 0 && (!t_test || !mean_test || !var_test)))
@@ -656,6 +692,7 @@ pssgp_status pssgp_posterior_batched(pssgp_model* m, int nseg, const int64_t* of
                                      const double* lengthscale, const double* noise_var, int64_t N,
                                      const double* t, const double* y, const uint8_t* mask, double* mean,
                                      double* var, double* nll, void* stream) {
+    NvtxCall nvtx_("pssgp_posterior_batched");
     pssgp_status st = check_args(m, N, t, y, mask);
     if (st) return st;
     if (nseg < 1 || !offsets || !nll) return fail(m, PSSGP_E_ARG, "bad batched arguments");
@@ -720,6 +757,7 @@ pssgp_status pssgp_posterior_batched(pssgp_model* m, int nseg, const int64_t* of
 pssgp_status pssgp_nll_grad_batched(pssgp_model* m, int nseg, const int64_t* offsets, const double* variance,
                                     const double* lengthscale, const double* noise_var, int64_t N, const double* t,
                                     const double* y, const uint8_t* mask, double* nll, double* grad, void* stream) {
+    NvtxCall nvtx_("pssgp_nll_grad_batched");
     pssgp_status st = check_args(m, N, t, y, mask);
     if (st) return st;
     if (nseg < 1 || !offsets || !nll || !grad) return fail(m, PSSGP_E_ARG, "bad batched-gradient arguments");
@@ -878,7 +916,7 @@ pssgp_status pssgp_check(pssgp_model* m) {
     if (e != cudaSuccess) return cuda_fail(m, e, "cudaMemcpy(error word)");
     if (w == ~0ULL) return PSSGP_OK;
     cudaMemset(m->d_err, 0xff, sizeof(unsigned long long));
-    cudaMemset(m->d_err + 1, 0, 2 * sizeof(unsigned long long));   // K3 publication flag, ticket
+    cudaMemset(m->d_err + 1, 0, 7 * sizeof(unsigned long long));   // K3 publication flag, ticket, counters
     const unsigned code = static_cast<unsigned>(w & 0xff);
     const int64_t idx = static_cast<int64_t>((w >> 8) & 0xffffffffffffULL);
     const char* what = code == kErrInput ? "invalid input (unsorted/non-finite t or non-finite observed y)"
@@ -1111,7 +1149,7 @@ int pssgp_profile_read(pssgp_model* m, double* ms, int64_t* launches, int cap) {
     return n;
 }
 
-const char* pssgp_profile_name(int slot) { return (slot >= 0 && slot < kSlots) ? kSlotNames[slot] : ""; }
+const char* pssgp_profile_name(int slot) { return slot_name(slot); }
 
 // ---------------------------------------------------------------- sharded path
 size_t pssgp_aggregate_bytes(const pssgp_model* m, int which) {
@@ -1204,6 +1242,7 @@ extern "C" {
 
 pssgp_status pssgp_shard_filter_reduce(pssgp_model* m, int64_t k0, int64_t n, int64_t N_global, const double* t,
                                        const double* y, const uint8_t* mask, void* filt_agg_out, void* stream) {
+    NvtxCall nvtx_("pssgp_shard_filter_reduce");
     pssgp_status st = shard_args(m, k0, n, N_global, t);
     if (st) return st;
     if (!y || !mask || !filt_agg_out) return fail(m, PSSGP_E_ARG, "NULL argument");
@@ -1217,6 +1256,7 @@ pssgp_status pssgp_shard_filter_reduce(pssgp_model* m, int64_t k0, int64_t n, in
 pssgp_status pssgp_shard_filter_apply(pssgp_model* m, int64_t k0, int64_t n, int64_t N_global, const double* t,
                                       const double* y, const uint8_t* mask, const void* all_filt_aggs, int rank,
                                       int world, void* smooth_agg_out, double* nll_partial, void* stream) {
+    NvtxCall nvtx_("pssgp_shard_filter_apply");
     pssgp_status st = shard_args(m, k0, n, N_global, t);
     if (st) return st;
     if (!y || !mask || !all_filt_aggs || !smooth_agg_out || rank < 0 || rank >= world)
@@ -1236,6 +1276,7 @@ pssgp_status pssgp_shard_filter_apply(pssgp_model* m, int64_t k0, int64_t n, int
 pssgp_status pssgp_shard_smoother_apply(pssgp_model* m, int64_t k0, int64_t n, int64_t N_global, const double* t,
                                         const void* all_smooth_aggs, int rank, int world, double* mean, double* var,
                                         double* nll, void* stream) {
+    NvtxCall nvtx_("pssgp_shard_smoother_apply");
     pssgp_status st = shard_args(m, k0, n, N_global, t);
     if (st) return st;
     if (!all_smooth_aggs || rank < 0 || rank >= world) return fail(m, PSSGP_E_ARG, "bad argument");

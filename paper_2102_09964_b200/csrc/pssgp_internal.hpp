@@ -9,6 +9,8 @@
 #include <utility>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/pssgp.h"
 #include "host_model.hpp"
 #include "pssgp_dims.h"
@@ -101,12 +103,22 @@ inline cudaEvent_t get_event(pssgp_model* m) {
     return e;
 }
 
+inline const char* slot_name(int slot) {
+    static const char* names[kSlots] = {"k_filter_reduce", "k_filter_scan", "k_filter_apply",
+                                        "k_smoother_scan", "k_smoother_apply", "k_nll_sum", "k_reduce_blocks",
+                                        "k_grad_fold", "k_discretize"};
+    return (slot >= 0 && slot < kSlots) ? names[slot] : "";
+}
+
+// One phase of a call: an NVTX range named after the profile slot (seen by nsys / ncu --nvtx; a no-op
+// without a tool attached) and, when profiling is enabled, CUDA events on the launch stream.
 struct ProfScope {
     pssgp_model* m;
     int slot;
     cudaStream_t s;
     cudaEvent_t a = nullptr;
     ProfScope(pssgp_model* m_, int slot_, cudaStream_t s_) : m(m_), slot(slot_), s(s_) {
+        nvtxRangePushA(slot_name(slot));
         if (m->prof) {
             a = get_event(m);
             cudaEventRecord(a, s);
@@ -118,7 +130,14 @@ struct ProfScope {
             cudaEventRecord(b, s);
             m->ev[slot].emplace_back(a, b);
         }
+        nvtxRangePop();
     }
+};
+
+// NVTX range around one C-ABI call (the pipeline stage of PAPER.md:168-172 it runs)
+struct NvtxCall {
+    explicit NvtxCall(const char* name) { nvtxRangePushA(name); }
+    ~NvtxCall() { nvtxRangePop(); }
 };
 
 #define LAUNCH_CHECK(m, where)                                    \

@@ -106,10 +106,23 @@ struct KParams {
     double* nll_out;        // nll scalar output (nullable)
     unsigned long long* err;
     int store_state;        // K3: write (xbar, P) and smoother aggregates (0 for NLL-only)
+    int fused;              // k_filter_fused (single pass): the carry scan waits for every block aggregate
     unsigned long long* flag;   // flag[0]: K3 block-carry publication word (set to 1 by logical CTA 0);
-                                // flag[1]: K3 tile ticket (logical CTA index = arrival order).  Both reset
-                                // to 0 by K1 (stream-ordered, so CUDA-graph replays are safe).
+                                // flag[1]: K3 tile ticket (logical CTA index = arrival order); both reset
+                                // to 0 by K1 (stream-ordered, so CUDA-graph replays are safe).  Single-pass
+                                // kernel: flag[2] counts published block aggregates, flag[3] finished
+                                // CTAs; the last CTA to finish resets flag[0..3].
 };
+
+// The last CTA of a K3 / single-pass launch resets the publication word, ticket and counters, so
+// every launch starts from zero whichever kernel ran before (K1 also resets flag[0..1]).
+__device__ __forceinline__ void k3_finish(unsigned long long* flag, int nb) {
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(flag + 3, 1ull) == static_cast<unsigned long long>(nb) - 1) {
+        flag[0] = 0ull; flag[1] = 0ull; flag[2] = 0ull; flag[3] = 0ull;
+        __threadfence();
+    }
+}
 
 // K3's logical CTA index: the arrival order of the CTAs (an atomic ticket), so the CTA that scans
 // the block aggregates and publishes every CTA's carry (logical 0) is the first one that ever ran.
@@ -159,6 +172,13 @@ __device__ __forceinline__ void load_aos(T& a, const real* base) {
     real* d = reinterpret_cast<real*>(&a);
 #pragma unroll
     for (int i = 0; i < n; ++i) d[i] = base[i];
+}
+template <typename T>
+__device__ __forceinline__ void load_aos_cg(T& a, const real* base) {   // L2 (written by other CTAs)
+    constexpr int n = sizeof(T) / sizeof(real);
+    real* d = reinterpret_cast<real*>(&a);
+#pragma unroll
+    for (int i = 0; i < n; ++i) d[i] = __ldcg(base + i);
 }
 template <typename T>
 __device__ __forceinline__ void store_aos(const T& a, real* base) {
@@ -312,18 +332,16 @@ __device__ __forceinline__ unsigned long long mask_word(const uint8_t* __restric
 }
 
 // ------------------------------------------------------------------ K1: fold chains
+// K1 body for logical CTA `bid` (the kernel below, and the fused single-pass k_filter_fused)
 template <int D, int MODE>
-__global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_reduce(const KParams<D> p) {
-    __shared__ AsyncStage st[kWarps];
-    __shared__ FAgg<D> wagg[kWarps];
+__device__ __forceinline__ void k1_body(const KParams<D>& p, int bid, AsyncStage* st, FAgg<D>* wagg) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int64_t c = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
+    const int64_t c = static_cast<int64_t>(bid) * kThreads + threadIdx.x;
     const int64_t nch = static_cast<int64_t>(p.nb) * kThreads;
-    const int64_t wbase = (static_cast<int64_t>(blockIdx.x) * kThreads + wid * 32) * p.K;
+    const int64_t wbase = (static_cast<int64_t>(bid) * kThreads + wid * 32) * p.K;
     const int64_t kb = c * p.K;
     const int64_t ke = min(kb + p.K, p.n);
 
-    if (blockIdx.x == 0 && threadIdx.x == 0) { p.flag[0] = 0ull; p.flag[1] = 0ull; }   // K3 publication word, ticket
     FAgg<D> a;
     set_identity(a);
     double tprev = 0.0;
@@ -412,8 +430,16 @@ set_zero(F);
             acc = r;
         }
         if (!ok) raise_error(p.err, p.k0 + kb, kErrNumeric);
-        store_aos(acc, p.block_f + static_cast<int64_t>(blockIdx.x) * FN(D));
+        store_aos(acc, p.block_f + static_cast<int64_t>(bid) * FN(D));
     }
+}
+
+template <int D, int MODE>
+__global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_reduce(const KParams<D> p) {
+    __shared__ AsyncStage st[kWarps];
+    __shared__ FAgg<D> wagg[kWarps];
+    if (blockIdx.x == 0 && threadIdx.x == 0) { p.flag[0] = 0ull; p.flag[1] = 0ull; }   // K3 publication word, ticket
+    k1_body<D, MODE>(p, blockIdx.x, st, wagg);
 }
 
 // ------------------------------------------------------------------ CTA-wide ordered reductions
@@ -545,13 +571,21 @@ __device__ __forceinline__ Gauss<D> filter_chain_carry(const KParams<D>& p, FAgg
     Gauss<D> cur;
     bool ok = true;
     if (bid == 0) {
+        if (p.fused) {
+            // single-pass kernel: every CTA of the (cooperative, co-resident) grid publishes its block
+            // aggregate before counting itself in flag[2]; logical CTA 0 scans once all have
+            if (threadIdx.x == 0)
+                while (atomicAdd(p.flag + 2, 0ull) < static_cast<unsigned long long>(p.nb)) __nanosleep(32);
+            __syncthreads();
+            __threadfence();
+        }
         const int per = (p.nb + kThreads - 1) / kThreads;
         const int b0 = min(static_cast<int>(threadIdx.x) * per, p.nb), b1 = min(b0 + per, p.nb);
         FAgg<D> a;
         set_identity(a);
         for (int b = b0; b < b1; ++b) {
             FAgg<D> e, r;
-            load_aos(e, p.block_f + static_cast<int64_t>(b) * FN(D));
+            load_aos_cg(e, p.block_f + static_cast<int64_t>(b) * FN(D));
             ok = combine(a, e, r) && ok;
             a = r;
         }
@@ -596,7 +630,7 @@ __device__ __forceinline__ Gauss<D> filter_chain_carry(const KParams<D>& p, FAgg
         for (int b = b0; b < b1; ++b) {
             store_aos(C, p.fcarry + static_cast<int64_t>(b) * CN(D));
             FAgg<D> e;
-            load_aos(e, p.block_f + static_cast<int64_t>(b) * FN(D));
+            load_aos_cg(e, p.block_f + static_cast<int64_t>(b) * FN(D));
             Gauss<D> r2;
             ok = apply_prefix(C, e, r2) && ok;
             C = r2;
@@ -659,15 +693,9 @@ __device__ __forceinline__ Gauss<D> filter_chain_carry(const KParams<D>& p, FAgg
 // ------------------------------------------------------------------ K3: Kalman rescan
 // STORE = false (NLL only): no filtered-state stores; SAGG = false: no smoother-aggregate
 // moments / aggregates (NLL only, and the gradient's primal pass which needs only the stores).
-template <int D, int MODE, bool STORE = true, bool SAGG = STORE>
-__global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KParams<D> p) {
-    __shared__ AsyncStage st[kWarps];
-    __shared__ FAgg<D> tot[kWarps];
-    __shared__ Gauss<D> wcar[kWarps];
-    __shared__ SAgg<D> stot[kWarps];
-    __shared__ double nred[kWarps];
-    __shared__ int s_bid;
-    const int bid = k3_ticket(p.flag, &s_bid);               // logical CTA index (arrival order)
+template <int D, int MODE, bool STORE, bool SAGG>
+__device__ __forceinline__ void k3_body(const KParams<D>& p, int bid, AsyncStage* st, FAgg<D>* tot, Gauss<D>* wcar,
+                                        SAgg<D>* stot, double* nred) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t c = static_cast<int64_t>(bid) * kThreads + threadIdx.x;
     const int64_t nch = static_cast<int64_t>(p.nb) * kThreads;
@@ -877,6 +905,46 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
             store_aos(acc, p.block_s + static_cast<int64_t>(bid) * SN(D));
         }
     }
+}
+
+template <int D, int MODE, bool STORE = true, bool SAGG = STORE>
+__global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KParams<D> p) {
+    __shared__ AsyncStage st[kWarps];
+    __shared__ FAgg<D> tot[kWarps];
+    __shared__ Gauss<D> wcar[kWarps];
+    __shared__ SAgg<D> stot[kWarps];
+    __shared__ double nred[kWarps];
+    __shared__ int s_bid;
+    const int bid = k3_ticket(p.flag, &s_bid);               // logical CTA index (arrival order)
+    k3_body<D, MODE, STORE, SAGG>(p, bid, st, tot, wcar, stot, nred);
+    k3_finish(p.flag, p.nb);
+}
+
+// ------------------------------------------------------------------ single-pass K1 + K3 (A/B variant)
+// The fold and the Kalman rescan in ONE launch (north_star's single-pass scan): each CTA folds its
+// chains and publishes its block aggregate (flag[2] counts them), logical CTA 0 scans all block
+// aggregates once every CTA has published and publishes the collapsed carries (flag[0]), every CTA
+// then rescans its chains - the inter-CTA exchange of the separate K1 / K3 launches done in place.
+// A look-back in which CTA i combines the aggregates of its predecessors itself would serialise
+// ~nb general operators (~1 us each at d = 3) on the last CTA, so the prefix scan stays with one CTA.
+// Needs every CTA co-resident: launched cooperatively (the one-wave plan fits by construction).
+template <int D, int MODE>
+__global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_fused(const KParams<D> p) {
+    __shared__ AsyncStage st[kWarps];
+    __shared__ FAgg<D> tot[kWarps];
+    __shared__ Gauss<D> wcar[kWarps];
+    __shared__ SAgg<D> stot[kWarps];
+    __shared__ double nred[kWarps];
+    __shared__ int s_bid;
+    const int bid = k3_ticket(p.flag, &s_bid);
+    k1_body<D, MODE>(p, bid, st, tot);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(p.flag + 2, 1ull);                          // block aggregate published
+    }
+    k3_body<D, MODE, true, true>(p, bid, st, tot, wcar, stot, nred);
+    k3_finish(p.flag, p.nb);
 }
 
 // Collapsed global suffix (m^s, P^s) after chain c (smoothed state at the first
