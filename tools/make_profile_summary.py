@@ -1,7 +1,7 @@
 """Build the committed ncu summary for one profiling round from tools/profile_round.sh output.
 
 usage: python tools/make_profile_summary.py gpurun_out/TAG profiles/ROUND N [TAG]
-Writes profiles/TAG/ncu_full_TAG_summary.csv (per hot kernel: duration, DRAM bytes in GB, fp64 pipe
+Writes profiles/TAG/ncu_full_TAG_summary.csv (per hot kernel: duration in us, DRAM bytes in GB, fp64 pipe
 and issue utilisation, stall ratios, executed fp64 instructions and flops per time step from the
 SASS source page), copies the launch list and the bench line."""
 import csv
@@ -14,6 +14,7 @@ src, dst, N = sys.argv[1], sys.argv[2], float(sys.argv[3])
 tag = sys.argv[4] if len(sys.argv) > 4 else os.path.basename(src.rstrip("/"))
 os.makedirs(dst, exist_ok=True)
 SCALE = {"byte": 1e-9, "Kbyte": 1e-6, "Mbyte": 1e-3, "Gbyte": 1.0, "Tbyte": 1e3}
+TSCALE = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
            "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
            "smsp__issue_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
@@ -58,6 +59,8 @@ for raw in sorted(glob.glob(os.path.join(src, "raw_*.csv"))):
         val = float(v[i])
         if m.startswith("dram__bytes"):
             val *= SCALE[u[i]]           # -> GB
+        if m == "gpu__time_duration.sum":
+            val *= TSCALE[u[i]]          # -> us
         rec[m] = val
     s = os.path.join(src, f"src_{k}.csv")
     if os.path.exists(s):
