@@ -208,6 +208,9 @@ bool fused_fits(pssgp_model* m, int nb) {
 template <int D>
 pssgp_status phase_filter_fused(pssgp_model* m, KParams<D>& p, cudaStream_t s) {
     ProfScope ps(m, S_K3, s);
+    // flag[0..3] from zero whichever kernel ran last (K3 leaves its publication word and ticket set)
+    cudaError_t e0 = cudaMemsetAsync(p.flag, 0, 4 * sizeof(unsigned long long), s);
+    if (e0 != cudaSuccess) return cuda_fail(m, e0, "cudaMemsetAsync(flags)");
     p.fused = 1;
     void* args[] = {&p};
     const void* fn = (m->mode == kClosed) ? reinterpret_cast<const void*>(k_filter_fused<D, kClosed>)

@@ -325,7 +325,6 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_batch_filter_apply(con
         }
         store_aos(acc, p.block_s + static_cast<int64_t>(bid) * SN(D));
     }
-    k3_finish(p.flag, p.nb);
 }
 
 // ------------------------------------------------------------------ K5b: RTS rescan

@@ -114,8 +114,8 @@ struct KParams {
                                 // CTAs; the last CTA to finish resets flag[0..3].
 };
 
-// The last CTA of a K3 / single-pass launch resets the publication word, ticket and counters, so
-// every launch starts from zero whichever kernel ran before (K1 also resets flag[0..1]).
+// The last CTA of a single-pass launch resets the publication word, ticket and counters (the host
+// also zeroes them before each single-pass launch; K1 resets flag[0..1] before every K3).
 __device__ __forceinline__ void k3_finish(unsigned long long* flag, int nb) {
     __syncthreads();
     if (threadIdx.x == 0 && atomicAdd(flag + 3, 1ull) == static_cast<unsigned long long>(nb) - 1) {
@@ -917,7 +917,6 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_apply(const KPa
     __shared__ int s_bid;
     const int bid = k3_ticket(p.flag, &s_bid);               // logical CTA index (arrival order)
     k3_body<D, MODE, STORE, SAGG>(p, bid, st, tot, wcar, stot, nred);
-    k3_finish(p.flag, p.nb);
 }
 
 // ------------------------------------------------------------------ single-pass K1 + K3 (A/B variant)
