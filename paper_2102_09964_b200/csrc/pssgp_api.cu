@@ -211,13 +211,11 @@ pssgp_status phase_filter_fused(pssgp_model* m, KParams<D>& p, cudaStream_t s) {
     // flag[0..3] from zero whichever kernel ran last (K3 leaves its publication word and ticket set)
     cudaError_t e0 = cudaMemsetAsync(p.flag, 0, 4 * sizeof(unsigned long long), s);
     if (e0 != cudaSuccess) return cuda_fail(m, e0, "cudaMemsetAsync(flags)");
-    p.fused = 1;
     void* args[] = {&p};
     const void* fn = (m->mode == kClosed) ? reinterpret_cast<const void*>(k_filter_fused<D, kClosed>)
                      : (m->mode == kPade) ? reinterpret_cast<const void*>(k_filter_fused<D, kPade>)
                                           : reinterpret_cast<const void*>(k_filter_fused<D, kTable>);
     const cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(p.nb), dim3(kThreads), args, 0, s);
-    p.fused = 0;
     if (e != cudaSuccess) return cuda_fail(m, e, "k_filter_fused (cooperative launch)");
     return PSSGP_OK;
 }

@@ -106,7 +106,6 @@ struct KParams {
     double* nll_out;        // nll scalar output (nullable)
     unsigned long long* err;
     int store_state;        // K3: write (xbar, P) and smoother aggregates (0 for NLL-only)
-    int fused;              // k_filter_fused (single pass): the carry scan waits for every block aggregate
     unsigned long long* flag;   // flag[0]: K3 block-carry publication word (set to 1 by logical CTA 0);
                                 // flag[1]: K3 tile ticket (logical CTA index = arrival order); both reset
                                 // to 0 by K1 (stream-ordered, so CUDA-graph replays are safe).  Single-pass
@@ -557,7 +556,7 @@ __device__ __forceinline__ void nll_accumulate(bool obs, double v, double vs, do
 
 // Collapsed global prefix (xbar, P) entering chain c (the block scan spread over
 // CTAs + the CTA's chain scan); shared scratch tot[kWarps], wcar[kWarps].
-template <int D>
+template <int D, bool FUSED = false>
 __device__ __forceinline__ Gauss<D> filter_chain_carry(const KParams<D>& p, FAgg<D>* tot, Gauss<D>* wcar, int64_t c,
                                                        int64_t nch, int lane, int wid, int bid) {
     // ---- collapsed prefix entering this CTA.  Logical CTA 0 (the first to arrive, k3_ticket) alone
@@ -571,7 +570,7 @@ __device__ __forceinline__ Gauss<D> filter_chain_carry(const KParams<D>& p, FAgg
     Gauss<D> cur;
     bool ok = true;
     if (bid == 0) {
-        if (p.fused) {
+        if (FUSED) {
             // single-pass kernel: every CTA of the (cooperative, co-resident) grid publishes its block
             // aggregate before counting itself in flag[2]; logical CTA 0 scans once all have
             if (threadIdx.x == 0)
@@ -585,7 +584,8 @@ __device__ __forceinline__ Gauss<D> filter_chain_carry(const KParams<D>& p, FAgg
         set_identity(a);
         for (int b = b0; b < b1; ++b) {
             FAgg<D> e, r;
-            load_aos_cg(e, p.block_f + static_cast<int64_t>(b) * FN(D));
+            if (FUSED) load_aos_cg(e, p.block_f + static_cast<int64_t>(b) * FN(D));   // written in this launch
+            else load_aos(e, p.block_f + static_cast<int64_t>(b) * FN(D));
             ok = combine(a, e, r) && ok;
             a = r;
         }
@@ -630,7 +630,8 @@ __device__ __forceinline__ Gauss<D> filter_chain_carry(const KParams<D>& p, FAgg
         for (int b = b0; b < b1; ++b) {
             store_aos(C, p.fcarry + static_cast<int64_t>(b) * CN(D));
             FAgg<D> e;
-            load_aos_cg(e, p.block_f + static_cast<int64_t>(b) * FN(D));
+            if (FUSED) load_aos_cg(e, p.block_f + static_cast<int64_t>(b) * FN(D));
+            else load_aos(e, p.block_f + static_cast<int64_t>(b) * FN(D));
             Gauss<D> r2;
             ok = apply_prefix(C, e, r2) && ok;
             C = r2;
@@ -693,7 +694,7 @@ __device__ __forceinline__ Gauss<D> filter_chain_carry(const KParams<D>& p, FAgg
 // ------------------------------------------------------------------ K3: Kalman rescan
 // STORE = false (NLL only): no filtered-state stores; SAGG = false: no smoother-aggregate
 // moments / aggregates (NLL only, and the gradient's primal pass which needs only the stores).
-template <int D, int MODE, bool STORE, bool SAGG>
+template <int D, int MODE, bool STORE, bool SAGG, bool FUSED = false>
 __device__ __forceinline__ void k3_body(const KParams<D>& p, int bid, AsyncStage* st, FAgg<D>* tot, Gauss<D>* wcar,
                                         SAgg<D>* stot, double* nred) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -704,7 +705,7 @@ __device__ __forceinline__ void k3_body(const KParams<D>& p, int bid, AsyncStage
     const int64_t kb = c * p.K;
     const int64_t ke = min(kb + p.K, p.n);
 
-    const Gauss<D> cur = filter_chain_carry<D>(p, tot, wcar, c, nch, lane, wid, bid);
+    const Gauss<D> cur = filter_chain_carry<D, FUSED>(p, tot, wcar, c, nch, lane, wid, bid);
 
     // ---- Kalman filter over the chain (supplement PAPER.md:285-315), carrying the
     // chain-entry moments E[x_k0 | y_1:k], Cov(x_k0 | y_1:k) and the cross-covariance
@@ -942,7 +943,7 @@ __global__ void __launch_bounds__(kThreads, PSSGP_MINB) k_filter_fused(const KPa
         __threadfence();
         atomicAdd(p.flag + 2, 1ull);                          // block aggregate published
     }
-    k3_body<D, MODE, true, true>(p, bid, st, tot, wcar, stot, nred);
+    k3_body<D, MODE, true, true, true>(p, bid, st, tot, wcar, stot, nred);
     k3_finish(p.flag, p.nb);
 }
 
