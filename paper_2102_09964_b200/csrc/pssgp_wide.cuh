@@ -881,21 +881,27 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WMINB) kw_filter_fold(cons
 constexpr int kQ = 4, kGL = 8;
 // staging slot of one step's (F_k, Q_k) record: only the per-step (STREAM) kernels reserve it
 PS_CX int FQS(int D, bool stream) { return stream ? FQW(D) : 1; }
-template <int D, bool STREAM>
+template <int D, bool STREAM, int G = kGL, int WPC = kWWarps>
 struct K1LSmem {
+    static constexpr int NP = 32 / G;
     SModel<D> m;
     double I[D][LD(D)], Z[D][LD(D)];
     struct PerWarp {
-        SF<D> q[kQ];
+        SF<D> q[NP];
         SCombF<D> s;
-        double U[kQ][D][LD(D)];
-        double fqs[kQ][2][FQS(D, STREAM)];         // STREAM: each quarter's (F_k, Q_k) staged one step ahead
-    } w[kWWarps];
+        double U[NP][D][LD(D)];
+        double fqs[NP][2][FQS(D, STREAM)];         // STREAM: each quarter's (F_k, Q_k) staged one step ahead
+    } w[WPC];
 };
 
 #ifndef PSSGP_WLPR_MINB
 #define PSSGP_WLPR_MINB 3                        // resident CTAs/SM the lane-per-row fold is register-capped for
 #endif
+// lane-per-row kernels with G-lane groups: G = 8 (D <= 8, four quarter chains per warp, 4 warps per CTA)
+// or G = 16 (9 <= D <= 16, two half chains per warp, 2 warps per CTA: the per-warp shared state of
+// d = 16 would otherwise cap residency at one CTA per SM); register cap 168 / 255
+PS_CX int lpr_minb(int G) { return G == kGL ? PSSGP_WLPR_MINB : 4; }
+PS_CX unsigned group_mask(int G, int gb) { return (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << gb; }
 
 // ------------------------------------------------------------------ KDl: lane-per-row discretisation
 // The same algorithm as kw_discretize (Taylor expm of G tau and the Van Loan series of Q_tau, then s
@@ -1040,11 +1046,12 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WDISC_MINB) kw_discretize_
         }
     }
 }
-template <int D, bool STREAM>
-__global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_filter_fold_lpr(const WParams p) {
-    static_assert(D <= kGL, "lane-per-row fold holds one row per lane of an 8-lane group");
+template <int D, bool STREAM, int G = kGL, int WPC = kWWarps>
+__global__ void __launch_bounds__(32 * WPC, lpr_minb(G)) kw_filter_fold_lpr(const WParams p) {
+    static_assert(D <= G, "lane-per-row fold holds one row per lane of a G-lane group");
+    constexpr int NP = 32 / G;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    K1LSmem<D, STREAM>& sh = *reinterpret_cast<K1LSmem<D, STREAM>*>(smem_raw);
+    K1LSmem<D, STREAM, G, WPC>& sh = *reinterpret_cast<K1LSmem<D, STREAM, G, WPC>*>(smem_raw);
     load_model<D>(sh.m, p.model);
     for (int e = threadIdx.x; e < D * D; e += blockDim.x) {
         const int i = e / D, j = e - (e / D) * D;
@@ -1053,16 +1060,16 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_filter_fold_
     }
     __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int c = blockIdx.x * kWWarps + wid;
+    const int c = blockIdx.x * WPC + wid;
     if (c >= p.nch) return;                                     // warp-uniform
-    const int q = lane / kGL, r = lane % kGL, gb = q * kGL;
+    const int q = lane / G, r = lane % G, gb = q * G;
     const bool act = r < D;
     const int rr = act ? r : 0;                                 // row addressed by idle lanes
     auto& W = sh.w[wid];
     const SModel<D>& M = sh.m;
     const int64_t kb = static_cast<int64_t>(c) * p.K;
     const int64_t ke = min(kb + p.K, p.n);
-    const int64_t Kq = (p.K + kQ - 1) / kQ;
+    const int64_t Kq = (p.K + NP - 1) / NP;
     const int64_t qb = min(kb + q * Kq, ke), qe = min(qb + Kq, ke);
 
     double Ac[D], Cr[D], Jr[D], b = 0.0, eta = 0.0;
@@ -1076,7 +1083,7 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_filter_fold_
     auto& fqs = W.fqs[q];
     if (STREAM) {
         if (qb < qe)
-            for (int i = r; i < FQW(D); i += kGL) cp_async8(&fqs[0][i], p.fq + qb * FQW(D) + i, 8);
+            for (int i = r; i < FQW(D); i += G) cp_async8(&fqs[0][i], p.fq + qb * FQW(D) + i, 8);
         cp_async_commit();
     }
     for (int64_t j = 0; j < Kq; ++j) {
@@ -1087,7 +1094,7 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_filter_fold_
             cp_async_wait<0>();
             __syncwarp();
             if (k + 1 < qe)
-                for (int i = r; i < FQW(D); i += kGL) cp_async8(&fqs[fb ^ 1][i], p.fq + (k + 1) * FQW(D) + i, 8);
+                for (int i = r; i < FQW(D); i += G) cp_async8(&fqs[fb ^ 1][i], p.fq + (k + 1) * FQW(D) + i, 8);
             cp_async_commit();
         }
         const bool valid = k < qe;
@@ -1156,7 +1163,7 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_filter_fold_
         if (!act) { HC = 0.0; w = 0.0; Fb = 0.0; }
         double S = hr * HC, hb = hr * Fb;
 #pragma unroll
-        for (int off = kGL / 2; off > 0; off >>= 1) {
+        for (int off = G / 2; off > 0; off >>= 1) {
             S += __shfl_xor_sync(0xffffffffu, S, off);
             hb += __shfl_xor_sync(0xffffffffu, hb, off);
         }
@@ -1190,15 +1197,15 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_filter_fold_
     __syncwarp();
     bool ok = true;
 #pragma unroll 1
-    for (int i = 1; i < kQ; ++i) {
+    for (int i = 1; i < NP; ++i) {
         // W.q[i - 1] is the prefix q0 (x) ... (x) q_{i-1}: the quarter rescans start from the
         // chain carry applied to it (kw_filter_apply_q)
-        if (p.qagg) gstore<D>(W.q[i - 1], p.qagg + (static_cast<int64_t>(c) * (kQ - 1) + (i - 1)) * FNW(D), lane);
+        if (p.qagg) gstore<D>(W.q[i - 1], p.qagg + (static_cast<int64_t>(c) * (NP - 1) + (i - 1)) * FNW(D), lane);
         ok = wcombine<D>(W.q[i - 1], W.q[i], W.q[i], W.s, lane) && ok;
         __syncwarp();
     }
     if (!ok && lane == 0) raise_error(p.err, p.k0 + kb, kErrNumeric);
-    gstore<D>(W.q[kQ - 1], p.fagg + static_cast<int64_t>(c) * FNW(D), lane);
+    gstore<D>(W.q[NP - 1], p.fagg + static_cast<int64_t>(c) * FNW(D), lane);
 }
 
 // ------------------------------------------------------------------ Kogge-Stone scan levels (1 warp per element)
@@ -2082,8 +2089,9 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_smoother_app
 // smoothed state after quarter q is the chain's suffix carry applied through the smoother
 // aggregates of the later quarters.  All four groups of a warp are busy (the
 // lane-per-row rescans kept one group busy per chain).
-__device__ __forceinline__ void quarter_bounds(int64_t kb, int64_t ke, int64_t K, int q, int64_t& qb, int64_t& qe) {
-    const int64_t Kq = (K + kQ - 1) / kQ;
+__device__ __forceinline__ void quarter_bounds(int64_t kb, int64_t ke, int64_t K, int q, int64_t& qb, int64_t& qe,
+                                               int np = kQ) {
+    const int64_t Kq = (K + np - 1) / np;
     qb = min(kb + q * Kq, ke);
     qe = min(qb + Kq, ke);
 }
@@ -2178,21 +2186,22 @@ __device__ void quarter_sagg(const WParams& p, const SModel<D>& M, const double 
 }
 
 // ------------------------------------------------------------------ K3q: quarter-parallel Kalman rescan
-template <int D, bool STREAM>
+template <int D, bool STREAM, int G = kGL, int WPC = kWWarps>
 struct K3QSmem {
+    static constexpr int NP = 32 / G;
     SModel<D> m;
     double I[D][LD(D)], Z[D][LD(D)];
     struct PerWarp {
-        double cx[kQ][D];                          // filtered state entering each quarter
-        double cP[kQ][D][LD(D)];
+        double cx[NP][D];                          // filtered state entering each quarter
+        double cP[NP][D][LD(D)];
         union {
             struct {                               // carry phase
                 SF<D> a;
                 SCombF<D> s;
             } c;
             struct {                               // step phase, one slot per group
-                double U[kQ][D][LD(D)];
-                double fqs[kQ][2][FQS(D, STREAM)];
+                double U[NP][D][LD(D)];
+                double fqs[NP][2][FQS(D, STREAM)];
             } st;
             struct {                               // quarter smoother aggregates, one quarter at a time
                 double P[D][LD(D)], Sg[D][LD(D)], P0[D][LD(D)];
@@ -2202,14 +2211,15 @@ struct K3QSmem {
                 SCombF<D> s;
             } ag;
         } u;
-    } w[kWWarps];
+    } w[WPC];
 };
 
-template <int D, bool STREAM>
-__global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_filter_apply_q(const WParams p) {
-    static_assert(D <= kGL, "one row per lane of an 8-lane group");
+template <int D, bool STREAM, int G = kGL, int WPC = kWWarps>
+__global__ void __launch_bounds__(32 * WPC, lpr_minb(G)) kw_filter_apply_q(const WParams p) {
+    static_assert(D <= G, "one row per lane of a G-lane group");
+    constexpr int NP = 32 / G;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    K3QSmem<D, STREAM>& sh = *reinterpret_cast<K3QSmem<D, STREAM>*>(smem_raw);
+    K3QSmem<D, STREAM, G, WPC>& sh = *reinterpret_cast<K3QSmem<D, STREAM, G, WPC>*>(smem_raw);
     load_model<D>(sh.m, p.model);
     for (int e = threadIdx.x; e < D * D; e += blockDim.x) {
         const int i = e / D, j = e - (e / D) * D;
@@ -2218,7 +2228,7 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_filter_apply
     }
     __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int c = blockIdx.x * kWWarps + wid;
+    const int c = blockIdx.x * WPC + wid;
     if (c >= p.nch) return;                                     // warp-uniform
     auto& W = sh.w[wid];
     const SModel<D>& M = sh.m;
@@ -2238,22 +2248,22 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_filter_apply
         gload<D>(W.u.c.a, p.fagg + static_cast<int64_t>(c - 1) * FNW(D), lane);
         ok = wapply_prefix<D>(W.cx[0], W.cP[0], W.u.c.a, W.u.c.s, lane) && ok;
     }
-    for (int q = 1; q < kQ; ++q) {
+    for (int q = 1; q < NP; ++q) {
         for (int e = lane; e < D * D; e += 32) W.cP[q][e / D][e % D] = W.cP[0][e / D][e % D];
         for (int i = lane; i < D; i += 32) W.cx[q][i] = W.cx[0][i];
         __syncwarp();
-        gload<D>(W.u.c.a, p.qagg + (static_cast<int64_t>(c) * (kQ - 1) + (q - 1)) * FNW(D), lane);
+        gload<D>(W.u.c.a, p.qagg + (static_cast<int64_t>(c) * (NP - 1) + (q - 1)) * FNW(D), lane);
         ok = wapply_prefix<D>(W.cx[q], W.cP[q], W.u.c.a, W.u.c.s, lane) && ok;
     }
     if (!ok && lane == 0) raise_error(p.err, p.k0 + kb, kErrNumeric);
 
     // ---- the four quarters, one per 8-lane group, in registers
-    const int q = lane / kGL, r0 = lane % kGL, gb = q * kGL;
-    const unsigned gm = 0xFFu << gb;
+    const int q = lane / G, r0 = lane % G, gb = q * G;
+    const unsigned gm = group_mask(G, gb);
     const bool act = r0 < D;
     const int r = act ? r0 : 0;
     int64_t qb, qe;
-    quarter_bounds(kb, ke, p.K, q, qb, qe);
+    quarter_bounds(kb, ke, p.K, q, qb, qe, NP);
     double Pr[D], Sgr[D], P0r[D], xr = W.cx[q][r], x0r = 0.0;
 #pragma unroll
     for (int j = 0; j < D; ++j) { Pr[j] = W.cP[q][r][j]; Sgr[j] = 0.0; P0r[j] = 0.0; }
@@ -2272,7 +2282,7 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_filter_apply
     auto& fqs = W.u.st.fqs[q];
     if (STREAM) {
         if (qb < qe)
-            for (int i = r0; i < FQW(D); i += kGL) cp_async8(&fqs[0][i], p.fq + qb * FQW(D) + i, 8);
+            for (int i = r0; i < FQW(D); i += G) cp_async8(&fqs[0][i], p.fq + qb * FQW(D) + i, 8);
         cp_async_commit();
     }
     for (int64_t k = qb; k < qe; ++k) {
@@ -2282,7 +2292,7 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_filter_apply
             cp_async_wait<0>();
             __syncwarp(gm);
             if (k + 1 < qe)
-                for (int i = r0; i < FQW(D); i += kGL) cp_async8(&fqs[fb ^ 1][i], p.fq + (k + 1) * FQW(D) + i, 8);
+                for (int i = r0; i < FQW(D); i += G) cp_async8(&fqs[fb ^ 1][i], p.fq + (k + 1) * FQW(D) + i, 8);
             cp_async_commit();
         }
         const double tk = tn_;
@@ -2313,7 +2323,7 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_filter_apply
             Uc[i] = su;
         }
 #pragma unroll
-        for (int qq = 0; qq < D; ++qq) xm = fma(Fp[r * LD(D) + qq], __shfl_sync(gm, xr, qq, kGL), xm);
+        for (int qq = 0; qq < D; ++qq) xm = fma(Fp[r * LD(D) + qq], __shfl_sync(gm, xr, qq, G), xm);
         if (act) {
 #pragma unroll
             for (int i = 0; i < D; ++i) U[i][r] = Uc[i];
@@ -2338,7 +2348,7 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_filter_apply
         if (!act) { HP = 0.0; SH = 0.0; }
         double S = hr * HP, hx = hr * xm;
 #pragma unroll
-        for (int off = kGL / 2; off > 0; off >>= 1) {
+        for (int off = G / 2; off > 0; off >>= 1) {
             S += __shfl_xor_sync(gm, S, off);
             hx += __shfl_xor_sync(gm, hx, off);
         }
@@ -2350,8 +2360,8 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_filter_apply
         const double HPs = HP * iS, SHs = SH * iS;
 #pragma unroll
         for (int j = 0; j < D; ++j) {
-            const double HPj = __shfl_sync(gm, HP, j, kGL);
-            const double SHj = __shfl_sync(gm, SH, j, kGL);
+            const double HPj = __shfl_sync(gm, HP, j, G);
+            const double SHj = __shfl_sync(gm, SH, j, G);
             const double Pn = fma(-HPs, HPj, Pm[j]);
             Pr[j] = Pn;
             if (first) {
@@ -2384,7 +2394,7 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_filter_apply
         double nl = nobs ? 0.5 * (quad + logs + nobs * 1.8378770664093453) : 0.0;
         double tot = 0.0;
 #pragma unroll
-        for (int qq = 0; qq < kQ; ++qq) tot += __shfl_sync(0xffffffffu, nl, qq * kGL);
+        for (int qq = 0; qq < NP; ++qq) tot += __shfl_sync(0xffffffffu, nl, qq * G);
         if (lane == 0) p.nll_chain[c] = tot;
     }
     if (!p.store_state) return;
@@ -2393,7 +2403,7 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_filter_apply
     SS<D>* acc = &W.u.ag.acc;
     SS<D>* cur = &W.u.ag.cur;
 #pragma unroll 1
-    for (int qq = 0; qq < kQ; ++qq) {
+    for (int qq = 0; qq < NP; ++qq) {
         if (q == qq && act) {
 #pragma unroll
             for (int j = 0; j < D; ++j) {
@@ -2406,11 +2416,11 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_filter_apply
         }
         __syncwarp();
         int64_t sb, se;
-        quarter_bounds(kb, ke, p.K, qq, sb, se);
-        const double tpq = __shfl_sync(0xffffffffu, tq, qq * kGL);
+        quarter_bounds(kb, ke, p.K, qq, sb, se, NP);
+        const double tpq = __shfl_sync(0xffffffffu, tq, qq * G);
         quarter_sagg<D>(p, M, W.u.ag.P, W.u.ag.x, W.u.ag.Sg, W.u.ag.P0, W.u.ag.x0, sb, se, tpq, *cur, W.u.ag.w, lane);
         if (qq > 0) {
-            gstore<D>(*cur, p.sqagg + (static_cast<int64_t>(c) * (kQ - 1) + (qq - 1)) * SNW(D), lane);
+            gstore<D>(*cur, p.sqagg + (static_cast<int64_t>(c) * (NP - 1) + (qq - 1)) * SNW(D), lane);
             __syncwarp();
             wcombine<D>(*acc, *cur, *cur, W.u.ag.s, lane);   // acc (x) cur, earlier quarter on the left
         }
@@ -2421,13 +2431,14 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_filter_apply
 }
 
 // ------------------------------------------------------------------ K5q: quarter-parallel RTS rescan
-template <int D, bool STREAM>
+template <int D, bool STREAM, int G = kGL, int WPC = kWWarps>
 struct K5QSmem {
+    static constexpr int NP = 32 / G;
     SModel<D> m;
     double I[D][LD(D)], Z[D][LD(D)];
     struct PerWarp {
-        double cm[kQ][D];                          // smoothed state after each quarter
-        double cP[kQ][D][LD(D)];
+        double cm[NP][D];                          // smoothed state after each quarter
+        double cP[NP][D][LD(D)];
         union {
             struct {                               // carry phase
                 SS<D> a;
@@ -2436,18 +2447,20 @@ struct K5QSmem {
             struct Grp {                           // step phase, one slot per group
                 double xst[2][CNW(D)];             // staged packed (xbar, P) records (cp.async)
                 double U[D][LD(D)], Pm[D][LD(D)], Ps[D][LD(D)] /* P^s_{k+1} - P^- */, X[D][LD(D)];
+                double L[G > kGL ? D : 1][LD(D)];  // 16-lane groups: the Cholesky factor of P^-
                 double dm[D];
                 double fqs[2][FQS(D, STREAM)];     // STREAM: (F_{k+1}, Q_{k+1}) staged with record k
-            } g[kQ];
+            } g[NP];
         } u;
-    } w[kWWarps];
+    } w[WPC];
 };
 
-template <int D, bool STREAM>
-__global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_smoother_apply_q(const WParams p) {
-    static_assert(D <= kGL, "one row per lane of an 8-lane group");
+template <int D, bool STREAM, int G = kGL, int WPC = kWWarps>
+__global__ void __launch_bounds__(32 * WPC, lpr_minb(G)) kw_smoother_apply_q(const WParams p) {
+    static_assert(D <= G, "one row per lane of a G-lane group");
+    constexpr int NP = 32 / G;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    K5QSmem<D, STREAM>& sh = *reinterpret_cast<K5QSmem<D, STREAM>*>(smem_raw);
+    K5QSmem<D, STREAM, G, WPC>& sh = *reinterpret_cast<K5QSmem<D, STREAM, G, WPC>*>(smem_raw);
     load_model<D>(sh.m, p.model);
     for (int e = threadIdx.x; e < D * D; e += blockDim.x) {
         const int i = e / D, j = e - (e / D) * D;
@@ -2456,7 +2469,7 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_smoother_app
     }
     __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int c = blockIdx.x * kWWarps + wid;
+    const int c = blockIdx.x * WPC + wid;
     if (c >= p.nch) return;
     auto& W = sh.w[wid];
     const SModel<D>& M = sh.m;
@@ -2464,31 +2477,31 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_smoother_app
     const int64_t ke = min(kb + p.K, p.n);
     // ---- carries: collapsed suffix after the chain (incoming sharded, scanned chains > c), then
     // back through the smoother aggregates of quarters 3, 2, 1 (kw_filter_apply_q)
-    auto& c3P = W.cP[kQ - 1];
+    auto& c3P = W.cP[NP - 1];
     for (int e = lane; e < D * D; e += 32) c3P[e / D][e % D] = 0.0;
-    for (int i = lane; i < D; i += 32) W.cm[kQ - 1][i] = 0.0;
+    for (int i = lane; i < D; i += 32) W.cm[NP - 1][i] = 0.0;
     __syncwarp();
     for (int g = p.world - 1; g > p.rank && p.in_smooth; --g) {
         gload<D>(W.u.c.a, p.in_smooth + static_cast<int64_t>(g) * (SNW(D) + 1), lane);   // blob = aggregate + NLL partial
-        wapply_suffix<D>(W.u.c.a, W.cm[kQ - 1], c3P, W.u.c.s, lane);
+        wapply_suffix<D>(W.u.c.a, W.cm[NP - 1], c3P, W.u.c.s, lane);
     }
     if (c + 1 < p.nch) {
         gload<D>(W.u.c.a, p.sagg + static_cast<int64_t>(c + 1) * SNW(D), lane);
-        wapply_suffix<D>(W.u.c.a, W.cm[kQ - 1], c3P, W.u.c.s, lane);
+        wapply_suffix<D>(W.u.c.a, W.cm[NP - 1], c3P, W.u.c.s, lane);
     }
-    for (int q = kQ - 2; q >= 0; --q) {
+    for (int q = NP - 2; q >= 0; --q) {
         for (int e = lane; e < D * D; e += 32) W.cP[q][e / D][e % D] = W.cP[q + 1][e / D][e % D];
         for (int i = lane; i < D; i += 32) W.cm[q][i] = W.cm[q + 1][i];
         __syncwarp();
-        gload<D>(W.u.c.a, p.sqagg + (static_cast<int64_t>(c) * (kQ - 1) + q) * SNW(D), lane);   // quarter q + 1
+        gload<D>(W.u.c.a, p.sqagg + (static_cast<int64_t>(c) * (NP - 1) + q) * SNW(D), lane);   // quarter q + 1
         wapply_suffix<D>(W.u.c.a, W.cm[q], W.cP[q], W.u.c.s, lane);
     }
-    const int q = lane / kGL, r0 = lane % kGL, gb = q * kGL;
-    const unsigned gm = 0xFFu << gb;
+    const int q = lane / G, r0 = lane % G, gb = q * G;
+    const unsigned gm = group_mask(G, gb);
     const bool act = r0 < D;
     const int r = act ? r0 : 0;
     int64_t qb, qe;
-    quarter_bounds(kb, ke, p.K, q, qb, qe);
+    quarter_bounds(kb, ke, p.K, q, qb, qe, NP);
     double Psr[D], msr = W.cm[q][r];
 #pragma unroll
     for (int j = 0; j < D; ++j) Psr[j] = W.cP[q][r][j];
@@ -2500,10 +2513,10 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_smoother_app
     double tk_next = 0.0;
     if (qe > qb) {
         const double* src = xpc + (qe - 1 - kb) * CNW(D);
-        for (int i = r0; i < CNW(D); i += kGL) cp_async8(&Gs.xst[0][i], src + i, 8);
+        for (int i = r0; i < CNW(D); i += G) cp_async8(&Gs.xst[0][i], src + i, 8);
         if (STREAM && p.k0 + qe < p.nglob) {        // F, Q of the transition out of qe - 1 (record qe)
             const double* fsrc = p.fq + qe * FQW(D);
-            for (int i = r0; i < FQW(D); i += kGL) cp_async8(&Gs.fqs[0][i], fsrc + i, 8);
+            for (int i = r0; i < FQW(D); i += G) cp_async8(&Gs.fqs[0][i], fsrc + i, 8);
         }
         cp_async_commit();
         tk_next = __ldg(p.t + qe - 1);
@@ -2517,28 +2530,38 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_smoother_app
         __syncwarp(gm);
         if (k > qb) {
             const double* src = xpc + (k - 1 - kb) * CNW(D);
-            for (int i = r0; i < CNW(D); i += kGL) cp_async8(&Gs.xst[sb ^ 1][i], src + i, 8);
+            for (int i = r0; i < CNW(D); i += G) cp_async8(&Gs.xst[sb ^ 1][i], src + i, 8);
             if (STREAM) {                           // record k: the transition out of k - 1
                 const double* fsrc = p.fq + k * FQW(D);
-                for (int i = r0; i < FQW(D); i += kGL) cp_async8(&Gs.fqs[sb ^ 1][i], fsrc + i, 8);
+                for (int i = r0; i < FQW(D); i += G) cp_async8(&Gs.fqs[sb ^ 1][i], fsrc + i, 8);
             }
             cp_async_commit();
             tk_next = __ldg(p.t + k - 1);
         }
         const int fb = sb;
-        double xa[D], Pr[D];
-        {
-            const double* src = Gs.xst[sb];
+        // this step's filtered (xbar_k, row r of P_k): registers for 8-lane groups, read from the staged
+        // record on use for 16-lane groups (register budget of d = 16)
+        const double* rec = Gs.xst[sb];
+        double xa_r[G == kGL ? D : 1], Pr_r[G == kGL ? D : 1];
+        if constexpr (G == kGL) {
 #pragma unroll
-            for (int i = 0; i < D; ++i) xa[i] = src[i];
+            for (int i = 0; i < D; ++i) xa_r[i] = rec[i];
 #pragma unroll
-            for (int j = 0; j < D; ++j) Pr[j] = src[D + si(D, r, j)];
+            for (int j = 0; j < D; ++j) Pr_r[j] = rec[D + si(D, r, j)];
         }
+        auto XA = [&](int i) -> double {
+            if constexpr (G == kGL) return xa_r[i];
+            else return rec[i];
+        };
+        auto PR = [&](int j) -> double {
+            if constexpr (G == kGL) return Pr_r[j];
+            else return rec[D + si(D, r, j)];
+        };
         sb ^= 1;
         if (g == p.nglob - 1) {                     // terminal element: smoothed = filtered
 #pragma unroll
-            for (int j = 0; j < D; ++j) Psr[j] = Pr[j];
-            msr = xa[r];
+            for (int j = 0; j < D; ++j) Psr[j] = PR(j);
+            msr = XA(r);
         } else {
             const int kind = wdisc_kind(tnext - tk, M.udt, STREAM);
             const double* Fp;
@@ -2554,11 +2577,11 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_smoother_app
             for (int i = 0; i < D; ++i) {
                 double su = 0.0;
 #pragma unroll
-                for (int qq = 0; qq < D; ++qq) su = fma(Fp[i * LD(D) + qq], Pr[qq], su);
+                for (int qq = 0; qq < D; ++qq) su = fma(Fp[i * LD(D) + qq], PR(qq), su);
                 Uc[i] = su;
             }
 #pragma unroll
-            for (int qq = 0; qq < D; ++qq) xm = fma(Fp[r * LD(D) + qq], xa[qq], xm);
+            for (int qq = 0; qq < D; ++qq) xm = fma(Fp[r * LD(D) + qq], XA(qq), xm);
             if (act) {
 #pragma unroll
                 for (int i = 0; i < D; ++i) Gs.U[i][r] = Uc[i];
@@ -2579,59 +2602,106 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_smoother_app
                 Gs.dm[r] = msr - xm;
             }
             __syncwarp(gm);
-            double L[D][D], Li[D];
+            // column r of X = (P^-)^-1 F P: registers for 8-lane groups, the group's shared X (column r)
+            // for 16-lane groups
+            double Xc[G == kGL ? D : 1];
+            if constexpr (G == kGL) {
+                // D <= 8: every lane factors P^- itself (L in registers)
+                double L[D][D], Li[D];
 #pragma unroll
-            for (int j = 0; j < D; ++j) {
-                double sd = Gs.Pm[j][j];
+                for (int j = 0; j < D; ++j) {
+                    double sd = Gs.Pm[j][j];
 #pragma unroll
-                for (int qq = 0; qq < j; ++qq) sd = fma(-L[j][qq], L[j][qq], sd);
-                bad = bad || !(sd > 0.0);
-                Li[j] = rsqrt(sd);
+                    for (int qq = 0; qq < j; ++qq) sd = fma(-L[j][qq], L[j][qq], sd);
+                    bad = bad || !(sd > 0.0);
+                    Li[j] = rsqrt(sd);
 #pragma unroll
-                for (int i = j + 1; i < D; ++i) {
-                    double so = Gs.Pm[j][i];
+                    for (int i = j + 1; i < D; ++i) {
+                        double so = Gs.Pm[j][i];
 #pragma unroll
-                    for (int qq = 0; qq < j; ++qq) so = fma(-L[i][qq], L[j][qq], so);
-                    L[i][j] = so * Li[j];
+                        for (int qq = 0; qq < j; ++qq) so = fma(-L[i][qq], L[j][qq], so);
+                        L[i][j] = so * Li[j];
+                    }
+                    L[j][j] = sd * Li[j];
                 }
-                L[j][j] = sd * Li[j];
+#pragma unroll
+                for (int i = 0; i < D; ++i) {
+                    double z = Uc[i];
+#pragma unroll
+                    for (int qq = 0; qq < i; ++qq) z = fma(-L[i][qq], Xc[qq], z);
+                    Xc[i] = z * Li[i];
+                }
+#pragma unroll
+                for (int i = D - 1; i >= 0; --i) {
+                    double z = Xc[i];
+#pragma unroll
+                    for (int qq = i + 1; qq < D; ++qq) z = fma(-L[qq][i], Xc[qq], z);
+                    Xc[i] = z * Li[i];
+                }
+            } else {
+                // 9 <= D <= 16: cooperative left-looking Cholesky, lane r building row r of L in
+                // registers (row j of L from lane j by shuffles, column j's pivot from lane j), then
+                // L through shared memory for each lane's two triangular solves on its column
+                // (the diagonal slot of the shared factor holds 1 / L_jj: the solves never read L_jj)
+                double Lr[D];
+#pragma unroll
+                for (int j = 0; j < D; ++j) {
+                    double sv = Gs.Pm[r][j];
+#pragma unroll
+                    for (int qq = 0; qq < j; ++qq) sv = fma(-Lr[qq], __shfl_sync(gm, Lr[qq], j, G), sv);
+                    const double sj = __shfl_sync(gm, sv, j, G);
+                    bad = bad || !(sj > 0.0);
+                    const double lij = rsqrt(sj);
+                    Lr[j] = (r == j) ? lij : sv * lij;    // row r: L_rj (j < r), 1 / L_rr; j > r unused
+                }
+                if (act) {
+#pragma unroll
+                    for (int qq = 0; qq < D; ++qq) Gs.L[r][qq] = Lr[qq];
+                }
+                __syncwarp(gm);
+                // the two solves on column r, in place in the shared X (U still holds F P's columns)
+                if (act) {
+#pragma unroll 4
+                    for (int i = 0; i < D; ++i) {
+                        double z = Gs.U[i][r];
+                        for (int qq = 0; qq < i; ++qq) z = fma(-Gs.L[i][qq], Gs.X[qq][r], z);
+                        Gs.X[i][r] = z * Gs.L[i][i];
+                    }
+#pragma unroll 4
+                    for (int i = D - 1; i >= 0; --i) {
+                        double z = Gs.X[i][r];
+                        for (int qq = i + 1; qq < D; ++qq) z = fma(-Gs.L[qq][i], Gs.X[qq][r], z);
+                        Gs.X[i][r] = z * Gs.L[i][i];
+                    }
+                }
             }
-            double Xc[D];
+            auto XC = [&](int i) -> double {
+                if constexpr (G == kGL) return Xc[i];
+                else return Gs.X[i][r];
+            };
+            double ms_new = XA(r), V[D];
 #pragma unroll
-            for (int i = 0; i < D; ++i) {
-                double z = Uc[i];
-#pragma unroll
-                for (int qq = 0; qq < i; ++qq) z = fma(-L[i][qq], Xc[qq], z);
-                Xc[i] = z * Li[i];
-            }
-#pragma unroll
-            for (int i = D - 1; i >= 0; --i) {
-                double z = Xc[i];
-#pragma unroll
-                for (int qq = i + 1; qq < D; ++qq) z = fma(-L[qq][i], Xc[qq], z);
-                Xc[i] = z * Li[i];
-            }
-            double ms_new = xa[r], V[D];
-#pragma unroll
-            for (int qq = 0; qq < D; ++qq) ms_new = fma(Xc[qq], Gs.dm[qq], ms_new);
+            for (int qq = 0; qq < D; ++qq) ms_new = fma(XC(qq), Gs.dm[qq], ms_new);
 #pragma unroll
             for (int bb = 0; bb < D; ++bb) {
                 double v = 0.0;
 #pragma unroll
                 for (int a = 0; a < D; ++a) {
                     const int lo = a < bb ? a : bb, hi = a < bb ? bb : a;
-                    v = fma(Xc[a], Gs.Ps[lo][hi], v);
+                    v = fma(XC(a), Gs.Ps[lo][hi], v);
                 }
                 V[bb] = v;
             }
-            if (act) {
+            if constexpr (G == kGL) {
+                if (act) {
 #pragma unroll
-                for (int i = 0; i < D; ++i) Gs.X[i][r] = Xc[i];
+                    for (int i = 0; i < D; ++i) Gs.X[i][r] = Xc[i];
+                }
             }
             __syncwarp(gm);
 #pragma unroll
             for (int j = 0; j < D; ++j) {
-                double s2 = Pr[j];
+                double s2 = PR(j);
 #pragma unroll
                 for (int bb = 0; bb < D; ++bb) s2 = fma(V[bb], Gs.X[bb][j], s2);
                 Psr[j] = s2;
@@ -2645,7 +2715,7 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_smoother_app
         for (int j = 0; j < D; ++j) vo = fma(Psr[j], M.H[j], vo);
         vo *= hr;
 #pragma unroll
-        for (int off = kGL / 2; off > 0; off >>= 1) {
+        for (int off = G / 2; off > 0; off >>= 1) {
             mo += __shfl_xor_sync(gm, mo, off);
             vo += __shfl_xor_sync(gm, vo, off);
         }

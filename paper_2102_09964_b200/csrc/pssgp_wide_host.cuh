@@ -15,6 +15,10 @@
 namespace pssgp_internal {
 namespace widehost {
 using namespace pssgp;
+// 9 <= D <= 16: lane-per-row kernels in 16-lane groups, two half chains per warp, 2 warps per CTA
+constexpr int kHalfG = 16, kHalfWPC = 2;
+template <int D>
+constexpr bool wide_halves() { return D > pssgp::wide::kGL && D <= kHalfG; }
 // ========================================================================== wide path (d >= 4)
 
 // The >48 KB dynamic shared-memory opt-in is a per-device function attribute: set it once per
@@ -38,6 +42,14 @@ void wide_set_smem_attrs(int device) {
         cudaFuncSetAttribute(kw_filter_apply_q<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K3QSmem<D, true>));
         cudaFuncSetAttribute(kw_smoother_apply_q<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K5QSmem<D, false>));
         cudaFuncSetAttribute(kw_smoother_apply_q<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K5QSmem<D, true>));
+    } else if constexpr (wide_halves<D>()) {
+        constexpr int G = kHalfG, W = kHalfWPC;
+        cudaFuncSetAttribute(kw_filter_fold_lpr<D, false, G, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K1LSmem<D, false, G, W>));
+        cudaFuncSetAttribute(kw_filter_fold_lpr<D, true, G, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K1LSmem<D, true, G, W>));
+        cudaFuncSetAttribute(kw_filter_apply_q<D, false, G, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K3QSmem<D, false, G, W>));
+        cudaFuncSetAttribute(kw_filter_apply_q<D, true, G, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K3QSmem<D, true, G, W>));
+        cudaFuncSetAttribute(kw_smoother_apply_q<D, false, G, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K5QSmem<D, false, G, W>));
+        cudaFuncSetAttribute(kw_smoother_apply_q<D, true, G, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K5QSmem<D, true, G, W>));
     }
     cudaFuncSetAttribute(kw_filter_apply<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K3Smem<D>));
     cudaFuncSetAttribute(kw_smoother_apply<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K5Smem<D>));
@@ -57,10 +69,13 @@ void wide_set_smem_attrs(int device) {
 // busy; needs bit 0, whose fold stores the quarter prefix aggregates)); env PSSGP_WIDE_LPR overrides
 // the default 255 for A/B runs (0 = the shared-memory kernels)
 inline int wide_lpr_mask() {
-    static const int v = [] { const char* e = getenv("PSSGP_WIDE_LPR"); return e && *e ? atoi(e) : 255; }();
+    static const int v = [] { const char* e = getenv("PSSGP_WIDE_LPR"); return e && *e ? atoi(e) : 511; }();
     return v;
 }
 inline bool wide_quarter_rescans() { return (wide_lpr_mask() & 129) == 129; }
+// bit 8: 9 <= D <= 16 on the lane-per-row fold and half-chain rescans (16-lane groups, two half
+// chains per warp, 2 warps per CTA: kHalfG / kHalfWPC)
+inline bool wide_half_rescans() { return (wide_lpr_mask() & 256) != 0; }
 
 struct WPlan {
     int64_t K = 0;
@@ -109,9 +124,28 @@ WPlan make_wplan(pssgp_model* m, int64_t n) {
             // fewer, longer chains slow the shared-memory rescans: 26.2 -> 28.3 ms, so not there)
             if ((wide_lpr_mask() & 8) && (m->mode != kPade || (wide_lpr_mask() & 32))) m->wocc = std::max(1, std::min(m->wocc, std::min(l1, l5)));
             if (wide_quarter_rescans()) m->wocc = std::max(1, std::min(l1, std::min(l3, l5)));
+        } else if constexpr (wide_halves<D>()) {
+            if (wide_half_rescans()) {   // one wave of the half-chain kernels (2-warp CTAs)
+                constexpr int G = kHalfG, W = kHalfWPC;
+                int l1 = 0, l3 = 0, l5 = 0;
+                if (m->mode == kPade) {
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l1, kw_filter_fold_lpr<D, true, G, W>, 32 * W, sizeof(K1LSmem<D, true, G, W>));
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l3, kw_filter_apply_q<D, true, G, W>, 32 * W, sizeof(K3QSmem<D, true, G, W>));
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l5, kw_smoother_apply_q<D, true, G, W>, 32 * W, sizeof(K5QSmem<D, true, G, W>));
+                } else {
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l1, kw_filter_fold_lpr<D, false, G, W>, 32 * W, sizeof(K1LSmem<D, false, G, W>));
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l3, kw_filter_apply_q<D, false, G, W>, 32 * W, sizeof(K3QSmem<D, false, G, W>));
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l5, kw_smoother_apply_q<D, false, G, W>, 32 * W, sizeof(K5QSmem<D, false, G, W>));
+                }
+                m->wchains = std::max(1, std::min(l1, std::min(l3, l5))) * W;
+                if (getenv("PSSGP_WIDE_DEBUG"))
+                    fprintf(stderr, "wide plan D=%d half-chain kernels: fold %d, apply %d, smoother %d CTAs/SM of %d warps\n",
+                            D, l1, l3, l5, W);
+            }
         }
     }
-    const int64_t target = static_cast<int64_t>(m->sm_count) * m->wocc * kWWarps;
+    const int64_t per_sm = m->wchains > 0 ? m->wchains : static_cast<int64_t>(m->wocc) * kWWarps;   // chains per SM
+    const int64_t target = static_cast<int64_t>(m->sm_count) * per_sm;
     WPlan pl;
     pl.K = m->forced_K > 0 ? m->forced_K : std::max<int64_t>(16, (n + target - 1) / target);
     pl.nch = static_cast<int>(std::max<int64_t>(1, (n + pl.K - 1) / pl.K));
@@ -123,7 +157,7 @@ template <int D>
 pssgp_status wide_setup(pssgp_model* m, const WPlan& pl, pssgp::wide::WParams& p) {
     using namespace pssgp::wide;
     const size_t nch = static_cast<size_t>(pl.nch);
-    const bool quarters = D <= kGL && wide_quarter_rescans();
+    const bool quarters = (D <= kGL && wide_quarter_rescans()) || (wide_halves<D>() && wide_half_rescans());
     const size_t nq = quarters ? nch * (kQ - 1) * (FNW(D) + SNW(D)) : 0;   // quarter prefix / smoother aggregates
     const size_t need = (2 * nch * FNW(D) + nch * pl.K * CNW(D) + 2 * nch * SNW(D) + nch + nq + 64) * sizeof(double);
     if (need > m->ws_bytes) {
@@ -304,6 +338,15 @@ pssgp_status wide_fold(pssgp_model* m, pssgp::wide::WParams& p, int nb, cudaStre
             LAUNCH_CHECK(m, "kw_filter_fold_lpr");
             return PSSGP_OK;
         }
+    } else if constexpr (wide_halves<D>()) {
+        if (wide_half_rescans()) {   // lane-per-row fold in 16-lane groups (two half chains per warp)
+            constexpr int G = kHalfG, W = kHalfWPC;
+            const int nbh = (p.nch + W - 1) / W;
+            if (p.fq) kw_filter_fold_lpr<D, true, G, W><<<nbh, 32 * W, sizeof(K1LSmem<D, true, G, W>), s>>>(p);
+            else kw_filter_fold_lpr<D, false, G, W><<<nbh, 32 * W, sizeof(K1LSmem<D, false, G, W>), s>>>(p);
+            LAUNCH_CHECK(m, "kw_filter_fold_lpr (16-lane)");
+            return PSSGP_OK;
+        }
     }
     kw_filter_fold<D><<<nb, 32 * kWWarps, sizeof(K1Smem<D>), s>>>(p);
     LAUNCH_CHECK(m, "kw_filter_fold");
@@ -326,6 +369,15 @@ pssgp_status wide_fapply(pssgp_model* m, pssgp::wide::WParams& p, int nb, cudaSt
             if (p.fq) kw_filter_apply_lpr<D, true><<<nb, 32 * kWWarps, sizeof(K3LSmem<D, true>), s>>>(p);
             else kw_filter_apply_lpr<D, false><<<nb, 32 * kWWarps, sizeof(K3LSmem<D, false>), s>>>(p);
             LAUNCH_CHECK(m, "kw_filter_apply_lpr");
+            return PSSGP_OK;
+        }
+    } else if constexpr (wide_halves<D>()) {
+        if (p.qagg) {   // half-chain Kalman rescan (the fold stored the half prefix aggregates)
+            constexpr int G = kHalfG, W = kHalfWPC;
+            const int nbh = (p.nch + W - 1) / W;
+            if (p.fq) kw_filter_apply_q<D, true, G, W><<<nbh, 32 * W, sizeof(K3QSmem<D, true, G, W>), s>>>(p);
+            else kw_filter_apply_q<D, false, G, W><<<nbh, 32 * W, sizeof(K3QSmem<D, false, G, W>), s>>>(p);
+            LAUNCH_CHECK(m, "kw_filter_apply_q (16-lane)");
             return PSSGP_OK;
         }
     }
@@ -351,6 +403,15 @@ pssgp_status wide_sapply(pssgp_model* m, pssgp::wide::WParams& p, int nb, cudaSt
             if (p.fq) kw_smoother_apply_lpr<D, true><<<nb, 32 * kWWarps, sizeof(K5LSmem<D, true>), s>>>(p);
             else kw_smoother_apply_lpr<D, false><<<nb, 32 * kWWarps, sizeof(K5LSmem<D, false>), s>>>(p);
             LAUNCH_CHECK(m, "kw_smoother_apply_lpr");
+            return PSSGP_OK;
+        }
+    } else if constexpr (wide_halves<D>()) {
+        if (p.sqagg) {  // half-chain RTS rescan
+            constexpr int G = kHalfG, W = kHalfWPC;
+            const int nbh = (p.nch + W - 1) / W;
+            if (p.fq) kw_smoother_apply_q<D, true, G, W><<<nbh, 32 * W, sizeof(K5QSmem<D, true, G, W>), s>>>(p);
+            else kw_smoother_apply_q<D, false, G, W><<<nbh, 32 * W, sizeof(K5QSmem<D, false, G, W>), s>>>(p);
+            LAUNCH_CHECK(m, "kw_smoother_apply_q (16-lane)");
             return PSSGP_OK;
         }
     }
