@@ -418,6 +418,16 @@ pssgp_status pssgp_create(const pssgp_component* comps, int n_comps, double nois
     }
     m->ssm = parts.size() == 1 ? parts[0] : ph::block_sum(parts);
     m->d = m->ssm.d;
+    {   // F = e^{G dt} (and Q) are block diagonal wherever G and W are: the smallest aligned block
+        // size 2 or 4 that contains every nonzero of both (else d), for the half-chain kernels
+        auto blocked = [&](int B) {
+            for (int i = 0; i < m->d; ++i)
+                for (int j = 0; j < m->d; ++j)
+                    if ((m->ssm.G[i * m->d + j] != 0.0L || m->ssm.W[i * m->d + j] != 0.0L) && i / B != j / B) return false;
+            return true;
+        };
+        m->fblock = blocked(2) ? 2 : (blocked(4) ? 4 : m->d);
+    }
     {   // embed the per-component derivatives into the d x d state (block-diagonal sum)
         int o = 0;
         for (size_t c = 0; c < parts.size(); ++c) {

@@ -888,8 +888,10 @@ struct K1LSmem {
     double I[D][LD(D)], Z[D][LD(D)];
     struct PerWarp {
         SF<D> q[NP];
-        SCombF<D> s;
-        double U[NP][D][LD(D)];
+        union {                                    // U in the step loop, s in the final combination
+            SCombF<D> s;
+            double U[NP][D][LD(D)];
+        };
         double fqs[NP][2][FQS(D, STREAM)];         // STREAM: each quarter's (F_k, Q_k) staged one step ahead
     } w[WPC];
 };
@@ -901,6 +903,13 @@ struct K1LSmem {
 // or G = 16 (9 <= D <= 16, two half chains per warp, 2 warps per CTA: the per-warp shared state of
 // d = 16 would otherwise cap residency at one CTA per SM); register cap 168 / 255
 PS_CX int lpr_minb(int G) { return G == kGL ? PSSGP_WLPR_MINB : 4; }
+// F's block-diagonal structure (sum models: one block per component; periodic components: 2 x 2
+// rotation blocks; quasi-periodic products: blocks of 2 m): FB = the aligned block size every
+// nonzero of G and W lies within (the host checks it, pssgp_model::fblock; FB = D = dense), so
+// products with F skip its structural zeros at compile time: row i of F is nonzero only in columns
+// [fblo(i), fbhi(i)).
+PS_CX int fblo(int i, int FB) { return (i / FB) * FB; }
+PS_CX int fbhi(int i, int FB, int D) { return (i / FB) * FB + FB < D ? (i / FB) * FB + FB : D; }
 PS_CX unsigned group_mask(int G, int gb) { return (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << gb; }
 
 // ------------------------------------------------------------------ KDl: lane-per-row discretisation
@@ -1046,7 +1055,7 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WDISC_MINB) kw_discretize_
         }
     }
 }
-template <int D, bool STREAM, int G = kGL, int WPC = kWWarps>
+template <int D, bool STREAM, int G = kGL, int WPC = kWWarps, int FB = D>
 __global__ void __launch_bounds__(32 * WPC, lpr_minb(G)) kw_filter_fold_lpr(const WParams p) {
     static_assert(D <= G, "lane-per-row fold holds one row per lane of a G-lane group");
     constexpr int NP = 32 / G;
@@ -1127,7 +1136,7 @@ __global__ void __launch_bounds__(32 * WPC, lpr_minb(G)) kw_filter_fold_lpr(cons
         for (int i = 0; i < D; ++i) {
             double sa = 0.0, su = 0.0;
 #pragma unroll
-            for (int kk = 0; kk < D; ++kk) {
+            for (int kk = fblo(i, FB); kk < fbhi(i, FB, D); ++kk) {
                 const double f = Fp[i * LD(D) + kk];
                 sa = fma(f, Ac[kk], sa);
                 su = fma(f, Cr[kk], su);
@@ -1155,7 +1164,7 @@ __global__ void __launch_bounds__(32 * WPC, lpr_minb(G)) kw_filter_fold_lpr(cons
         for (int jj = 0; jj < D; ++jj) {
             double s = Qp[rr * LD(D) + jj];
 #pragma unroll
-            for (int kk = 0; kk < D; ++kk) s = fma(Ur[kk], Fp[jj * LD(D) + kk], s);
+            for (int kk = fblo(jj, FB); kk < fbhi(jj, FB, D); ++kk) s = fma(Ur[kk], Fp[jj * LD(D) + kk], s);
             Cm[jj] = s;
             HC = fma(s, M.H[jj], HC);
             w = fma(M.H[jj], FAc[jj], w);
@@ -2192,10 +2201,10 @@ struct K3QSmem {
     SModel<D> m;
     double I[D][LD(D)], Z[D][LD(D)];
     struct PerWarp {
-        double cx[NP][D];                          // filtered state entering each quarter
-        double cP[NP][D][LD(D)];
         union {
-            struct {                               // carry phase
+            struct {                               // carry phase (the carries are read once, before the
+                double cx[NP][D];                  // step phase reuses the space): filtered state
+                double cP[NP][D][LD(D)];           // entering each quarter
                 SF<D> a;
                 SCombF<D> s;
             } c;
@@ -2207,14 +2216,16 @@ struct K3QSmem {
                 double P[D][LD(D)], Sg[D][LD(D)], P0[D][LD(D)];
                 double x[D], x0[D];
                 SS<D> acc, cur;
-                SQScratch<D> w;
-                SCombF<D> s;
+                union {                            // used one after the other
+                    SQScratch<D> w;
+                    SCombF<D> s;
+                };
             } ag;
         } u;
     } w[WPC];
 };
 
-template <int D, bool STREAM, int G = kGL, int WPC = kWWarps>
+template <int D, bool STREAM, int G = kGL, int WPC = kWWarps, int FB = D>
 __global__ void __launch_bounds__(32 * WPC, lpr_minb(G)) kw_filter_apply_q(const WParams p) {
     static_assert(D <= G, "one row per lane of a G-lane group");
     constexpr int NP = 32 / G;
@@ -2236,24 +2247,24 @@ __global__ void __launch_bounds__(32 * WPC, lpr_minb(G)) kw_filter_apply_q(const
     const int64_t ke = min(kb + p.K, p.n);
     // ---- carries: the chain's (incoming sharded (x) scanned chains < c), then through the quarter
     // prefix aggregates of the fold
-    for (int e = lane; e < D * D; e += 32) W.cP[0][e / D][e % D] = 0.0;
-    for (int i = lane; i < D; i += 32) W.cx[0][i] = 0.0;
+    for (int e = lane; e < D * D; e += 32) W.u.c.cP[0][e / D][e % D] = 0.0;
+    for (int i = lane; i < D; i += 32) W.u.c.cx[0][i] = 0.0;
     __syncwarp();
     bool ok = true;
     for (int g = 0; g < p.rank && p.in_filt; ++g) {
         gload<D>(W.u.c.a, p.in_filt + static_cast<int64_t>(g) * FNW(D), lane);
-        ok = wapply_prefix<D>(W.cx[0], W.cP[0], W.u.c.a, W.u.c.s, lane) && ok;
+        ok = wapply_prefix<D>(W.u.c.cx[0], W.u.c.cP[0], W.u.c.a, W.u.c.s, lane) && ok;
     }
     if (c > 0) {
         gload<D>(W.u.c.a, p.fagg + static_cast<int64_t>(c - 1) * FNW(D), lane);
-        ok = wapply_prefix<D>(W.cx[0], W.cP[0], W.u.c.a, W.u.c.s, lane) && ok;
+        ok = wapply_prefix<D>(W.u.c.cx[0], W.u.c.cP[0], W.u.c.a, W.u.c.s, lane) && ok;
     }
     for (int q = 1; q < NP; ++q) {
-        for (int e = lane; e < D * D; e += 32) W.cP[q][e / D][e % D] = W.cP[0][e / D][e % D];
-        for (int i = lane; i < D; i += 32) W.cx[q][i] = W.cx[0][i];
+        for (int e = lane; e < D * D; e += 32) W.u.c.cP[q][e / D][e % D] = W.u.c.cP[0][e / D][e % D];
+        for (int i = lane; i < D; i += 32) W.u.c.cx[q][i] = W.u.c.cx[0][i];
         __syncwarp();
         gload<D>(W.u.c.a, p.qagg + (static_cast<int64_t>(c) * (NP - 1) + (q - 1)) * FNW(D), lane);
-        ok = wapply_prefix<D>(W.cx[q], W.cP[q], W.u.c.a, W.u.c.s, lane) && ok;
+        ok = wapply_prefix<D>(W.u.c.cx[q], W.u.c.cP[q], W.u.c.a, W.u.c.s, lane) && ok;
     }
     if (!ok && lane == 0) raise_error(p.err, p.k0 + kb, kErrNumeric);
 
@@ -2264,9 +2275,9 @@ __global__ void __launch_bounds__(32 * WPC, lpr_minb(G)) kw_filter_apply_q(const
     const int r = act ? r0 : 0;
     int64_t qb, qe;
     quarter_bounds(kb, ke, p.K, q, qb, qe, NP);
-    double Pr[D], Sgr[D], P0r[D], xr = W.cx[q][r], x0r = 0.0;
+    double Pr[D], Sgr[D], P0r[D], xr = W.u.c.cx[q][r], x0r = 0.0;
 #pragma unroll
-    for (int j = 0; j < D; ++j) { Pr[j] = W.cP[q][r][j]; Sgr[j] = 0.0; P0r[j] = 0.0; }
+    for (int j = 0; j < D; ++j) { Pr[j] = W.u.c.cP[q][r][j]; Sgr[j] = 0.0; P0r[j] = 0.0; }
     const double hr = act ? M.H[r] : 0.0;
     __syncwarp();                                               // W.u is reused by the step phase
     double tprev = (qb < qe && (qb > 0 || p.k0 > 0)) ? __ldg(p.t + qb - 1) : 0.0;
@@ -2319,7 +2330,7 @@ __global__ void __launch_bounds__(32 * WPC, lpr_minb(G)) kw_filter_apply_q(const
         for (int i = 0; i < D; ++i) {
             double su = 0.0;
 #pragma unroll
-            for (int qq = 0; qq < D; ++qq) su = fma(Fp[i * LD(D) + qq], Pr[qq], su);
+            for (int qq = fblo(i, FB); qq < fbhi(i, FB, D); ++qq) su = fma(Fp[i * LD(D) + qq], Pr[qq], su);
             Uc[i] = su;
         }
 #pragma unroll
@@ -2334,7 +2345,7 @@ __global__ void __launch_bounds__(32 * WPC, lpr_minb(G)) kw_filter_apply_q(const
         for (int j = 0; j < D; ++j) {
             double s2 = Qp[r * LD(D) + j], s3 = 0.0;
 #pragma unroll
-            for (int qq = 0; qq < D; ++qq) {
+            for (int qq = fblo(j, FB); qq < fbhi(j, FB, D); ++qq) {
                 const double f = Fp[j * LD(D) + qq];
                 s2 = fma(U[r][qq], f, s2);
                 s3 = fma(Sgr[qq], f, s3);
@@ -2437,17 +2448,16 @@ struct K5QSmem {
     SModel<D> m;
     double I[D][LD(D)], Z[D][LD(D)];
     struct PerWarp {
-        double cm[NP][D];                          // smoothed state after each quarter
-        double cP[NP][D][LD(D)];
         union {
-            struct {                               // carry phase
+            struct {                               // carry phase (read once before the step phase)
+                double cm[NP][D];                  // smoothed state after each quarter
+                double cP[NP][D][LD(D)];
                 SS<D> a;
                 SSufScratch<D> s;
             } c;
             struct Grp {                           // step phase, one slot per group
                 double xst[2][CNW(D)];             // staged packed (xbar, P) records (cp.async)
                 double U[D][LD(D)], Pm[D][LD(D)], Ps[D][LD(D)] /* P^s_{k+1} - P^- */, X[D][LD(D)];
-                double L[G > kGL ? D : 1][LD(D)];  // 16-lane groups: the Cholesky factor of P^-
                 double dm[D];
                 double fqs[2][FQS(D, STREAM)];     // STREAM: (F_{k+1}, Q_{k+1}) staged with record k
             } g[NP];
@@ -2455,7 +2465,7 @@ struct K5QSmem {
     } w[WPC];
 };
 
-template <int D, bool STREAM, int G = kGL, int WPC = kWWarps>
+template <int D, bool STREAM, int G = kGL, int WPC = kWWarps, int FB = D>
 __global__ void __launch_bounds__(32 * WPC, lpr_minb(G)) kw_smoother_apply_q(const WParams p) {
     static_assert(D <= G, "one row per lane of a G-lane group");
     constexpr int NP = 32 / G;
@@ -2477,24 +2487,24 @@ __global__ void __launch_bounds__(32 * WPC, lpr_minb(G)) kw_smoother_apply_q(con
     const int64_t ke = min(kb + p.K, p.n);
     // ---- carries: collapsed suffix after the chain (incoming sharded, scanned chains > c), then
     // back through the smoother aggregates of quarters 3, 2, 1 (kw_filter_apply_q)
-    auto& c3P = W.cP[NP - 1];
+    auto& c3P = W.u.c.cP[NP - 1];
     for (int e = lane; e < D * D; e += 32) c3P[e / D][e % D] = 0.0;
-    for (int i = lane; i < D; i += 32) W.cm[NP - 1][i] = 0.0;
+    for (int i = lane; i < D; i += 32) W.u.c.cm[NP - 1][i] = 0.0;
     __syncwarp();
     for (int g = p.world - 1; g > p.rank && p.in_smooth; --g) {
         gload<D>(W.u.c.a, p.in_smooth + static_cast<int64_t>(g) * (SNW(D) + 1), lane);   // blob = aggregate + NLL partial
-        wapply_suffix<D>(W.u.c.a, W.cm[NP - 1], c3P, W.u.c.s, lane);
+        wapply_suffix<D>(W.u.c.a, W.u.c.cm[NP - 1], c3P, W.u.c.s, lane);
     }
     if (c + 1 < p.nch) {
         gload<D>(W.u.c.a, p.sagg + static_cast<int64_t>(c + 1) * SNW(D), lane);
-        wapply_suffix<D>(W.u.c.a, W.cm[NP - 1], c3P, W.u.c.s, lane);
+        wapply_suffix<D>(W.u.c.a, W.u.c.cm[NP - 1], c3P, W.u.c.s, lane);
     }
     for (int q = NP - 2; q >= 0; --q) {
-        for (int e = lane; e < D * D; e += 32) W.cP[q][e / D][e % D] = W.cP[q + 1][e / D][e % D];
-        for (int i = lane; i < D; i += 32) W.cm[q][i] = W.cm[q + 1][i];
+        for (int e = lane; e < D * D; e += 32) W.u.c.cP[q][e / D][e % D] = W.u.c.cP[q + 1][e / D][e % D];
+        for (int i = lane; i < D; i += 32) W.u.c.cm[q][i] = W.u.c.cm[q + 1][i];
         __syncwarp();
         gload<D>(W.u.c.a, p.sqagg + (static_cast<int64_t>(c) * (NP - 1) + q) * SNW(D), lane);   // quarter q + 1
-        wapply_suffix<D>(W.u.c.a, W.cm[q], W.cP[q], W.u.c.s, lane);
+        wapply_suffix<D>(W.u.c.a, W.u.c.cm[q], W.u.c.cP[q], W.u.c.s, lane);
     }
     const int q = lane / G, r0 = lane % G, gb = q * G;
     const unsigned gm = group_mask(G, gb);
@@ -2502,9 +2512,9 @@ __global__ void __launch_bounds__(32 * WPC, lpr_minb(G)) kw_smoother_apply_q(con
     const int r = act ? r0 : 0;
     int64_t qb, qe;
     quarter_bounds(kb, ke, p.K, q, qb, qe, NP);
-    double Psr[D], msr = W.cm[q][r];
+    double Psr[D], msr = W.u.c.cm[q][r];
 #pragma unroll
-    for (int j = 0; j < D; ++j) Psr[j] = W.cP[q][r][j];
+    for (int j = 0; j < D; ++j) Psr[j] = W.u.c.cP[q][r][j];
     const double hr = act ? M.H[r] : 0.0;
     __syncwarp();                                   // W.u (carry scratch) is reused by the staging below
     auto& Gs = W.u.g[q];
@@ -2577,7 +2587,7 @@ __global__ void __launch_bounds__(32 * WPC, lpr_minb(G)) kw_smoother_apply_q(con
             for (int i = 0; i < D; ++i) {
                 double su = 0.0;
 #pragma unroll
-                for (int qq = 0; qq < D; ++qq) su = fma(Fp[i * LD(D) + qq], PR(qq), su);
+                for (int qq = fblo(i, FB); qq < fbhi(i, FB, D); ++qq) su = fma(Fp[i * LD(D) + qq], PR(qq), su);
                 Uc[i] = su;
             }
 #pragma unroll
@@ -2595,7 +2605,7 @@ __global__ void __launch_bounds__(32 * WPC, lpr_minb(G)) kw_smoother_apply_q(con
                 for (int j = 0; j < D; ++j) {
                     double s2 = Qp[r * LD(D) + j];
 #pragma unroll
-                    for (int qq = 0; qq < D; ++qq) s2 = fma(Ur[qq], Fp[j * LD(D) + qq], s2);
+                    for (int qq = fblo(j, FB); qq < fbhi(j, FB, D); ++qq) s2 = fma(Ur[qq], Fp[j * LD(D) + qq], s2);
                     Gs.Pm[r][j] = s2;
                     Gs.Ps[r][j] = Psr[j] - s2;          // Delta = P^s_{k+1} - P^- (row r)
                 }
@@ -2654,9 +2664,10 @@ __global__ void __launch_bounds__(32 * WPC, lpr_minb(G)) kw_smoother_apply_q(con
                     const double lij = rsqrt(sj);
                     Lr[j] = (r == j) ? lij : sv * lij;    // row r: L_rj (j < r), 1 / L_rr; j > r unused
                 }
+                auto& Lm = Gs.Pm;                    // the factor overwrites P^-: lane r read only row r
                 if (act) {
 #pragma unroll
-                    for (int qq = 0; qq < D; ++qq) Gs.L[r][qq] = Lr[qq];
+                    for (int qq = 0; qq < D; ++qq) Lm[r][qq] = Lr[qq];
                 }
                 __syncwarp(gm);
                 // the two solves on column r, in place in the shared X (U still holds F P's columns)
@@ -2664,14 +2675,14 @@ __global__ void __launch_bounds__(32 * WPC, lpr_minb(G)) kw_smoother_apply_q(con
 #pragma unroll 4
                     for (int i = 0; i < D; ++i) {
                         double z = Gs.U[i][r];
-                        for (int qq = 0; qq < i; ++qq) z = fma(-Gs.L[i][qq], Gs.X[qq][r], z);
-                        Gs.X[i][r] = z * Gs.L[i][i];
+                        for (int qq = 0; qq < i; ++qq) z = fma(-Lm[i][qq], Gs.X[qq][r], z);
+                        Gs.X[i][r] = z * Lm[i][i];
                     }
 #pragma unroll 4
                     for (int i = D - 1; i >= 0; --i) {
                         double z = Gs.X[i][r];
-                        for (int qq = i + 1; qq < D; ++qq) z = fma(-Gs.L[qq][i], Gs.X[qq][r], z);
-                        Gs.X[i][r] = z * Gs.L[i][i];
+                        for (int qq = i + 1; qq < D; ++qq) z = fma(-Lm[qq][i], Gs.X[qq][r], z);
+                        Gs.X[i][r] = z * Lm[i][i];
                     }
                 }
             }

@@ -4,6 +4,7 @@
 #pragma once
 #include <algorithm>
 #include <atomic>
+#include <type_traits>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -19,6 +20,15 @@ using namespace pssgp;
 constexpr int kHalfG = 16, kHalfWPC = 2;
 template <int D>
 constexpr bool wide_halves() { return D > pssgp::wide::kGL && D <= kHalfG; }
+// the F block size of the half-chain kernels (pssgp_model::fblock: 2, 4, or dense), compile time
+template <int D, typename Fn>
+void with_fblock(const pssgp_model* m, Fn&& fn) {
+    if constexpr (D > 4) {
+        if (m->fblock == 2) { fn(std::integral_constant<int, 2>{}); return; }
+        if (m->fblock == 4) { fn(std::integral_constant<int, 4>{}); return; }
+    }
+    fn(std::integral_constant<int, D>{});
+}
 // ========================================================================== wide path (d >= 4)
 
 // The >48 KB dynamic shared-memory opt-in is a per-device function attribute: set it once per
@@ -43,13 +53,20 @@ void wide_set_smem_attrs(int device) {
         cudaFuncSetAttribute(kw_smoother_apply_q<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K5QSmem<D, false>));
         cudaFuncSetAttribute(kw_smoother_apply_q<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K5QSmem<D, true>));
     } else if constexpr (wide_halves<D>()) {
-        constexpr int G = kHalfG, W = kHalfWPC;
-        cudaFuncSetAttribute(kw_filter_fold_lpr<D, false, G, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K1LSmem<D, false, G, W>));
-        cudaFuncSetAttribute(kw_filter_fold_lpr<D, true, G, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K1LSmem<D, true, G, W>));
-        cudaFuncSetAttribute(kw_filter_apply_q<D, false, G, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K3QSmem<D, false, G, W>));
-        cudaFuncSetAttribute(kw_filter_apply_q<D, true, G, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K3QSmem<D, true, G, W>));
-        cudaFuncSetAttribute(kw_smoother_apply_q<D, false, G, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K5QSmem<D, false, G, W>));
-        cudaFuncSetAttribute(kw_smoother_apply_q<D, true, G, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K5QSmem<D, true, G, W>));
+        auto set = [](auto fbc) {
+            constexpr int G = kHalfG, W = kHalfWPC, FB = decltype(fbc)::value;
+            cudaFuncSetAttribute(kw_filter_fold_lpr<D, false, G, W, FB>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K1LSmem<D, false, G, W>));
+            cudaFuncSetAttribute(kw_filter_fold_lpr<D, true, G, W, FB>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K1LSmem<D, true, G, W>));
+            cudaFuncSetAttribute(kw_filter_apply_q<D, false, G, W, FB>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K3QSmem<D, false, G, W>));
+            cudaFuncSetAttribute(kw_filter_apply_q<D, true, G, W, FB>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K3QSmem<D, true, G, W>));
+            cudaFuncSetAttribute(kw_smoother_apply_q<D, false, G, W, FB>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K5QSmem<D, false, G, W>));
+            cudaFuncSetAttribute(kw_smoother_apply_q<D, true, G, W, FB>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K5QSmem<D, true, G, W>));
+        };
+        set(std::integral_constant<int, D>{});
+        if constexpr (D > 4) {
+            set(std::integral_constant<int, 2>{});
+            set(std::integral_constant<int, 4>{});
+        }
     }
     cudaFuncSetAttribute(kw_filter_apply<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K3Smem<D>));
     cudaFuncSetAttribute(kw_smoother_apply<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K5Smem<D>));
@@ -128,15 +145,18 @@ WPlan make_wplan(pssgp_model* m, int64_t n) {
             if (wide_half_rescans()) {   // one wave of the half-chain kernels (2-warp CTAs)
                 constexpr int G = kHalfG, W = kHalfWPC;
                 int l1 = 0, l3 = 0, l5 = 0;
-                if (m->mode == kPade) {
-                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l1, kw_filter_fold_lpr<D, true, G, W>, 32 * W, sizeof(K1LSmem<D, true, G, W>));
-                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l3, kw_filter_apply_q<D, true, G, W>, 32 * W, sizeof(K3QSmem<D, true, G, W>));
-                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l5, kw_smoother_apply_q<D, true, G, W>, 32 * W, sizeof(K5QSmem<D, true, G, W>));
-                } else {
-                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l1, kw_filter_fold_lpr<D, false, G, W>, 32 * W, sizeof(K1LSmem<D, false, G, W>));
-                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l3, kw_filter_apply_q<D, false, G, W>, 32 * W, sizeof(K3QSmem<D, false, G, W>));
-                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l5, kw_smoother_apply_q<D, false, G, W>, 32 * W, sizeof(K5QSmem<D, false, G, W>));
-                }
+                with_fblock<D>(m, [&](auto fbc) {
+                    constexpr int FB = decltype(fbc)::value;
+                    if (m->mode == kPade) {
+                        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l1, kw_filter_fold_lpr<D, true, G, W, FB>, 32 * W, sizeof(K1LSmem<D, true, G, W>));
+                        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l3, kw_filter_apply_q<D, true, G, W, FB>, 32 * W, sizeof(K3QSmem<D, true, G, W>));
+                        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l5, kw_smoother_apply_q<D, true, G, W, FB>, 32 * W, sizeof(K5QSmem<D, true, G, W>));
+                    } else {
+                        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l1, kw_filter_fold_lpr<D, false, G, W, FB>, 32 * W, sizeof(K1LSmem<D, false, G, W>));
+                        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l3, kw_filter_apply_q<D, false, G, W, FB>, 32 * W, sizeof(K3QSmem<D, false, G, W>));
+                        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l5, kw_smoother_apply_q<D, false, G, W, FB>, 32 * W, sizeof(K5QSmem<D, false, G, W>));
+                    }
+                });
                 m->wchains = std::max(1, std::min(l1, std::min(l3, l5))) * W;
                 if (getenv("PSSGP_WIDE_DEBUG"))
                     fprintf(stderr, "wide plan D=%d half-chain kernels: fold %d, apply %d, smoother %d CTAs/SM of %d warps\n",
@@ -342,8 +362,11 @@ pssgp_status wide_fold(pssgp_model* m, pssgp::wide::WParams& p, int nb, cudaStre
         if (wide_half_rescans()) {   // lane-per-row fold in 16-lane groups (two half chains per warp)
             constexpr int G = kHalfG, W = kHalfWPC;
             const int nbh = (p.nch + W - 1) / W;
-            if (p.fq) kw_filter_fold_lpr<D, true, G, W><<<nbh, 32 * W, sizeof(K1LSmem<D, true, G, W>), s>>>(p);
-            else kw_filter_fold_lpr<D, false, G, W><<<nbh, 32 * W, sizeof(K1LSmem<D, false, G, W>), s>>>(p);
+            with_fblock<D>(m, [&](auto fbc) {
+                constexpr int FB = decltype(fbc)::value;
+                if (p.fq) kw_filter_fold_lpr<D, true, G, W, FB><<<nbh, 32 * W, sizeof(K1LSmem<D, true, G, W>), s>>>(p);
+                else kw_filter_fold_lpr<D, false, G, W, FB><<<nbh, 32 * W, sizeof(K1LSmem<D, false, G, W>), s>>>(p);
+            });
             LAUNCH_CHECK(m, "kw_filter_fold_lpr (16-lane)");
             return PSSGP_OK;
         }
@@ -375,8 +398,11 @@ pssgp_status wide_fapply(pssgp_model* m, pssgp::wide::WParams& p, int nb, cudaSt
         if (p.qagg) {   // half-chain Kalman rescan (the fold stored the half prefix aggregates)
             constexpr int G = kHalfG, W = kHalfWPC;
             const int nbh = (p.nch + W - 1) / W;
-            if (p.fq) kw_filter_apply_q<D, true, G, W><<<nbh, 32 * W, sizeof(K3QSmem<D, true, G, W>), s>>>(p);
-            else kw_filter_apply_q<D, false, G, W><<<nbh, 32 * W, sizeof(K3QSmem<D, false, G, W>), s>>>(p);
+            with_fblock<D>(m, [&](auto fbc) {
+                constexpr int FB = decltype(fbc)::value;
+                if (p.fq) kw_filter_apply_q<D, true, G, W, FB><<<nbh, 32 * W, sizeof(K3QSmem<D, true, G, W>), s>>>(p);
+                else kw_filter_apply_q<D, false, G, W, FB><<<nbh, 32 * W, sizeof(K3QSmem<D, false, G, W>), s>>>(p);
+            });
             LAUNCH_CHECK(m, "kw_filter_apply_q (16-lane)");
             return PSSGP_OK;
         }
@@ -409,8 +435,11 @@ pssgp_status wide_sapply(pssgp_model* m, pssgp::wide::WParams& p, int nb, cudaSt
         if (p.sqagg) {  // half-chain RTS rescan
             constexpr int G = kHalfG, W = kHalfWPC;
             const int nbh = (p.nch + W - 1) / W;
-            if (p.fq) kw_smoother_apply_q<D, true, G, W><<<nbh, 32 * W, sizeof(K5QSmem<D, true, G, W>), s>>>(p);
-            else kw_smoother_apply_q<D, false, G, W><<<nbh, 32 * W, sizeof(K5QSmem<D, false, G, W>), s>>>(p);
+            with_fblock<D>(m, [&](auto fbc) {
+                constexpr int FB = decltype(fbc)::value;
+                if (p.fq) kw_smoother_apply_q<D, true, G, W, FB><<<nbh, 32 * W, sizeof(K5QSmem<D, true, G, W>), s>>>(p);
+                else kw_smoother_apply_q<D, false, G, W, FB><<<nbh, 32 * W, sizeof(K5QSmem<D, false, G, W>), s>>>(p);
+            });
             LAUNCH_CHECK(m, "kw_smoother_apply_q (16-lane)");
             return PSSGP_OK;
         }
