@@ -32,6 +32,12 @@ PS_CX int SNW(int D) { return 2 * D * D + D; }     // full smoother aggregate: E
 PS_CX int CNW(int D) { return D + D * (D + 1) / 2; } // filtered (x, P packed upper)
 PS_CX int MODW(int D) { return 5 * D * D + D + 2; }  // model: F, Q, Pinf, H, r, udt, G, W
 PS_CX int FQW(int D) { return 2 * D * LD(D); }     // per-step F, Q (rows of stride LD) in kPade mode
+// Taylor coefficient matrices of F(dt) = sum_k G^k / k! dt^k (k = 0..kPolyM) and Q(dt) = sum_k M_k dt^k
+// (k = 1..kPolyM+1, M_1 = W, M_{k+1} = (G M_k + M_k G^T) / (k + 1): the Lyapunov ODE's series), host-
+// computed in long double and appended to the model buffer after MODW doubles
+constexpr int kPolyM = 12;
+constexpr double kPolyNorm = 0.05;               // ||G dt||_1 up to which the polynomial path is used
+PS_CX int MODP(int D) { return 2 * (kPolyM + 1) * D * D; }
 
 struct WParams {
     const double* t;
@@ -692,6 +698,23 @@ __global__ void __launch_bounds__(32 * kWWarps) kw_discretize(const double* __re
         const double dt = __ldg(t + k) - __ldg(t + k - 1);
         if (dt == 0.0 || !(dt == dt)) continue;
         const double nrm = sh.gnorm * fabs(dt);
+        if (nrm <= kPolyNorm) {   // small step: Taylor polynomials in dt (as kw_discretize_lpr)
+            double* o = fq + k * FQW(D);
+            const double* fc = model + MODW(D);
+            const double* qc = fc + (kPolyM + 1) * D * D;
+            for (int e = lane; e < D * D; e += 32) {
+                const int i = e / D, j = e - (e / D) * D;
+                double f = __ldg(fc + kPolyM * D * D + e), q = __ldg(qc + kPolyM * D * D + e);
+#pragma unroll
+                for (int kk = kPolyM - 1; kk >= 0; --kk) {
+                    f = fma(f, dt, __ldg(fc + kk * D * D + e));
+                    q = fma(q, dt, __ldg(qc + kk * D * D + e));
+                }
+                o[i * LD(D) + j] = f;
+                o[(D + i) * LD(D) + j] = q * dt;
+            }
+            continue;
+        }
         int s = 0;
         if (nrm > 0.125) frexp(nrm / 0.125, &s);
         const bool low = (nrm <= 0.017);
@@ -965,12 +988,41 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WDISC_MINB) kw_discretize_
     }
     constexpr double c[13] = {1.0, 1.0, 1.0 / 2, 1.0 / 6, 1.0 / 24, 1.0 / 120, 1.0 / 720, 1.0 / 5040, 1.0 / 40320,
                               1.0 / 362880, 1.0 / 3628800, 1.0 / 39916800, 1.0 / 479001600};
+    // the Taylor coefficient matrices (MODP) in shared memory for the polynomial path
+    __shared__ double FCs[kPolyM + 1][D * D], QCs[kPolyM + 1][D * D];
+    for (int e = threadIdx.x; e < (kPolyM + 1) * D * D; e += blockDim.x) {
+        FCs[e / (D * D)][e % (D * D)] = __ldg(model + MODW(D) + e);
+        QCs[e / (D * D)][e % (D * D)] = __ldg(model + MODW(D) + (kPolyM + 1) * D * D + e);
+    }
+    __syncthreads();
     const int64_t ng = static_cast<int64_t>(gridDim.x) * blockDim.x / kGL;
     for (int64_t k = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / kGL; k < nfq; k += ng) {
         if (k0 + k == 0) continue;
         const double dt = __ldg(t + k) - __ldg(t + k - 1);
         if (dt == 0.0 || !(dt == dt)) continue;
         const double nrm = gnorm * fabs(dt);
+        if (nrm <= kPolyNorm) {
+            // small step: F and Q are their Taylor polynomials in the scalar dt (Horner, row r of each
+            // coefficient matrix; truncation <= (2 ||G dt||)^13 / 13! relative): no matrix products, no
+            // shuffles.  The coefficients are exactly symmetric for Q, so lane j's (j, r) equals (r, j).
+            if (act) {
+                double* o = fq + k * FQW(D);
+#pragma unroll
+                for (int j = 0; j < D; ++j) {
+                    double f = FCs[kPolyM][r * D + j], q = QCs[kPolyM][r * D + j];
+#pragma unroll
+                    for (int kk = kPolyM - 1; kk >= 0; --kk) {
+                        f = fma(f, dt, FCs[kk][r * D + j]);
+                        q = fma(q, dt, QCs[kk][r * D + j]);
+                    }
+                    o[r * LD(D) + j] = f;
+                    o[(D + r) * LD(D) + j] = q * dt;
+                }
+                o[r * LD(D) + D] = 0.0;
+                o[(D + r) * LD(D) + D] = 0.0;
+            }
+            continue;
+        }
         int s = 0;
         if (nrm > 0.125) frexp(nrm / 0.125, &s);
         const bool low = (nrm <= 0.017);

@@ -191,7 +191,7 @@ pssgp_status wide_setup(pssgp_model* m, const WPlan& pl, pssgp::wide::WParams& p
         m->ws_bytes = need;
     }
     if (!m->d_model) {
-        std::vector<double> h(MODW(D), 0.0);
+        std::vector<double> h(MODW(D) + MODP(D), 0.0);
         for (int i = 0; i < D * D; ++i) {
             h[i] = m->udt > 0.0 ? m->Fu[i] : 0.0;
             h[D * D + i] = m->udt > 0.0 ? m->Qu[i] : 0.0;
@@ -202,6 +202,25 @@ pssgp_status wide_setup(pssgp_model* m, const WPlan& pl, pssgp::wide::WParams& p
         h[3 * D * D + D + 1] = m->udt > 0.0 ? m->udt : -1.0;
         for (int i = 0; i < D * D; ++i) h[3 * D * D + D + 2 + i] = static_cast<double>(m->ssm.G[i]);
         for (int i = 0; i < D * D; ++i) h[4 * D * D + D + 2 + i] = static_cast<double>(m->ssm.W[i]);
+        {   // Taylor coefficients of F(dt), Q(dt) (kw_discretize_lpr's polynomial path), long double
+            using pssgp_host::Mat;
+            const Mat& G = m->ssm.G;
+            Mat Fk = pssgp_host::eye(D), Mk = m->ssm.W;
+            for (int k = 0; k <= kPolyM; ++k) {
+                for (int i = 0; i < D * D; ++i) {
+                    h[MODW(D) + k * D * D + i] = static_cast<double>(Fk[i]);
+                    h[MODW(D) + (kPolyM + 1 + k) * D * D + i] = static_cast<double>(Mk[i]);   // M_{k+1}
+                }
+                Fk = pssgp_host::matmul(Fk, G, D);
+                for (auto& v : Fk) v /= static_cast<pssgp_host::ld>(k + 1);
+                const Mat GM = pssgp_host::matmul(G, Mk, D);
+                Mat Mn = pssgp_host::zeros(D);
+                for (int i = 0; i < D; ++i)
+                    for (int j = 0; j < D; ++j)
+                        Mn[i * D + j] = (GM[i * D + j] + GM[j * D + i]) / static_cast<pssgp_host::ld>(k + 2);
+                Mk = Mn;
+            }
+        }
         if (cudaMalloc(&m->d_model, h.size() * sizeof(double)) != cudaSuccess) {
             cudaGetLastError();
             return fail(m, PSSGP_E_NOMEM, "cudaMalloc(model)");
