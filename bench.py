@@ -63,10 +63,12 @@ def alg_bytes(slot: str, d: int, wide_stream: bool = False, f32: bool = False) -
 
 
 # kernel families behind each profile slot (thread path d <= 3, wide path d >= 4)
-_FAMILY = {"k_filter_reduce": ("k_filter_reduce", "kw_filter_fold"), "k_filter_apply": ("k_filter_apply", "kw_filter_apply"),
-           "k_smoother_apply": ("k_smoother_apply", "kw_smoother_apply"), "k_grad_fold": ("k_grad_fold", "k_grad_fold"),
-           "k_discretize": ("k_discretize", "kw_discretize"), "k_filter_scan": ("", "kw_scan_filter"),
-           "k_smoother_scan": ("", "kw_scan_smoother")}
+_FAMILY = {"k_filter_reduce": ("k_filter_reduce", ("kw_filter_fold",)),
+           "k_filter_apply": ("k_filter_apply", ("kw_filter_apply", "kw_grad_forward")),
+           "k_smoother_apply": ("k_smoother_apply", ("kw_smoother_apply",)),
+           "k_grad_fold": ("k_grad_fold", ("k_grad_fold", "kw_grad_backward")),
+           "k_discretize": ("k_discretize", ("kw_discretize",)), "k_filter_scan": ("", ("kw_scan_filter",)),
+           "k_smoother_scan": ("", ("kw_scan_smoother", "kw_scan_adjoint"))}
 
 
 def _ncu_row(slot: str, d: int, cfg_key: str, f32: bool = False):
@@ -79,8 +81,9 @@ def _ncu_row(slot: str, d: int, cfg_key: str, f32: bool = False):
     fam = _FAMILY.get(slot)
     if fam is None:
         return None, None
-    fam = fam[0] if d <= 3 else fam[1]
-    if not fam:
+    fams = (fam[0],) if (d <= 3 and cfg_key != "gradco2") else fam[1]
+    fams = [f for f in fams if f]
+    if not fams:
         return None, None
 
     def tag_key(f):
@@ -95,7 +98,7 @@ def _ncu_row(slot: str, d: int, cfg_key: str, f32: bool = False):
             continue
         for row in csv.DictReader(open(f)):
             name = row["Kernel Name"]
-            if fam + "<" in name or fam + "_lpr<" in name:
+            if any(fam + "<" in name or fam + "_lpr<" in name or fam + "_q<" in name for fam in fams):
                 targs = name[name.index("<") + 1:]
                 if targs.startswith(f"{d},") or targs.startswith(f"{d}>"):
                     return row, os.path.relpath(f, ROOT)
@@ -138,7 +141,7 @@ def parse():
     ap.add_argument("--N", type=int, default=2 ** 24)
     ap.add_argument("--uniform", action="store_true", help="uniform dt (secondary row)")
     ap.add_argument("--kind", default="matern52")
-    ap.add_argument("--config", default="metric", choices=["metric", "c2", "c3", "c4", "c5", "batched", "grad", "gradb", "f32"],
+    ap.add_argument("--config", default="metric", choices=["metric", "c2", "c3", "c4", "c5", "batched", "grad", "gradb", "gradco2", "f32"],
                     help="workload (default: the BASELINE metric); c3/c4 are the d = 6 / d = 16 rows")
     ap.add_argument("--irregular", action="store_true", help="c3/c4 on a jittered grid (device Pade discretisation)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -296,6 +299,9 @@ def make_workload(args):
         return synth.metric_workload(3200 * 4, kind="matern52")
     if args.config == "grad":
         return synth.metric_workload(args.N)
+    if args.config == "gradco2":
+        # the paper's HMC model C_Per x C_Mat + C_Mat at n_x = 18 (J = 3), weekly grid
+        return synth.co2_product(n=args.N if args.N != 2 ** 24 else 2 ** 20, order=3)
     return synth.metric_workload(args.N, uniform=args.uniform, kind=args.kind)
 
 
@@ -390,13 +396,14 @@ def main():
             def step():
                 P.pssgp_nll_grad_batched(model.h, B, off, VB, EB, RB, N, t, y, mk, nllb, gb, stream)
         n_local = N
-    elif args.config == "grad":
-        # f1: NLL + d NLL / d (log s2, log ell, log r) on the metric grid (one L-BFGS / HMC evaluation)
+    elif args.config in ("grad", "gradco2"):
+        # f1: NLL + its gradient in every log hyper-parameter (one L-BFGS / HMC evaluation): the metric
+        # grid (one Matern component, 3 parameters) or the CO2 model (reverse mode, 8 parameters)
         t = torch.from_numpy(w.t).to(dev)
         y = torch.from_numpy(w.y).to(dev)
         mk = torch.from_numpy(w.mask).to(dev)
         nll = torch.zeros(1, dtype=torch.float64, device=dev)
-        gr = torch.zeros(3, dtype=torch.float64, device=dev)
+        gr = torch.zeros(model.num_params, dtype=torch.float64, device=dev)
 
         def step():
             P.pssgp_nll_grad(model.h, N, t, y, mk, nll, gr, stream)
@@ -470,13 +477,13 @@ def main():
     ms_step = ms_total / args.steps
     # independent problems per rank (batched series, gradient evaluations): weak scaling, the
     # job's units are all ranks' steps; the time-sharded posterior: strong scaling over one grid
-    replicas = args.config in ("batched", "grad", "gradb") and world > 1
+    replicas = args.config in ("batched", "grad", "gradb", "gradco2") and world > 1
     units = N * world if replicas else N
     value = units / (ms_step * 1e-3)
 
     # ---- e2e through the public host API (pinned buffers, copies inside the timed region)
     e2e = None
-    if world == 1 and args.config not in ("batched", "grad", "gradb", "f32"):
+    if world == 1 and args.config not in ("batched", "grad", "gradb", "gradco2", "f32"):
         th = torch.from_numpy(w.t).pin_memory()
         yh = torch.from_numpy(w.y).pin_memory()
         mh = torch.from_numpy(w.mask).pin_memory()
@@ -587,8 +594,8 @@ def main():
         cpu = cpu_baseline(w, args.cpu_sample)
     if args.config == "metric" and not args.uniform:
         metric = METRIC
-    elif args.config == "grad":
-        metric = f"time-steps/s (NLL + 3-parameter gradient, fp64) {w.name} N={N}"
+    elif args.config in ("grad", "gradco2"):
+        metric = f"time-steps/s (NLL + {model.num_params}-parameter gradient, fp64) {w.name} N={N}"
     elif args.config == "f32":
         metric = f"time-steps/s (filter+smoother+NLL, fp32 state) {w.name} N={N}"
     elif args.config == "gradb":
@@ -597,8 +604,9 @@ def main():
         metric = (f"time-steps/s (filter+smoother+NLL, fp64) "
                   f"{w.name if args.config != 'batched' else 'batched Matern-5/2 series of 3200'} N={N}")
     extra = {}
-    if args.config == "grad":
-        # latency of one NLL+gradient evaluation at the sunspot size N = 3,200 (Table 1)
+    if args.config in ("grad", "gradco2"):
+        # latency of one NLL+gradient evaluation at the sunspot size N = 3,200 (Table 1;
+        # the CO2 series has ~3,200 weekly points)
         n1 = 3200
         t1, y1, m1 = t[:n1].contiguous(), y[:n1].contiguous(), mk[:n1].contiguous()
         for _ in range(5):
