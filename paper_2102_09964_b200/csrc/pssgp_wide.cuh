@@ -63,7 +63,9 @@ struct WParams {
     const double* fq;           // per-step (F, Q) [n(+1)][FQW] from kw_discretize (irregular dt), else NULL
     double* qagg;               // [nch][kQ-1][FNW] quarter prefix filter aggregates (lane-per-row fold, D <= 8)
     double* sqagg;              // [nch][kQ-1][SNW] smoother aggregates of quarters 1..3 (quarter Kalman rescan)
+    double* qmom;               // [nch][2][QMW] half-chain rescan (9 <= D <= 16): each half's end moments
 };
+PS_CX int QMW(int D) { return 3 * D * D + 2 * D; }   // (P, Sg, P0 full; x, x0)
 
 // ------------------------------------------------------------------ shared-memory model
 template <int D>
@@ -910,9 +912,11 @@ struct K1LSmem {
     SModel<D> m;
     double I[D][LD(D)], Z[D][LD(D)];
     struct PerWarp {
-        SF<D> q[NP];
+        // 8-lane groups combine the quarter aggregates here; 16-lane groups write their halves to
+        // global memory from registers (kw_combine_halves combines them)
+        std::conditional_t<(G == kGL), SF<D>[NP], char> q;
         union {                                    // U in the step loop, s in the final combination
-            SCombF<D> s;
+            std::conditional_t<(G == kGL), SCombF<D>, char> s;
             double U[NP][D][LD(D)];
         };
         double fqs[NP][2][FQS(D, STREAM)];         // STREAM: each quarter's (F_k, Q_k) staged one step ahead
@@ -1107,6 +1111,13 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WDISC_MINB) kw_discretize_
         }
     }
 }
+// scratch of one general filtering operator on two loaded aggregates (scans, half combination)
+template <int D>
+struct ScanSmemF {
+    SF<D> a, b;
+    SCombF<D> s;
+};
+
 template <int D, bool STREAM, int G = kGL, int WPC = kWWarps, int FB = D>
 __global__ void __launch_bounds__(32 * WPC, lpr_minb(G)) kw_filter_fold_lpr(const WParams p) {
     static_assert(D <= G, "lane-per-row fold holds one row per lane of a G-lane group");
@@ -1243,6 +1254,24 @@ __global__ void __launch_bounds__(32 * WPC, lpr_minb(G)) kw_filter_fold_lpr(cons
         b = fma(HC, vs, Fb);
         eta = fma(w, vs, eta);
     }
+    if constexpr (G > kGL) {
+        // two half aggregates straight from registers to global memory (A by columns, C and J by rows,
+        // the gstore layout): q0 -> qagg[c] (the prefix the second half's rescan starts from), q1 ->
+        // fbuf[c]; kw_combine_halves forms fagg[c] = q0 (x) q1
+        static_assert(NP == 2, "16-lane groups: two halves");
+        if (act) {
+            double* g = (q == 0) ? p.qagg + static_cast<int64_t>(c) * FNW(D) : p.fbuf + static_cast<int64_t>(c) * FNW(D);
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+                g[i * D + r] = Ac[i];
+                g[D * D + D + r * D + i] = Cr[i];
+                g[2 * D * D + 2 * D + r * D + i] = Jr[i];
+            }
+            g[D * D + r] = b;
+            g[2 * D * D + D + r] = eta;
+        }
+        return;
+    } else {
     // quarter aggregates -> shared, ordered combination, store
     if (act) {
         SF<D>& o = W.q[q];
@@ -1267,14 +1296,23 @@ __global__ void __launch_bounds__(32 * WPC, lpr_minb(G)) kw_filter_fold_lpr(cons
     }
     if (!ok && lane == 0) raise_error(p.err, p.k0 + kb, kErrNumeric);
     gstore<D>(W.q[NP - 1], p.fagg + static_cast<int64_t>(c) * FNW(D), lane);
+    }
+}
+
+// fagg[c] = qagg[c] (x) fbuf[c]: the chain aggregate from the two half aggregates of the 16-lane fold
+// (PAPER.md:116-121).  One warp per chain.
+template <int D>
+__global__ void __launch_bounds__(32) kw_combine_halves(const WParams p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    ScanSmemF<D>& sh = *reinterpret_cast<ScanSmemF<D>*>(smem_raw);
+    const int lane = threadIdx.x, c = blockIdx.x;
+    gload<D>(sh.a, p.qagg + static_cast<int64_t>(c) * FNW(D), lane);
+    gload<D>(sh.b, p.fbuf + static_cast<int64_t>(c) * FNW(D), lane);
+    if (!wcombine<D>(sh.a, sh.b, sh.b, sh.s, lane) && lane == 0) raise_error(p.err, p.k0 + static_cast<int64_t>(c) * p.K, kErrNumeric);
+    gstore<D>(sh.b, p.fagg + static_cast<int64_t>(c) * FNW(D), lane);
 }
 
 // ------------------------------------------------------------------ Kogge-Stone scan levels (1 warp per element)
-template <int D>
-struct ScanSmemF {
-    SF<D> a, b;
-    SCombF<D> s;
-};
 template <int D>
 __global__ void __launch_bounds__(32) kw_scan_filter(const double* __restrict__ in, double* __restrict__ out, int nch,
                                                      int off, unsigned long long* err) {
@@ -2247,6 +2285,16 @@ __device__ void quarter_sagg(const WParams& p, const SModel<D>& M, const double 
 }
 
 // ------------------------------------------------------------------ K3q: quarter-parallel Kalman rescan
+template <int D>
+struct QAgPhase {                                  // one quarter's moments and the running aggregate
+    double P[D][LD(D)], Sg[D][LD(D)], P0[D][LD(D)];
+    double x[D], x0[D];
+    SS<D> acc, cur;
+    union {                                        // used one after the other
+        SQScratch<D> w;
+        SCombF<D> s;
+    };
+};
 template <int D, bool STREAM, int G = kGL, int WPC = kWWarps>
 struct K3QSmem {
     static constexpr int NP = 32 / G;
@@ -2264,15 +2312,9 @@ struct K3QSmem {
                 double U[NP][D][LD(D)];
                 double fqs[NP][2][FQS(D, STREAM)];
             } st;
-            struct {                               // quarter smoother aggregates, one quarter at a time
-                double P[D][LD(D)], Sg[D][LD(D)], P0[D][LD(D)];
-                double x[D], x0[D];
-                SS<D> acc, cur;
-                union {                            // used one after the other
-                    SQScratch<D> w;
-                    SCombF<D> s;
-                };
-            } ag;
+            // quarter smoother aggregates, one quarter at a time (8-lane groups; the half-chain kernel
+            // hands its moments to kw_part_sagg instead)
+            std::conditional_t<(G == kGL), QAgPhase<D>, char> ag;
         } u;
     } w[WPC];
 };
@@ -2461,6 +2503,21 @@ __global__ void __launch_bounds__(32 * WPC, lpr_minb(G)) kw_filter_apply_q(const
         if (lane == 0) p.nll_chain[c] = tot;
     }
     if (!p.store_state) return;
+    if constexpr (G > kGL) {
+        // half chains: each group's end moments to global memory (kw_part_sagg forms the half smoother
+        // aggregates and the chain's), keeping this kernel's shared memory small
+        if (act) {
+            double* o = p.qmom + (static_cast<int64_t>(c) * NP + q) * QMW(D);
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                o[r * D + j] = Pr[j];
+                o[D * D + r * D + j] = Sgr[j];
+                o[2 * D * D + r * D + j] = P0r[j];
+            }
+            o[3 * D * D + r] = xr;
+            o[3 * D * D + D + r] = x0r;
+        }
+    } else {
     // ---- quarter smoother aggregates (E, g, L), combined in time order into the chain's
     const double tq = tprev;
     SS<D>* acc = &W.u.ag.acc;
@@ -2486,6 +2543,50 @@ __global__ void __launch_bounds__(32 * WPC, lpr_minb(G)) kw_filter_apply_q(const
             gstore<D>(*cur, p.sqagg + (static_cast<int64_t>(c) * (NP - 1) + (qq - 1)) * SNW(D), lane);
             __syncwarp();
             wcombine<D>(*acc, *cur, *cur, W.u.ag.s, lane);   // acc (x) cur, earlier quarter on the left
+        }
+        SS<D>* t = acc; acc = cur; cur = t;
+        __syncwarp();
+    }
+    gstore<D>(*acc, p.sagg + static_cast<int64_t>(c) * SNW(D), lane);
+    }
+}
+
+// The half smoother aggregates and the chain's from the half-chain rescan's end moments (p.qmom):
+// the quarter-aggregate phase of kw_filter_apply_q for 16-lane groups, one warp per chain.
+template <int D, int NP>
+__global__ void __launch_bounds__(32) kw_part_sagg(const WParams p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    QAgPhase<D>& A = *reinterpret_cast<QAgPhase<D>*>(smem_raw);
+    __shared__ SModel<D> M;
+    load_model<D>(M, p.model);
+    __syncwarp();
+    const int lane = threadIdx.x, c = blockIdx.x;
+    const int64_t kb = static_cast<int64_t>(c) * p.K;
+    const int64_t ke = min(kb + p.K, p.n);
+    SS<D>* acc = &A.acc;
+    SS<D>* cur = &A.cur;
+#pragma unroll 1
+    for (int qq = 0; qq < NP; ++qq) {
+        const double* o = p.qmom + (static_cast<int64_t>(c) * NP + qq) * QMW(D);
+        for (int e = lane; e < D * D; e += 32) {
+            const int i = e / D, j = e - (e / D) * D;
+            A.P[i][j] = o[e];
+            A.Sg[i][j] = o[D * D + e];
+            A.P0[i][j] = o[2 * D * D + e];
+        }
+        for (int i = lane; i < D; i += 32) {
+            A.x[i] = o[3 * D * D + i];
+            A.x0[i] = o[3 * D * D + D + i];
+        }
+        __syncwarp();
+        int64_t sb, se;
+        quarter_bounds(kb, ke, p.K, qq, sb, se, NP);
+        const double tpq = (se > sb) ? __ldg(p.t + se - 1) : 0.0;
+        quarter_sagg<D>(p, M, A.P, A.x, A.Sg, A.P0, A.x0, sb, se, tpq, *cur, A.w, lane);
+        if (qq > 0) {
+            gstore<D>(*cur, p.sqagg + (static_cast<int64_t>(c) * (NP - 1) + (qq - 1)) * SNW(D), lane);
+            __syncwarp();
+            wcombine<D>(*acc, *cur, *cur, A.s, lane);
         }
         SS<D>* t = acc; acc = cur; cur = t;
         __syncwarp();

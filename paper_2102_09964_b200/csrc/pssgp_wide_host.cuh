@@ -63,6 +63,8 @@ void wide_set_smem_attrs(int device) {
             cudaFuncSetAttribute(kw_smoother_apply_q<D, true, G, W, FB>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K5QSmem<D, true, G, W>));
         };
         set(std::integral_constant<int, D>{});
+        cudaFuncSetAttribute(kw_combine_halves<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(ScanSmemF<D>));
+        cudaFuncSetAttribute(kw_part_sagg<D, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(QAgPhase<D>));
         if constexpr (D > 4) {
             set(std::integral_constant<int, 2>{});
             set(std::integral_constant<int, 4>{});
@@ -178,7 +180,9 @@ pssgp_status wide_setup(pssgp_model* m, const WPlan& pl, pssgp::wide::WParams& p
     using namespace pssgp::wide;
     const size_t nch = static_cast<size_t>(pl.nch);
     const bool quarters = (D <= kGL && wide_quarter_rescans()) || (wide_halves<D>() && wide_half_rescans());
-    const size_t nq = quarters ? nch * (kQ - 1) * (FNW(D) + SNW(D)) : 0;   // quarter prefix / smoother aggregates
+    const bool halves = wide_halves<D>() && wide_half_rescans();
+    // quarter prefix / smoother aggregates (+ the halves' end moments for kw_part_sagg)
+    const size_t nq = quarters ? nch * (kQ - 1) * (FNW(D) + SNW(D)) + (halves ? nch * 2 * QMW(D) : 0) : 0;
     const size_t need = (2 * nch * FNW(D) + nch * pl.K * CNW(D) + 2 * nch * SNW(D) + nch + nq + 64) * sizeof(double);
     if (need > m->ws_bytes) {
         if (m->ws) cudaFree(m->ws);
@@ -237,7 +241,8 @@ pssgp_status wide_setup(pssgp_model* m, const WPlan& pl, pssgp::wide::WParams& p
     p.nll_chain = w; w += nch;
     if (quarters) {
         p.qagg = w; w += nch * (kQ - 1) * FNW(D);
-        p.sqagg = w;
+        p.sqagg = w; w += nch * (kQ - 1) * SNW(D);
+        if (halves) p.qmom = w;
     }
     p.K = pl.K;
     p.nch = pl.nch;
@@ -387,6 +392,8 @@ pssgp_status wide_fold(pssgp_model* m, pssgp::wide::WParams& p, int nb, cudaStre
                 else kw_filter_fold_lpr<D, false, G, W, FB><<<nbh, 32 * W, sizeof(K1LSmem<D, false, G, W>), s>>>(p);
             });
             LAUNCH_CHECK(m, "kw_filter_fold_lpr (16-lane)");
+            kw_combine_halves<D><<<p.nch, 32, sizeof(ScanSmemF<D>), s>>>(p);   // fagg = half 0 (x) half 1
+            LAUNCH_CHECK(m, "kw_combine_halves");
             return PSSGP_OK;
         }
     }
@@ -423,6 +430,10 @@ pssgp_status wide_fapply(pssgp_model* m, pssgp::wide::WParams& p, int nb, cudaSt
                 else kw_filter_apply_q<D, false, G, W, FB><<<nbh, 32 * W, sizeof(K3QSmem<D, false, G, W>), s>>>(p);
             });
             LAUNCH_CHECK(m, "kw_filter_apply_q (16-lane)");
+            if (p.store_state) {   // the half smoother aggregates and the chain's from the end moments
+                kw_part_sagg<D, 2><<<p.nch, 32, sizeof(QAgPhase<D>), s>>>(p);
+                LAUNCH_CHECK(m, "kw_part_sagg");
+            }
             return PSSGP_OK;
         }
     }
