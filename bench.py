@@ -352,6 +352,9 @@ def main():
     dist = None
     nccl_info = None
     if world > 1:
+        # NCCL's own INIT lines (communicator size, ring / NVLS setup) in the log, once at start-up
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
         # communicator check: one all_reduce of ones over NCCL must equal the world size

@@ -977,7 +977,7 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WDISC_MINB) kw_discretize_
                                                                    const double* __restrict__ model, double* fq) {
     static_assert(D <= kGL, "one row per lane of an 8-lane group");
     const int lane = threadIdx.x & 31, grp = lane / kGL, r0 = lane % kGL;
-    const bool act = r0 < D;
+    const bool act = (D == kGL) || r0 < D;
     const int r = act ? r0 : 0;
     const unsigned gm = 0xFFu << (grp * kGL);
     double Gr[D], Wr[D];
@@ -1135,7 +1135,7 @@ __global__ void __launch_bounds__(32 * WPC, lpr_minb(G)) kw_filter_fold_lpr(cons
     const int c = blockIdx.x * WPC + wid;
     if (c >= p.nch) return;                                     // warp-uniform
     const int q = lane / G, r = lane % G, gb = q * G;
-    const bool act = r < D;
+    const bool act = (D == G) || r < D;                       // compile-time true when the group is full
     const int rr = act ? r : 0;                                 // row addressed by idle lanes
     auto& W = sh.w[wid];
     const SModel<D>& M = sh.m;
@@ -2365,7 +2365,7 @@ __global__ void __launch_bounds__(32 * WPC, lpr_minb(G)) kw_filter_apply_q(const
     // ---- the four quarters, one per 8-lane group, in registers
     const int q = lane / G, r0 = lane % G, gb = q * G;
     const unsigned gm = group_mask(G, gb);
-    const bool act = r0 < D;
+    const bool act = (D == G) || r0 < D;                      // compile-time true when the group is full
     const int r = act ? r0 : 0;
     int64_t qb, qe;
     quarter_bounds(kb, ke, p.K, q, qb, qe, NP);
@@ -2661,7 +2661,7 @@ __global__ void __launch_bounds__(32 * WPC, lpr_minb(G)) kw_smoother_apply_q(con
     }
     const int q = lane / G, r0 = lane % G, gb = q * G;
     const unsigned gm = group_mask(G, gb);
-    const bool act = r0 < D;
+    const bool act = (D == G) || r0 < D;                      // compile-time true when the group is full
     const int r = act ? r0 : 0;
     int64_t qb, qe;
     quarter_bounds(kb, ke, p.K, q, qb, qe, NP);
@@ -2839,9 +2839,17 @@ __global__ void __launch_bounds__(32 * WPC, lpr_minb(G)) kw_smoother_apply_q(con
                     }
                 }
             }
+            // 16-lane groups: column r of X back from its shared slot into registers for the two
+            // products below (one shared load per element instead of one per use)
+            double Xr[G == kGL ? 1 : D];
+            if constexpr (G > kGL) {
+                __syncwarp(gm);
+#pragma unroll
+                for (int i = 0; i < D; ++i) Xr[i] = Gs.X[i][r];
+            }
             auto XC = [&](int i) -> double {
                 if constexpr (G == kGL) return Xc[i];
-                else return Gs.X[i][r];
+                else return Xr[i];
             };
             double ms_new = XA(r), V[D];
 #pragma unroll
