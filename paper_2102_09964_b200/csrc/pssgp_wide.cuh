@@ -924,7 +924,7 @@ struct K1LSmem {
 };
 
 #ifndef PSSGP_WLPR_MINB
-#define PSSGP_WLPR_MINB 3                        // resident CTAs/SM the lane-per-row fold is register-capped for
+#define PSSGP_WLPR_MINB 4                        // resident CTAs/SM the lane-per-row fold is register-capped for
 #endif
 // lane-per-row kernels with G-lane groups: G = 8 (D <= 8, four quarter chains per warp, 4 warps per CTA)
 // or G = 16 (9 <= D <= 16, two half chains per warp, 2 warps per CTA: the per-warp shared state of
