@@ -222,6 +222,27 @@ pssgp_status pssgp_nll_grad_batched(pssgp_model* m, int nseg, const int64_t* off
                                     const double* t, const double* y, const uint8_t* mask, double* nll,
                                     double* grad, void* stream);
 
+/* Batched independent series with PER-SERIES log hyper-parameters for any sum of Matern,
+ * periodic and quasi-periodic components on a uniform grid (SURVEY.md §8(f) row 2 widened: HMC
+ * chains / multi-start fits on the paper's CO2 model).  The model m
+ * gives the structure (components, orders, uniform_dt > 0); theta (device, nseg x
+ * pssgp_num_params(m), row b = series b, the order of pssgp_nll_grad) replaces its
+ * hyper-parameters per series.  Series b = steps [offsets[b], offsets[b+1]) (device int64[nseg+1],
+ * non-decreasing, offsets[nseg] = N); each starts from its stationary prior; steps inside a series
+ * are uniform_dt apart or ties (dt = 0), else PSSGP_E_UNSUPPORTED from pssgp_check.  The per-series
+ * F, Q, P_inf and their theta-derivatives are closed forms built on the device
+ * (pssgp_batch_theta.cuh); one warp runs each series' sequential Kalman filter and RTS smoother /
+ * reverse-mode adjoint (series share nothing, so no scan).  Outputs (device): mean[N], var[N]
+ * (nullable), nll[nseg], grad[nseg x pssgp_num_params].  RBF components -> PSSGP_E_UNSUPPORTED. */
+pssgp_status pssgp_posterior_batched_theta(pssgp_model* m, int nseg, const int64_t* offsets,
+                                           const double* theta, int64_t N, const double* t,
+                                           const double* y, const uint8_t* mask, double* mean,
+                                           double* var, double* nll, void* stream);
+pssgp_status pssgp_nll_grad_batched_theta(pssgp_model* m, int nseg, const int64_t* offsets,
+                                          const double* theta, int64_t N, const double* t,
+                                          const double* y, const uint8_t* mask, double* nll,
+                                          double* grad, void* stream);
+
 /* Synchronise the handle's last stream and return the first device-detected
  * error (PSSGP_E_INPUT / PSSGP_E_NUMERIC / PSSGP_E_UNSUPPORTED) since the last
  * pssgp_check, or PSSGP_OK.  Clears the latched error. */

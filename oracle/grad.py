@@ -335,3 +335,18 @@ def kf_nll_grad_general(components, noise_var, t, y, mask, h: float = 1e-20):
         tc[p] += 1j * h
         grad[p] = np.imag(kf_nll_theta(components, tc, t, y, mask)) / h
     return nll, grad
+
+
+def components_at(components, theta):
+    """The kernel spec and noise variance at log-hyper-parameters theta (param_names order)."""
+    import dataclasses
+    out, i = [], 0
+    for c in components:
+        kw = dict(variance=math.exp(theta[i]), lengthscale=math.exp(theta[i + 1]))
+        i += 2
+        if c.kind in ("periodic", "quasiperiodic"):
+            kw["period"] = math.exp(theta[i]); i += 1
+        if c.kind == "quasiperiodic":
+            kw["mat_lengthscale"] = math.exp(theta[i]); i += 1
+        out.append(dataclasses.replace(c, **kw))
+    return out, math.exp(theta[i])

@@ -26,7 +26,8 @@ __all__ = ["Model", "PssgpError", "build", "lib", "pssgp_create", "pssgp_destroy
            "pssgp_aggregate_bytes", "pssgp_shard_filter_reduce", "pssgp_shard_filter_apply",
            "pssgp_shard_smoother_apply", "pssgp_profile_enable", "pssgp_profile_read", "pssgp_profile_name",
            "pssgp_merge_grid", "pssgp_gather", "pssgp_predict", "pssgp_posterior_batched", "pssgp_nll_grad_batched",
-           "pssgp_posterior_f32", "pssgp_plan_f32", "pssgp_measure_fp64_peak", "pssgp_num_params"]
+           "pssgp_posterior_f32", "pssgp_plan_f32", "pssgp_measure_fp64_peak", "pssgp_num_params",
+           "pssgp_posterior_batched_theta", "pssgp_nll_grad_batched_theta"]
 
 
 def _ptr(x) -> Optional[int]:
@@ -232,6 +233,16 @@ def pssgp_shard_smoother_apply(h, k0, n, N_global, t_ptr, all_ptr, rank, world, 
                                stream=None) -> None:
     _raise(h, lib().pssgp_shard_smoother_apply(h, int(k0), int(n), int(N_global), t_ptr, all_ptr, int(rank),
                                                int(world), mean_ptr, var_ptr, nll_ptr, _stream_ptr(stream)))
+
+
+def pssgp_posterior_batched_theta(h, nseg, offsets, theta, N, t, y, mask, mean, var, nll, stream=None) -> None:
+    _raise(h, lib().pssgp_posterior_batched_theta(h, int(nseg), _ptr(offsets), _ptr(theta), int(N), _ptr(t), _ptr(y),
+                                                  _ptr(mask), _ptr(mean), _ptr(var), _ptr(nll), _stream_ptr(stream)))
+
+
+def pssgp_nll_grad_batched_theta(h, nseg, offsets, theta, N, t, y, mask, nll, grad, stream=None) -> None:
+    _raise(h, lib().pssgp_nll_grad_batched_theta(h, int(nseg), _ptr(offsets), _ptr(theta), int(N), _ptr(t), _ptr(y),
+                                                 _ptr(mask), _ptr(nll), _ptr(grad), _stream_ptr(stream)))
 
 
 def pssgp_num_params(h) -> int:

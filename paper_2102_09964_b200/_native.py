@@ -115,6 +115,10 @@ SIGNATURES = {
                                                _vp, _vp, _vp]),
     "pssgp_nll_grad_batched": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp,
                                               _vp, _vp]),
+    "pssgp_posterior_batched_theta": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp,
+                                                     _vp, _vp]),
+    "pssgp_nll_grad_batched_theta": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp,
+                                                    _vp]),
     "pssgp_error_index": (ctypes.c_int64, [_vp]),
     "pssgp_last_error": (ctypes.c_char_p, [_vp]),
     "pssgp_get_ssm": (ctypes.c_int, [_vp, _dp, _dp, _dp, _dp, _dp]),

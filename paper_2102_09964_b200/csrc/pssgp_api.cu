@@ -357,6 +357,8 @@ pssgp_status pssgp_create(const pssgp_component* comps, int n_comps, double nois
     // variance: W and P_inf scale; time-scale parameter: G, W scale as 1 / tau (host_model.hpp)
     auto vscale = [](const ph::Ssm& p) { return ph::ParamDeriv{ph::zeros(p.d), p.W, p.Pinf}; };
     auto tscale = [](const ph::Ssm& p) { return ph::ParamDeriv{ph::scaled(p.G, -1.0L), ph::scaled(p.W, -1.0L), ph::zeros(p.d)}; };
+    int boff = 0, bpar = 0;
+    m->bt_ok = true;
     for (int c = 0; c < n_comps; ++c) {
         const pssgp_component& k = comps[c];
         if (!(k.variance > 0.0) || !std::isfinite(k.variance) || !(k.lengthscale > 0.0) || !std::isfinite(k.lengthscale)) {
@@ -414,6 +416,14 @@ pssgp_status pssgp_create(const pssgp_component* comps, int n_comps, double nois
             return PSSGP_E_UNSUPPORTED;
         }
         if (k.kind != PSSGP_PERIODIC && k.kind != PSSGP_QUASIPERIODIC) cder.push_back({vscale(part), tscale(part)});
+        {   // structure for the batched per-series-theta path (closed-form models only, not RBF)
+            const int bk = (k.kind <= PSSGP_MATERN52) ? 1 : (k.kind == PSSGP_PERIODIC ? 2 : (k.kind == PSSGP_QUASIPERIODIC ? 3 : 0));
+            if (bk == 0) m->bt_ok = false;
+            const int nu2 = (k.kind <= PSSGP_MATERN52) ? 2 * k.kind - 1 : k.mat_nu2;
+            m->bdesc.insert(m->bdesc.end(), {bk, k.order, nu2, boff, part.d, bpar});
+            boff += part.d;
+            bpar += static_cast<int>(cder.back().size());
+        }
         parts.push_back(part);
     }
     m->ssm = parts.size() == 1 ? parts[0] : ph::block_sum(parts);
@@ -483,6 +493,7 @@ void pssgp_destroy(pssgp_model* m) {
     if (m->d_model) cudaFree(m->d_model);
     if (m->d_gder) cudaFree(m->d_gder);
     if (m->gw) cudaFree(m->gw);
+    if (m->bw) cudaFree(m->bw);
     for (int s = 0; s < kSlots; ++s)
         for (auto& pr : m->ev[s]) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
     for (auto e : m->ev_pool) cudaEventDestroy(e);
@@ -915,6 +926,42 @@ pssgp_status pssgp_measure_fp64_peak(pssgp_model* m, double* tflops) {
     if (e != cudaSuccess) return cuda_fail(m, e, "fp64 probe");
     *tflops = best;
     return PSSGP_OK;
+}
+
+// batched series with per-series log hyper-parameters (pssgp_batch_theta.cuh)
+static pssgp_status batched_theta(pssgp_model* m, int nseg, const int64_t* offsets, const double* theta, int64_t N,
+                                  const double* t, const double* y, const uint8_t* mask, double* mean, double* var,
+                                  double* nll, double* grad, void* stream) {
+    pssgp_status st = check_args(m, N, t, y, mask);
+    if (st) return st;
+    if (nseg < 1 || !offsets || !theta || !nll) return fail(m, PSSGP_E_ARG, "bad batched-theta arguments");
+    if (!m->bt_ok || !(m->udt > 0.0))
+        return fail(m, PSSGP_E_UNSUPPORTED,
+                    "batched per-series hyper-parameters need Matern / periodic / quasi-periodic components on a "
+                    "uniform grid (options.uniform_dt > 0)");
+    if ((st = ensure_device(m))) return st;
+    auto s = static_cast<cudaStream_t>(stream);
+    m->last_stream = s;
+    pssgp::batch::k_batch_check_offsets<<<(nseg + 256) / 256, 256, 0, s>>>(offsets, nseg, N, m->d_err);
+    LAUNCH_CHECK(m, "k_batch_check_offsets");
+    const WideOps* ops = wide_ops_for(m->d);
+    if (!ops) return fail(m, PSSGP_E_UNSUPPORTED, "state dimension not compiled");
+    return ops->batched_theta(m, nseg, offsets, theta, N, t, y, mask, mean, var, nll, grad, s);
+}
+
+pssgp_status pssgp_posterior_batched_theta(pssgp_model* m, int nseg, const int64_t* offsets, const double* theta,
+                                           int64_t N, const double* t, const double* y, const uint8_t* mask,
+                                           double* mean, double* var, double* nll, void* stream) {
+    NvtxCall nvtx_("pssgp_posterior_batched_theta");
+    return batched_theta(m, nseg, offsets, theta, N, t, y, mask, mean, var, nll, nullptr, stream);
+}
+
+pssgp_status pssgp_nll_grad_batched_theta(pssgp_model* m, int nseg, const int64_t* offsets, const double* theta,
+                                          int64_t N, const double* t, const double* y, const uint8_t* mask,
+                                          double* nll, double* grad, void* stream) {
+    NvtxCall nvtx_("pssgp_nll_grad_batched_theta");
+    if (!grad) return fail(m, PSSGP_E_ARG, "grad is NULL");
+    return batched_theta(m, nseg, offsets, theta, N, t, y, mask, nullptr, nullptr, nll, grad, stream);
 }
 
 pssgp_status pssgp_check(pssgp_model* m) {

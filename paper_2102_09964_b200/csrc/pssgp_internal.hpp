@@ -31,6 +31,11 @@ struct pssgp_model {
     double udt = 0.0;
     std::vector<double> Fu, Qu;  // F(udt), Q(udt) row-major d x d
     std::vector<pssgp_host::ParamDeriv> pder;   // d(G, W, P_inf) / d theta_p, p < npar - 1 (log noise last)
+    std::vector<int> bdesc;      // per component: kind (1 Matern, 2 periodic, 3 quasi, 0 other), order,
+                                 // 2 nu, state offset, block size, first parameter (batched-theta path)
+    bool bt_ok = false;          // every component has a closed-form per-series model
+    char* bw = nullptr;          // batched-theta workspace (series model records, filtered moments)
+    size_t bw_bytes = 0;
     double* d_gder = nullptr;    // device: per parameter dF, dQ (at udt), dP_inf (d x d each)
     char* gw = nullptr;          // general-model gradient workspace
     size_t gw_bytes = 0;
@@ -168,6 +173,9 @@ struct WideOps {
     pssgp_status (*debug_disc)(pssgp_model*, double dt, double* F, double* Q);
     pssgp_status (*nll_grad)(pssgp_model*, int64_t N, const double* t, const double* y, const uint8_t* mask,
                              double* nll, double* grad, cudaStream_t s);
+    pssgp_status (*batched_theta)(pssgp_model*, int nseg, const int64_t* off, const double* theta, int64_t N,
+                                  const double* t, const double* y, const uint8_t* mask, double* mean, double* var,
+                                  double* nll, double* grad, cudaStream_t s);
     void (*plan)(pssgp_model*, int64_t N, int64_t* K, int64_t* nch, int* nb, int* threads);
 };
 template <int D>

@@ -12,6 +12,7 @@
 
 #include "pssgp_internal.hpp"
 #include "pssgp_wide.cuh"
+#include "pssgp_batch_theta.cuh"
 
 namespace pssgp_internal {
 namespace widehost {
@@ -669,6 +670,73 @@ pssgp_status wide_nll_grad(pssgp_model* m, int64_t N, const double* t, const dou
         LAUNCH_CHECK(m, "k_grad_contract");
     }
     if (nll) return nll_sum(m, p.nll_chain, p.nch, nll, s);
+    return PSSGP_OK;
+}
+
+
+// ---- batched series with per-series log hyper-parameters (pssgp_batch_theta.cuh): the series
+// models on the device, then one warp per series for the posterior or the NLL gradient
+template <int D>
+pssgp_status wide_batched_theta(pssgp_model* m, int nseg, const int64_t* off, const double* theta, int64_t N,
+                                const double* t, const double* y, const uint8_t* mask, double* mean, double* var,
+                                double* nll, double* grad, cudaStream_t s) {
+    using namespace pssgp::wide;
+    if (!m->bt_ok || !(m->udt > 0.0))
+        return fail(m, PSSGP_E_UNSUPPORTED,
+                    "batched per-series hyper-parameters need Matern / periodic / quasi-periodic components on a "
+                    "uniform grid (options.uniform_dt > 0)");
+    const int nc = static_cast<int>(m->bdesc.size() / 6);
+    if (nc > kBMaxComp) return fail(m, PSSGP_E_UNSUPPORTED, "too many components");
+    BModelDesc md;
+    std::memset(&md, 0, sizeof(md));
+    md.nc = nc;
+    md.npar = static_cast<int>(m->pder.size()) + 1;
+    md.d = D;
+    md.udt = m->udt;
+    for (int c = 0; c < nc; ++c) {
+        const int* v = &m->bdesc[6 * c];
+        md.c[c] = BComp{v[0], v[1], v[2], v[3], v[4], v[5]};
+    }
+    const size_t nrec = static_cast<size_t>(nseg) * BREC(D, md.npar);
+    const size_t need = (nrec + static_cast<size_t>(N) * CNW(D) + D + 8) * sizeof(double);
+    if (need > m->bw_bytes) {
+        if (m->bw) cudaFree(m->bw);
+        m->bw = nullptr;
+        m->bw_bytes = 0;
+        if (cudaMalloc(&m->bw, need) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(m, PSSGP_E_NOMEM, "cudaMalloc(batched-theta workspace)");
+        }
+        m->bw_bytes = need;
+    }
+    double* recs = reinterpret_cast<double*>(m->bw);
+    double* xs = recs + nrec;
+    double* Hd = xs + static_cast<size_t>(N) * CNW(D);
+    {
+        double hh[D];
+        for (int i = 0; i < D; ++i) hh[i] = static_cast<double>(m->ssm.H[i]);
+        cudaMemcpyAsync(Hd, hh, sizeof(hh), cudaMemcpyHostToDevice, s);
+        cudaStreamSynchronize(s);   // hh is a host stack buffer
+    }
+    {
+        ProfScope ps(m, S_DISC, s);
+        kb_build<D><<<(nseg + 127) / 128, 128, 0, s>>>(md, nseg, theta, recs);
+        LAUNCH_CHECK(m, "kb_build");
+    }
+    BParamsT q;
+    q.off = off; q.nseg = nseg; q.npar = md.npar; q.udt = m->udt; q.recs = recs;
+    q.t = t; q.y = y; q.mask = mask; q.xs = xs;
+    q.mean = mean; q.var = var; q.nll = nll; q.grad = grad; q.err = m->d_err;
+    static_assert(sizeof(BSmem<D>) <= 48 * 1024, "per-series shared state");
+    if (grad) {
+        ProfScope ps(m, S_GRAD, s);
+        kb_nll_grad<D><<<nseg, 32, sizeof(BSmem<D>), s>>>(q, Hd);
+        LAUNCH_CHECK(m, "kb_nll_grad");
+    } else {
+        ProfScope ps(m, S_K3, s);
+        kb_posterior<D><<<nseg, 32, sizeof(BSmem<D>), s>>>(q, Hd);
+        LAUNCH_CHECK(m, "kb_posterior");
+    }
     return PSSGP_OK;
 }
 

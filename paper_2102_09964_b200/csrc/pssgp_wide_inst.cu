@@ -24,7 +24,8 @@ template <>
 const WideOps* wide_ops<D>() {
     static const WideOps ops = {widehost::wide_posterior<D>, widehost::wide_shard_reduce<D>,
                                 widehost::wide_shard_fapply<D>, widehost::wide_shard_sapply<D>,
-                                widehost::wide_debug_discretize<D>, widehost::wide_nll_grad<D>, wplan};
+                                widehost::wide_debug_discretize<D>, widehost::wide_nll_grad<D>,
+                                widehost::wide_batched_theta<D>, wplan};
     return &ops;
 }
 }  // namespace pssgp_internal

@@ -12,6 +12,7 @@ import numpy as np
 import pytest
 import torch
 
+import oracle
 import synth
 from oracle import grad as og
 import paper_2102_09964_b200 as P
@@ -283,3 +284,96 @@ def test_grad_general_needs_uniform_grid(cuda_device):
     with pytest.raises(P.PssgpError) as e:
         m.nll_grad(t, y, mk)
     assert e.value.status == 6                       # PSSGP_E_UNSUPPORTED
+
+
+# ---------------------------------------------------------------- batched series, per-series theta
+BT_MODELS = {
+    "co2_J1": [synth.Component("quasiperiodic", 2.0, 1.0, period=52.0, order=1, mat_lengthscale=300.0, mat_nu2=3),
+               synth.Component("matern32", 10.0, 1040.0)],
+    "co2_J2": [synth.Component("quasiperiodic", 2.0, 1.0, period=52.0, order=2, mat_lengthscale=300.0, mat_nu2=3),
+               synth.Component("matern32", 10.0, 1040.0)],
+    "per3+m52": [synth.Component("periodic", 1.5, 0.8, period=40.0, order=3), synth.Component("matern52", 1.0, 60.0)],
+    "m12+m32": [synth.Component("matern12", 1.0, 30.0), synth.Component("matern32", 0.5, 200.0)],
+    "quasi_m12": [synth.Component("quasiperiodic", 1.0, 0.9, period=30.0, order=2, mat_lengthscale=100.0, mat_nu2=1)],
+}
+
+
+def _batched_theta_problem(name, lens=(1, 2, 300, 701, 1200), seed=3):
+    """Series on a weekly grid (dt = 1 week), each with its own log hyper-parameters near the base."""
+    comps = BT_MODELS[name]
+    rng = np.random.default_rng(seed)
+    th0 = og.theta0(comps, 0.09)
+    ts, ys, ms, thetas = [], [], [], []
+    for i, n in enumerate(lens):
+        t = 17.0 * i + np.arange(n, dtype=np.float64)
+        mask = (rng.random(n) > 0.1).astype(np.uint8)
+        y = synth.co2_like(t / 52.0) + 0.3 * rng.standard_normal(n)
+        y[mask == 0] = np.nan
+        ts.append(t); ys.append(y); ms.append(mask)
+        thetas.append(th0 + rng.uniform(-0.25, 0.25, th0.shape[0]))
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    return comps, ts, ys, ms, np.array(thetas), off
+
+
+@pytest.mark.parametrize("name", list(BT_MODELS))
+def test_batched_theta_grad_and_posterior(cuda_device, name):
+    """Per-series hyper-parameters for sums of Matern / periodic / quasi-periodic components (the
+    paper's HMC chains on the CO2 model): each series against the oracle at its own theta
+    (complex-step gradient; sequential KF + RTS posterior)."""
+    comps, ts, ys, ms, thetas, off = _batched_theta_problem(name)
+    B, npar = thetas.shape
+    m = P.Model(comps, 0.09, uniform_dt=1.0)
+    assert m.num_params == npar
+    dev = "cuda:0"
+    t = torch.from_numpy(np.concatenate(ts)).to(dev)
+    y = torch.from_numpy(np.concatenate(ys)).to(dev)
+    mk = torch.from_numpy(np.concatenate(ms)).to(dev)
+    N = int(t.shape[0])
+    offd = torch.from_numpy(off).to(dev)
+    th = torch.from_numpy(np.ascontiguousarray(thetas)).to(dev)
+    nll = torch.zeros(B, dtype=torch.float64, device=dev)
+    grad = torch.zeros(B * npar, dtype=torch.float64, device=dev)
+    P.pssgp_nll_grad_batched_theta(m.h, B, offd, th, N, t, y, mk, nll, grad)
+    mean = torch.zeros(N, dtype=torch.float64, device=dev)
+    var = torch.zeros(N, dtype=torch.float64, device=dev)
+    nll2 = torch.zeros(B, dtype=torch.float64, device=dev)
+    P.pssgp_posterior_batched_theta(m.h, B, offd, th, N, t, y, mk, mean, var, nll2)
+    m.check()
+    g = grad.cpu().numpy().reshape(B, npar)
+    nl, nl2, mean, var = nll.cpu().numpy(), nll2.cpu().numpy(), mean.cpu().numpy(), var.cpu().numpy()
+    for b in range(B):
+        cb, rb = og.components_at(comps, thetas[b])
+        nll_r, g_r = og.kf_nll_grad_general(cb, rb, ts[b], ys[b], ms[b])
+        assert abs(nl[b] - nll_r) <= NLL_TOL * max(abs(nll_r), 1.0), (b, nl[b], nll_r)
+        assert nl2[b] == nl[b]
+        err = grad_err(g[b], g_r)
+        assert np.all(err <= GRAD_TOL), (b, g[b], g_r, err)
+        o = oracle.posterior(synth.Workload("bt", cb, rb, ts[b], ys[b], ms[b]))
+        sl = slice(off[b], off[b + 1])
+        assert np.max(np.abs(mean[sl] - o["mean"])) <= 1e-8 * max(np.max(np.abs(o["mean"])), 1e-300)
+        assert np.max(np.abs(var[sl] - o["var"]) / o["var"]) <= 1e-8
+
+
+def test_batched_theta_rejects_rbf_and_irregular(cuda_device):
+    comps = [synth.Component("rbf", 1.0, 0.5, order=4)]
+    m = P.Model(comps, 0.02, uniform_dt=0.01)
+    dev = "cuda:0"
+    t = torch.arange(10, dtype=torch.float64, device=dev) * 0.01
+    y = torch.zeros(10, dtype=torch.float64, device=dev)
+    mk = torch.ones(10, dtype=torch.uint8, device=dev)
+    off = torch.tensor([0, 10], dtype=torch.int64, device=dev)
+    th = torch.zeros((1, m.num_params), dtype=torch.float64, device=dev)
+    nll = torch.zeros(1, dtype=torch.float64, device=dev)
+    with pytest.raises(P.PssgpError) as e:
+        P.pssgp_posterior_batched_theta(m.h, 1, off, th, 10, t, y, mk, None, None, nll)
+    assert e.value.status == 6
+    # a non-uniform step inside a series is reported by pssgp_check
+    m = P.Model([synth.Component("matern32", 1.0, 0.5), synth.Component("matern12", 1.0, 2.0)], 0.02, uniform_dt=0.01)
+    th = torch.from_numpy(og.theta0(m_comps := [synth.Component("matern32", 1.0, 0.5),
+                                                synth.Component("matern12", 1.0, 2.0)], 0.02)[None, :]).to(dev)
+    t2 = t.clone()
+    t2[5:] += 0.003
+    P.pssgp_posterior_batched_theta(m.h, 1, off, th, 10, t2, y, mk, None, None, nll)
+    with pytest.raises(P.PssgpError) as e:
+        m.check()
+    assert e.value.status == 6
