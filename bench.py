@@ -64,10 +64,10 @@ def alg_bytes(slot: str, d: int, wide_stream: bool = False, f32: bool = False) -
 
 # kernel families behind each profile slot (thread path d <= 3, wide path d >= 4)
 _FAMILY = {"k_filter_reduce": ("k_filter_reduce", ("kw_filter_fold",)),
-           "k_filter_apply": ("k_filter_apply", ("kw_filter_apply", "kw_grad_forward")),
+           "k_filter_apply": ("k_filter_apply", ("kw_filter_apply", "kw_grad_forward", "kb_posterior")),
            "k_smoother_apply": ("k_smoother_apply", ("kw_smoother_apply",)),
-           "k_grad_fold": ("k_grad_fold", ("k_grad_fold", "kw_grad_backward")),
-           "k_discretize": ("k_discretize", ("kw_discretize",)), "k_filter_scan": ("", ("kw_scan_filter",)),
+           "k_grad_fold": ("k_grad_fold", ("k_grad_fold", "kw_grad_backward", "kb_nll_grad")),
+           "k_discretize": ("k_discretize", ("kw_discretize", "kb_build")), "k_filter_scan": ("", ("kw_scan_filter",)),
            "k_smoother_scan": ("", ("kw_scan_smoother", "kw_scan_adjoint"))}
 
 
@@ -141,7 +141,8 @@ def parse():
     ap.add_argument("--N", type=int, default=2 ** 24)
     ap.add_argument("--uniform", action="store_true", help="uniform dt (secondary row)")
     ap.add_argument("--kind", default="matern52")
-    ap.add_argument("--config", default="metric", choices=["metric", "c2", "c3", "c4", "c5", "batched", "grad", "gradb", "gradco2", "f32"],
+    ap.add_argument("--config", default="metric", choices=["metric", "c2", "c3", "c4", "c5", "batched", "grad", "gradb", "gradco2", "gradbt",
+                                                          "batchedbt", "f32"],
                     help="workload (default: the BASELINE metric); c3/c4 are the d = 6 / d = 16 rows")
     ap.add_argument("--irregular", action="store_true", help="c3/c4 on a jittered grid (device Pade discretisation)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -299,6 +300,10 @@ def make_workload(args):
         return synth.metric_workload(3200 * 4, kind="matern52")
     if args.config == "grad":
         return synth.metric_workload(args.N)
+    if args.config in ("gradbt", "batchedbt"):
+        # B HMC chains / multi-start fits of the paper's CO2 model (J = 3, n_x = 18), one 3,200-week
+        # series each
+        return synth.co2_product(n=3200, order=3)
     if args.config == "gradco2":
         # the paper's HMC model C_Per x C_Mat + C_Mat at n_x = 18 (J = 3), weekly grid
         return synth.co2_product(n=args.N if args.N != 2 ** 24 else 2 ** 20, order=3)
@@ -399,6 +404,29 @@ def main():
             def step():
                 P.pssgp_nll_grad_batched(model.h, B, off, VB, EB, RB, N, t, y, mk, nllb, gb, stream)
         n_local = N
+    elif args.config in ("gradbt", "batchedbt"):
+        # f2 widened: B series of the CO2 grid, each at its own log hyper-parameters (theta_b drawn
+        # around the model's own, +-0.25), one launch: the HMC-chain shape of PAPER.md:224-235
+        B = max(1, args.N // 3200) if args.N != 2 ** 24 else 1024
+        rng = np.random.default_rng(rank)
+        lens = np.full(B, w.N, np.int64)
+        off = torch.from_numpy(np.concatenate([[0], np.cumsum(lens)])).to(dev)
+        th = torch.from_numpy(model.theta[None, :] + rng.uniform(-0.25, 0.25, (B, model.num_params))).to(dev)
+        N = int(lens.sum())
+        t = torch.from_numpy(np.tile(w.t, B)).to(dev)
+        y = torch.from_numpy(np.tile(w.y, B)).to(dev)
+        mk = torch.from_numpy(np.tile(w.mask, B)).to(dev)
+        nllb = torch.empty(B, dtype=torch.float64, device=dev)
+        gb = torch.empty(B * model.num_params, dtype=torch.float64, device=dev)
+        mean = torch.empty(N, dtype=torch.float64, device=dev)
+        var = torch.empty_like(mean)
+        if args.config == "gradbt":
+            def step():
+                P.pssgp_nll_grad_batched_theta(model.h, B, off, th, N, t, y, mk, nllb, gb, stream)
+        else:
+            def step():
+                P.pssgp_posterior_batched_theta(model.h, B, off, th, N, t, y, mk, mean, var, nllb, stream)
+        n_local = N
     elif args.config in ("grad", "gradco2"):
         # f1: NLL + its gradient in every log hyper-parameter (one L-BFGS / HMC evaluation): the metric
         # grid (one Matern component, 3 parameters) or the CO2 model (reverse mode, 8 parameters)
@@ -480,13 +508,13 @@ def main():
     ms_step = ms_total / args.steps
     # independent problems per rank (batched series, gradient evaluations): weak scaling, the
     # job's units are all ranks' steps; the time-sharded posterior: strong scaling over one grid
-    replicas = args.config in ("batched", "grad", "gradb", "gradco2") and world > 1
+    replicas = args.config in ("batched", "grad", "gradb", "gradco2", "gradbt", "batchedbt") and world > 1
     units = N * world if replicas else N
     value = units / (ms_step * 1e-3)
 
     # ---- e2e through the public host API (pinned buffers, copies inside the timed region)
     e2e = None
-    if world == 1 and args.config not in ("batched", "grad", "gradb", "gradco2", "f32"):
+    if world == 1 and args.config not in ("batched", "grad", "gradb", "gradco2", "gradbt", "batchedbt", "f32"):
         th = torch.from_numpy(w.t).pin_memory()
         yh = torch.from_numpy(w.y).pin_memory()
         mh = torch.from_numpy(w.mask).pin_memory()
@@ -603,6 +631,11 @@ def main():
         metric = f"time-steps/s (filter+smoother+NLL, fp32 state) {w.name} N={N}"
     elif args.config == "gradb":
         metric = f"time-steps/s (per-series NLL + gradient, fp64) batched Matern-5/2 series of 3200 N={N}"
+    elif args.config == "gradbt":
+        metric = (f"time-steps/s (per-series NLL + {model.num_params}-parameter gradient at per-series theta, fp64) "
+                  f"{w.name} x {N // w.N} series N={N}")
+    elif args.config == "batchedbt":
+        metric = f"time-steps/s (filter+smoother+NLL at per-series theta, fp64) {w.name} x {N // w.N} series N={N}"
     else:
         metric = (f"time-steps/s (filter+smoother+NLL, fp64) "
                   f"{w.name if args.config != 'batched' else 'batched Matern-5/2 series of 3200'} N={N}")

@@ -332,6 +332,38 @@ class Model:
         pssgp_nll_grad(self.h, N, t, y, mask, nll, grad, stream)
         return nll, grad
 
+    @property
+    def theta(self) -> np.ndarray:
+        """The model's own log hyper-parameters in the order of nll_grad (host array)."""
+        th = []
+        for c in self.components:
+            th += [np.log(c.variance), np.log(c.lengthscale)]
+            if c.kind in ("periodic", "quasiperiodic"):
+                th.append(np.log(c.period))
+            if c.kind == "quasiperiodic":
+                th.append(np.log(c.mat_lengthscale))
+        return np.array(th + [np.log(self.noise_var)], dtype=np.float64)
+
+    def nll_grad_batched_theta(self, offsets, theta, t, y, mask, stream=None):
+        """Series b = [offsets[b], offsets[b+1]) with its own log hyper-parameters theta[b]
+        (device [B, num_params]): (nll[B], grad[B, num_params])."""
+        import torch
+        B = int(offsets.shape[0]) - 1
+        nll = torch.zeros(B, dtype=torch.float64, device=t.device)
+        grad = torch.zeros((B, self.num_params), dtype=torch.float64, device=t.device)
+        pssgp_nll_grad_batched_theta(self.h, B, offsets, theta, int(t.shape[0]), t, y, mask, nll, grad, stream)
+        return nll, grad
+
+    def posterior_batched_theta(self, offsets, theta, t, y, mask, stream=None):
+        """(mean[N], var[N], nll[B]) of B series, each at its own log hyper-parameters theta[b]."""
+        import torch
+        B, N = int(offsets.shape[0]) - 1, int(t.shape[0])
+        mean = torch.empty(N, dtype=torch.float64, device=t.device)
+        var = torch.empty_like(mean)
+        nll = torch.zeros(B, dtype=torch.float64, device=t.device)
+        pssgp_posterior_batched_theta(self.h, B, offsets, theta, N, t, y, mask, mean, var, nll, stream)
+        return mean, var, nll
+
     def posterior_host(self, t: np.ndarray, y: np.ndarray, mask: np.ndarray, mean=None, var=None, nll=None):
         N = int(t.shape[0])
         mean = np.empty(N) if mean is None else mean

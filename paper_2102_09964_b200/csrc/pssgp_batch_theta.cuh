@@ -32,16 +32,51 @@ namespace wide {
     for (int v##_0 = 0; v##_0 < (n); v##_0 += 32) \
         if (const int v = v##_0 + lane; v < (n))
 
-// Out = op(A) op(B) (+ Cadd), one warp, shared operands (no aliasing of Out with A, B)
+// Out = op(A) op(B) (+ Cadd), one warp, shared operands (no aliasing of Out with A, B).  D >= 6:
+// the lanes form a 4 x 8 grid and each holds a register tile of RB contiguous rows x CB columns
+// strided by 8 (RB = ceil(D / 4), CB = ceil(D / 8); 5 x 3 at D = 18): RB + CB shared loads per
+// RB * CB FMAs instead of 2 per FMA; edge lanes clamp their loads and skip their stores.
 template <int D, bool TA = false, bool TB = false>
 __device__ __forceinline__ void bmm(double (*Out)[LD(D)], const double (*A)[LD(D)], const double (*B)[LD(D)],
                                     const double (*Cadd)[LD(D)], int lane) {
-    BT_EACH(e, D * D) {
-        const int i = e / D, j = e - (e / D) * D;
-        double s = Cadd ? Cadd[i][j] : 0.0;
-#pragma unroll 8
-        for (int k = 0; k < D; ++k) s = fma(TA ? A[k][i] : A[i][k], TB ? B[j][k] : B[k][j], s);
-        Out[i][j] = s;
+    if constexpr (D * D <= 32) {
+        BT_EACH(e, D * D) {
+            const int i = e / D, j = e - (e / D) * D;
+            double s = Cadd ? Cadd[i][j] : 0.0;
+#pragma unroll
+            for (int k = 0; k < D; ++k) s = fma(TA ? A[k][i] : A[i][k], TB ? B[j][k] : B[k][j], s);
+            Out[i][j] = s;
+        }
+    } else {
+        constexpr int PC = 8, RB = (D + 3) / 4, CB = (D + PC - 1) / PC;
+        const int i0 = (lane / PC) * RB, pc = lane % PC;
+        int ri[RB], cj[CB];
+#pragma unroll
+        for (int r = 0; r < RB; ++r) ri[r] = min(i0 + r, D - 1);
+#pragma unroll
+        for (int c = 0; c < CB; ++c) cj[c] = min(pc + c * PC, D - 1);
+        double acc[RB][CB];
+#pragma unroll
+        for (int r = 0; r < RB; ++r)
+#pragma unroll
+            for (int c = 0; c < CB; ++c) acc[r][c] = Cadd ? Cadd[ri[r]][cj[c]] : 0.0;
+#pragma unroll 2
+        for (int k = 0; k < D; ++k) {
+            double a[RB], b[CB];
+#pragma unroll
+            for (int r = 0; r < RB; ++r) a[r] = TA ? A[k][ri[r]] : A[ri[r]][k];
+#pragma unroll
+            for (int c = 0; c < CB; ++c) b[c] = TB ? B[cj[c]][k] : B[k][cj[c]];
+#pragma unroll
+            for (int r = 0; r < RB; ++r)
+#pragma unroll
+                for (int c = 0; c < CB; ++c) acc[r][c] = fma(a[r], b[c], acc[r][c]);
+        }
+#pragma unroll
+        for (int r = 0; r < RB; ++r)
+#pragma unroll
+            for (int c = 0; c < CB; ++c)
+                if (i0 + r < D && pc + c * PC < D) Out[i0 + r][pc + c * PC] = acc[r][c];
     }
 }
 template <int D>

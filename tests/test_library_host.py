@@ -205,3 +205,5 @@ def test_num_params_order():
                   [synth.Component("rbf", 1.0, 0.5, order=6)]):
         m = P.Model(comps, 0.1, uniform_dt=0.01)
         assert m.num_params == len(og.param_names(comps))
+        # Model.theta (the row layout of the batched per-series calls) = the oracle's theta0
+        np.testing.assert_allclose(m.theta, og.theta0(comps, 0.1), rtol=0, atol=1e-15)
