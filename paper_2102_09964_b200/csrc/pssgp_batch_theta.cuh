@@ -24,22 +24,31 @@
 namespace pssgp {
 namespace wide {
 
-// Lane-strided loops with a trip count that is the same in every lane (the guard, not the loop,
-// diverges).  ptxas 12.9 elides the __syncwarp that ends an iteration of the series loop when the
-// last loop before it had lane-dependent trip counts (D * D > 32) without re-converging the warp:
-// the lanes that finished early then ran into the next step and read half-updated shared state.
+// NW warps per series (NT = 32 NW threads).  Thread-strided loops with a trip count that is the
+// same in every thread (the guard, not the loop, diverges): ptxas 12.9 dropped the end-of-step
+// __syncwarp of a one-warp series loop whose last inner loop had lane-dependent trip counts (D * D
+// > 32) without re-converging the warp, and lanes that finished early read half-updated shared
+// state.  Loops over D (<= 20) elements run in warp 0 only.
 #define BT_EACH(v, n) \
-    for (int v##_0 = 0; v##_0 < (n); v##_0 += 32) \
-        if (const int v = v##_0 + lane; v < (n))
+    for (int v##_0 = 0; v##_0 < (n); v##_0 += NT) \
+        if (const int v = v##_0 + tid; v < (n))
 
-// Out = op(A) op(B) (+ Cadd), one warp, shared operands (no aliasing of Out with A, B).  D >= 6:
-// the lanes form a 4 x 8 grid and each holds a register tile of RB contiguous rows x CB columns
-// strided by 8 (RB = ceil(D / 4), CB = ceil(D / 8); 5 x 3 at D = 18): RB + CB shared loads per
-// RB * CB FMAs instead of 2 per FMA; edge lanes clamp their loads and skip their stores.
-template <int D, bool TA = false, bool TB = false>
+template <int NW>
+__device__ __forceinline__ void bsync() {
+    if constexpr (NW == 1) __syncwarp();
+    else __syncthreads();
+}
+
+// Out = op(A) op(B) (+ Cadd) by the series' NT threads, shared operands (Out aliases neither A nor
+// B).  D * D > NT: the threads form an (NT / 8) x 8 grid and each holds a register tile of RB
+// contiguous rows x CB columns strided by 8 (RB = ceil(D / (NT / 8)), CB = ceil(D / 8); 2 x 3 at
+// D = 18, NW = 4): RB + CB shared loads per RB * CB FMAs instead of 2 per FMA; edge threads clamp
+// their loads and skip their stores.
+template <int D, int NW, bool TA = false, bool TB = false>
 __device__ __forceinline__ void bmm(double (*Out)[LD(D)], const double (*A)[LD(D)], const double (*B)[LD(D)],
-                                    const double (*Cadd)[LD(D)], int lane) {
-    if constexpr (D * D <= 32) {
+                                    const double (*Cadd)[LD(D)], int tid) {
+    constexpr int NT = 32 * NW;
+    if constexpr (D * D <= NT) {
         BT_EACH(e, D * D) {
             const int i = e / D, j = e - (e / D) * D;
             double s = Cadd ? Cadd[i][j] : 0.0;
@@ -48,8 +57,8 @@ __device__ __forceinline__ void bmm(double (*Out)[LD(D)], const double (*A)[LD(D
             Out[i][j] = s;
         }
     } else {
-        constexpr int PC = 8, RB = (D + 3) / 4, CB = (D + PC - 1) / PC;
-        const int i0 = (lane / PC) * RB, pc = lane % PC;
+        constexpr int PC = 8, PR = NT / PC, RB = (D + PR - 1) / PR, CB = (D + PC - 1) / PC;
+        const int i0 = (tid / PC) * RB, pc = tid % PC;
         int ri[RB], cj[CB];
 #pragma unroll
         for (int r = 0; r < RB; ++r) ri[r] = min(i0 + r, D - 1);
@@ -79,10 +88,50 @@ __device__ __forceinline__ void bmm(double (*Out)[LD(D)], const double (*A)[LD(D
                 if (i0 + r < D && pc + c * PC < D) Out[i0 + r][pc + c * PC] = acc[r][c];
     }
 }
+
+// X = S^-1 R for SPD S (Gauss-Jordan without pivoting, one row per lane, pivot rows by shuffles):
+// every warp eliminates S, warp w carries the right-hand-side columns c = w (mod NW).
+template <int D, int NW>
+__device__ __forceinline__ bool bgj_solve(const double (*S)[LD(D)], const double (*R)[LD(D)], double (*X)[LD(D)],
+                                          int tid) {
+    static_assert(D <= 32, "one row per lane");
+    constexpr int CW = (D + NW - 1) / NW;
+    const int lane = tid & 31, w = tid >> 5;
+    const int r = lane < D ? lane : D - 1;
+    double a[D], b[CW];
+#pragma unroll
+    for (int j = 0; j < D; ++j) a[j] = S[r][j];
+#pragma unroll
+    for (int c = 0; c < CW; ++c) b[c] = (w + NW * c < D) ? R[r][w + NW * c] : 0.0;
+    bool ok = true;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        const double piv = __shfl_sync(0xffffffffu, a[j], j);
+        ok = ok && (piv > 0.0);
+        const double ip = 1.0 / piv;
+        const double f = (lane == j) ? 0.0 : a[j] * ip;
+#pragma unroll
+        for (int k = j + 1; k < D; ++k) {
+            const double pk = __shfl_sync(0xffffffffu, a[k], j);
+            a[k] = (lane == j) ? a[k] * ip : fma(-f, pk, a[k]);
+        }
+#pragma unroll
+        for (int c = 0; c < CW; ++c) {
+            const double pk = __shfl_sync(0xffffffffu, b[c], j);
+            b[c] = (lane == j) ? b[c] * ip : fma(-f, pk, b[c]);
+        }
+    }
+    if (lane < D) {
+#pragma unroll
+        for (int c = 0; c < CW; ++c)
+            if (w + NW * c < D) X[lane][w + NW * c] = b[c];
+    }
+    return ok;
+}
 template <int D>
-__device__ __forceinline__ double bdot(const double* a, const double* b, int lane) {
-    double s = 0.0;
-    BT_EACH(i, D) s = fma(a[i], b[i], s);
+__device__ __forceinline__ double bdot(const double* a, const double* b, int lane) {   // in every warp
+    static_assert(D <= 32, "one element per lane");
+    const double s = lane < D ? a[lane] * b[lane] : 0.0;
     return wsum(s);
 }
 
@@ -259,7 +308,6 @@ struct BSmem {
         double P[D][LD(D)], FP[D][LD(D)], Pm[D][LD(D)], T[D][LD(D)], C[D][LD(D)], Cm[D][LD(D)], Z[D][LD(D)],
             Cs[D][LD(D)];
         double x[D], xm[D], HP[D], K[D], b[D], bm[D], CK[D], KT[D], Mb[D], dm[D];
-        double W2[D][2 * D + 1];
     } w[1];
 };
 
@@ -273,30 +321,32 @@ __device__ __forceinline__ int b_kind(const BParamsT& q, int64_t k, int64_t s0, 
 }
 
 // Kalman filter over one series (warp-cooperative), storing the filtered moments; returns its NLL.
-template <int D>
+template <int D, int NW>
 __device__ double b_filter(const BParamsT& q, typename BSmem<D>::PerWarp& W, const double* H, double r, int64_t s0,
-                           int64_t s1, int lane) {
+                           int64_t s1, int tid) {
+    constexpr int NT = 32 * NW;
+    const int lane = tid & 31;
     double quad = 0.0, logs = 0.0;
     int nobs = 0;
     BT_EACH(i, D) W.x[i] = 0.0;
     BT_EACH(e, D * D) W.P[e / D][e % D] = 0.0;
-    __syncwarp();
+    bsync<NW>();
     for (int64_t k = s0; k < s1; ++k) {
         const double tk = __ldg(q.t + k);
         const bool obs = __ldg(q.mask + k) != 0;
         const double yk = obs ? __ldg(q.y + k) : 0.0;
         const int kind = b_kind(q, k, s0, tk);
-        if (lane == 0 && (kind == 2 || !isfinite(tk) || (obs && !isfinite(yk))))
+        if (tid == 0 && (kind == 2 || !isfinite(tk) || (obs && !isfinite(yk))))
             raise_error(q.err, k, kind == 2 ? kErrUnsupported : kErrInput);
         if (kind == 0) {
-            bmm<D>(W.FP, W.F, W.P, nullptr, lane);
+            bmm<D, NW>(W.FP, W.F, W.P, nullptr, tid);
             BT_EACH(i, D) {
                 double s = 0.0;
                 for (int j = 0; j < D; ++j) s = fma(W.F[i][j], W.x[j], s);
                 W.xm[i] = s;
             }
-            __syncwarp();
-            bmm<D, false, true>(W.Pm, W.FP, W.F, W.Q, lane);
+            bsync<NW>();
+            bmm<D, NW, false, true>(W.Pm, W.FP, W.F, W.Q, tid);
         } else {
             BT_EACH(e, D * D) {
                 const int i = e / D, j = e - (e / D) * D;
@@ -304,16 +354,16 @@ __device__ double b_filter(const BParamsT& q, typename BSmem<D>::PerWarp& W, con
             }
             BT_EACH(i, D) W.xm[i] = (kind == 1) ? W.x[i] : 0.0;
         }
-        __syncwarp();
+        bsync<NW>();
         BT_EACH(i, D) {
             double s = 0.0;
             for (int j = 0; j < D; ++j) s = fma(W.Pm[i][j], H[j], s);
             W.HP[i] = s;
         }
-        __syncwarp();
+        bsync<NW>();
         const double S = bdot<D>(H, W.HP, lane) + r;
         const double hx = bdot<D>(H, W.xm, lane);
-        if (lane == 0 && obs && !(S > 0.0 && S < INFINITY)) raise_error(q.err, k, kErrNumeric);
+        if (tid == 0 && obs && !(S > 0.0 && S < INFINITY)) raise_error(q.err, k, kErrNumeric);
         const double iS = obs ? 1.0 / S : 0.0;
         const double v = obs ? (yk - hx) : 0.0;
         BT_EACH(e, D * D) {
@@ -326,44 +376,46 @@ __device__ double b_filter(const BParamsT& q, typename BSmem<D>::PerWarp& W, con
             logs += log(S);
             ++nobs;
         }
-        __syncwarp();
+        bsync<NW>();
         double* o = q.xs + k * CNW(D);
         BT_EACH(i, D) o[i] = W.x[i];
         BT_EACH(e, D * D) {
             const int i = e / D, j = e - (e / D) * D;
             if (j >= i) o[D + si(D, i, j)] = W.P[i][j];
         }
-        __syncwarp();
+        bsync<NW>();
     }
     return nobs ? 0.5 * (quad + logs + nobs * 1.8378770664093453) : 0.0;
 }
 
-template <int D>
-__device__ void b_load_model(const double* rec, typename BSmem<D>::PerWarp& W, int lane) {
+template <int D, int NW>
+__device__ void b_load_model(const double* rec, typename BSmem<D>::PerWarp& W, int tid) {
+    constexpr int NT = 32 * NW;
     BT_EACH(e, D * D) {
         const int i = e / D, j = e - (e / D) * D;
         W.F[i][j] = rec[e];
         W.Q[i][j] = rec[D * D + e];
         W.Pinf[i][j] = rec[2 * D * D + e];
     }
-    __syncwarp();
+    bsync<NW>();
 }
 
 // posterior: filter, then the RTS smoother from the series' terminal element; mean / var of f
-template <int D>
-__global__ void __launch_bounds__(32) kb_posterior(const BParamsT q, const double* __restrict__ Hg) {
+template <int D, int NW>
+__global__ void __launch_bounds__(32 * NW) kb_posterior(const BParamsT q, const double* __restrict__ Hg) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     BSmem<D>& sh = *reinterpret_cast<BSmem<D>*>(smem_raw);
     auto& W = sh.w[0];
-    const int lane = threadIdx.x, b = blockIdx.x;
+    constexpr int NT = 32 * NW;
+    const int tid = threadIdx.x, lane = tid & 31, b = blockIdx.x;
     const int64_t s0 = __ldg(q.off + b), s1 = __ldg(q.off + b + 1);
     const double* rec = q.recs + static_cast<int64_t>(b) * BREC(D, q.npar);
     const double r = rec[(3 + 3 * (q.npar - 1)) * D * D];
     __shared__ double H[D];
     BT_EACH(i, D) H[i] = Hg[i];
-    b_load_model<D>(rec, W, lane);
-    const double nl = b_filter<D>(q, W, H, r, s0, s1, lane);
-    if (lane == 0) q.nll[b] = nl;
+    b_load_model<D, NW>(rec, W, tid);
+    const double nl = b_filter<D, NW>(q, W, H, r, s0, s1, tid);
+    if (tid == 0) q.nll[b] = nl;
     // RTS (supplement PAPER.md:422-430): (m^s, P^s) in (x, P) from the terminal (= filtered) state
     bool bad = false;
     for (int64_t k = s1 - 1; k >= s0; --k) {
@@ -375,16 +427,16 @@ __global__ void __launch_bounds__(32) kb_posterior(const BParamsT q, const doubl
             const int kind = b_kind(q, k + 1, s0, __ldg(q.t + k + 1));   // transition out of k
             BT_EACH(i, D) W.dm[i] = src[i];         // filtered x_k
             BT_EACH(e, D * D) W.T[e / D][e % D] = src[D + si(D, e / D, e % D)];
-            __syncwarp();
+            bsync<NW>();
             if (kind == 0) {
-                bmm<D>(W.FP, W.F, W.T, nullptr, lane);                      // F P_k
+                bmm<D, NW>(W.FP, W.F, W.T, nullptr, tid);                      // F P_k
                 BT_EACH(i, D) {
                     double s = 0.0;
                     for (int j = 0; j < D; ++j) s = fma(W.F[i][j], W.dm[j], s);
                     W.xm[i] = s;
                 }
-                __syncwarp();
-                bmm<D, false, true>(W.Pm, W.FP, W.F, W.Q, lane);            // P^-
+                bsync<NW>();
+                bmm<D, NW, false, true>(W.Pm, W.FP, W.F, W.Q, tid);            // P^-
             } else {
                 BT_EACH(e, D * D) {
                     W.FP[e / D][e % D] = W.T[e / D][e % D];
@@ -392,27 +444,27 @@ __global__ void __launch_bounds__(32) kb_posterior(const BParamsT q, const doubl
                 }
                 BT_EACH(i, D) W.xm[i] = W.dm[i];
             }
-            __syncwarp();
-            bad = !wgj_solve<D>(W.Pm, W.FP, W.C, lane) || bad;             // X = (P^-)^-1 F P (gain = X^T)
+            bsync<NW>();
+            bad = !bgj_solve<D, NW>(W.Pm, W.FP, W.C, tid) || bad;             // X = (P^-)^-1 F P (gain = X^T)
             BT_EACH(i, D) W.K[i] = W.x[i] - W.xm[i];    // m^s_{k+1} - x^-
             BT_EACH(e, D * D) W.Cm[e / D][e % D] = W.P[e / D][e % D] - W.Pm[e / D][e % D];
-            __syncwarp();
+            bsync<NW>();
             BT_EACH(i, D) {
                 double s = W.dm[i];
                 for (int j = 0; j < D; ++j) s = fma(W.C[j][i], W.K[j], s);
                 W.xm[i] = s;
             }
-            bmm<D>(W.Z, W.Cm, W.C, nullptr, lane);                           // (P^s - P^-) X
-            __syncwarp();
-            bmm<D, true, false>(W.FP, W.C, W.Z, W.T, lane);                  // P + X^T (...) X
-            __syncwarp();
+            bmm<D, NW>(W.Z, W.Cm, W.C, nullptr, tid);                           // (P^s - P^-) X
+            bsync<NW>();
+            bmm<D, NW, true, false>(W.FP, W.C, W.Z, W.T, tid);                  // P + X^T (...) X
+            bsync<NW>();
             BT_EACH(e, D * D) {
                 const int i = e / D, j = e - (e / D) * D;
                 W.P[i][j] = 0.5 * (W.FP[i][j] + W.FP[j][i]);
             }
             BT_EACH(i, D) W.x[i] = W.xm[i];
         }
-        __syncwarp();
+        bsync<NW>();
         double mo = 0.0, vo = 0.0;
         BT_EACH(i, D) {
             double s = 0.0;
@@ -422,30 +474,31 @@ __global__ void __launch_bounds__(32) kb_posterior(const BParamsT q, const doubl
         }
         mo = wsum(mo);
         vo = wsum(vo);
-        if (lane == 0) {
+        if (tid == 0) {
             if (q.mean) q.mean[k] = mo;
             if (q.var) q.var[k] = vo;
         }
-        __syncwarp();
+        bsync<NW>();
     }
-    if (bad && lane == 0) raise_error(q.err, s0, kErrNumeric);
+    if (bad && tid == 0) raise_error(q.err, s0, kErrNumeric);
 }
 
 // NLL + gradient: filter, then the reverse-mode adjoint of the filter from the series end (b = C = 0)
 // accumulating Z, Cs, gr, C0 and contracting them with the series' own dF, dQ, dP_inf.
-template <int D>
-__global__ void __launch_bounds__(32) kb_nll_grad(const BParamsT q, const double* __restrict__ Hg) {
+template <int D, int NW>
+__global__ void __launch_bounds__(32 * NW) kb_nll_grad(const BParamsT q, const double* __restrict__ Hg) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     BSmem<D>& sh = *reinterpret_cast<BSmem<D>*>(smem_raw);
     auto& W = sh.w[0];
-    const int lane = threadIdx.x, b = blockIdx.x;
+    constexpr int NT = 32 * NW;
+    const int tid = threadIdx.x, lane = tid & 31, b = blockIdx.x;
     const int64_t s0 = __ldg(q.off + b), s1 = __ldg(q.off + b + 1);
     const double* rec = q.recs + static_cast<int64_t>(b) * BREC(D, q.npar);
     const double r = rec[(3 + 3 * (q.npar - 1)) * D * D];
     __shared__ double H[D];
     BT_EACH(i, D) H[i] = Hg[i];
-    b_load_model<D>(rec, W, lane);
-    const double nl = b_filter<D>(q, W, H, r, s0, s1, lane);
+    b_load_model<D, NW>(rec, W, tid);
+    const double nl = b_filter<D, NW>(q, W, H, r, s0, s1, tid);
     BT_EACH(e, D * D) {
         W.C[e / D][e % D] = 0.0;
         W.Z[e / D][e % D] = 0.0;
@@ -453,7 +506,7 @@ __global__ void __launch_bounds__(32) kb_nll_grad(const BParamsT q, const double
         W.Pm[e / D][e % D] = 0.0;   // C0 stays here after the loop (series start)
     }
     BT_EACH(i, D) W.b[i] = 0.0;
-    __syncwarp();
+    bsync<NW>();
     double gr = 0.0;
     bool have_c0 = false;
     for (int64_t k = s1 - 1; k >= s0; --k) {
@@ -465,40 +518,40 @@ __global__ void __launch_bounds__(32) kb_nll_grad(const BParamsT q, const double
             const double* src = q.xs + (k - 1) * CNW(D);
             BT_EACH(i, D) W.dm[i] = src[i];
             BT_EACH(e, D * D) W.T[e / D][e % D] = src[D + si(D, e / D, e % D)];
-            __syncwarp();
+            bsync<NW>();
         }
         if (kind == 0) {
-            bmm<D>(W.FP, W.F, W.T, nullptr, lane);
+            bmm<D, NW>(W.FP, W.F, W.T, nullptr, tid);
             BT_EACH(i, D) {
                 double s = 0.0;
                 for (int j = 0; j < D; ++j) s = fma(W.F[i][j], W.dm[j], s);
                 W.xm[i] = s;
             }
-            __syncwarp();
-            bmm<D, false, true>(W.P, W.FP, W.F, W.Q, lane);                 // P^- (in P)
+            bsync<NW>();
+            bmm<D, NW, false, true>(W.P, W.FP, W.F, W.Q, tid);                 // P^- (in P)
         } else {
             BT_EACH(e, D * D) W.P[e / D][e % D] = (kind == 1) ? W.T[e / D][e % D] : W.Pinf[e / D][e % D];
             BT_EACH(i, D) W.xm[i] = (kind == 1) ? W.dm[i] : 0.0;
         }
-        __syncwarp();
+        bsync<NW>();
         if (obs) {
             BT_EACH(i, D) {
                 double s = 0.0;
                 for (int j = 0; j < D; ++j) s = fma(W.P[i][j], H[j], s);
                 W.HP[i] = s;
             }
-            __syncwarp();
+            bsync<NW>();
             const double S = bdot<D>(H, W.HP, lane) + r;
             const double v = yk - bdot<D>(H, W.xm, lane);
             const double iS = 1.0 / S, vs = v * iS, c1 = 0.5 * (iS - vs * vs);
             BT_EACH(i, D) W.K[i] = W.HP[i] * iS;
-            __syncwarp();
+            bsync<NW>();
             BT_EACH(i, D) {
                 double s = 0.0;
                 for (int j = 0; j < D; ++j) s = fma(W.C[i][j], W.K[j], s);
                 W.CK[i] = s;
             }
-            __syncwarp();
+            bsync<NW>();
             const double bK = bdot<D>(W.b, W.K, lane), KCK = bdot<D>(W.K, W.CK, lane);
             gr += c1 - bK * vs + KCK;
             BT_EACH(e, D * D) {
@@ -507,13 +560,13 @@ __global__ void __launch_bounds__(32) kb_nll_grad(const BParamsT q, const double
                 W.Cm[i][j] = fma(-W.CK[i], H[j], W.C[i][j]);   // C (I - K h^T)
             }
             BT_EACH(i, D) W.Mb[i] = fma(-H[i], bK, W.b[i]);
-            __syncwarp();
+            bsync<NW>();
             BT_EACH(j, D) {
                 double s = 0.0;
                 for (int i = 0; i < D; ++i) s = fma(W.K[i], W.Cm[i][j], s);
                 W.KT[j] = s;
             }
-            __syncwarp();
+            bsync<NW>();
             BT_EACH(e, D * D) {
                 const int i = e / D, j = e - (e / D) * D;
                 const double hi = H[i], hj = H[j];
@@ -524,30 +577,30 @@ __global__ void __launch_bounds__(32) kb_nll_grad(const BParamsT q, const double
             BT_EACH(e, D * D) W.Cm[e / D][e % D] = W.C[e / D][e % D];
             BT_EACH(i, D) W.bm[i] = W.b[i];
         }
-        __syncwarp();
+        bsync<NW>();
         if (kind == 3) {
             BT_EACH(e, D * D) W.Pm[e / D][e % D] = W.Cm[e / D][e % D];   // C0
             have_c0 = true;
             break;
         }
         if (kind == 0) {
-            bmm<D>(W.T, W.Cm, W.FP, nullptr, lane);                          // C^- F P_{k-1}
-            __syncwarp();
+            bmm<D, NW>(W.T, W.Cm, W.FP, nullptr, tid);                          // C^- F P_{k-1}
+            bsync<NW>();
             BT_EACH(e, D * D) {
                 const int i = e / D, j = e - (e / D) * D;
                 W.Z[i][j] += fma(W.bm[i], W.dm[j], 2.0 * W.T[i][j]);
                 W.Cs[i][j] += W.Cm[i][j];
             }
-            __syncwarp();
-            bmm<D>(W.T, W.Cm, W.F, nullptr, lane);                           // C^- F
+            bsync<NW>();
+            bmm<D, NW>(W.T, W.Cm, W.F, nullptr, tid);                           // C^- F
             BT_EACH(i, D) {
                 double s = 0.0;
                 for (int j = 0; j < D; ++j) s = fma(W.F[j][i], W.bm[j], s);
                 W.b[i] = s;
             }
-            __syncwarp();
-            bmm<D, true, false>(W.FP, W.F, W.T, nullptr, lane);              // F^T C^- F
-            __syncwarp();
+            bsync<NW>();
+            bmm<D, NW, true, false>(W.FP, W.F, W.T, nullptr, tid);              // F^T C^- F
+            bsync<NW>();
             BT_EACH(e, D * D) {
                 const int i = e / D, j = e - (e / D) * D;
                 W.C[i][j] = 0.5 * (W.FP[i][j] + W.FP[j][i]);
@@ -556,10 +609,12 @@ __global__ void __launch_bounds__(32) kb_nll_grad(const BParamsT q, const double
             BT_EACH(e, D * D) W.C[e / D][e % D] = W.Cm[e / D][e % D];
             BT_EACH(i, D) W.b[i] = W.bm[i];
         }
-        __syncwarp();
+        bsync<NW>();
     }
     (void)have_c0;
-    // contraction with the series' derivative records (fixed order: deterministic)
+    // contraction with the series' derivative records (fixed order: deterministic): warp partials,
+    // then the NW warp sums in order
+    __shared__ double red[NW];
     const double* der = rec + 3 * D * D;
     for (int pp = 0; pp < q.npar; ++pp) {
         double acc = 0.0;
@@ -569,13 +624,21 @@ __global__ void __launch_bounds__(32) kb_nll_grad(const BParamsT q, const double
                 const int i = e / D, j = e - (e / D) * D;
                 acc += dd[e] * W.Z[i][j] + dd[D * D + e] * W.Cs[i][j] + dd[2 * D * D + e] * W.Pm[i][j];
             }
-        } else if (lane == 0) {
+        } else if (tid == 0) {
             acc = r * gr;
         }
         acc = wsum(acc);
-        if (lane == 0) q.grad[static_cast<int64_t>(b) * q.npar + pp] = acc;
+        if (lane == 0) red[tid >> 5] = acc;
+        bsync<NW>();
+        if (tid == 0) {
+            double g = 0.0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) g += red[w];
+            q.grad[static_cast<int64_t>(b) * q.npar + pp] = g;
+        }
+        bsync<NW>();
     }
-    if (lane == 0) q.nll[b] = nl;
+    if (tid == 0) q.nll[b] = nl;
 }
 
 }  // namespace wide

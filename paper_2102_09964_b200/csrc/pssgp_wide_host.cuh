@@ -728,16 +728,31 @@ pssgp_status wide_batched_theta(pssgp_model* m, int nseg, const int64_t* off, co
     q.t = t; q.y = y; q.mask = mask; q.xs = xs;
     q.mean = mean; q.var = var; q.nll = nll; q.grad = grad; q.err = m->d_err;
     static_assert(sizeof(BSmem<D>) <= 48 * 1024, "per-series shared state");
-    if (grad) {
-        ProfScope ps(m, S_GRAD, s);
-        kb_nll_grad<D><<<nseg, 32, sizeof(BSmem<D>), s>>>(q, Hd);
-        LAUNCH_CHECK(m, "kb_nll_grad");
-    } else {
-        ProfScope ps(m, S_K3, s);
-        kb_posterior<D><<<nseg, 32, sizeof(BSmem<D>), s>>>(q, Hd);
-        LAUNCH_CHECK(m, "kb_posterior");
+    // warps per series: one by default.  2 or 4 (PSSGP_BT_NW, A/B) split the series' matrix products
+    // over more threads but pay a CTA barrier per phase: measured on 1,024 CO2 J = 3 series (d = 18),
+    // NLL + gradient 46.0 / 56.7 / 78.0 ms and posterior 70.3 / 86.7 / 140.9 ms for 1 / 2 / 4 warps
+    // (profiles/r2/bt_nw_ab.txt)
+    int nw = 1;
+    if (const char* e = getenv("PSSGP_BT_NW")) {
+        const int v = atoi(e);
+        if (v == 1 || v == 2 || v == 4) nw = v;
     }
-    return PSSGP_OK;
+    auto launch = [&](auto nwc) {
+        constexpr int NW = decltype(nwc)::value;
+        if (grad) {
+            ProfScope ps(m, S_GRAD, s);
+            kb_nll_grad<D, NW><<<nseg, 32 * NW, sizeof(BSmem<D>), s>>>(q, Hd);
+            LAUNCH_CHECK(m, "kb_nll_grad");
+        } else {
+            ProfScope ps(m, S_K3, s);
+            kb_posterior<D, NW><<<nseg, 32 * NW, sizeof(BSmem<D>), s>>>(q, Hd);
+            LAUNCH_CHECK(m, "kb_posterior");
+        }
+        return PSSGP_OK;
+    };
+    if (nw == 4) return launch(std::integral_constant<int, 4>{});
+    if (nw == 2) return launch(std::integral_constant<int, 2>{});
+    return launch(std::integral_constant<int, 1>{});
 }
 
 }  // namespace widehost
