@@ -793,6 +793,161 @@ __global__ void __launch_bounds__(32 * kWWarps) kw_discretize(const double* __re
     (void)err;
 }
 
+// Per-step (F, Q) of a model whose G and W are block diagonal with B x B blocks (pssgp_model::fblock:
+// sums of components, periodic harmonics as 2 x 2 rotations, quasi-periodic products in blocks of 2m):
+// expm and the Lyapunov integral act block by block, so one LANE per (step, block) runs
+// kw_discretize's algorithm on its B x B block in registers — the Taylor series of degree 12 of
+// F_tau = e^{G tau} and of Q_tau = sum_k Z_k (Z_1 = tau W, Z_{k+1} = sym(G tau Z_k) 2 / (k + 1)) at
+// tau = dt / 2^s with ||G_b tau||_1 <= 1/8 for the block's own norm, then s doublings
+// Q <- F Q F^T + Q, F <- F F.  A warp takes SPW <= 32 / NB consecutive steps at a time, assembles
+// their records (zeros off the blocks) in shared memory and writes them out as one contiguous,
+// coalesced run.  O(B^3) per block instead of O(D^3) warp products per step.
+constexpr int kBlkWarps = 2;
+template <int D, int B>
+struct BlkDisc {
+    static constexpr int NB = (D + B - 1) / B;   // the last block may be partial (d = 14 in blocks of 4)
+    // steps per warp: one lane per block, staged records within 40 KB of static shared memory per CTA
+    static constexpr int SPW0 = 32 / NB, SPWM = 40960 / (kBlkWarps * FQW(D) * 8);
+    static constexpr int SPW = SPW0 < SPWM ? SPW0 : SPWM;
+};
+template <int D, int B>
+__global__ void __launch_bounds__(32 * kBlkWarps) kw_discretize_blk(const double* __restrict__ t, int64_t nfq,
+                                                                    int64_t k0, const double* __restrict__ model,
+                                                                    double* fq) {
+    constexpr int NB = BlkDisc<D, B>::NB, SPW = BlkDisc<D, B>::SPW;
+    static_assert(NB <= 32, "one lane per block");
+    __shared__ double rec[kBlkWarps][SPW * FQW(D)];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    double* sr = rec[wid];
+    const int js = lane / NB, bb = lane - js * NB, o0 = bb * B, bs = min(B, D - o0);
+    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kBlkWarps;
+    for (int64_t kw = (static_cast<int64_t>(blockIdx.x) * kBlkWarps + wid) * SPW; kw < nfq; kw += nwarps * SPW) {
+        const int nst = static_cast<int>(min(static_cast<int64_t>(SPW), nfq - kw));
+        for (int e = lane; e < SPW * FQW(D); e += 32) sr[e] = 0.0;
+        __syncwarp();
+        const int64_t k = kw + js;
+        bool act = js < nst && k0 + k != 0;
+        const double dt = act ? __ldg(t + k) - __ldg(t + k - 1) : 0.0;
+        act = act && dt != 0.0 && dt == dt;
+        if (act) {
+            double G[B][B], Wm[B][B];
+            double nrm = 0.0;
+#pragma unroll
+            for (int j = 0; j < B; ++j) {
+                double c = 0.0;
+#pragma unroll
+                for (int i = 0; i < B; ++i) {
+                    const bool in = i < bs && j < bs;   // padding of a partial block: G = W = 0
+                    G[i][j] = in ? __ldg(model + 3 * D * D + D + 2 + (o0 + i) * D + o0 + j) : 0.0;
+                    Wm[i][j] = in ? __ldg(model + 4 * D * D + D + 2 + (o0 + i) * D + o0 + j) : 0.0;
+                    c += fabs(G[i][j]);
+                }
+                nrm = fmax(nrm, c);
+            }
+            nrm *= fabs(dt);
+            int s = 0;
+            if (nrm > 0.125) frexp(nrm / 0.125, &s);
+            const double tau = ldexp(dt, -s);
+            double A[B][B], F[B][B], Z[B][B], Q[B][B];
+#pragma unroll
+            for (int i = 0; i < B; ++i)
+#pragma unroll
+                for (int j = 0; j < B; ++j) {
+                    A[i][j] = G[i][j] * tau;
+                    F[i][j] = (i == j) ? 1.0 : 0.0;
+                    Z[i][j] = Wm[i][j] * tau;
+                    Q[i][j] = Z[i][j];
+                }
+            // F_tau by Horner: F = I + A/m (I + A/(m-1) (...)), m = 12
+#pragma unroll
+            for (int kk = 12; kk >= 1; --kk) {
+                double T[B][B];
+                const double ik = 1.0 / kk;
+#pragma unroll
+                for (int i = 0; i < B; ++i)
+#pragma unroll
+                    for (int j = 0; j < B; ++j) {
+                        double a = 0.0;
+#pragma unroll
+                        for (int l = 0; l < B; ++l) a = fma(A[i][l], F[l][j], a);
+                        T[i][j] = fma(a, ik, (i == j) ? 1.0 : 0.0);
+                    }
+#pragma unroll
+                for (int i = 0; i < B; ++i)
+#pragma unroll
+                    for (int j = 0; j < B; ++j) F[i][j] = T[i][j];
+            }
+            // Q_tau = sum_{k=1}^{12} Z_k
+#pragma unroll
+            for (int kk = 1; kk < 12; ++kk) {
+                double Y[B][B];
+#pragma unroll
+                for (int i = 0; i < B; ++i)
+#pragma unroll
+                    for (int j = 0; j < B; ++j) {
+                        double a = 0.0;
+#pragma unroll
+                        for (int l = 0; l < B; ++l) a = fma(A[i][l], Z[l][j], a);
+                        Y[i][j] = a;
+                    }
+                const double ik = 1.0 / (kk + 1);
+#pragma unroll
+                for (int i = 0; i < B; ++i)
+#pragma unroll
+                    for (int j = 0; j < B; ++j) {
+                        Z[i][j] = (Y[i][j] + Y[j][i]) * ik;
+                        Q[i][j] += Z[i][j];
+                    }
+            }
+            for (int q = 0; q < s; ++q) {   // doublings
+                double FQ[B][B], Fn[B][B];
+#pragma unroll
+                for (int i = 0; i < B; ++i)
+#pragma unroll
+                    for (int j = 0; j < B; ++j) {
+                        double a = 0.0, f = 0.0;
+#pragma unroll
+                        for (int l = 0; l < B; ++l) {
+                            a = fma(F[i][l], Q[l][j], a);
+                            f = fma(F[i][l], F[l][j], f);
+                        }
+                        FQ[i][j] = a;
+                        Fn[i][j] = f;
+                    }
+#pragma unroll
+                for (int i = 0; i < B; ++i)
+#pragma unroll
+                    for (int j = 0; j < B; ++j) {
+                        double a = Q[i][j];
+#pragma unroll
+                        for (int l = 0; l < B; ++l) a = fma(FQ[i][l], F[j][l], a);
+                        Z[i][j] = a;
+                    }
+#pragma unroll
+                for (int i = 0; i < B; ++i)
+#pragma unroll
+                    for (int j = 0; j < B; ++j) {
+                        Q[i][j] = Z[i][j];
+                        F[i][j] = Fn[i][j];
+                    }
+            }
+            double* o = sr + js * FQW(D);
+#pragma unroll
+            for (int i = 0; i < B; ++i)
+#pragma unroll
+                for (int jb = 0; jb < B; ++jb)
+                    if (i < bs && jb < bs) {
+                        o[(o0 + i) * LD(D) + o0 + jb] = F[i][jb];
+                        o[(D + o0 + i) * LD(D) + o0 + jb] = 0.5 * (Q[i][jb] + Q[jb][i]);
+                    }
+        }
+        __syncwarp();
+        double* g = fq + kw * FQW(D);
+        for (int e = lane; e < nst * FQW(D); e += 32) g[e] = sr[e];
+        __syncwarp();
+    }
+}
+
 // ------------------------------------------------------------------ K1w: fold
 template <int D>
 struct K1Smem {

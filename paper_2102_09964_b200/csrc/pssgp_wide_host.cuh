@@ -86,10 +86,12 @@ void wide_set_smem_attrs(int device) {
 // rescans also with per-step (F, Q) staged in shared memory, bit 3: one-wave plan for them on the
 // table path, bit 4: Kalman rescan, bit 5: the one-wave plan also on the per-step (F, Q) path, bit 6:
 // lane-per-row discretisation, bit 7: quarter-parallel rescans (all four 8-lane groups of a warp
-// busy; needs bit 0, whose fold stores the quarter prefix aggregates)); env PSSGP_WIDE_LPR overrides
-// the default 255 for A/B runs (0 = the shared-memory kernels)
+// busy; needs bit 0, whose fold stores the quarter prefix aggregates), bit 8: see below, bit 9:
+// per-block discretisation of block-diagonal models (kw_discretize_blk) where the lane-per-row one
+// does not run); env PSSGP_WIDE_LPR overrides the default 1023 for A/B runs (0 = the shared-memory
+// kernels)
 inline int wide_lpr_mask() {
-    static const int v = [] { const char* e = getenv("PSSGP_WIDE_LPR"); return e && *e ? atoi(e) : 511; }();
+    static const int v = [] { const char* e = getenv("PSSGP_WIDE_LPR"); return e && *e ? atoi(e) : 1023; }();
     return v;
 }
 inline bool wide_quarter_rescans() { return (wide_lpr_mask() & 129) == 129; }
@@ -289,6 +291,27 @@ pssgp_status wide_prepare(pssgp_model* m, pssgp::wide::WParams& p, cudaStream_t 
             return PSSGP_OK;
         }
     }
+    if (m->fblock > 0 && m->fblock < D && (wide_lpr_mask() & 512)) {   // block-diagonal G, W: per-block threads
+        bool done = false;
+        with_fblock<D>(m, [&](auto fbc) {
+            constexpr int FB = decltype(fbc)::value;
+            if constexpr (FB < D) {
+                constexpr int SPW = BlkDisc<D, FB>::SPW;
+                int occ = 0;
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kw_discretize_blk<D, FB>, 32 * kBlkWarps, 0);
+                const int64_t want = (nfq + SPW * kBlkWarps - 1) / (SPW * kBlkWarps);
+                const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(m->sm_count) * std::max(1, occ))));
+                ProfScope ps(m, S_DISC, s);
+                kw_discretize_blk<D, FB><<<grid, 32 * kBlkWarps, 0, s>>>(p.t, nfq, p.k0, m->d_model, m->fq);
+                done = true;
+            }
+        });
+        if (done) {
+            LAUNCH_CHECK(m, "kw_discretize_blk");
+            p.fq = m->fq;
+            return PSSGP_OK;
+        }
+    }
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kw_discretize<D>, 32 * kWWarps, sizeof(KDSmem<D>));
     const int64_t want = (nfq + kWWarps - 1) / kWWarps;
@@ -324,7 +347,17 @@ pssgp_status wide_debug_discretize(pssgp_model* m, double dt, double* F, double*
     if constexpr (D <= kGL) {
         if (lpr) kw_discretize_lpr<D><<<1, 32 * kWWarps>>>(tbuf, 2, 0, m->d_model, fq);
     }
-    if (!lpr) {
+    bool blk = false;
+    if (!lpr && m->fblock > 0 && m->fblock < D && (wide_lpr_mask() & 512)) {
+        with_fblock<D>(m, [&](auto fbc) {
+            constexpr int FB = decltype(fbc)::value;
+            if constexpr (FB < D) {
+                kw_discretize_blk<D, FB><<<1, 32 * kBlkWarps>>>(tbuf, 2, 0, m->d_model, fq);
+                blk = true;
+            }
+        });
+    }
+    if (!lpr && !blk) {
         cudaFuncSetAttribute(kw_discretize<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(KDSmem<D>));
         kw_discretize<D><<<1, 32 * kWWarps, sizeof(KDSmem<D>)>>>(tbuf, 2, 0, m->d_model, fq, m->d_err);
     }

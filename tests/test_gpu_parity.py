@@ -372,6 +372,11 @@ PADE_MODELS = {
     "per3+m32": [synth.Component("periodic", 1.5, 1.0, period=0.7, order=3), synth.Component("matern32", 1.0, 2.0)],
     "per6+m32": [synth.Component("periodic", 4.0, 1.0, period=1.0, order=6), synth.Component("matern32", 10.0, 20.0)],
     "quasi1": [synth.Component("quasiperiodic", 2.0, 1.0, period=0.5, order=1, mat_lengthscale=3.0, mat_nu2=3)],
+    # d = 12 in 4 x 4 blocks (the per-block discretisation kw_discretize_blk<12, 4>)
+    "quasi2": [synth.Component("quasiperiodic", 2.0, 1.0, period=0.5, order=2, mat_lengthscale=3.0, mat_nu2=3)],
+    # d = 14 in blocks of 4, the last one partial (rows 12, 13: the Matern-3/2 trend)
+    "quasi2+m32": [synth.Component("quasiperiodic", 2.0, 1.0, period=0.5, order=2, mat_lengthscale=3.0, mat_nu2=3),
+                   synth.Component("matern32", 1.0, 2.0)],
 }
 
 
@@ -483,10 +488,12 @@ def _mp_van_loan(G, W, dt, dps=40):
     return np.array(F.tolist(), dtype=float), np.array(Q.tolist(), dtype=float)
 
 
-@pytest.mark.parametrize("name", ["rbf6", "quasi1", "per3+m32"])
+@pytest.mark.parametrize("name", ["rbf6", "quasi1", "per3+m32", "per6+m32", "quasi2", "quasi2+m32"])
 @pytest.mark.parametrize("dt", [1e-9, 2.4e-7, 1.22e-4, 1e-3, 0.02, 0.3, 2.5])
 def test_kw_discretize_vs_high_precision(cuda_device, name, dt):
-    """kw_discretize (d > 3, uniform_dt = 0) for one step against a 40-digit Van Loan: F and Q
+    """The per-step discretisation the wide path launches for the model (d > 3, uniform_dt = 0:
+    lane-per-row for d <= 8, per-block for block-diagonal d > 8 — per3+m32, per6+m32 in 2 x 2
+    blocks, quasi2 in 4 x 4 — else kw_discretize) for one step against a 40-digit Van Loan: F and Q
     to ~1e-13 of their scale and, for small steps, every entry of Q above the rounding level of
     the matrix to relative accuracy (the regime where the stationary shortcut cancels)."""
     m = P.Model(PADE_MODELS[name], 0.05)
