@@ -3055,6 +3055,338 @@ __global__ void __launch_bounds__(32 * WPC, lpr_minb(G)) kw_smoother_apply_q(con
 }
 
 
+// ------------------------------------------------------------------ K5m: RTS rescan in adjoint form
+// The modified Bryson-Frazier form of the RTS recursion (an exact rewriting of supplement
+// PAPER.md:422-430): with the filtered (x_k, P_k), the smoothed moments are
+//   m^s_k = x_k - P_k lh_k,   P^s_k = P_k - P_k Lh_k P_k,
+// where (lh, Lh) run backwards without any solve:
+//   lt_k = (I - K_k h)^T lh_k - h^T v_k / S_k,   Lt_k = (I - K_k h)^T Lh_k (I - K_k h) + h^T h / S_k
+//   (a missing y_k: lt = lh, Lt = Lh),   lh_{k-1} = F_k^T lt_k,   Lh_{k-1} = F_k^T Lt_k F_k,
+// K_k, S_k, v_k being the Kalman gain, innovation variance and innovation of step k, recomputed
+// from the filtered record of k - 1 (only P^- h^T is needed, never P^-).  Only f = h x is output, so
+//   mean_k = h x_k - (P_k h^T) . lh_k,   var_k = h P_k h^T - (P_k h^T)^T Lh_k (P_k h^T)
+// and a step costs O(d^2) (O(d^2 FB) for the F products of a block-diagonal F) instead of the RTS
+// step's Cholesky factor, two triangular solves and congruence (O(d^3)).  The group's carry (the
+// smoothed moments at its end, from the chain scan and the quarter / half smoother aggregates as in
+// kw_smoother_apply_q) enters once:  lh = X^T (x^- - m^s), Lh = X^T (P^- - P^s) X with
+// X = (P^-)^-1 F of the transition out of the group's last step (one cooperative Cholesky factor and
+// two triangular solves per group).  Lane r of a G-lane group holds row r of Lh and lh_r.
+template <int D, bool STREAM, int G = kGL, int WPC = kWWarps>
+struct K5MSmem {
+    static constexpr int NP = 32 / G;
+    SModel<D> m;
+    double I[D][LD(D)], Z[D][LD(D)];
+    struct PerWarp {
+        union {
+            struct {                               // carry phase
+                double cm[NP][D];
+                double cP[NP][D][LD(D)];
+                SS<D> a;
+                SSufScratch<D> s;
+            } c;
+            struct Grp {                           // step phase, one slot per group
+                double xst[3][CNW(D)];             // filtered records k, k - 1 and k - 2 (cp.async ring)
+                double Pm[D][LD(D)], Ps[D][LD(D)], X[D][LD(D)];   // boundary: P^- (then L), P^- - P^s, X
+                double dm[D];
+                double fqs[2][FQS(D, STREAM)];     // STREAM: (F_k, Q_k) of the transition into k
+            } g[NP];
+        } u;
+    } w[WPC];
+};
+
+template <int D, bool STREAM, int G = kGL, int WPC = kWWarps, int FB = D>
+__global__ void __launch_bounds__(32 * WPC, lpr_minb(G)) kw_smoother_mbf_q(const WParams p) {
+    static_assert(D <= G, "one row per lane of a G-lane group");
+    constexpr int NP = 32 / G;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    K5MSmem<D, STREAM, G, WPC>& sh = *reinterpret_cast<K5MSmem<D, STREAM, G, WPC>*>(smem_raw);
+    load_model<D>(sh.m, p.model);
+    for (int e = threadIdx.x; e < D * D; e += blockDim.x) {
+        const int i = e / D, j = e - (e / D) * D;
+        sh.I[i][j] = (i == j) ? 1.0 : 0.0;
+        sh.Z[i][j] = 0.0;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int c = blockIdx.x * WPC + wid;
+    if (c >= p.nch) return;
+    auto& W = sh.w[wid];
+    const SModel<D>& M = sh.m;
+    const int64_t kb = static_cast<int64_t>(c) * p.K;
+    const int64_t ke = min(kb + p.K, p.n);
+    // ---- carries (as kw_smoother_apply_q): smoothed moments after each group's last step
+    auto& c3P = W.u.c.cP[NP - 1];
+    for (int e = lane; e < D * D; e += 32) c3P[e / D][e % D] = 0.0;
+    for (int i = lane; i < D; i += 32) W.u.c.cm[NP - 1][i] = 0.0;
+    __syncwarp();
+    for (int g = p.world - 1; g > p.rank && p.in_smooth; --g) {
+        gload<D>(W.u.c.a, p.in_smooth + static_cast<int64_t>(g) * (SNW(D) + 1), lane);
+        wapply_suffix<D>(W.u.c.a, W.u.c.cm[NP - 1], c3P, W.u.c.s, lane);
+    }
+    if (c + 1 < p.nch) {
+        gload<D>(W.u.c.a, p.sagg + static_cast<int64_t>(c + 1) * SNW(D), lane);
+        wapply_suffix<D>(W.u.c.a, W.u.c.cm[NP - 1], c3P, W.u.c.s, lane);
+    }
+    for (int q = NP - 2; q >= 0; --q) {
+        for (int e = lane; e < D * D; e += 32) W.u.c.cP[q][e / D][e % D] = W.u.c.cP[q + 1][e / D][e % D];
+        for (int i = lane; i < D; i += 32) W.u.c.cm[q][i] = W.u.c.cm[q + 1][i];
+        __syncwarp();
+        gload<D>(W.u.c.a, p.sqagg + (static_cast<int64_t>(c) * (NP - 1) + q) * SNW(D), lane);
+        wapply_suffix<D>(W.u.c.a, W.u.c.cm[q], W.u.c.cP[q], W.u.c.s, lane);
+    }
+    const int q = lane / G, r0 = lane % G, gb = q * G;
+    const unsigned gm = group_mask(G, gb);
+    const bool act = (D == G) || r0 < D;
+    const double af = act ? 1.0 : 0.0;
+    const int r = act ? r0 : 0;
+    int64_t qb, qe;
+    quarter_bounds(kb, ke, p.K, q, qb, qe, NP);
+    double Psr[D], msr = W.u.c.cm[q][r];
+#pragma unroll
+    for (int j = 0; j < D; ++j) Psr[j] = W.u.c.cP[q][r][j];
+    const double hr = act ? M.H[r] : 0.0;
+    __syncwarp();                                   // W.u (carry scratch) is reused below
+    auto& Gs = W.u.g[q];
+    const double* xp = p.xp;                        // record of local step k at xp + k CNW
+    auto gsum = [&](double v) {
+#pragma unroll
+        for (int off = G / 2; off > 0; off >>= 1) v += __shfl_xor_sync(gm, v, off);
+        return v;
+    };
+    auto stage_rec = [&](int64_t k) {
+        double* dst = Gs.xst[static_cast<int>(k % 3)];
+        const double* src = xp + k * CNW(D);
+        for (int i = r0; i < CNW(D); i += G) cp_async8(&dst[i], src + i, 8);
+    };
+    auto stage_fq = [&](int64_t k) {                // (F_k, Q_k): the transition into local step k
+        if (STREAM) {
+            const double* fsrc = p.fq + k * FQW(D);
+            for (int i = r0; i < FQW(D); i += G) cp_async8(&Gs.fqs[static_cast<int>(k & 1)][i], fsrc + i, 8);
+        }
+    };
+    // (F, Q) of the transition into local step k (shared pointers)
+    auto fq_into = [&](int64_t k, const double*& Fp, const double*& Qp) {
+        const int kind = wdisc_kind(__ldg(p.t + k) - __ldg(p.t + k - 1), M.udt, STREAM);
+        if (kind == 0) {
+            if (STREAM) { Fp = &Gs.fqs[static_cast<int>(k & 1)][0]; Qp = Fp + D * LD(D); }
+            else { Fp = &M.F[0][0]; Qp = &M.Q[0][0]; }
+        } else {
+            Fp = &sh.I[0][0]; Qp = &sh.Z[0][0];
+        }
+    };
+    double lh = 0.0, Lh[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) Lh[j] = 0.0;
+    bool bad = false;
+    if (qe > qb) {
+        const bool carry = p.k0 + qe - 1 != p.nglob - 1;   // else the group ends the series: lh = Lh = 0
+        stage_rec(qe - 1);
+        if (qe - 1 > qb) stage_rec(qe - 2);
+        if (carry) stage_fq(qe);
+        if (qe - 1 > qb) stage_fq(qe - 1);
+        cp_async_commit();
+        cp_async_wait<0>();
+        __syncwarp(gm);
+        if (carry) {
+            // ---- boundary: lh = X^T (x^- - m^s), Lh = X^T (P^- - P^s) X, X = (P^-)^-1 F (transition qe)
+            const double* rec = Gs.xst[static_cast<int>((qe - 1) % 3)];
+            const double* Fp;
+            const double* Qp;
+            fq_into(qe, Fp, Qp);
+            double FPr[D], xm = 0.0;                // row r of F P_{qe-1}, (F x)_r
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                double s2 = 0.0;
+#pragma unroll
+                for (int t = 0; t < FB; ++t) {
+                    const int qq = fblo(r, FB) + t;
+                    if (qq < D) s2 = fma(Fp[r * LD(D) + qq], rec[D + si(D, qq, j)], s2);
+                }
+                FPr[j] = s2;
+            }
+#pragma unroll
+            for (int t = 0; t < FB; ++t) {
+                const int qq = fblo(r, FB) + t;
+                if (qq < D) xm = fma(Fp[r * LD(D) + qq], rec[qq], xm);
+            }
+            if (act) {
+#pragma unroll
+                for (int j = 0; j < D; ++j) {
+                    double s2 = Qp[r * LD(D) + j];
+#pragma unroll
+                    for (int qq = fblo(j, FB); qq < fbhi(j, FB, D); ++qq) s2 = fma(FPr[qq], Fp[j * LD(D) + qq], s2);
+                    Gs.Pm[r][j] = s2;
+                    Gs.Ps[r][j] = s2 - Psr[j];       // P^- - P^s
+                }
+                Gs.dm[r] = xm - msr;                 // x^- - m^s
+#pragma unroll
+                for (int i = 0; i < D; ++i) Gs.X[i][r] = Fp[i * LD(D) + r];   // right-hand side: column r of F
+            }
+            __syncwarp(gm);
+            // cooperative Cholesky of P^- (lane r builds row r of L; 1 / L_rr on the diagonal), then
+            // the two triangular solves in place on column r of X
+            double Lr[D];
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                double sv = Gs.Pm[r][j];
+#pragma unroll
+                for (int qq = 0; qq < j; ++qq) sv = fma(-Lr[qq], __shfl_sync(gm, Lr[qq], j, G), sv);
+                const double sj = __shfl_sync(gm, sv, j, G);
+                bad = bad || !(sj > 0.0);
+                const double lij = rsqrt(sj);
+                Lr[j] = (r == j) ? lij : sv * lij;
+            }
+            __syncwarp(gm);
+            auto& Lm = Gs.Pm;
+            if (act) {
+#pragma unroll
+                for (int qq = 0; qq < D; ++qq) Lm[r][qq] = Lr[qq];
+            }
+            __syncwarp(gm);
+            if (act) {
+#pragma unroll 4
+                for (int i = 0; i < D; ++i) {
+                    double z = Gs.X[i][r];
+                    for (int qq = 0; qq < i; ++qq) z = fma(-Lm[i][qq], Gs.X[qq][r], z);
+                    Gs.X[i][r] = z * Lm[i][i];
+                }
+#pragma unroll 4
+                for (int i = D - 1; i >= 0; --i) {
+                    double z = Gs.X[i][r];
+                    for (int qq = i + 1; qq < D; ++qq) z = fma(-Lm[qq][i], Gs.X[qq][r], z);
+                    Gs.X[i][r] = z * Lm[i][i];
+                }
+            }
+            __syncwarp(gm);
+            double Xr[D], V[D];
+#pragma unroll
+            for (int i = 0; i < D; ++i) Xr[i] = Gs.X[i][r];
+#pragma unroll
+            for (int i = 0; i < D; ++i) lh = fma(Xr[i], Gs.dm[i], lh);
+#pragma unroll
+            for (int bb = 0; bb < D; ++bb) {
+                double v = 0.0;
+#pragma unroll
+                for (int a = 0; a < D; ++a) v = fma(Xr[a], Gs.Ps[a][bb], v);
+                V[bb] = v;
+            }
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                double s2 = 0.0;
+#pragma unroll
+                for (int bb = 0; bb < D; ++bb) s2 = fma(V[bb], Gs.X[bb][j], s2);
+                Lh[j] = s2;
+            }
+            __syncwarp(gm);
+        }
+    }
+    double hrow[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) hrow[j] = M.H[j];
+    for (int64_t k = qe - 1; k >= qb; --k) {
+        // prefetch the record of k - 2 and (F, Q) into k - 1 (the next step's update)
+        if (k - 2 >= qb) stage_rec(k - 2);
+        if (k - 1 > qb) stage_fq(k - 1);
+        cp_async_commit();
+        const double* rec = Gs.xst[static_cast<int>(k % 3)];
+        // ---- output: mean = h x - (P h^T) . lh, var = h P h^T - (P h^T)^T Lh (P h^T)
+        double Ph = 0.0, hx = 0.0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            Ph = fma(rec[D + si(D, r, j)], hrow[j], Ph);
+            hx = fma(hrow[j], rec[j], hx);
+        }
+        double LPh = 0.0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) LPh = fma(Lh[j], __shfl_sync(gm, Ph, j, G), LPh);
+        const double s_quad = gsum(af * Ph * LPh), s_lph = gsum(af * Ph * lh), s_hph = gsum(hr * Ph);
+        if (r0 == 0) {
+            if (p.mean) p.mean[k] = hx - s_lph;
+            if (p.var) p.var[k] = s_hph - s_quad;
+        }
+        if (k > qb) {
+            // ---- update at k, then back through F_k to k - 1
+            const double* prv = Gs.xst[static_cast<int>((k - 1) % 3)];
+            const double* Fp;
+            const double* Qp;
+            fq_into(k, Fp, Qp);
+            const bool obs = __ldg(p.mask + k) != 0;
+            const double yk = obs ? __ldg(p.y + k) : 0.0;
+            // g = F^T h^T (all of it), P_{k-1} g (row r), P^- h^T = F (P g) + Q h^T (row r), x^- = F x
+            double gv[D];
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+                double s2 = 0.0;
+#pragma unroll
+                for (int qq = fblo(i, FB); qq < fbhi(i, FB, D); ++qq) s2 = fma(Fp[qq * LD(D) + i], hrow[qq], s2);
+                gv[i] = s2;
+            }
+            double Pg = 0.0;
+#pragma unroll
+            for (int j = 0; j < D; ++j) Pg = fma(prv[D + si(D, r, j)], gv[j], Pg);
+            double PmH = 0.0, xm = 0.0;
+#pragma unroll
+            for (int t = 0; t < FB; ++t) {
+                const int qq = fblo(r, FB) + t;
+                const double pgq = __shfl_sync(gm, Pg, qq < D ? qq : 0, G);
+                if (qq < D) {
+                    const double f = Fp[r * LD(D) + qq];
+                    PmH = fma(f, pgq, PmH);
+                    PmH = fma(Qp[r * LD(D) + qq], hrow[qq], PmH);
+                    xm = fma(f, prv[qq], xm);
+                }
+            }
+            double lt = lh, Lt[D];
+#pragma unroll
+            for (int j = 0; j < D; ++j) Lt[j] = Lh[j];
+            const double S = gsum(hr * PmH) + M.r, hxm = gsum(hr * xm);
+            if (obs) {
+                bad = bad || !(S > 0.0);
+                const double iS = 1.0 / S, vs = (yk - hxm) * iS;
+                const double Kr = PmH * iS;
+                double w = 0.0;
+#pragma unroll
+                for (int j = 0; j < D; ++j) w = fma(Lh[j], __shfl_sync(gm, Kr, j, G), w);
+                const double cK = gsum(af * Kr * w), Kl = gsum(af * Kr * lh);
+#pragma unroll
+                for (int j = 0; j < D; ++j) {
+                    const double wj = __shfl_sync(gm, w, j, G);
+                    Lt[j] = fma(-hr, wj, fma(-w, hrow[j], fma((cK + iS) * hr, hrow[j], Lh[j])));
+                }
+                lt = fma(-hr, Kl + vs, lh);
+            }
+            // lh <- F^T lt, Lh <- F^T Lt F (row r: the rows of Lt F in r's block, by shuffles)
+            double LF[D];
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                double s2 = 0.0;
+#pragma unroll
+                for (int qq = fblo(j, FB); qq < fbhi(j, FB, D); ++qq) s2 = fma(Lt[qq], Fp[qq * LD(D) + j], s2);
+                LF[j] = s2;
+            }
+            double lhn = 0.0, Lhn[D];
+#pragma unroll
+            for (int j = 0; j < D; ++j) Lhn[j] = 0.0;
+#pragma unroll
+            for (int t = 0; t < FB; ++t) {
+                const int qq = fblo(r, FB) + t;
+                const int src = qq < D ? qq : 0;
+                const double fqr = (qq < D) ? Fp[qq * LD(D) + r] : 0.0;
+                lhn = fma(fqr, __shfl_sync(gm, lt, src, G), lhn);
+#pragma unroll
+                for (int j = 0; j < D; ++j) Lhn[j] = fma(fqr, __shfl_sync(gm, LF[j], src, G), Lhn[j]);
+            }
+            lh = lhn;
+#pragma unroll
+            for (int j = 0; j < D; ++j) Lh[j] = Lhn[j];
+        }
+        cp_async_wait<0>();
+        __syncwarp(gm);
+    }
+    if (bad && r0 == 0) raise_error(p.err, p.k0 + qb, kErrNumeric);
+}
+
+
 // ================================================================== NLL gradient of any model (uniform dt)
 // Reverse mode over the Kalman recursion (supplement PAPER.md:304-315; the paper differentiates the
 // parallel filter by AD).  With the adjoint (b_k, C_k) = d NLL_{>k} / d (x_k, P_k) of

@@ -53,6 +53,8 @@ void wide_set_smem_attrs(int device) {
         cudaFuncSetAttribute(kw_filter_apply_q<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K3QSmem<D, true>));
         cudaFuncSetAttribute(kw_smoother_apply_q<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K5QSmem<D, false>));
         cudaFuncSetAttribute(kw_smoother_apply_q<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K5QSmem<D, true>));
+        cudaFuncSetAttribute(kw_smoother_mbf_q<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K5MSmem<D, false>));
+        cudaFuncSetAttribute(kw_smoother_mbf_q<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K5MSmem<D, true>));
     } else if constexpr (wide_halves<D>()) {
         auto set = [](auto fbc) {
             constexpr int G = kHalfG, W = kHalfWPC, FB = decltype(fbc)::value;
@@ -62,6 +64,8 @@ void wide_set_smem_attrs(int device) {
             cudaFuncSetAttribute(kw_filter_apply_q<D, true, G, W, FB>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K3QSmem<D, true, G, W>));
             cudaFuncSetAttribute(kw_smoother_apply_q<D, false, G, W, FB>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K5QSmem<D, false, G, W>));
             cudaFuncSetAttribute(kw_smoother_apply_q<D, true, G, W, FB>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K5QSmem<D, true, G, W>));
+            cudaFuncSetAttribute(kw_smoother_mbf_q<D, false, G, W, FB>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K5MSmem<D, false, G, W>));
+            cudaFuncSetAttribute(kw_smoother_mbf_q<D, true, G, W, FB>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K5MSmem<D, true, G, W>));
         };
         set(std::integral_constant<int, D>{});
         cudaFuncSetAttribute(kw_combine_halves<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(ScanSmemF<D>));
@@ -88,16 +92,22 @@ void wide_set_smem_attrs(int device) {
 // lane-per-row discretisation, bit 7: quarter-parallel rescans (all four 8-lane groups of a warp
 // busy; needs bit 0, whose fold stores the quarter prefix aggregates), bit 8: see below, bit 9:
 // per-block discretisation of block-diagonal models (kw_discretize_blk) where the lane-per-row one
-// does not run); env PSSGP_WIDE_LPR overrides the default 1023 for A/B runs (0 = the shared-memory
-// kernels)
+// does not run), bits 10, 11: see below); env PSSGP_WIDE_LPR overrides the default 2047 for A/B runs
+// (0 = the shared-memory kernels)
 inline int wide_lpr_mask() {
-    static const int v = [] { const char* e = getenv("PSSGP_WIDE_LPR"); return e && *e ? atoi(e) : 1023; }();
+    static const int v = [] { const char* e = getenv("PSSGP_WIDE_LPR"); return e && *e ? atoi(e) : 2047; }();
     return v;
 }
 inline bool wide_quarter_rescans() { return (wide_lpr_mask() & 129) == 129; }
 // bit 8: 9 <= D <= 16 on the lane-per-row fold and half-chain rescans (16-lane groups, two half
 // chains per warp, 2 warps per CTA: kHalfG / kHalfWPC)
 inline bool wide_half_rescans() { return (wide_lpr_mask() & 256) != 0; }
+// bit 10: the half-chain RTS rescan (9 <= D <= 16) in adjoint (modified Bryson-Frazier) form,
+// kw_smoother_mbf_q: O(d^2 FB) per step instead of a Cholesky solve per step (C4 K5w 75.3 -> 17.7
+// ms); bit 11: the same for the quarter rescans of D <= 8 (dense F there: F^T Lt F costs 2 d^3,
+// measured 1.42 -> 1.57 ms at C3, so off by default)
+inline bool wide_mbf() { return (wide_lpr_mask() & 1024) != 0; }
+inline bool wide_mbf_quarters() { return (wide_lpr_mask() & 3072) == 3072; }
 
 struct WPlan {
     int64_t K = 0;
@@ -122,11 +132,13 @@ WPlan make_wplan(pssgp_model* m, int64_t n) {
                 if (m->mode == kPade) {
                     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l1, kw_filter_fold_lpr<D, true>, 32 * kWWarps, sizeof(K1LSmem<D, true>));
                     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l3, kw_filter_apply_q<D, true>, 32 * kWWarps, sizeof(K3QSmem<D, true>));
-                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l5, kw_smoother_apply_q<D, true>, 32 * kWWarps, sizeof(K5QSmem<D, true>));
+                    if (wide_mbf_quarters()) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l5, kw_smoother_mbf_q<D, true>, 32 * kWWarps, sizeof(K5MSmem<D, true>));
+                    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l5, kw_smoother_apply_q<D, true>, 32 * kWWarps, sizeof(K5QSmem<D, true>));
                 } else {
                     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l1, kw_filter_fold_lpr<D, false>, 32 * kWWarps, sizeof(K1LSmem<D, false>));
                     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l3, kw_filter_apply_q<D, false>, 32 * kWWarps, sizeof(K3QSmem<D, false>));
-                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l5, kw_smoother_apply_q<D, false>, 32 * kWWarps, sizeof(K5QSmem<D, false>));
+                    if (wide_mbf_quarters()) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l5, kw_smoother_mbf_q<D, false>, 32 * kWWarps, sizeof(K5MSmem<D, false>));
+                    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l5, kw_smoother_apply_q<D, false>, 32 * kWWarps, sizeof(K5QSmem<D, false>));
                 }
             } else if (m->mode == kPade) {   // per-step (F, Q) variants (their staging buffers cost shared memory)
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l1, kw_filter_fold_lpr<D, true>, 32 * kWWarps, sizeof(K1LSmem<D, true>));
@@ -155,11 +167,13 @@ WPlan make_wplan(pssgp_model* m, int64_t n) {
                     if (m->mode == kPade) {
                         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l1, kw_filter_fold_lpr<D, true, G, W, FB>, 32 * W, sizeof(K1LSmem<D, true, G, W>));
                         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l3, kw_filter_apply_q<D, true, G, W, FB>, 32 * W, sizeof(K3QSmem<D, true, G, W>));
-                        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l5, kw_smoother_apply_q<D, true, G, W, FB>, 32 * W, sizeof(K5QSmem<D, true, G, W>));
+                        if (wide_mbf()) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l5, kw_smoother_mbf_q<D, true, G, W, FB>, 32 * W, sizeof(K5MSmem<D, true, G, W>));
+                        else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l5, kw_smoother_apply_q<D, true, G, W, FB>, 32 * W, sizeof(K5QSmem<D, true, G, W>));
                     } else {
                         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l1, kw_filter_fold_lpr<D, false, G, W, FB>, 32 * W, sizeof(K1LSmem<D, false, G, W>));
                         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l3, kw_filter_apply_q<D, false, G, W, FB>, 32 * W, sizeof(K3QSmem<D, false, G, W>));
-                        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l5, kw_smoother_apply_q<D, false, G, W, FB>, 32 * W, sizeof(K5QSmem<D, false, G, W>));
+                        if (wide_mbf()) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l5, kw_smoother_mbf_q<D, false, G, W, FB>, 32 * W, sizeof(K5MSmem<D, false, G, W>));
+                        else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l5, kw_smoother_apply_q<D, false, G, W, FB>, 32 * W, sizeof(K5QSmem<D, false, G, W>));
                     }
                 });
                 m->wchains = std::max(1, std::min(l1, std::min(l3, l5))) * W;
@@ -482,8 +496,13 @@ pssgp_status wide_sapply(pssgp_model* m, pssgp::wide::WParams& p, int nb, cudaSt
     ProfScope ps(m, S_K5, s);
     if constexpr (D <= kGL) {
         if (p.sqagg) {  // quarter-parallel RTS rescan (kw_filter_apply_q stored the quarter smoother aggregates)
-            if (p.fq) kw_smoother_apply_q<D, true><<<nb, 32 * kWWarps, sizeof(K5QSmem<D, true>), s>>>(p);
-            else kw_smoother_apply_q<D, false><<<nb, 32 * kWWarps, sizeof(K5QSmem<D, false>), s>>>(p);
+            if (wide_mbf_quarters()) {
+                if (p.fq) kw_smoother_mbf_q<D, true><<<nb, 32 * kWWarps, sizeof(K5MSmem<D, true>), s>>>(p);
+                else kw_smoother_mbf_q<D, false><<<nb, 32 * kWWarps, sizeof(K5MSmem<D, false>), s>>>(p);
+            } else {
+                if (p.fq) kw_smoother_apply_q<D, true><<<nb, 32 * kWWarps, sizeof(K5QSmem<D, true>), s>>>(p);
+                else kw_smoother_apply_q<D, false><<<nb, 32 * kWWarps, sizeof(K5QSmem<D, false>), s>>>(p);
+            }
             LAUNCH_CHECK(m, "kw_smoother_apply_q");
             return PSSGP_OK;
         }
@@ -501,8 +520,13 @@ pssgp_status wide_sapply(pssgp_model* m, pssgp::wide::WParams& p, int nb, cudaSt
             const int nbh = (p.nch + W - 1) / W;
             with_fblock<D>(m, [&](auto fbc) {
                 constexpr int FB = decltype(fbc)::value;
-                if (p.fq) kw_smoother_apply_q<D, true, G, W, FB><<<nbh, 32 * W, sizeof(K5QSmem<D, true, G, W>), s>>>(p);
-                else kw_smoother_apply_q<D, false, G, W, FB><<<nbh, 32 * W, sizeof(K5QSmem<D, false, G, W>), s>>>(p);
+                if (wide_mbf()) {
+                    if (p.fq) kw_smoother_mbf_q<D, true, G, W, FB><<<nbh, 32 * W, sizeof(K5MSmem<D, true, G, W>), s>>>(p);
+                    else kw_smoother_mbf_q<D, false, G, W, FB><<<nbh, 32 * W, sizeof(K5MSmem<D, false, G, W>), s>>>(p);
+                } else {
+                    if (p.fq) kw_smoother_apply_q<D, true, G, W, FB><<<nbh, 32 * W, sizeof(K5QSmem<D, true, G, W>), s>>>(p);
+                    else kw_smoother_apply_q<D, false, G, W, FB><<<nbh, 32 * W, sizeof(K5QSmem<D, false, G, W>), s>>>(p);
+                }
             });
             LAUNCH_CHECK(m, "kw_smoother_apply_q (16-lane)");
             return PSSGP_OK;
