@@ -496,7 +496,7 @@ pssgp_status wide_sapply(pssgp_model* m, pssgp::wide::WParams& p, int nb, cudaSt
     ProfScope ps(m, S_K5, s);
     if constexpr (D <= kGL) {
         if (p.sqagg) {  // quarter-parallel RTS rescan (kw_filter_apply_q stored the quarter smoother aggregates)
-            if (wide_mbf_quarters()) {
+            if (wide_mbf_quarters() && p.y && p.mask) {   // the adjoint form needs y (the shard phase has none)
                 if (p.fq) kw_smoother_mbf_q<D, true><<<nb, 32 * kWWarps, sizeof(K5MSmem<D, true>), s>>>(p);
                 else kw_smoother_mbf_q<D, false><<<nb, 32 * kWWarps, sizeof(K5MSmem<D, false>), s>>>(p);
             } else {
@@ -520,7 +520,7 @@ pssgp_status wide_sapply(pssgp_model* m, pssgp::wide::WParams& p, int nb, cudaSt
             const int nbh = (p.nch + W - 1) / W;
             with_fblock<D>(m, [&](auto fbc) {
                 constexpr int FB = decltype(fbc)::value;
-                if (wide_mbf()) {
+                if (wide_mbf() && p.y && p.mask) {   // the adjoint form needs y (the shard phase has none)
                     if (p.fq) kw_smoother_mbf_q<D, true, G, W, FB><<<nbh, 32 * W, sizeof(K5MSmem<D, true, G, W>), s>>>(p);
                     else kw_smoother_mbf_q<D, false, G, W, FB><<<nbh, 32 * W, sizeof(K5MSmem<D, false, G, W>), s>>>(p);
                 } else {
