@@ -3086,13 +3086,47 @@ struct K5MSmem {
             } c;
             struct Grp {                           // step phase, one slot per group
                 double xst[3][CNW(D)];             // filtered records k, k - 1 and k - 2 (cp.async ring)
-                double Pm[D][LD(D)], Ps[D][LD(D)], X[D][LD(D)];   // boundary: P^- (then L), P^- - P^s, X
+                // boundary: P^- (then L), P^- - P^s, X; in the step loop Pm holds the rows of Lt F
+                // (stride D) and Ps the exchanged vectors (P h^T, P_{k-1} g, K, Lh K) - 16-byte rows
+                alignas(16) double Pm[D][LD(D)];
+                alignas(16) double Ps[D][LD(D)];
+                double X[D][LD(D)];
                 double dm[D];
                 double fqs[2][FQS(D, STREAM)];     // STREAM: (F_k, Q_k) of the transition into k
             } g[NP];
         } u;
     } w[WPC];
 };
+
+// sum_j a(j) b(j) with four interleaved accumulators (a dependent FMA chain of D / 4)
+template <int N, typename FA, typename FB2>
+__device__ __forceinline__ double dot4(FA&& a, FB2&& b) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; j += 4) {
+        s0 = fma(a(j), b(j), s0);
+        if (j + 1 < N) s1 = fma(a(j + 1), b(j + 1), s1);
+        if (j + 2 < N) s2 = fma(a(j + 2), b(j + 2), s2);
+        if (j + 3 < N) s3 = fma(a(j + 3), b(j + 3), s3);
+    }
+    return (s0 + s1) + (s2 + s3);
+}
+
+// n doubles of a 16-byte aligned shared row into registers (128-bit loads when n is even)
+template <int N>
+__device__ __forceinline__ void ld_row(const double* src, double (&dst)[N]) {
+    if constexpr (N % 2 == 0) {
+#pragma unroll
+        for (int i = 0; i < N / 2; ++i) {
+            const double2 v = reinterpret_cast<const double2*>(src)[i];
+            dst[2 * i] = v.x;
+            dst[2 * i + 1] = v.y;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < N; ++i) dst[i] = src[i];
+    }
+}
 
 template <int D, bool STREAM, int G = kGL, int WPC = kWWarps, int FB = D>
 __global__ void __launch_bounds__(32 * WPC, lpr_minb(G)) kw_smoother_mbf_q(const WParams p) {
@@ -3290,15 +3324,19 @@ __global__ void __launch_bounds__(32 * WPC, lpr_minb(G)) kw_smoother_mbf_q(const
         cp_async_commit();
         const double* rec = Gs.xst[static_cast<int>(k % 3)];
         // ---- output: mean = h x - (P h^T) . lh, var = h P h^T - (P h^T)^T Lh (P h^T)
-        double Ph = 0.0, hx = 0.0;
-#pragma unroll
-        for (int j = 0; j < D; ++j) {
-            Ph = fma(rec[D + si(D, r, j)], hrow[j], Ph);
-            hx = fma(hrow[j], rec[j], hx);
-        }
-        double LPh = 0.0;
-#pragma unroll
-        for (int j = 0; j < D; ++j) LPh = fma(Lh[j], __shfl_sync(gm, Ph, j, G), LPh);
+        const double Ph = dot4<D>([&](int j) { return rec[D + si(D, r, j)]; }, [&](int j) { return hrow[j]; });
+        const double hx = dot4<D>([&](int j) { return hrow[j]; }, [&](int j) { return rec[j]; });
+        // row vectors are exchanged through the group's shared slots (one store, vector loads)
+        double* vPh = &Gs.Ps[0][0];                 // [D]: P_k h^T
+        double* vPg = vPh + 2 * ((D + 1) / 2);      // [D]: P_{k-1} g
+        double* vK = vPg + 2 * ((D + 1) / 2);       // [D]: K_k
+        double* vw = vK + 2 * ((D + 1) / 2);        // [D]: Lh K
+        double (*LFs)[LD(D)] = Gs.Pm;               // rows of Lt F_k (padded stride: conflict-free columns)
+        if (act) vPh[r] = Ph;
+        __syncwarp(gm);
+        double tmp[D];
+        ld_row<D>(vPh, tmp);
+        const double LPh = dot4<D>([&](int j) { return Lh[j]; }, [&](int j) { return tmp[j]; });
         const double s_quad = gsum(af * Ph * LPh), s_lph = gsum(af * Ph * lh), s_hph = gsum(hr * Ph);
         if (r0 == 0) {
             if (p.mean) p.mean[k] = hx - s_lph;
@@ -3321,17 +3359,16 @@ __global__ void __launch_bounds__(32 * WPC, lpr_minb(G)) kw_smoother_mbf_q(const
                 for (int qq = fblo(i, FB); qq < fbhi(i, FB, D); ++qq) s2 = fma(Fp[qq * LD(D) + i], hrow[qq], s2);
                 gv[i] = s2;
             }
-            double Pg = 0.0;
-#pragma unroll
-            for (int j = 0; j < D; ++j) Pg = fma(prv[D + si(D, r, j)], gv[j], Pg);
+            const double Pg = dot4<D>([&](int j) { return prv[D + si(D, r, j)]; }, [&](int j) { return gv[j]; });
+            if (act) vPg[r] = Pg;
+            __syncwarp(gm);
             double PmH = 0.0, xm = 0.0;
 #pragma unroll
             for (int t = 0; t < FB; ++t) {
                 const int qq = fblo(r, FB) + t;
-                const double pgq = __shfl_sync(gm, Pg, qq < D ? qq : 0, G);
                 if (qq < D) {
                     const double f = Fp[r * LD(D) + qq];
-                    PmH = fma(f, pgq, PmH);
+                    PmH = fma(f, vPg[qq], PmH);
                     PmH = fma(Qp[r * LD(D) + qq], hrow[qq], PmH);
                     xm = fma(f, prv[qq], xm);
                 }
@@ -3344,18 +3381,21 @@ __global__ void __launch_bounds__(32 * WPC, lpr_minb(G)) kw_smoother_mbf_q(const
                 bad = bad || !(S > 0.0);
                 const double iS = 1.0 / S, vs = (yk - hxm) * iS;
                 const double Kr = PmH * iS;
-                double w = 0.0;
+                if (act) vK[r] = Kr;
+                __syncwarp(gm);
+                ld_row<D>(vK, tmp);
+                const double w = dot4<D>([&](int j) { return Lh[j]; }, [&](int j) { return tmp[j]; });
+                if (act) vw[r] = w;
+                const double cK = gsum(af * Kr * w), Kl = gsum(af * Kr * lh);   // (the reduction orders the store)
+                __syncwarp(gm);
+                ld_row<D>(vw, tmp);
 #pragma unroll
-                for (int j = 0; j < D; ++j) w = fma(Lh[j], __shfl_sync(gm, Kr, j, G), w);
-                const double cK = gsum(af * Kr * w), Kl = gsum(af * Kr * lh);
-#pragma unroll
-                for (int j = 0; j < D; ++j) {
-                    const double wj = __shfl_sync(gm, w, j, G);
-                    Lt[j] = fma(-hr, wj, fma(-w, hrow[j], fma((cK + iS) * hr, hrow[j], Lh[j])));
-                }
+                for (int j = 0; j < D; ++j)
+                    Lt[j] = fma(-hr, tmp[j], fma(-w, hrow[j], fma((cK + iS) * hr, hrow[j], Lh[j])));
                 lt = fma(-hr, Kl + vs, lh);
             }
-            // lh <- F^T lt, Lh <- F^T Lt F (row r: the rows of Lt F in r's block, by shuffles)
+            // lh <- F^T lt, Lh <- F^T Lt F: row r of Lt F in registers and shared, then the rows of
+            // r's block
             double LF[D];
 #pragma unroll
             for (int j = 0; j < D; ++j) {
@@ -3364,17 +3404,25 @@ __global__ void __launch_bounds__(32 * WPC, lpr_minb(G)) kw_smoother_mbf_q(const
                 for (int qq = fblo(j, FB); qq < fbhi(j, FB, D); ++qq) s2 = fma(Lt[qq], Fp[qq * LD(D) + j], s2);
                 LF[j] = s2;
             }
+            __syncwarp(gm);                         // every lane is done with the previous LFs
+            if (act) {
+#pragma unroll
+                for (int j = 0; j < D; ++j) LFs[r][j] = LF[j];
+                vPh[r] = lt;                        // (vPh is free again: reused for lt)
+            }
+            __syncwarp(gm);
             double lhn = 0.0, Lhn[D];
 #pragma unroll
             for (int j = 0; j < D; ++j) Lhn[j] = 0.0;
 #pragma unroll
             for (int t = 0; t < FB; ++t) {
                 const int qq = fblo(r, FB) + t;
-                const int src = qq < D ? qq : 0;
-                const double fqr = (qq < D) ? Fp[qq * LD(D) + r] : 0.0;
-                lhn = fma(fqr, __shfl_sync(gm, lt, src, G), lhn);
+                if (qq < D) {
+                    const double fqr = Fp[qq * LD(D) + r];
+                    lhn = fma(fqr, vPh[qq], lhn);
 #pragma unroll
-                for (int j = 0; j < D; ++j) Lhn[j] = fma(fqr, __shfl_sync(gm, LF[j], src, G), Lhn[j]);
+                    for (int j = 0; j < D; ++j) Lhn[j] = fma(fqr, LFs[qq][j], Lhn[j]);
+                }
             }
             lh = lhn;
 #pragma unroll
