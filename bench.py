@@ -575,10 +575,10 @@ def main():
         b = alg_bytes(k, d, wide_stream, f32) * n_local
         fl = flops_per_step(k, d, ckey)
         if args.config in ("gradbt", "batchedbt") and k in ("k_grad_fold", "k_filter_apply"):
-            # one warp per series: the algorithmic count of its sequential filter + adjoint (14 d^3 +
-            # 34 d^2) or filter + RTS (15 d^3 + 15 d^2) per step; the SASS count of
-            # the register-tiled kernels includes the padded tile rows / columns
-            fl = 14 * d ** 3 + 34 * d ** 2 if k == "k_grad_fold" else 15 * d ** 3 + 15 * d ** 2
+            # one warp per series: the algorithmic count of its sequential filter + adjoint (10 d^3 +
+            # 38 d^2) or filter + adjoint-form RTS (8 d^3 + 32 d^2) per step; the SASS
+            # count of the register-tiled kernels includes the padded tile rows / columns
+            fl = 10 * d ** 3 + 38 * d ** 2 if k == "k_grad_fold" else 8 * d ** 3 + 32 * d ** 2
         launch_ms = kms / kl
         e = {"ms_per_step": kms / args.steps, "launches_per_step": kl / args.steps, "alg_bytes_per_step": alg_bytes(k, d, wide_stream, f32)}
         if b:

@@ -89,45 +89,6 @@ __device__ __forceinline__ void bmm(double (*Out)[LD(D)], const double (*A)[LD(D
     }
 }
 
-// X = S^-1 R for SPD S (Gauss-Jordan without pivoting, one row per lane, pivot rows by shuffles):
-// every warp eliminates S, warp w carries the right-hand-side columns c = w (mod NW).
-template <int D, int NW>
-__device__ __forceinline__ bool bgj_solve(const double (*S)[LD(D)], const double (*R)[LD(D)], double (*X)[LD(D)],
-                                          int tid) {
-    static_assert(D <= 32, "one row per lane");
-    constexpr int CW = (D + NW - 1) / NW;
-    const int lane = tid & 31, w = tid >> 5;
-    const int r = lane < D ? lane : D - 1;
-    double a[D], b[CW];
-#pragma unroll
-    for (int j = 0; j < D; ++j) a[j] = S[r][j];
-#pragma unroll
-    for (int c = 0; c < CW; ++c) b[c] = (w + NW * c < D) ? R[r][w + NW * c] : 0.0;
-    bool ok = true;
-#pragma unroll
-    for (int j = 0; j < D; ++j) {
-        const double piv = __shfl_sync(0xffffffffu, a[j], j);
-        ok = ok && (piv > 0.0);
-        const double ip = 1.0 / piv;
-        const double f = (lane == j) ? 0.0 : a[j] * ip;
-#pragma unroll
-        for (int k = j + 1; k < D; ++k) {
-            const double pk = __shfl_sync(0xffffffffu, a[k], j);
-            a[k] = (lane == j) ? a[k] * ip : fma(-f, pk, a[k]);
-        }
-#pragma unroll
-        for (int c = 0; c < CW; ++c) {
-            const double pk = __shfl_sync(0xffffffffu, b[c], j);
-            b[c] = (lane == j) ? b[c] * ip : fma(-f, pk, b[c]);
-        }
-    }
-    if (lane < D) {
-#pragma unroll
-        for (int c = 0; c < CW; ++c)
-            if (w + NW * c < D) X[lane][w + NW * c] = b[c];
-    }
-    return ok;
-}
 template <int D>
 __device__ __forceinline__ double bdot(const double* a, const double* b, int lane) {   // in every warp
     static_assert(D <= 32, "one element per lane");
@@ -416,69 +377,105 @@ __global__ void __launch_bounds__(32 * NW) kb_posterior(const BParamsT q, const 
     b_load_model<D, NW>(rec, W, tid);
     const double nl = b_filter<D, NW>(q, W, H, r, s0, s1, tid);
     if (tid == 0) q.nll[b] = nl;
-    // RTS (supplement PAPER.md:422-430): (m^s, P^s) in (x, P) from the terminal (= filtered) state
+    // RTS smoother (supplement PAPER.md:422-430) in its adjoint (modified Bryson-Frazier) form, as
+    // kw_smoother_mbf_q: m^s_k = x_k - P_k lh_k, P^s_k = P_k - P_k Lh_k P_k with lh (W.b),
+    // Lh (W.C) zero at the series end and, backwards, the rank-one update of step k and F_k^T . F_k;
+    // only mean = h m^s and var = h P^s h^T are formed.
     bool bad = false;
+    BT_EACH(i, D) W.b[i] = 0.0;
+    BT_EACH(e, D * D) W.C[e / D][e % D] = 0.0;
+    bsync<NW>();
     for (int64_t k = s1 - 1; k >= s0; --k) {
         const double* src = q.xs + k * CNW(D);
-        if (k == s1 - 1) {
-            BT_EACH(i, D) W.x[i] = src[i];
-            BT_EACH(e, D * D) W.P[e / D][e % D] = src[D + si(D, e / D, e % D)];
-        } else {
-            const int kind = b_kind(q, k + 1, s0, __ldg(q.t + k + 1));   // transition out of k
-            BT_EACH(i, D) W.dm[i] = src[i];         // filtered x_k
-            BT_EACH(e, D * D) W.T[e / D][e % D] = src[D + si(D, e / D, e % D)];
-            bsync<NW>();
+        BT_EACH(i, D) {                                  // P_k h^T
+            double s = 0.0;
+            for (int j = 0; j < D; ++j) s = fma(src[D + si(D, i, j)], H[j], s);
+            W.HP[i] = s;
+            W.x[i] = src[i];
+        }
+        bsync<NW>();
+        BT_EACH(i, D) {                                  // Lh (P_k h^T)
+            double s = 0.0;
+            for (int j = 0; j < D; ++j) s = fma(W.C[i][j], W.HP[j], s);
+            W.CK[i] = s;
+        }
+        bsync<NW>();
+        const double hx = bdot<D>(H, W.x, lane), lph = bdot<D>(W.HP, W.b, lane);
+        const double hph = bdot<D>(H, W.HP, lane), quad = bdot<D>(W.HP, W.CK, lane);
+        if (tid == 0) {
+            if (q.mean) q.mean[k] = hx - lph;
+            if (q.var) q.var[k] = hph - quad;
+        }
+        if (k > s0) {
+            const int kind = b_kind(q, k, s0, __ldg(q.t + k));   // transition into k: 0 uniform, 1 tie
+            const double* prv = q.xs + (k - 1) * CNW(D);
+            const bool obs = __ldg(q.mask + k) != 0;
+            const double yk = obs ? __ldg(q.y + k) : 0.0;
             if (kind == 0) {
-                bmm<D, NW>(W.FP, W.F, W.T, nullptr, tid);                      // F P_k
-                BT_EACH(i, D) {
+                BT_EACH(i, D) {                          // g = F^T h^T
                     double s = 0.0;
-                    for (int j = 0; j < D; ++j) s = fma(W.F[i][j], W.dm[j], s);
-                    W.xm[i] = s;
+                    for (int j = 0; j < D; ++j) s = fma(W.F[j][i], H[j], s);
+                    W.dm[i] = s;
                 }
                 bsync<NW>();
-                bmm<D, NW, false, true>(W.Pm, W.FP, W.F, W.Q, tid);            // P^-
-            } else {
-                BT_EACH(e, D * D) {
-                    W.FP[e / D][e % D] = W.T[e / D][e % D];
-                    W.Pm[e / D][e % D] = W.T[e / D][e % D];
+                BT_EACH(i, D) {                          // P_{k-1} g
+                    double s = 0.0;
+                    for (int j = 0; j < D; ++j) s = fma(prv[D + si(D, i, j)], W.dm[j], s);
+                    W.bm[i] = s;
                 }
-                BT_EACH(i, D) W.xm[i] = W.dm[i];
+                bsync<NW>();
+                BT_EACH(i, D) {                          // P^- h^T = F (P g) + Q h^T, x^- = F x_{k-1}
+                    double s = 0.0, xm = 0.0;
+                    for (int j = 0; j < D; ++j) {
+                        s = fma(W.F[i][j], W.bm[j], fma(W.Q[i][j], H[j], s));
+                        xm = fma(W.F[i][j], prv[j], xm);
+                    }
+                    W.Mb[i] = s;
+                    W.xm[i] = xm;
+                }
+            } else {                                     // a tie: F = I, Q = 0
+                BT_EACH(i, D) {
+                    double s = 0.0;
+                    for (int j = 0; j < D; ++j) s = fma(prv[D + si(D, i, j)], H[j], s);
+                    W.Mb[i] = s;
+                    W.xm[i] = prv[i];
+                }
             }
             bsync<NW>();
-            bad = !bgj_solve<D, NW>(W.Pm, W.FP, W.C, tid) || bad;             // X = (P^-)^-1 F P (gain = X^T)
-            BT_EACH(i, D) W.K[i] = W.x[i] - W.xm[i];    // m^s_{k+1} - x^-
-            BT_EACH(e, D * D) W.Cm[e / D][e % D] = W.P[e / D][e % D] - W.Pm[e / D][e % D];
-            bsync<NW>();
-            BT_EACH(i, D) {
-                double s = W.dm[i];
-                for (int j = 0; j < D; ++j) s = fma(W.C[j][i], W.K[j], s);
-                W.xm[i] = s;
+            const double S = bdot<D>(H, W.Mb, lane) + r, hxm = bdot<D>(H, W.xm, lane);
+            if (obs) {
+                bad = bad || !(S > 0.0);
+                const double iS = 1.0 / S, vs = (yk - hxm) * iS;
+                BT_EACH(i, D) W.K[i] = W.Mb[i] * iS;
+                bsync<NW>();
+                BT_EACH(i, D) {                          // w = Lh K
+                    double s = 0.0;
+                    for (int j = 0; j < D; ++j) s = fma(W.C[i][j], W.K[j], s);
+                    W.KT[i] = s;
+                }
+                bsync<NW>();
+                const double cK = bdot<D>(W.K, W.KT, lane), Kl = bdot<D>(W.K, W.b, lane);
+                bsync<NW>();
+                BT_EACH(e, D * D) {                      // Lt = (I - K h)^T Lh (I - K h) + h^T h / S
+                    const int i = e / D, j = e - (e / D) * D;
+                    W.C[i][j] = fma(-H[i], W.KT[j], fma(-W.KT[i], H[j], fma((cK + iS) * H[i], H[j], W.C[i][j])));
+                }
+                BT_EACH(i, D) W.b[i] = fma(-H[i], Kl + vs, W.b[i]);
+                bsync<NW>();
             }
-            bmm<D, NW>(W.Z, W.Cm, W.C, nullptr, tid);                           // (P^s - P^-) X
-            bsync<NW>();
-            bmm<D, NW, true, false>(W.FP, W.C, W.Z, W.T, tid);                  // P + X^T (...) X
-            bsync<NW>();
-            BT_EACH(e, D * D) {
-                const int i = e / D, j = e - (e / D) * D;
-                W.P[i][j] = 0.5 * (W.FP[i][j] + W.FP[j][i]);
+            if (kind == 0) {                             // lh <- F^T lt, Lh <- F^T Lt F
+                bmm<D, NW>(W.T, W.C, W.F, nullptr, tid);
+                BT_EACH(i, D) {
+                    double s = 0.0;
+                    for (int j = 0; j < D; ++j) s = fma(W.F[j][i], W.b[j], s);
+                    W.x[i] = s;
+                }
+                bsync<NW>();
+                bmm<D, NW, true, false>(W.C, W.F, W.T, nullptr, tid);
+                BT_EACH(i, D) W.b[i] = W.x[i];
+                bsync<NW>();
             }
-            BT_EACH(i, D) W.x[i] = W.xm[i];
         }
-        bsync<NW>();
-        double mo = 0.0, vo = 0.0;
-        BT_EACH(i, D) {
-            double s = 0.0;
-            for (int j = 0; j < D; ++j) s = fma(W.P[i][j], H[j], s);
-            mo = fma(H[i], W.x[i], mo);
-            vo = fma(H[i], s, vo);
-        }
-        mo = wsum(mo);
-        vo = wsum(vo);
-        if (tid == 0) {
-            if (q.mean) q.mean[k] = mo;
-            if (q.var) q.var[k] = vo;
-        }
-        bsync<NW>();
     }
     if (bad && tid == 0) raise_error(q.err, s0, kErrNumeric);
 }
@@ -520,27 +517,39 @@ __global__ void __launch_bounds__(32 * NW) kb_nll_grad(const BParamsT q, const d
             BT_EACH(e, D * D) W.T[e / D][e % D] = src[D + si(D, e / D, e % D)];
             bsync<NW>();
         }
+        // P^- h^T (W.HP) and x^- (W.xm) of step k; P^- itself is never formed (only its product with h)
         if (kind == 0) {
-            bmm<D, NW>(W.FP, W.F, W.T, nullptr, tid);
-            BT_EACH(i, D) {
-                double s = 0.0;
-                for (int j = 0; j < D; ++j) s = fma(W.F[i][j], W.dm[j], s);
-                W.xm[i] = s;
+            BT_EACH(i, D) {                              // g = F^T h^T (in W.x), x^- = F x_{k-1}
+                double s = 0.0, xm = 0.0;
+                for (int j = 0; j < D; ++j) {
+                    s = fma(W.F[j][i], H[j], s);
+                    xm = fma(W.F[i][j], W.dm[j], xm);
+                }
+                W.x[i] = s;
+                W.xm[i] = xm;
             }
             bsync<NW>();
-            bmm<D, NW, false, true>(W.P, W.FP, W.F, W.Q, tid);                 // P^- (in P)
+            BT_EACH(i, D) {                              // P_{k-1} g (in W.bm, rewritten below)
+                double s = 0.0;
+                for (int j = 0; j < D; ++j) s = fma(W.T[i][j], W.x[j], s);
+                W.bm[i] = s;
+            }
+            bsync<NW>();
+            BT_EACH(i, D) {                              // F (P g) + Q h^T
+                double s = 0.0;
+                for (int j = 0; j < D; ++j) s = fma(W.F[i][j], W.bm[j], fma(W.Q[i][j], H[j], s));
+                W.HP[i] = s;
+            }
         } else {
-            BT_EACH(e, D * D) W.P[e / D][e % D] = (kind == 1) ? W.T[e / D][e % D] : W.Pinf[e / D][e % D];
-            BT_EACH(i, D) W.xm[i] = (kind == 1) ? W.dm[i] : 0.0;
+            BT_EACH(i, D) {
+                double s = 0.0;
+                for (int j = 0; j < D; ++j) s = fma((kind == 1) ? W.T[i][j] : W.Pinf[i][j], H[j], s);
+                W.HP[i] = s;
+                W.xm[i] = (kind == 1) ? W.dm[i] : 0.0;
+            }
         }
         bsync<NW>();
         if (obs) {
-            BT_EACH(i, D) {
-                double s = 0.0;
-                for (int j = 0; j < D; ++j) s = fma(W.P[i][j], H[j], s);
-                W.HP[i] = s;
-            }
-            bsync<NW>();
             const double S = bdot<D>(H, W.HP, lane) + r;
             const double v = yk - bdot<D>(H, W.xm, lane);
             const double iS = 1.0 / S, vs = v * iS, c1 = 0.5 * (iS - vs * vs);
@@ -556,7 +565,6 @@ __global__ void __launch_bounds__(32 * NW) kb_nll_grad(const BParamsT q, const d
             gr += c1 - bK * vs + KCK;
             BT_EACH(e, D * D) {
                 const int i = e / D, j = e - (e / D) * D;
-                W.FP[i][j] = (kind == 0) ? W.FP[i][j] : 0.0;   // (F P_{k-1}: kept for Z below)
                 W.Cm[i][j] = fma(-W.CK[i], H[j], W.C[i][j]);   // C (I - K h^T)
             }
             BT_EACH(i, D) W.Mb[i] = fma(-H[i], bK, W.b[i]);
@@ -584,26 +592,21 @@ __global__ void __launch_bounds__(32 * NW) kb_nll_grad(const BParamsT q, const d
             break;
         }
         if (kind == 0) {
-            bmm<D, NW>(W.T, W.Cm, W.FP, nullptr, tid);                          // C^- F P_{k-1}
-            bsync<NW>();
-            BT_EACH(e, D * D) {
-                const int i = e / D, j = e - (e / D) * D;
-                W.Z[i][j] += fma(W.bm[i], W.dm[j], 2.0 * W.T[i][j]);
-                W.Cs[i][j] += W.Cm[i][j];
-            }
-            bsync<NW>();
-            bmm<D, NW>(W.T, W.Cm, W.F, nullptr, tid);                           // C^- F
+            bmm<D, NW>(W.FP, W.Cm, W.F, nullptr, tid);                          // C^- F
             BT_EACH(i, D) {
                 double s = 0.0;
                 for (int j = 0; j < D; ++j) s = fma(W.F[j][i], W.bm[j], s);
                 W.b[i] = s;
             }
             bsync<NW>();
-            bmm<D, NW, true, false>(W.FP, W.F, W.T, nullptr, tid);              // F^T C^- F
+            bmm<D, NW>(W.Pm, W.FP, W.T, nullptr, tid);                          // C^- F P_{k-1}
+            bmm<D, NW, true, false>(W.P, W.F, W.FP, nullptr, tid);              // F^T C^- F
             bsync<NW>();
             BT_EACH(e, D * D) {
                 const int i = e / D, j = e - (e / D) * D;
-                W.C[i][j] = 0.5 * (W.FP[i][j] + W.FP[j][i]);
+                W.Z[i][j] += fma(W.bm[i], W.dm[j], 2.0 * W.Pm[i][j]);
+                W.Cs[i][j] += W.Cm[i][j];
+                W.C[i][j] = 0.5 * (W.P[i][j] + W.P[j][i]);
             }
         } else {
             BT_EACH(e, D * D) W.C[e / D][e % D] = W.Cm[e / D][e % D];
