@@ -103,6 +103,9 @@ struct Blk {
     static constexpr int CB = (D == 16) ? 4 : 2;
 };
 
+#ifndef PSSGP_WMM_TILED
+#define PSSGP_WMM_TILED 1
+#endif
 template <int D, bool TA = false, bool TB = false>
 __device__ __forceinline__ void wmm(double (*Out)[LD(D)], const double (*A)[LD(D)], const double (*B)[LD(D)],
                                     const double (*Cadd)[LD(D)], int lane) {
@@ -130,7 +133,7 @@ __device__ __forceinline__ void wmm(double (*Out)[LD(D)], const double (*A)[LD(D
         for (int r = 0; r < RB; ++r)
 #pragma unroll
             for (int c = 0; c < CB; ++c) Out[i0 + r][j0 + c] = acc[r][c];
-    } else {
+    } else if constexpr (D * D <= 32 || !PSSGP_WMM_TILED) {
         for (int e = lane; e < D * D; e += 32) {
             const int i = e / D, j = e - (e / D) * D;
             double s = Cadd ? Cadd[i][j] : 0.0;
@@ -138,6 +141,39 @@ __device__ __forceinline__ void wmm(double (*Out)[LD(D)], const double (*A)[LD(D
             for (int k = 0; k < D; ++k) s = fma(TA ? A[k][i] : A[i][k], TB ? B[j][k] : B[k][j], s);
             Out[i][j] = s;
         }
+    } else {
+        // other D: a 4 x 8 lane grid, each lane a register tile of RB = ceil(D / 4) contiguous rows x
+        // CB = ceil(D / 8) columns strided by 8 (RB + CB shared loads per RB CB FMAs instead of 2 per
+        // FMA); edge lanes clamp their loads and skip their stores.  No lane-dependent trip count.
+        constexpr int PC = 8, RB = (D + 3) / 4, CB = (D + PC - 1) / PC;
+        const int i0 = (lane / PC) * RB, pc = lane % PC;
+        int ri[RB], cj[CB];
+#pragma unroll
+        for (int r = 0; r < RB; ++r) ri[r] = min(i0 + r, D - 1);
+#pragma unroll
+        for (int c = 0; c < CB; ++c) cj[c] = min(pc + c * PC, D - 1);
+        double acc[RB][CB];
+#pragma unroll
+        for (int r = 0; r < RB; ++r)
+#pragma unroll
+            for (int c = 0; c < CB; ++c) acc[r][c] = Cadd ? Cadd[ri[r]][cj[c]] : 0.0;
+#pragma unroll 2
+        for (int k = 0; k < D; ++k) {
+            double a[RB], b[CB];
+#pragma unroll
+            for (int r = 0; r < RB; ++r) a[r] = TA ? A[k][ri[r]] : A[ri[r]][k];
+#pragma unroll
+            for (int c = 0; c < CB; ++c) b[c] = TB ? B[cj[c]][k] : B[k][cj[c]];
+#pragma unroll
+            for (int r = 0; r < RB; ++r)
+#pragma unroll
+                for (int c = 0; c < CB; ++c) acc[r][c] = fma(a[r], b[c], acc[r][c]);
+        }
+#pragma unroll
+        for (int r = 0; r < RB; ++r)
+#pragma unroll
+            for (int c = 0; c < CB; ++c)
+                if (i0 + r < D && pc + c * PC < D) Out[i0 + r][pc + c * PC] = acc[r][c];
     }
 }
 
@@ -3703,30 +3739,39 @@ __global__ void __launch_bounds__(32 * kWWarps) kw_grad_backward(const WParams p
             }
             __syncwarp();
         }
+        // P^- h^T (W.HP) and x^- (W.xm); P^- itself is never formed
         if (kind == 0) {
-            wmm<D>(W.FP, M.F, W.Pp, nullptr, lane);
-            for (int i = lane; i < D; i += 32) {
-                double s2 = 0.0;
-                for (int q = 0; q < D; ++q) s2 = fma(M.F[i][q], W.xp[q], s2);
-                W.xm[i] = s2;
+            for (int i = lane; i < D; i += 32) {     // g = F^T h^T (in W.bm, rewritten below), x^- = F x
+                double s2 = 0.0, xm = 0.0;
+                for (int q = 0; q < D; ++q) {
+                    s2 = fma(M.F[q][i], M.H[q], s2);
+                    xm = fma(M.F[i][q], W.xp[q], xm);
+                }
+                W.bm[i] = s2;
+                W.xm[i] = xm;
             }
             __syncwarp();
-            wmm<D, false, true>(W.Pm, W.FP, M.F, M.Q, lane);
-        } else {
-            for (int e = lane; e < D * D; e += 32) {
-                const int i = e / D, j = e - (e / D) * D;
-                W.Pm[i][j] = (kind == 1) ? W.Pp[i][j] : M.Pinf[i][j];
+            for (int i = lane; i < D; i += 32) {     // P_{k-1} g (in W.Mb, rewritten below)
+                double s2 = 0.0;
+                for (int q = 0; q < D; ++q) s2 = fma(W.Pp[i][q], W.bm[q], s2);
+                W.Mb[i] = s2;
             }
-            for (int i = lane; i < D; i += 32) W.xm[i] = (kind == 1) ? W.xp[i] : 0.0;
+            __syncwarp();
+            for (int i = lane; i < D; i += 32) {     // F (P g) + Q h^T
+                double s2 = 0.0;
+                for (int q = 0; q < D; ++q) s2 = fma(M.F[i][q], W.Mb[q], fma(M.Q[i][q], M.H[q], s2));
+                W.HP[i] = s2;
+            }
+        } else {
+            for (int i = lane; i < D; i += 32) {
+                double hp = 0.0;
+                for (int q = 0; q < D; ++q) hp = fma((kind == 1) ? W.Pp[i][q] : M.Pinf[i][q], M.H[q], hp);
+                W.HP[i] = hp;
+                W.xm[i] = (kind == 1) ? W.xp[i] : 0.0;
+            }
         }
         __syncwarp();
         if (obs) {
-            for (int i = lane; i < D; i += 32) {
-                double hp = 0.0;
-                for (int q = 0; q < D; ++q) hp = fma(W.Pm[i][q], M.H[q], hp);
-                W.HP[i] = hp;
-            }
-            __syncwarp();
             const double S = wdot<D>(M.H, W.HP, lane) + M.r;
             const double v = yk - wdot<D>(M.H, W.xm, lane);
             const double iS = 1.0 / S, vs = v * iS, c1 = 0.5 * (iS - vs * vs);
@@ -3769,25 +3814,20 @@ __global__ void __launch_bounds__(32 * kWWarps) kw_grad_backward(const WParams p
             break;
         }
         if (kind == 0) {
-            wmm<D>(W.T, W.Cm, W.FP, nullptr, lane);                  // C^- F P_{k-1}
-            __syncwarp();
-            for (int e = lane; e < D * D; e += 32) {
-                const int i = e / D, j = e - (e / D) * D;
-                W.Z[i][j] += fma(W.bm[i], W.xp[j], 2.0 * W.T[i][j]);
-                W.Cs[i][j] += W.Cm[i][j];
-            }
-            __syncwarp();
-            wmm<D>(W.T, W.Cm, M.F, nullptr, lane);                   // C^- F
+            wmm<D>(W.FP, W.Cm, M.F, nullptr, lane);                  // C^- F
             for (int i = lane; i < D; i += 32) {
                 double s2 = 0.0;
                 for (int q = 0; q < D; ++q) s2 = fma(M.F[q][i], W.bm[q], s2);
                 W.b[i] = s2;                                          // F^T b^-
             }
             __syncwarp();
-            wmm<D, true, false>(W.Pm, M.F, W.T, nullptr, lane);      // F^T C^- F
+            wmm<D>(W.T, W.FP, W.Pp, nullptr, lane);                  // C^- F P_{k-1}
+            wmm<D, true, false>(W.Pm, M.F, W.FP, nullptr, lane);     // F^T C^- F
             __syncwarp();
             for (int e = lane; e < D * D; e += 32) {
                 const int i = e / D, j = e - (e / D) * D;
+                W.Z[i][j] += fma(W.bm[i], W.xp[j], 2.0 * W.T[i][j]);
+                W.Cs[i][j] += W.Cm[i][j];
                 W.C[i][j] = 0.5 * (W.Pm[i][j] + W.Pm[j][i]);
             }
         } else {

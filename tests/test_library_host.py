@@ -207,3 +207,22 @@ def test_num_params_order():
         assert m.num_params == len(og.param_names(comps))
         # Model.theta (the row layout of the batched per-series calls) = the oracle's theta0
         np.testing.assert_allclose(m.theta, og.theta0(comps, 0.1), rtol=0, atol=1e-15)
+
+
+def test_no_unenclosed_lane_strided_loops():
+    """ptxas may drop a __syncwarp after a lane-strided loop with lane-dependent trip counts without
+    re-converging the warp ("A compiler finding"): scan the SASS of every built kernel
+    for such loops outside any BSSY/BSYNC region; the only ones allowed are global copies that end
+    in EXIT (kw_scan_*) and reductions that continue with re-converging shuffles (k_grad_contract)."""
+    import glob
+    import shutil
+    import subprocess
+    import sys
+    objs = sorted(glob.glob(os.path.join(os.path.dirname(P.__file__), "build", "*.o")))
+    if not objs or shutil.which("cuobjdump") is None:
+        pytest.skip("no built objects / cuobjdump")
+    tool = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools", "sass_divergent_loops.py")
+    out = subprocess.run([sys.executable, tool, *objs], capture_output=True, text=True, check=True).stdout
+    bad = [ln for ln in out.splitlines()
+           if " loop " in ln and not ("kw_scan_" in ln and "then: EXIT" in ln) and "k_grad_contract" not in ln]
+    assert not bad, "\n".join(bad[:10])

@@ -24,26 +24,33 @@ def functions(path):
         yield name, body
 
 
+def scan(path):
+    lines = []
+    for name, body in functions(path):
+        regions = [(pc, int(m.group(1), 16)) for pc, ins in body
+                   for m in [re.match(r"BSSY(?:\.RECONVERGENT)?\s+B\d+,\s*0x([0-9a-f]+)", ins)] if m]
+        for pc, ins in body:
+            m = re.match(r"@!?P\d\s+BRA\s+0x([0-9a-f]+)", ins)
+            if not m:
+                continue
+            tgt = int(m.group(1), 16)
+            if tgt >= pc or any(b < tgt and r > pc for b, r in regions):
+                continue
+            loop = [i for p, i in body if tgt <= p <= pc]
+            after = [i for p, i in body if p > pc][:3]
+            if any(re.search(r"(VIADD|IADD3).*0x20 ?$", i) for i in loop) and len(loop) < 120:
+                lines.append(f"{path.split('/')[-1]} {name[:80]} loop {hex(tgt)}-{hex(pc)} ({len(loop)} instr), "
+                             "then: " + " | ".join(after))
+    return lines
+
+
 def main(paths):
-    total = 0
-    for path in paths:
-        for name, body in functions(path):
-            regions = [(pc, int(m.group(1), 16)) for pc, ins in body
-                       for m in [re.match(r"BSSY(?:\.RECONVERGENT)?\s+B\d+,\s*0x([0-9a-f]+)", ins)] if m]
-            for pc, ins in body:
-                m = re.match(r"@!?P\d\s+BRA\s+0x([0-9a-f]+)", ins)
-                if not m:
-                    continue
-                tgt = int(m.group(1), 16)
-                if tgt >= pc or any(b < tgt and r > pc for b, r in regions):
-                    continue
-                loop = [i for p, i in body if tgt <= p <= pc]
-                after = [i for p, i in body if p > pc][:3]
-                if any(re.search(r"(VIADD|IADD3).*0x20 ?$", i) for i in loop) and len(loop) < 120:
-                    total += 1
-                    print(f"{path.split('/')[-1]} {name[:80]} loop {hex(tgt)}-{hex(pc)} ({len(loop)} instr), then: "
-                          + " | ".join(after))
-    print("unenclosed lane-strided loops:", total)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=16) as ex:
+        found = [ln for lines in ex.map(scan, paths) for ln in lines]
+    for ln in found:
+        print(ln)
+    print("unenclosed lane-strided loops:", len(found))
 
 
 if __name__ == "__main__":
