@@ -65,7 +65,7 @@ def alg_bytes(slot: str, d: int, wide_stream: bool = False, f32: bool = False) -
 # kernel families behind each profile slot (thread path d <= 3, wide path d >= 4)
 _FAMILY = {"k_filter_reduce": ("k_filter_reduce", ("kw_filter_fold",)),
            "k_filter_apply": ("k_filter_apply", ("kw_filter_apply", "kw_grad_forward", "kb_posterior")),
-           "k_smoother_apply": ("k_smoother_apply", ("kw_smoother_apply",)),
+           "k_smoother_apply": ("k_smoother_apply", ("kw_smoother_apply", "kw_smoother_mbf")),
            "k_grad_fold": ("k_grad_fold", ("k_grad_fold", "kw_grad_backward", "kb_nll_grad")),
            "k_discretize": ("k_discretize", ("kw_discretize", "kb_build")), "k_filter_scan": ("", ("kw_scan_filter",)),
            "k_smoother_scan": ("", ("kw_scan_smoother", "kw_scan_adjoint"))}
@@ -113,11 +113,25 @@ def ncu_traffic(slot: str, d: int, cfg_key: str, f32: bool = False):
     return (float(row["dram__bytes_read.sum"]) + float(row["dram__bytes_write.sum"])) * 1e9, src
 
 
+# warp-cooperative kernels whose d x d products (per step, per chain) run through the register-tiled
+# wmm (pssgp_wide.cuh) for d outside {8, 16}: the padded tile rows / columns execute FMAs that are
+# not algorithmic work
+_TILED_PRODUCTS = {"kw_filter_fold<": 3, "kw_grad_forward<": 3, "kw_grad_backward<": 3}
+
+
 def flops_per_step(slot: str, d: int, cfg_key: str):
-    """Executed fp64 flops per time step (DFMA = 2) from the SASS counts of the committed capture."""
+    """Algorithmic fp64 flops per time step (DFMA = 2): the SASS counts of the committed capture, less
+    the padded-tile FMAs of the register-tiled warp products (2 (32 RB CB d - d^3) each)."""
     row, _ = _ncu_row(slot, d, cfg_key)
     if row is not None and row.get("fp64_flops_per_step"):
-        return float(row["fp64_flops_per_step"])
+        fl = float(row["fp64_flops_per_step"])
+        name = row["Kernel Name"]
+        if d * d > 32 and d not in (8, 16):
+            rb, cb = (d + 3) // 4, (d + 7) // 8
+            for k, n in _TILED_PRODUCTS.items():
+                if k in name:
+                    fl -= n * 2 * (32 * rb * cb * d - d ** 3)
+        return fl
     return None
 
 
