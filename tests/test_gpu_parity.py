@@ -5,6 +5,8 @@ measures = SURVEY.md §8(c) reading Z14):
     var : elementwise max|dv / v_ref|           <= 1e-8
     nll : |dNLL| / |NLL_ref|                   <= 1e-9
 """
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -608,3 +610,35 @@ def test_host_async_slot_reuse(cuda_device):
     for w, (mo, vo, no) in zip(ws, outs):
         mean, var, nll = m.posterior_host(w.t, w.y, w.mask)
         assert np.array_equal(mo.numpy(), mean) and np.array_equal(vo.numpy(), var) and float(no[0]) == float(nll[0])
+
+
+@pytest.mark.parametrize("model", ["rbf6", "quasi1"])
+def test_wide_quarter_adjoint_rescan_variant(cuda_device, model, tmp_path):
+    """The non-default adjoint-form RTS rescan of the quarter path (d <= 8; PSSGP_WIDE_LPR bit 11,
+    read once per process, so in a subprocess) against the sequential oracle."""
+    import subprocess
+    import sys
+    code = f"""
+import sys, numpy as np, torch
+sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})
+sys.path.insert(0, {os.path.dirname(os.path.abspath(__file__))!r})
+import synth, oracle
+import paper_2102_09964_b200 as P
+from test_gpu_parity import PADE_MODELS, _uniform
+comps = PADE_MODELS[{model!r}]
+rp = synth.random_problem(7, 3001, kind="matern32", p_missing=0.2)
+for w in (_uniform(comps, 0.05, 4001, 0.01, p_missing=0.2, seed=5),
+          synth.Workload("jittered", comps, 0.05, rp.t, rp.y, rp.mask)):
+    m = P.Model(w.components, w.noise_var, uniform_dt=w.uniform_dt)
+    t, y, mk = (torch.from_numpy(a).cuda() for a in (w.t, w.y, w.mask))
+    mean, var, nll = m.posterior(t, y, mk)
+    m.check()
+    o = oracle.posterior(w)
+    em = np.max(np.abs(mean.cpu().numpy() - o["mean"])) / np.max(np.abs(o["mean"]))
+    ev = np.max(np.abs(var.cpu().numpy() - o["var"]) / o["var"])
+    assert em < 1e-9 and ev < 1e-9, (em, ev)
+print("ok")
+"""
+    env = dict(os.environ, PSSGP_WIDE_LPR="4095")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-2000:] + r.stderr[-2000:]
