@@ -464,8 +464,125 @@ struct SCombF {
 
 // out = ei (x) ej, with Minv = (I + C_i J_j)^-1 and
 // (I + J_j C_i)^-1 = Minv^T.  out may alias ej but not ei.
+#ifndef PSSGP_WCOMBINE_GJ
+#define PSSGP_WCOMBINE_GJ 1
+#endif
+// The filtering operator by one warp, solve form: X = (I + C_i J_j)^-1 [A_i | v1 |
+// C_i] (v1 = b_i + C_i eta_j) by a register Gauss-Jordan elimination with partial pivoting, one row
+// of the augmented system per lane and the pivot row broadcast by shuffles (no shared traffic, no
+// explicit inverse); then A = A_j X_A, b = A_j X_v + b_j, C = A_j X_C A_j^T + C_j,
+// eta = X_A^T (eta_j - J_j b_i) + eta_i, J = X_A^T J_j A_i + J_i (X_A^T = A_i^T (I + J_j C_i)^-1 by
+// the symmetry of C and J) - five register-tiled products.  out may alias ej.
+template <int D>
+__device__ bool wcombine_gj(const SF<D>& ei, SF<D>& ej, SF<D>& out, SCombF<D>& s, int lane) {
+    static_assert(D <= 32, "one row per lane");
+    double (*Wm)[LD(D)] = reinterpret_cast<double (*)[LD(D)]>(&s.W[0][0]);   // D x LD fits in D x (2D + 1)
+    wmm<D>(s.M, ei.C, ej.J, nullptr, lane);                                     // C_i J_j
+    if (lane < D) {
+        double a1 = ei.b[lane], a2 = ej.eta[lane];
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            a1 = fma(ei.C[lane][k], ej.eta[k], a1);
+            a2 = fma(-ej.J[lane][k], ei.b[k], a2);
+        }
+        s.v1[lane] = a1;
+        s.v2[lane] = a2;
+    }
+    __syncwarp();
+    constexpr int NX = 2 * D + 1;
+    const bool act = lane < D;
+    const int r = act ? lane : D - 1;
+    double a[D], x[NX];
+#pragma unroll
+    for (int j = 0; j < D; ++j) a[j] = s.M[r][j] + ((j == r) ? 1.0 : 0.0);
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        x[j] = ei.A[r][j];
+        x[D + 1 + j] = ei.C[r][j];
+    }
+    x[D] = s.v1[r];
+    bool ok = true;
+    unsigned used = 0u;
+    int myj = -1;                                   // the column this lane's row pivots
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        double v = (act && !((used >> lane) & 1u)) ? fabs(a[j]) : -1.0;
+        int who = lane;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, v, off);
+            const int ow = __shfl_xor_sync(0xffffffffu, who, off);
+            if (ov > v || (ov == v && ow < who)) { v = ov; who = ow; }
+        }
+        ok = ok && (v > 0.0);
+        used |= 1u << who;
+        if (lane == who) myj = j;
+        const double ip = 1.0 / __shfl_sync(0xffffffffu, a[j], who);
+        const double f = (lane == who) ? 0.0 : a[j] * ip;
+#pragma unroll
+        for (int k = j + 1; k < D; ++k) {
+            const double pk = __shfl_sync(0xffffffffu, a[k], who);
+            a[k] = (lane == who) ? a[k] * ip : fma(-f, pk, a[k]);
+        }
+#pragma unroll
+        for (int c = 0; c < NX; ++c) {
+            const double pc = __shfl_sync(0xffffffffu, x[c], who);
+            x[c] = (lane == who) ? x[c] * ip : fma(-f, pc, x[c]);
+        }
+    }
+    __syncwarp();                                   // everyone is done reading s.v1 / s.M
+    if (act) {                                      // solution row myj: X_A, X_v, X_C
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            s.T2[myj][j] = x[j];
+            s.T1[myj][j] = x[D + 1 + j];
+        }
+        s.v1[myj] = x[D];
+    }
+    __syncwarp();
+    wmm<D>(s.M, ej.A, s.T1, nullptr, lane);                                     // A_j X_C
+    wmm<D>(Wm, ej.J, ei.A, nullptr, lane);                                      // J_j A_i
+    double nb = 0.0, ne = 0.0;
+    if (act) {
+        nb = ej.b[lane];
+        ne = ei.eta[lane];
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            nb = fma(ej.A[lane][k], s.v1[k], nb);
+            ne = fma(s.T2[k][lane], s.v2[k], ne);
+        }
+    }
+    __syncwarp();
+    wmm<D, false, true>(s.T1, s.M, ej.A, ej.C, lane);                           // C = A_j X_C A_j^T + C_j
+    __syncwarp();
+    wmm<D>(s.M, ej.A, s.T2, nullptr, lane);                                     // A = A_j X_A
+    __syncwarp();                                   // A_j, J_j, C_j are read for the last time above
+    wmm<D, true, false>(out.A, s.T2, Wm, ei.J, lane);                           // X_A^T J_j A_i + J_i (in out.A)
+    __syncwarp();
+    for (int e0 = 0; e0 < D * D; e0 += 32) {        // J, C symmetrised (the same trip count in every lane)
+        const int e = e0 + lane;
+        if (e < D * D) {
+            const int i = e / D, j = e - (e / D) * D;
+            out.J[i][j] = 0.5 * (out.A[i][j] + out.A[j][i]);
+            out.C[i][j] = 0.5 * (s.T1[i][j] + s.T1[j][i]);
+        }
+    }
+    __syncwarp();
+    for (int e0 = 0; e0 < D * D; e0 += 32) {
+        const int e = e0 + lane;
+        if (e < D * D) out.A[e / D][e % D] = s.M[e / D][e % D];
+    }
+    if (act) {
+        out.b[lane] = nb;
+        out.eta[lane] = ne;
+    }
+    __syncwarp();
+    return ok;
+}
+
 template <int D>
 __device__ bool wcombine(const SF<D>& ei, SF<D>& ej, SF<D>& out, SCombF<D>& s, int lane) {
+    if constexpr (PSSGP_WCOMBINE_GJ && D <= 32) return wcombine_gj<D>(ei, ej, out, s, lane);
     // M = I + C_i J_j
     for (int e = lane; e < D * D; e += 32) {
         const int i = e / D, j = e - (e / D) * D;
