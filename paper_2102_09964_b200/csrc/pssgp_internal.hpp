@@ -53,6 +53,7 @@ struct pssgp_model {
     double* d_model = nullptr;            // wide path: F, Q, Pinf, H, r, udt (device copy)
     int wocc = 0;                         // wide path: resident CTAs / SM
     int wchains = 0;                      // wide path: resident chains / SM when the kernels use other CTA shapes
+    int wocc_grad = 0;                    // wide path, d > 16: resident CTAs / SM of the gradient kernels
     int fblock = 0;                       // aligned block size (2, 4 or d) containing every nonzero of G and W
     char* io = nullptr;                   // e2e device buffers
     size_t io_bytes = 0;

@@ -731,6 +731,89 @@ __device__ bool wapply_prefix(double* x, double (*P)[LD(D)], const SF<D>& a, SCo
     return ok;
 }
 
+// (x, P) <- (x, P) (x) a in solve form with caller scratch (three D x LD matrices, two D vectors):
+// [X_P | X_x] = (I + P J)^-1 [P | x + P eta] by the register Gauss-Jordan of wcombine_gj, then
+// P = A X_P A^T + C (symmetrised), x = A X_x + b.
+template <int D>
+__device__ bool wapply_prefix_gj(double* x, double (*P)[LD(D)], const SF<D>& a, double (*Mb)[LD(D)],
+                                 double (*Xb)[LD(D)], double (*Tb)[LD(D)], double* v1, double* v2, int lane) {
+    static_assert(D <= 32, "one row per lane");
+    wmm<D>(Mb, P, a.J, nullptr, lane);                                          // P J
+    if (lane < D) {
+        double acc = x[lane];
+#pragma unroll
+        for (int k = 0; k < D; ++k) acc = fma(P[lane][k], a.eta[k], acc);
+        v1[lane] = acc;
+    }
+    __syncwarp();
+    constexpr int NX = D + 1;
+    const bool act = lane < D;
+    const int r = act ? lane : D - 1;
+    double am[D], xr[NX];
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        am[j] = Mb[r][j] + ((j == r) ? 1.0 : 0.0);
+        xr[j] = P[r][j];
+    }
+    xr[D] = v1[r];
+    bool ok = true;
+    unsigned used = 0u;
+    int myj = -1;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        double v = (act && !((used >> lane) & 1u)) ? fabs(am[j]) : -1.0;
+        int who = lane;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, v, off);
+            const int ow = __shfl_xor_sync(0xffffffffu, who, off);
+            if (ov > v || (ov == v && ow < who)) { v = ov; who = ow; }
+        }
+        ok = ok && (v > 0.0);
+        used |= 1u << who;
+        if (lane == who) myj = j;
+        const double ip = 1.0 / __shfl_sync(0xffffffffu, am[j], who);
+        const double f = (lane == who) ? 0.0 : am[j] * ip;
+#pragma unroll
+        for (int k = j + 1; k < D; ++k) {
+            const double pk = __shfl_sync(0xffffffffu, am[k], who);
+            am[k] = (lane == who) ? am[k] * ip : fma(-f, pk, am[k]);
+        }
+#pragma unroll
+        for (int c = 0; c < NX; ++c) {
+            const double pc = __shfl_sync(0xffffffffu, xr[c], who);
+            xr[c] = (lane == who) ? xr[c] * ip : fma(-f, pc, xr[c]);
+        }
+    }
+    __syncwarp();
+    if (act) {
+#pragma unroll
+        for (int j = 0; j < D; ++j) Xb[myj][j] = xr[j];
+        v2[myj] = xr[D];
+    }
+    __syncwarp();
+    wmm<D>(Tb, a.A, Xb, nullptr, lane);                                         // A X_P
+    double xn = 0.0;
+    if (act) {
+        xn = a.b[lane];
+#pragma unroll
+        for (int k = 0; k < D; ++k) xn = fma(a.A[lane][k], v2[k], xn);
+    }
+    __syncwarp();
+    wmm<D, false, true>(Mb, Tb, a.A, a.C, lane);                                // A X_P A^T + C
+    __syncwarp();
+    for (int e0 = 0; e0 < D * D; e0 += 32) {
+        const int e = e0 + lane;
+        if (e < D * D) {
+            const int i = e / D, j = e - (e / D) * D;
+            P[i][j] = 0.5 * (Mb[i][j] + Mb[j][i]);
+        }
+    }
+    if (act) x[lane] = xn;
+    __syncwarp();
+    return ok;
+}
+
 // scratch of the suffix application (no inverse needed)
 template <int D>
 struct SSufScratch {
@@ -3622,16 +3705,9 @@ struct GFwdSmem {
     struct PerWarp {
         double P[D][LD(D)], M[D][LD(D)], Gam[D][LD(D)];
         double x[D], U[D];
-        union {
-            struct {
-                SF<D> a;
-                SCombF<D> s;
-            } c;
-            struct {
-                double FP[D][LD(D)], Pm[D][LD(D)], FM[D][LD(D)];
-                double xm[D], HP[D], w[D];
-            } st;
-        } u;
+        double FP[D][LD(D)], Pm[D][LD(D)], FM[D][LD(D)];   // step scratch (also the carry's)
+        double xm[D], HP[D], w[D];
+        SF<D> a;                                             // the scanned aggregate before the chain
     } w[kWWarps];
 };
 
@@ -3650,8 +3726,9 @@ __global__ void __launch_bounds__(32 * kWWarps) kw_grad_forward(const WParams p,
     for (int i = lane; i < D; i += 32) W.x[i] = 0.0;
     __syncwarp();
     if (c > 0) {
-        gload<D>(W.u.c.a, p.fagg + static_cast<int64_t>(c - 1) * FNW(D), lane);
-        if (!wapply_prefix<D>(W.x, W.P, W.u.c.a, W.u.c.s, lane) && lane == 0) raise_error(p.err, p.k0, kErrNumeric);
+        gload<D>(W.a, p.fagg + static_cast<int64_t>(c - 1) * FNW(D), lane);
+        if (!wapply_prefix_gj<D>(W.x, W.P, W.a, W.FP, W.Pm, W.FM, W.xm, W.HP, lane) && lane == 0)
+            raise_error(p.err, p.k0, kErrNumeric);
     }
     {   // filtered state entering the chain (for the backward rescan's first step)
         double* o = gb.gcar + static_cast<int64_t>(c) * CNW(D);
@@ -3682,36 +3759,36 @@ __global__ void __launch_bounds__(32 * kWWarps) kw_grad_forward(const WParams p,
         const int kind = (g == 0) ? 3 : wdisc_kind(tk - tprev, M.udt, false);
         tprev = tk;
         if (kind == 0) {
-            wmm<D>(W.u.st.FP, M.F, W.P, nullptr, lane);
-            wmm<D>(W.u.st.FM, M.F, W.M, nullptr, lane);
+            wmm<D>(W.FP, M.F, W.P, nullptr, lane);
+            wmm<D>(W.FM, M.F, W.M, nullptr, lane);
             for (int i = lane; i < D; i += 32) {
                 double s2 = 0.0;
                 for (int q = 0; q < D; ++q) s2 = fma(M.F[i][q], W.x[q], s2);
-                W.u.st.xm[i] = s2;
+                W.xm[i] = s2;
             }
             __syncwarp();
-            wmm<D, false, true>(W.u.st.Pm, W.u.st.FP, M.F, M.Q, lane);
+            wmm<D, false, true>(W.Pm, W.FP, M.F, M.Q, lane);
         } else {
             for (int e = lane; e < D * D; e += 32) {
                 const int i = e / D, j = e - (e / D) * D;
-                W.u.st.FM[i][j] = (kind == 1) ? W.M[i][j] : 0.0;
-                W.u.st.Pm[i][j] = (kind == 1) ? W.P[i][j] : M.Pinf[i][j];
+                W.FM[i][j] = (kind == 1) ? W.M[i][j] : 0.0;
+                W.Pm[i][j] = (kind == 1) ? W.P[i][j] : M.Pinf[i][j];
             }
-            for (int i = lane; i < D; i += 32) W.u.st.xm[i] = (kind == 1) ? W.x[i] : 0.0;
+            for (int i = lane; i < D; i += 32) W.xm[i] = (kind == 1) ? W.x[i] : 0.0;
         }
         __syncwarp();
         for (int i = lane; i < D; i += 32) {
             double hp = 0.0, ww = 0.0;
             for (int q = 0; q < D; ++q) {
-                hp = fma(W.u.st.Pm[i][q], M.H[q], hp);
-                ww = fma(W.u.st.FM[q][i], M.H[q], ww);
+                hp = fma(W.Pm[i][q], M.H[q], hp);
+                ww = fma(W.FM[q][i], M.H[q], ww);
             }
-            W.u.st.HP[i] = hp;
-            W.u.st.w[i] = ww;
+            W.HP[i] = hp;
+            W.w[i] = ww;
         }
         __syncwarp();
-        const double S = wdot<D>(M.H, W.u.st.HP, lane) + M.r;
-        const double hx = wdot<D>(M.H, W.u.st.xm, lane);
+        const double S = wdot<D>(M.H, W.HP, lane) + M.r;
+        const double hx = wdot<D>(M.H, W.xm, lane);
         if (lane == 0 && obs && !(S > 0.0 && S < INFINITY)) raise_error(p.err, g, kErrNumeric);
         const double iS = obs ? 1.0 / S : 0.0;
         const double v = obs ? (yk - hx) : 0.0;
@@ -3719,16 +3796,16 @@ __global__ void __launch_bounds__(32 * kWWarps) kw_grad_forward(const WParams p,
         const double c1 = obs ? 0.5 * (iS - vs * vs) : 0.0;
         for (int e = lane; e < D * D; e += 32) {
             const int i = e / D, j = e - (e / D) * D;
-            const double hpi = W.u.st.HP[i] * iS;
-            W.P[i][j] = fma(-hpi, W.u.st.HP[j], W.u.st.Pm[i][j]);
-            W.M[i][j] = fma(-hpi, W.u.st.w[j], W.u.st.FM[i][j]);
-            const double wi = W.u.st.w[i], wj = W.u.st.w[j];
+            const double hpi = W.HP[i] * iS;
+            W.P[i][j] = fma(-hpi, W.HP[j], W.Pm[i][j]);
+            W.M[i][j] = fma(-hpi, W.w[j], W.FM[i][j]);
+            const double wi = W.w[i], wj = W.w[j];
             W.Gam[i][j] += fma(c1 * wi, wj, -0.5 * vs * (wi * W.U[j] + W.U[i] * wj));
         }
         __syncwarp();
         for (int i = lane; i < D; i += 32) {
-            W.x[i] = fma(W.u.st.HP[i], vs, W.u.st.xm[i]);
-            W.U[i] = fma(vs, W.u.st.w[i], W.U[i]);
+            W.x[i] = fma(W.HP[i], vs, W.xm[i]);
+            W.U[i] = fma(vs, W.w[i], W.U[i]);
         }
         if (obs) {
             quad = fma(v, vs, quad);

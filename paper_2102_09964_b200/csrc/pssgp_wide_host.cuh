@@ -115,9 +115,23 @@ struct WPlan {
 };
 
 template <int D>
-WPlan make_wplan(pssgp_model* m, int64_t n) {
+WPlan make_wplan(pssgp_model* m, int64_t n, bool grad = false) {
     using namespace pssgp::wide;
     wide_set_smem_attrs<D>(m->device);
+    if constexpr (D > 16) {
+        // the gradient runs the fold and the two gradient rescans only: its own occupancy (the
+        // posterior's RTS kernel holds fewer CTAs per SM)
+        if (grad && m->wocc_grad == 0) {
+            int a = 0, b = 0, c = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, kw_filter_fold<D>, 32 * kWWarps, sizeof(K1Smem<D>));
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kw_grad_forward<D>, 32 * kWWarps, sizeof(GFwdSmem<D>));
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, kw_grad_backward<D>, 32 * kWWarps, sizeof(GBwdSmem<D>));
+            m->wocc_grad = std::max(1, std::min(a, std::min(b, c)));
+            if (getenv("PSSGP_WIDE_DEBUG"))
+                fprintf(stderr, "wide gradient plan D=%d occupancy: fold %d, forward %d, backward %d (smem %zu / %zu / %zu)\n",
+                        D, a, b, c, sizeof(K1Smem<D>), sizeof(GFwdSmem<D>), sizeof(GBwdSmem<D>));
+        }
+    }
     if (m->wocc == 0) {
         int a = 0, b = 0, c = 0;
         // (the lane-per-row fold of D <= 8 is not part of the plan's occupancy: it is register-
@@ -183,7 +197,8 @@ WPlan make_wplan(pssgp_model* m, int64_t n) {
             }
         }
     }
-    const int64_t per_sm = m->wchains > 0 ? m->wchains : static_cast<int64_t>(m->wocc) * kWWarps;   // chains per SM
+    int64_t per_sm = m->wchains > 0 ? m->wchains : static_cast<int64_t>(m->wocc) * kWWarps;   // chains per SM
+    if (D > 16 && grad && m->wocc_grad > 0) per_sm = static_cast<int64_t>(m->wocc_grad) * kWWarps;
     const int64_t target = static_cast<int64_t>(m->sm_count) * per_sm;
     WPlan pl;
     // small N: chains of at least 16 steps (8 for the warp-cooperative kernels of d > 16, whose chain
@@ -676,7 +691,7 @@ pssgp_status wide_nll_grad(pssgp_model* m, int64_t N, const double* t, const dou
         }
         if (!hbuf.empty()) cudaMemcpy(m->d_gder, hbuf.data(), hbuf.size() * sizeof(double), cudaMemcpyHostToDevice);
     }
-    const WPlan pl = make_wplan<D>(m, N);
+    const WPlan pl = make_wplan<D>(m, N, true);
     WParams p;
     pssgp_status st = wide_setup<D>(m, pl, p);
     if (st) return st;
