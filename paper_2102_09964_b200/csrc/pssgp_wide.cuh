@@ -3889,6 +3889,7 @@ struct GBwdSmem {
         double C[D][LD(D)], Z[D][LD(D)], Cs[D][LD(D)], Pp[D][LD(D)], FP[D][LD(D)], Pm[D][LD(D)], T[D][LD(D)],
             Cm[D][LD(D)];
         double b[D], xp[D], xm[D], HP[D], K[D], CK[D], KT[D], Mb[D], bm[D];
+        double rec[CNW(D)];                 // the packed filtered record of the previous step
     } w[kWWarps];
 };
 
@@ -3918,20 +3919,53 @@ __global__ void __launch_bounds__(32 * kWWarps) kw_grad_backward(const WParams p
     const int64_t ke = min(kb + p.K, p.n);
     const double* xpc = p.xp + static_cast<int64_t>(c) * p.K * CNW(D);
     double gr = 0.0;
+    // the filtered record of step k - 1 and the inputs of step k are loaded one step ahead into
+    // registers (the global-load latency overlaps the previous step's work)
+    constexpr int NPL = (CNW(D) + 31) / 32;
+    double pre[NPL];
+    auto load_rec = [&](int64_t k) {
+        const double* src = (k > kb) ? xpc + (k - 1 - kb) * CNW(D) : gb.gcar + static_cast<int64_t>(c) * CNW(D);
+#pragma unroll
+        for (int q = 0; q < NPL; ++q) {
+            const int e = lane + 32 * q;
+            pre[q] = (e < CNW(D)) ? src[e] : 0.0;
+        }
+    };
+    double tn = 0.0, tpn = 0.0, yn = 0.0;
+    bool on = false;
+    auto load_in = [&](int64_t k) {
+        tn = __ldg(p.t + k);
+        tpn = (p.k0 + k > 0) ? __ldg(p.t + k - 1) : 0.0;
+        on = __ldg(p.mask + k) != 0;
+        yn = on ? __ldg(p.y + k) : 0.0;
+    };
+    if (ke > kb) {
+        load_rec(ke - 1);
+        load_in(ke - 1);
+    }
     for (int64_t k = ke - 1; k >= kb; --k) {
         const int64_t g = p.k0 + k;
-        const double tk = __ldg(p.t + k);
-        const int kind = (g == 0) ? 3 : wdisc_kind(tk - __ldg(p.t + k - 1), M.udt, false);
-        const bool obs = __ldg(p.mask + k) != 0;
-        const double yk = obs ? __ldg(p.y + k) : 0.0;
-        if (kind != 3) {   // filtered state of the previous step
-            const double* src = (k > kb) ? xpc + (k - 1 - kb) * CNW(D) : gb.gcar + static_cast<int64_t>(c) * CNW(D);
-            for (int i = lane; i < D; i += 32) W.xp[i] = src[i];
-            for (int e = lane; e < D * D; e += 32) {
-                const int i = e / D, j = e - (e / D) * D;
-                W.Pp[i][j] = src[D + si(D, i, j)];
+        const double tk = tn;
+        const int kind = (g == 0) ? 3 : wdisc_kind(tk - tpn, M.udt, false);
+        const bool obs = on;
+        const double yk = yn;
+        if (kind != 3) {   // filtered state of the previous step (prefetched)
+#pragma unroll
+            for (int q = 0; q < NPL; ++q) {
+                const int e = lane + 32 * q;
+                if (e < CNW(D)) W.rec[e] = pre[q];
             }
             __syncwarp();
+            for (int i = lane; i < D; i += 32) W.xp[i] = W.rec[i];
+            for (int e = lane; e < D * D; e += 32) {
+                const int i = e / D, j = e - (e / D) * D;
+                W.Pp[i][j] = W.rec[D + si(D, i, j)];
+            }
+            __syncwarp();
+        }
+        if (k - 1 >= kb) {
+            load_rec(k - 1);
+            load_in(k - 1);
         }
         // P^- h^T (W.HP) and x^- (W.xm); P^- itself is never formed
         if (kind == 0) {
