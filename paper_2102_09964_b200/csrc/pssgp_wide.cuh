@@ -3751,10 +3751,23 @@ __global__ void __launch_bounds__(32 * kWWarps) kw_grad_forward(const WParams p,
     double quad = 0.0, logs = 0.0;
     int nobs = 0;
     double* xpc = p.xp + static_cast<int64_t>(c) * p.K * CNW(D);
+    // the step inputs are loaded one step ahead (their latency overlaps the previous step)
+    double tn = 0.0, yn = 0.0;
+    bool on = false;
+    if (kb < ke) {
+        tn = __ldg(p.t + kb);
+        on = __ldg(p.mask + kb) != 0;
+        yn = on ? __ldg(p.y + kb) : 0.0;
+    }
     for (int64_t k = kb; k < ke; ++k) {
-        const double tk = __ldg(p.t + k);
-        const bool obs = __ldg(p.mask + k) != 0;
-        const double yk = obs ? __ldg(p.y + k) : 0.0;
+        const double tk = tn;
+        const bool obs = on;
+        const double yk = yn;
+        if (k + 1 < ke) {
+            tn = __ldg(p.t + k + 1);
+            on = __ldg(p.mask + k + 1) != 0;
+            yn = on ? __ldg(p.y + k + 1) : 0.0;
+        }
         const int64_t g = p.k0 + k;
         const int kind = (g == 0) ? 3 : wdisc_kind(tk - tprev, M.udt, false);
         tprev = tk;
