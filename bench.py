@@ -156,7 +156,7 @@ def parse():
     ap.add_argument("--uniform", action="store_true", help="uniform dt (secondary row)")
     ap.add_argument("--kind", default="matern52")
     ap.add_argument("--config", default="metric", choices=["metric", "c2", "c3", "c4", "c5", "batched", "grad", "gradb", "gradco2", "gradbt",
-                                                          "batchedbt", "f32"],
+                                                          "batchedbt", "co2post", "f32"],
                     help="workload (default: the BASELINE metric); c3/c4 are the d = 6 / d = 16 rows")
     ap.add_argument("--irregular", action="store_true", help="c3/c4 on a jittered grid (device Pade discretisation)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -318,6 +318,9 @@ def make_workload(args):
         # B HMC chains / multi-start fits of the paper's CO2 model (J = 3, n_x = 18), one 3,200-week
         # series each
         return synth.co2_product(n=3200, order=3)
+    if args.config == "co2post":
+        # the posterior of the paper's CO2 model C_Per x C_Mat + C_Mat at n_x = 18 (J = 3), weekly grid
+        return synth.co2_product(n=args.N if args.N != 2 ** 24 else 2 ** 20, order=3)
     if args.config == "gradco2":
         # the paper's HMC model C_Per x C_Mat + C_Mat at n_x = 18 (J = 3), weekly grid
         return synth.co2_product(n=args.N if args.N != 2 ** 24 else 2 ** 20, order=3)

@@ -814,6 +814,58 @@ __device__ bool wapply_prefix_gj(double* x, double (*P)[LD(D)], const SF<D>& a, 
     return ok;
 }
 
+// E = S A^-1 for a symmetric A by one warp: rows of [A | S^T] per lane, the register Gauss-Jordan of
+// wcombine_gj (partial pivoting); E must alias neither S nor A.
+template <int D>
+__device__ bool wright_div_sym_gj(double (*E)[LD(D)], const double (*S)[LD(D)], const double (*A)[LD(D)],
+                                  int lane) {
+    static_assert(D <= 32, "one row per lane");
+    const bool act = lane < D;
+    const int r = act ? lane : D - 1;
+    double am[D], xr[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        am[j] = A[r][j];
+        xr[j] = S[j][r];
+    }
+    bool ok = true;
+    unsigned used = 0u;
+    int myj = -1;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        double v = (act && !((used >> lane) & 1u)) ? fabs(am[j]) : -1.0;
+        int who = lane;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, v, off);
+            const int ow = __shfl_xor_sync(0xffffffffu, who, off);
+            if (ov > v || (ov == v && ow < who)) { v = ov; who = ow; }
+        }
+        ok = ok && (v > 0.0);
+        used |= 1u << who;
+        if (lane == who) myj = j;
+        const double ip = 1.0 / __shfl_sync(0xffffffffu, am[j], who);
+        const double f = (lane == who) ? 0.0 : am[j] * ip;
+#pragma unroll
+        for (int k = j + 1; k < D; ++k) {
+            const double pk = __shfl_sync(0xffffffffu, am[k], who);
+            am[k] = (lane == who) ? am[k] * ip : fma(-f, pk, am[k]);
+        }
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+            const double pc = __shfl_sync(0xffffffffu, xr[c], who);
+            xr[c] = (lane == who) ? xr[c] * ip : fma(-f, pc, xr[c]);
+        }
+    }
+    __syncwarp();
+    if (act) {
+#pragma unroll
+        for (int i = 0; i < D; ++i) E[i][myj] = xr[i];
+    }
+    __syncwarp();
+    return ok;
+}
+
 // scratch of the suffix application (no inverse needed)
 template <int D>
 struct SSufScratch {
@@ -1751,14 +1803,14 @@ struct K3Smem {
         double P[D][LD(D)];
         double x[D];
         union {
-            struct {                  // carry phase
+            struct {                  // carry phase (wapply_prefix_gj with its own scratch)
                 SF<D> a;
-                SCombF<D> s;
+                double Mb[D][LD(D)], Xb[D][LD(D)], Tb[D][LD(D)];
+                double v1[D], v2[D];
             } c;
             struct {                  // step phase (+ chain smoother aggregate)
                 double Sg[D][LD(D)], P0[D][LD(D)], Sm[D][LD(D)], Pm[D][LD(D)], FP[D][LD(D)];
                 double xm[D], x0[D], HP[D], SH[D];
-                double W2[D][2 * D + 1];
                 SS<D> sagg;
             } st;
         } u;
@@ -1821,12 +1873,9 @@ __device__ void k3w_chain_sagg(const WParams& p, typename K3Smem<D>::PerWarp& W,
             W.u.st.Pm[i][j] = s;
         }
         __syncwarp();
-        // E = Sm Pm^-1 : invert Pm (into W.u.st.FP via winverse on a copy)
-        for (int e = lane; e < D * D; e += 32) W.u.st.FP[e / D][e % D] = W.u.st.Pm[e / D][e % D];
-        __syncwarp();
-        if (!winverse<D>(W.u.st.FP, W.u.st.W2, lane) && lane == 0) raise_error(p.err, p.k0 + ke, kErrNumeric);
-        wmm<D>(sagg->E, W.u.st.Sm, W.u.st.FP, nullptr, lane);
-        __syncwarp();
+        // E = Sm Pm^-1 (Pm symmetric): a register Gauss-Jordan solve, no explicit inverse
+        if (!wright_div_sym_gj<D>(sagg->E, W.u.st.Sm, W.u.st.Pm, lane) && lane == 0)
+            raise_error(p.err, p.k0 + ke, kErrNumeric);
         for (int i = lane; i < D; i += 32) {
             double a = W.u.st.x0[i];
             for (int q = 0; q < D; ++q) a = fma(-sagg->E[i][q], W.u.st.xm[q], a);
@@ -1865,11 +1914,11 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WMINB) kw_filter_apply(con
     __syncwarp();
     for (int g = 0; g < p.rank && p.in_filt; ++g) {
         gload<D>(W.u.c.a, p.in_filt + static_cast<int64_t>(g) * FNW(D), lane);
-        if (!wapply_prefix<D>(W.x, W.P, W.u.c.a, W.u.c.s, lane) && lane == 0) raise_error(p.err, p.k0, kErrNumeric);
+        if (!wapply_prefix_gj<D>(W.x, W.P, W.u.c.a, W.u.c.Mb, W.u.c.Xb, W.u.c.Tb, W.u.c.v1, W.u.c.v2, lane) && lane == 0) raise_error(p.err, p.k0, kErrNumeric);
     }
     if (c > 0) {
         gload<D>(W.u.c.a, p.fagg + static_cast<int64_t>(c - 1) * FNW(D), lane);
-        if (!wapply_prefix<D>(W.x, W.P, W.u.c.a, W.u.c.s, lane) && lane == 0) raise_error(p.err, p.k0, kErrNumeric);
+        if (!wapply_prefix_gj<D>(W.x, W.P, W.u.c.a, W.u.c.Mb, W.u.c.Xb, W.u.c.Tb, W.u.c.v1, W.u.c.v2, lane) && lane == 0) raise_error(p.err, p.k0, kErrNumeric);
     }
     const int64_t kb = static_cast<int64_t>(c) * p.K;
     const int64_t ke = min(kb + p.K, p.n);
@@ -2004,11 +2053,11 @@ __global__ void __launch_bounds__(32 * kWWarps, PSSGP_WLPR_MINB) kw_filter_apply
     __syncwarp();
     for (int g = 0; g < p.rank && p.in_filt; ++g) {
         gload<D>(W.u.c.a, p.in_filt + static_cast<int64_t>(g) * FNW(D), lane);
-        if (!wapply_prefix<D>(W.x, W.P, W.u.c.a, W.u.c.s, lane) && lane == 0) raise_error(p.err, p.k0, kErrNumeric);
+        if (!wapply_prefix_gj<D>(W.x, W.P, W.u.c.a, W.u.c.Mb, W.u.c.Xb, W.u.c.Tb, W.u.c.v1, W.u.c.v2, lane) && lane == 0) raise_error(p.err, p.k0, kErrNumeric);
     }
     if (c > 0) {
         gload<D>(W.u.c.a, p.fagg + static_cast<int64_t>(c - 1) * FNW(D), lane);
-        if (!wapply_prefix<D>(W.x, W.P, W.u.c.a, W.u.c.s, lane) && lane == 0) raise_error(p.err, p.k0, kErrNumeric);
+        if (!wapply_prefix_gj<D>(W.x, W.P, W.u.c.a, W.u.c.Mb, W.u.c.Xb, W.u.c.Tb, W.u.c.v1, W.u.c.v2, lane) && lane == 0) raise_error(p.err, p.k0, kErrNumeric);
     }
     const bool act = lane < D;
     const int r = act ? lane : 0;

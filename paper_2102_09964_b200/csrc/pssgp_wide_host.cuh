@@ -31,6 +31,7 @@ void with_fblock(const pssgp_model* m, Fn&& fn) {
     fn(std::integral_constant<int, D>{});
 }
 // ========================================================================== wide path (d >= 4)
+constexpr int kMbfWPC = 2;   // d > 16: warps (chains) per CTA of the adjoint-form RTS rescan
 
 // The >48 KB dynamic shared-memory opt-in is a per-device function attribute: set it once per
 // device (bit `device` of a process-wide mask; setting it twice is harmless, so a race only repeats
@@ -77,6 +78,16 @@ void wide_set_smem_attrs(int device) {
     }
     cudaFuncSetAttribute(kw_filter_apply<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K3Smem<D>));
     cudaFuncSetAttribute(kw_smoother_apply<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K5Smem<D>));
+    if constexpr (D > 16) {   // adjoint-form RTS rescan, one 32-lane group (row per lane) per chain
+        auto setm = [](auto fbc) {
+            constexpr int FB = decltype(fbc)::value;
+            cudaFuncSetAttribute(kw_smoother_mbf_q<D, false, 32, kMbfWPC, FB>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K5MSmem<D, false, 32, kMbfWPC>));
+            cudaFuncSetAttribute(kw_smoother_mbf_q<D, true, 32, kMbfWPC, FB>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K5MSmem<D, true, 32, kMbfWPC>));
+        };
+        setm(std::integral_constant<int, D>{});
+        setm(std::integral_constant<int, 2>{});
+        setm(std::integral_constant<int, 4>{});
+    }
     cudaFuncSetAttribute(kw_scan_filter<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(ScanSmemF<D>));
     cudaFuncSetAttribute(kw_scan_smoother<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(ScanSmemS<D>));
     cudaFuncSetAttribute(kw_discretize<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(KDSmem<D>));
@@ -140,6 +151,22 @@ WPlan make_wplan(pssgp_model* m, int64_t n, bool grad = false) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kw_filter_apply<D>, 32 * kWWarps, sizeof(K3Smem<D>));
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, kw_smoother_apply<D>, 32 * kWWarps, sizeof(K5Smem<D>));
         m->wocc = std::max(1, std::min(a, std::min(b, c)));
+        if constexpr (D > 16) {
+            if (wide_mbf()) {   // the RTS rescan in adjoint form replaces kw_smoother_apply in the plan
+                int l5 = 0;
+                with_fblock<D>(m, [&](auto fbc) {
+                    constexpr int FB = decltype(fbc)::value;
+                    if (m->mode == kPade)
+                        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l5, kw_smoother_mbf_q<D, true, 32, kMbfWPC, FB>, 32 * kMbfWPC, sizeof(K5MSmem<D, true, 32, kMbfWPC>));
+                    else
+                        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l5, kw_smoother_mbf_q<D, false, 32, kMbfWPC, FB>, 32 * kMbfWPC, sizeof(K5MSmem<D, false, 32, kMbfWPC>));
+                });
+                m->wchains = std::max(1, std::min(std::min(a, b) * kWWarps, l5 * kMbfWPC));
+                if (getenv("PSSGP_WIDE_DEBUG"))
+                    fprintf(stderr, "wide plan D=%d: fold %d, apply %d CTAs/SM of %d warps, adjoint RTS %d of %d -> %d chains/SM\n",
+                            D, a, b, kWWarps, l5, kMbfWPC, m->wchains);
+            }
+        }
         if constexpr (D <= kGL) {
             int l1 = 0, l5 = 0, l3 = 0;
             if (wide_quarter_rescans()) {
@@ -547,6 +574,18 @@ pssgp_status wide_sapply(pssgp_model* m, pssgp::wide::WParams& p, int nb, cudaSt
                 }
             });
             LAUNCH_CHECK(m, "kw_smoother_apply_q (16-lane)");
+            return PSSGP_OK;
+        }
+    }
+    if constexpr (D > 16) {
+        if (wide_mbf() && p.y && p.mask && p.sagg) {   // adjoint form (needs y; the shard phase has none)
+            const int nbm = (p.nch + kMbfWPC - 1) / kMbfWPC;
+            with_fblock<D>(m, [&](auto fbc) {
+                constexpr int FB = decltype(fbc)::value;
+                if (p.fq) kw_smoother_mbf_q<D, true, 32, kMbfWPC, FB><<<nbm, 32 * kMbfWPC, sizeof(K5MSmem<D, true, 32, kMbfWPC>), s>>>(p);
+                else kw_smoother_mbf_q<D, false, 32, kMbfWPC, FB><<<nbm, 32 * kMbfWPC, sizeof(K5MSmem<D, false, 32, kMbfWPC>), s>>>(p);
+            });
+            LAUNCH_CHECK(m, "kw_smoother_mbf_q (32-lane)");
             return PSSGP_OK;
         }
     }

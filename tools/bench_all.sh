@@ -30,3 +30,4 @@ run gradb --config gradb
 run gradco2 --config gradco2
 run gradbt --config gradbt
 run batchedbt --config batchedbt
+run co2post --config co2post
