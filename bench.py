@@ -116,7 +116,7 @@ def ncu_traffic(slot: str, d: int, cfg_key: str, f32: bool = False):
 # warp-cooperative kernels whose d x d products (per step, per chain) run through the register-tiled
 # wmm (pssgp_wide.cuh) for d outside {8, 16}: the padded tile rows / columns execute FMAs that are
 # not algorithmic work
-_TILED_PRODUCTS = {"kw_filter_fold<": 3, "kw_grad_forward<": 3, "kw_grad_backward<": 3}
+_TILED_PRODUCTS = {"kw_filter_fold<": 3, "kw_filter_apply<": 3, "kw_grad_forward<": 3, "kw_grad_backward<": 3}
 
 
 def flops_per_step(slot: str, d: int, cfg_key: str):
