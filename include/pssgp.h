@@ -231,8 +231,9 @@ pssgp_status pssgp_nll_grad_batched(pssgp_model* m, int nseg, const int64_t* off
  * non-decreasing, offsets[nseg] = N); each starts from its stationary prior; steps inside a series
  * are uniform_dt apart or ties (dt = 0), else PSSGP_E_UNSUPPORTED from pssgp_check.  The per-series
  * F, Q, P_inf and their theta-derivatives are closed forms built on the device
- * (pssgp_batch_theta.cuh); one warp runs each series' sequential Kalman filter and RTS smoother /
- * reverse-mode adjoint (series share nothing, so no scan).  Outputs (device): mean[N], var[N]
+ * (pssgp_batch_theta.cuh); one warp runs each series' sequential Kalman filter and then the RTS
+ * smoother in its solve-free adjoint form / the reverse-mode adjoint of the filter (series share
+ * nothing, so no scan).  Outputs (device): mean[N], var[N]
  * (nullable), nll[nseg], grad[nseg x pssgp_num_params].  RBF components -> PSSGP_E_UNSUPPORTED. */
 pssgp_status pssgp_posterior_batched_theta(pssgp_model* m, int nseg, const int64_t* offsets,
                                            const double* theta, int64_t N, const double* t,
