@@ -673,12 +673,7 @@ __device__ void wcombine(const SS<D>& ei, SS<D>& ej, SS<D>& out, SCombF<D>& s, i
         s.v1[i] = a;
     }
     __syncwarp();
-    for (int e = lane; e < D * D; e += 32) {
-        const int i = e / D, j = e - (e / D) * D;
-        double a = ei.L[i][j];
-        for (int k = 0; k < D; ++k) a = fma(s.T1[i][k], ei.E[j][k], a);
-        s.M[i][j] = a;
-    }
+    wmm<D, false, true>(s.M, s.T1, ei.E, ei.L, lane);   // E_i L_j E_i^T + L_i
     __syncwarp();
     for (int e = lane; e < D * D; e += 32) {
         const int i = e / D, j = e - (e / D) * D;
@@ -715,12 +710,7 @@ __device__ bool wapply_prefix(double* x, double (*P)[LD(D)], const SF<D>& a, SCo
         for (int k = 0; k < D; ++k) acc = fma(s.T1[i][k], s.v1[k], acc);
         s.v2[i] = acc;
     }
-    for (int e = lane; e < D * D; e += 32) {
-        const int i = e / D, j = e - (e / D) * D;
-        double acc = a.C[i][j];
-        for (int k = 0; k < D; ++k) acc = fma(s.T2[i][k], a.A[j][k], acc);
-        s.M[i][j] = acc;
-    }
+    wmm<D, false, true>(s.M, s.T2, a.A, a.C, lane);      // A Minv P A^T + C
     __syncwarp();
     for (int e = lane; e < D * D; e += 32) {
         const int i = e / D, j = e - (e / D) * D;
@@ -884,12 +874,7 @@ __device__ void wapply_suffix(const SS<D>& a, double* m, double (*P)[LD(D)], Scr
         s.v1[i] = acc;
     }
     __syncwarp();
-    for (int e = lane; e < D * D; e += 32) {
-        const int i = e / D, j = e - (e / D) * D;
-        double acc = a.L[i][j];
-        for (int k = 0; k < D; ++k) acc = fma(s.T1[i][k], a.E[j][k], acc);
-        s.M[i][j] = acc;
-    }
+    wmm<D, false, true>(s.M, s.T1, a.E, a.L, lane);     // E P E^T + L
     __syncwarp();
     for (int e = lane; e < D * D; e += 32) {
         const int i = e / D, j = e - (e / D) * D;
