@@ -265,15 +265,18 @@ def test_wide_ties_and_small_chains(cuda_device):
     assert_parity(w, chain_len=3)
 
 
-@pytest.mark.parametrize("model", ["rbf6", "per4+m32"])
+@pytest.mark.parametrize("model", ["rbf6", "per4+m32", "quasi3+m32"])
 @pytest.mark.parametrize("world", [2, 3])
 def test_wide_virtual_sharding(cuda_device, world, model):
-    """Shard phases of the wide path (d = 6 quarters; d = 12 half chains, whose unsharded RTS rescan
-    runs in adjoint form while the shard phase, which has no y, keeps the RTS step) against the
-    unsharded posterior."""
+    """Shard phases of the wide path (d = 6 quarters; d = 12 half chains and d = 18 warp chains,
+    whose unsharded RTS rescan runs in adjoint form while the shard phase, which has no y, keeps the
+    RTS step) against the unsharded posterior."""
     comps = {"rbf6": [synth.Component("rbf", 1.0, 0.5, order=6)],
              "per4+m32": [synth.Component("periodic", 1.5, 1.0, period=0.7, order=4),
-                          synth.Component("matern32", 1.0, 2.0)]}[model]
+                          synth.Component("matern32", 1.0, 2.0)],
+             "quasi3+m32": [synth.Component("quasiperiodic", 2.0, 1.0, period=0.5, order=3, mat_lengthscale=3.0,
+                                            mat_nu2=3),
+                            synth.Component("matern32", 1.0, 2.0)]}[model]
     w = _uniform(comps, 0.01, 6001, 0.002, p_missing=0.2, seed=9)
     ref_mean, ref_var, ref_nll, _ = run_gpu(w)
     from paper_2102_09964_b200 import sharded
