@@ -343,7 +343,9 @@ def run_reference(args, rank: int):
             times.append(time.perf_counter() - t0)
     tot = sum(times)
     val = n * args.steps / tot
-    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+    metric = METRIC if (args.config == "metric" and not args.uniform) else \
+        f"time-steps/s (filter+smoother+NLL, fp64) {w.name} N={w.N}"
+    line = {"impl": "reference", "metric": metric, "value": val, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": w.name, "N": w.N, "sample_steps": n},
